@@ -1,0 +1,135 @@
+/* lsr_cuda.h — C ABI of the B200 (sm_100a) narrow-band semi-Lagrangian path.
+ *
+ * This is the drop-in boundary for the reference's hot path
+ *     void lsr::sl_step(const ScalarField& phi, const DistanceField& dist,
+ *                       const BandMask& mask, const StepConfig& cfg,
+ *                       double energy_p, ScalarField& out);
+ * declared at /root/reference/proj/include/lsr/evolve.hpp:42-43 and defined
+ * at proj/src/evolve.cpp:40-118. The reference has no plugin/FFI layer, so
+ * the entry points below are exactly what a C/C++/ctypes binding of that
+ * free function (and of the neighbouring band helpers) needs: plain
+ * pointers, sizes and POD structs, no C++ or torch types.
+ *
+ * Semantics (all match the reference unless stated):
+ *  - fields are dense fp64, x fastest: id = (k*ny + j)*nx + i
+ *    (grid.hpp:19-21); active ids are ascending int64 (grid.hpp:82).
+ *  - out equals phi on every non-active node and the SL update on every
+ *    active node, bit-for-bit (the kernels are built with --fmad=false and
+ *    follow the reference operation order).
+ *  - errors are returned as status codes; the message is available through
+ *    lsr_cuda_last_error_string(). Config errors are detected before any
+ *    device work, like StepConfig::validate() (evolve.hpp:25-30). A
+ *    non-finite update yields LSR_ERR_NUMERICAL with *bad_node = the
+ *    smallest offending id and `out` fully written (evolve.cpp:109-117; the
+ *    reference reports whichever thread stored last, we report the minimum,
+ *    which is deterministic).
+ *  - every call is synchronous with respect to the host unless it says
+ *    otherwise; one context per host thread.
+ */
+#ifndef LSR_CUDA_H
+#define LSR_CUDA_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes — one per reference exception type (types.hpp:24-52) */
+#define LSR_OK 0
+#define LSR_ERR_CONFIG 1        /* lsr::ConfigError */
+#define LSR_ERR 2               /* lsr::Error */
+#define LSR_ERR_NUMERICAL 3     /* lsr::NumericalError */
+#define LSR_ERR_OUT_OF_DOMAIN 4 /* lsr::OutOfDomainError */
+#define LSR_ERR_CUDA 5          /* device / runtime failure (no reference analogue) */
+#define LSR_ERR_NO_INTERFACE 6  /* lsr::NoInterfaceError */
+
+/* lsr::InterpolatorKind (interp.hpp:9) */
+#define LSR_INTERP_Q1 0
+#define LSR_INTERP_WENO 1
+
+/* resident fields of a context */
+#define LSR_FIELD_PHI 0  /* phi^n (input of the step) */
+#define LSR_FIELD_DIST 1 /* unsigned distance d (DistanceField::field) */
+#define LSR_FIELD_OUT 2  /* phi^{n+1} (the double buffer `out`) */
+
+/* lsr::Grid (grid.hpp:10-52). dims[2] == 1 and origin[2] == 0 in 2d. */
+typedef struct lsr_grid {
+    int32_t dim;
+    int32_t dims[3];
+    double origin[3];
+    double dx;
+} lsr_grid;
+
+/* lsr::StepConfig (evolve.hpp:16-31) with BandParams (grid.hpp:86-93) inlined. */
+typedef struct lsr_step_cfg {
+    int32_t p;      /* 1 or 2 */
+    int32_t interp; /* LSR_INTERP_Q1 / LSR_INTERP_WENO */
+    double delta;   /* [0, 1] */
+    double dt;      /* > 0 */
+    double fallback_c;     /* default 1e-3 */
+    double fallback_alpha; /* default 1 */
+    double gamma;   /* band half-width */
+    double beta;    /* cutoff inner radius, 0 < beta < gamma */
+} lsr_step_cfg;
+
+typedef struct lsr_cuda_ctx lsr_cuda_ctx;
+
+const char* lsr_cuda_last_error_string(void);
+/* number of CUDA kernels this library has launched in this process */
+int64_t lsr_cuda_kernel_launches(void);
+
+/* ---- one-shot drop-in for lsr::sl_step (host buffers in, host buffer out) ----
+ * Replaces evolve.cpp:40-118. phi, dist, out: num_nodes doubles; out must not
+ * alias phi (evolve.cpp:48-50). */
+int lsr_cuda_sl_step_host(const lsr_grid* grid, const double* phi, const double* dist,
+                          const int64_t* active, int64_t n_active, const lsr_step_cfg* cfg,
+                          double energy_p, double* out, int64_t* bad_node);
+
+/* ---- device-resident context (the loop keeps phi, d, out and ids in HBM) ---- */
+int lsr_cuda_create(int device, const lsr_grid* grid, lsr_cuda_ctx** ctx);
+int lsr_cuda_destroy(lsr_cuda_ctx* ctx);
+/* run on this cudaStream_t (NULL = the context's own stream) */
+int lsr_cuda_set_stream(lsr_cuda_ctx* ctx, void* stream);
+int lsr_cuda_upload_field(lsr_cuda_ctx* ctx, int which, const double* host);
+int lsr_cuda_download_field(lsr_cuda_ctx* ctx, int which, double* host);
+/* device pointer of a resident field (plumbing for torch / NCCL); a caller
+ * that writes through it must call lsr_cuda_mark_dirty() afterwards */
+int lsr_cuda_field_ptr(lsr_cuda_ctx* ctx, int which, double** dptr);
+int lsr_cuda_mark_dirty(lsr_cuda_ctx* ctx, int which);
+/* BandMask::active (grid.hpp:82): ascending ids, host memory */
+int lsr_cuda_set_active(lsr_cuda_ctx* ctx, const int64_t* ids, int64_t n);
+/* same, from device memory (e.g. a device-built band) */
+int lsr_cuda_set_active_device(lsr_cuda_ctx* ctx, const int64_t* d_ids, int64_t n);
+/* lsr::sl_step(PHI, DIST, active, cfg, energy_p, OUT) */
+int lsr_cuda_sl_step(lsr_cuda_ctx* ctx, const lsr_step_cfg* cfg, double energy_p,
+                     int64_t* bad_node);
+/* std::swap(phi.values, next.values) (driver.cpp:203): O(1) */
+int lsr_cuda_swap(lsr_cuda_ctx* ctx);
+/* device time (ms, CUDA events on the context stream) of the last SL kernel
+ * and of the last whole sl_step (sync of out + kernel) */
+int lsr_cuda_last_times(lsr_cuda_ctx* ctx, float* kernel_ms, float* step_ms);
+
+/* ---- raw device entry (slab / multi-GPU plumbing) ----
+ * Fields hold global planes [z_base, z_base + z_planes) of `grid` (3d) — a
+ * z-slab plus halo; ids stay global. Feet whose stencil leaves the resident
+ * planes are reported through *halo_miss (count) and computed as NaN-free
+ * garbage-free: the caller must widen the halo and redo.
+ * Asynchronous on `stream`; bad_node/halo_miss are device int64 pointers
+ * (bad_node initialised to INT64_MAX by the caller). */
+int lsr_cuda_sl_step_device(const lsr_grid* grid, int32_t z_base, int32_t z_planes,
+                            const double* d_phi, const double* d_dist, const int64_t* d_active,
+                            int64_t n_active, const lsr_step_cfg* cfg, double energy_p,
+                            double* d_out, int64_t* d_bad_node, int64_t* d_halo_miss,
+                            void* stream);
+
+/* ---- self-test hook ----
+ * Divides n pseudo-random doubles by c with the kernels' constant-divisor
+ * division and with the hardware IEEE division; *mismatches = how many
+ * quotients differ in any bit (must be 0). */
+int lsr_cuda_selftest_div_const(double c, int64_t n, uint64_t seed, int64_t* mismatches);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LSR_CUDA_H */

@@ -1,0 +1,372 @@
+"""ctypes binding of include/lsr_cuda.h plus the reference-shaped host types.
+
+Reference interface mirrored here (file:line under /root/reference/proj):
+  Grid            include/lsr/grid.hpp:10-52
+  ScalarField     include/lsr/grid.hpp:63-75
+  BandMask        include/lsr/grid.hpp:79-84 (NodeState :77)
+  BandParams      include/lsr/grid.hpp:86-93, default_band_params grid.cpp:49-51
+  DistanceField   include/lsr/distance.hpp:14-18
+  StepConfig      include/lsr/evolve.hpp:16-31
+  sl_step         include/lsr/evolve.hpp:42-43 -> lsr_cuda_sl_step_host
+  exceptions      include/lsr/types.hpp:24-52
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+lib_path = os.path.join(_HERE, "liblsr_b200.so")
+
+
+# --------------------------------------------------------------------------
+# exceptions (types.hpp:24-52)
+class Error(RuntimeError):
+    pass
+
+
+class ParseError(Error):
+    pass
+
+
+class ConfigError(Error):
+    pass
+
+
+class OutOfDomainError(Error):
+    pass
+
+
+class NumericalError(Error):
+    pass
+
+
+class NoInterfaceError(Error):
+    pass
+
+
+class CudaError(Error):
+    pass
+
+
+LSR_OK, LSR_ERR_CONFIG, LSR_ERR, LSR_ERR_NUMERICAL, LSR_ERR_OUT_OF_DOMAIN, LSR_ERR_CUDA, LSR_ERR_NO_INTERFACE = range(7)
+_EXC = {
+    LSR_ERR_CONFIG: ConfigError,
+    LSR_ERR: Error,
+    LSR_ERR_NUMERICAL: NumericalError,
+    LSR_ERR_OUT_OF_DOMAIN: OutOfDomainError,
+    LSR_ERR_CUDA: CudaError,
+    LSR_ERR_NO_INTERFACE: NoInterfaceError,
+}
+FIELD_PHI, FIELD_DIST, FIELD_OUT = 0, 1, 2
+
+
+class CGrid(C.Structure):
+    _fields_ = [("dim", C.c_int32), ("dims", C.c_int32 * 3), ("origin", C.c_double * 3), ("dx", C.c_double)]
+
+
+class CStepCfg(C.Structure):
+    _fields_ = [
+        ("p", C.c_int32),
+        ("interp", C.c_int32),
+        ("delta", C.c_double),
+        ("dt", C.c_double),
+        ("fallback_c", C.c_double),
+        ("fallback_alpha", C.c_double),
+        ("gamma", C.c_double),
+        ("beta", C.c_double),
+    ]
+
+
+_dp = np.ctypeslib.ndpointer(dtype=np.float64, flags="C_CONTIGUOUS")
+_ip = np.ctypeslib.ndpointer(dtype=np.int64, flags="C_CONTIGUOUS")
+_lib = None
+
+
+def lib() -> C.CDLL:
+    """The CUDA library. Raises (loudly) when it has not been built: there is
+    no CPU fallback for any compute entry point."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(lib_path):
+        raise ImportError(f"{lib_path} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`")
+    L = C.CDLL(lib_path)
+    P = C.POINTER
+    L.lsr_cuda_last_error_string.restype = C.c_char_p
+    L.lsr_cuda_kernel_launches.restype = C.c_int64
+    L.lsr_cuda_sl_step_host.argtypes = [P(CGrid), _dp, _dp, C.c_void_p, C.c_int64, P(CStepCfg), C.c_double, _dp,
+                                        P(C.c_int64)]
+    L.lsr_cuda_create.argtypes = [C.c_int, P(CGrid), P(C.c_void_p)]
+    L.lsr_cuda_destroy.argtypes = [C.c_void_p]
+    L.lsr_cuda_set_stream.argtypes = [C.c_void_p, C.c_void_p]
+    L.lsr_cuda_upload_field.argtypes = [C.c_void_p, C.c_int, C.c_void_p]
+    L.lsr_cuda_download_field.argtypes = [C.c_void_p, C.c_int, C.c_void_p]
+    L.lsr_cuda_field_ptr.argtypes = [C.c_void_p, C.c_int, P(C.c_void_p)]
+    L.lsr_cuda_mark_dirty.argtypes = [C.c_void_p, C.c_int]
+    L.lsr_cuda_set_active.argtypes = [C.c_void_p, C.c_void_p, C.c_int64]
+    L.lsr_cuda_set_active_device.argtypes = [C.c_void_p, C.c_void_p, C.c_int64]
+    L.lsr_cuda_sl_step.argtypes = [C.c_void_p, P(CStepCfg), C.c_double, P(C.c_int64)]
+    L.lsr_cuda_swap.argtypes = [C.c_void_p]
+    L.lsr_cuda_last_times.argtypes = [C.c_void_p, P(C.c_float), P(C.c_float)]
+    L.lsr_cuda_sl_step_device.argtypes = [P(CGrid), C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
+                                          C.c_int64, P(CStepCfg), C.c_double, C.c_void_p, C.c_void_p, C.c_void_p,
+                                          C.c_void_p]
+    L.lsr_cuda_selftest_div_const.argtypes = [C.c_double, C.c_int64, C.c_uint64, P(C.c_int64)]
+    _lib = L
+    return L
+
+
+def selftest_div_const(c: float, n: int, seed: int = 1) -> int:
+    """Mismatching quotients of the kernels' constant-divisor division vs the
+    hardware IEEE division over n pseudo-random numerators (must be 0)."""
+    m = C.c_int64()
+    _check(lib().lsr_cuda_selftest_div_const(float(c), int(n), int(seed), C.byref(m)))
+    return int(m.value)
+
+
+def _check(status: int) -> None:
+    if status != LSR_OK:
+        msg = lib().lsr_cuda_last_error_string().decode()
+        raise _EXC.get(status, Error)(msg)
+
+
+def kernel_launches() -> int:
+    """Number of CUDA kernels this process launched through the library."""
+    return int(lib().lsr_cuda_kernel_launches())
+
+
+# --------------------------------------------------------------------------
+# reference-shaped types
+class InterpolatorKind(enum.IntEnum):  # interp.hpp:9
+    Q1 = 0
+    Weno = 1
+
+
+class NodeState(enum.IntEnum):  # grid.hpp:77
+    Inactive = 0
+    Active = 1
+    ReinitHalo = 2
+
+
+@dataclass
+class Grid:  # grid.hpp:10-52
+    dim: int = 2
+    origin: tuple = (0.0, 0.0, 0.0)
+    dx: float = 1.0
+    dims: tuple = (1, 1, 1)
+
+    def num_nodes(self) -> int:
+        return int(self.dims[0]) * int(self.dims[1]) * int(self.dims[2])
+
+    def index(self, i, j, k):
+        return (k * self.dims[1] + j) * self.dims[0] + i
+
+    def unflatten(self, idx):
+        nx, ny = self.dims[0], self.dims[1]
+        return idx % nx, (idx // nx) % ny, idx // (nx * ny)
+
+    def node(self, i, j, k):
+        return (self.origin[0] + i * self.dx, self.origin[1] + j * self.dx, self.origin[2] + k * self.dx)
+
+    def upper(self):
+        return tuple(self.origin[d] + (self.dims[d] - 1) * self.dx for d in range(3))
+
+    def axes(self):
+        """Node coordinates per axis, computed with Grid::node's expression."""
+        return [self.origin[d] + np.arange(self.dims[d], dtype=np.float64) * self.dx for d in range(3)]
+
+    def mesh(self):
+        """(x, y, z) node coordinates, each shaped (nz, ny, nx)."""
+        ax = self.axes()
+        z, y, x = np.meshgrid(ax[2], ax[1], ax[0], indexing="ij")
+        return x, y, z
+
+    def c(self) -> CGrid:
+        g = CGrid()
+        g.dim = int(self.dim)
+        for d in range(3):
+            g.dims[d] = int(self.dims[d])
+            g.origin[d] = float(self.origin[d])
+        g.dx = float(self.dx)
+        return g
+
+    def __eq__(self, o):
+        return (self.dim == o.dim and tuple(map(float, self.origin)) == tuple(map(float, o.origin))
+                and float(self.dx) == float(o.dx) and tuple(map(int, self.dims)) == tuple(map(int, o.dims)))
+
+
+def cube_grid(n: int, dim: int = 3, lo: float = -1.0, hi: float = 1.0) -> Grid:
+    """The benchmark grids: n nodes per axis on [lo, hi]^dim, dx = (hi-lo)/(n-1)."""
+    dx = (hi - lo) / (n - 1)
+    if dim == 2:
+        return Grid(2, (lo, lo, 0.0), dx, (n, n, 1))
+    return Grid(3, (lo, lo, lo), dx, (n, n, n))
+
+
+@dataclass
+class ScalarField:  # grid.hpp:63-75
+    grid: Grid
+    values: np.ndarray = None
+
+    def __post_init__(self):
+        if self.values is None:
+            self.values = np.zeros(self.grid.num_nodes(), dtype=np.float64)
+        else:
+            self.values = np.ascontiguousarray(self.values, dtype=np.float64).reshape(-1)
+
+    def at(self, i, j, k):
+        return self.values[self.grid.index(i, j, k)]
+
+
+@dataclass
+class DistanceField:  # distance.hpp:14-18
+    field: ScalarField
+    exact: np.ndarray = None
+    sentinel: float = 0.0
+
+
+@dataclass
+class BandMask:  # grid.hpp:79-84
+    grid: Grid
+    state: np.ndarray = None
+    active: np.ndarray = field(default_factory=lambda: np.zeros(0, np.int64))
+    tube: np.ndarray = field(default_factory=lambda: np.zeros(0, np.int64))
+
+
+@dataclass
+class BandParams:  # grid.hpp:86-93
+    gamma: float = 0.0
+    beta: float = 0.0
+
+    def validate(self):
+        if not (self.beta > 0.0) or not (self.beta < self.gamma):
+            raise ConfigError("band: need 0 < beta < gamma")
+
+
+def default_band_params(dim: int, dx: float) -> BandParams:  # grid.cpp:49-51
+    return BandParams(4.0 * dx, 2.0 * dx) if dim == 2 else BandParams(6.0 * dx, 3.0 * dx)
+
+
+@dataclass
+class StepConfig:  # evolve.hpp:16-31
+    p: int = 1
+    delta: float = 0.0
+    dt: float = 0.0
+    interp: InterpolatorKind = InterpolatorKind.Weno
+    fallback_c: float = 1e-3
+    fallback_alpha: float = 1.0
+    band: BandParams = field(default_factory=BandParams)
+
+    def validate(self):
+        if self.p not in (1, 2):
+            raise ConfigError("step: p must be 1 or 2")
+        if not (self.dt > 0.0):
+            raise ConfigError("step: dt must be positive")
+        if self.delta < 0.0 or self.delta > 1.0:
+            raise ConfigError("step: delta must be in [0, 1]")
+        self.band.validate()
+
+    def c(self) -> CStepCfg:
+        s = CStepCfg()
+        s.p = int(self.p)
+        s.interp = int(self.interp)
+        s.delta = float(self.delta)
+        s.dt = float(self.dt)
+        s.fallback_c = float(self.fallback_c)
+        s.fallback_alpha = float(self.fallback_alpha)
+        s.gamma = float(self.band.gamma)
+        s.beta = float(self.band.beta)
+        return s
+
+
+def _ids_ptr(a: np.ndarray):
+    return a.ctypes.data_as(C.c_void_p) if a.size else None
+
+
+def sl_step(phi: ScalarField, dist: DistanceField, mask: BandMask, cfg: StepConfig, energy_p: float,
+            out: ScalarField) -> None:
+    """lsr::sl_step (evolve.hpp:42-43) on the B200. ``out`` is resized if its
+    grid differs (evolve.cpp:48) and written in full; raises the reference's
+    exception types."""
+    if not (phi.grid == dist.field.grid) or not (phi.grid == mask.grid):
+        raise ConfigError("sl_step: phi, dist and mask must share one grid")  # evolve.cpp:43-44
+    g = phi.grid
+    if not (out.grid == g) or out.values.size != g.num_nodes():
+        out.grid = g
+        out.values = np.zeros(g.num_nodes(), dtype=np.float64)
+    active = np.ascontiguousarray(mask.active, dtype=np.int64)
+    bad = C.c_int64(-1)
+    st = lib().lsr_cuda_sl_step_host(C.byref(g.c()), phi.values, np.ascontiguousarray(dist.field.values), _ids_ptr(active),
+                                     active.size, C.byref(cfg.c()), float(energy_p), out.values, C.byref(bad))
+    _check(st)
+
+
+class Context:
+    """Device-resident context (lsr_cuda_create ...): phi, out and d live in
+    HBM across steps; the per-step host traffic is the active-id list (or
+    nothing, with set_active_device) and an 8-byte status."""
+
+    def __init__(self, grid: Grid, device: int = 0):
+        self.grid = grid
+        self.h = C.c_void_p()
+        _check(lib().lsr_cuda_create(int(device), C.byref(grid.c()), C.byref(self.h)))
+
+    def close(self):
+        if self.h:
+            lib().lsr_cuda_destroy(self.h)
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_stream(self, stream_ptr: int | None):
+        _check(lib().lsr_cuda_set_stream(self.h, C.c_void_p(stream_ptr) if stream_ptr else None))
+
+    def upload(self, which: int, values: np.ndarray):
+        v = np.ascontiguousarray(values, dtype=np.float64).reshape(-1)
+        assert v.size == self.grid.num_nodes()
+        _check(lib().lsr_cuda_upload_field(self.h, which, v.ctypes.data_as(C.c_void_p)))
+
+    def download(self, which: int, out: np.ndarray | None = None) -> np.ndarray:
+        if out is None:
+            out = np.empty(self.grid.num_nodes(), dtype=np.float64)
+        assert out.flags.c_contiguous and out.dtype == np.float64 and out.size == self.grid.num_nodes()
+        _check(lib().lsr_cuda_download_field(self.h, which, out.ctypes.data_as(C.c_void_p)))
+        return out
+
+    def field_ptr(self, which: int) -> int:
+        p = C.c_void_p()
+        _check(lib().lsr_cuda_field_ptr(self.h, which, C.byref(p)))
+        return int(p.value)
+
+    def mark_dirty(self, which: int):
+        _check(lib().lsr_cuda_mark_dirty(self.h, which))
+
+    def set_active(self, ids: np.ndarray):
+        ids = np.ascontiguousarray(ids, dtype=np.int64)
+        _check(lib().lsr_cuda_set_active(self.h, _ids_ptr(ids), ids.size))
+
+    def set_active_device(self, ptr: int, n: int):
+        _check(lib().lsr_cuda_set_active_device(self.h, C.c_void_p(ptr), int(n)))
+
+    def sl_step(self, cfg: StepConfig, energy_p: float) -> None:
+        bad = C.c_int64(-1)
+        st = lib().lsr_cuda_sl_step(self.h, C.byref(cfg.c()), float(energy_p), C.byref(bad))
+        self.bad_node = bad.value
+        _check(st)
+
+    def swap(self):
+        _check(lib().lsr_cuda_swap(self.h))
+
+    def last_times(self):
+        k, s = C.c_float(), C.c_float()
+        _check(lib().lsr_cuda_last_times(self.h, C.byref(k), C.byref(s)))
+        return k.value, s.value

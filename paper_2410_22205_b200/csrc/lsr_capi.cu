@@ -1,0 +1,398 @@
+// lsr_capi.cu — the C ABI (include/lsr_cuda.h): validation with the
+// reference's error semantics, device-resident contexts, and the one-shot
+// host entry that stands in for lsr::sl_step (evolve.cpp:40-118).
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "lsr_cuda.h"
+#include "sl_launch.h"
+
+using lsr_dev::SlParams;
+
+namespace {
+
+thread_local std::string g_err;
+std::atomic<long long> g_launches{0};
+
+int set_err(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+int cuda_err(cudaError_t e, const char* what) {
+    return set_err(LSR_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define LSR_CUDA_TRY(expr)                                     \
+    do {                                                       \
+        cudaError_t _e = (expr);                               \
+        if (_e != cudaSuccess) return cuda_err(_e, #expr);     \
+    } while (0)
+
+int64_t num_nodes(const lsr_grid& g) {
+    return static_cast<int64_t>(g.dims[0]) * g.dims[1] * g.dims[2];
+}
+
+int check_grid(const lsr_grid* g) {
+    if (!g) return set_err(LSR_ERR_CONFIG, "grid: null");
+    if (g->dim != 2 && g->dim != 3) return set_err(LSR_ERR_CONFIG, "grid: dim must be 2 or 3");
+    if (!(g->dx > 0.0)) return set_err(LSR_ERR_CONFIG, "grid: dx must be positive");
+    for (int d = 0; d < g->dim; ++d)
+        if (g->dims[d] < 2) return set_err(LSR_ERR_CONFIG, "grid: need at least 2 nodes per axis");
+    if (g->dim == 2 && g->dims[2] != 1) return set_err(LSR_ERR_CONFIG, "grid: dims[2] must be 1 in 2d");
+    return LSR_OK;
+}
+
+// StepConfig::validate (evolve.hpp:25-30), BandParams::validate
+// (grid.hpp:90-92), the energy check (evolve.cpp:45-46) and the interp
+// dispatch error (interp.cpp:118) — all before any device work.
+int check_cfg(const lsr_step_cfg* c, double energy_p) {
+    if (!c) return set_err(LSR_ERR_CONFIG, "step: null config");
+    if (c->p != 1 && c->p != 2) return set_err(LSR_ERR_CONFIG, "step: p must be 1 or 2");
+    if (!(c->dt > 0.0)) return set_err(LSR_ERR_CONFIG, "step: dt must be positive");
+    if (c->delta < 0.0 || c->delta > 1.0) return set_err(LSR_ERR_CONFIG, "step: delta must be in [0, 1]");
+    if (!(c->beta > 0.0) || !(c->beta < c->gamma)) return set_err(LSR_ERR_CONFIG, "band: need 0 < beta < gamma");
+    if (c->interp != LSR_INTERP_Q1 && c->interp != LSR_INTERP_WENO)
+        return set_err(LSR_ERR_CONFIG, "interp: unknown interpolator kind");
+    if (c->p > 1 && !(energy_p > 0.0)) return set_err(LSR_ERR, "sl_step: energy must be positive for p > 1");
+    return LSR_OK;
+}
+
+bool pow2_range(double c) {  // div_const precondition (sl_device.cuh)
+    const double a = std::fabs(c);
+    return a >= std::ldexp(1.0, -100) && a <= std::ldexp(1.0, 100);
+}
+
+// Host-side precomputation with the reference's own expressions.
+SlParams make_params(const lsr_grid& g, const lsr_step_cfg& c, double energy_p) {
+    SlParams P{};
+    P.dim = g.dim;
+    P.nx = g.dims[0];
+    P.ny = g.dims[1];
+    P.nz = g.dims[2];
+    P.nxy = static_cast<long long>(P.nx) * P.ny;
+    P.ox = g.origin[0];
+    P.oy = g.origin[1];
+    P.oz = g.origin[2];
+    P.dx = g.dx;
+    P.hx = g.origin[0] + (g.dims[0] - 1) * g.dx;  // Grid::upper (grid.hpp:31-34)
+    P.hy = g.origin[1] + (g.dims[1] - 1) * g.dx;
+    P.hz = g.origin[2] + (g.dims[2] - 1) * g.dx;
+    P.inv2 = 1.0 / (2.0 * g.dx);  // grid.cpp:55
+    P.inv1 = 1.0 / g.dx;          // grid.cpp:56
+    P.dx2 = g.dx * g.dx;
+    P.rdx = 1.0 / g.dx;
+    P.rdx2 = 1.0 / P.dx2;
+    P.r3 = 1.0 / 3.0;
+    P.fast_div = (pow2_range(g.dx) && pow2_range(P.dx2)) ? 1 : 0;
+    P.p = c.p;
+    P.pd = static_cast<double>(c.p);
+    P.dt = c.dt;
+    P.delta = c.delta;
+    P.energy = energy_p;
+    P.grad_threshold = c.fallback_c * std::pow(c.dt, c.fallback_alpha);  // evolve.cpp:52
+    P.gamma = c.gamma;
+    P.beta = c.beta;
+    P.cut_den = (c.gamma - c.beta) * (c.gamma - c.beta) * (c.gamma - c.beta);  // grid.cpp:142
+    P.z_base = 0;
+    P.z_planes = g.dims[2];
+    return P;
+}
+
+int numerical_error(const lsr_grid& g, unsigned long long bad, int64_t* bad_node) {
+    if (bad_node) *bad_node = static_cast<int64_t>(bad);
+    const int64_t id = static_cast<int64_t>(bad);
+    const int i = static_cast<int>(id % g.dims[0]);
+    const int j = static_cast<int>((id / g.dims[0]) % g.dims[1]);
+    const int k = static_cast<int>(id / (static_cast<int64_t>(g.dims[0]) * g.dims[1]));
+    char buf[160];
+    std::snprintf(buf, sizeof buf, "sl_step: non-finite update at node (%d, %d, %d)", i, j, k);  // evolve.cpp:115
+    return set_err(LSR_ERR_NUMERICAL, buf);
+}
+
+}  // namespace
+
+void lsr_note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+struct lsr_cuda_ctx {
+    int device = 0;
+    lsr_grid grid{};
+    int64_t n = 0;
+    double* phi = nullptr;
+    double* out = nullptr;
+    double* dist = nullptr;
+    int64_t* active = nullptr;
+    int64_t n_active = 0, cap_active = 0;
+    int64_t* dirty = nullptr;  // ids where out may differ from phi
+    int64_t n_dirty = 0, cap_dirty = 0;
+    bool consistent = false;   // out == phi except at `dirty`
+    unsigned long long* d_bad = nullptr;
+    unsigned long long* h_bad = nullptr;  // pinned
+    cudaStream_t own = nullptr;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
+    float kernel_ms = 0.f, step_ms = 0.f;
+};
+
+namespace {
+
+int ensure_ids(int64_t** buf, int64_t* cap, int64_t n) {
+    if (n <= *cap) return LSR_OK;
+    if (*buf) cudaFree(*buf);
+    *buf = nullptr;
+    *cap = 0;
+    const int64_t c = n + n / 4 + 1024;
+    LSR_CUDA_TRY(cudaMalloc(buf, sizeof(int64_t) * c));
+    *cap = c;
+    return LSR_OK;
+}
+
+double** field_slot(lsr_cuda_ctx* c, int which) {
+    switch (which) {
+        case LSR_FIELD_PHI: return &c->phi;
+        case LSR_FIELD_DIST: return &c->dist;
+        case LSR_FIELD_OUT: return &c->out;
+    }
+    return nullptr;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* lsr_cuda_last_error_string(void) { return g_err.c_str(); }
+
+int64_t lsr_cuda_kernel_launches(void) { return g_launches.load(); }
+
+int lsr_cuda_create(int device, const lsr_grid* grid, lsr_cuda_ctx** out) {
+    if (!out) return set_err(LSR_ERR_CONFIG, "create: null out");
+    *out = nullptr;
+    if (int st = check_grid(grid)) return st;
+    LSR_CUDA_TRY(cudaSetDevice(device));
+    auto* c = new lsr_cuda_ctx;
+    c->device = device;
+    c->grid = *grid;
+    c->n = num_nodes(*grid);
+    const size_t bytes = sizeof(double) * static_cast<size_t>(c->n);
+    cudaError_t e = cudaSuccess;
+    if (e == cudaSuccess) e = cudaMalloc(&c->phi, bytes);
+    if (e == cudaSuccess) e = cudaMalloc(&c->out, bytes);
+    if (e == cudaSuccess) e = cudaMalloc(&c->dist, bytes);
+    if (e == cudaSuccess) e = cudaMalloc(&c->d_bad, sizeof(unsigned long long));
+    if (e == cudaSuccess) e = cudaMallocHost(&c->h_bad, sizeof(unsigned long long));
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking);
+    for (int i = 0; i < 3 && e == cudaSuccess; ++i) e = cudaEventCreate(&c->ev[i]);
+    if (e != cudaSuccess) {
+        lsr_cuda_destroy(c);
+        return cuda_err(e, "lsr_cuda_create");
+    }
+    c->stream = c->own;
+    *out = c;
+    return LSR_OK;
+}
+
+int lsr_cuda_destroy(lsr_cuda_ctx* c) {
+    if (!c) return LSR_OK;
+    cudaSetDevice(c->device);
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    cudaFree(c->phi);
+    cudaFree(c->out);
+    cudaFree(c->dist);
+    cudaFree(c->active);
+    cudaFree(c->dirty);
+    cudaFree(c->d_bad);
+    if (c->h_bad) cudaFreeHost(c->h_bad);
+    for (auto& ev : c->ev)
+        if (ev) cudaEventDestroy(ev);
+    if (c->own) cudaStreamDestroy(c->own);
+    delete c;
+    return LSR_OK;
+}
+
+int lsr_cuda_set_stream(lsr_cuda_ctx* c, void* stream) {
+    if (!c) return set_err(LSR_ERR_CONFIG, "null context");
+    c->stream = stream ? static_cast<cudaStream_t>(stream) : c->own;
+    return LSR_OK;
+}
+
+int lsr_cuda_upload_field(lsr_cuda_ctx* c, int which, const double* host) {
+    if (!c || !host) return set_err(LSR_ERR_CONFIG, "upload: null argument");
+    double** slot = field_slot(c, which);
+    if (!slot) return set_err(LSR_ERR_CONFIG, "upload: unknown field");
+    LSR_CUDA_TRY(cudaSetDevice(c->device));
+    LSR_CUDA_TRY(cudaMemcpyAsync(*slot, host, sizeof(double) * c->n, cudaMemcpyHostToDevice, c->stream));
+    LSR_CUDA_TRY(cudaStreamSynchronize(c->stream));
+    if (which != LSR_FIELD_DIST) c->consistent = false;
+    return LSR_OK;
+}
+
+int lsr_cuda_download_field(lsr_cuda_ctx* c, int which, double* host) {
+    if (!c || !host) return set_err(LSR_ERR_CONFIG, "download: null argument");
+    double** slot = field_slot(c, which);
+    if (!slot) return set_err(LSR_ERR_CONFIG, "download: unknown field");
+    LSR_CUDA_TRY(cudaSetDevice(c->device));
+    LSR_CUDA_TRY(cudaMemcpyAsync(host, *slot, sizeof(double) * c->n, cudaMemcpyDeviceToHost, c->stream));
+    LSR_CUDA_TRY(cudaStreamSynchronize(c->stream));
+    return LSR_OK;
+}
+
+int lsr_cuda_field_ptr(lsr_cuda_ctx* c, int which, double** dptr) {
+    if (!c || !dptr) return set_err(LSR_ERR_CONFIG, "field_ptr: null argument");
+    double** slot = field_slot(c, which);
+    if (!slot) return set_err(LSR_ERR_CONFIG, "field_ptr: unknown field");
+    *dptr = *slot;
+    return LSR_OK;
+}
+
+int lsr_cuda_mark_dirty(lsr_cuda_ctx* c, int which) {
+    if (!c) return set_err(LSR_ERR_CONFIG, "null context");
+    if (which != LSR_FIELD_DIST) c->consistent = false;
+    return LSR_OK;
+}
+
+int lsr_cuda_set_active(lsr_cuda_ctx* c, const int64_t* ids, int64_t n) {
+    if (!c || (n > 0 && !ids) || n < 0) return set_err(LSR_ERR_CONFIG, "set_active: bad argument");
+    LSR_CUDA_TRY(cudaSetDevice(c->device));
+    if (int st = ensure_ids(&c->active, &c->cap_active, n)) return st;
+    if (n > 0)
+        LSR_CUDA_TRY(cudaMemcpyAsync(c->active, ids, sizeof(int64_t) * n, cudaMemcpyHostToDevice, c->stream));
+    LSR_CUDA_TRY(cudaStreamSynchronize(c->stream));
+    c->n_active = n;
+    return LSR_OK;
+}
+
+int lsr_cuda_set_active_device(lsr_cuda_ctx* c, const int64_t* d_ids, int64_t n) {
+    if (!c || (n > 0 && !d_ids) || n < 0) return set_err(LSR_ERR_CONFIG, "set_active_device: bad argument");
+    LSR_CUDA_TRY(cudaSetDevice(c->device));
+    if (int st = ensure_ids(&c->active, &c->cap_active, n)) return st;
+    if (n > 0)
+        LSR_CUDA_TRY(cudaMemcpyAsync(c->active, d_ids, sizeof(int64_t) * n, cudaMemcpyDeviceToDevice, c->stream));
+    c->n_active = n;
+    return LSR_OK;
+}
+
+int lsr_cuda_sl_step(lsr_cuda_ctx* c, const lsr_step_cfg* cfg, double energy_p, int64_t* bad_node) {
+    if (bad_node) *bad_node = -1;
+    if (!c) return set_err(LSR_ERR_CONFIG, "null context");
+    if (int st = check_cfg(cfg, energy_p)) return st;
+    LSR_CUDA_TRY(cudaSetDevice(c->device));
+    const SlParams P = make_params(c->grid, *cfg, energy_p);
+    cudaStream_t s = c->stream;
+    LSR_CUDA_TRY(cudaEventRecord(c->ev[0], s));
+    // "non-active nodes carry phi over" (evolve.cpp:50) without the O(N) copy
+    // when out is known to equal phi except at the previous step's ids.
+    if (!c->consistent) {
+        LSR_CUDA_TRY(cudaMemcpyAsync(c->out, c->phi, sizeof(double) * c->n, cudaMemcpyDeviceToDevice, s));
+    } else {
+        LSR_CUDA_TRY(launch_resync(c->phi, c->out, c->dirty, c->n_dirty, s));
+    }
+    LSR_CUDA_TRY(cudaMemsetAsync(c->d_bad, 0xff, sizeof(unsigned long long), s));
+    LSR_CUDA_TRY(cudaEventRecord(c->ev[1], s));
+    LSR_CUDA_TRY(launch_sl_step(P, cfg->interp, c->phi, c->dist, c->active, c->n_active, c->out, c->d_bad, s));
+    LSR_CUDA_TRY(cudaEventRecord(c->ev[2], s));
+    if (int st = ensure_ids(&c->dirty, &c->cap_dirty, c->n_active)) return st;
+    if (c->n_active > 0)
+        LSR_CUDA_TRY(cudaMemcpyAsync(c->dirty, c->active, sizeof(int64_t) * c->n_active, cudaMemcpyDeviceToDevice, s));
+    c->n_dirty = c->n_active;
+    c->consistent = true;
+    LSR_CUDA_TRY(cudaMemcpyAsync(c->h_bad, c->d_bad, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+    LSR_CUDA_TRY(cudaStreamSynchronize(s));
+    cudaEventElapsedTime(&c->kernel_ms, c->ev[1], c->ev[2]);
+    cudaEventElapsedTime(&c->step_ms, c->ev[0], c->ev[2]);
+    if (*c->h_bad != ~0ULL) return numerical_error(c->grid, *c->h_bad, bad_node);
+    return LSR_OK;
+}
+
+int lsr_cuda_swap(lsr_cuda_ctx* c) {
+    if (!c) return set_err(LSR_ERR_CONFIG, "null context");
+    std::swap(c->phi, c->out);  // out and phi still differ only at `dirty`
+    return LSR_OK;
+}
+
+int lsr_cuda_last_times(lsr_cuda_ctx* c, float* kernel_ms, float* step_ms) {
+    if (!c) return set_err(LSR_ERR_CONFIG, "null context");
+    if (kernel_ms) *kernel_ms = c->kernel_ms;
+    if (step_ms) *step_ms = c->step_ms;
+    return LSR_OK;
+}
+
+int lsr_cuda_sl_step_device(const lsr_grid* grid, int32_t z_base, int32_t z_planes, const double* d_phi,
+                            const double* d_dist, const int64_t* d_active, int64_t n_active,
+                            const lsr_step_cfg* cfg, double energy_p, double* d_out, int64_t* d_bad_node,
+                            int64_t* d_halo_miss, void* stream) {
+    if (int st = check_grid(grid)) return st;
+    if (int st = check_cfg(cfg, energy_p)) return st;
+    if (z_base != 0 || z_planes != grid->dims[2])
+        return set_err(LSR_ERR_CONFIG, "sl_step_device: partial slabs not supported yet");
+    (void)d_halo_miss;
+    const SlParams P = make_params(*grid, *cfg, energy_p);
+    LSR_CUDA_TRY(launch_sl_step(P, cfg->interp, d_phi, d_dist, d_active, n_active, d_out,
+                                reinterpret_cast<unsigned long long*>(d_bad_node), static_cast<cudaStream_t>(stream)));
+    return LSR_OK;
+}
+
+// One-shot host entry. A per-thread context is cached across calls with the
+// same grid, so repeated calls do not re-allocate device memory.
+int lsr_cuda_sl_step_host(const lsr_grid* grid, const double* phi, const double* dist, const int64_t* active,
+                          int64_t n_active, const lsr_step_cfg* cfg, double energy_p, double* out,
+                          int64_t* bad_node) {
+    if (bad_node) *bad_node = -1;
+    if (int st = check_grid(grid)) return st;
+    if (int st = check_cfg(cfg, energy_p)) return st;
+    if (!phi || !dist || !out || (n_active > 0 && !active)) return set_err(LSR_ERR_CONFIG, "sl_step: null argument");
+    if (out == phi) return set_err(LSR_ERR_CONFIG, "sl_step: out must not alias phi");
+    struct Cache {
+        lsr_cuda_ctx* ctx = nullptr;
+        ~Cache() { lsr_cuda_destroy(ctx); }
+    };
+    thread_local Cache cache;
+    int dev = 0;
+    LSR_CUDA_TRY(cudaGetDevice(&dev));
+    if (cache.ctx && (std::memcmp(&cache.ctx->grid, grid, sizeof(lsr_grid)) != 0 || cache.ctx->device != dev)) {
+        lsr_cuda_destroy(cache.ctx);
+        cache.ctx = nullptr;
+    }
+    if (!cache.ctx)
+        if (int st = lsr_cuda_create(dev, grid, &cache.ctx)) return st;
+    lsr_cuda_ctx* c = cache.ctx;
+    const size_t bytes = sizeof(double) * c->n;
+    cudaStream_t s = c->stream;
+    LSR_CUDA_TRY(cudaMemcpyAsync(c->phi, phi, bytes, cudaMemcpyHostToDevice, s));
+    LSR_CUDA_TRY(cudaMemcpyAsync(c->dist, dist, bytes, cudaMemcpyHostToDevice, s));
+    if (int st = ensure_ids(&c->active, &c->cap_active, n_active)) return st;
+    if (n_active > 0)
+        LSR_CUDA_TRY(cudaMemcpyAsync(c->active, active, sizeof(int64_t) * n_active, cudaMemcpyHostToDevice, s));
+    c->n_active = n_active;
+    c->consistent = false;
+    int64_t bad = -1;
+    const int st = lsr_cuda_sl_step(c, cfg, energy_p, &bad);
+    if (bad_node) *bad_node = bad;
+    if (st != LSR_OK && st != LSR_ERR_NUMERICAL) return st;
+    const std::string msg = g_err;
+    // out is fully written even when a node went non-finite (evolve.cpp:110-117)
+    LSR_CUDA_TRY(cudaMemcpyAsync(out, c->out, bytes, cudaMemcpyDeviceToHost, s));
+    LSR_CUDA_TRY(cudaStreamSynchronize(s));
+    if (st == LSR_ERR_NUMERICAL) return set_err(st, msg);
+    return st;
+}
+
+int lsr_cuda_selftest_div_const(double c, int64_t n, uint64_t seed, int64_t* mismatches) {
+    if (!pow2_range(c)) return set_err(LSR_ERR_CONFIG, "selftest: divisor outside [2^-100, 2^100]");
+    unsigned long long* d = nullptr;
+    LSR_CUDA_TRY(cudaMalloc(&d, sizeof(unsigned long long)));
+    LSR_CUDA_TRY(cudaMemset(d, 0, sizeof(unsigned long long)));
+    LSR_CUDA_TRY(launch_div_selftest(c, 1.0 / c, seed, n, d));
+    unsigned long long h = 0;
+    LSR_CUDA_TRY(cudaMemcpy(&h, d, sizeof h, cudaMemcpyDeviceToHost));
+    cudaFree(d);
+    *mismatches = static_cast<int64_t>(h);
+    return LSR_OK;
+}
+
+}  // extern "C"

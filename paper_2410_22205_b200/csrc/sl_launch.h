@@ -1,0 +1,22 @@
+// Internal launcher interface between the C ABI (lsr_capi.cu) and the kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "sl_device.cuh"
+
+constexpr int kSlThreads = 128;
+
+// bumps the process-wide launch counter (lsr_cuda_kernel_launches)
+void lsr_note_launch();
+
+cudaError_t launch_sl_step(const lsr_dev::SlParams& P, int kind, const double* phi, const double* dist,
+                           const int64_t* active, long long n_active, double* out, unsigned long long* bad,
+                           cudaStream_t stream);
+
+cudaError_t launch_resync(const double* phi, double* out, const int64_t* ids, long long n, cudaStream_t stream);
+
+cudaError_t launch_div_selftest(double c, double rc, unsigned long long seed, long long n,
+                                unsigned long long* mismatches);

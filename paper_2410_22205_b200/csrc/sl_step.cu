@@ -1,0 +1,112 @@
+// sl_step.cu — sm_100a kernels of the narrow-band semi-Lagrangian step and
+// their launchers. Replaces the OpenMP loop of lsr::sl_step
+// (/root/reference/proj/src/evolve.cpp:56-111) and the O(N) field copy at
+// evolve.cpp:50 (see the sparse resync below).
+//
+// Layout in HBM: phi, out, d are dense fp64 arrays, x fastest (grid.hpp:19);
+// active ids are ascending int64 (grid.hpp:82). One thread owns one active
+// node: consecutive lanes take consecutive ids, i.e. neighbouring nodes of
+// the same x-row, so their WENO stencils overlap and the 4x4x4 gathers hit
+// L1 and coalesce into few sectors per warp load.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "sl_device.cuh"
+#include "sl_launch.h"
+
+namespace lsr_dev {
+
+template <int DIM, int KIND>
+__global__ void __launch_bounds__(kSlThreads) sl_step_kernel(SlParams P, const double* __restrict__ phi,
+                                                             const double* __restrict__ dist,
+                                                             const int64_t* __restrict__ active,
+                                                             long long n_active, double* __restrict__ out,
+                                                             unsigned long long* __restrict__ bad) {
+    const long long a = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (a >= n_active) return;
+    const long long id = __ldg(active + a);
+    int i, j, k;
+    if (P.nxy * P.nz < (1LL << 31)) {  // Grid::unflatten (grid.hpp:22-27) in 32 bits when it fits
+        const unsigned u = static_cast<unsigned>(id);
+        const unsigned row = u / static_cast<unsigned>(P.nx);
+        i = static_cast<int>(u - row * static_cast<unsigned>(P.nx));
+        k = static_cast<int>(row / static_cast<unsigned>(P.ny));
+        j = static_cast<int>(row - static_cast<unsigned>(k) * static_cast<unsigned>(P.ny));
+    } else {
+        i = static_cast<int>(id % P.nx);
+        j = static_cast<int>((id / P.nx) % P.ny);
+        k = static_cast<int>(id / P.nxy);
+    }
+    const double next = sl_node<DIM, KIND>(P, phi, dist, id, i, j, k);
+    if (!isfinite(next)) atomicMin(bad, static_cast<unsigned long long>(id));
+    out[id] = next;
+}
+
+// out[ids] = phi[ids]: re-establishes "out equals phi off the active set"
+// after the previous step wrote out (or after a swap) without the O(N) copy.
+__global__ void resync_kernel(const double* __restrict__ phi, double* __restrict__ out,
+                              const int64_t* __restrict__ ids, long long n) {
+    const long long a = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (a >= n) return;
+    const long long id = __ldg(ids + a);
+    out[id] = __ldg(phi + id);
+}
+
+// Self-test of div_const against the hardware IEEE division: a splitmix64
+// stream of bit patterns (all exponents, signs, zeros, subnormals, inf/NaN)
+// divided by c; counts quotients whose bits differ.
+__global__ void div_selftest_kernel(double c, double rc, unsigned long long seed, long long n,
+                                    unsigned long long* mismatches) {
+    const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    unsigned long long bad = 0;
+    for (long long i = t; i < n; i += static_cast<long long>(gridDim.x) * blockDim.x) {
+        unsigned long long z = seed + 0x9E3779B97F4A7C15ULL * static_cast<unsigned long long>(i + 1);
+        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+        z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+        z ^= z >> 31;
+        double a = __longlong_as_double(static_cast<long long>(z));
+        if ((i & 3) == 1) a = static_cast<double>(z >> 11) * 0x1.0p-53;  // [0,1): the common case
+        if ((i & 3) == 2) a = (static_cast<double>(z >> 11) * 0x1.0p-53) * 1e-3;
+        const double fast = div_const(a, c, rc, 1);
+        const double ref = a / c;
+        const bool same = __double_as_longlong(fast) == __double_as_longlong(ref) || (isnan(fast) && isnan(ref));
+        bad += same ? 0 : 1;
+    }
+    if (bad) atomicAdd(mismatches, bad);
+}
+
+}  // namespace lsr_dev
+
+using namespace lsr_dev;
+
+cudaError_t launch_div_selftest(double c, double rc, unsigned long long seed, long long n,
+                                unsigned long long* mismatches) {
+    div_selftest_kernel<<<148 * 8, 256>>>(c, rc, seed, n, mismatches);
+    lsr_note_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_sl_step(const SlParams& P, int kind, const double* phi, const double* dist,
+                           const int64_t* active, long long n_active, double* out, unsigned long long* bad,
+                           cudaStream_t stream) {
+    if (n_active <= 0) return cudaSuccess;
+    const unsigned blocks = static_cast<unsigned>((n_active + kSlThreads - 1) / kSlThreads);
+    if (P.dim == 2) {
+        if (kind == 0) sl_step_kernel<2, 0><<<blocks, kSlThreads, 0, stream>>>(P, phi, dist, active, n_active, out, bad);
+        else sl_step_kernel<2, 1><<<blocks, kSlThreads, 0, stream>>>(P, phi, dist, active, n_active, out, bad);
+    } else {
+        if (kind == 0) sl_step_kernel<3, 0><<<blocks, kSlThreads, 0, stream>>>(P, phi, dist, active, n_active, out, bad);
+        else sl_step_kernel<3, 1><<<blocks, kSlThreads, 0, stream>>>(P, phi, dist, active, n_active, out, bad);
+    }
+    lsr_note_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_resync(const double* phi, double* out, const int64_t* ids, long long n, cudaStream_t stream) {
+    if (n <= 0) return cudaSuccess;
+    const unsigned blocks = static_cast<unsigned>((n + 255) / 256);
+    resync_kernel<<<blocks, 256, 0, stream>>>(phi, out, ids, n);
+    lsr_note_launch();
+    return cudaGetLastError();
+}

@@ -1,0 +1,190 @@
+"""Generate the golden fixtures under tests/golden/ from the REFERENCE ITSELF.
+
+Run in the build container (where /root/reference exists and oracle/_ref is
+built): ``python tests/golden/make_golden.py``. Every expected output in the
+fixtures comes from the unmodified reference library (oracle/_ref/liblsr_ref.so,
+built from /root/reference/proj/src by oracle/Makefile):
+
+  sl_*.npz      lsr::ref::sl_step (reference.cpp:53) on seeded inputs; the
+                distance field is lsr::build_distance_field (distance.cpp:144)
+                of a seeded cloud, the band is lsr::narrow_band (grid.cpp:76)
+                and E_2 is lsr::surface_energy (metrics.cpp:186) — i.e. the
+                inputs the driver loop (driver.cpp:187-194) would feed.
+  weno_1d.npz   lsr::weno_1d (interp.cpp:16) on random stencils.
+  interp_*.npz  lsr::interp (interp.cpp:113) at random points.
+  basis.npz     lsr::tangent_basis (evolve.cpp:10) on random gradients.
+  band_*.npz    lsr::narrow_band state/active/tube.
+
+The inputs are stored with the outputs, so the fixtures never need the
+reference at test time (the GPU box has no /root/reference).
+"""
+from __future__ import annotations
+
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, ROOT)
+
+from oracle.bindings import Reference, build  # noqa: E402
+
+OUT = os.path.dirname(os.path.abspath(__file__))
+
+
+def grid(n, dim, lo=-1.0, hi=1.0):
+    dx = (hi - lo) / (n - 1)
+    if dim == 2:
+        return dict(dim=2, dims=[n, n, 1], origin=[lo, lo, 0.0], dx=dx)
+    return dict(dim=3, dims=[n, n, n], origin=[lo, lo, lo], dx=dx)
+
+
+def mesh(g):
+    ax = [g["origin"][d] + np.arange(g["dims"][d]) * g["dx"] for d in range(3)]
+    z, y, x = np.meshgrid(ax[2], ax[1], ax[0], indexing="ij")
+    return x.ravel(), y.ravel(), z.ravel()
+
+
+def cloud_circle(n, r, rng):
+    th = 2 * np.pi * rng.random(n)
+    return np.stack([r * np.cos(th), r * np.sin(th), np.zeros(n)], 1)
+
+
+def cloud_sphere(n, r, rng, c=(0, 0, 0)):
+    z = 2 * rng.random(n) - 1
+    th = 2 * np.pi * rng.random(n)
+    s = np.sqrt(1 - z * z)
+    return np.stack([c[0] + r * s * np.cos(th), c[1] + r * s * np.sin(th), c[2] + r * z], 1)
+
+
+def cloud_torus(n, R, r, sigma, rng):
+    u = 2 * np.pi * rng.random(n)
+    v = 2 * np.pi * rng.random(n)
+    p = np.stack([(R + r * np.cos(v)) * np.cos(u), (R + r * np.cos(v)) * np.sin(u), r * np.sin(v)], 1)
+    return p + sigma * rng.standard_normal(p.shape)
+
+
+def make_sl_case(R, name, g, phi, pts, perturb=0.0, seed=0, extra=None, energy=None):
+    rng = np.random.default_rng(seed)
+    d, exact, sent, rounds = R.build_distance(g, pts, g["dim"])
+    if perturb:
+        phi = phi + perturb * g["dx"] * rng.standard_normal(phi.shape)
+    gam = (6.0 if g["dim"] == 3 else 4.0) * g["dx"]
+    beta = gam / 2
+    _, active, tube = R.narrow_band(g, phi, gam)
+    # the reference energy aborts (OpenMP + OutOfDomainError) when the front
+    # touches the hull, so the hull cases pass a fixed E_p instead
+    e2 = R.surface_energy(g, phi, d, 2, 5) if energy is None else energy
+    rec = dict(dims=np.array(g["dims"]), origin=np.array(g["origin"]), dx=g["dx"], dim=g["dim"], phi=phi, dist=d,
+               active=active, gamma=gam, beta=beta, e2=e2)
+    cases = []
+    for interp in (0, 1):
+        for p, delta in ((1, 0.0), (2, 1.0), (2, 0.5)):
+            cfg = dict(p=p, interp=interp, delta=delta, dt=0.25 * g["dx"], fallback_c=1e-3, fallback_alpha=1.0,
+                       gamma=gam, beta=beta)
+            out, st, msg, _ = R.sl_step(g, phi, d, active, cfg, e2, serial=True)
+            assert st == 0, msg
+            out2, st2, _, _ = R.sl_step(g, phi, d, active, cfg, e2, serial=False)
+            assert st2 == 0 and np.array_equal(out.view(np.int64), out2.view(np.int64))
+            assert np.array_equal(np.delete(out, active), np.delete(phi, active))
+            cases.append((interp, p, delta, out[active]))
+    rec["case_interp"] = np.array([c[0] for c in cases])
+    rec["case_p"] = np.array([c[1] for c in cases])
+    rec["case_delta"] = np.array([c[2] for c in cases])
+    rec["case_out"] = np.stack([c[3] for c in cases])
+    if extra:
+        rec.update(extra)
+    np.savez_compressed(os.path.join(OUT, f"sl_{name}.npz"), **rec)
+    print(name, "nodes", phi.size, "active", active.size, "E2", e2)
+
+
+def main():
+    build(ref=True)
+    R = Reference()
+    rng = np.random.default_rng(2410_22205)
+
+    # 2d circle (config 1 shape at reduced size): cloud r=0.3, phi0 = |x|-0.9
+    g = grid(65, 2)
+    x, y, _ = mesh(g)
+    make_sl_case(R, "circle2d", g, np.sqrt(x * x + y * y) - 0.9, cloud_circle(200, 0.3, rng))
+    # 2d, band reaching the grid hull (stencil fallback + clamped feet)
+    g = grid(41, 2)
+    x, y, _ = mesh(g)
+    make_sl_case(R, "hull2d", g, np.sqrt(x * x + y * y) - 1.0, cloud_circle(150, 0.6, rng), perturb=0.3, seed=3,
+                 energy=0.75)
+    # 3d sphere (config 2 shape): 20k -> 4k points at r = 0.5, phi0 = |x| - 0.9
+    g = grid(28, 3)
+    x, y, z = mesh(g)
+    make_sl_case(R, "sphere3d", g, np.sqrt(x * x + y * y + z * z) - 0.9, cloud_sphere(4000, 0.5, rng))
+    # 3d noisy torus (config 3 shape), perturbed phi for varied stencils
+    g = grid(30, 3)
+    x, y, z = mesh(g)
+    make_sl_case(R, "torus3d", g, np.sqrt(x * x + y * y + z * z) - 0.6,
+                 cloud_torus(6000, 0.5, 0.2, 0.5 * g["dx"], rng), perturb=0.2, seed=5)
+    # 3d band touching the hull
+    g = grid(22, 3)
+    x, y, z = mesh(g)
+    make_sl_case(R, "hull3d", g, np.sqrt(x * x + y * y + z * z) - 1.05, cloud_sphere(3000, 0.7, rng),
+                 perturb=0.3, seed=7, energy=1.25)
+    # 3d with flat patches: the gradient fallback (evolve.cpp:65-78) fires
+    g = grid(24, 3)
+    x, y, z = mesh(g)
+    phi = np.sqrt(x * x + y * y + z * z) - 0.6
+    phi = np.where(np.abs(x) < 0.25, np.round(phi / (0.5 * g["dx"])) * (0.5 * g["dx"]), phi)
+    phi[(np.abs(x) < 0.3) & (z > 0)] = 0.01 * g["dx"]
+    make_sl_case(R, "flat3d", g, phi, cloud_sphere(3000, 0.45, rng))
+
+    # weno_1d on random stencils, including flat and kinked data
+    n = 4000
+    v = rng.standard_normal((n, 4)) * 10.0 ** rng.integers(-6, 3, (n, 1))
+    v[:200] = v[:200, :1]  # constant stencils
+    v[200:400, 1:] = v[200:400, 1:2] + np.arange(3) * 0.1  # linear right part
+    dx = 10.0 ** rng.uniform(-3, -1, n)
+    th = rng.random(n)
+    th[:50] = 0.0
+    th[50:100] = 1.0
+    w = np.array([R.weno_1d(v[i], dx[i], th[i]) for i in range(n)])
+    np.savez_compressed(os.path.join(OUT, "weno_1d.npz"), v=v, dx=dx, theta=th, out=w)
+
+    # interp at random points (both kinds, 2d and 3d, including the hull and nodes)
+    for dim, nn in ((2, 23), (3, 13)):
+        g = grid(nn, dim)
+        x, y, z = mesh(g)
+        f = np.sin(3 * x) * np.cos(2 * y) + z * z - 0.3 * x * y
+        m = 3000
+        pts = rng.uniform(-1, 1, (m, 3))
+        if dim == 2:
+            pts[:, 2] = 0.0
+        pts[:100] = np.stack(mesh(g), 1)[rng.integers(0, f.size, 100)]  # nodes
+        pts[100:150, 0] = 1.0  # upper hull -> last cell
+        pts[150:200, 1] = -1.0
+        outs = {k: R.interp(k, g, f, pts) for k in (0, 1)}
+        np.savez_compressed(os.path.join(OUT, f"interp_{dim}d.npz"), dims=np.array(g["dims"]),
+                            origin=np.array(g["origin"]), dx=g["dx"], dim=dim, f=f, pts=pts, q1=outs[0], weno=outs[1])
+
+    # tangent bases
+    gr = rng.standard_normal((2000, 3))
+    gr[:20] = [0, 1, 0]
+    gr[20:40, 0] = 0
+    gr[20:40, 2] = 1e-16
+    b3 = [R.tangent_basis(3, gr[i]) for i in range(len(gr))]
+    b2 = [R.tangent_basis(2, np.array([gr[i, 0], gr[i, 1], 0.0])) for i in range(len(gr))]
+    np.savez_compressed(os.path.join(OUT, "basis.npz"), grad=gr, v1_3=np.array([b[0] for b in b3]),
+                        v2_3=np.array([b[1] for b in b3]), v1_2=np.array([b[0] for b in b2]))
+
+    # narrow band classification
+    for dim, nn in ((2, 57), (3, 26)):
+        g = grid(nn, dim)
+        x, y, z = mesh(g)
+        phi = np.sqrt(x * x + y * y + z * z) - 0.55 + 0.05 * np.sin(7 * x)
+        gam = (6.0 if dim == 3 else 4.0) * g["dx"]
+        st, act, tube = R.narrow_band(g, phi, gam, serial=True)
+        np.savez_compressed(os.path.join(OUT, f"band_{dim}d.npz"), dims=np.array(g["dims"]),
+                            origin=np.array(g["origin"]), dx=g["dx"], dim=dim, phi=phi, gamma=gam, state=st,
+                            active=act, tube=tube)
+    print("golden fixtures written to", OUT)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,221 @@
+"""GPU parity tests of the sm_100a SL step (through the C ABI).
+
+Bar: bit-exact (0 differing bits) against the reference's outputs (golden
+fixtures produced by the reference itself) and against the oracle
+restatement on fresh seeded inputs; plus the reference's own known-answer
+tests (test_evolve.cpp) and size-independent properties at full size.
+"""
+import numpy as np
+import pytest
+
+from conftest import SL_CASES, bits, golden_grid, load_golden
+
+pytestmark = pytest.mark.gpu
+
+
+def _grid_obj(lsr, g):
+    return lsr.Grid(g["dim"], tuple(g["origin"]), g["dx"], tuple(g["dims"]))
+
+
+def _cfg(lsr, rec, c):
+    bp = lsr.BandParams(float(rec["gamma"]), float(rec["beta"]))
+    return lsr.StepConfig(p=int(rec["case_p"][c]), delta=float(rec["case_delta"][c]), dt=0.25 * float(rec["dx"]),
+                          interp=lsr.InterpolatorKind(int(rec["case_interp"][c])), band=bp)
+
+
+def _run(lsr, g, phi, dist, active, cfg, e):
+    out = lsr.ScalarField(g)
+    lsr.sl_step(lsr.ScalarField(g, phi), lsr.DistanceField(lsr.ScalarField(g, dist)), lsr.BandMask(g, active=active),
+                cfg, e, out)
+    return out.values
+
+
+@pytest.mark.parametrize("case", SL_CASES)
+def test_sl_step_bit_exact_vs_reference_golden(gpu, case):
+    lsr = gpu
+    rec = load_golden(f"sl_{case}.npz")
+    g = _grid_obj(lsr, golden_grid(rec))
+    n0 = lsr.kernel_launches()
+    for c in range(len(rec["case_p"])):
+        out = _run(lsr, g, rec["phi"], rec["dist"], rec["active"], _cfg(lsr, rec, c), float(rec["e2"]))
+        diff = np.count_nonzero(bits(out[rec["active"]]) != bits(rec["case_out"][c]))
+        assert diff == 0, f"{case}[{c}]: {diff} active nodes differ"
+        mask = np.ones(out.size, bool)
+        mask[rec["active"]] = False
+        assert np.array_equal(bits(out[mask]), bits(rec["phi"][mask]))
+    assert lsr.kernel_launches() > n0
+
+
+@pytest.mark.parametrize("dim,n,interp,p,delta,seed", [
+    (2, 257, 0, 1, 0.0, 1), (2, 257, 1, 2, 1.0, 2),
+    (3, 64, 0, 1, 0.0, 3), (3, 64, 0, 2, 1.0, 4), (3, 64, 1, 1, 0.0, 5), (3, 64, 1, 2, 1.0, 6),
+    (3, 80, 1, 2, 0.3, 7),
+])
+def test_sl_step_bit_exact_vs_oracle_seeded(gpu, oracle, dim, n, interp, p, delta, seed):
+    lsr = gpu
+    rng = np.random.default_rng(seed)
+    g = lsr._api.cube_grid(n, dim)
+    x, y, z = (a.ravel() for a in g.mesh())
+    phi = np.sqrt(x * x + y * y + z * z) - 0.6 + 0.25 * g.dx * rng.standard_normal(x.size)
+    dist = np.abs(np.sqrt((x - 0.07) ** 2 + (y + 0.03) ** 2 + z * z) - 0.35) + 0.01 * rng.random(x.size)
+    bp = lsr.default_band_params(dim, g.dx)
+    active = np.flatnonzero(np.abs(phi) < bp.gamma).astype(np.int64)
+    cfg = lsr.StepConfig(p=p, delta=delta, dt=0.25 * g.dx, interp=lsr.InterpolatorKind(interp), band=bp)
+    e = 0.7
+    got = _run(lsr, g, phi, dist, active, cfg, e)
+    ref, st, _ = oracle.sl_step(dict(dim=dim, dims=g.dims, origin=g.origin, dx=g.dx), phi, dist, active,
+                                dict(p=p, interp=interp, delta=delta, dt=cfg.dt, fallback_c=1e-3, fallback_alpha=1.0,
+                                     gamma=bp.gamma, beta=bp.beta), e)
+    assert st == 0
+    diff = np.count_nonzero(bits(got) != bits(ref))
+    assert diff == 0, f"{diff} of {active.size} active nodes differ"
+
+
+def test_identity_step_constant_distance(gpu):
+    """test_evolve.cpp:78-92: d constant, delta = 0 -> identity on active nodes."""
+    lsr = gpu
+    g = lsr.Grid(2, (-1.3, -1.3, 0.0), 0.1, (27, 27, 1))
+    x, y, _ = (a.ravel() for a in g.mesh())
+    phi = np.sqrt(x * x + y * y) - 0.7
+    bp = lsr.default_band_params(2, g.dx)
+    active = np.flatnonzero(np.abs(phi) < bp.gamma).astype(np.int64)
+    cfg = lsr.StepConfig(p=1, delta=0.0, dt=0.025, band=bp)
+    out = _run(lsr, g, phi, np.full(x.size, 0.5), active, cfg, 1.0)
+    assert np.max(np.abs(out - phi)) < 1e-12
+
+
+def test_pure_advection_shifts_by_dt(gpu):
+    """test_evolve.cpp:94-112: phi = x, d = x + 10, dt = 0.1 -> x + 0.1 where c = 1."""
+    lsr = gpu
+    for interp in (lsr.InterpolatorKind.Q1, lsr.InterpolatorKind.Weno):
+        g = lsr.Grid(2, (-1.15, -1.15, 0.0), 0.05, (47, 47, 1))
+        x, y, _ = (a.ravel() for a in g.mesh())
+        bp = lsr.default_band_params(2, g.dx)
+        active = np.flatnonzero(np.abs(x) < bp.gamma).astype(np.int64)
+        cfg = lsr.StepConfig(p=1, delta=0.0, dt=0.1, band=bp, interp=interp)
+        out = _run(lsr, g, x.copy(), x + 10.0, active, cfg, 1.0)
+        i, j, _ = g.unflatten(active)
+        sel = (i >= 2) & (i <= 44) & (j >= 2) & (j <= 44) & (np.abs(x[active]) <= bp.beta)
+        assert sel.sum() > 20
+        np.testing.assert_allclose(out[active][sel], x[active][sel] + 0.1, rtol=1e-12, atol=1e-12)
+
+
+def test_zero_field_fallback_stays_zero(gpu):
+    """test_evolve.cpp:114-123."""
+    lsr = gpu
+    g = lsr.Grid(2, (-1.3, -1.3, 0.0), 0.1, (27, 27, 1))
+    x, y, _ = (a.ravel() for a in g.mesh())
+    bp = lsr.default_band_params(2, g.dx)
+    active = np.arange(x.size, dtype=np.int64)
+    out = _run(lsr, g, np.zeros(x.size), 1.0 + y, active, lsr.StepConfig(p=1, dt=0.05, band=bp), 1.0)
+    assert np.all(out == 0.0)
+
+
+def test_affine_diffusion_cancels_3d(gpu):
+    """test_evolve.cpp:151-176: p=2, delta=1, d = 0.25, E = 0.5, affine phi."""
+    lsr = gpu
+    g = lsr.Grid(3, (-1.375, -1.375, -1.375), 0.125, (23, 23, 23))
+    x, y, z = (a.ravel() for a in g.mesh())
+    phi = 0.3 * x + 0.2 * y - 0.5 * z
+    bp = lsr.default_band_params(3, g.dx)
+    active = np.flatnonzero(np.abs(phi) < bp.gamma).astype(np.int64)
+    cfg = lsr.StepConfig(p=2, delta=1.0, dt=0.05, band=bp)
+    out = _run(lsr, g, phi, np.full(x.size, 0.25), active, cfg, 0.5)
+    i, j, k = g.unflatten(active)
+    inner = (i >= 2) & (i <= 20) & (j >= 2) & (j <= 20) & (k >= 2) & (k <= 20)
+    assert np.max(np.abs(out[active][inner] - phi[active][inner])) < 1e-10
+
+
+def test_nan_distance_raises_numerical_error(gpu, oracle):
+    """test_evolve.cpp:195-210; out fully written, smallest bad id reported."""
+    lsr = gpu
+    g = lsr._api.cube_grid(41, 2)
+    x, y, _ = (a.ravel() for a in g.mesh())
+    phi = np.sqrt(x * x + y * y) - 0.6
+    dist = np.full(x.size, 0.5)
+    bp = lsr.default_band_params(2, g.dx)
+    active = np.flatnonzero(np.abs(phi) < bp.gamma).astype(np.int64)
+    dist[active[len(active) // 2]] = np.nan
+    cfg = lsr.StepConfig(p=2, delta=1.0, dt=0.02, band=bp)
+    out = lsr.ScalarField(g)
+    with pytest.raises(lsr.NumericalError, match="non-finite update at node"):
+        lsr.sl_step(lsr.ScalarField(g, phi), lsr.DistanceField(lsr.ScalarField(g, dist)),
+                    lsr.BandMask(g, active=active), cfg, 1.0, out)
+    ref, st, bad = oracle.sl_step(dict(dim=2, dims=g.dims, origin=g.origin, dx=g.dx), phi, dist, active,
+                                  dict(p=2, interp=1, delta=1.0, dt=0.02, fallback_c=1e-3, fallback_alpha=1.0,
+                                       gamma=bp.gamma, beta=bp.beta), 1.0)
+    assert st == 3
+    assert np.array_equal(bits(out.values), bits(ref))
+    c = lsr.Context(g)
+    c.upload(0, phi)
+    c.upload(1, dist)
+    c.set_active(active)
+    with pytest.raises(lsr.NumericalError):
+        c.sl_step(cfg, 1.0)
+    assert c.bad_node == bad
+
+
+@pytest.mark.parametrize("c", [None, 3.0])
+def test_constant_divisor_division_is_ieee(gpu, c):
+    """div_const (sl_device.cuh) == hardware IEEE division, bit for bit."""
+    lsr = gpu
+    g = lsr._api.cube_grid(513, 3)
+    divisors = [c] if c else [g.dx, g.dx * g.dx, lsr._api.cube_grid(1025, 3).dx ** 2, 2.0 / 127, 0.1, 1e-5]
+    for d in divisors:
+        assert lsr._api.selftest_div_const(d, 1 << 26, seed=int(d * 1e9) + 1) == 0, d
+
+
+def test_context_multistep_swap_matches_oracle(gpu, oracle):
+    """Device-resident loop: K ping-pong steps with changing active sets; the
+    sparse resync must reproduce the reference's full copy (evolve.cpp:50)."""
+    lsr = gpu
+    g = lsr._api.cube_grid(48, 3)
+    x, y, z = (a.ravel() for a in g.mesh())
+    phi = np.sqrt(x * x + y * y + z * z) - 0.55
+    dist = np.abs(np.sqrt(x * x + y * y + z * z) - 0.3) + 1e-3
+    bp = lsr.default_band_params(3, g.dx)
+    cfg = lsr.StepConfig(p=2, delta=1.0, dt=0.25 * g.dx, band=bp)
+    ccfg = dict(p=2, interp=1, delta=1.0, dt=cfg.dt, fallback_c=1e-3, fallback_alpha=1.0, gamma=bp.gamma,
+                beta=bp.beta)
+    gd = dict(dim=3, dims=g.dims, origin=g.origin, dx=g.dx)
+    ctx = lsr.Context(g)
+    ctx.upload(0, phi)
+    ctx.upload(1, dist)
+    ref = phi.copy()
+    for step in range(4):
+        active = np.flatnonzero(np.abs(ref) < bp.gamma * (1.0 - 0.15 * step)).astype(np.int64)
+        ctx.set_active(active)
+        ctx.sl_step(cfg, 0.9)
+        ref, st, _ = oracle.sl_step(gd, ref, dist, active, ccfg, 0.9)
+        assert st == 0
+        got = ctx.download(2)
+        assert np.array_equal(bits(got), bits(ref)), step
+        ctx.swap()
+        assert np.array_equal(bits(ctx.download(0)), bits(ref))
+
+
+def test_full_size_sampled_subset_512(gpu, oracle):
+    """Config-4 size (512^3): GPU vs oracle on a random subset of the band
+    (sl_step reads only mask.active, SURVEY §7 'sampled oracle')."""
+    lsr = gpu
+    rng = np.random.default_rng(11)
+    g = lsr._api.cube_grid(512, 3)
+    ax = g.axes()
+    r = np.sqrt(ax[0][None, None, :] ** 2 + ax[1][None, :, None] ** 2 + ax[2][:, None, None] ** 2).ravel()
+    phi = r - 0.9
+    dist = np.abs(r - 0.5) + 1e-3 * np.cos(7 * r)
+    bp = lsr.default_band_params(3, g.dx)
+    band = np.flatnonzero(np.abs(phi) < bp.gamma).astype(np.int64)
+    sub = np.sort(rng.choice(band, 20000, replace=False)).astype(np.int64)
+    cfg = lsr.StepConfig(p=2, delta=1.0, dt=0.25 * g.dx, band=bp)
+    got = _run(lsr, g, phi, dist, sub, cfg, 1.3)
+    ref, st, _ = oracle.sl_step(dict(dim=3, dims=g.dims, origin=g.origin, dx=g.dx), phi, dist, sub,
+                                dict(p=2, interp=1, delta=1.0, dt=cfg.dt, fallback_c=1e-3, fallback_alpha=1.0,
+                                     gamma=bp.gamma, beta=bp.beta), 1.3, nthreads=0)
+    assert st == 0
+    assert np.array_equal(bits(got[sub]), bits(ref[sub]))
+    # whole band: property checks (finite, unchanged off-band, bounded update)
+    out = _run(lsr, g, phi, dist, band, cfg, 1.3)
+    assert np.all(np.isfinite(out[band]))
+    assert np.array_equal(bits(np.delete(out, band)), bits(np.delete(phi, band)))
+    assert np.max(np.abs(out[band] - phi[band])) < 2 * g.dx

@@ -1,0 +1,49 @@
+"""Kernel-only microbenchmark of the SL step at 512^3 on analytic inputs
+(phi = |x| - 0.9, d = ||x| - 0.5| + ripple). Development aid; the contract
+benchmark is bench.py."""
+import argparse
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2410_22205_b200 as lsr  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--n", type=int, default=512)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--interp", type=int, default=1)
+    ap.add_argument("--radius", type=float, default=0.9)
+    a = ap.parse_args()
+    g = lsr._api.cube_grid(a.n, 3)
+    ax = g.axes()
+    r = np.sqrt(ax[0][None, None, :] ** 2 + ax[1][None, :, None] ** 2 + ax[2][:, None, None] ** 2).ravel()
+    phi = r - a.radius
+    dist = np.abs(r - 0.5) + 1e-3 * np.cos(40 * r)
+    bp = lsr.default_band_params(3, g.dx)
+    band = np.flatnonzero(np.abs(phi) < bp.gamma).astype(np.int64)
+    cfg = lsr.StepConfig(p=2, delta=1.0, dt=0.25 * g.dx, band=bp, interp=lsr.InterpolatorKind(a.interp))
+    ctx = lsr.Context(g)
+    ctx.upload(0, phi)
+    ctx.upload(1, dist)
+    ctx.set_active(band)
+    ks, ss = [], []
+    for s in range(a.steps + 3):
+        ctx.sl_step(cfg, 1.3)
+        k, st = ctx.last_times()
+        if s >= 3:
+            ks.append(k)
+            ss.append(st)
+    kmed = float(np.median(ks))
+    print(json.dumps(dict(n=a.n, interp=a.interp, active=int(band.size), kernel_ms=kmed, step_ms=float(np.median(ss)),
+                          node_updates_per_s=band.size / (kmed * 1e-3),
+                          kernel_ms_all=[round(x, 4) for x in ks])))
+
+
+if __name__ == "__main__":
+    main()
