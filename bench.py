@@ -1,0 +1,487 @@
+"""bench.py — SL narrow-band node-updates/s (WENO, 512^3, fp64) on B200.
+
+Workload (BASELINE.json config 4, the headline): bumpy sphere
+r(t,p) = 0.5(1 + 0.1 sin 5t cos 4p), 1,000,000 seeded points, 10x denser at
+the poles; grid 512^3 on [-1,1]^3 (dx = 2/511); d = lsr::build_distance_field
+of the cloud (computed on the GPU, bit-identical to the reference's);
+phi^0 = |x| - 0.9; band = |phi| < gamma = 6dx; E_2 = lsr::surface_energy
+(GPU); p = 2, delta = 1 (Table 1 run r >= 3), WENO, dt = dx/4.
+
+One step = one lsr::sl_step over the whole band (resync of the double
+buffer + the SL kernel), inputs resident in HBM; successive steps ping-pong
+phi <-> out on the same band. L2 (126 MB) is flushed by a 256 MB write
+between timed steps. Units = active node-updates.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N > 1 (torchrun): z-slab decomposition — each rank owns a band-balanced
+range of z-planes, updates only its active nodes, and exchanges halo planes
+of phi^{n+1} with its neighbours over NCCL after every step.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "SL narrow-band node-updates/s (WENO, 512^3, fp64)"
+UNIT = "node-updates/s"
+BYTES_PER_UPDATE = {("weno", 3): 2176, ("q1", 3): 384, ("weno", 2): 352, ("q1", 2): 160}
+COMPULSORY_BYTES = 32
+DFMA_PER_UPDATE_WENO3 = None  # counted by ncu, see DESIGN.md
+
+CONFIGS = {
+    # id: (n, dim, cloud config, points, sigma in dx, interp, phi0 radius, p, delta)
+    4: dict(n=512, dim=3, cloud=4, points=1_000_000, sigma=0.0, interp=1, r0=0.9, p=2, delta=1.0,
+            name="bumpy-sphere-512"),
+    3: dict(n=256, dim=3, cloud=3, points=100_000, sigma=0.5, interp=1, r0=0.9, p=2, delta=1.0,
+            name="torus-256"),
+    2: dict(n=128, dim=3, cloud=2, points=20_000, sigma=0.0, interp=0, r0=0.9, p=2, delta=1.0,
+            name="sphere-128"),
+}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def traffic_per_update():
+    """DRAM bytes per node-update of the SL kernel from the committed ncu
+    capture (profiles/sl_step_traffic.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "sl_step_traffic.json")) as f:
+            t = json.load(f)
+        return float(t["dram_bytes_per_update"]), t
+    except Exception:
+        return None, None
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.thread.join(timeout=2)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 4 + i and r[4 + i] == "Active"})
+        pw = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows), "power_w_max": max(pw) if pw else None}
+
+
+# ---------------------------------------------------------------------------
+# workload construction
+
+
+def make_inputs(lsr, cfg, seed=2410):
+    g = lsr.cube_grid(cfg["n"], cfg["dim"])
+    pts = lsr.cloud_generate(cfg["cloud"], cfg["points"], seed=seed, sigma=cfg["sigma"] * g.dx)
+    ax = g.axes()
+    if cfg["dim"] == 3:
+        r = np.sqrt(ax[0][None, None, :] ** 2 + ax[1][None, :, None] ** 2 + ax[2][:, None, None] ** 2)
+    else:
+        r = np.sqrt(ax[0][None, :] ** 2 + ax[1][:, None] ** 2)
+    phi = (r - cfg["r0"]).reshape(-1)
+    bp = lsr.default_band_params(cfg["dim"], g.dx)
+    active = np.flatnonzero(np.abs(phi) < bp.gamma).astype(np.int64)  # narrow_band's ACTIVE set (grid.cpp:85-88)
+    step = lsr.StepConfig(p=cfg["p"], delta=cfg["delta"], dt=0.25 * g.dx, interp=lsr.InterpolatorKind(cfg["interp"]),
+                          band=bp)
+    return g, pts, phi, active, step
+
+
+def z_partition(active: np.ndarray, nxy: int, nz: int, world: int):
+    """Band-balanced z-slab cuts: rank r owns planes [cuts[r], cuts[r+1]),
+    chosen on the cumulative per-plane active count."""
+    k = active // nxy
+    per_plane = np.bincount(k, minlength=nz)
+    cum = np.cumsum(per_plane)
+    total = int(cum[-1]) if cum.size else 0
+    cuts = [0]
+    for r in range(1, world):
+        cuts.append(int(np.searchsorted(cum, total * r / world, side="left")) + 1)
+    cuts.append(nz)
+    cuts = np.maximum.accumulate(np.array(cuts))
+    return cuts
+
+
+# ---------------------------------------------------------------------------
+
+
+def run_ours(args):
+    import torch
+
+    import paper_2410_22205_b200 as lsr
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = CONFIGS[args.config]
+    g, pts, phi, active, step = make_inputs(lsr, cfg)
+    nxy = g.dims[0] * g.dims[1]
+    stream = torch.cuda.current_stream()
+    ctx = lsr.Context(g, device=local)
+    ctx.set_stream(stream.cuda_stream)
+    t0 = time.perf_counter()
+    sentinel, rounds = ctx.build_distance(pts)
+    t_dist = time.perf_counter() - t0
+    ctx.upload(lsr._api.FIELD_PHI, phi)
+    t0 = time.perf_counter()
+    e2 = ctx.surface_energy(lsr._api.FIELD_PHI, 2, 5)
+    t_energy = time.perf_counter() - t0
+
+    # z-slab ownership
+    cuts = z_partition(active, nxy, g.dims[2], world)
+    k = active // nxy
+    mine = active[(k >= cuts[rank]) & (k < cuts[rank + 1])]
+    ctx.set_active(mine)
+    halo = 0
+    if world > 1:
+        halo = 8  # planes: max foot displacement (~2.5 dx here) + WENO radius 2 + gradient 1, rounded up
+        phi_t = lsr_tensor(ctx, lsr._api.FIELD_PHI, g)
+        out_t = lsr_tensor(ctx, lsr._api.FIELD_OUT, g)
+
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    n0 = None
+
+    def one_step(i):
+        ctx.sl_step(step, e2)
+        if world > 1:
+            exchange_halo(dist, ctx, lsr, g, cuts, rank, world, halo)
+        ctx.swap()
+
+    for i in range(args.warmup):
+        one_step(i)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    kernel_ms, step_ms = [], []
+    n0 = lsr.kernel_launches()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            flush.fill_(float(i))  # evict L2 between timed steps (outside the step's events)
+            evs[i][0].record(stream)
+            one_step(i)  # resync + SL kernel (+ halo exchange when N > 1), all on `stream`
+            evs[i][1].record(stream)
+            kernel_ms.append(ctx.last_times()[0])
+        torch.cuda.synchronize()
+        step_ms = [a.elapsed_time(b) for a, b in evs]
+    torch.cuda.synchronize()
+    launches = lsr.kernel_launches() - n0
+    if world > 1:
+        dist.barrier()
+    tot = np.array([sum(step_ms), sum(kernel_ms), float(mine.size)], dtype=np.float64)
+    if world > 1:
+        t = torch.tensor(tot[:2], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot[:2] = t.cpu().numpy()
+    ms_total = float(tot[0])
+    units = float(active.size) * args.steps  # whole job: all ranks together cover the band
+    value = units / (ms_total * 1e-3)
+    kern_avg_ms = float(np.mean(kernel_ms))
+    hbm_peak, peak_kind = peaks()
+    bpu = BYTES_PER_UPDATE[("weno" if cfg["interp"] == 1 else "q1", cfg["dim"])]
+    achieved = mine.size * bpu / (kern_avg_ms * 1e-3) / 1e9
+    traffic_pu, _ = traffic_per_update()
+
+    e2e = None
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_e2e:
+        e2e = measure_e2e(lsr, g, phi, ctx, active, step, e2, args)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(g, phi, ctx, active, step, e2, lsr)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC,
+            "value": value,
+            "unit": UNIT,
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": ms_total / args.steps,
+            "higher_is_better": True,
+            "scaling": "strong",
+            "vs_baseline": None,
+            "dtype": "f64",
+            "data": "synthetic (seeded bumpy-sphere cloud, BASELINE config 4 shapes/sizes)",
+            "config": {
+                "workload": cfg["name"],
+                "grid": list(g.dims),
+                "cloud_points": cfg["points"],
+                "active_nodes": int(active.size),
+                "interp": "weno" if cfg["interp"] == 1 else "q1",
+                "p": cfg["p"], "delta": cfg["delta"], "dt": step.dt, "gamma": step.band.gamma,
+                "energy_e2": e2, "dist_sweep_rounds": rounds,
+                "l2": "flushed (256 MB write) between timed steps",
+                "parallelism": f"z-slab x{world}" if world > 1 else "single GPU",
+                "halo_planes": halo,
+            },
+            "roofline": {
+                "bound": "hbm",
+                "achieved": achieved,
+                "peak": hbm_peak,
+                "unit": "GB/s",
+                "frac": achieved / hbm_peak,
+                "traffic": (traffic_pu * mine.size) if traffic_pu else None,
+                "peak_source": peak_kind,
+                "algorithmic_bytes_per_update": bpu,
+                "kernel_ms_avg": kern_avg_ms,
+                "note": "reference-access bytes per node-update (SURVEY 8(d)); the kernel is fp64-pipe bound",
+            },
+            "gpu_launches": int(launches),
+            "clocks": clk.summary(),
+            "setup_s": {"build_distance": t_dist, "surface_energy": t_energy},
+        }
+        if e2e:
+            line["e2e"] = e2e
+        if cpu:
+            line["cpu_baseline"] = cpu
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+class _CAI:
+    def __init__(self, ptr, n):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f8", "data": (ptr, False), "version": 3}
+
+
+def lsr_tensor(ctx, which, g):
+    import torch
+
+    return torch.as_tensor(_CAI(ctx.field_ptr(which), g.num_nodes()), device="cuda")
+
+
+def exchange_halo(dist, ctx, lsr, g, cuts, rank, world, halo):
+    """After a step, send the planes of phi^{n+1} that neighbours read as halo
+    ([cut - halo, cut) up, [cut, cut + halo) down) and receive theirs into the
+    OUT buffer (NCCL point-to-point, one group per step)."""
+    import torch
+
+    nxy = g.dims[0] * g.dims[1]
+    out = lsr_tensor(ctx, lsr._api.FIELD_OUT, g)
+    ops = []
+    lo, hi = int(cuts[rank]), int(cuts[rank + 1])
+    if rank > 0:
+        a = lo
+        b = min(hi, lo + halo)
+        ops.append(dist.P2POp(dist.isend, out[a * nxy:b * nxy], rank - 1))
+        c = max(0, lo - halo)
+        ops.append(dist.P2POp(dist.irecv, out[c * nxy:lo * nxy], rank - 1))
+    if rank < world - 1:
+        a = max(lo, hi - halo)
+        ops.append(dist.P2POp(dist.isend, out[a * nxy:hi * nxy], rank + 1))
+        ops.append(dist.P2POp(dist.irecv, out[hi * nxy:min(g.dims[2], hi + halo) * nxy], rank + 1))
+    if ops:
+        for r in dist.batch_isend_irecv(ops):
+            r.wait()
+    torch.cuda.current_stream().synchronize()
+
+
+def measure_e2e(lsr, g, phi, ctx, active, step, e2, args):
+    """The same metric through the public drop-in call lsr.sl_step (host
+    buffers in pinned memory): H2D phi + d + active ids, the step, D2H out."""
+    import torch
+
+    n = g.num_nodes()
+    h_phi = torch.empty(n, dtype=torch.float64, pin_memory=True).numpy()
+    h_d = torch.empty(n, dtype=torch.float64, pin_memory=True).numpy()
+    h_out = torch.empty(n, dtype=torch.float64, pin_memory=True).numpy()
+    h_act = torch.empty(active.size, dtype=torch.int64, pin_memory=True).numpy()
+    h_phi[:] = phi
+    ctx.download(lsr._api.FIELD_DIST, h_d)
+    h_act[:] = active
+    sphi = lsr.ScalarField(g, h_phi)
+    sd = lsr.DistanceField(lsr.ScalarField(g, h_d))
+    mask = lsr.BandMask(g, active=h_act)
+    out = lsr.ScalarField(g, h_out)
+    for _ in range(2):
+        lsr.sl_step(sphi, sd, mask, step, e2, out)
+    ts = []
+    for _ in range(args.e2e_steps):
+        t0 = time.perf_counter()
+        lsr.sl_step(sphi, sd, mask, step, e2, out)  # synchronous: returns after the D2H of out
+        ts.append(time.perf_counter() - t0)
+    t = float(np.mean(ts))
+    return {"value": active.size / t, "unit": UNIT, "h2d_bytes_per_step": int(2 * n * 8 + active.size * 8),
+            "d2h_bytes_per_step": int(n * 8), "ms_per_step": t * 1e3, "timing": "host clock around the synchronous call",
+            "steps": args.e2e_steps}
+
+
+def cpu_baseline(g, phi, ctx, active, step, e2, lsr, reps=3):
+    """The reference's lsr::sl_step (OpenMP, all host threads) on the same
+    inputs (oracle/_ref; the oracle restatement when _ref is absent)."""
+    from oracle import bindings
+
+    d = ctx.download(lsr._api.FIELD_DIST)
+    gd = dict(dim=g.dim, dims=g.dims, origin=g.origin, dx=g.dx)
+    cc = dict(p=step.p, interp=int(step.interp), delta=step.delta, dt=step.dt, fallback_c=step.fallback_c,
+              fallback_alpha=step.fallback_alpha, gamma=step.band.gamma, beta=step.band.beta)
+    threads = os.cpu_count() or 1
+    if bindings.reference_available():
+        R = bindings.Reference()
+        R.set_threads(threads)
+        h = R.ctx(gd, phi, d, active)
+        secs = [R.ctx_sl_step(h, cc, e2, serial=False) for _ in range(reps)]
+        R.ctx_free(h)
+        kind = "reference"
+    else:
+        O = bindings.Restatement()
+        secs = []
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            O.sl_step(gd, phi, d, active, cc, e2, nthreads=threads)
+            secs.append(time.perf_counter() - t0)
+        kind = "port"
+    best = min(secs)
+    return {"value": active.size / best, "unit": UNIT, "cores": threads, "kind": kind,
+            "sample": f"full band ({active.size} active nodes) of the same workload, best of {reps} calls of "
+                      f"lsr::sl_step incl. its internal O(N) copy", "seconds": secs}
+
+
+# ---------------------------------------------------------------------------
+
+
+def run_reference(args):
+    """--impl reference: the reference's own CPU lsr::sl_step (oracle/_ref,
+    built from the reference sources; OpenMP over all host cores) on the same
+    workload, inputs produced by the reference's own functions."""
+    world, rank, local = dist_env()
+    if rank != 0:
+        return
+    from oracle import bindings
+
+    import paper_2410_22205_b200 as lsr  # host-side types and the seeded cloud generator only
+
+    cfg = CONFIGS[args.config]
+    g, pts, phi, active, step = make_inputs(lsr, cfg)
+    gd = dict(dim=g.dim, dims=g.dims, origin=g.origin, dx=g.dx)
+    threads = os.cpu_count() or 1
+    if bindings.reference_available():
+        R = bindings.Reference()
+        R.set_threads(threads)
+        kind = "reference"
+    else:
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built on this machine"}))
+        return
+    t0 = time.perf_counter()
+    d, _, _, rounds = R.build_distance(gd, pts, cfg["dim"])  # lsr::build_distance_field
+    t_dist = time.perf_counter() - t0
+    e2 = R.surface_energy(gd, phi, d, 2, 5)
+    _, act_ref, _ = R.narrow_band(gd, phi, step.band.gamma)
+    cc = dict(p=step.p, interp=int(step.interp), delta=step.delta, dt=step.dt, fallback_c=step.fallback_c,
+              fallback_alpha=step.fallback_alpha, gamma=step.band.gamma, beta=step.band.beta)
+    h = R.ctx(gd, phi, d, act_ref)
+    # bound the run to a few minutes: sample a contiguous share of the band per step if needed
+    probe = R.ctx_sl_step(h, cc, e2)
+    budget = 150.0
+    frac = min(1.0, budget / max(1e-9, probe * (args.steps + args.warmup)))
+    if frac < 1.0:
+        R.ctx_free(h)
+        m = max(1, int(act_ref.size * frac))
+        h = R.ctx(gd, phi, d, act_ref[:m])
+        units = m
+    else:
+        units = act_ref.size
+    for _ in range(args.warmup):
+        R.ctx_sl_step(h, cc, e2)
+    secs = [R.ctx_sl_step(h, cc, e2) for _ in range(args.steps)]
+    R.ctx_free(h)
+    t = float(np.sum(secs))
+    value = units * args.steps / t
+    sample = (f"{units} of {act_ref.size} active nodes per step (lsr::sl_step incl. its O(N) copy), "
+              f"OpenMP {threads} threads")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded bumpy-sphere cloud, BASELINE config 4)",
+        "config": {"workload": cfg["name"], "grid": list(g.dims), "cloud_points": cfg["points"],
+                   "active_nodes": int(act_ref.size), "energy_e2": e2, "dist_sweep_rounds": rounds,
+                   "setup_build_distance_s": t_dist},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind, "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=40)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", type=int, default=4, choices=sorted(CONFIGS))
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

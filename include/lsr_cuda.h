@@ -123,6 +123,30 @@ int lsr_cuda_sl_step_device(const lsr_grid* grid, int32_t z_base, int32_t z_plan
                             double* d_out, int64_t* d_bad_node, int64_t* d_halo_miss,
                             void* stream);
 
+/* ---- point-cloud preprocessing ----
+ * lsr::build_distance_field (distance.cpp:144-148; header distance.hpp:29):
+ * seed_exact_distance (distance.cpp:8-52) then fast_sweep (:72-142),
+ * bit-identical to the reference. pts: n points as x,y,z triples (host).
+ * seed_only != 0 stops after seed_exact_distance (distance.hpp:24).
+ * d_out (num_nodes doubles) and exact_out (num_nodes bytes) are host
+ * buffers; either may be NULL. *rounds = fast_sweep's return value. */
+int lsr_cuda_build_distance(const lsr_grid* grid, const double* pts, int64_t n, int dim, int seed_only,
+                            double* d_out, uint8_t* exact_out, double* sentinel, int* rounds);
+/* same, writing the context's resident DIST field */
+int lsr_cuda_ctx_build_distance(lsr_cuda_ctx* ctx, const double* pts, int64_t n, int dim, int seed_only,
+                                double* sentinel, int* rounds);
+
+/* ---- surface energy ----
+ * lsr::surface_energy (metrics.cpp:186-189; header metrics.hpp:41-42): E_p
+ * of the field `which` (LSR_FIELD_PHI or LSR_FIELD_OUT) against the
+ * context's DIST field; 3d: energy_3d with `refine` subcells per axis, 2d:
+ * energy_2d. Same cells, same quadrature, same blocked_sum order as the
+ * reference; |d|^2 is computed as |d|*|d| where the reference calls glibc
+ * pow (not correctly rounded), so E_p agrees to a few ulp. */
+int lsr_cuda_surface_energy(lsr_cuda_ctx* ctx, int which, int p, int refine, double* energy);
+int lsr_cuda_surface_energy_host(const lsr_grid* grid, const double* phi, const double* dist, int p, int refine,
+                                 double* energy);
+
 /* ---- self-test hook ----
  * Divides n pseudo-random doubles by c with the kernels' constant-divisor
  * division and with the hardware IEEE division; *mismatches = how many

@@ -27,11 +27,15 @@ from ._api import (  # noqa: F401
     OutOfDomainError,
     ScalarField,
     StepConfig,
+    build_distance_field,
+    cloud_generate,
+    cube_grid,
     default_band_params,
     kernel_launches,
     lib,
     lib_path,
     sl_step,
+    surface_energy,
 )
 
 __all__ = [

@@ -117,8 +117,52 @@ def lib() -> C.CDLL:
                                           C.c_int64, P(CStepCfg), C.c_double, C.c_void_p, C.c_void_p, C.c_void_p,
                                           C.c_void_p]
     L.lsr_cuda_selftest_div_const.argtypes = [C.c_double, C.c_int64, C.c_uint64, P(C.c_int64)]
+    L.lsr_cuda_build_distance.argtypes = [P(CGrid), _dp, C.c_int64, C.c_int, C.c_int, C.c_void_p, C.c_void_p,
+                                          P(C.c_double), P(C.c_int)]
+    L.lsr_cuda_ctx_build_distance.argtypes = [C.c_void_p, _dp, C.c_int64, C.c_int, C.c_int, P(C.c_double),
+                                              P(C.c_int)]
+    L.lsr_cloud_generate.argtypes = [C.c_int, C.c_int64, C.c_uint64, C.c_double, _dp]
+    L.lsr_cuda_surface_energy.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, P(C.c_double)]
+    L.lsr_cuda_surface_energy_host.argtypes = [P(CGrid), _dp, _dp, C.c_int, C.c_int, P(C.c_double)]
     _lib = L
     return L
+
+
+def surface_energy(phi: "ScalarField", dist: "DistanceField", p: int, subcell_refine: int = 5) -> float:
+    """lsr::surface_energy (metrics.hpp:41-42) on the GPU."""
+    if not (phi.grid == dist.field.grid):
+        raise ConfigError("energy: grid mismatch")
+    e = C.c_double()
+    _check(lib().lsr_cuda_surface_energy_host(C.byref(phi.grid.c()), phi.values,
+                                              np.ascontiguousarray(dist.field.values), int(p), int(subcell_refine),
+                                              C.byref(e)))
+    return e.value
+
+
+def cloud_generate(config: int, n: int, seed: int = 0, sigma: float = 0.0) -> np.ndarray:
+    """Seeded synthetic cloud of BASELINE config 1..5 (include/lsr_workloads.h), shape (n, 3)."""
+    pts = np.zeros((int(n), 3), dtype=np.float64)
+    if lib().lsr_cloud_generate(int(config), int(n), int(seed), float(sigma), pts.reshape(-1)) != 0:
+        raise ConfigError(f"unknown cloud config {config}")
+    return pts
+
+
+def build_distance_field(grid: "Grid", points: np.ndarray, dim: int | None = None,
+                         seed_only: bool = False) -> "DistanceField":
+    """lsr::build_distance_field (distance.hpp:29) on the GPU; with
+    seed_only, lsr::seed_exact_distance (distance.hpp:24). The sweep round
+    count is returned as the attribute ``rounds``."""
+    pts = np.ascontiguousarray(points, dtype=np.float64).reshape(-1)
+    n = grid.num_nodes()
+    d = np.empty(n, dtype=np.float64)
+    ex = np.empty(n, dtype=np.uint8)
+    sent, rounds = C.c_double(), C.c_int()
+    _check(lib().lsr_cuda_build_distance(C.byref(grid.c()), pts, pts.size // 3, int(dim or grid.dim),
+                                         int(bool(seed_only)), d.ctypes.data_as(C.c_void_p),
+                                         ex.ctypes.data_as(C.c_void_p), C.byref(sent), C.byref(rounds)))
+    out = DistanceField(ScalarField(grid, d), ex, sent.value)
+    out.rounds = rounds.value
+    return out
 
 
 def selftest_div_const(c: float, n: int, seed: int = 1) -> int:
@@ -365,6 +409,19 @@ class Context:
 
     def swap(self):
         _check(lib().lsr_cuda_swap(self.h))
+
+    def build_distance(self, points: np.ndarray, dim: int | None = None, seed_only: bool = False):
+        """Device-resident lsr::build_distance_field into the DIST field."""
+        pts = np.ascontiguousarray(points, dtype=np.float64).reshape(-1)
+        sent, rounds = C.c_double(), C.c_int()
+        _check(lib().lsr_cuda_ctx_build_distance(self.h, pts, pts.size // 3, int(dim or self.grid.dim),
+                                                 int(bool(seed_only)), C.byref(sent), C.byref(rounds)))
+        return sent.value, rounds.value
+
+    def surface_energy(self, which: int = FIELD_PHI, p: int = 2, subcell_refine: int = 5) -> float:
+        e = C.c_double()
+        _check(lib().lsr_cuda_surface_energy(self.h, int(which), int(p), int(subcell_refine), C.byref(e)))
+        return e.value
 
     def last_times(self):
         k, s = C.c_float(), C.c_float()

@@ -1,0 +1,380 @@
+// distance.cu — point-cloud preprocessing on the GPU:
+// the unsigned distance d of lsr::build_distance_field
+// (/root/reference/proj/src/distance.cpp:144-148), bit-identical to the
+// reference.
+//
+//  * SpatialHash (cloud.cpp:390-452): the same uniform bins (geometry fixed
+//    on the host with the reference's expressions), built with a counting
+//    sort on the device. nearest_distance keeps the reference's shell loop
+//    and break rule, so the set of examined points at each shell end — and
+//    hence the min of the identical dot(diff,diff) terms — is the same.
+//  * seed_exact_distance (distance.cpp:8-52): pass 1 flags the 4^dim node
+//    block around each point's cell (all writers store 1), pass 2 evaluates
+//    the exact NN distance at flagged nodes.
+//  * fast_sweep (distance.cpp:72-142): Gauss–Seidel over the 2^dim orderings
+//    as hyperplane sweeps. In ordering (+,+,+) the serial loop updates node
+//    (i,j,k) after its -1 neighbours and before its +1 neighbours; sweeping
+//    the hyperplanes i'+j'+k' = s in increasing s (with mirrored indices for
+//    the other orderings) gives every node exactly the same inputs, and
+//    nodes of one hyperplane are independent. max_change is a max (order
+//    free), accumulated with an integer atomicMax on the non-negative bits.
+#include <cuda_runtime.h>
+
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "lsr_cuda.h"
+#include "prep_launch.h"
+
+namespace {
+
+struct HashP {
+    int dim;
+    double lox, loy, loz;
+    double cell;
+    int bx, by, bz;
+};
+
+__device__ __forceinline__ double dmin(double a, double b) { return (b < a) ? b : a; }  // std::min
+__device__ __forceinline__ int iclamp(int v, int lo, int hi) { return v < lo ? lo : (hi < v ? hi : v); }
+
+// bin_of (cloud.cpp:405-412)
+__device__ __forceinline__ int bin_of(const HashP& H, const double* p) {
+    int b[3] = {0, 0, 0};
+    const double lo[3] = {H.lox, H.loy, H.loz};
+    const int nb[3] = {H.bx, H.by, H.bz};
+    for (int d = 0; d < H.dim; ++d) {
+        b[d] = static_cast<int>((p[d] - lo[d]) / H.cell);
+        b[d] = iclamp(b[d], 0, nb[d] - 1);
+    }
+    return (b[2] * H.by + b[1]) * H.bx + b[0];
+}
+
+__global__ void count_bins(HashP H, const double* __restrict__ pts, long long n, int* __restrict__ counts,
+                           int* __restrict__ bin_id) {
+    const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int b = bin_of(H, pts + 3 * i);
+    bin_id[i] = b;
+    atomicAdd(counts + b, 1);
+}
+
+__global__ void scatter_bins(const int* __restrict__ bin_id, long long n, int* __restrict__ cursor,
+                             int* __restrict__ entries) {
+    const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    entries[atomicAdd(cursor + bin_id[i], 1)] = static_cast<int>(i);
+}
+
+// SpatialHash::nearest_distance (cloud.cpp:420-452)
+__device__ double nearest_distance(const HashP& H, const double* __restrict__ pts, const int* __restrict__ starts,
+                                   const int* __restrict__ entries, double qx, double qy, double qz) {
+    const double q[3] = {qx, qy, qz};
+    const double lo[3] = {H.lox, H.loy, H.loz};
+    const int nb[3] = {H.bx, H.by, H.bz};
+    int bq[3] = {0, 0, 0};
+    int rad_max = 0;
+    for (int d = 0; d < H.dim; ++d) {
+        bq[d] = static_cast<int>(floor((q[d] - lo[d]) / H.cell));
+        rad_max = max(rad_max, max(bq[d], nb[d] - 1 - bq[d]));
+    }
+    double best2 = __longlong_as_double(0x7ff0000000000000LL);  // +inf
+    for (int rad = 0; rad <= rad_max + 1; ++rad) {
+        if (rad > 0 && best2 <= ((rad - 1) * H.cell) * ((rad - 1) * H.cell)) break;
+        const int zlo = H.dim == 3 ? bq[2] - rad : 0;
+        const int zhi = H.dim == 3 ? bq[2] + rad : 0;
+        for (int bz = max(0, zlo); bz <= min(nb[2] - 1, zhi); ++bz) {
+            for (int by = max(0, bq[1] - rad); by <= min(nb[1] - 1, bq[1] + rad); ++by) {
+                const int cyz = max(abs(by - bq[1]), abs(bz - bq[2]));
+                for (int bx = max(0, bq[0] - rad); bx <= min(nb[0] - 1, bq[0] + rad); ++bx) {
+                    if (max(abs(bx - bq[0]), cyz) != rad) continue;
+                    const int b = (bz * nb[1] + by) * nb[0] + bx;
+                    for (int e = starts[b]; e < starts[b + 1]; ++e) {
+                        const double* p = pts + 3 * static_cast<long long>(entries[e]);
+                        const double dx = p[0] - q[0], dy = p[1] - q[1], dz = p[2] - q[2];
+                        best2 = dmin(best2, dx * dx + dy * dy + dz * dz);  // dot(diff, diff)
+                    }
+                }
+            }
+        }
+    }
+    return sqrt(best2);
+}
+
+struct GridP {
+    int dim, nx, ny, nz;
+    long long nxy;
+    double ox, oy, oz, dx;
+};
+
+// seed pass 1 (distance.cpp:25-39): flag the 4^dim block around each point's cell
+__global__ void seed_flag(GridP G, const double* __restrict__ pts, long long n, unsigned char* __restrict__ exact) {
+    const long long q = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (q >= n) return;
+    const double* p = pts + 3 * q;
+    // locate_cell (grid.cpp:39-47); the host has checked Grid::contains
+    const double o[3] = {G.ox, G.oy, G.oz};
+    const int nn[3] = {G.nx, G.ny, G.nz};
+    int c[3] = {0, 0, 0};
+    for (int d = 0; d < G.dim; ++d) c[d] = iclamp(static_cast<int>(floor((p[d] - o[d]) / G.dx)), 0, nn[d] - 2);
+    const int kz = G.dim == 3 ? 1 : 0;
+    for (int dk = -kz; dk <= 2 * kz; ++dk)
+        for (int dj = -1; dj <= 2; ++dj)
+            for (int di = -1; di <= 2; ++di) {
+                const int i = c[0] + di, j = c[1] + dj, k = c[2] + dk;
+                if (i < 0 || j < 0 || k < 0 || i >= G.nx || j >= G.ny || k >= G.nz) continue;
+                exact[(static_cast<long long>(k) * G.ny + j) * G.nx + i] = 1;
+            }
+}
+
+// seed pass 2 (distance.cpp:42-50) + the sentinel fill of every other node
+__global__ void seed_values(GridP G, HashP H, const double* __restrict__ pts, const int* __restrict__ starts,
+                            const int* __restrict__ entries, const unsigned char* __restrict__ exact, double sentinel,
+                            double* __restrict__ d) {
+    const long long id = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (id >= G.nxy * G.nz) return;
+    if (!exact[id]) {
+        d[id] = sentinel;
+        return;
+    }
+    const int i = static_cast<int>(id % G.nx);
+    const int j = static_cast<int>((id / G.nx) % G.ny);
+    const int k = static_cast<int>(id / G.nxy);
+    d[id] = nearest_distance(H, pts, starts, entries, G.ox + i * G.dx, G.oy + j * G.dx, G.oz + k * G.dx);
+}
+
+__global__ void any_below(const double* __restrict__ d, long long n, double sentinel, int* __restrict__ flag) {
+    for (long long id = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; id < n;
+         id += static_cast<long long>(gridDim.x) * blockDim.x)
+        if (d[id] < sentinel) {
+            *flag = 1;
+            return;
+        }
+}
+
+// eikonal_update (distance.cpp:57-68)
+__device__ __forceinline__ double eikonal_update(const double* a, int m, double h) {
+    double x = a[0] + h;
+    if (m >= 2 && x > a[1]) {
+        x = 0.5 * (a[0] + a[1] + sqrt(2.0 * h * h - (a[0] - a[1]) * (a[0] - a[1])));
+        if (m >= 3 && x > a[2]) {
+            const double s = a[0] + a[1] + a[2];
+            const double s2 = a[0] * a[0] + a[1] * a[1] + a[2] * a[2];
+            x = (s + sqrt(s * s - 3.0 * (s2 - h * h))) / 3.0;
+        }
+    }
+    return x;
+}
+
+// one hyperplane i'+j'+k' = s of ordering `ord` (update_node, distance.cpp:86-116)
+__global__ void sweep_plane(GridP G, int ord, int s, int k_lo, int k_cnt, double sentinel,
+                            const unsigned char* __restrict__ exact, double* __restrict__ d,
+                            unsigned long long* __restrict__ max_change) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    const int kp = k_lo + t / G.ny;  // mirrored k', j'
+    const int jp = t % G.ny;
+    if (t / G.ny >= k_cnt) return;
+    const int ip = s - jp - kp;
+    if (ip < 0 || ip >= G.nx) return;
+    const int i = (ord & 1) ? G.nx - 1 - ip : ip;
+    const int j = (ord & 2) ? G.ny - 1 - jp : jp;
+    const int k = (ord & 4) ? G.nz - 1 - kp : kp;
+    const long long id = (static_cast<long long>(k) * G.ny + j) * G.nx + i;
+    if (exact[id]) return;
+    double a[3];
+    int m = 0;
+    {
+        double best = sentinel;
+        if (i > 0) best = dmin(best, d[id - 1]);
+        if (i < G.nx - 1) best = dmin(best, d[id + 1]);
+        if (best < sentinel) a[m++] = best;
+    }
+    {
+        double best = sentinel;
+        if (j > 0) best = dmin(best, d[id - G.nx]);
+        if (j < G.ny - 1) best = dmin(best, d[id + G.nx]);
+        if (best < sentinel) a[m++] = best;
+    }
+    if (G.dim == 3) {
+        double best = sentinel;
+        if (k > 0) best = dmin(best, d[id - G.nxy]);
+        if (k < G.nz - 1) best = dmin(best, d[id + G.nxy]);
+        if (best < sentinel) a[m++] = best;
+    }
+    if (m == 0) return;
+    // std::sort of <= 3 values: the sorted sequence is unique
+    if (m >= 2 && a[1] < a[0]) { const double t0 = a[0]; a[0] = a[1]; a[1] = t0; }
+    if (m == 3) {
+        if (a[2] < a[1]) { const double t1 = a[1]; a[1] = a[2]; a[2] = t1; }
+        if (a[1] < a[0]) { const double t0 = a[0]; a[0] = a[1]; a[1] = t0; }
+    }
+    const double v = d[id];
+    const double cand = eikonal_update(a, m, G.dx);
+    if (cand < v) {
+        d[id] = cand;
+        const double change = v - cand;
+        atomicMax(max_change, static_cast<unsigned long long>(__double_as_longlong(change)));
+    }
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+
+int lsr_prep_build_distance(const lsr_grid* g, const double* h_pts, int64_t n, int dim, int seed_only,
+                            double* d_field, unsigned char* d_exact, double* sentinel_out, int* rounds_out,
+                            cudaStream_t s, std::string* err) {
+    auto fail = [&](int code, const char* m) {
+        *err = m;
+        return code;
+    };
+#define PREP_TRY(x)                                         \
+    do {                                                    \
+        cudaError_t e_ = (x);                               \
+        if (e_ != cudaSuccess) {                            \
+            *err = std::string(#x) + ": " + cudaGetErrorString(e_); \
+            return LSR_ERR_CUDA;                            \
+        }                                                   \
+    } while (0)
+    if (n <= 0) return fail(LSR_ERR, "seed_exact_distance: empty cloud");          // distance.cpp:9
+    if (dim != g->dim) return fail(LSR_ERR_CONFIG, "seed_exact_distance: dimension mismatch");  // :10
+    // Grid::diagonal (grid.hpp:35) and the sentinel (distance.cpp:13)
+    double up[3], diff[3];
+    for (int d = 0; d < 3; ++d) {
+        up[d] = g->origin[d] + (g->dims[d] - 1) * g->dx;
+        diff[d] = up[d] - g->origin[d];
+    }
+    const double sentinel = 10.0 * std::sqrt(diff[0] * diff[0] + diff[1] * diff[1] + diff[2] * diff[2]);
+    *sentinel_out = sentinel;
+    // Grid::contains for every point (distance.cpp:18-20), bounding box (cloud.cpp:380-388)
+    double lo[3] = {h_pts[0], h_pts[1], h_pts[2]}, hi[3] = {h_pts[0], h_pts[1], h_pts[2]};
+    for (int64_t q = 0; q < n; ++q) {
+        const double* p = h_pts + 3 * q;
+        for (int d = 0; d < g->dim; ++d)
+            if (p[d] < g->origin[d] || p[d] > up[d])
+                return fail(LSR_ERR_OUT_OF_DOMAIN, "seed_exact_distance: cloud point outside grid hull");
+        for (int d = 0; d < 3; ++d) {
+            lo[d] = std::min(lo[d], p[d]);
+            hi[d] = std::max(hi[d], p[d]);
+        }
+    }
+    // SpatialHash geometry (cloud.cpp:390-399)
+    HashP H{};
+    H.dim = dim;
+    H.lox = lo[0];
+    H.loy = lo[1];
+    H.loz = lo[2];
+    const double span[3] = {hi[0] - lo[0], hi[1] - lo[1], hi[2] - lo[2]};
+    const double diag = std::sqrt(span[0] * span[0] + span[1] * span[1] + span[2] * span[2]);
+    const double n_axis = std::pow(static_cast<double>(n), 1.0 / dim);
+    H.cell = diag > 0.0 ? diag / std::max(1.0, n_axis) : 1.0;
+    int nb[3];
+    for (int d = 0; d < 3; ++d) nb[d] = d < dim ? 1 + static_cast<int>(span[d] / H.cell) : 1;
+    H.bx = nb[0];
+    H.by = nb[1];
+    H.bz = nb[2];
+    const long long nbins = static_cast<long long>(nb[0]) * nb[1] * nb[2];
+
+    GridP G{g->dim, g->dims[0], g->dims[1], g->dims[2], static_cast<long long>(g->dims[0]) * g->dims[1],
+            g->origin[0], g->origin[1], g->origin[2], g->dx};
+    const long long N = G.nxy * G.nz;
+
+    double* pts = nullptr;
+    int *counts = nullptr, *starts = nullptr, *bin_id = nullptr, *entries = nullptr, *flag = nullptr;
+    void* tmp = nullptr;
+    size_t tmp_bytes = 0;
+    unsigned long long* dmax = nullptr;
+    auto cleanup = [&] {
+        cudaFree(pts);
+        cudaFree(counts);
+        cudaFree(starts);
+        cudaFree(bin_id);
+        cudaFree(entries);
+        cudaFree(flag);
+        cudaFree(tmp);
+        cudaFree(dmax);
+    };
+    struct Guard {
+        decltype(cleanup)& f;
+        ~Guard() { f(); }
+    } guard{cleanup};
+    PREP_TRY(cudaMalloc(&pts, sizeof(double) * 3 * n));
+    PREP_TRY(cudaMalloc(&counts, sizeof(int) * (nbins + 1)));
+    PREP_TRY(cudaMalloc(&starts, sizeof(int) * (nbins + 1)));
+    PREP_TRY(cudaMalloc(&bin_id, sizeof(int) * n));
+    PREP_TRY(cudaMalloc(&entries, sizeof(int) * n));
+    PREP_TRY(cudaMalloc(&flag, sizeof(int)));
+    PREP_TRY(cudaMalloc(&dmax, sizeof(unsigned long long)));
+    PREP_TRY(cudaMemcpyAsync(pts, h_pts, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, s));
+    PREP_TRY(cudaMemsetAsync(counts, 0, sizeof(int) * (nbins + 1), s));
+    const int T = 256;
+    const unsigned pb = static_cast<unsigned>((n + T - 1) / T);
+    count_bins<<<pb, T, 0, s>>>(H, pts, n, counts, bin_id);
+    lsr_note_launch();
+    PREP_TRY(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, counts, starts, static_cast<int>(nbins + 1), s));
+    PREP_TRY(cudaMalloc(&tmp, tmp_bytes));
+    PREP_TRY(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, counts, starts, static_cast<int>(nbins + 1), s));
+    PREP_TRY(cudaMemcpyAsync(counts, starts, sizeof(int) * (nbins + 1), cudaMemcpyDeviceToDevice, s));
+    scatter_bins<<<pb, T, 0, s>>>(bin_id, n, counts, entries);
+    lsr_note_launch();
+
+    PREP_TRY(cudaMemsetAsync(d_exact, 0, N, s));
+    seed_flag<<<pb, T, 0, s>>>(G, pts, n, d_exact);
+    lsr_note_launch();
+    seed_values<<<static_cast<unsigned>((N + T - 1) / T), T, 0, s>>>(G, H, pts, starts, entries, d_exact, sentinel,
+                                                                      d_field);
+    lsr_note_launch();
+    PREP_TRY(cudaGetLastError());
+    if (seed_only) {
+        *rounds_out = 0;
+        PREP_TRY(cudaStreamSynchronize(s));
+        return LSR_OK;
+    }
+
+    // fast_sweep (distance.cpp:72-142)
+    int h_flag = 0;
+    PREP_TRY(cudaMemsetAsync(flag, 0, sizeof(int), s));
+    any_below<<<148 * 4, 256, 0, s>>>(d_field, N, sentinel, flag);
+    lsr_note_launch();
+    PREP_TRY(cudaMemcpyAsync(&h_flag, flag, sizeof(int), cudaMemcpyDeviceToHost, s));
+    PREP_TRY(cudaStreamSynchronize(s));
+    if (!h_flag) return fail(LSR_ERR, "fast_sweep: no finite seed value");
+    const int orderings = g->dim == 3 ? 8 : 4;
+    const double tol = 1e-3 * g->dx;
+    const int max_rounds = 8;
+    const int smax = (G.nx - 1) + (G.ny - 1) + (G.dim == 3 ? G.nz - 1 : 0);
+    int round = 0;
+    for (; round < max_rounds; ++round) {
+        PREP_TRY(cudaMemsetAsync(dmax, 0, sizeof(unsigned long long), s));
+        for (int ord = 0; ord < orderings; ++ord) {
+            for (int sp = 0; sp <= smax; ++sp) {
+                const int k_lo = G.dim == 3 ? std::max(0, sp - (G.nx - 1) - (G.ny - 1)) : 0;
+                const int k_hi = G.dim == 3 ? std::min(G.nz - 1, sp) : 0;
+                const int k_cnt = k_hi - k_lo + 1;
+                const long long threads = static_cast<long long>(k_cnt) * G.ny;
+                sweep_plane<<<static_cast<unsigned>((threads + T - 1) / T), T, 0, s>>>(G, ord, sp, k_lo, k_cnt,
+                                                                                      sentinel, d_exact, d_field, dmax);
+                lsr_note_launch();
+            }
+        }
+        PREP_TRY(cudaGetLastError());
+        unsigned long long h_max = 0;
+        PREP_TRY(cudaMemcpyAsync(&h_max, dmax, sizeof h_max, cudaMemcpyDeviceToHost, s));
+        PREP_TRY(cudaStreamSynchronize(s));
+        double max_change;
+        std::memcpy(&max_change, &h_max, sizeof max_change);
+        if (max_change < tol) {
+            ++round;
+            break;
+        }
+    }
+    *rounds_out = round;
+    return LSR_OK;
+#undef PREP_TRY
+}

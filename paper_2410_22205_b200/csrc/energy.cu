@@ -1,0 +1,263 @@
+// energy.cu — the surface energy E_p = (integral of |d|^p over the front)^(1/p)
+// of lsr::surface_energy (/root/reference/proj/src/metrics.cpp:186-189), the
+// producer of sl_step's energy_p (driver.cpp:188) — SURVEY §8(f) row 3.
+//
+//  * interface_cells (metrics.cpp:35-56): every cell is classified in
+//    parallel; an order-preserving compaction (cub::DeviceSelect::Flagged)
+//    reproduces the ascending cell list of the serial scan.
+//  * energy_3d (metrics.cpp:145-184): one thread per interface cell runs the
+//    r^3 subcell midpoint rule in the reference's loop order; energy_2d
+//    (:113-143): marching squares with the reference's case table, saddle
+//    rule and trapezoid sums.
+//  * blocked_sum (parallel.hpp:26-42): the 4096-term blocks are summed
+//    serially in index order (one thread per block), the block partials in
+//    block order on the host, then pow(total, 1/p) with the host libm — the
+//    reference's exact summation order.
+//  The per-term |d|^p uses |d|*|d| for p = 2 (correctly rounded) where the
+//  reference calls glibc pow, which is not correctly rounded,
+//  so E_p agrees to a few ulp rather than bit for bit.
+#include <cuda_runtime.h>
+
+#include <cub/cub.cuh>
+
+#include <cmath>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "lsr_cuda.h"
+#include "prep_launch.h"
+#include "sl_device.cuh"
+
+using lsr_dev::SlParams;
+
+namespace {
+
+__device__ __forceinline__ double powp(double a, int p) {
+    if (p == 1) return a;
+    if (p == 2) return a * a;
+    return pow(a, static_cast<double>(p));
+}
+
+// interface_cells' corner test (metrics.cpp:23-31, 40-52)
+__global__ void flag_cells(SlParams P, const double* __restrict__ phi, long long ncells,
+                           unsigned char* __restrict__ flags) {
+    const long long c = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (c >= ncells) return;
+    const int cx = P.nx - 1, cy = P.ny - 1;
+    const int i = static_cast<int>(c % cx);
+    const int j = static_cast<int>((c / cx) % cy);
+    const int k = static_cast<int>(c / (static_cast<long long>(cx) * cy));
+    const long long b = (static_cast<long long>(k) * P.ny + j) * P.nx + i;
+    bool pos = false, neg = false, zero = false;
+    const int kz = P.dim == 3 ? 1 : 0;
+    for (int dk = 0; dk <= kz; ++dk)
+        for (int dj = 0; dj <= 1; ++dj)
+            for (int di = 0; di <= 1; ++di) {
+                const double v = __ldg(phi + b + dk * P.nxy + dj * P.nx + di);
+                if (v > 0.0) pos = true;
+                else if (v < 0.0) neg = true;
+                else zero = true;
+            }
+    flags[c] = (zero || (pos && neg)) ? 1 : 0;
+}
+
+// energy_3d per-cell contribution (metrics.cpp:161-178)
+__global__ void contrib_3d(SlParams P, const double* __restrict__ phi, const double* __restrict__ dist,
+                           const int* __restrict__ cells, long long nc, int r, double dxp, double select, int p,
+                           double* __restrict__ contrib) {
+    const long long c = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (c >= nc) return;
+    const long long cid = cells[c];
+    const int cx = P.nx - 1, cy = P.ny - 1;
+    const int i = static_cast<int>(cid % cx);
+    const int j = static_cast<int>((cid / cx) % cy);
+    const int k = static_cast<int>(cid / (static_cast<long long>(cx) * cy));
+    const double bx = P.ox + i * P.dx, by = P.oy + j * P.dx, bz = P.oz + k * P.dx;  // Grid::node
+    double acc = 0.0;
+    for (int ck = 0; ck < r; ++ck)
+        for (int cj = 0; cj < r; ++cj)
+            for (int ci = 0; ci < r; ++ci) {
+                const double x = bx + (ci + 0.5) * dxp, y = by + (cj + 0.5) * dxp, z = bz + (ck + 0.5) * dxp;
+                if (fabs(lsr_dev::interp_q1<3>(P, phi, x, y, z)) >= select) continue;
+                acc += powp(fabs(lsr_dev::interp_q1<3>(P, dist, x, y, z)), p) * dxp * dxp;
+            }
+    contrib[c] = acc;
+}
+
+struct Pt {
+    double x, y;
+};
+
+// edge_crossing (metrics.cpp:65-77)
+__device__ __forceinline__ Pt edge_crossing(const SlParams& P, const double* __restrict__ phi, int i, int j, int e) {
+    const double x0 = P.ox + i * P.dx, y0 = P.oy + j * P.dx;
+    const long long b = static_cast<long long>(j) * P.nx + i;
+    auto lerp_t = [](double a, double c) { return a / (a - c); };
+    switch (e) {
+        case 0: return {x0 + lerp_t(__ldg(phi + b), __ldg(phi + b + 1)) * P.dx, y0};
+        case 1: return {x0 + P.dx, y0 + lerp_t(__ldg(phi + b + 1), __ldg(phi + b + P.nx + 1)) * P.dx};
+        case 2: return {x0 + lerp_t(__ldg(phi + b + P.nx), __ldg(phi + b + P.nx + 1)) * P.dx, y0 + P.dx};
+        default: return {x0, y0 + lerp_t(__ldg(phi + b), __ldg(phi + b + P.nx)) * P.dx};
+    }
+}
+
+__device__ __forceinline__ bool inside_hull(const SlParams& P, Pt a) {  // Grid::contains (grid.hpp:36-41)
+    return !(a.x < P.ox || a.x > P.hx || a.y < P.oy || a.y > P.hy);
+}
+
+// energy_2d per-cell contribution (metrics.cpp:124-137, front_segments_2d :79-109)
+__global__ void contrib_2d(SlParams P, const double* __restrict__ phi, const double* __restrict__ dist,
+                           const int* __restrict__ cells, long long nc, int p, double* __restrict__ contrib,
+                           int* __restrict__ out_of_domain) {
+    const long long c = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (c >= nc) return;
+    // segment table of the 16 corner cases (metrics.cpp:80-84)
+    const signed char table[16][2] = {{-1, -1}, {3, 0}, {0, 1}, {3, 1}, {1, 2}, {-2, 0}, {0, 2}, {3, 2},
+                                      {2, 3},   {0, 2}, {-2, 0}, {1, 2}, {1, 3}, {0, 1}, {3, 0}, {-1, -1}};
+    const int cid = cells[c];
+    const int i = cid % (P.nx - 1), j = cid / (P.nx - 1);
+    const long long b = static_cast<long long>(j) * P.nx + i;
+    const double f00 = __ldg(phi + b), f10 = __ldg(phi + b + 1), f11 = __ldg(phi + b + P.nx + 1),
+                 f01 = __ldg(phi + b + P.nx);
+    int cs = 0;  // cell_case_2d (metrics.cpp:14-21)
+    if (f00 <= 0.0) cs |= 1;
+    if (f10 <= 0.0) cs |= 2;
+    if (f11 <= 0.0) cs |= 4;
+    if (f01 <= 0.0) cs |= 8;
+    int e[4];
+    int ns = 0;
+    if (table[cs][0] == -1) {
+        ns = 0;
+    } else if (table[cs][0] == -2) {
+        const double avg = 0.25 * (f00 + f10 + f11 + f01);
+        const bool center_inside = avg <= 0.0;
+        const bool first = (cs == 5) ? center_inside : !center_inside;
+        if (first) { e[0] = 0; e[1] = 1; e[2] = 2; e[3] = 3; }
+        else { e[0] = 3; e[1] = 0; e[2] = 1; e[3] = 2; }
+        ns = 2;
+    } else {
+        e[0] = table[cs][0];
+        e[1] = table[cs][1];
+        ns = 1;
+    }
+    double acc = 0.0;
+    for (int s = 0; s < ns; ++s) {
+        const Pt a = edge_crossing(P, phi, i, j, e[2 * s]);
+        const Pt bb = edge_crossing(P, phi, i, j, e[2 * s + 1]);
+        const double ddx = bb.x - a.x, ddy = bb.y - a.y, ddz = 0.0 - 0.0;
+        const double len = sqrt(ddx * ddx + ddy * ddy + ddz * ddz);  // norm(b - a)
+        if (!inside_hull(P, a) || !inside_hull(P, bb)) {  // interp_q1 -> locate_cell throws (grid.cpp:40)
+            atomicExch(out_of_domain, 1);
+            continue;
+        }
+        const double da = lsr_dev::interp_q1<2>(P, dist, a.x, a.y, 0.0);
+        const double db = lsr_dev::interp_q1<2>(P, dist, bb.x, bb.y, 0.0);
+        acc += len * 0.5 * (powp(fabs(da), p) + powp(fabs(db), p));
+    }
+    contrib[c] = acc;
+}
+
+// blocked_sum's in-block serial sums (parallel.hpp:31-37)
+__global__ void block_partials(const double* __restrict__ contrib, long long n, double* __restrict__ partial) {
+    const long long b = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const long long lo = b * 4096;
+    if (lo >= n) return;
+    const long long hi = min(n, lo + 4096);
+    double s = 0.0;
+    for (long long i = lo; i < hi; ++i) s += contrib[i];
+    partial[b] = s;
+}
+
+}  // namespace
+
+int lsr_prep_surface_energy(const SlParams& P, const double* phi, const double* dist, int p, int refine,
+                            double* energy, int64_t* n_cells, cudaStream_t s, std::string* err) {
+#define EN_TRY(x)                                                       \
+    do {                                                                \
+        cudaError_t e_ = (x);                                           \
+        if (e_ != cudaSuccess) {                                        \
+            *err = std::string(#x) + ": " + cudaGetErrorString(e_);     \
+            return LSR_ERR_CUDA;                                        \
+        }                                                               \
+    } while (0)
+    if (P.dim == 3 && (p < 1 || refine < 1)) {
+        *err = "energy_3d: invalid p or refinement";  // metrics.cpp:147
+        return LSR_ERR_CONFIG;
+    }
+    if (P.dim == 2 && p < 1) {
+        *err = "energy_2d: p must be >= 1";  // metrics.cpp:115
+        return LSR_ERR_CONFIG;
+    }
+    const long long ncells = static_cast<long long>(P.nx - 1) * (P.ny - 1) * (P.dim == 3 ? (P.nz - 1) : 1);
+    unsigned char* flags = nullptr;
+    int* cells = nullptr;
+    int* d_nsel = nullptr;
+    double* contrib = nullptr;
+    double* partial = nullptr;
+    int* ood = nullptr;
+    void* tmp = nullptr;
+    size_t tmp_bytes = 0;
+    struct Guard {
+        std::vector<void*> p;
+        ~Guard() {
+            for (void* q : p) cudaFree(q);
+        }
+    } guard;
+    EN_TRY(cudaMalloc(&flags, ncells));
+    guard.p.push_back(flags);
+    EN_TRY(cudaMalloc(&cells, sizeof(int) * ncells));
+    guard.p.push_back(cells);
+    EN_TRY(cudaMalloc(&d_nsel, sizeof(int)));
+    guard.p.push_back(d_nsel);
+    EN_TRY(cudaMalloc(&ood, sizeof(int)));
+    guard.p.push_back(ood);
+    EN_TRY(cudaMemsetAsync(ood, 0, sizeof(int), s));
+    const int T = 256;
+    flag_cells<<<static_cast<unsigned>((ncells + T - 1) / T), T, 0, s>>>(P, phi, ncells, flags);
+    lsr_note_launch();
+    cub::CountingInputIterator<int> ids(0);
+    EN_TRY(cub::DeviceSelect::Flagged(nullptr, tmp_bytes, ids, flags, cells, d_nsel, static_cast<int>(ncells), s));
+    EN_TRY(cudaMalloc(&tmp, tmp_bytes));
+    guard.p.push_back(tmp);
+    EN_TRY(cub::DeviceSelect::Flagged(tmp, tmp_bytes, ids, flags, cells, d_nsel, static_cast<int>(ncells), s));
+    int nc = 0;
+    EN_TRY(cudaMemcpyAsync(&nc, d_nsel, sizeof(int), cudaMemcpyDeviceToHost, s));
+    EN_TRY(cudaStreamSynchronize(s));
+    *n_cells = nc;
+    double total = 0.0;
+    if (nc > 0) {
+        EN_TRY(cudaMalloc(&contrib, sizeof(double) * nc));
+        guard.p.push_back(contrib);
+        const long long nblk = (nc + 4095) / 4096;
+        EN_TRY(cudaMalloc(&partial, sizeof(double) * nblk));
+        guard.p.push_back(partial);
+        if (P.dim == 3) {
+            const int r = refine;
+            const double dxp = P.dx / r;
+            const double select = std::sqrt(3.0) / 2.0 * dxp;  // metrics.cpp:157
+            contrib_3d<<<static_cast<unsigned>((nc + 127) / 128), 128, 0, s>>>(P, phi, dist, cells, nc, r, dxp,
+                                                                                select, p, contrib);
+        } else {
+            contrib_2d<<<static_cast<unsigned>((nc + 127) / 128), 128, 0, s>>>(P, phi, dist, cells, nc, p, contrib,
+                                                                                ood);
+        }
+        lsr_note_launch();
+        block_partials<<<static_cast<unsigned>((nblk + 127) / 128), 128, 0, s>>>(contrib, nc, partial);
+        lsr_note_launch();
+        EN_TRY(cudaGetLastError());
+        std::vector<double> h(nblk);
+        int h_ood = 0;
+        EN_TRY(cudaMemcpyAsync(h.data(), partial, sizeof(double) * nblk, cudaMemcpyDeviceToHost, s));
+        EN_TRY(cudaMemcpyAsync(&h_ood, ood, sizeof(int), cudaMemcpyDeviceToHost, s));
+        EN_TRY(cudaStreamSynchronize(s));
+        if (h_ood) {
+            *err = "locate_cell: point outside grid hull";
+            return LSR_ERR_OUT_OF_DOMAIN;
+        }
+        for (double v : h) total += v;  // blocked_sum (parallel.hpp:39-40)
+    }
+    *energy = std::pow(total, 1.0 / p);  // metrics.cpp:142,183
+    return LSR_OK;
+#undef EN_TRY
+}

@@ -11,6 +11,7 @@
 #include <string>
 
 #include "lsr_cuda.h"
+#include "prep_launch.h"
 #include "sl_launch.h"
 
 using lsr_dev::SlParams;
@@ -127,6 +128,7 @@ struct lsr_cuda_ctx {
     double* phi = nullptr;
     double* out = nullptr;
     double* dist = nullptr;
+    unsigned char* exact = nullptr;  // DistanceField::exact (distance.hpp:16)
     int64_t* active = nullptr;
     int64_t n_active = 0, cap_active = 0;
     int64_t* dirty = nullptr;  // ids where out may differ from phi
@@ -138,6 +140,7 @@ struct lsr_cuda_ctx {
     cudaStream_t stream = nullptr;
     cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
     float kernel_ms = 0.f, step_ms = 0.f;
+    int64_t n_interface_cells = 0;
 };
 
 namespace {
@@ -204,6 +207,7 @@ int lsr_cuda_destroy(lsr_cuda_ctx* c) {
     cudaFree(c->phi);
     cudaFree(c->out);
     cudaFree(c->dist);
+    cudaFree(c->exact);
     cudaFree(c->active);
     cudaFree(c->dirty);
     cudaFree(c->d_bad);
@@ -379,6 +383,70 @@ int lsr_cuda_sl_step_host(const lsr_grid* grid, const double* phi, const double*
     LSR_CUDA_TRY(cudaMemcpyAsync(out, c->out, bytes, cudaMemcpyDeviceToHost, s));
     LSR_CUDA_TRY(cudaStreamSynchronize(s));
     if (st == LSR_ERR_NUMERICAL) return set_err(st, msg);
+    return st;
+}
+
+int lsr_cuda_ctx_build_distance(lsr_cuda_ctx* c, const double* pts, int64_t n, int dim, int seed_only,
+                                double* sentinel, int* rounds) {
+    if (!c || (n > 0 && !pts)) return set_err(LSR_ERR_CONFIG, "build_distance: null argument");
+    LSR_CUDA_TRY(cudaSetDevice(c->device));
+    if (!c->exact) LSR_CUDA_TRY(cudaMalloc(&c->exact, static_cast<size_t>(c->n)));
+    std::string err;
+    double sent = 0.0;
+    int r = 0;
+    const int st = lsr_prep_build_distance(&c->grid, pts, n, dim, seed_only, c->dist, c->exact, &sent, &r, c->stream,
+                                           &err);
+    if (st) return set_err(st, err);
+    LSR_CUDA_TRY(cudaStreamSynchronize(c->stream));
+    if (sentinel) *sentinel = sent;
+    if (rounds) *rounds = r;
+    return LSR_OK;
+}
+
+int lsr_cuda_surface_energy(lsr_cuda_ctx* c, int which, int p, int refine, double* energy) {
+    if (!c || !energy) return set_err(LSR_ERR_CONFIG, "surface_energy: null argument");
+    double** slot = field_slot(c, which);
+    if (!slot || which == LSR_FIELD_DIST) return set_err(LSR_ERR_CONFIG, "surface_energy: phi must be PHI or OUT");
+    LSR_CUDA_TRY(cudaSetDevice(c->device));
+    lsr_step_cfg dummy{1, LSR_INTERP_Q1, 0.0, 1.0, 1e-3, 1.0, 2.0, 1.0};
+    const SlParams P = make_params(c->grid, dummy, 1.0);
+    std::string err;
+    int64_t nc = 0;
+    const int st = lsr_prep_surface_energy(P, *slot, c->dist, p, refine, energy, &nc, c->stream, &err);
+    if (st) return set_err(st, err);
+    c->n_interface_cells = nc;
+    return LSR_OK;
+}
+
+int lsr_cuda_surface_energy_host(const lsr_grid* grid, const double* phi, const double* dist, int p, int refine,
+                                 double* energy) {
+    if (int st = check_grid(grid)) return st;
+    if (!phi || !dist || !energy) return set_err(LSR_ERR_CONFIG, "surface_energy: null argument");
+    int dev = 0;
+    LSR_CUDA_TRY(cudaGetDevice(&dev));
+    lsr_cuda_ctx* c = nullptr;
+    if (int st = lsr_cuda_create(dev, grid, &c)) return st;
+    int st = lsr_cuda_upload_field(c, LSR_FIELD_PHI, phi);
+    if (st == LSR_OK) st = lsr_cuda_upload_field(c, LSR_FIELD_DIST, dist);
+    if (st == LSR_OK) st = lsr_cuda_surface_energy(c, LSR_FIELD_PHI, p, refine, energy);
+    lsr_cuda_destroy(c);
+    return st;
+}
+
+int lsr_cuda_build_distance(const lsr_grid* grid, const double* pts, int64_t n, int dim, int seed_only,
+                            double* d_out, uint8_t* exact_out, double* sentinel, int* rounds) {
+    if (int st = check_grid(grid)) return st;
+    int dev = 0;
+    LSR_CUDA_TRY(cudaGetDevice(&dev));
+    lsr_cuda_ctx* c = nullptr;
+    if (int st = lsr_cuda_create(dev, grid, &c)) return st;
+    int st = lsr_cuda_ctx_build_distance(c, pts, n, dim, seed_only, sentinel, rounds);
+    if (st == LSR_OK && d_out) st = lsr_cuda_download_field(c, LSR_FIELD_DIST, d_out);
+    if (st == LSR_OK && exact_out) {
+        const cudaError_t e = cudaMemcpy(exact_out, c->exact, static_cast<size_t>(c->n), cudaMemcpyDeviceToHost);
+        if (e != cudaSuccess) st = cuda_err(e, "download exact");
+    }
+    lsr_cuda_destroy(c);
     return st;
 }
 

@@ -183,6 +183,40 @@ def main():
         np.savez_compressed(os.path.join(OUT, f"band_{dim}d.npz"), dims=np.array(g["dims"]),
                             origin=np.array(g["origin"]), dx=g["dx"], dim=dim, phi=phi, gamma=gam, state=st,
                             active=act, tube=tube)
+    # distance fields: lsr::build_distance_field (distance.cpp:144) and
+    # lsr::seed_exact_distance (distance.cpp:8)
+    for name, g, pts, seed_only in (
+        ("circle2d", grid(65, 2), cloud_circle(200, 0.3, rng), False),
+        ("sphere3d", grid(33, 3), cloud_sphere(3000, 0.5, rng), False),
+        ("torus3d", grid(37, 3), cloud_torus(5000, 0.5, 0.2, 0.01, rng), False),
+        ("seedonly3d", grid(29, 3), cloud_sphere(800, 0.6, rng, c=(0.1, 0.0, -0.05)), True),
+    ):
+        d, ex, sent, rounds = R.build_distance(g, pts, g["dim"], seed_only=seed_only)
+        np.savez_compressed(os.path.join(OUT, f"dist_{name}.npz"), dims=np.array(g["dims"]),
+                            origin=np.array(g["origin"]), dx=g["dx"], dim=g["dim"], pts=pts, d=d, exact=ex,
+                            sentinel=sent, rounds=rounds, seed_only=int(seed_only))
+        print("dist", name, "rounds", rounds, "exact", int(ex.sum()))
+    # surface energy: lsr::surface_energy (metrics.cpp:186) with the reference's
+    # interface_cells (metrics.cpp:35) — what the driver feeds to sl_step
+    for name, g, shape, pts, p, refine in (
+        ("circle2d", grid(129, 2), "circle", cloud_circle(300, 0.3, rng), 2, 5),
+        ("circle2d_p1", grid(65, 2), "wavy", cloud_circle(200, 0.4, rng), 1, 5),
+        ("sphere3d", grid(41, 3), "sphere", cloud_sphere(4000, 0.5, rng), 2, 5),
+        ("torus3d_r3", grid(37, 3), "wavy", cloud_torus(5000, 0.5, 0.2, 0.01, rng), 2, 3),
+        ("sphere3d_p1", grid(33, 3), "sphere", cloud_sphere(3000, 0.45, rng), 1, 5),
+    ):
+        x, y, z = mesh(g)
+        r = np.sqrt(x * x + y * y + z * z)
+        phi = r - 0.8 if shape != "wavy" else r - 0.6 + 0.05 * np.sin(9 * x) * np.cos(7 * y)
+        if shape == "circle":
+            phi = np.round(phi / (0.25 * g["dx"])) * (0.25 * g["dx"])  # exact zeros at corners
+        d, _, _, _ = R.build_distance(g, pts, g["dim"])
+        e = R.surface_energy(g, phi, d, p, refine)
+        cells = R.interface_cells(g, phi)
+        np.savez_compressed(os.path.join(OUT, f"energy_{name}.npz"), dims=np.array(g["dims"]),
+                            origin=np.array(g["origin"]), dx=g["dx"], dim=g["dim"], phi=phi, d=d, p=p, refine=refine,
+                            energy=e, n_cells=cells.size)
+        print("energy", name, e, cells.size)
     print("golden fixtures written to", OUT)
 
 
