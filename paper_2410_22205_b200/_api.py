@@ -20,7 +20,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-lib_path = os.path.join(_HERE, "liblsr_b200.so")
+lib_path = os.environ.get("LSR_B200_LIB") or os.path.join(_HERE, "liblsr_b200.so")  # override: kernel experiments
 
 
 # --------------------------------------------------------------------------

@@ -7,7 +7,14 @@
 
 #include "sl_device.cuh"
 
-constexpr int kSlThreads = 128;
+#ifndef LSR_SL_THREADS
+#define LSR_SL_THREADS 128
+#endif
+#ifndef LSR_SL_MIN_BLOCKS
+#define LSR_SL_MIN_BLOCKS 4
+#endif
+constexpr int kSlThreads = LSR_SL_THREADS;
+constexpr int kSlMinBlocks = LSR_SL_MIN_BLOCKS;  // resident CTAs per SM the register budget must allow
 
 // bumps the process-wide launch counter (lsr_cuda_kernel_launches)
 void lsr_note_launch();

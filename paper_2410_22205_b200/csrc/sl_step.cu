@@ -18,7 +18,7 @@
 namespace lsr_dev {
 
 template <int DIM, int KIND>
-__global__ void __launch_bounds__(kSlThreads) sl_step_kernel(SlParams P, const double* __restrict__ phi,
+__global__ void __launch_bounds__(kSlThreads, kSlMinBlocks) sl_step_kernel(SlParams P, const double* __restrict__ phi,
                                                              const double* __restrict__ dist,
                                                              const int64_t* __restrict__ active,
                                                              long long n_active, double* __restrict__ out,
