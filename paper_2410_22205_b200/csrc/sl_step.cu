@@ -38,7 +38,12 @@ __global__ void __launch_bounds__(kSlThreads, kSlMinBlocks) sl_step_kernel(SlPar
         j = static_cast<int>((id / P.nx) % P.ny);
         k = static_cast<int>(id / P.nxy);
     }
-    const double next = sl_node<DIM, KIND>(P, phi, dist, id, i, j, k);
+    double* sb = nullptr;
+    if (LSR_SMEM_FEET && DIM == 3 && KIND == 1) {  // per-thread double-buffered stencil columns
+        __shared__ double sbuf[2 * 16 * kSlThreads];
+        sb = sbuf + threadIdx.x;
+    }
+    const double next = sl_node<DIM, KIND, kSlThreads>(P, phi, dist, id, i, j, k, sb);
     if (!isfinite(next)) atomicMin(bad, static_cast<unsigned long long>(id));
     out[id] = next;
 }
