@@ -1,0 +1,17 @@
+#!/bin/bash
+# Round measurement recipe (run under gpurun on one B200):
+#   tools/profile_round.sh r01
+# 1. the contract bench line, 2. the plain run of the profiled command,
+# 3. the ncu launch list of that command, 4. one ncu --set full capture of the
+# SL kernel. Outputs land in gpurun_out/; summaries are made locally with
+# tools/ncu_summary.py and committed under profiles/.
+R=${1:-r01}
+python bench.py > gpurun_out/bench_$R.json 2> gpurun_out/bench_$R.err
+CMD="python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu-baseline"
+$CMD > gpurun_out/plain_$R.log 2>&1 || exit 1
+ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"sl_step_kernel|resync_kernel|FillFunctor" \
+    -c 40 --csv --log-file gpurun_out/launches_$R.csv $CMD > gpurun_out/ncu_launch_$R.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:sl_step_kernel -s 4 -c 1 \
+    -o gpurun_out/sl_full_$R $CMD > gpurun_out/ncu_full_$R.log 2>&1
+tail -2 gpurun_out/ncu_full_$R.log
+cat gpurun_out/bench_$R.json
