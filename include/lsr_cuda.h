@@ -147,6 +147,49 @@ int lsr_cuda_surface_energy(lsr_cuda_ctx* ctx, int which, int p, int refine, dou
 int lsr_cuda_surface_energy_host(const lsr_grid* grid, const double* phi, const double* dist, int p, int refine,
                                  double* energy);
 
+/* ---- band rebuild ----
+ * lsr::narrow_band (grid.cpp:76-124; grid.hpp:105) of field `which` (PHI or
+ * OUT): NodeState per node, ascending ACTIVE and tube (ACTIVE+REINIT_HALO)
+ * lists, bit-identical; the ACTIVE list also becomes the context's active
+ * set for lsr_cuda_sl_step. lsr_cuda_band_download copies the last band to
+ * host (state: num_nodes bytes; active/tube: n_active/n_tube ids; any may be
+ * NULL). lsr::clamp_field (grid.cpp:126-134) in place. */
+int lsr_cuda_narrow_band(lsr_cuda_ctx* ctx, int which, double gamma, int64_t* n_active, int64_t* n_tube);
+int lsr_cuda_band_download(lsr_cuda_ctx* ctx, uint8_t* state, int64_t* active, int64_t* tube);
+int lsr_cuda_clamp_field(lsr_cuda_ctx* ctx, int which, double gamma);
+
+/* ---- reinitialisation ----
+ * lsr::reinitialize (reinit.cpp:133-145; reinit.hpp:43-44) of field `which`
+ * on the band last built by lsr_cuda_narrow_band: interface_one_step,
+ * Jacobi reinit_iterate on tube minus frozen, clamp to [-gamma, gamma].
+ * Bit-identical, same iteration count. ReinitConfig (reinit.hpp:7-18): */
+typedef struct lsr_reinit_cfg {
+    double dtau;
+    int32_t max_iters;
+    double residual_tol;
+    double sign_eps;
+} lsr_reinit_cfg;
+int lsr_cuda_reinitialize(lsr_cuda_ctx* ctx, int which, double gamma, const lsr_reinit_cfg* cfg, int* iterations,
+                          int* had_interface);
+/* ReinitConfig::defaults(dx, gamma) (reinit.cpp:8-16) */
+void lsr_cuda_reinit_defaults(double dx, double gamma, lsr_reinit_cfg* cfg);
+
+/* ---- one iteration of the driver loop body on the device ----
+ * driver.cpp:187-203 on a fixed grid: band of PHI, E_2 of PHI (or
+ * energy_override when >= 0), sl_step PHI -> OUT, reinitialize OUT on the
+ * band of PHI, swap. Per-phase device times in ms[0..3] (band, energy, SL,
+ * reinit). */
+typedef struct lsr_loop_stats {
+    double energy;
+    int64_t n_active;
+    int64_t n_tube;
+    int32_t reinit_iterations;
+    int32_t had_interface;
+    float ms[4];
+} lsr_loop_stats;
+int lsr_cuda_loop_step(lsr_cuda_ctx* ctx, const lsr_step_cfg* cfg, const lsr_reinit_cfg* rcfg, int energy_refine,
+                       double energy_override, lsr_loop_stats* stats);
+
 /* ---- self-test hook ----
  * Divides n pseudo-random doubles by c with the kernels' constant-divisor
  * division and with the hardware IEEE division; *mismatches = how many

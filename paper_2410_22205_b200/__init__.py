@@ -25,6 +25,7 @@ from ._api import (  # noqa: F401
     NodeState,
     NumericalError,
     OutOfDomainError,
+    ReinitConfig,
     ScalarField,
     StepConfig,
     build_distance_field,

@@ -124,8 +124,42 @@ def lib() -> C.CDLL:
     L.lsr_cloud_generate.argtypes = [C.c_int, C.c_int64, C.c_uint64, C.c_double, _dp]
     L.lsr_cuda_surface_energy.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, P(C.c_double)]
     L.lsr_cuda_surface_energy_host.argtypes = [P(CGrid), _dp, _dp, C.c_int, C.c_int, P(C.c_double)]
+    L.lsr_cuda_narrow_band.argtypes = [C.c_void_p, C.c_int, C.c_double, P(C.c_int64), P(C.c_int64)]
+    L.lsr_cuda_band_download.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+    L.lsr_cuda_clamp_field.argtypes = [C.c_void_p, C.c_int, C.c_double]
+    L.lsr_cuda_reinitialize.argtypes = [C.c_void_p, C.c_int, C.c_double, P(CReinitCfg), P(C.c_int), P(C.c_int)]
+    L.lsr_cuda_reinit_defaults.argtypes = [C.c_double, C.c_double, P(CReinitCfg)]
+    L.lsr_cuda_reinit_defaults.restype = None
+    L.lsr_cuda_loop_step.argtypes = [C.c_void_p, P(CStepCfg), P(CReinitCfg), C.c_int, C.c_double, P(CLoopStats)]
     _lib = L
     return L
+
+
+class CReinitCfg(C.Structure):  # ReinitConfig (reinit.hpp:7-18)
+    _fields_ = [("dtau", C.c_double), ("max_iters", C.c_int32), ("residual_tol", C.c_double),
+                ("sign_eps", C.c_double)]
+
+
+class CLoopStats(C.Structure):
+    _fields_ = [("energy", C.c_double), ("n_active", C.c_int64), ("n_tube", C.c_int64),
+                ("reinit_iterations", C.c_int32), ("had_interface", C.c_int32), ("ms", C.c_float * 4)]
+
+
+@dataclass
+class ReinitConfig:  # reinit.hpp:7-18
+    dtau: float = 0.0
+    max_iters: int = 0
+    residual_tol: float = 1e-3
+    sign_eps: float = 0.0
+
+    @staticmethod
+    def defaults(dx: float, gamma: float) -> "ReinitConfig":  # reinit.cpp:8-16
+        c = CReinitCfg()
+        lib().lsr_cuda_reinit_defaults(float(dx), float(gamma), C.byref(c))
+        return ReinitConfig(c.dtau, c.max_iters, c.residual_tol, c.sign_eps)
+
+    def c(self) -> CReinitCfg:
+        return CReinitCfg(float(self.dtau), int(self.max_iters), float(self.residual_tol), float(self.sign_eps))
 
 
 def surface_energy(phi: "ScalarField", dist: "DistanceField", p: int, subcell_refine: int = 5) -> float:
@@ -422,6 +456,44 @@ class Context:
         e = C.c_double()
         _check(lib().lsr_cuda_surface_energy(self.h, int(which), int(p), int(subcell_refine), C.byref(e)))
         return e.value
+
+    def narrow_band(self, gamma: float, which: int = FIELD_PHI):
+        """lsr::narrow_band on the device; returns (n_active, n_tube). The
+        ACTIVE list becomes this context's active set."""
+        na, nt = C.c_int64(), C.c_int64()
+        _check(lib().lsr_cuda_narrow_band(self.h, int(which), float(gamma), C.byref(na), C.byref(nt)))
+        self.n_active, self.n_tube = na.value, nt.value
+        return na.value, nt.value
+
+    def band(self) -> "BandMask":
+        """The last device-built band as a host BandMask (state, active, tube)."""
+        n = self.grid.num_nodes()
+        st = np.empty(n, np.uint8)
+        act = np.empty(self.n_active, np.int64)
+        tube = np.empty(self.n_tube, np.int64)
+        _check(lib().lsr_cuda_band_download(self.h, st.ctypes.data_as(C.c_void_p), act.ctypes.data_as(C.c_void_p),
+                                            tube.ctypes.data_as(C.c_void_p)))
+        return BandMask(self.grid, st, act, tube)
+
+    def clamp_field(self, gamma: float, which: int = FIELD_PHI):
+        _check(lib().lsr_cuda_clamp_field(self.h, int(which), float(gamma)))
+
+    def reinitialize(self, gamma: float, cfg: "ReinitConfig", which: int = FIELD_OUT):
+        """lsr::reinitialize of `which` on the last built band; returns
+        (iterations, had_interface)."""
+        it, had = C.c_int(), C.c_int()
+        _check(lib().lsr_cuda_reinitialize(self.h, int(which), float(gamma), C.byref(cfg.c()), C.byref(it),
+                                           C.byref(had)))
+        return it.value, bool(had.value)
+
+    def loop_step(self, cfg: StepConfig, rcfg: "ReinitConfig", energy_refine: int = 5,
+                  energy_override: float | None = None) -> dict:
+        """One driver iteration (driver.cpp:187-203) on the device."""
+        s = CLoopStats()
+        _check(lib().lsr_cuda_loop_step(self.h, C.byref(cfg.c()), C.byref(rcfg.c()), int(energy_refine),
+                                        -1.0 if energy_override is None else float(energy_override), C.byref(s)))
+        return dict(energy=s.energy, n_active=s.n_active, n_tube=s.n_tube, reinit_iterations=s.reinit_iterations,
+                    had_interface=bool(s.had_interface), ms=list(s.ms))
 
     def last_times(self):
         k, s = C.c_float(), C.c_float()

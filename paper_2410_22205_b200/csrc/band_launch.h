@@ -1,0 +1,53 @@
+// Internal interface of the band rebuild and reinitialisation kernels
+// (band_reinit.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <string>
+
+#include "sl_device.cuh"
+
+void lsr_note_launch();
+
+// BandMask on the device (grid.hpp:79-84): state per node, ascending
+// active / tube id lists.
+struct BandBuffers {
+    unsigned char* state = nullptr;
+    long long* active = nullptr;
+    long long* tube = nullptr;
+    long long* counts = nullptr;
+    void* tmp = nullptr;
+    size_t tmp_bytes = 0;
+    long long cap = 0;
+    long long n_active = 0, n_tube = 0;
+    int reserve(long long n, std::string* err);
+    void release();
+};
+
+// ReinitConfig (reinit.hpp:7-18)
+struct ReinitParams {
+    double dtau;
+    int max_iters;
+    double residual_tol;
+    double sign_eps;
+};
+
+struct ReinitBuffers {
+    unsigned char* frozen = nullptr;
+    long long* nodes = nullptr;
+    double* sgn = nullptr;
+    unsigned long long* scal = nullptr;
+    void* tmp = nullptr;
+    size_t tmp_bytes = 0;
+    long long cap = 0;
+    int reserve(long long n, std::string* err);
+    void release();
+};
+
+int lsr_band_build(const lsr_dev::SlParams& P, const double* phi, double gamma, BandBuffers& B, long long* n_active,
+                   long long* n_tube, cudaStream_t s, std::string* err);
+int lsr_clamp(double* f, long long n, double gamma, cudaStream_t s, std::string* err);
+int lsr_reinitialize(const lsr_dev::SlParams& P, double** phi, double** scratch, const BandBuffers& B, double gamma,
+                     const ReinitParams& R, ReinitBuffers& W, int* iterations, int* had_interface, cudaStream_t s,
+                     std::string* err);

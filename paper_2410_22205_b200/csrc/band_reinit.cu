@@ -1,0 +1,372 @@
+// band_reinit.cu — the band rebuild and the constrained reinitialisation on
+// the GPU, bit-identical to the reference.
+//
+//  narrow_band (/root/reference/proj/src/grid.cpp:76-124): one fused pass
+//    classifies every node (ACTIVE if |phi| < gamma, else REINIT_HALO if any
+//    of its 3^dim neighbours is ACTIVE). The reference's in-place halo pass
+//    only reads ACTIVE flags and only writes INACTIVE nodes, so evaluating
+//    the neighbours' ACTIVE test directly is the same function. The
+//    ascending `active` and `tube` lists come from order-preserving
+//    compactions (cub::DeviceSelect).
+//  clamp_field (grid.cpp:126-134): elementwise std::min(std::max(v,-g), g).
+//  interface_one_step (reinit.cpp:18-59): out of place (the reference reads a
+//    full copy `prev`), so every node sees the pre-pass values.
+//  reinit_iterate (reinit.cpp:88-131): the node list is the tube minus the
+//    frozen nodes (order preserved); Jacobi sweeps write the other buffer;
+//    the residual max is an integer atomicMax on the non-negative bits of
+//    |upd| (max is order free); the two buffers only ever differ on the node
+//    list, so the reference's `std::swap` is a pointer swap.
+#include <cuda_runtime.h>
+
+#include <cub/cub.cuh>
+
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <string>
+
+#include "band_launch.h"
+#include "lsr_cuda.h"
+#include "sl_device.cuh"
+
+using lsr_dev::SlParams;
+
+namespace {
+
+__device__ __forceinline__ double smax(double a, double b) { return (a < b) ? b : a; }
+__device__ __forceinline__ double smin(double a, double b) { return (b < a) ? b : a; }
+
+// narrow_band state (grid.cpp:85-116): 1 ACTIVE, 2 REINIT_HALO, 0 INACTIVE
+__global__ void band_state(SlParams P, const double* __restrict__ phi, double gamma, long long n,
+                           unsigned char* __restrict__ state) {
+    const long long id = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (id >= n) return;
+    if (fabs(__ldg(phi + id)) < gamma) {
+        state[id] = 1;
+        return;
+    }
+    const int i = static_cast<int>(id % P.nx);
+    const int j = static_cast<int>((id / P.nx) % P.ny);
+    const int k = static_cast<int>(id / P.nxy);
+    const int kz = P.dim == 3 ? 1 : 0;
+    bool near = false;
+    for (int dk = -kz; dk <= kz && !near; ++dk)
+        for (int dj = -1; dj <= 1 && !near; ++dj)
+            for (int di = -1; di <= 1 && !near; ++di) {
+                const int ni = i + di, nj = j + dj, nk = k + dk;
+                if (ni < 0 || nj < 0 || nk < 0 || ni >= P.nx || nj >= P.ny || nk >= P.nz) continue;
+                near = fabs(__ldg(phi + (static_cast<long long>(nk) * P.ny + nj) * P.nx + ni)) < gamma;
+            }
+    state[id] = near ? 2 : 0;
+}
+
+struct IsActive {
+    const unsigned char* s;
+    __device__ bool operator()(long long id) const { return s[id] == 1; }
+};
+struct InTube {
+    const unsigned char* s;
+    __device__ bool operator()(long long id) const { return s[id] != 0; }
+};
+struct InTubeNotFrozen {
+    const unsigned char* s;
+    const unsigned char* frozen;
+    __device__ bool operator()(long long id) const { return s[id] != 0 && !frozen[id]; }
+};
+
+__global__ void clamp_kernel(double* __restrict__ f, long long n, double gamma) {
+    const long long id = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (id >= n) return;
+    f[id] = smin(smax(f[id], -gamma), gamma);
+}
+
+// interface_one_step (reinit.cpp:24-46); `prev` is read-only, `out` gets every node
+__global__ void one_step(SlParams P, const double* __restrict__ prev, double* __restrict__ out,
+                         unsigned char* __restrict__ frozen, long long n, int* __restrict__ any_frozen,
+                         int* __restrict__ any_zero) {
+    const long long id = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (id >= n) return;
+    const double pj = __ldg(prev + id);
+    frozen[id] = 0;
+    out[id] = pj;
+    if (pj == 0.0) {
+        *any_zero = 1;
+        return;
+    }
+    const int i = static_cast<int>(id % P.nx);
+    const int j = static_cast<int>((id / P.nx) % P.ny);
+    const int k = static_cast<int>(id / P.nxy);
+    const int ijk[3] = {i, j, k};
+    const int nn[3] = {P.nx, P.ny, P.nz};
+    const long long st[3] = {1, P.nx, P.nxy};
+    double best = -1.0;
+    for (int ax = 0; ax < P.dim; ++ax) {
+        for (int s = -1; s <= 1; s += 2) {
+            const int c = ijk[ax] + s;
+            if (c < 0 || c >= nn[ax]) continue;
+            const double pk = __ldg(prev + id + s * st[ax]);
+            if (pj * pk >= 0.0) continue;
+            const double crossing = P.dx * fabs(pj) / (fabs(pj) + fabs(pk));
+            best = best < 0.0 ? crossing : smin(best, crossing);
+        }
+    }
+    if (best >= 0.0) {
+        out[id] = pj > 0.0 ? best : -best;
+        frozen[id] = 1;
+        *any_frozen = 1;
+    }
+}
+
+// smoothed sign at entry (reinit.cpp:250-257)
+__global__ void sign_kernel(const double* __restrict__ phi, const long long* __restrict__ nodes, long long nn,
+                            double eps2, double* __restrict__ sgn) {
+    const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t >= nn) return;
+    const double v = __ldg(phi + nodes[t]);
+    sgn[t] = v / sqrt(v * v + eps2);
+}
+
+// godunov_norm (reinit.cpp:63-84)
+__device__ __forceinline__ double godunov_norm(const SlParams& P, const double* __restrict__ phi, long long id, int i,
+                                               int j, int k, double sgn) {
+    const int ijk[3] = {i, j, k};
+    const int nn[3] = {P.nx, P.ny, P.nz};
+    const long long st[3] = {1, P.nx, P.nxy};
+    const double pc = __ldg(phi + id);
+    double acc = 0.0;
+    for (int ax = 0; ax < P.dim; ++ax) {
+        double dminus = 0.0, dplus = 0.0;
+        if (ijk[ax] > 0) dminus = lsr_dev::div_const(pc - __ldg(phi + id - st[ax]), P.dx, P.rdx, P.fast_div);
+        if (ijk[ax] < nn[ax] - 1) dplus = lsr_dev::div_const(__ldg(phi + id + st[ax]) - pc, P.dx, P.rdx, P.fast_div);
+        if (sgn > 0.0) {
+            const double a = smax(dminus, 0.0), b = smin(dplus, 0.0);
+            acc += smax(a * a, b * b);
+        } else {
+            const double a = smin(dminus, 0.0), b = smax(dplus, 0.0);
+            acc += smax(a * a, b * b);
+        }
+    }
+    return sqrt(acc);
+}
+
+// one Jacobi iteration (reinit.cpp:111-124)
+__global__ void jacobi(SlParams P, const double* __restrict__ cur, double* __restrict__ nxt,
+                       const long long* __restrict__ nodes, const double* __restrict__ sgn, long long nn, double dtau,
+                       unsigned long long* __restrict__ residual) {
+    const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t >= nn) return;
+    const long long id = nodes[t];
+    const int i = static_cast<int>(id % P.nx);
+    const int j = static_cast<int>((id / P.nx) % P.ny);
+    const int k = static_cast<int>(id / P.nxy);
+    const double s = sgn[t];
+    const double gn = godunov_norm(P, cur, id, i, j, k, s);
+    const double upd = -dtau * s * (gn - 1.0);
+    nxt[id] = __ldg(cur + id) + upd;
+    const double a = fabs(upd);
+    // std::max(residual, |upd|): a NaN update never raises the running max
+    if (a > 0.0) atomicMax(residual, static_cast<unsigned long long>(__double_as_longlong(a)));
+}
+
+__global__ void copy_ids(const double* __restrict__ src, double* __restrict__ dst, const long long* __restrict__ ids,
+                         long long n) {
+    const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    const long long id = ids[t];
+    dst[id] = src[id];
+}
+
+}  // namespace
+
+#define BR_TRY(x)                                                    \
+    do {                                                             \
+        cudaError_t e_ = (x);                                        \
+        if (e_ != cudaSuccess) {                                     \
+            *err = std::string(#x) + ": " + cudaGetErrorString(e_);  \
+            return LSR_ERR_CUDA;                                     \
+        }                                                            \
+    } while (0)
+
+int BandBuffers::reserve(long long n, std::string* err) {
+    if (n <= cap) return LSR_OK;
+    release();
+    BR_TRY(cudaMalloc(&state, n));
+    BR_TRY(cudaMalloc(&active, sizeof(long long) * n));
+    BR_TRY(cudaMalloc(&tube, sizeof(long long) * n));
+    BR_TRY(cudaMalloc(&counts, sizeof(long long) * 2));
+    cap = n;
+    return LSR_OK;
+}
+
+void BandBuffers::release() {
+    cudaFree(state);
+    cudaFree(active);
+    cudaFree(tube);
+    cudaFree(counts);
+    cudaFree(tmp);
+    state = nullptr;
+    active = tube = nullptr;
+    counts = nullptr;
+    tmp = nullptr;
+    tmp_bytes = 0;
+    cap = 0;
+}
+
+static int ensure_tmp(BandBuffers& B, size_t bytes, std::string* err) {
+    if (bytes <= B.tmp_bytes) return LSR_OK;
+    cudaFree(B.tmp);
+    B.tmp = nullptr;
+    BR_TRY(cudaMalloc(&B.tmp, bytes));
+    B.tmp_bytes = bytes;
+    return LSR_OK;
+}
+
+int lsr_band_build(const SlParams& P, const double* phi, double gamma, BandBuffers& B, long long* n_active,
+                   long long* n_tube, cudaStream_t s, std::string* err) {
+    if (!(gamma > 0.0)) {
+        *err = "narrow_band: gamma must be positive";  // grid.cpp:77
+        return LSR_ERR_CONFIG;
+    }
+    const long long n = P.nxy * P.nz;
+    if (int st = B.reserve(n, err)) return st;
+    band_state<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(P, phi, gamma, n, B.state);
+    lsr_note_launch();
+    cub::CountingInputIterator<long long> ids(0);
+    size_t b1 = 0, b2 = 0;
+    BR_TRY(cub::DeviceSelect::If(nullptr, b1, ids, B.active, B.counts, n, IsActive{B.state}, s));
+    BR_TRY(cub::DeviceSelect::If(nullptr, b2, ids, B.tube, B.counts + 1, n, InTube{B.state}, s));
+    if (int st = ensure_tmp(B, b1 > b2 ? b1 : b2, err)) return st;
+    BR_TRY(cub::DeviceSelect::If(B.tmp, b1, ids, B.active, B.counts, n, IsActive{B.state}, s));
+    BR_TRY(cub::DeviceSelect::If(B.tmp, b2, ids, B.tube, B.counts + 1, n, InTube{B.state}, s));
+    long long h[2];
+    BR_TRY(cudaMemcpyAsync(h, B.counts, sizeof h, cudaMemcpyDeviceToHost, s));
+    BR_TRY(cudaStreamSynchronize(s));
+    *n_active = h[0];
+    *n_tube = h[1];
+    B.n_active = h[0];
+    B.n_tube = h[1];
+    return LSR_OK;
+}
+
+int lsr_clamp(double* f, long long n, double gamma, cudaStream_t s, std::string* err) {
+    if (!(gamma > 0.0)) {
+        *err = "clamp_field: gamma must be positive";  // grid.cpp:127
+        return LSR_ERR_CONFIG;
+    }
+    clamp_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(f, n, gamma);
+    lsr_note_launch();
+    BR_TRY(cudaGetLastError());
+    return LSR_OK;
+}
+
+int ReinitBuffers::reserve(long long n, std::string* err) {
+    if (n <= cap) return LSR_OK;
+    release();
+    BR_TRY(cudaMalloc(&frozen, n));
+    BR_TRY(cudaMalloc(&nodes, sizeof(long long) * n));
+    BR_TRY(cudaMalloc(&sgn, sizeof(double) * n));
+    BR_TRY(cudaMalloc(&scal, sizeof(unsigned long long) * 4));
+    cap = n;
+    return LSR_OK;
+}
+
+void ReinitBuffers::release() {
+    cudaFree(frozen);
+    cudaFree(nodes);
+    cudaFree(sgn);
+    cudaFree(scal);
+    cudaFree(tmp);
+    frozen = nullptr;
+    nodes = nullptr;
+    sgn = nullptr;
+    scal = nullptr;
+    tmp = nullptr;
+    tmp_bytes = 0;
+    cap = 0;
+}
+
+// reinitialize (reinit.cpp:133-145) of the field in *phi (device), on the
+// band B (tube list + state of the band field). *phi and *scratch are two
+// full-grid buffers; on return *phi holds the result (pointers may swap).
+int lsr_reinitialize(const SlParams& P, double** phi, double** scratch, const BandBuffers& B, double gamma,
+                     const ReinitParams& R, ReinitBuffers& W, int* iterations, int* had_interface, cudaStream_t s,
+                     std::string* err) {
+    if (!(R.dtau > 0.0)) {
+        *err = "reinit: dtau must be positive";  // reinit.hpp:46-47
+        return LSR_ERR_CONFIG;
+    }
+    if (R.max_iters < 1) {
+        *err = "reinit: max_iters must be >= 1";
+        return LSR_ERR_CONFIG;
+    }
+    const long long n = P.nxy * P.nz;
+    if (int st = W.reserve(n, err)) return st;
+    *iterations = 0;
+    *had_interface = 0;
+    int* flags = reinterpret_cast<int*>(W.scal);  // [0] any_frozen, [1] any_zero
+    BR_TRY(cudaMemsetAsync(W.scal, 0, sizeof(unsigned long long) * 4, s));
+    // interface_one_step: *phi -> *scratch (every node), frozen flags
+    one_step<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(P, *phi, *scratch, W.frozen, n, flags,
+                                                                     flags + 1);
+    lsr_note_launch();
+    int hf[2];
+    BR_TRY(cudaMemcpyAsync(hf, flags, sizeof hf, cudaMemcpyDeviceToHost, s));
+    BR_TRY(cudaStreamSynchronize(s));
+    if (!hf[0] && !hf[1]) {
+        // NoInterfaceError caught by reinitialize (reinit.cpp:140-142): phi is
+        // left as it was (the one-step wrote nothing), then clamped
+        return lsr_clamp(*phi, n, gamma, s, err);
+    }
+    std::swap(*phi, *scratch);  // *phi = one-step result
+    *had_interface = 1;
+    // nodes = tube minus frozen, ascending (reinit.cpp:94-98)
+    cub::CountingInputIterator<long long> ids(0);
+    size_t tb = 0;
+    long long* d_nn = reinterpret_cast<long long*>(W.scal + 2);
+    BR_TRY(cub::DeviceSelect::If(nullptr, tb, ids, W.nodes, d_nn, n, InTubeNotFrozen{B.state, W.frozen}, s));
+    if (tb > W.tmp_bytes) {
+        cudaFree(W.tmp);
+        W.tmp = nullptr;
+        BR_TRY(cudaMalloc(&W.tmp, tb));
+        W.tmp_bytes = tb;
+    }
+    BR_TRY(cub::DeviceSelect::If(W.tmp, tb, ids, W.nodes, d_nn, n, InTubeNotFrozen{B.state, W.frozen}, s));
+    long long nn = 0;
+    BR_TRY(cudaMemcpyAsync(&nn, d_nn, sizeof nn, cudaMemcpyDeviceToHost, s));
+    BR_TRY(cudaStreamSynchronize(s));
+    const unsigned gb = static_cast<unsigned>((nn + 255) / 256);
+    if (nn > 0) {
+        sign_kernel<<<gb, 256, 0, s>>>(*phi, W.nodes, nn, R.sign_eps * R.sign_eps, W.sgn);
+        lsr_note_launch();
+    }
+    // `next = phi` (reinit.cpp:259): the scratch buffer holds the pre-one-step
+    // field, which differs from phi on the frozen nodes -> one full copy
+    BR_TRY(cudaMemcpyAsync(*scratch, *phi, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+    const double tol = R.residual_tol * P.dx;
+    int iter = 0;
+    unsigned long long* d_res = W.scal + 3;
+    for (; iter < R.max_iters; ++iter) {
+        BR_TRY(cudaMemsetAsync(d_res, 0, sizeof(unsigned long long), s));
+        if (nn > 0) {
+            jacobi<<<gb, 256, 0, s>>>(P, *phi, *scratch, W.nodes, W.sgn, nn, R.dtau, d_res);
+            lsr_note_launch();
+        }
+        unsigned long long hr = 0;
+        BR_TRY(cudaMemcpyAsync(&hr, d_res, sizeof hr, cudaMemcpyDeviceToHost, s));
+        BR_TRY(cudaStreamSynchronize(s));
+        std::swap(*phi, *scratch);  // std::swap(phi.values, next.values) (reinit.cpp:274)
+        double residual;
+        std::memcpy(&residual, &hr, sizeof residual);
+        if (residual < tol) {
+            ++iter;
+            break;
+        }
+    }
+    // keep the two buffers equal on the node list for the caller's next use
+    if (nn > 0) {
+        copy_ids<<<gb, 256, 0, s>>>(*phi, *scratch, W.nodes, nn);
+        lsr_note_launch();
+    }
+    *iterations = iter;
+    return lsr_clamp(*phi, n, gamma, s, err);
+}

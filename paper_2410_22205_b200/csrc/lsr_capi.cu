@@ -11,6 +11,7 @@
 #include <string>
 
 #include "lsr_cuda.h"
+#include "band_launch.h"
 #include "prep_launch.h"
 #include "sl_launch.h"
 
@@ -141,6 +142,9 @@ struct lsr_cuda_ctx {
     cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
     float kernel_ms = 0.f, step_ms = 0.f;
     int64_t n_interface_cells = 0;
+    BandBuffers band;        // last narrow_band built on the device
+    ReinitBuffers rb;        // reinitialisation scratch
+    double* scratch = nullptr;  // third full-grid field (reinit double buffer)
 };
 
 namespace {
@@ -208,6 +212,9 @@ int lsr_cuda_destroy(lsr_cuda_ctx* c) {
     cudaFree(c->out);
     cudaFree(c->dist);
     cudaFree(c->exact);
+    cudaFree(c->scratch);
+    c->band.release();
+    c->rb.release();
     cudaFree(c->active);
     cudaFree(c->dirty);
     cudaFree(c->d_bad);
@@ -448,6 +455,141 @@ int lsr_cuda_build_distance(const lsr_grid* grid, const double* pts, int64_t n, 
     }
     lsr_cuda_destroy(c);
     return st;
+}
+
+// ---- band rebuild / reinitialisation / the whole loop body ----------------
+
+static SlParams grid_params(const lsr_grid& g) {
+    const lsr_step_cfg dummy{1, LSR_INTERP_Q1, 0.0, 1.0, 1e-3, 1.0, 2.0, 1.0};
+    return make_params(g, dummy, 1.0);
+}
+
+int lsr_cuda_narrow_band(lsr_cuda_ctx* c, int which, double gamma, int64_t* n_active, int64_t* n_tube) {
+    if (!c) return set_err(LSR_ERR_CONFIG, "null context");
+    double** slot = field_slot(c, which);
+    if (!slot || which == LSR_FIELD_DIST) return set_err(LSR_ERR_CONFIG, "narrow_band: phi must be PHI or OUT");
+    LSR_CUDA_TRY(cudaSetDevice(c->device));
+    std::string err;
+    long long na = 0, nt = 0;
+    if (int st = lsr_band_build(grid_params(c->grid), *slot, gamma, c->band, &na, &nt, c->stream, &err))
+        return set_err(st, err);
+    // the band's ACTIVE list becomes the context's active set
+    if (int st = ensure_ids(&c->active, &c->cap_active, na)) return st;
+    if (na > 0)
+        LSR_CUDA_TRY(cudaMemcpyAsync(c->active, c->band.active, sizeof(int64_t) * na, cudaMemcpyDeviceToDevice,
+                                     c->stream));
+    c->n_active = na;
+    if (n_active) *n_active = na;
+    if (n_tube) *n_tube = nt;
+    return LSR_OK;
+}
+
+int lsr_cuda_band_download(lsr_cuda_ctx* c, uint8_t* state, int64_t* active, int64_t* tube) {
+    if (!c || !c->band.state) return set_err(LSR_ERR_CONFIG, "band_download: no band built");
+    LSR_CUDA_TRY(cudaSetDevice(c->device));
+    if (state) LSR_CUDA_TRY(cudaMemcpyAsync(state, c->band.state, c->n, cudaMemcpyDeviceToHost, c->stream));
+    if (active && c->band.n_active)
+        LSR_CUDA_TRY(cudaMemcpyAsync(active, c->band.active, sizeof(int64_t) * c->band.n_active,
+                                     cudaMemcpyDeviceToHost, c->stream));
+    if (tube && c->band.n_tube)
+        LSR_CUDA_TRY(cudaMemcpyAsync(tube, c->band.tube, sizeof(int64_t) * c->band.n_tube, cudaMemcpyDeviceToHost,
+                                     c->stream));
+    LSR_CUDA_TRY(cudaStreamSynchronize(c->stream));
+    return LSR_OK;
+}
+
+int lsr_cuda_clamp_field(lsr_cuda_ctx* c, int which, double gamma) {
+    if (!c) return set_err(LSR_ERR_CONFIG, "null context");
+    double** slot = field_slot(c, which);
+    if (!slot) return set_err(LSR_ERR_CONFIG, "clamp_field: unknown field");
+    LSR_CUDA_TRY(cudaSetDevice(c->device));
+    std::string err;
+    if (int st = lsr_clamp(*slot, c->n, gamma, c->stream, &err)) return set_err(st, err);
+    LSR_CUDA_TRY(cudaStreamSynchronize(c->stream));
+    if (which != LSR_FIELD_DIST) c->consistent = false;
+    return LSR_OK;
+}
+
+int lsr_cuda_reinitialize(lsr_cuda_ctx* c, int which, double gamma, const lsr_reinit_cfg* rc, int* iterations,
+                          int* had_interface) {
+    if (!c || !rc) return set_err(LSR_ERR_CONFIG, "reinitialize: null argument");
+    double** slot = field_slot(c, which);
+    if (!slot || which == LSR_FIELD_DIST) return set_err(LSR_ERR_CONFIG, "reinitialize: phi must be PHI or OUT");
+    if (!c->band.state) return set_err(LSR_ERR_CONFIG, "reinitialize: build the band first (lsr_cuda_narrow_band)");
+    LSR_CUDA_TRY(cudaSetDevice(c->device));
+    if (!c->scratch) LSR_CUDA_TRY(cudaMalloc(&c->scratch, sizeof(double) * c->n));
+    const ReinitParams R{rc->dtau, rc->max_iters, rc->residual_tol, rc->sign_eps};
+    std::string err;
+    int it = 0, had = 0;
+    const int st = lsr_reinitialize(grid_params(c->grid), slot, &c->scratch, c->band, gamma, R, c->rb, &it, &had,
+                                    c->stream, &err);
+    if (st) return set_err(st, err);
+    LSR_CUDA_TRY(cudaStreamSynchronize(c->stream));
+    c->consistent = false;  // the clamp may touch any node
+    if (iterations) *iterations = it;
+    if (had_interface) *had_interface = had;
+    return LSR_OK;
+}
+
+void lsr_cuda_reinit_defaults(double dx, double gamma, lsr_reinit_cfg* rc) {  // ReinitConfig::defaults (reinit.cpp:8-16)
+    rc->dtau = 0.5 * dx;
+    rc->max_iters = 4 * static_cast<int>(std::ceil(gamma / dx));
+    rc->residual_tol = 1e-3;
+    rc->sign_eps = dx;
+}
+
+int lsr_cuda_loop_step(lsr_cuda_ctx* c, const lsr_step_cfg* cfg, const lsr_reinit_cfg* rc, int energy_refine,
+                       double energy_override, lsr_loop_stats* stats) {
+    if (!c || !cfg || !rc) return set_err(LSR_ERR_CONFIG, "loop_step: null argument");
+    if (int st = check_cfg(cfg, 1.0)) return st;
+    LSR_CUDA_TRY(cudaSetDevice(c->device));
+    cudaEvent_t ev[5];
+    for (auto& e : ev) LSR_CUDA_TRY(cudaEventCreate(&e));
+    struct EvGuard {
+        cudaEvent_t* e;
+        ~EvGuard() {
+            for (int i = 0; i < 5; ++i) cudaEventDestroy(e[i]);
+        }
+    } evg{ev};
+    lsr_loop_stats S{};
+    cudaEventRecord(ev[0], c->stream);
+    int64_t na = 0, nt = 0;
+    // 1. band of phi^n (driver.cpp:187)
+    if (int st = lsr_cuda_narrow_band(c, LSR_FIELD_PHI, cfg->gamma, &na, &nt)) return st;
+    cudaEventRecord(ev[1], c->stream);
+    // 2. E_2 of phi^n (driver.cpp:188)
+    double e2 = energy_override;
+    if (!(energy_override >= 0.0)) {
+        if (int st = lsr_cuda_surface_energy(c, LSR_FIELD_PHI, 2, energy_refine, &e2)) return st;
+    }
+    cudaEventRecord(ev[2], c->stream);
+    // 3. the SL step, skipped when p > 1 and E_2 == 0 (driver.cpp:191-195)
+    if (cfg->p > 1 && e2 == 0.0) {
+        LSR_CUDA_TRY(cudaMemcpyAsync(c->out, c->phi, sizeof(double) * c->n, cudaMemcpyDeviceToDevice, c->stream));
+        c->consistent = false;
+    } else {
+        int64_t bad = -1;
+        if (int st = lsr_cuda_sl_step(c, cfg, e2, &bad)) return st;
+    }
+    cudaEventRecord(ev[3], c->stream);
+    // 4. reinitialise phi^{n+1} on the band of phi^n (driver.cpp:196)
+    int it = 0, had = 0;
+    if (int st = lsr_cuda_reinitialize(c, LSR_FIELD_OUT, cfg->gamma, rc, &it, &had)) return st;
+    cudaEventRecord(ev[4], c->stream);
+    // 5. swap (driver.cpp:203)
+    std::swap(c->phi, c->out);
+    LSR_CUDA_TRY(cudaStreamSynchronize(c->stream));
+    S.energy = e2;
+    S.n_active = na;
+    S.n_tube = nt;
+    S.reinit_iterations = it;
+    S.had_interface = had;
+    cudaEventElapsedTime(&S.ms[0], ev[0], ev[1]);
+    cudaEventElapsedTime(&S.ms[1], ev[1], ev[2]);
+    cudaEventElapsedTime(&S.ms[2], ev[2], ev[3]);
+    cudaEventElapsedTime(&S.ms[3], ev[3], ev[4]);
+    if (stats) *stats = S;
+    return LSR_OK;
 }
 
 int lsr_cuda_selftest_div_const(double c, int64_t n, uint64_t seed, int64_t* mismatches) {

@@ -217,6 +217,55 @@ def main():
                             origin=np.array(g["origin"]), dx=g["dx"], dim=g["dim"], phi=phi, d=d, p=p, refine=refine,
                             energy=e, n_cells=cells.size)
         print("energy", name, e, cells.size)
+    # reinitialisation: lsr::reinitialize (reinit.cpp:133) on the band of a
+    # (possibly different) band field, as the driver does (driver.cpp:187,196)
+    for name, g, kind in (("sphere3d", grid(30, 3), "scaled"), ("circle2d", grid(65, 2), "scaled"),
+                          ("zeros3d", grid(26, 3), "zeros"), ("nointerface3d", grid(20, 3), "positive")):
+        x, y, z = mesh(g)
+        r = np.sqrt(x * x + y * y + z * z)
+        band_phi = r - 0.55
+        if kind == "scaled":
+            phi = 0.6 * (r - 0.55) + 0.3 * g["dx"] * np.sin(11 * x) * np.cos(5 * y)
+        elif kind == "zeros":
+            phi = np.round((r - 0.5) / (0.5 * g["dx"])) * (0.5 * g["dx"]) * 0.7
+        else:
+            phi = r + 0.2
+            band_phi = r - 0.55
+        gam = (6.0 if g["dim"] == 3 else 4.0) * g["dx"]
+        rc = R.reinit_defaults(g["dx"], gam)
+        out, iters, had = R.reinitialize(g, phi, band_phi, gam, rc)
+        np.savez_compressed(os.path.join(OUT, f"reinit_{name}.npz"), dims=np.array(g["dims"]),
+                            origin=np.array(g["origin"]), dx=g["dx"], dim=g["dim"], phi=phi, band_phi=band_phi,
+                            gamma=gam, out=out, iterations=iters, had_interface=int(had), **{f"rc_{k}": v for k, v in rc.items()})
+        print("reinit", name, iters, had)
+
+    # whole loop iterations: driver.cpp:185-203 on a fixed grid (band, E_2,
+    # sl_step, reinitialize, swap), K steps; per-step E_2 recorded so the GPU
+    # loop can be fed the reference's energies (glibc pow)
+    for name, g, pts, interp, p, delta, r0, steps in (
+        ("circle2d_q1", grid(65, 2), cloud_circle(200, 0.3, rng), 0, 1, 0.0, 0.9, 6),
+        ("sphere3d_weno_p2", grid(30, 3), cloud_sphere(4000, 0.5, rng), 1, 2, 1.0, 0.85, 4),
+        ("torus3d_weno_p1", grid(28, 3), cloud_torus(4000, 0.5, 0.2, 0.01, rng), 1, 1, 0.0, 0.8, 4),
+    ):
+        x, y, z = mesh(g)
+        phi = np.sqrt(x * x + y * y + z * z) - r0
+        d, _, _, _ = R.build_distance(g, pts, g["dim"])
+        gam = (6.0 if g["dim"] == 3 else 4.0) * g["dx"]
+        cfg = dict(p=p, interp=interp, delta=delta, dt=0.25 * g["dx"], fallback_c=1e-3, fallback_alpha=1.0,
+                   gamma=gam, beta=gam / 2)
+        phis, e2s, nas, its = [phi], [], [], []
+        cur = phi
+        for _ in range(steps):
+            cur, e2, na, it, _ = R.loop_step(g, cur, d, cfg)
+            phis.append(cur)
+            e2s.append(e2)
+            nas.append(na)
+            its.append(it)
+        np.savez_compressed(os.path.join(OUT, f"loop_{name}.npz"), dims=np.array(g["dims"]),
+                            origin=np.array(g["origin"]), dx=g["dx"], dim=g["dim"], phi0=phi, d=d, phis=np.stack(phis),
+                            e2=np.array(e2s), n_active=np.array(nas), reinit_iters=np.array(its), p=p, interp=interp,
+                            delta=delta, gamma=gam)
+        print("loop", name, e2s, nas, its)
     print("golden fixtures written to", OUT)
 
 
