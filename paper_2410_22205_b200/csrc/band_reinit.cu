@@ -36,6 +36,12 @@ namespace {
 __device__ __forceinline__ double smax(double a, double b) { return (a < b) ? b : a; }
 __device__ __forceinline__ double smin(double a, double b) { return (b < a) ? b : a; }
 
+struct IterState {  // device-side control of the Jacobi sweeps
+    unsigned long long residual_bits;
+    int done;
+    int iterations;
+};
+
 // narrow_band state (grid.cpp:85-116): 1 ACTIVE, 2 REINIT_HALO, 0 INACTIVE
 __global__ void band_state(SlParams P, const double* __restrict__ phi, double gamma, long long n,
                            unsigned char* __restrict__ state) {
@@ -45,9 +51,8 @@ __global__ void band_state(SlParams P, const double* __restrict__ phi, double ga
         state[id] = 1;
         return;
     }
-    const int i = static_cast<int>(id % P.nx);
-    const int j = static_cast<int>((id / P.nx) % P.ny);
-    const int k = static_cast<int>(id / P.nxy);
+    int i, j, k;
+    lsr_dev::unflatten(P, id, i, j, k);
     const int kz = P.dim == 3 ? 1 : 0;
     bool near = false;
     for (int dk = -kz; dk <= kz && !near; ++dk)
@@ -93,9 +98,8 @@ __global__ void one_step(SlParams P, const double* __restrict__ prev, double* __
         *any_zero = 1;
         return;
     }
-    const int i = static_cast<int>(id % P.nx);
-    const int j = static_cast<int>((id / P.nx) % P.ny);
-    const int k = static_cast<int>(id / P.nxy);
+    int i, j, k;
+    lsr_dev::unflatten(P, id, i, j, k);
     const int ijk[3] = {i, j, k};
     const int nn[3] = {P.nx, P.ny, P.nz};
     const long long st[3] = {1, P.nx, P.nxy};
@@ -149,23 +153,42 @@ __device__ __forceinline__ double godunov_norm(const SlParams& P, const double* 
     return sqrt(acc);
 }
 
-// one Jacobi iteration (reinit.cpp:111-124)
+// one Jacobi iteration (reinit.cpp:111-124). The running max of |upd| is
+// kept as the bits of a non-negative double (integer order = double order);
+// std::max(residual, x) never lets a NaN in, nor does `a > 0`. The max is
+// reduced within each warp before one atomic per warp.
 __global__ void jacobi(SlParams P, const double* __restrict__ cur, double* __restrict__ nxt,
                        const long long* __restrict__ nodes, const double* __restrict__ sgn, long long nn, double dtau,
-                       unsigned long long* __restrict__ residual) {
+                       IterState* __restrict__ st) {
+    if (*reinterpret_cast<volatile int*>(&st->done)) return;
     const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (t >= nn) return;
-    const long long id = nodes[t];
-    const int i = static_cast<int>(id % P.nx);
-    const int j = static_cast<int>((id / P.nx) % P.ny);
-    const int k = static_cast<int>(id / P.nxy);
-    const double s = sgn[t];
-    const double gn = godunov_norm(P, cur, id, i, j, k, s);
-    const double upd = -dtau * s * (gn - 1.0);
-    nxt[id] = __ldg(cur + id) + upd;
-    const double a = fabs(upd);
-    // std::max(residual, |upd|): a NaN update never raises the running max
-    if (a > 0.0) atomicMax(residual, static_cast<unsigned long long>(__double_as_longlong(a)));
+    unsigned long long bitsmax = 0;
+    if (t < nn) {
+        const long long id = nodes[t];
+        int i, j, k;
+        lsr_dev::unflatten(P, id, i, j, k);
+        const double s = sgn[t];
+        const double gn = godunov_norm(P, cur, id, i, j, k, s);
+        const double upd = -dtau * s * (gn - 1.0);
+        nxt[id] = __ldg(cur + id) + upd;
+        const double a = fabs(upd);
+        if (a > 0.0) bitsmax = static_cast<unsigned long long>(__double_as_longlong(a));
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        const unsigned long long o = __shfl_xor_sync(0xffffffffu, bitsmax, off);
+        bitsmax = o > bitsmax ? o : bitsmax;
+    }
+    if ((threadIdx.x & 31) == 0 && bitsmax) atomicMax(&st->residual_bits, bitsmax);
+}
+
+// the stop rule after a sweep (reinit.cpp:275-278)
+__global__ void iter_check(IterState* st, double tol) {
+    if (st->done) return;
+    st->iterations += 1;
+    const double residual = __longlong_as_double(static_cast<long long>(st->residual_bits));
+    st->residual_bits = 0;
+    if (residual < tol) st->done = 1;
 }
 
 __global__ void copy_ids(const double* __restrict__ src, double* __restrict__ dst, const long long* __restrict__ ids,
@@ -342,26 +365,30 @@ int lsr_reinitialize(const SlParams& P, double** phi, double** scratch, const Ba
     // `next = phi` (reinit.cpp:259): the scratch buffer holds the pre-one-step
     // field, which differs from phi on the frozen nodes -> one full copy
     BR_TRY(cudaMemcpyAsync(*scratch, *phi, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+    // All max_iters sweeps are queued without host round trips: sweep k reads
+    // buf[k&1] and writes buf[(k+1)&1]; a one-thread check after each sweep
+    // applies the reference's stop rule (reinit.cpp:275-278) and raises a
+    // device flag that turns the remaining sweeps into no-ops. The number of
+    // sweeps done tells which buffer holds the result.
     const double tol = R.residual_tol * P.dx;
-    int iter = 0;
-    unsigned long long* d_res = W.scal + 3;
-    for (; iter < R.max_iters; ++iter) {
-        BR_TRY(cudaMemsetAsync(d_res, 0, sizeof(unsigned long long), s));
+    IterState* st = reinterpret_cast<IterState*>(W.scal);  // reuses the flag words
+    BR_TRY(cudaMemsetAsync(st, 0, sizeof(IterState), s));
+    double* buf[2] = {*phi, *scratch};
+    for (int k = 0; k < R.max_iters; ++k) {
         if (nn > 0) {
-            jacobi<<<gb, 256, 0, s>>>(P, *phi, *scratch, W.nodes, W.sgn, nn, R.dtau, d_res);
+            jacobi<<<gb, 256, 0, s>>>(P, buf[k & 1], buf[(k + 1) & 1], W.nodes, W.sgn, nn, R.dtau, st);
             lsr_note_launch();
         }
-        unsigned long long hr = 0;
-        BR_TRY(cudaMemcpyAsync(&hr, d_res, sizeof hr, cudaMemcpyDeviceToHost, s));
-        BR_TRY(cudaStreamSynchronize(s));
-        std::swap(*phi, *scratch);  // std::swap(phi.values, next.values) (reinit.cpp:274)
-        double residual;
-        std::memcpy(&residual, &hr, sizeof residual);
-        if (residual < tol) {
-            ++iter;
-            break;
-        }
+        iter_check<<<1, 1, 0, s>>>(st, tol);
+        lsr_note_launch();
     }
+    BR_TRY(cudaGetLastError());
+    IterState h{};
+    BR_TRY(cudaMemcpyAsync(&h, st, sizeof h, cudaMemcpyDeviceToHost, s));
+    BR_TRY(cudaStreamSynchronize(s));
+    const int iter = static_cast<int>(h.iterations);
+    *phi = buf[iter & 1];
+    *scratch = buf[(iter + 1) & 1];
     // keep the two buffers equal on the node list for the caller's next use
     if (nn > 0) {
         copy_ids<<<gb, 256, 0, s>>>(*phi, *scratch, W.nodes, nn);

@@ -21,6 +21,7 @@
 #include <cub/cub.cuh>
 
 #include <cmath>
+#include <mutex>
 #include <cstdint>
 #include <string>
 #include <vector>
@@ -44,10 +45,11 @@ __global__ void flag_cells(SlParams P, const double* __restrict__ phi, long long
                            unsigned char* __restrict__ flags) {
     const long long c = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (c >= ncells) return;
-    const int cx = P.nx - 1, cy = P.ny - 1;
-    const int i = static_cast<int>(c % cx);
-    const int j = static_cast<int>((c / cx) % cy);
-    const int k = static_cast<int>(c / (static_cast<long long>(cx) * cy));
+    const unsigned cx = P.nx - 1, cy = P.ny - 1;  // cells < 2^31 (cub's int item count)
+    const unsigned row = static_cast<unsigned>(c) / cx;
+    const int i = static_cast<int>(static_cast<unsigned>(c) - row * cx);
+    const int k = static_cast<int>(row / cy);
+    const int j = static_cast<int>(row - static_cast<unsigned>(k) * cy);
     const long long b = (static_cast<long long>(k) * P.ny + j) * P.nx + i;
     bool pos = false, neg = false, zero = false;
     const int kz = P.dim == 3 ? 1 : 0;
@@ -69,10 +71,11 @@ __global__ void contrib_3d(SlParams P, const double* __restrict__ phi, const dou
     const long long c = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (c >= nc) return;
     const long long cid = cells[c];
-    const int cx = P.nx - 1, cy = P.ny - 1;
-    const int i = static_cast<int>(cid % cx);
-    const int j = static_cast<int>((cid / cx) % cy);
-    const int k = static_cast<int>(cid / (static_cast<long long>(cx) * cy));
+    const unsigned cx = P.nx - 1, cy = P.ny - 1;
+    const unsigned row = static_cast<unsigned>(cid) / cx;
+    const int i = static_cast<int>(static_cast<unsigned>(cid) - row * cx);
+    const int k = static_cast<int>(row / cy);
+    const int j = static_cast<int>(row - static_cast<unsigned>(k) * cy);
     const double bx = P.ox + i * P.dx, by = P.oy + j * P.dx, bz = P.oz + k * P.dx;  // Grid::node
     double acc = 0.0;
     for (int ck = 0; ck < r; ++ck)
@@ -190,66 +193,81 @@ int lsr_prep_surface_energy(const SlParams& P, const double* phi, const double* 
         return LSR_ERR_CONFIG;
     }
     const long long ncells = static_cast<long long>(P.nx - 1) * (P.ny - 1) * (P.dim == 3 ? (P.nz - 1) : 1);
-    unsigned char* flags = nullptr;
-    int* cells = nullptr;
-    int* d_nsel = nullptr;
-    double* contrib = nullptr;
-    double* partial = nullptr;
-    int* ood = nullptr;
-    void* tmp = nullptr;
-    size_t tmp_bytes = 0;
-    struct Guard {
-        std::vector<void*> p;
-        ~Guard() {
-            for (void* q : p) cudaFree(q);
-        }
-    } guard;
-    EN_TRY(cudaMalloc(&flags, ncells));
-    guard.p.push_back(flags);
-    EN_TRY(cudaMalloc(&cells, sizeof(int) * ncells));
-    guard.p.push_back(cells);
-    EN_TRY(cudaMalloc(&d_nsel, sizeof(int)));
-    guard.p.push_back(d_nsel);
-    EN_TRY(cudaMalloc(&ood, sizeof(int)));
-    guard.p.push_back(ood);
-    EN_TRY(cudaMemsetAsync(ood, 0, sizeof(int), s));
+    // process-wide workspace, grown on demand (no per-call cudaMalloc)
+    static std::mutex mu;
+    static struct Work {
+        unsigned char* flags = nullptr;
+        int* cells = nullptr;
+        int* scal = nullptr;  // [0] selected count, [1] out-of-domain flag
+        void* tmp = nullptr;
+        size_t tmp_bytes = 0;
+        long long cap = 0;
+        double* contrib = nullptr;
+        double* partial = nullptr;
+        long long ccap = 0;
+    } W;
+    std::lock_guard<std::mutex> lock(mu);
+    if (ncells > W.cap) {
+        cudaFree(W.flags);
+        cudaFree(W.cells);
+        W.flags = nullptr;
+        W.cells = nullptr;
+        W.cap = 0;
+        EN_TRY(cudaMalloc(&W.flags, ncells));
+        EN_TRY(cudaMalloc(&W.cells, sizeof(int) * ncells));
+        W.cap = ncells;
+    }
+    if (!W.scal) EN_TRY(cudaMalloc(&W.scal, sizeof(int) * 2));
+    EN_TRY(cudaMemsetAsync(W.scal, 0, sizeof(int) * 2, s));
     const int T = 256;
-    flag_cells<<<static_cast<unsigned>((ncells + T - 1) / T), T, 0, s>>>(P, phi, ncells, flags);
+    flag_cells<<<static_cast<unsigned>((ncells + T - 1) / T), T, 0, s>>>(P, phi, ncells, W.flags);
     lsr_note_launch();
     cub::CountingInputIterator<int> ids(0);
-    EN_TRY(cub::DeviceSelect::Flagged(nullptr, tmp_bytes, ids, flags, cells, d_nsel, static_cast<int>(ncells), s));
-    EN_TRY(cudaMalloc(&tmp, tmp_bytes));
-    guard.p.push_back(tmp);
-    EN_TRY(cub::DeviceSelect::Flagged(tmp, tmp_bytes, ids, flags, cells, d_nsel, static_cast<int>(ncells), s));
+    size_t tb = 0;
+    EN_TRY(cub::DeviceSelect::Flagged(nullptr, tb, ids, W.flags, W.cells, W.scal, static_cast<int>(ncells), s));
+    if (tb > W.tmp_bytes) {
+        cudaFree(W.tmp);
+        W.tmp = nullptr;
+        W.tmp_bytes = 0;
+        EN_TRY(cudaMalloc(&W.tmp, tb));
+        W.tmp_bytes = tb;
+    }
+    EN_TRY(cub::DeviceSelect::Flagged(W.tmp, tb, ids, W.flags, W.cells, W.scal, static_cast<int>(ncells), s));
     int nc = 0;
-    EN_TRY(cudaMemcpyAsync(&nc, d_nsel, sizeof(int), cudaMemcpyDeviceToHost, s));
+    EN_TRY(cudaMemcpyAsync(&nc, W.scal, sizeof(int), cudaMemcpyDeviceToHost, s));
     EN_TRY(cudaStreamSynchronize(s));
     *n_cells = nc;
     double total = 0.0;
     if (nc > 0) {
-        EN_TRY(cudaMalloc(&contrib, sizeof(double) * nc));
-        guard.p.push_back(contrib);
         const long long nblk = (nc + 4095) / 4096;
-        EN_TRY(cudaMalloc(&partial, sizeof(double) * nblk));
-        guard.p.push_back(partial);
+        if (nc > W.ccap) {
+            cudaFree(W.contrib);
+            cudaFree(W.partial);
+            W.contrib = nullptr;
+            W.partial = nullptr;
+            W.ccap = 0;
+            EN_TRY(cudaMalloc(&W.contrib, sizeof(double) * nc));
+            EN_TRY(cudaMalloc(&W.partial, sizeof(double) * ((nc + 4095) / 4096)));
+            W.ccap = nc;
+        }
         if (P.dim == 3) {
             const int r = refine;
             const double dxp = P.dx / r;
             const double select = std::sqrt(3.0) / 2.0 * dxp;  // metrics.cpp:157
-            contrib_3d<<<static_cast<unsigned>((nc + 127) / 128), 128, 0, s>>>(P, phi, dist, cells, nc, r, dxp,
-                                                                                select, p, contrib);
+            contrib_3d<<<static_cast<unsigned>((nc + 127) / 128), 128, 0, s>>>(P, phi, dist, W.cells, nc, r, dxp,
+                                                                                select, p, W.contrib);
         } else {
-            contrib_2d<<<static_cast<unsigned>((nc + 127) / 128), 128, 0, s>>>(P, phi, dist, cells, nc, p, contrib,
-                                                                                ood);
+            contrib_2d<<<static_cast<unsigned>((nc + 127) / 128), 128, 0, s>>>(P, phi, dist, W.cells, nc, p,
+                                                                                W.contrib, W.scal + 1);
         }
         lsr_note_launch();
-        block_partials<<<static_cast<unsigned>((nblk + 127) / 128), 128, 0, s>>>(contrib, nc, partial);
+        block_partials<<<static_cast<unsigned>((nblk + 127) / 128), 128, 0, s>>>(W.contrib, nc, W.partial);
         lsr_note_launch();
         EN_TRY(cudaGetLastError());
         std::vector<double> h(nblk);
         int h_ood = 0;
-        EN_TRY(cudaMemcpyAsync(h.data(), partial, sizeof(double) * nblk, cudaMemcpyDeviceToHost, s));
-        EN_TRY(cudaMemcpyAsync(&h_ood, ood, sizeof(int), cudaMemcpyDeviceToHost, s));
+        EN_TRY(cudaMemcpyAsync(h.data(), W.partial, sizeof(double) * nblk, cudaMemcpyDeviceToHost, s));
+        EN_TRY(cudaMemcpyAsync(&h_ood, W.scal + 1, sizeof(int), cudaMemcpyDeviceToHost, s));
         EN_TRY(cudaStreamSynchronize(s));
         if (h_ood) {
             *err = "locate_cell: point outside grid hull";
