@@ -145,21 +145,6 @@ def make_inputs(lsr, cfg, seed=2410):
     return g, pts, phi, active, step
 
 
-def z_partition(active: np.ndarray, nxy: int, nz: int, world: int):
-    """Band-balanced z-slab cuts: rank r owns planes [cuts[r], cuts[r+1]),
-    chosen on the cumulative per-plane active count."""
-    k = active // nxy
-    per_plane = np.bincount(k, minlength=nz)
-    cum = np.cumsum(per_plane)
-    total = int(cum[-1]) if cum.size else 0
-    cuts = [0]
-    for r in range(1, world):
-        cuts.append(int(np.searchsorted(cum, total * r / world, side="left")) + 1)
-    cuts.append(nz)
-    cuts = np.maximum.accumulate(np.array(cuts))
-    return cuts
-
-
 # ---------------------------------------------------------------------------
 
 
@@ -189,30 +174,65 @@ def run_ours(args):
     e2 = ctx.surface_energy(lsr._api.FIELD_PHI, 2, 5)
     t_energy = time.perf_counter() - t0
 
-    # z-slab ownership
-    cuts = z_partition(active, nxy, g.dims[2], world)
-    k = active // nxy
-    mine = active[(k >= cuts[rank]) & (k < cuts[rank + 1])]
-    ctx.set_active(mine)
-    halo = 0
-    if world > 1:
-        halo = 8  # planes: max foot displacement (~2.5 dx here) + WENO radius 2 + gradient 1, rounded up
-        phi_t = lsr_tensor(ctx, lsr._api.FIELD_PHI, g)
-        out_t = lsr_tensor(ctx, lsr._api.FIELD_OUT, g)
-
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
-    n0 = None
+    halo = 0
+    if world == 1:
+        mine = active
+        ctx.set_active(mine)
 
-    def one_step(i):
-        ctx.sl_step(step, e2)
-        if world > 1:
-            exchange_halo(dist, ctx, lsr, g, cuts, rank, world, halo)
-        ctx.swap()
+        def one_step(i):
+            ctx.sl_step(step, e2)
+            ctx.swap()
+            return ctx.last_times()[0]
+    else:
+        # z-slabs (paper_2410_22205_b200/zslab.py): slab-sized resident buffers,
+        # the slab-mode kernel on owned ids, NCCL halo exchange, buffer swap
+        import ctypes as C
+
+        from paper_2410_22205_b200 import zslab
+
+        h_d = ctx.download(lsr._api.FIELD_DIST)
+        halo = zslab.halo_planes(max_displacement(g, h_d, active, step, e2), g.dx, cfg["interp"])
+        cuts = zslab.plan_cuts(active, nxy, g.dims[2], world, min_planes=halo)
+        s = zslab.make_slab(cuts, rank, halo, nxy, g.dims[2])
+        mine = zslab.owned_ids(active, s)
+        sl = slice(s.z_base * nxy, (s.z_base + s.z_planes) * nxy)
+        phi_t = torch.from_numpy(phi[sl].copy()).cuda()
+        out_t = phi_t.clone()
+        d_t = torch.from_numpy(h_d[sl].copy()).cuda()
+        ids_t = torch.from_numpy(mine).cuda()
+        del h_d
+        ctx.close()  # the whole-grid context was only needed for d and E_2
+        bad_t = torch.full((1,), np.iinfo(np.int64).max, dtype=torch.int64, device="cuda")
+        miss_t = torch.zeros(1, dtype=torch.int64, device="cuda")
+        L = lsr.lib()
+        cg, cc = g.c(), step.c()
+        kev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+
+        def compute(p, d, o, slab, ids):
+            kev[0].record(stream)
+            st = L.lsr_cuda_sl_step_device(C.byref(cg), slab.z_base, slab.z_planes, C.c_void_p(p.data_ptr()),
+                                           C.c_void_p(d.data_ptr()), C.c_void_p(ids_t.data_ptr()), ids_t.numel(),
+                                           C.byref(cc), e2, C.c_void_p(o.data_ptr()), C.c_void_p(bad_t.data_ptr()),
+                                           C.c_void_p(miss_t.data_ptr()), C.c_void_p(stream.cuda_stream))
+            kev[1].record(stream)
+            if st != 0:
+                raise RuntimeError(L.lsr_cuda_last_error_string().decode())
+            return 0
+
+        stepper = zslab.SlabStepper(dist, s, halo, phi_t, d_t, out_t, ids_t, compute)
+
+        def one_step(i):
+            stepper.step()
+            torch.cuda.current_stream().synchronize()
+            return kev[0].elapsed_time(kev[1])
 
     for i in range(args.warmup):
         one_step(i)
     if world > 1:
         dist.barrier()
+        if int(miss_t.item()) or int(bad_t.item()) != np.iinfo(np.int64).max:
+            raise RuntimeError(f"rank {rank}: halo of {halo} planes too thin or non-finite update")
     torch.cuda.synchronize()
     kernel_ms, step_ms = [], []
     n0 = lsr.kernel_launches()
@@ -221,9 +241,9 @@ def run_ours(args):
         for i in range(args.steps):
             flush.fill_(float(i))  # evict L2 between timed steps (outside the step's events)
             evs[i][0].record(stream)
-            one_step(i)  # resync + SL kernel (+ halo exchange when N > 1), all on `stream`
+            km = one_step(i)  # resync + SL kernel (+ halo exchange when N > 1), all on `stream`
             evs[i][1].record(stream)
-            kernel_ms.append(ctx.last_times()[0])
+            kernel_ms.append(km)
         torch.cuda.synchronize()
         step_ms = [a.elapsed_time(b) for a, b in evs]
     torch.cuda.synchronize()
@@ -246,6 +266,8 @@ def run_ours(args):
 
     e2e = None
     cpu = None
+    if world > 1 and (int(miss_t.item()) or int(bad_t.item()) != np.iinfo(np.int64).max):
+        raise RuntimeError(f"rank {rank}: halo of {halo} planes too thin or non-finite update")
     if rank == 0 and world == 1 and not args.no_e2e:
         e2e = measure_e2e(lsr, g, phi, ctx, active, step, e2, args)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -302,41 +324,22 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
-class _CAI:
-    def __init__(self, ptr, n):
-        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f8", "data": (ptr, False), "version": 3}
-
-
-def lsr_tensor(ctx, which, g):
-    import torch
-
-    return torch.as_tensor(_CAI(ctx.field_ptr(which), g.num_nodes()), device="cuda")
-
-
-def exchange_halo(dist, ctx, lsr, g, cuts, rank, world, halo):
-    """After a step, send the planes of phi^{n+1} that neighbours read as halo
-    ([cut - halo, cut) up, [cut, cut + halo) down) and receive theirs into the
-    OUT buffer (NCCL point-to-point, one group per step)."""
-    import torch
-
-    nxy = g.dims[0] * g.dims[1]
-    out = lsr_tensor(ctx, lsr._api.FIELD_OUT, g)
-    ops = []
-    lo, hi = int(cuts[rank]), int(cuts[rank + 1])
-    if rank > 0:
-        a = lo
-        b = min(hi, lo + halo)
-        ops.append(dist.P2POp(dist.isend, out[a * nxy:b * nxy], rank - 1))
-        c = max(0, lo - halo)
-        ops.append(dist.P2POp(dist.irecv, out[c * nxy:lo * nxy], rank - 1))
-    if rank < world - 1:
-        a = max(lo, hi - halo)
-        ops.append(dist.P2POp(dist.isend, out[a * nxy:hi * nxy], rank + 1))
-        ops.append(dist.P2POp(dist.irecv, out[hi * nxy:min(g.dims[2], hi + halo) * nxy], rank + 1))
-    if ops:
-        for r in dist.batch_isend_irecv(ops):
-            r.wait()
-    torch.cuda.current_stream().synchronize()
+def max_displacement(g, h_d, active, step, e2):
+    """Upper bound of |foot - node| over the band (evolve.cpp:83-101):
+    C dt |grad d| + spread * sqrt(2), C = d/E (p = 2) or 1."""
+    nx, ny, nz = g.dims
+    d3 = h_d.reshape(nz, ny, nx)
+    k = active // (nx * ny)
+    j = (active // nx) % ny
+    i = active % nx
+    gx = (d3[k, j, np.minimum(i + 1, nx - 1)] - d3[k, j, np.maximum(i - 1, 0)]) / g.dx
+    gy = (d3[k, np.minimum(j + 1, ny - 1), i] - d3[k, np.maximum(j - 1, 0), i]) / g.dx
+    gz = (d3[np.minimum(k + 1, nz - 1), j, i] - d3[np.maximum(k - 1, 0), j, i]) / g.dx
+    dj = h_d[active]
+    c = dj / e2 if step.p == 2 else np.ones_like(dj)
+    spread = np.sqrt(np.maximum(0.0, c * step.delta * dj * step.dt / step.p))
+    disp = c * step.dt * np.sqrt(gx * gx + gy * gy + gz * gz) + spread * np.sqrt(2.0)
+    return float(disp.max()) if disp.size else 0.0
 
 
 def measure_e2e(lsr, g, phi, ctx, active, step, e2, args):

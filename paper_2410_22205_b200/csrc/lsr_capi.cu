@@ -339,11 +339,18 @@ int lsr_cuda_sl_step_device(const lsr_grid* grid, int32_t z_base, int32_t z_plan
                             int64_t* d_halo_miss, void* stream) {
     if (int st = check_grid(grid)) return st;
     if (int st = check_cfg(cfg, energy_p)) return st;
-    if (z_base != 0 || z_planes != grid->dims[2])
-        return set_err(LSR_ERR_CONFIG, "sl_step_device: partial slabs not supported yet");
-    (void)d_halo_miss;
-    const SlParams P = make_params(*grid, *cfg, energy_p);
-    LSR_CUDA_TRY(launch_sl_step(P, cfg->interp, d_phi, d_dist, d_active, n_active, d_out,
+    const bool slab = z_base != 0 || z_planes != grid->dims[2];
+    if (slab && (grid->dim != 3 || z_base < 0 || z_planes < 1 || z_base + z_planes > grid->dims[2]))
+        return set_err(LSR_ERR_CONFIG, "sl_step_device: slabs are z-plane ranges of a 3d grid");
+    if (slab && !d_halo_miss) return set_err(LSR_ERR_CONFIG, "sl_step_device: slab mode needs a halo_miss counter");
+    SlParams P = make_params(*grid, *cfg, energy_p);
+    P.z_base = z_base;
+    P.z_planes = z_planes;
+    P.halo_miss = slab ? reinterpret_cast<unsigned long long*>(d_halo_miss) : nullptr;
+    // the resident planes start at global plane z_base: shift the bases so
+    // that global ids index them directly
+    const long long shift = static_cast<long long>(z_base) * grid->dims[0] * grid->dims[1];
+    LSR_CUDA_TRY(launch_sl_step(P, cfg->interp, d_phi - shift, d_dist - shift, d_active, n_active, d_out - shift,
                                 reinterpret_cast<unsigned long long*>(d_bad_node), static_cast<cudaStream_t>(stream)));
     return LSR_OK;
 }
