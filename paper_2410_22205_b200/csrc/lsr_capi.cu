@@ -93,6 +93,7 @@ SlParams make_params(const lsr_grid& g, const lsr_step_cfg& c, double energy_p) 
     P.rdx2 = 1.0 / P.dx2;
     P.r3 = 1.0 / 3.0;
     P.fast_div = (pow2_range(g.dx) && pow2_range(P.dx2)) ? 1 : 0;
+    P.fast_weno = (P.fast_div && g.dx >= std::ldexp(1.0, -30) && g.dx <= 1.0) ? 1 : 0;  // weno1_fast's range argument
     P.p = c.p;
     P.pd = static_cast<double>(c.p);
     P.dt = c.dt;

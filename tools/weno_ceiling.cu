@@ -103,6 +103,7 @@ int main() {
     P.rdx2 = 1.0 / P.dx2;
     P.r3 = 1.0 / 3.0;
     P.fast_div = 1;
+    P.fast_weno = 1;
     for (int b : {2, 4, 6, 8}) {
         run_tp<1>(P, out, bad, b);
         run_tp<2>(P, out, bad, b);
