@@ -266,6 +266,29 @@ def main():
                             e2=np.array(e2s), n_active=np.array(nas), reinit_iters=np.array(its), p=p, interp=interp,
                             delta=delta, gamma=gam)
         print("loop", name, e2s, nas, its)
+    # BASELINE config 1 end to end: 2d circle, 200 seeded points at r = 0.3,
+    # 257^2 grid, phi0 = |x| - 0.9, multilinear, 200 loop iterations of the
+    # reference driver body (Table 1 run 1: p = 1, delta = 0). Stores the
+    # field after 50, 100 and 200 steps.
+    g = grid(257, 2)
+    x, y, _ = mesh(g)
+    phi = np.sqrt(x * x + y * y) - 0.9
+    th = 2 * np.pi * np.random.default_rng(1).random(200)
+    pts = np.stack([0.3 * np.cos(th), 0.3 * np.sin(th), np.zeros(200)], 1)
+    d, _, _, _ = R.build_distance(g, pts, 2)
+    gam = 4.0 * g["dx"]
+    cfg = dict(p=1, interp=0, delta=0.0, dt=0.25 * g["dx"], fallback_c=1e-3, fallback_alpha=1.0, gamma=gam,
+               beta=gam / 2)
+    cur, keep, e2s = phi, {}, []
+    for k in range(1, 201):
+        cur, e2, na, it, _ = R.loop_step(g, cur, d, cfg)
+        e2s.append(e2)
+        if k in (50, 100, 200):
+            keep[f"phi{k}"] = cur
+    np.savez_compressed(os.path.join(OUT, "config1_circle_200.npz"), dims=np.array(g["dims"]),
+                        origin=np.array(g["origin"]), dx=g["dx"], dim=2, pts=pts, phi0=phi, d=d, gamma=gam,
+                        e2=np.array(e2s), **keep)
+    print("config1: E2 after 200 steps", e2s[-1])
     print("golden fixtures written to", OUT)
 
 

@@ -1,0 +1,74 @@
+"""BASELINE configs end to end on the GPU (driver loop body on the device:
+band, E_2, SL step, reinitialisation, swap) against the reference.
+
+* config 1 (2d circle, 257^2, multilinear, 200 steps): bit-identical to the
+  reference's 200-step run (golden fixture made by the reference itself);
+* configs 2 and 3 (128^3 sphere / Q1, 256^3 noisy torus / WENO, p = 2,
+  delta = 1) against the live reference loop (oracle/_ref), the GPU loop fed
+  the reference's per-step E_2 (glibc pow) so the fields stay
+  bit-identical; the GPU's own E_2 is checked to 16 ulp.
+"""
+import numpy as np
+import pytest
+
+from conftest import bits, golden_grid, load_golden
+
+pytestmark = pytest.mark.gpu
+ULP16 = 16 * np.finfo(np.float64).eps
+
+
+def test_config1_circle_200_steps_bit_exact(gpu):
+    lsr = gpu
+    rec = load_golden("config1_circle_200.npz")
+    gg = golden_grid(rec)
+    g = lsr.Grid(2, tuple(gg["origin"]), gg["dx"], tuple(gg["dims"]))
+    gam = float(rec["gamma"])
+    d = lsr.build_distance_field(g, rec["pts"], 2)
+    assert np.array_equal(bits(d.field.values), bits(rec["d"]))
+    cfg = lsr.StepConfig(p=1, delta=0.0, dt=0.25 * g.dx, interp=lsr.InterpolatorKind.Q1,
+                         band=lsr.BandParams(gam, gam / 2))
+    rc = lsr.ReinitConfig.defaults(g.dx, gam)
+    ctx = lsr.Context(g)
+    ctx.upload(0, rec["phi0"])
+    ctx.upload(1, rec["d"])
+    for k in range(1, 201):
+        s = ctx.loop_step(cfg, rc, 5)
+        assert abs(s["energy"] - rec["e2"][k - 1]) <= ULP16 * rec["e2"][k - 1]
+        if k in (50, 100, 200):
+            got = ctx.download(0)
+            assert np.array_equal(bits(got), bits(rec[f"phi{k}"])), f"step {k}"
+
+
+@pytest.mark.parametrize("config,n,steps", [(2, 128, 8), (3, 256, 3)])
+def test_configs_2_3_vs_live_reference(gpu, reference, config, n, steps):
+    lsr = gpu
+    g = lsr.cube_grid(n, 3)
+    npts = {2: 20_000, 3: 100_000}[config]
+    sigma = {2: 0.0, 3: 0.5 * g.dx}[config]
+    interp = {2: lsr.InterpolatorKind.Q1, 3: lsr.InterpolatorKind.Weno}[config]
+    pts = lsr.cloud_generate(config, npts, seed=2410, sigma=sigma)
+    ax = g.axes()
+    phi = (np.sqrt(ax[0][None, None, :] ** 2 + ax[1][None, :, None] ** 2 + ax[2][:, None, None] ** 2) - 0.9).ravel()
+    gd = dict(dim=3, dims=g.dims, origin=g.origin, dx=g.dx)
+    bp = lsr.default_band_params(3, g.dx)
+    cfg = lsr.StepConfig(p=2, delta=1.0, dt=0.25 * g.dx, interp=interp, band=bp)
+    ccfg = dict(p=2, interp=int(interp), delta=1.0, dt=cfg.dt, fallback_c=1e-3, fallback_alpha=1.0, gamma=bp.gamma,
+                beta=bp.beta)
+    ctx = lsr.Context(g)
+    ctx.build_distance(pts)
+    d = ctx.download(1)
+    dref, _, _, _ = reference.build_distance(gd, pts, 3)
+    assert np.array_equal(bits(d), bits(dref))
+    ctx.upload(0, phi)
+    rc = lsr.ReinitConfig.defaults(g.dx, bp.gamma)
+    cur = phi
+    for k in range(steps):
+        cur, e2, na, it, _ = reference.loop_step(gd, cur, dref, ccfg)
+        s = ctx.loop_step(cfg, rc, 5, energy_override=e2)
+        assert s["n_active"] == na and s["reinit_iterations"] == it
+        got = ctx.download(0)
+        diff = np.count_nonzero(bits(got) != bits(cur))
+        assert diff == 0, f"config {config} step {k}: {diff} nodes differ"
+    own = lsr.surface_energy(lsr.ScalarField(g, cur), lsr.DistanceField(lsr.ScalarField(g, dref)), 2, 5)
+    ref_e = reference.surface_energy(gd, cur, dref, 2, 5)
+    assert abs(own - ref_e) <= ULP16 * ref_e
