@@ -93,7 +93,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "20"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
         except Exception:
@@ -272,6 +272,9 @@ def run_ours(args):
         e2e = measure_e2e(lsr, g, phi, ctx, active, step, e2, args)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(g, phi, ctx, active, step, e2, lsr)
+    loop = None
+    if rank == 0 and world == 1 and not args.no_loop:
+        loop = measure_loop(lsr, g, phi, ctx, step, cpu_too=not args.no_cpu_baseline)
 
     if rank == 0:
         line = {
@@ -319,6 +322,8 @@ def run_ours(args):
             line["e2e"] = e2e
         if cpu:
             line["cpu_baseline"] = cpu
+        if loop:
+            line["loop"] = loop
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
@@ -370,6 +375,34 @@ def measure_e2e(lsr, g, phi, ctx, active, step, e2, args):
     return {"value": active.size / t, "unit": UNIT, "h2d_bytes_per_step": int(2 * n * 8 + active.size * 8),
             "d2h_bytes_per_step": int(n * 8), "ms_per_step": t * 1e3, "timing": "host clock around the synchronous call",
             "steps": args.e2e_steps}
+
+
+def measure_loop(lsr, g, phi, ctx, step, steps=4, cpu_too=True):
+    """The whole driver iteration (driver.cpp:187-203: band, E_2, SL,
+    reinit, swap) from phi^0 on the device, per-phase device ms, next to one
+    iteration of the reference's own loop body on the host cores."""
+    ctx.upload(lsr._api.FIELD_PHI, phi)
+    rc = lsr.ReinitConfig.defaults(g.dx, step.band.gamma)
+    stats = [ctx.loop_step(step, rc, 5) for _ in range(steps)]
+    ms = np.array([s["ms"] for s in stats[1:]])  # first iteration includes workspace allocation
+    out = {"gpu_ms_per_step": dict(zip(("band", "energy", "sl", "reinit"), map(float, ms.mean(0)))),
+           "gpu_total_ms_per_step": float(ms.sum(1).mean()), "steps": steps,
+           "reinit_iterations": [s["reinit_iterations"] for s in stats]}
+    if cpu_too:
+        from oracle import bindings
+
+        if bindings.reference_available():
+            R = bindings.Reference()
+            R.set_threads(os.cpu_count() or 1)
+            d = ctx.download(lsr._api.FIELD_DIST)
+            cc = dict(p=step.p, interp=int(step.interp), delta=step.delta, dt=step.dt, fallback_c=step.fallback_c,
+                      fallback_alpha=step.fallback_alpha, gamma=step.band.gamma, beta=step.band.beta)
+            _, _, _, _, sec = R.loop_step(dict(dim=g.dim, dims=g.dims, origin=g.origin, dx=g.dx), phi, d, cc)
+            out["cpu_reference_ms_per_step"] = dict(zip(("band", "energy", "sl", "reinit"), map(lambda v: 1e3 * v, sec)))
+            out["cpu_reference_total_ms_per_step"] = float(1e3 * sum(sec))
+            out["cpu_cores"] = os.cpu_count()
+            out["loop_speedup_vs_cpu_reference"] = out["cpu_reference_total_ms_per_step"] / out["gpu_total_ms_per_step"]
+    return out
 
 
 def cpu_baseline(g, phi, ctx, active, step, e2, lsr, reps=3):
@@ -477,6 +510,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-loop", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

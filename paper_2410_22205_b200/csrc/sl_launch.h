@@ -11,7 +11,7 @@
 #define LSR_SL_THREADS 128
 #endif
 #ifndef LSR_SL_MIN_BLOCKS
-#define LSR_SL_MIN_BLOCKS 8
+#define LSR_SL_MIN_BLOCKS 7
 #endif
 constexpr int kSlThreads = LSR_SL_THREADS;
 constexpr int kSlMinBlocks = LSR_SL_MIN_BLOCKS;  // resident CTAs per SM the register budget must allow
