@@ -36,33 +36,68 @@ namespace {
 __device__ __forceinline__ double smax(double a, double b) { return (a < b) ? b : a; }
 __device__ __forceinline__ double smin(double a, double b) { return (b < a) ? b : a; }
 
+// div_const's guard (sl_device.cuh) as a predicate: a == +0 or
+// 2^-900 <= |a| < 2^900
+__device__ __forceinline__ bool markstein_ok(double a) {
+    const long long bits = __double_as_longlong(a);
+    const unsigned e = static_cast<unsigned>(bits >> 32) & 0x7ff00000u;
+    return ((e - 0x07b00000u) <= (0x78300000u - 0x07b00000u)) | (bits == 0);
+}
+__device__ __forceinline__ double markstein(double a, double c, double rc) {
+    const double q = a * rc;
+    return __fma_rn(__fma_rn(-q, c, a), rc, q);
+}
+
 struct IterState {  // device-side control of the Jacobi sweeps
     unsigned long long residual_bits;
     int done;
     int iterations;
 };
 
-// narrow_band state (grid.cpp:85-116): 1 ACTIVE, 2 REINIT_HALO, 0 INACTIVE
-__global__ void band_state(SlParams P, const double* __restrict__ phi, double gamma, long long n,
-                           unsigned char* __restrict__ state) {
+// narrow_band state (grid.cpp:85-116): 1 ACTIVE, 2 REINIT_HALO, 0 INACTIVE.
+// The halo test "some node of the 3^dim box is ACTIVE" is a separable
+// max-dilation of the ACTIVE indicator: dilate along x (pass 1, which also
+// evaluates |phi| < gamma), then y (pass 2), then z (pass 3). Per node:
+// bit 0 = dilated indicator, bit 1 = the node itself is ACTIVE.
+__global__ void band_pass_x(SlParams P, const double* __restrict__ phi, double gamma, long long n,
+                            unsigned char* __restrict__ t) {
     const long long id = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (id >= n) return;
-    if (fabs(__ldg(phi + id)) < gamma) {
-        state[id] = 1;
-        return;
-    }
     int i, j, k;
     lsr_dev::unflatten(P, id, i, j, k);
-    const int kz = P.dim == 3 ? 1 : 0;
-    bool near = false;
-    for (int dk = -kz; dk <= kz && !near; ++dk)
-        for (int dj = -1; dj <= 1 && !near; ++dj)
-            for (int di = -1; di <= 1 && !near; ++di) {
-                const int ni = i + di, nj = j + dj, nk = k + dk;
-                if (ni < 0 || nj < 0 || nk < 0 || ni >= P.nx || nj >= P.ny || nk >= P.nz) continue;
-                near = fabs(__ldg(phi + (static_cast<long long>(nk) * P.ny + nj) * P.nx + ni)) < gamma;
-            }
-    state[id] = near ? 2 : 0;
+    const bool c = fabs(__ldg(phi + id)) < gamma;
+    bool d = c;
+    if (i > 0) d = d || fabs(__ldg(phi + id - 1)) < gamma;
+    if (i < P.nx - 1) d = d || fabs(__ldg(phi + id + 1)) < gamma;
+    t[id] = static_cast<unsigned char>((c ? 2 : 0) | (d ? 1 : 0));
+}
+
+__global__ void band_pass_y(SlParams P, const unsigned char* __restrict__ t, long long n,
+                            unsigned char* __restrict__ u, unsigned char* __restrict__ state) {
+    const long long id = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (id >= n) return;
+    int i, j, k;
+    lsr_dev::unflatten(P, id, i, j, k);
+    const unsigned char c = t[id];
+    unsigned char d = c & 1;
+    if (j > 0) d |= t[id - P.nx] & 1;
+    if (j < P.ny - 1) d |= t[id + P.nx] & 1;
+    const unsigned char v = static_cast<unsigned char>((c & 2) | d);
+    if (P.dim == 2) state[id] = (v & 2) ? 1 : ((v & 1) ? 2 : 0);
+    else u[id] = v;
+}
+
+__global__ void band_pass_z(SlParams P, const unsigned char* __restrict__ u, long long n,
+                            unsigned char* __restrict__ state) {
+    const long long id = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (id >= n) return;
+    int i, j, k;
+    lsr_dev::unflatten(P, id, i, j, k);
+    const unsigned char c = u[id];
+    unsigned char d = c & 1;
+    if (k > 0) d |= u[id - P.nxy] & 1;
+    if (k < P.nz - 1) d |= u[id + P.nxy] & 1;
+    state[id] = (c & 2) ? 1 : (d ? 2 : 0);
 }
 
 struct IsActive {
@@ -73,11 +108,6 @@ struct InTube {
     const unsigned char* s;
     __device__ bool operator()(long long id) const { return s[id] != 0; }
 };
-struct InTubeNotFrozen {
-    const unsigned char* s;
-    const unsigned char* frozen;
-    __device__ bool operator()(long long id) const { return s[id] != 0 && !frozen[id]; }
-};
 
 __global__ void clamp_kernel(double* __restrict__ f, long long n, double gamma) {
     const long long id = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -85,41 +115,55 @@ __global__ void clamp_kernel(double* __restrict__ f, long long n, double gamma) 
     f[id] = smin(smax(f[id], -gamma), gamma);
 }
 
-// interface_one_step (reinit.cpp:24-46); `prev` is read-only, `out` gets every node
+// interface_one_step (reinit.cpp:24-46); `prev` is read-only, `out` gets every
+// node. The two "any" flags are raised once per warp (a single-address store
+// from every frozen node serialises in L2).
 __global__ void one_step(SlParams P, const double* __restrict__ prev, double* __restrict__ out,
                          unsigned char* __restrict__ frozen, long long n, int* __restrict__ any_frozen,
                          int* __restrict__ any_zero) {
     const long long id = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (id >= n) return;
-    const double pj = __ldg(prev + id);
-    frozen[id] = 0;
-    out[id] = pj;
-    if (pj == 0.0) {
-        *any_zero = 1;
-        return;
-    }
-    int i, j, k;
-    lsr_dev::unflatten(P, id, i, j, k);
-    const int ijk[3] = {i, j, k};
-    const int nn[3] = {P.nx, P.ny, P.nz};
-    const long long st[3] = {1, P.nx, P.nxy};
-    double best = -1.0;
-    for (int ax = 0; ax < P.dim; ++ax) {
-        for (int s = -1; s <= 1; s += 2) {
-            const int c = ijk[ax] + s;
-            if (c < 0 || c >= nn[ax]) continue;
-            const double pk = __ldg(prev + id + s * st[ax]);
-            if (pj * pk >= 0.0) continue;
-            const double crossing = P.dx * fabs(pj) / (fabs(pj) + fabs(pk));
-            best = best < 0.0 ? crossing : smin(best, crossing);
+    bool is_zero = false, is_frozen = false;
+    if (id < n) {
+        const double pj = __ldg(prev + id);
+        double val = pj;
+        if (pj == 0.0) {
+            is_zero = true;
+        } else {
+            int i, j, k;
+            lsr_dev::unflatten(P, id, i, j, k);
+            const int ijk[3] = {i, j, k};
+            const int nn[3] = {P.nx, P.ny, P.nz};
+            const long long st[3] = {1, P.nx, P.nxy};
+            double best = -1.0;
+            for (int ax = 0; ax < P.dim; ++ax) {
+                for (int s = -1; s <= 1; s += 2) {
+                    const int c = ijk[ax] + s;
+                    if (c < 0 || c >= nn[ax]) continue;
+                    const double pk = __ldg(prev + id + s * st[ax]);
+                    if (pj * pk >= 0.0) continue;
+                    const double crossing = P.dx * fabs(pj) / (fabs(pj) + fabs(pk));
+                    best = best < 0.0 ? crossing : smin(best, crossing);
+                }
+            }
+            if (best >= 0.0) {
+                val = pj > 0.0 ? best : -best;
+                is_frozen = true;
+            }
         }
+        out[id] = val;
+        frozen[id] = is_frozen ? 1 : 0;
     }
-    if (best >= 0.0) {
-        out[id] = pj > 0.0 ? best : -best;
-        frozen[id] = 1;
-        *any_frozen = 1;
+    const unsigned zb = __ballot_sync(0xffffffffu, is_zero), fb = __ballot_sync(0xffffffffu, is_frozen);
+    if ((threadIdx.x & 31) == 0) {
+        if (zb) *any_zero = 1;
+        if (fb) *any_frozen = 1;
     }
 }
+
+struct NotFrozen {  // tube ids that were not frozen by the one-step (reinit.cpp:94-98)
+    const unsigned char* frozen;
+    __device__ bool operator()(long long id) const { return !frozen[id]; }
+};
 
 // smoothed sign at entry (reinit.cpp:250-257)
 __global__ void sign_kernel(const double* __restrict__ phi, const long long* __restrict__ nodes, long long nn,
@@ -130,18 +174,33 @@ __global__ void sign_kernel(const double* __restrict__ phi, const long long* __r
     sgn[t] = v / sqrt(v * v + eps2);
 }
 
-// godunov_norm (reinit.cpp:63-84)
-__device__ __forceinline__ double godunov_norm(const SlParams& P, const double* __restrict__ phi, long long id, int i,
-                                               int j, int k, double sgn) {
-    const int ijk[3] = {i, j, k};
-    const int nn[3] = {P.nx, P.ny, P.nz};
-    const long long st[3] = {1, P.nx, P.nxy};
-    const double pc = __ldg(phi + id);
+// godunov_norm (reinit.cpp:63-84) on values already loaded: pc = phi at the
+// node, vm/vp = phi at its -1/+1 neighbours per axis (hm/hp: they exist). The
+// one-sided differences are divided by dx with div_const's Markstein form;
+// the six range guards are combined into one branch (they pass in practice),
+// the plain division is the fallback.
+__device__ __forceinline__ double godunov_vals(const SlParams& P, double pc, const double* vm, const double* vp,
+                                               const bool* hm, const bool* hp, double sgn) {
+    double dm[3], dp[3];
+    bool fast = P.fast_div != 0;
+#pragma unroll
+    for (int ax = 0; ax < 3; ++ax) {
+        dm[ax] = hm[ax] ? pc - vm[ax] : 0.0;
+        dp[ax] = hp[ax] ? vp[ax] - pc : 0.0;
+        fast = fast & markstein_ok(dm[ax]) & markstein_ok(dp[ax]);
+    }
     double acc = 0.0;
-    for (int ax = 0; ax < P.dim; ++ax) {
+#pragma unroll
+    for (int ax = 0; ax < 3; ++ax) {
+        if (ax >= P.dim) break;
         double dminus = 0.0, dplus = 0.0;
-        if (ijk[ax] > 0) dminus = lsr_dev::div_const(pc - __ldg(phi + id - st[ax]), P.dx, P.rdx, P.fast_div);
-        if (ijk[ax] < nn[ax] - 1) dplus = lsr_dev::div_const(__ldg(phi + id + st[ax]) - pc, P.dx, P.rdx, P.fast_div);
+        if (fast) {
+            if (hm[ax]) dminus = markstein(dm[ax], P.dx, P.rdx);
+            if (hp[ax]) dplus = markstein(dp[ax], P.dx, P.rdx);
+        } else {
+            if (hm[ax]) dminus = dm[ax] / P.dx;
+            if (hp[ax]) dplus = dp[ax] / P.dx;
+        }
         if (sgn > 0.0) {
             const double a = smax(dminus, 0.0), b = smin(dplus, 0.0);
             acc += smax(a * a, b * b);
@@ -153,26 +212,59 @@ __device__ __forceinline__ double godunov_norm(const SlParams& P, const double* 
     return sqrt(acc);
 }
 
-// one Jacobi iteration (reinit.cpp:111-124). The running max of |upd| is
-// kept as the bits of a non-negative double (integer order = double order);
-// std::max(residual, x) never lets a NaN in, nor does `a > 0`. The max is
+// one Jacobi iteration (reinit.cpp:111-124). Memory-latency bound (one id
+// load, then 7 dependent gathers per node), so each thread takes kJacNPT
+// nodes and issues all their loads before any arithmetic. The running max of
+// |upd| is kept as the bits of a non-negative double (integer order = double
+// order); std::max(residual, x) never lets a NaN in, nor does `a > 0`; it is
 // reduced within each warp before one atomic per warp.
-__global__ void jacobi(SlParams P, const double* __restrict__ cur, double* __restrict__ nxt,
-                       const long long* __restrict__ nodes, const double* __restrict__ sgn, long long nn, double dtau,
-                       IterState* __restrict__ st) {
+constexpr int kJacNPT = 4;
+constexpr int kJacThreads = 256;
+
+__global__ void __launch_bounds__(kJacThreads) jacobi(SlParams P, const double* __restrict__ cur,
+                                                      double* __restrict__ nxt, const long long* __restrict__ nodes,
+                                                      const double* __restrict__ sgn, long long nn, double dtau,
+                                                      IterState* __restrict__ st) {
     if (*reinterpret_cast<volatile int*>(&st->done)) return;
-    const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const long long base = static_cast<long long>(blockIdx.x) * (kJacThreads * kJacNPT) + threadIdx.x;
+    long long id[kJacNPT];
+    double sg[kJacNPT];
+#pragma unroll
+    for (int r = 0; r < kJacNPT; ++r) {
+        const long long t = base + r * kJacThreads;
+        id[r] = t < nn ? nodes[t] : -1;
+        sg[r] = t < nn ? sgn[t] : 0.0;
+    }
+    const long long stv[3] = {1, P.nx, P.nxy};
+    const int nnv[3] = {P.nx, P.ny, P.nz};
+    double pc[kJacNPT], vm[kJacNPT][3], vp[kJacNPT][3];
+    bool hm[kJacNPT][3], hp[kJacNPT][3];
+#pragma unroll
+    for (int r = 0; r < kJacNPT; ++r) {
+        int ijk[3] = {0, 0, 0};
+        if (id[r] >= 0) lsr_dev::unflatten(P, id[r], ijk[0], ijk[1], ijk[2]);
+        pc[r] = id[r] >= 0 ? __ldg(cur + id[r]) : 0.0;
+#pragma unroll
+        for (int ax = 0; ax < 3; ++ax) {
+            hm[r][ax] = id[r] >= 0 && ax < P.dim && ijk[ax] > 0;
+            hp[r][ax] = id[r] >= 0 && ax < P.dim && ijk[ax] < nnv[ax] - 1;
+            vm[r][ax] = hm[r][ax] ? __ldg(cur + id[r] - stv[ax]) : 0.0;
+            vp[r][ax] = hp[r][ax] ? __ldg(cur + id[r] + stv[ax]) : 0.0;
+        }
+    }
     unsigned long long bitsmax = 0;
-    if (t < nn) {
-        const long long id = nodes[t];
-        int i, j, k;
-        lsr_dev::unflatten(P, id, i, j, k);
-        const double s = sgn[t];
-        const double gn = godunov_norm(P, cur, id, i, j, k, s);
+#pragma unroll
+    for (int r = 0; r < kJacNPT; ++r) {
+        if (id[r] < 0) continue;
+        const double s = sg[r];
+        const double gn = godunov_vals(P, pc[r], vm[r], vp[r], hm[r], hp[r], s);
         const double upd = -dtau * s * (gn - 1.0);
-        nxt[id] = __ldg(cur + id) + upd;
+        nxt[id[r]] = pc[r] + upd;
         const double a = fabs(upd);
-        if (a > 0.0) bitsmax = static_cast<unsigned long long>(__double_as_longlong(a));
+        if (a > 0.0) {
+            const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(a));
+            bitsmax = b > bitsmax ? b : bitsmax;
+        }
     }
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) {
@@ -252,8 +344,17 @@ int lsr_band_build(const SlParams& P, const double* phi, double gamma, BandBuffe
     }
     const long long n = P.nxy * P.nz;
     if (int st = B.reserve(n, err)) return st;
-    band_state<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(P, phi, gamma, n, B.state);
+    const unsigned gb = static_cast<unsigned>((n + 255) / 256);
+    // scratch bytes for the two dilation passes live in the active/tube id
+    // buffers, which are only written by the compaction afterwards
+    unsigned char* t = reinterpret_cast<unsigned char*>(B.active);
+    unsigned char* u = reinterpret_cast<unsigned char*>(B.tube);
+    band_pass_x<<<gb, 256, 0, s>>>(P, phi, gamma, n, t);
+    band_pass_y<<<gb, 256, 0, s>>>(P, t, n, u, B.state);
+    if (P.dim == 3) band_pass_z<<<gb, 256, 0, s>>>(P, u, n, B.state);
     lsr_note_launch();
+    lsr_note_launch();
+    if (P.dim == 3) lsr_note_launch();
     cub::CountingInputIterator<long long> ids(0);
     size_t b1 = 0, b2 = 0;
     BR_TRY(cub::DeviceSelect::If(nullptr, b1, ids, B.active, B.counts, n, IsActive{B.state}, s));
@@ -343,17 +444,16 @@ int lsr_reinitialize(const SlParams& P, double** phi, double** scratch, const Ba
     std::swap(*phi, *scratch);  // *phi = one-step result
     *had_interface = 1;
     // nodes = tube minus frozen, ascending (reinit.cpp:94-98)
-    cub::CountingInputIterator<long long> ids(0);
     size_t tb = 0;
     long long* d_nn = reinterpret_cast<long long*>(W.scal + 2);
-    BR_TRY(cub::DeviceSelect::If(nullptr, tb, ids, W.nodes, d_nn, n, InTubeNotFrozen{B.state, W.frozen}, s));
+    BR_TRY(cub::DeviceSelect::If(nullptr, tb, B.tube, W.nodes, d_nn, B.n_tube, NotFrozen{W.frozen}, s));
     if (tb > W.tmp_bytes) {
         cudaFree(W.tmp);
         W.tmp = nullptr;
         BR_TRY(cudaMalloc(&W.tmp, tb));
         W.tmp_bytes = tb;
     }
-    BR_TRY(cub::DeviceSelect::If(W.tmp, tb, ids, W.nodes, d_nn, n, InTubeNotFrozen{B.state, W.frozen}, s));
+    BR_TRY(cub::DeviceSelect::If(W.tmp, tb, B.tube, W.nodes, d_nn, B.n_tube, NotFrozen{W.frozen}, s));
     long long nn = 0;
     BR_TRY(cudaMemcpyAsync(&nn, d_nn, sizeof nn, cudaMemcpyDeviceToHost, s));
     BR_TRY(cudaStreamSynchronize(s));
@@ -376,7 +476,8 @@ int lsr_reinitialize(const SlParams& P, double** phi, double** scratch, const Ba
     double* buf[2] = {*phi, *scratch};
     for (int k = 0; k < R.max_iters; ++k) {
         if (nn > 0) {
-            jacobi<<<gb, 256, 0, s>>>(P, buf[k & 1], buf[(k + 1) & 1], W.nodes, W.sgn, nn, R.dtau, st);
+            jacobi<<<static_cast<unsigned>((nn + kJacThreads * kJacNPT - 1) / (kJacThreads * kJacNPT)), kJacThreads, 0,
+                     s>>>(P, buf[k & 1], buf[(k + 1) & 1], W.nodes, W.sgn, nn, R.dtau, st);
             lsr_note_launch();
         }
         iter_check<<<1, 1, 0, s>>>(st, tol);
