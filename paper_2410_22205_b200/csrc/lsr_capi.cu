@@ -9,6 +9,8 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <vector>
+#include <algorithm>
 
 #include "lsr_cuda.h"
 #include "band_launch.h"
@@ -105,6 +107,8 @@ SlParams make_params(const lsr_grid& g, const lsr_step_cfg& c, double energy_p) 
     P.cut_den = (c.gamma - c.beta) * (c.gamma - c.beta) * (c.gamma - c.beta);  // grid.cpp:142
     P.z_base = 0;
     P.z_planes = g.dims[2];
+    P.own_lo = 0;
+    P.own_hi = g.dims[2];
     return P;
 }
 
@@ -146,6 +150,11 @@ struct lsr_cuda_ctx {
     BandBuffers band;        // last narrow_band built on the device
     ReinitBuffers rb;        // reinitialisation scratch
     double* scratch = nullptr;  // third full-grid field (reinit double buffer)
+    // pipelined host entry: compute / D2H streams, per-chunk events, miss counter
+    cudaStream_t s_cmp = nullptr, s_down = nullptr;
+    cudaEvent_t ev_up[32] = {}, ev_cmp[32] = {};
+    unsigned long long* d_miss = nullptr;
+    int64_t pipeline_fallbacks = 0;
 };
 
 namespace {
@@ -216,6 +225,13 @@ int lsr_cuda_destroy(lsr_cuda_ctx* c) {
     cudaFree(c->scratch);
     c->band.release();
     c->rb.release();
+    cudaFree(c->d_miss);
+    for (auto& e : c->ev_up)
+        if (e) cudaEventDestroy(e);
+    for (auto& e : c->ev_cmp)
+        if (e) cudaEventDestroy(e);
+    if (c->s_cmp) cudaStreamDestroy(c->s_cmp);
+    if (c->s_down) cudaStreamDestroy(c->s_down);
     cudaFree(c->active);
     cudaFree(c->dirty);
     cudaFree(c->d_bad);
@@ -356,6 +372,95 @@ int lsr_cuda_sl_step_device(const lsr_grid* grid, int32_t z_base, int32_t z_plan
     return LSR_OK;
 }
 
+// The one-shot host entry, pipelined over z-chunks for 3d grids: the H2D
+// of phi and d (plane order), the SL kernel of each chunk (as soon as its
+// planes plus a halo are resident) and the D2H of finished out planes run on
+// three streams, so the PCIe directions overlap each other and the compute.
+// Each chunk runs the kernel in slab mode: a stencil that reaches a plane not
+// yet uploaded, or an id outside the chunk's planes (unsorted input), is
+// counted; any count makes the whole step rerun unpipelined (exact either
+// way).
+static constexpr int kNotPipelined = -1000;
+
+static int sl_step_host_pipelined(lsr_cuda_ctx* c, const double* phi, const double* dist, const int64_t* active,
+                                  int64_t n_active, const lsr_step_cfg* cfg, double energy_p, double* out,
+                                  int64_t* bad_node) {
+    const lsr_grid& g = c->grid;
+    const int nz = g.dims[2];
+    const long long nxy = static_cast<long long>(g.dims[0]) * g.dims[1];
+    const int kChunks = 16;
+    const int zc = (nz + kChunks - 1) / kChunks;
+    const int nch = (nz + zc - 1) / zc;
+    const int halo = 8;  // lead of the upload over the compute (planes)
+    LSR_CUDA_TRY(cudaSetDevice(c->device));
+    if (!c->s_cmp) {
+        LSR_CUDA_TRY(cudaStreamCreateWithFlags(&c->s_cmp, cudaStreamNonBlocking));
+        LSR_CUDA_TRY(cudaStreamCreateWithFlags(&c->s_down, cudaStreamNonBlocking));
+        for (auto& e : c->ev_up) LSR_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        for (auto& e : c->ev_cmp) LSR_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        LSR_CUDA_TRY(cudaMalloc(&c->d_miss, sizeof(unsigned long long)));
+    }
+    if (nch > static_cast<int>(sizeof(c->ev_up) / sizeof(c->ev_up[0]))) return kNotPipelined;
+    cudaStream_t up = c->stream, cmp = c->s_cmp, down = c->s_down;
+    if (int st = ensure_ids(&c->active, &c->cap_active, n_active)) return st;
+    LSR_CUDA_TRY(cudaMemcpyAsync(c->active, active, sizeof(int64_t) * n_active, cudaMemcpyHostToDevice, up));
+    LSR_CUDA_TRY(cudaMemsetAsync(c->d_bad, 0xff, sizeof(unsigned long long), up));
+    LSR_CUDA_TRY(cudaMemsetAsync(c->d_miss, 0, sizeof(unsigned long long), up));
+    c->n_active = n_active;
+    // per-chunk ranges of the (ascending) ids
+    std::vector<int64_t> first(nch + 1);
+    for (int ch = 0; ch <= nch; ++ch) {
+        const int64_t bound = static_cast<int64_t>(std::min(nz, ch * zc)) * nxy;
+        first[ch] = std::lower_bound(active, active + n_active, bound) - active;
+    }
+    first[nch] = n_active;
+    SlParams P = make_params(g, *cfg, energy_p);
+    P.halo_miss = c->d_miss;
+    for (int ch = 0; ch < nch; ++ch) {  // uploads in plane order
+        const long long o = static_cast<long long>(ch) * zc * nxy;
+        const long long cnt = static_cast<long long>(std::min(nz, (ch + 1) * zc) - ch * zc) * nxy;
+        LSR_CUDA_TRY(cudaMemcpyAsync(c->phi + o, phi + o, sizeof(double) * cnt, cudaMemcpyHostToDevice, up));
+        LSR_CUDA_TRY(cudaMemcpyAsync(c->dist + o, dist + o, sizeof(double) * cnt, cudaMemcpyHostToDevice, up));
+        LSR_CUDA_TRY(cudaMemcpyAsync(c->out + o, c->phi + o, sizeof(double) * cnt, cudaMemcpyDeviceToDevice, up));
+        LSR_CUDA_TRY(cudaEventRecord(c->ev_up[ch], up));
+    }
+    for (int ch = 0; ch < nch; ++ch) {
+        const int z0 = ch * zc, z1 = std::min(nz, (ch + 1) * zc);
+        const int need = std::min(nz, z1 + halo);           // planes that must be resident
+        const int up_ch = std::min(nch - 1, (need - 1) / zc);  // last upload chunk needed
+        LSR_CUDA_TRY(cudaStreamWaitEvent(cmp, c->ev_up[up_ch], 0));
+        P.z_base = 0;
+        P.z_planes = std::min(nz, (up_ch + 1) * zc);
+        P.own_lo = z0;
+        P.own_hi = z1;
+        const long long n = first[ch + 1] - first[ch];
+        LSR_CUDA_TRY(launch_sl_step(P, cfg->interp, c->phi, c->dist, c->active + first[ch], n, c->out, c->d_bad, cmp));
+        LSR_CUDA_TRY(cudaEventRecord(c->ev_cmp[ch], cmp));
+        LSR_CUDA_TRY(cudaStreamWaitEvent(down, c->ev_cmp[ch], 0));
+        const long long o = static_cast<long long>(z0) * nxy, cnt = static_cast<long long>(z1 - z0) * nxy;
+        LSR_CUDA_TRY(cudaMemcpyAsync(out + o, c->out + o, sizeof(double) * cnt, cudaMemcpyDeviceToHost, down));
+    }
+    unsigned long long h[2] = {0, 0};
+    LSR_CUDA_TRY(cudaStreamSynchronize(down));
+    LSR_CUDA_TRY(cudaStreamSynchronize(cmp));
+    LSR_CUDA_TRY(cudaMemcpy(&h[0], c->d_miss, sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+    LSR_CUDA_TRY(cudaMemcpy(&h[1], c->d_bad, sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+    c->consistent = false;
+    if (h[0] != 0) {  // rerun unpipelined (everything is resident now)
+        P.halo_miss = nullptr;
+        P.z_base = 0;
+        P.z_planes = nz;
+        LSR_CUDA_TRY(cudaMemsetAsync(c->d_bad, 0xff, sizeof(unsigned long long), up));
+        LSR_CUDA_TRY(launch_sl_step(P, cfg->interp, c->phi, c->dist, c->active, n_active, c->out, c->d_bad, up));
+        LSR_CUDA_TRY(cudaMemcpyAsync(out, c->out, sizeof(double) * c->n, cudaMemcpyDeviceToHost, up));
+        LSR_CUDA_TRY(cudaMemcpyAsync(&h[1], c->d_bad, sizeof(unsigned long long), cudaMemcpyDeviceToHost, up));
+        LSR_CUDA_TRY(cudaStreamSynchronize(up));
+        c->pipeline_fallbacks++;
+    }
+    if (h[1] != ~0ULL) return numerical_error(g, h[1], bad_node);
+    return LSR_OK;
+}
+
 // One-shot host entry. A per-thread context is cached across calls with the
 // same grid, so repeated calls do not re-allocate device memory.
 int lsr_cuda_sl_step_host(const lsr_grid* grid, const double* phi, const double* dist, const int64_t* active,
@@ -380,6 +485,10 @@ int lsr_cuda_sl_step_host(const lsr_grid* grid, const double* phi, const double*
     if (!cache.ctx)
         if (int st = lsr_cuda_create(dev, grid, &cache.ctx)) return st;
     lsr_cuda_ctx* c = cache.ctx;
+    if (grid->dim == 3 && grid->dims[2] >= 64 && n_active > 0) {
+        const int st = sl_step_host_pipelined(c, phi, dist, active, n_active, cfg, energy_p, out, bad_node);
+        if (st != kNotPipelined) return st;
+    }
     const size_t bytes = sizeof(double) * c->n;
     cudaStream_t s = c->stream;
     LSR_CUDA_TRY(cudaMemcpyAsync(c->phi, phi, bytes, cudaMemcpyHostToDevice, s));

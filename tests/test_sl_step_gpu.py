@@ -219,3 +219,32 @@ def test_full_size_sampled_subset_512(gpu, oracle):
     assert np.all(np.isfinite(out[band]))
     assert np.array_equal(bits(np.delete(out, band)), bits(np.delete(phi, band)))
     assert np.max(np.abs(out[band] - phi[band])) < 2 * g.dx
+
+
+@pytest.mark.parametrize("case", ["sorted", "unsorted", "far_feet"])
+def test_pipelined_host_entry_exact(gpu, oracle, case):
+    """The one-shot host entry pipelines 3d grids over z-chunks (slab-mode
+    kernels, three streams); unsorted ids or feet beyond the upload lead must
+    fall back to the unpipelined step and stay exact."""
+    lsr = gpu
+    rng = np.random.default_rng(5)
+    g = lsr._api.cube_grid(96, 3)
+    x, y, z = (a.ravel() for a in g.mesh())
+    phi = np.sqrt(x * x + y * y + z * z) - 0.6 + 0.2 * g.dx * rng.standard_normal(x.size)
+    dist = np.abs(np.sqrt(x * x + y * y + z * z) - 0.3) + 0.01 * rng.random(x.size)
+    bp = lsr.default_band_params(3, g.dx)
+    active = np.flatnonzero(np.abs(phi) < bp.gamma).astype(np.int64)
+    e = 0.7
+    dt = 0.25 * g.dx
+    if case == "unsorted":
+        active = active.copy()
+        rng.shuffle(active)
+    if case == "far_feet":
+        dt = 6.0 * g.dx  # displacements of several planes: beyond the pipeline's upload lead
+    cfg = lsr.StepConfig(p=2, delta=1.0, dt=dt, band=bp)
+    got = _run(lsr, g, phi, dist, active, cfg, e)
+    ref, st, _ = oracle.sl_step(dict(dim=3, dims=g.dims, origin=g.origin, dx=g.dx), phi, dist, active,
+                                dict(p=2, interp=1, delta=1.0, dt=dt, fallback_c=1e-3, fallback_alpha=1.0,
+                                     gamma=bp.gamma, beta=bp.beta), e)
+    assert st == 0
+    assert np.count_nonzero(bits(got) != bits(ref)) == 0
