@@ -19,6 +19,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--interp", type=int, default=1)
     ap.add_argument("--radius", type=float, default=0.9)
+    ap.add_argument("--delta", type=float, default=1.0)
     a = ap.parse_args()
     g = lsr._api.cube_grid(a.n, 3)
     ax = g.axes()
@@ -27,7 +28,7 @@ def main():
     dist = np.abs(r - 0.5) + 1e-3 * np.cos(40 * r)
     bp = lsr.default_band_params(3, g.dx)
     band = np.flatnonzero(np.abs(phi) < bp.gamma).astype(np.int64)
-    cfg = lsr.StepConfig(p=2, delta=1.0, dt=0.25 * g.dx, band=bp, interp=lsr.InterpolatorKind(a.interp))
+    cfg = lsr.StepConfig(p=2, delta=a.delta, dt=0.25 * g.dx, band=bp, interp=lsr.InterpolatorKind(a.interp))
     ctx = lsr.Context(g)
     ctx.upload(0, phi)
     ctx.upload(1, dist)
