@@ -112,9 +112,9 @@ int lsr_cuda_last_times(lsr_cuda_ctx* ctx, float* kernel_ms, float* step_ms);
 
 /* ---- raw device entry (slab / multi-GPU plumbing) ----
  * Fields hold global planes [z_base, z_base + z_planes) of `grid` (3d) — a
- * z-slab plus halo; ids stay global. Feet whose stencil leaves the resident
- * planes are reported through *halo_miss (count) and computed as NaN-free
- * garbage-free: the caller must widen the halo and redo.
+ * z-slab plus halo; ids stay global. A node whose gradient or foot stencil
+ * leaves the resident planes is counted in *halo_miss and its output is not
+ * meaningful: the caller must widen the halo and redo.
  * Asynchronous on `stream`; bad_node/halo_miss are device int64 pointers
  * (bad_node initialised to INT64_MAX by the caller). */
 int lsr_cuda_sl_step_device(const lsr_grid* grid, int32_t z_base, int32_t z_planes,
@@ -135,6 +135,14 @@ int lsr_cuda_build_distance(const lsr_grid* grid, const double* pts, int64_t n, 
 /* same, writing the context's resident DIST field */
 int lsr_cuda_ctx_build_distance(lsr_cuda_ctx* ctx, const double* pts, int64_t n, int dim, int seed_only,
                                 double* sentinel, int* rounds);
+
+/* lsr::compute_stats (cloud.cpp:480-489; cloud.hpp:52-53): h_S =
+ * estimate_resolution (mean exact nearest-neighbour distance over a seeded
+ * Fisher-Yates sample of round(fraction*n) points, blocked_sum order),
+ * gamma_S = k_s * h_S and the bounding box (bbox6 = lo[3], hi[3]).
+ * Bit-identical to the reference. */
+int lsr_cuda_compute_stats(const double* pts, int64_t n, int dim, double sample_fraction, double k_s, uint64_t seed,
+                           double* h_s, double* gamma_s, double* bbox6);
 
 /* ---- surface energy ----
  * lsr::surface_energy (metrics.cpp:186-189; header metrics.hpp:41-42): E_p

@@ -29,6 +29,7 @@ from ._api import (  # noqa: F401
     ScalarField,
     StepConfig,
     build_distance_field,
+    compute_stats,
     cloud_generate,
     cube_grid,
     default_band_params,

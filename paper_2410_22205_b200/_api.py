@@ -131,6 +131,8 @@ def lib() -> C.CDLL:
     L.lsr_cuda_reinit_defaults.argtypes = [C.c_double, C.c_double, P(CReinitCfg)]
     L.lsr_cuda_reinit_defaults.restype = None
     L.lsr_cuda_loop_step.argtypes = [C.c_void_p, P(CStepCfg), P(CReinitCfg), C.c_int, C.c_double, P(CLoopStats)]
+    L.lsr_cuda_compute_stats.argtypes = [_dp, C.c_int64, C.c_int, C.c_double, C.c_double, C.c_uint64, P(C.c_double),
+                                         P(C.c_double), _dp]
     _lib = L
     return L
 
@@ -179,6 +181,28 @@ def cloud_generate(config: int, n: int, seed: int = 0, sigma: float = 0.0) -> np
     if lib().lsr_cloud_generate(int(config), int(n), int(seed), float(sigma), pts.reshape(-1)) != 0:
         raise ConfigError(f"unknown cloud config {config}")
     return pts
+
+
+@dataclass
+class CloudStats:  # cloud.hpp:19-26
+    h_s: float
+    gamma_s: float
+    k_s: float
+    bbox_min: tuple
+    bbox_max: tuple
+    sample_seed: int
+
+
+def compute_stats(points: np.ndarray, dim: int, sample_fraction: float = 0.1, k_s: float = 2.0,
+                  seed: int = 0) -> CloudStats:
+    """lsr::compute_stats (cloud.hpp:52-53): h_S from the exact NN distances
+    of a seeded sample (computed on the GPU), gamma_S = k_s * h_S, bbox."""
+    pts = np.ascontiguousarray(points, dtype=np.float64).reshape(-1)
+    h, gm = C.c_double(), C.c_double()
+    bb = np.zeros(6)
+    _check(lib().lsr_cuda_compute_stats(pts, pts.size // 3, int(dim), float(sample_fraction), float(k_s), int(seed),
+                                        C.byref(h), C.byref(gm), bb))
+    return CloudStats(h.value, gm.value, float(k_s), tuple(bb[:3]), tuple(bb[3:]), int(seed))
 
 
 def build_distance_field(grid: "Grid", points: np.ndarray, dim: int | None = None,

@@ -26,6 +26,7 @@
 #include <cmath>
 #include <cstdint>
 #include <cstring>
+#include <random>
 #include <string>
 #include <vector>
 
@@ -74,7 +75,8 @@ __global__ void scatter_bins(const int* __restrict__ bin_id, long long n, int* _
 
 // SpatialHash::nearest_distance (cloud.cpp:420-452)
 __device__ double nearest_distance(const HashP& H, const double* __restrict__ pts, const int* __restrict__ starts,
-                                   const int* __restrict__ entries, double qx, double qy, double qz) {
+                                   const int* __restrict__ entries, double qx, double qy, double qz,
+                                   int exclude = -1) {
     const double q[3] = {qx, qy, qz};
     const double lo[3] = {H.lox, H.loy, H.loz};
     const int nb[3] = {H.bx, H.by, H.bz};
@@ -96,6 +98,7 @@ __device__ double nearest_distance(const HashP& H, const double* __restrict__ pt
                     if (max(abs(bx - bq[0]), cyz) != rad) continue;
                     const int b = (bz * nb[1] + by) * nb[0] + bx;
                     for (int e = starts[b]; e < starts[b + 1]; ++e) {
+                        if (entries[e] == exclude) continue;
                         const double* p = pts + 3 * static_cast<long long>(entries[e]);
                         const double dx = p[0] - q[0], dy = p[1] - q[1], dz = p[2] - q[2];
                         best2 = dmin(best2, dx * dx + dy * dy + dz * dz);  // dot(diff, diff)
@@ -221,6 +224,29 @@ __global__ void sweep_plane(GridP G, int ord, int s, int k_lo, int k_cnt, double
         const double change = v - cand;
         atomicMax(max_change, static_cast<unsigned long long>(__double_as_longlong(change)));
     }
+}
+
+// estimate_resolution's terms (cloud.cpp:473-476): the exact NN distance of
+// sampled point idx[i] to the rest of the cloud
+__global__ void sample_nn(HashP H, const double* __restrict__ pts, const int* __restrict__ starts,
+                          const int* __restrict__ entries, const int* __restrict__ idx, long long m,
+                          double* __restrict__ term) {
+    const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    const int id = idx[i];
+    const double* q = pts + 3 * static_cast<long long>(id);
+    term[i] = nearest_distance(H, pts, starts, entries, q[0], q[1], q[2], id);
+}
+
+// blocked_sum's in-block serial sums (parallel.hpp:31-37)
+__global__ void block_sums(const double* __restrict__ term, long long n, double* __restrict__ partial) {
+    const long long b = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const long long lo = b * 4096;
+    if (lo >= n) return;
+    const long long hi = min(n, lo + 4096);
+    double acc = 0.0;
+    for (long long i = lo; i < hi; ++i) acc += term[i];
+    partial[b] = acc;
 }
 
 }  // namespace
@@ -377,4 +403,160 @@ int lsr_prep_build_distance(const lsr_grid* g, const double* h_pts, int64_t n, i
     *rounds_out = round;
     return LSR_OK;
 #undef PREP_TRY
+}
+
+// SpatialHash geometry (cloud.cpp:390-399) from a host cloud, plus its CSR
+// bins built on the device (counting sort).
+struct DeviceHash {
+    HashP H{};
+    double* pts = nullptr;
+    int* starts = nullptr;
+    int* entries = nullptr;
+    ~DeviceHash() {
+        cudaFree(pts);
+        cudaFree(starts);
+        cudaFree(entries);
+    }
+};
+
+static int build_hash(const double* h_pts, int64_t n, int dim, DeviceHash& D, cudaStream_t s, std::string* err) {
+#define HB_TRY(x)                                                    \
+    do {                                                             \
+        cudaError_t e_ = (x);                                        \
+        if (e_ != cudaSuccess) {                                     \
+            *err = std::string(#x) + ": " + cudaGetErrorString(e_);  \
+            return LSR_ERR_CUDA;                                     \
+        }                                                            \
+    } while (0)
+    double lo[3] = {h_pts[0], h_pts[1], h_pts[2]}, hi[3] = {h_pts[0], h_pts[1], h_pts[2]};
+    for (int64_t q = 0; q < n; ++q)  // bounding_box (cloud.cpp:380-388)
+        for (int d = 0; d < 3; ++d) {
+            lo[d] = std::min(lo[d], h_pts[3 * q + d]);
+            hi[d] = std::max(hi[d], h_pts[3 * q + d]);
+        }
+    HashP& H = D.H;
+    H.dim = dim;
+    H.lox = lo[0];
+    H.loy = lo[1];
+    H.loz = lo[2];
+    const double span[3] = {hi[0] - lo[0], hi[1] - lo[1], hi[2] - lo[2]};
+    const double diag = std::sqrt(span[0] * span[0] + span[1] * span[1] + span[2] * span[2]);
+    const double n_axis = std::pow(static_cast<double>(n), 1.0 / dim);
+    H.cell = diag > 0.0 ? diag / std::max(1.0, n_axis) : 1.0;
+    int nb[3];
+    for (int d = 0; d < 3; ++d) nb[d] = d < dim ? 1 + static_cast<int>(span[d] / H.cell) : 1;
+    H.bx = nb[0];
+    H.by = nb[1];
+    H.bz = nb[2];
+    const long long nbins = static_cast<long long>(nb[0]) * nb[1] * nb[2];
+    int *counts = nullptr, *bin_id = nullptr;
+    void* tmp = nullptr;
+    size_t tb = 0;
+    struct G {
+        int** a;
+        int** b;
+        void** c;
+        ~G() {
+            cudaFree(*a);
+            cudaFree(*b);
+            cudaFree(*c);
+        }
+    } guard{&counts, &bin_id, &tmp};
+    HB_TRY(cudaMalloc(&D.pts, sizeof(double) * 3 * n));
+    HB_TRY(cudaMalloc(&D.starts, sizeof(int) * (nbins + 1)));
+    HB_TRY(cudaMalloc(&D.entries, sizeof(int) * n));
+    HB_TRY(cudaMalloc(&counts, sizeof(int) * (nbins + 1)));
+    HB_TRY(cudaMalloc(&bin_id, sizeof(int) * n));
+    HB_TRY(cudaMemcpyAsync(D.pts, h_pts, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, s));
+    HB_TRY(cudaMemsetAsync(counts, 0, sizeof(int) * (nbins + 1), s));
+    const unsigned pb = static_cast<unsigned>((n + 255) / 256);
+    count_bins<<<pb, 256, 0, s>>>(H, D.pts, n, counts, bin_id);
+    lsr_note_launch();
+    HB_TRY(cub::DeviceScan::ExclusiveSum(nullptr, tb, counts, D.starts, static_cast<int>(nbins + 1), s));
+    HB_TRY(cudaMalloc(&tmp, tb));
+    HB_TRY(cub::DeviceScan::ExclusiveSum(tmp, tb, counts, D.starts, static_cast<int>(nbins + 1), s));
+    HB_TRY(cudaMemcpyAsync(counts, D.starts, sizeof(int) * (nbins + 1), cudaMemcpyDeviceToDevice, s));
+    scatter_bins<<<pb, 256, 0, s>>>(bin_id, n, counts, D.entries);
+    lsr_note_launch();
+    HB_TRY(cudaStreamSynchronize(s));
+    return LSR_OK;
+#undef HB_TRY
+}
+
+// compute_stats (cloud.cpp:480-489) with estimate_resolution (:454-478):
+// the seeded Fisher-Yates prefix stays on the host (mt19937_64 and the
+// unbiased bounded draw, cloud.cpp:20-27); the sampled exact NN distances
+// run on the device; blocked_sum order is kept (serial 4096-term blocks,
+// block partials summed in order on the host).
+int lsr_prep_compute_stats(const double* h_pts, int64_t n, int dim, double fraction, double k_s, uint64_t seed,
+                           double* h_s, double* gamma_s, double* bbox6, cudaStream_t s, std::string* err) {
+    if (n < 2) {
+        *err = "estimate_resolution: need at least 2 points";
+        return LSR_ERR;
+    }
+    if (!(fraction > 0.0) || fraction > 1.0) {
+        *err = "estimate_resolution: sample_fraction must be in (0, 1]";
+        return LSR_ERR_CONFIG;
+    }
+    int64_t m = std::llround(fraction * static_cast<double>(n));
+    m = std::min<int64_t>(std::max<int64_t>(m, 1), n);
+    std::vector<int> idx(static_cast<size_t>(n));
+    for (int64_t i = 0; i < n; ++i) idx[i] = static_cast<int>(i);
+    std::mt19937_64 rng(seed);
+    for (int64_t i = 0; i < m; ++i) {
+        const uint64_t range = static_cast<uint64_t>(n - i);
+        const uint64_t limit = UINT64_MAX - UINT64_MAX % range;
+        uint64_t x = rng();
+        while (x >= limit) x = rng();
+        std::swap(idx[i], idx[i + static_cast<int64_t>(x % range)]);
+    }
+    DeviceHash D;
+    if (int st = build_hash(h_pts, n, dim, D, s, err)) return st;
+    int* d_idx = nullptr;
+    double* term = nullptr;
+    double* partial = nullptr;
+    const long long nblk = (m + 4095) / 4096;
+    struct G {
+        int** a;
+        double** b;
+        double** c;
+        ~G() {
+            cudaFree(*a);
+            cudaFree(*b);
+            cudaFree(*c);
+        }
+    } guard{&d_idx, &term, &partial};
+    auto cuda_fail = [&](cudaError_t e, const char* w) {
+        *err = std::string(w) + ": " + cudaGetErrorString(e);
+        return LSR_ERR_CUDA;
+    };
+    cudaError_t e;
+    if ((e = cudaMalloc(&d_idx, sizeof(int) * m)) != cudaSuccess) return cuda_fail(e, "cudaMalloc");
+    if ((e = cudaMalloc(&term, sizeof(double) * m)) != cudaSuccess) return cuda_fail(e, "cudaMalloc");
+    if ((e = cudaMalloc(&partial, sizeof(double) * nblk)) != cudaSuccess) return cuda_fail(e, "cudaMalloc");
+    if ((e = cudaMemcpyAsync(d_idx, idx.data(), sizeof(int) * m, cudaMemcpyHostToDevice, s)) != cudaSuccess)
+        return cuda_fail(e, "cudaMemcpyAsync");
+    sample_nn<<<static_cast<unsigned>((m + 127) / 128), 128, 0, s>>>(D.H, D.pts, D.starts, D.entries, d_idx, m, term);
+    lsr_note_launch();
+    block_sums<<<static_cast<unsigned>((nblk + 127) / 128), 128, 0, s>>>(term, m, partial);
+    lsr_note_launch();
+    std::vector<double> hp(static_cast<size_t>(nblk));
+    if ((e = cudaMemcpyAsync(hp.data(), partial, sizeof(double) * nblk, cudaMemcpyDeviceToHost, s)) != cudaSuccess)
+        return cuda_fail(e, "cudaMemcpyAsync");
+    if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return cuda_fail(e, "cudaStreamSynchronize");
+    double total = 0.0;
+    for (double v : hp) total += v;
+    *h_s = total / static_cast<double>(m);
+    *gamma_s = k_s * *h_s;
+    double lo[3] = {h_pts[0], h_pts[1], h_pts[2]}, hi[3] = {h_pts[0], h_pts[1], h_pts[2]};
+    for (int64_t q = 0; q < n; ++q)
+        for (int d = 0; d < 3; ++d) {
+            lo[d] = std::min(lo[d], h_pts[3 * q + d]);
+            hi[d] = std::max(hi[d], h_pts[3 * q + d]);
+        }
+    for (int d = 0; d < 3; ++d) {
+        bbox6[d] = lo[d];
+        bbox6[3 + d] = hi[d];
+    }
+    return LSR_OK;
 }

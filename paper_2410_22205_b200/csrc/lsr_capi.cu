@@ -709,6 +709,16 @@ int lsr_cuda_loop_step(lsr_cuda_ctx* c, const lsr_step_cfg* cfg, const lsr_reini
     return LSR_OK;
 }
 
+int lsr_cuda_compute_stats(const double* pts, int64_t n, int dim, double sample_fraction, double k_s, uint64_t seed,
+                           double* h_s, double* gamma_s, double* bbox6) {
+    if ((n > 0 && !pts) || !h_s || !gamma_s || !bbox6) return set_err(LSR_ERR_CONFIG, "compute_stats: null argument");
+    if (dim != 2 && dim != 3) return set_err(LSR_ERR_CONFIG, "compute_stats: dim must be 2 or 3");
+    std::string err;
+    const int st = lsr_prep_compute_stats(pts, n, dim, sample_fraction, k_s, seed, h_s, gamma_s, bbox6, nullptr, &err);
+    if (st) return set_err(st, err);
+    return LSR_OK;
+}
+
 int lsr_cuda_selftest_div_const(double c, int64_t n, uint64_t seed, int64_t* mismatches) {
     if (!pow2_range(c)) return set_err(LSR_ERR_CONFIG, "selftest: divisor outside [2^-100, 2^100]");
     unsigned long long* d = nullptr;

@@ -20,3 +20,7 @@ int lsr_prep_build_distance(const lsr_grid* g, const double* h_pts, int64_t n, i
 // lsr::surface_energy on device fields (energy.cu); synchronous.
 int lsr_prep_surface_energy(const lsr_dev::SlParams& P, const double* phi, const double* dist, int p, int refine,
                             double* energy, int64_t* n_cells, cudaStream_t s, std::string* err);
+
+// lsr::compute_stats (cloud.cpp:480-489) with the NN sample on the device.
+int lsr_prep_compute_stats(const double* h_pts, int64_t n, int dim, double fraction, double k_s, uint64_t seed,
+                           double* h_s, double* gamma_s, double* bbox6, cudaStream_t s, std::string* err);

@@ -266,6 +266,18 @@ def main():
                             e2=np.array(e2s), n_active=np.array(nas), reinit_iters=np.array(its), p=p, interp=interp,
                             delta=delta, gamma=gam)
         print("loop", name, e2s, nas, its)
+    # cloud statistics: lsr::compute_stats (cloud.cpp:480) — seeded
+    # estimate_resolution (Fisher-Yates sample + exact NN + blocked_sum)
+    stats = []
+    for name, pts, dim, frac, seed in (("circle", cloud_circle(64, 1.0, rng), 2, 1.0, 0),
+                                       ("sphere", cloud_sphere(20000, 0.5, rng), 3, 0.1, 7),
+                                       ("torus", cloud_torus(50000, 0.5, 0.2, 0.002, rng), 3, 0.25, 11)):
+        h, gm, bb = R.compute_stats(pts, dim, frac, 2.0, seed)
+        stats.append(dict(name=name, pts=pts, dim=dim, frac=frac, seed=seed, h=h, g=gm, bb=bb))
+    np.savez_compressed(os.path.join(OUT, "stats.npz"),
+                        **{f"{s['name']}_{k}": v for s in stats for k, v in s.items() if k != "name"})
+    print("stats", [(s["name"], s["h"]) for s in stats])
+
     # BASELINE config 1 end to end: 2d circle, 200 seeded points at r = 0.3,
     # 257^2 grid, phi0 = |x| - 0.9, multilinear, 200 loop iterations of the
     # reference driver body (Table 1 run 1: p = 1, delta = 0). Stores the

@@ -103,3 +103,31 @@ def test_distance_512_properties(gpu):
         assert d.field.values[idx] == pytest.approx(np.min(np.linalg.norm(pts - q, axis=1)), rel=1e-13)
     assert np.all(d.field.values[seeded] <= 3.5 * g.dx)  # 4^3 block around the point's cell
     assert np.all(d.field.values < d.sentinel)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["circle", "sphere", "torus"])
+def test_compute_stats_vs_reference_golden(gpu, name):
+    """lsr::compute_stats (cloud.cpp:480): the seeded sample, the exact NN
+    distances and blocked_sum order are reproduced bit for bit."""
+    lsr = gpu
+    rec = load_golden("stats.npz")
+    st = lsr.compute_stats(rec[f"{name}_pts"], int(rec[f"{name}_dim"]), float(rec[f"{name}_frac"]), 2.0,
+                           int(rec[f"{name}_seed"]))
+    assert st.h_s == float(rec[f"{name}_h"]) and st.gamma_s == float(rec[f"{name}_g"])
+    assert np.array_equal(np.array(st.bbox_min + st.bbox_max), rec[f"{name}_bb"])
+
+
+@pytest.mark.gpu
+def test_compute_stats_known_answer_and_errors(gpu):
+    """test_cloud.cpp: 64 lattice points on the unit circle -> h_S = 2 sin(pi/64)."""
+    lsr = gpu
+    th = 2 * np.pi * np.arange(64) / 64
+    pts = np.stack([np.cos(th), np.sin(th), np.zeros(64)], 1)
+    st = lsr.compute_stats(pts, 2, 1.0, 2.0, 3)
+    assert st.h_s == pytest.approx(2 * np.sin(np.pi / 64), rel=1e-13)
+    assert st.gamma_s == 2.0 * st.h_s
+    with pytest.raises(lsr.ConfigError):
+        lsr.compute_stats(pts, 2, 0.0)
+    with pytest.raises(lsr.Error):
+        lsr.compute_stats(pts[:1], 2, 1.0)
