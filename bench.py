@@ -197,8 +197,12 @@ def run_ours(args):
         s = zslab.make_slab(cuts, rank, halo, nxy, g.dims[2])
         mine = zslab.owned_ids(active, s)
         sl = slice(s.z_base * nxy, (s.z_base + s.z_planes) * nxy)
-        phi_t = torch.from_numpy(phi[sl].copy()).cuda()
-        out_t = phi_t.clone()
+        # the two resident phi buffers are whole cudaMalloc allocations so that
+        # their CUDA IPC handles map them on the neighbours (fused path)
+        phi_t = raw_device_tensor(lsr, s.n_resident, torch)
+        out_t = raw_device_tensor(lsr, s.n_resident, torch)
+        phi_t.copy_(torch.from_numpy(phi[sl]))
+        out_t.copy_(phi_t)
         d_t = torch.from_numpy(h_d[sl].copy()).cuda()
         ids_t = torch.from_numpy(mine).cuda()
         del h_d
@@ -220,7 +224,30 @@ def run_ours(args):
                 raise RuntimeError(L.lsr_cuda_last_error_string().decode())
             return 0
 
-        stepper = zslab.SlabStepper(dist, s, halo, phi_t, d_t, out_t, ids_t, compute)
+        fused = None
+        if args.exchange == "fused":
+            fused = setup_fused(L, C, dist, torch, s, halo, phi_t, out_t, world, rank)
+        if fused is not None:
+            peer_lo, peer_hi = fused
+            tiny = torch.zeros(1, device="cuda")
+
+            def compute_fused(src, dst, lo, hi, slab, push):
+                kev[0].record(stream)
+                st = L.lsr_cuda_sl_step_device_fused(
+                    C.byref(cg), slab.z_base, slab.z_planes, slab.lo, slab.hi, C.c_void_p(src.data_ptr()),
+                    C.c_void_p(d_t.data_ptr()), C.c_void_p(ids_t.data_ptr()), ids_t.numel(), C.byref(cc), e2,
+                    C.c_void_p(dst.data_ptr()), C.c_void_p(lo[0]), lo[1], push if lo[0] else 0, C.c_void_p(hi[0]),
+                    hi[1], push if hi[0] else 0, C.c_void_p(bad_t.data_ptr()), C.c_void_p(miss_t.data_ptr()),
+                    C.c_void_p(stream.cuda_stream))
+                kev[1].record(stream)
+                if st != 0:
+                    raise RuntimeError(L.lsr_cuda_last_error_string().decode())
+
+            stepper = zslab.FusedSlabStepper(s, halo, (phi_t, out_t), peer_lo, peer_hi, compute_fused,
+                                             barrier=lambda: dist.all_reduce(tiny))  # stream-ordered
+        else:
+            stepper = zslab.SlabStepper(dist, s, halo, phi_t, d_t, out_t, ids_t, compute)
+        exchange_mode = "fused SL + peer halo push (CUDA IPC)" if fused is not None else "NCCL plane send/recv"
 
         def one_step(i):
             stepper.step()
@@ -300,6 +327,7 @@ def run_ours(args):
                 "energy_e2": e2, "dist_sweep_rounds": rounds,
                 "l2": "flushed (256 MB write) between timed steps",
                 "parallelism": f"z-slab x{world}" if world > 1 else "single GPU",
+                "halo_exchange": exchange_mode if world > 1 else None,
                 "halo_planes": halo,
             },
             "roofline": {
@@ -327,6 +355,74 @@ def run_ours(args):
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+class _CudaArray:
+    """__cuda_array_interface__ view of a raw device allocation (torch.as_tensor shares it)."""
+
+    def __init__(self, ptr, n, owner):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f8", "data": (ptr, False), "version": 3}
+        self.owner = owner
+
+
+class _RawAlloc:
+    def __init__(self, lsr, nbytes):
+        import ctypes as C
+
+        self.lib = lsr.lib()
+        p = C.c_void_p()
+        if self.lib.lsr_cuda_malloc(nbytes, C.byref(p)) != 0:
+            raise RuntimeError(self.lib.lsr_cuda_last_error_string().decode())
+        self.ptr = p.value
+
+    def __del__(self):
+        try:
+            import ctypes as C
+
+            self.lib.lsr_cuda_free(C.c_void_p(self.ptr))
+        except Exception:
+            pass
+
+
+_RAW_KEEP = []
+
+
+def raw_device_tensor(lsr, n, torch):
+    a = _RawAlloc(lsr, 8 * n)
+    _RAW_KEEP.append(a)  # keep the allocation alive for the process
+    return torch.as_tensor(_CudaArray(a.ptr, n, a), device="cuda")
+
+
+def setup_fused(L, C, dist, torch, s, halo, phi_t, out_t, world, rank):
+    """Map the neighbours' resident buffers into this process (CUDA IPC over
+    NVLink/NVSwitch) for the fused SL + halo-push kernel. Every rank must
+    succeed, else all fall back to the NCCL plane exchange."""
+    handles, ok = [], True
+    for t in (phi_t, out_t):
+        h = C.create_string_buffer(64)
+        ok = ok and L.lsr_cuda_ipc_handle(C.c_void_p(t.data_ptr()), h) == 0
+        handles.append(h.raw)
+    info = [None] * world
+    dist.all_gather_object(info, {"handles": handles, "z_base": s.z_base, "ok": ok})
+
+    def open_peer(r):
+        if not info[r]["ok"]:
+            return None
+        ptrs = []
+        for hb in info[r]["handles"]:
+            p = C.c_void_p()
+            if L.lsr_cuda_ipc_open(hb, C.byref(p)) != 0:
+                return None
+            ptrs.append(p.value)
+        return tuple(ptrs), info[r]["z_base"]
+
+    lo = open_peer(rank - 1) if rank > 0 else None
+    hi = open_peer(rank + 1) if rank < world - 1 else None
+    good = torch.tensor([1.0 if ok and (rank == 0 or lo) and (rank == world - 1 or hi) else 0.0], device="cuda")
+    dist.all_reduce(good, op=dist.ReduceOp.MIN)
+    if good.item() < 1.0:
+        return None
+    return lo, hi
 
 
 def max_displacement(g, h_d, active, step, e2):
@@ -511,6 +607,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-loop", action="store_true")
+    ap.add_argument("--exchange", choices=["fused", "nccl"], default="fused",
+                    help="N > 1: fused SL + peer halo push (default) or NCCL plane exchange")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

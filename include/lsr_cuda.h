@@ -29,6 +29,7 @@
 #ifndef LSR_CUDA_H
 #define LSR_CUDA_H
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -122,6 +123,29 @@ int lsr_cuda_sl_step_device(const lsr_grid* grid, int32_t z_base, int32_t z_plan
                             int64_t n_active, const lsr_step_cfg* cfg, double energy_p,
                             double* d_out, int64_t* d_bad_node, int64_t* d_halo_miss,
                             void* stream);
+
+/* Fused SL step + halo exchange (SURVEY §8(e) phase 2): as above with an
+ * owned plane range [own_lo, own_hi); every update of a node in the first
+ * push_lo_planes owned planes is ALSO stored into d_peer_lo_out (the lower
+ * neighbour's resident out buffer, whose first resident plane is
+ * peer_lo_zbase; a peer-mapped NVLink pointer from lsr_cuda_ipc_open), and
+ * of a node in the last push_hi_planes owned planes into d_peer_hi_out. The
+ * neighbours read those planes next step, so no plane exchange follows the
+ * kernel; the caller only orders the ranks (a stream-ordered barrier). Peer
+ * pointers may be NULL. */
+int lsr_cuda_sl_step_device_fused(const lsr_grid* grid, int32_t z_base, int32_t z_planes, int32_t own_lo,
+                                  int32_t own_hi, const double* d_phi, const double* d_dist, const int64_t* d_active,
+                                  int64_t n_active, const lsr_step_cfg* cfg, double energy_p, double* d_out,
+                                  double* d_peer_lo_out, int32_t peer_lo_zbase, int32_t push_lo_planes,
+                                  double* d_peer_hi_out, int32_t peer_hi_zbase, int32_t push_hi_planes,
+                                  int64_t* d_bad_node, int64_t* d_halo_miss, void* stream);
+/* raw device buffers (whole allocations, so CUDA IPC handles cover them) and
+ * CUDA IPC for the peer pointers of the fused path (handles are 64 bytes) */
+int lsr_cuda_malloc(size_t bytes, void** dptr);
+int lsr_cuda_free(void* dptr);
+int lsr_cuda_ipc_handle(void* dptr, uint8_t* handle64);
+int lsr_cuda_ipc_open(const uint8_t* handle64, void** dptr);
+int lsr_cuda_ipc_close(void* dptr);
 
 /* ---- point-cloud preprocessing ----
  * lsr::build_distance_field (distance.cpp:144-148; header distance.hpp:29):

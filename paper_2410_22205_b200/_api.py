@@ -131,6 +131,15 @@ def lib() -> C.CDLL:
     L.lsr_cuda_reinit_defaults.argtypes = [C.c_double, C.c_double, P(CReinitCfg)]
     L.lsr_cuda_reinit_defaults.restype = None
     L.lsr_cuda_loop_step.argtypes = [C.c_void_p, P(CStepCfg), P(CReinitCfg), C.c_int, C.c_double, P(CLoopStats)]
+    L.lsr_cuda_sl_step_device_fused.argtypes = [P(CGrid), C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_void_p,
+                                                C.c_void_p, C.c_void_p, C.c_int64, P(CStepCfg), C.c_double,
+                                                C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_int32,
+                                                C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p]
+    L.lsr_cuda_malloc.argtypes = [C.c_size_t, P(C.c_void_p)]
+    L.lsr_cuda_free.argtypes = [C.c_void_p]
+    L.lsr_cuda_ipc_handle.argtypes = [C.c_void_p, C.c_char_p]
+    L.lsr_cuda_ipc_open.argtypes = [C.c_char_p, P(C.c_void_p)]
+    L.lsr_cuda_ipc_close.argtypes = [C.c_void_p]
     L.lsr_cuda_compute_stats.argtypes = [_dp, C.c_int64, C.c_int, C.c_double, C.c_double, C.c_uint64, P(C.c_double),
                                          P(C.c_double), _dp]
     _lib = L

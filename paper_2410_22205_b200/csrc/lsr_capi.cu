@@ -372,6 +372,66 @@ int lsr_cuda_sl_step_device(const lsr_grid* grid, int32_t z_base, int32_t z_plan
     return LSR_OK;
 }
 
+int lsr_cuda_sl_step_device_fused(const lsr_grid* grid, int32_t z_base, int32_t z_planes, int32_t own_lo,
+                                  int32_t own_hi, const double* d_phi, const double* d_dist, const int64_t* d_active,
+                                  int64_t n_active, const lsr_step_cfg* cfg, double energy_p, double* d_out,
+                                  double* d_peer_lo_out, int32_t peer_lo_zbase, int32_t push_lo_planes,
+                                  double* d_peer_hi_out, int32_t peer_hi_zbase, int32_t push_hi_planes,
+                                  int64_t* d_bad_node, int64_t* d_halo_miss, void* stream) {
+    if (int st = check_grid(grid)) return st;
+    if (int st = check_cfg(cfg, energy_p)) return st;
+    if (grid->dim != 3 || z_base < 0 || z_planes < 1 || z_base + z_planes > grid->dims[2] || own_lo < z_base ||
+        own_hi > z_base + z_planes || own_lo >= own_hi || !d_halo_miss)
+        return set_err(LSR_ERR_CONFIG, "sl_step_device_fused: bad slab description");
+    SlParams P = make_params(*grid, *cfg, energy_p);
+    const long long nxy = static_cast<long long>(grid->dims[0]) * grid->dims[1];
+    P.z_base = z_base;
+    P.z_planes = z_planes;
+    P.own_lo = own_lo;
+    P.own_hi = own_hi;
+    P.halo_miss = reinterpret_cast<unsigned long long*>(d_halo_miss);
+    // peer buffers hold their owners' resident planes: shift to global ids
+    P.peer_lo = d_peer_lo_out ? d_peer_lo_out - static_cast<long long>(peer_lo_zbase) * nxy : nullptr;
+    P.peer_hi = d_peer_hi_out ? d_peer_hi_out - static_cast<long long>(peer_hi_zbase) * nxy : nullptr;
+    P.push_lo_below = own_lo + push_lo_planes;
+    P.push_hi_from = own_hi - push_hi_planes;
+    const long long shift = static_cast<long long>(z_base) * nxy;
+    LSR_CUDA_TRY(launch_sl_step(P, cfg->interp, d_phi - shift, d_dist - shift, d_active, n_active, d_out - shift,
+                                reinterpret_cast<unsigned long long*>(d_bad_node), static_cast<cudaStream_t>(stream)));
+    return LSR_OK;
+}
+
+int lsr_cuda_malloc(size_t bytes, void** dptr) {
+    if (!dptr) return set_err(LSR_ERR_CONFIG, "malloc: null out");
+    LSR_CUDA_TRY(cudaMalloc(dptr, bytes));
+    return LSR_OK;
+}
+
+int lsr_cuda_free(void* dptr) {
+    LSR_CUDA_TRY(cudaFree(dptr));
+    return LSR_OK;
+}
+
+int lsr_cuda_ipc_handle(void* dptr, uint8_t* handle64) {
+    cudaIpcMemHandle_t h;
+    LSR_CUDA_TRY(cudaIpcGetMemHandle(&h, dptr));
+    static_assert(sizeof(h) == 64, "CUDA IPC handles are 64 bytes");
+    std::memcpy(handle64, &h, sizeof h);
+    return LSR_OK;
+}
+
+int lsr_cuda_ipc_open(const uint8_t* handle64, void** dptr) {
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle64, sizeof h);
+    LSR_CUDA_TRY(cudaIpcOpenMemHandle(dptr, h, cudaIpcMemLazyEnablePeerAccess));
+    return LSR_OK;
+}
+
+int lsr_cuda_ipc_close(void* dptr) {
+    LSR_CUDA_TRY(cudaIpcCloseMemHandle(dptr));
+    return LSR_OK;
+}
+
 // The one-shot host entry, pipelined over z-chunks for 3d grids: the H2D
 // of phi and d (plane order), the SL kernel of each chunk (as soon as its
 // planes plus a halo are resident) and the D2H of finished out planes run on

@@ -46,6 +46,19 @@ __global__ void __launch_bounds__(kSlThreads, kSlMinBlocks) sl_step_kernel(SlPar
     const double next = sl_node<DIM, KIND, kSlThreads>(P, phi, dist, id, i, j, k, sb);
     if (!isfinite(next)) atomicMin(bad, static_cast<unsigned long long>(id));
     out[id] = next;
+    // fused halo exchange: the neighbours read these planes next step, so the
+    // update goes straight into their resident buffers over NVLink (peer
+    // mapped) instead of a separate plane exchange after the kernel
+    bool pushed = false;
+    if (P.peer_lo != nullptr && k < P.push_lo_below) {
+        P.peer_lo[id] = next;
+        pushed = true;
+    }
+    if (P.peer_hi != nullptr && k >= P.push_hi_from) {
+        P.peer_hi[id] = next;
+        pushed = true;
+    }
+    if (pushed) __threadfence_system();
 }
 
 // out[ids] = phi[ids]: re-establishes "out equals phi off the active set"

@@ -109,6 +109,42 @@ def halo_planes(max_displacement: float, dx: float, interp: int) -> int:
     return int(np.ceil(max_displacement / dx)) + (2 if interp == 1 else 1) + 1
 
 
+class FusedSlabStepper:
+    """SURVEY §8(e) phase 2: one kernel per step computes the owned updates
+    and stores those of the first/last `push` owned planes straight into the
+    neighbours' resident out buffers (peer-mapped over NVLink). The only
+    inter-rank operation left is ordering: `barrier()` (stream-ordered) after
+    the kernel so a neighbour starts step n+1 only once our pushes landed.
+
+    bufs: this rank's two resident buffers (device pointers; step n writes
+    bufs[(n+1) % 2] from bufs[n % 2]); peer_lo / peer_hi: the lower / upper
+    neighbour's two buffers (or None) and their first resident plane."""
+
+    def __init__(self, slab: Slab, push: int, bufs, peer_lo, peer_hi, compute_fused, barrier=None):
+        self.s, self.push, self.bufs = slab, push, bufs
+        self.peer_lo, self.peer_hi = peer_lo, peer_hi
+        self.compute = compute_fused
+        self.barrier = barrier
+        self.n = 0
+
+    def pointers(self):
+        src, dst = self.bufs[self.n % 2], self.bufs[(self.n + 1) % 2]
+        lo = (self.peer_lo[0][(self.n + 1) % 2], self.peer_lo[1]) if self.peer_lo else (None, 0)
+        hi = (self.peer_hi[0][(self.n + 1) % 2], self.peer_hi[1]) if self.peer_hi else (None, 0)
+        return src, dst, lo, hi
+
+    def step(self) -> None:
+        src, dst, lo, hi = self.pointers()
+        self.compute(src, dst, lo, hi, self.s, self.push)
+        if self.barrier is not None:
+            self.barrier()
+        self.n += 1
+
+    @property
+    def current(self):
+        return self.bufs[self.n % 2]
+
+
 class SlabStepper:
     """Drives one rank's slab through K steps: compute(phi, dist, out, slab,
     ids) updates the owned ids (returns the halo-miss count), then the halo

@@ -118,6 +118,86 @@ def test_plan_cuts_balance_and_thickness():
 
 
 @pytest.mark.gpu
+def test_fused_peer_push_two_slabs_one_gpu(gpu):
+    """The fused SL + halo-push kernel, two slabs emulated on one GPU: the
+    'peer' pointers are the other slab's buffers, the slabs' kernels run one
+    after the other (neither waits on the other). K steps must reproduce the
+    whole-grid evolution bit for bit with no plane exchange at all."""
+    import ctypes as C
+
+    import torch
+
+    lsr = gpu
+    from paper_2410_22205_b200 import zslab
+
+    _, phi, dfield, active, cfgd = _inputs()
+    g = lsr._api.cube_grid(N, 3)
+    bp = lsr.BandParams(cfgd["gamma"], cfgd["beta"])
+    cfg = lsr.StepConfig(p=2, delta=1.0, dt=cfgd["dt"], band=bp)
+    nxy = N * N
+    halo = 5
+    K = 4
+    # whole grid, K ping-pong steps on the same band
+    ctx = lsr.Context(g)
+    ctx.upload(0, phi)
+    ctx.upload(1, dfield)
+    ctx.set_active(active)
+    for _ in range(K):
+        ctx.sl_step(cfg, 0.8)
+        ctx.swap()
+    whole = ctx.download(0)
+
+    cuts = zslab.plan_cuts(active, nxy, N, 2, min_planes=halo)
+    slabs = [zslab.make_slab(cuts, r, halo, nxy, N) for r in range(2)]
+    bufs, dbuf, ids, miss, bad = [], [], [], [], []
+    for s in slabs:
+        sl = slice(s.z_base * nxy, (s.z_base + s.z_planes) * nxy)
+        t = torch.from_numpy(phi[sl].copy()).cuda()
+        bufs.append((t, t.clone()))
+        dbuf.append(torch.from_numpy(dfield[sl].copy()).cuda())
+        ids.append(torch.from_numpy(zslab.owned_ids(active, s)).cuda())
+        miss.append(torch.zeros(1, dtype=torch.int64, device="cuda"))
+        bad.append(torch.full((1,), np.iinfo(np.int64).max, dtype=torch.int64, device="cuda"))
+    L = lsr.lib()
+    cg, cc = g.c(), cfg.c()
+    stream = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+    def make_compute(r):
+        def compute(src, dst, lo, hi, s, push):
+            st = L.lsr_cuda_sl_step_device_fused(
+                C.byref(cg), s.z_base, s.z_planes, s.lo, s.hi, C.c_void_p(src.data_ptr()),
+                C.c_void_p(dbuf[r].data_ptr()), C.c_void_p(ids[r].data_ptr()), ids[r].numel(), C.byref(cc), 0.8,
+                C.c_void_p(dst.data_ptr()), C.c_void_p(lo[0].data_ptr() if lo[0] is not None else None), lo[1],
+                push if lo[0] is not None else 0, C.c_void_p(hi[0].data_ptr() if hi[0] is not None else None), hi[1],
+                push if hi[0] is not None else 0, C.c_void_p(bad[r].data_ptr()), C.c_void_p(miss[r].data_ptr()),
+                stream)
+            assert st == 0, L.lsr_cuda_last_error_string()
+        return compute
+
+    steppers = [
+        zslab.FusedSlabStepper(slabs[0], halo, bufs[0], None, (bufs[1], slabs[1].z_base), make_compute(0)),
+        zslab.FusedSlabStepper(slabs[1], halo, bufs[1], (bufs[0], slabs[0].z_base), None, make_compute(1)),
+    ]
+    for _ in range(K):
+        for st in steppers:
+            st.step()
+    torch.cuda.synchronize()
+    assert int(miss[0].item()) == 0 and int(miss[1].item()) == 0
+    got = np.empty_like(phi)
+    for st, s in zip(steppers, slabs):
+        cur = st.current.cpu().numpy()
+        got[s.lo * nxy:s.hi * nxy] = cur[(s.lo - s.z_base) * nxy:(s.hi - s.z_base) * nxy]
+    # planes outside every slab's ownership do not exist (cuts cover [0, N))
+    assert np.array_equal(bits(got), bits(whole))
+    # the buffers can be exported for peer mapping (CUDA IPC)
+    h = C.create_string_buffer(64)
+    p = C.c_void_p()
+    assert L.lsr_cuda_malloc(1 << 20, C.byref(p)) == 0
+    assert L.lsr_cuda_ipc_handle(p, h) == 0 and any(h.raw)
+    assert L.lsr_cuda_free(p) == 0
+
+
+@pytest.mark.gpu
 def test_slab_kernel_matches_whole_grid_and_counts_misses(gpu):
     """Two slabs computed one after the other on one GPU (no kernel waits on
     another) reproduce the whole-grid step; a too-thin halo is reported."""
