@@ -45,6 +45,8 @@ CONFIGS = {
             name="bumpy-sphere-512"),
     3: dict(n=256, dim=3, cloud=3, points=100_000, sigma=0.5, interp=1, r0=0.9, p=2, delta=1.0,
             name="torus-256"),
+    5: dict(n=1024, dim=3, cloud=5, points=4_000_000, sigma=0.25, interp=1, r0=0.95, p=2, delta=1.0,
+            name="three-tori-1024"),
     2: dict(n=128, dim=3, cloud=2, points=20_000, sigma=0.0, interp=0, r0=0.9, p=2, delta=1.0,
             name="sphere-128"),
 }
