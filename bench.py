@@ -470,8 +470,13 @@ def measure_e2e(lsr, g, phi, ctx, active, step, e2, args):
         lsr.sl_step(sphi, sd, mask, step, e2, out)  # synchronous: returns after the D2H of out
         ts.append(time.perf_counter() - t0)
     t = float(np.mean(ts))
-    return {"value": active.size / t, "unit": UNIT, "h2d_bytes_per_step": int(2 * n * 8 + active.size * 8),
-            "d2h_bytes_per_step": int(n * 8), "ms_per_step": t * 1e3, "timing": "host clock around the synchronous call",
+    import ctypes as C
+
+    h2d, d2h = C.c_int64(), C.c_int64()
+    lsr.lib().lsr_cuda_last_transfer_bytes(C.byref(h2d), C.byref(d2h))  # what the call actually copied
+    return {"value": active.size / t, "unit": UNIT, "h2d_bytes_per_step": int(h2d.value),
+            "d2h_bytes_per_step": int(d2h.value), "ms_per_step": t * 1e3,
+            "timing": "host clock around the synchronous call (pinned host buffers: phi, d, ids in; out back)",
             "steps": args.e2e_steps}
 
 

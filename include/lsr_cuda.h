@@ -86,6 +86,9 @@ int64_t lsr_cuda_kernel_launches(void);
 int lsr_cuda_sl_step_host(const lsr_grid* grid, const double* phi, const double* dist,
                           const int64_t* active, int64_t n_active, const lsr_step_cfg* cfg,
                           double energy_p, double* out, int64_t* bad_node);
+/* bytes the calling thread's last lsr_cuda_sl_step_host moved H2D / D2H (3d
+ * grids upload only the rows of d that the band's gradients read) */
+void lsr_cuda_last_transfer_bytes(int64_t* h2d, int64_t* d2h);
 
 /* ---- device-resident context (the loop keeps phi, d, out and ids in HBM) ---- */
 int lsr_cuda_create(int device, const lsr_grid* grid, lsr_cuda_ctx** ctx);

@@ -135,6 +135,8 @@ def lib() -> C.CDLL:
                                                 C.c_void_p, C.c_void_p, C.c_int64, P(CStepCfg), C.c_double,
                                                 C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_int32,
                                                 C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p]
+    L.lsr_cuda_last_transfer_bytes.argtypes = [P(C.c_int64), P(C.c_int64)]
+    L.lsr_cuda_last_transfer_bytes.restype = None
     L.lsr_cuda_malloc.argtypes = [C.c_size_t, P(C.c_void_p)]
     L.lsr_cuda_free.argtypes = [C.c_void_p]
     L.lsr_cuda_ipc_handle.argtypes = [C.c_void_p, C.c_char_p]

@@ -22,6 +22,8 @@ using lsr_dev::SlParams;
 namespace {
 
 thread_local std::string g_err;
+// bytes the last lsr_cuda_sl_step_host call moved host->device / device->host
+thread_local int64_t g_h2d_bytes = 0, g_d2h_bytes = 0;
 std::atomic<long long> g_launches{0};
 
 int set_err(int code, const std::string& msg) {
@@ -186,6 +188,11 @@ extern "C" {
 const char* lsr_cuda_last_error_string(void) { return g_err.c_str(); }
 
 int64_t lsr_cuda_kernel_launches(void) { return g_launches.load(); }
+
+void lsr_cuda_last_transfer_bytes(int64_t* h2d, int64_t* d2h) {
+    if (h2d) *h2d = g_h2d_bytes;
+    if (d2h) *d2h = g_d2h_bytes;
+}
 
 int lsr_cuda_create(int device, const lsr_grid* grid, lsr_cuda_ctx** out) {
     if (!out) return set_err(LSR_ERR_CONFIG, "create: null out");
@@ -476,11 +483,43 @@ static int sl_step_host_pipelined(lsr_cuda_ctx* c, const double* phi, const doub
     first[nch] = n_active;
     SlParams P = make_params(g, *cfg, energy_p);
     P.halo_miss = c->d_miss;
+    // d is read only at active nodes and their axis neighbours (the centered
+    // gradient, grid.cpp:53-74): with ascending ids, the active rows of plane
+    // k span [row(first id), row(last id)], so plane k needs the d rows of
+    // planes k-1..k+1's active spans widened by one row. Ids that are not
+    // ascending are detected on the device (check_sorted below) and force
+    // the exact fallback with a full upload of d.
+    const int nx = g.dims[0], ny = g.dims[1];
+    std::vector<int> span_lo(nz, ny), span_hi(nz, -1);
+    for (int k = 0; k < nz; ++k) {
+        const int64_t a = std::lower_bound(active, active + n_active, static_cast<int64_t>(k) * nxy) - active;
+        const int64_t b = std::lower_bound(active, active + n_active, static_cast<int64_t>(k + 1) * nxy) - active;
+        if (a < b) {
+            span_lo[k] = static_cast<int>((active[a] - static_cast<int64_t>(k) * nxy) / nx);
+            span_hi[k] = static_cast<int>((active[b - 1] - static_cast<int64_t>(k) * nxy) / nx);
+        }
+    }
+    LSR_CUDA_TRY(launch_check_sorted(c->active, n_active, c->d_miss, up));
+    int64_t h2d = static_cast<int64_t>(sizeof(int64_t)) * n_active;
     for (int ch = 0; ch < nch; ++ch) {  // uploads in plane order
         const long long o = static_cast<long long>(ch) * zc * nxy;
         const long long cnt = static_cast<long long>(std::min(nz, (ch + 1) * zc) - ch * zc) * nxy;
         LSR_CUDA_TRY(cudaMemcpyAsync(c->phi + o, phi + o, sizeof(double) * cnt, cudaMemcpyHostToDevice, up));
-        LSR_CUDA_TRY(cudaMemcpyAsync(c->dist + o, dist + o, sizeof(double) * cnt, cudaMemcpyHostToDevice, up));
+        h2d += static_cast<int64_t>(sizeof(double)) * cnt;
+        for (int k = ch * zc; k < std::min(nz, (ch + 1) * zc); ++k) {
+            int lo = ny, hi = -1;
+            for (int kk = std::max(0, k - 1); kk <= std::min(nz - 1, k + 1); ++kk) {
+                lo = std::min(lo, span_lo[kk]);
+                hi = std::max(hi, span_hi[kk]);
+            }
+            if (hi < lo) continue;
+            lo = std::max(0, lo - 1);
+            hi = std::min(ny - 1, hi + 1);
+            const long long ro = static_cast<long long>(k) * nxy + static_cast<long long>(lo) * nx;
+            LSR_CUDA_TRY(cudaMemcpyAsync(c->dist + ro, dist + ro, sizeof(double) * (hi - lo + 1) * nx,
+                                         cudaMemcpyHostToDevice, up));
+            h2d += static_cast<int64_t>(sizeof(double)) * (hi - lo + 1) * nx;
+        }
         LSR_CUDA_TRY(cudaMemcpyAsync(c->out + o, c->phi + o, sizeof(double) * cnt, cudaMemcpyDeviceToDevice, up));
         LSR_CUDA_TRY(cudaEventRecord(c->ev_up[ch], up));
     }
@@ -506,7 +545,8 @@ static int sl_step_host_pipelined(lsr_cuda_ctx* c, const double* phi, const doub
     LSR_CUDA_TRY(cudaMemcpy(&h[0], c->d_miss, sizeof(unsigned long long), cudaMemcpyDeviceToHost));
     LSR_CUDA_TRY(cudaMemcpy(&h[1], c->d_bad, sizeof(unsigned long long), cudaMemcpyDeviceToHost));
     c->consistent = false;
-    if (h[0] != 0) {  // rerun unpipelined (everything is resident now)
+    if (h[0] != 0) {  // rerun unpipelined with the whole of d resident
+        LSR_CUDA_TRY(cudaMemcpyAsync(c->dist, dist, sizeof(double) * c->n, cudaMemcpyHostToDevice, up));
         P.halo_miss = nullptr;
         P.z_base = 0;
         P.z_planes = nz;
@@ -516,7 +556,10 @@ static int sl_step_host_pipelined(lsr_cuda_ctx* c, const double* phi, const doub
         LSR_CUDA_TRY(cudaMemcpyAsync(&h[1], c->d_bad, sizeof(unsigned long long), cudaMemcpyDeviceToHost, up));
         LSR_CUDA_TRY(cudaStreamSynchronize(up));
         c->pipeline_fallbacks++;
+        h2d += static_cast<int64_t>(sizeof(double)) * c->n;
     }
+    g_h2d_bytes = h2d;
+    g_d2h_bytes = static_cast<int64_t>(sizeof(double)) * c->n * (h[0] != 0 ? 2 : 1);
     if (h[1] != ~0ULL) return numerical_error(g, h[1], bad_node);
     return LSR_OK;
 }
@@ -563,6 +606,8 @@ int lsr_cuda_sl_step_host(const lsr_grid* grid, const double* phi, const double*
     if (bad_node) *bad_node = bad;
     if (st != LSR_OK && st != LSR_ERR_NUMERICAL) return st;
     const std::string msg = g_err;
+    g_h2d_bytes = static_cast<int64_t>(2 * bytes + sizeof(int64_t) * n_active);
+    g_d2h_bytes = static_cast<int64_t>(bytes);
     // out is fully written even when a node went non-finite (evolve.cpp:110-117)
     LSR_CUDA_TRY(cudaMemcpyAsync(out, c->out, bytes, cudaMemcpyDeviceToHost, s));
     LSR_CUDA_TRY(cudaStreamSynchronize(s));

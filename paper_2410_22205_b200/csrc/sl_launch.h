@@ -23,6 +23,8 @@ cudaError_t launch_sl_step(const lsr_dev::SlParams& P, int kind, const double* p
                            const int64_t* active, long long n_active, double* out, unsigned long long* bad,
                            cudaStream_t stream);
 
+cudaError_t launch_check_sorted(const int64_t* ids, long long n, unsigned long long* bad, cudaStream_t stream);
+
 cudaError_t launch_resync(const double* phi, double* out, const int64_t* ids, long long n, cudaStream_t stream);
 
 cudaError_t launch_div_selftest(double c, double rc, unsigned long long seed, long long n,

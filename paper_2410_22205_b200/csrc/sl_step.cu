@@ -71,6 +71,14 @@ __global__ void resync_kernel(const double* __restrict__ phi, double* __restrict
     out[id] = __ldg(phi + id);
 }
 
+// counts positions where the id list is not strictly ascending
+__global__ void check_sorted_kernel(const int64_t* __restrict__ ids, long long n, unsigned long long* __restrict__ bad) {
+    const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const bool wrong = i + 1 < n && !(__ldg(ids + i) < __ldg(ids + i + 1));
+    const unsigned b = __ballot_sync(0xffffffffu, wrong);
+    if ((threadIdx.x & 31) == 0 && b) atomicAdd(bad, static_cast<unsigned long long>(__popc(b)));
+}
+
 // Self-test of div_const against the hardware IEEE division: a splitmix64
 // stream of bit patterns (all exponents, signs, zeros, subnormals, inf/NaN)
 // divided by c; counts quotients whose bits differ.
@@ -117,6 +125,13 @@ cudaError_t launch_sl_step(const SlParams& P, int kind, const double* phi, const
         if (kind == 0) sl_step_kernel<3, 0><<<blocks, kSlThreads, 0, stream>>>(P, phi, dist, active, n_active, out, bad);
         else sl_step_kernel<3, 1><<<blocks, kSlThreads, 0, stream>>>(P, phi, dist, active, n_active, out, bad);
     }
+    lsr_note_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_check_sorted(const int64_t* ids, long long n, unsigned long long* bad, cudaStream_t stream) {
+    if (n <= 1) return cudaSuccess;
+    check_sorted_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, stream>>>(ids, n, bad);
     lsr_note_launch();
     return cudaGetLastError();
 }
