@@ -36,8 +36,6 @@ sys.path.insert(0, ROOT)
 METRIC = "SL narrow-band node-updates/s (WENO, 512^3, fp64)"
 UNIT = "node-updates/s"
 BYTES_PER_UPDATE = {("weno", 3): 2176, ("q1", 3): 384, ("weno", 2): 352, ("q1", 2): 160}
-COMPULSORY_BYTES = 32
-DFMA_PER_UPDATE_WENO3 = None  # counted by ncu, see DESIGN.md
 
 CONFIGS = {
     # id: (n, dim, cloud config, points, sigma in dx, interp, phi0 radius, p, delta)
