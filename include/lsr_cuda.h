@@ -87,8 +87,19 @@ int lsr_cuda_sl_step_host(const lsr_grid* grid, const double* phi, const double*
                           const int64_t* active, int64_t n_active, const lsr_step_cfg* cfg,
                           double energy_p, double* out, int64_t* bad_node);
 /* bytes the calling thread's last lsr_cuda_sl_step_host moved H2D / D2H (3d
- * grids upload only the rows of d that the band's gradients read) */
+ * grids move packed row runs: d where the gradients read it, phi around the
+ * band, the band's updated values back; the host copies phi to out) */
 void lsr_cuda_last_transfer_bytes(int64_t* h2d, int64_t* d2h);
+/* Host-only view of the packed uploads (no GPU needed): for these ascending
+ * active ids, copies into dist_field the d values the one-shot 3d step
+ * uploads (active nodes and their axis neighbours) and, when reach > 0, into
+ * phi_field the phi values of the Chebyshev ball of radius `reach` around
+ * every active node. counts[4] = d values, d row runs, phi values, phi row
+ * runs. LSR_ERR_CONFIG if the ids are not ascending in-grid (the one-shot
+ * step then uploads the fields whole). */
+int lsr_cuda_pack_host(const lsr_grid* grid, const int64_t* active, int64_t n_active, int32_t reach,
+                       const double* dist, const double* phi, double* dist_field, double* phi_field,
+                       int64_t* counts);
 
 /* ---- device-resident context (the loop keeps phi, d, out and ids in HBM) ---- */
 int lsr_cuda_create(int device, const lsr_grid* grid, lsr_cuda_ctx** ctx);

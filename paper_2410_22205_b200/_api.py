@@ -137,6 +137,8 @@ def lib() -> C.CDLL:
                                                 C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p]
     L.lsr_cuda_last_transfer_bytes.argtypes = [P(C.c_int64), P(C.c_int64)]
     L.lsr_cuda_last_transfer_bytes.restype = None
+    L.lsr_cuda_pack_host.argtypes = [P(CGrid), C.c_void_p, C.c_int64, C.c_int32, _dp, C.c_void_p, _dp, C.c_void_p,
+                                     P(C.c_int64)]
     L.lsr_cuda_malloc.argtypes = [C.c_size_t, P(C.c_void_p)]
     L.lsr_cuda_free.argtypes = [C.c_void_p]
     L.lsr_cuda_ipc_handle.argtypes = [C.c_void_p, C.c_char_p]
@@ -232,6 +234,35 @@ def build_distance_field(grid: "Grid", points: np.ndarray, dim: int | None = Non
     out = DistanceField(ScalarField(grid, d), ex, sent.value)
     out.rounds = rounds.value
     return out
+
+
+def last_transfer_bytes() -> tuple[int, int]:
+    """(H2D, D2H) bytes the calling thread's last one-shot sl_step moved."""
+    h2d, d2h = C.c_int64(), C.c_int64()
+    lib().lsr_cuda_last_transfer_bytes(C.byref(h2d), C.byref(d2h))
+    return int(h2d.value), int(d2h.value)
+
+
+def pack_host(dist: "DistanceField", active: np.ndarray, dist_field: np.ndarray, reach: int = 0,
+              phi: np.ndarray | None = None, phi_field: np.ndarray | None = None) -> tuple[int, int, int, int]:
+    """Host-only view of the one-shot step's packed uploads: writes into
+    dist_field the d values uploaded for these ascending active ids (active
+    nodes and their axis neighbours) and, for reach > 0, into phi_field the
+    phi values of the Chebyshev ball of radius `reach` around every active
+    node. Returns (d values, d runs, phi values, phi runs)."""
+    ids = np.ascontiguousarray(active, dtype=np.int64)
+    d = np.ascontiguousarray(dist.field.values, dtype=np.float64)
+    for f in (dist_field, phi_field) if reach > 0 else (dist_field,):
+        if f is None or f.dtype != np.float64 or not f.flags.c_contiguous or f.size != d.size:
+            raise ConfigError("pack_host: fields must be contiguous float64 arrays of the grid's size")
+    ph = None
+    if reach > 0:
+        ph = np.ascontiguousarray(phi, dtype=np.float64)
+    counts = (C.c_int64 * 4)()
+    _check(lib().lsr_cuda_pack_host(C.byref(dist.field.grid.c()), _ids_ptr(ids), ids.size, int(reach), d,
+                                    ph.ctypes.data_as(C.c_void_p) if ph is not None else None, dist_field,
+                                    phi_field.ctypes.data_as(C.c_void_p) if reach > 0 else None, counts))
+    return tuple(int(x) for x in counts)
 
 
 def selftest_div_const(c: float, n: int, seed: int = 1) -> int:

@@ -7,15 +7,22 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <functional>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <vector>
 #include <algorithm>
+#include <chrono>
+#include <cstdlib>
+#include <thread>
 
 #include "lsr_cuda.h"
 #include "band_launch.h"
 #include "prep_launch.h"
 #include "sl_launch.h"
+#include "host_pack.h"
+#include "transfer_launch.h"
 
 using lsr_dev::SlParams;
 
@@ -157,6 +164,24 @@ struct lsr_cuda_ctx {
     cudaEvent_t ev_up[32] = {}, ev_cmp[32] = {};
     unsigned long long* d_miss = nullptr;
     int64_t pipeline_fallbacks = 0;
+    // pipelined host entry, packed transfers (host_pack.h): pinned staging and
+    // device copies of the packed d and phi sets and of the chunk results
+    lsr_host::StepPacker packer;
+    std::unique_ptr<lsr_host::Pool> copy_pool;  // host out = phi copy and result scatter
+    int reach = 5;  // Chebyshev radius of the packed phi set; 0 = upload phi whole
+    cudaEvent_t ev_down[32] = {};
+    struct Packed {
+        double* h_vals = nullptr;
+        lsr_host::RunDesc* h_desc = nullptr;
+        double* d_vals = nullptr;
+        long long* d_desc = nullptr;  // RunDesc pairs (dst, src)
+        int64_t cap_hv = 0, cap_hd = 0, cap_dv = 0, cap_dd = 0;
+    } pk_d, pk_phi;
+    double* h_res = nullptr;
+    double* d_res = nullptr;
+    int64_t cap_hres = 0, cap_dres = 0;
+    unsigned long long* bm = nullptr;  // node bitmaps of the zero-copy pull (transfer.cu)
+    int64_t cap_bm = 0;
 };
 
 namespace {
@@ -233,6 +258,18 @@ int lsr_cuda_destroy(lsr_cuda_ctx* c) {
     c->band.release();
     c->rb.release();
     cudaFree(c->d_miss);
+    c->copy_pool.reset();
+    for (auto* q : {&c->pk_d, &c->pk_phi}) {
+        if (q->h_vals) cudaFreeHost(q->h_vals);
+        if (q->h_desc) cudaFreeHost(q->h_desc);
+        cudaFree(q->d_vals);
+        cudaFree(q->d_desc);
+    }
+    if (c->h_res) cudaFreeHost(c->h_res);
+    cudaFree(c->d_res);
+    cudaFree(c->bm);
+    for (auto& e : c->ev_down)
+        if (e) cudaEventDestroy(e);
     for (auto& e : c->ev_up)
         if (e) cudaEventDestroy(e);
     for (auto& e : c->ev_cmp)
@@ -440,127 +477,410 @@ int lsr_cuda_ipc_close(void* dptr) {
 }
 
 // The one-shot host entry, pipelined over z-chunks for 3d grids: the H2D
-// of phi and d (plane order), the SL kernel of each chunk (as soon as its
-// planes plus a halo are resident) and the D2H of finished out planes run on
-// three streams, so the PCIe directions overlap each other and the compute.
-// Each chunk runs the kernel in slab mode: a stencil that reaches a plane not
-// yet uploaded, or an id outside the chunk's planes (unsorted input), is
-// counted; any count makes the whole step rerun unpipelined (exact either
-// way).
+// of phi (plane order) and of the packed d values, the SL kernel of each
+// chunk (as soon as its planes plus a halo are resident) and the D2H of
+// finished out planes run on three streams, so the PCIe directions overlap
+// each other and the compute. d is read only at active nodes and their axis
+// neighbours, so host threads gather exactly those values (as row runs,
+// host_pack.h) into pinned staging while phi streams up, and a device kernel
+// scatters them into place. Each chunk runs the kernel in slab mode: a
+// stencil that reaches a plane not yet uploaded is counted, and any count
+// makes the whole step rerun unpipelined with all of d resident (exact
+// either way). Ids that are not ascending skip the pipeline altogether.
 static constexpr int kNotPipelined = -1000;
+
+static int host_threads() {
+    static const int n = [] {
+        if (const char* e = std::getenv("LSR_HOST_THREADS")) return std::max(1, std::atoi(e));
+        return static_cast<int>(std::min(16u, std::max(1u, std::thread::hardware_concurrency())));
+    }();
+    return n;
+}
+
+extern "C++" {
+template <class T>
+static int ensure_pinned(T** buf, int64_t* cap, int64_t n) {
+    if (n <= *cap) return LSR_OK;
+    if (*buf) cudaFreeHost(*buf);
+    *buf = nullptr;
+    *cap = 0;
+    const int64_t c = n + n / 4 + 4096;
+    LSR_CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(buf), sizeof(T) * c, cudaHostAllocDefault));
+    *cap = c;
+    return LSR_OK;
+}
+
+template <class T>
+static int ensure_device(T** buf, int64_t* cap, int64_t n) {
+    if (n <= *cap) return LSR_OK;
+    if (*buf) cudaFree(*buf);
+    *buf = nullptr;
+    *cap = 0;
+    const int64_t c = n + n / 4 + 4096;
+    LSR_CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(buf), sizeof(T) * c));
+    *cap = c;
+    return LSR_OK;
+}
+
+}  // extern "C++"
+
+// copies one packed set's chunk [z0, z1) to the device and counts the bytes
+static int upload_set(const lsr_host::PackSet& ps, lsr_cuda_ctx::Packed& q, int z0, int z1, cudaStream_t s,
+                      int64_t* h2d) {
+    const int64_t v0 = ps.values_before(z0), v1 = ps.values_before(z1);
+    const int64_t r0 = ps.runs_before(z0), r1 = ps.runs_before(z1);
+    if (v1 <= v0) return LSR_OK;
+    LSR_CUDA_TRY(cudaMemcpyAsync(q.d_vals + v0, q.h_vals + v0, sizeof(double) * (v1 - v0), cudaMemcpyHostToDevice, s));
+    LSR_CUDA_TRY(cudaMemcpyAsync(q.d_desc + 2 * r0, q.h_desc + r0, sizeof(lsr_host::RunDesc) * (r1 - r0),
+                                 cudaMemcpyHostToDevice, s));
+    *h2d += static_cast<int64_t>(sizeof(double)) * (v1 - v0) +
+            static_cast<int64_t>(sizeof(lsr_host::RunDesc)) * (r1 - r0);
+    return LSR_OK;
+}
+
+static int ensure_set(const lsr_host::PackSet& ps, lsr_cuda_ctx::Packed& q) {
+    if (int st = ensure_pinned(&q.h_vals, &q.cap_hv, ps.total_values())) return st;
+    if (int st = ensure_pinned(&q.h_desc, &q.cap_hd, ps.total_runs())) return st;
+    if (int st = ensure_device(&q.d_vals, &q.cap_dv, ps.total_values())) return st;
+    return ensure_device(reinterpret_cast<lsr_host::RunDesc**>(&q.d_desc), &q.cap_dd, ps.total_runs());
+}
+
+// the device address of n doubles of mapped (pinned) host memory, or null
+// when the GPU cannot read the whole range directly
+static const double* mapped_ptr(const double* h, int64_t n) {
+    cudaPointerAttributes a{}, b{};
+    if (cudaPointerGetAttributes(&a, h) != cudaSuccess || cudaPointerGetAttributes(&b, h + (n - 1)) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    if (a.type != cudaMemoryTypeHost || b.type != cudaMemoryTypeHost || !a.devicePointer || !b.devicePointer)
+        return nullptr;
+    const double* d = static_cast<const double*>(a.devicePointer);
+    return static_cast<const double*>(b.devicePointer) == d + (n - 1) ? d : nullptr;
+}
+
+struct Finally {
+    std::function<void()> f;
+    ~Finally() { f(); }
+};
 
 static int sl_step_host_pipelined(lsr_cuda_ctx* c, const double* phi, const double* dist, const int64_t* active,
                                   int64_t n_active, const lsr_step_cfg* cfg, double energy_p, double* out,
                                   int64_t* bad_node) {
     const lsr_grid& g = c->grid;
-    const int nz = g.dims[2];
-    const long long nxy = static_cast<long long>(g.dims[0]) * g.dims[1];
+    const int nx = g.dims[0], ny = g.dims[1], nz = g.dims[2];
+    const long long nxy = static_cast<long long>(nx) * ny;
     const int kChunks = 16;
     const int zc = (nz + kChunks - 1) / kChunks;
     const int nch = (nz + zc - 1) / zc;
-    const int halo = 8;  // lead of the upload over the compute (planes)
+    const int halo = 8;  // lead of the upload over the compute (planes); >= the packed reach
     LSR_CUDA_TRY(cudaSetDevice(c->device));
     if (!c->s_cmp) {
         LSR_CUDA_TRY(cudaStreamCreateWithFlags(&c->s_cmp, cudaStreamNonBlocking));
         LSR_CUDA_TRY(cudaStreamCreateWithFlags(&c->s_down, cudaStreamNonBlocking));
         for (auto& e : c->ev_up) LSR_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         for (auto& e : c->ev_cmp) LSR_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        for (auto& e : c->ev_down) LSR_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         LSR_CUDA_TRY(cudaMalloc(&c->d_miss, sizeof(unsigned long long)));
     }
     if (nch > static_cast<int>(sizeof(c->ev_up) / sizeof(c->ev_up[0]))) return kNotPipelined;
     cudaStream_t up = c->stream, cmp = c->s_cmp, down = c->s_down;
+    const auto chunk_off = [&](int ch) { return static_cast<long long>(std::min(nz, ch * zc)) * nxy; };
+    const auto upload_chunk_for = [&](int ch) {  // last upload chunk compute chunk ch needs
+        return std::min(nch - 1, (std::min(nz, std::min(nz, (ch + 1) * zc) + halo) - 1) / zc);
+    };
+    const int R = std::min(c->reach, halo);
+    const bool packed = R >= 3;  // >= 3 covers the degenerate-gradient fallback's stencils
+    // phi and d in mapped pinned memory: the GPU pulls the values it needs
+    // itself (transfer.cu); otherwise host threads pack them (host_pack.h)
+    static const bool zero_copy = !(std::getenv("LSR_ZERO_COPY") && std::atoi(std::getenv("LSR_ZERO_COPY")) == 0);
+    const double* phi_map = zero_copy ? mapped_ptr(phi, c->n) : nullptr;
+    const double* dist_map = zero_copy ? mapped_ptr(dist, c->n) : nullptr;
+    const bool mapped = phi_map && dist_map;
+    const int threads = host_threads();
+    static const int copy_env = std::getenv("LSR_COPY_THREADS") ? std::atoi(std::getenv("LSR_COPY_THREADS")) : 0;
+    const int copy_threads = !packed ? 0
+                             : copy_env > 0 ? std::min(copy_env, threads)
+                             : mapped       ? threads
+                                            : std::max(1, threads / 2);
+    static const bool trace = std::getenv("LSR_PIPE_TRACE") != nullptr;
+    const auto t_start = std::chrono::steady_clock::now();
+    const auto ms_since = [&] {
+        return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count();
+    };
+    // the ids (and, unpacked, phi's first chunks) go up while the host plans
     if (int st = ensure_ids(&c->active, &c->cap_active, n_active)) return st;
+    cudaEvent_t tev[4] = {};  // trace: device timeline (start, ids up, uploads done, compute done)
+    if (trace) {
+        for (auto& e : tev) LSR_CUDA_TRY(cudaEventCreate(&e));
+        LSR_CUDA_TRY(cudaEventRecord(tev[0], up));
+    }
     LSR_CUDA_TRY(cudaMemcpyAsync(c->active, active, sizeof(int64_t) * n_active, cudaMemcpyHostToDevice, up));
+    if (trace) LSR_CUDA_TRY(cudaEventRecord(tev[1], up));
     LSR_CUDA_TRY(cudaMemsetAsync(c->d_bad, 0xff, sizeof(unsigned long long), up));
     LSR_CUDA_TRY(cudaMemsetAsync(c->d_miss, 0, sizeof(unsigned long long), up));
+    // packed: chunks [0, nfull) still move phi and out whole over PCIe (the
+    // DMA engines are idle otherwise), the rest move packed values and the
+    // host threads copy phi to out for them — balancing PCIe time against
+    // host memory bandwidth. Unpacked: every chunk moves whole.
+    static const double full_env = std::getenv("LSR_PIPE_FULL") ? std::atof(std::getenv("LSR_PIPE_FULL")) : 0.35;
+    const int nfull = packed ? std::max(0, std::min(nch, static_cast<int>(std::lround(full_env * nch)))) : nch;
+    const int zfull = std::min(nz, nfull * zc);  // planes [0, zfull) move whole
+    const int prefetch = packed ? nfull : std::min(nch, 2);
+    if (prefetch)
+        LSR_CUDA_TRY(cudaMemcpyAsync(c->phi, phi, sizeof(double) * chunk_off(prefetch), cudaMemcpyHostToDevice, up));
     c->n_active = n_active;
+    c->consistent = false;
     // per-chunk ranges of the (ascending) ids
     std::vector<int64_t> first(nch + 1);
-    for (int ch = 0; ch <= nch; ++ch) {
-        const int64_t bound = static_cast<int64_t>(std::min(nz, ch * zc)) * nxy;
-        first[ch] = std::lower_bound(active, active + n_active, bound) - active;
-    }
+    for (int ch = 0; ch <= nch; ++ch) first[ch] = std::lower_bound(active, active + n_active, chunk_off(ch)) - active;
     first[nch] = n_active;
+    // packed: the host's out = phi copy starts at once on its own threads;
+    // each chunk's results are scattered into out once both its planes are
+    // copied and its results are back (event). Items run in ascending order.
+    std::unique_ptr<std::atomic<int>[]> copied(new std::atomic<int>[nz]), recorded(new std::atomic<int>[nch]),
+        gathered(new std::atomic<int>[nz]);
+    for (int k = 0; k < nz; ++k) copied[k].store(0, std::memory_order_relaxed);
+    for (int k = 0; k < nz; ++k) gathered[k].store(0, std::memory_order_relaxed);
+    for (int ch = 0; ch < nch; ++ch) recorded[ch].store(0, std::memory_order_relaxed);
+    std::atomic<int> copy_error{0};
+    std::atomic<bool> cancel{false};
+    std::atomic<int> n_copied{0};
+    double t_copied = 0.0, t_last_res = 0.0;  // trace: host copy finished, last results back
+    const bool host_copy = nfull < nch;
+    if (host_copy) {
+        if (int st = ensure_pinned(&c->h_res, &c->cap_hres, n_active)) return st;
+        if (int st = ensure_device(&c->d_res, &c->cap_dres, n_active)) return st;
+        if (!c->copy_pool || c->copy_pool->size() != copy_threads)
+            c->copy_pool.reset(new lsr_host::Pool(std::max(1, copy_threads)));
+        double* h_res = c->h_res;
+        cudaEvent_t* ev_down = c->ev_down;
+        constexpr int kParts = 8;  // scatter items per chunk, so the last chunk's scatter runs wide
+        c->copy_pool->post(nz - zfull + (nch - nfull) * kParts, [&, h_res, ev_down](int item) {
+            if (item < nz - zfull) {
+                const int k = zfull + item;
+                const long long o = static_cast<long long>(k) * nxy;
+                std::memcpy(out + o, phi + o, sizeof(double) * nxy);
+                copied[k].store(1, std::memory_order_release);
+                if (trace && ++n_copied == nz - zfull) t_copied = ms_since();
+                return;
+            }
+            const int ch = nfull + (item - (nz - zfull)) / kParts, part = (item - (nz - zfull)) % kParts;
+            for (int k = ch * zc; k < std::min(nz, (ch + 1) * zc); ++k)
+                while (!copied[k].load(std::memory_order_acquire)) std::this_thread::yield();
+            // the chunk's results: wait until this call has queued their D2H
+            while (!recorded[ch].load(std::memory_order_acquire) && !cancel.load()) std::this_thread::yield();
+            if (cancel.load()) return;
+            if (cudaEventSynchronize(ev_down[ch]) != cudaSuccess) {
+                copy_error = 1;
+                return;
+            }
+            if (trace && ch == nch - 1 && part == 0) t_last_res = ms_since();
+            const int64_t len = first[ch + 1] - first[ch];
+            const int64_t t0 = first[ch] + len * part / kParts, t1 = first[ch] + len * (part + 1) / kParts;
+            for (int64_t t = t0; t < t1; ++t) out[active[t]] = h_res[t];
+        });
+    }
+    // on every exit the host jobs (which reference this frame) are joined;
+    // on an early exit, copy items whose results were never queued give up
+    bool copy_joined = !host_copy;
+    const Finally copy_guard{[&] {
+        if (copy_joined) return;
+        cancel.store(true);
+        c->copy_pool->wait();
+    }};
+    lsr_host::StepPacker& pk = c->packer;
+    const Finally gather_guard{[&] { pk.wait(); }};
+    const long long words = lsr_bitmap_words(nx, ny, nz);
+    unsigned long long *bmA = nullptr, *bmD = nullptr, *bmB = nullptr;
+    if (mapped) {
+        // bitmaps of what the step reads; unsorted or out-of-grid ids count
+        // as misses (the chunking needs ascending ids) and rerun the step whole
+        if (int st = ensure_device(&c->bm, &c->cap_bm, 4 * words + 8)) return st;
+        bmA = c->bm;
+        bmD = c->bm + words;
+        bmB = c->bm + 2 * words;
+        LSR_CUDA_TRY(cudaMemsetAsync(c->bm + 4 * words, 0, 8 * sizeof(unsigned long long), up));
+        LSR_CUDA_TRY(launch_build_bitmaps(nx, ny, nz, c->active, n_active, packed ? R : 0, bmA, bmD, bmB,
+                                          c->bm + 3 * words, c->d_miss, up));
+        LSR_CUDA_TRY(launch_check_sorted(c->active, n_active, c->d_miss, up));
+        LSR_CUDA_TRY(launch_count_bits(nx, ny, nz, 0, nz, bmD, c->bm + 4 * words, up));
+        if (packed) LSR_CUDA_TRY(launch_count_bits(nx, ny, nz, zfull, nz, bmB, c->bm + 4 * words + 1, up));
+    } else if (!pk.plan(active, n_active, nx, ny, nz, packed ? R : 0, std::max(1, threads - copy_threads))) {
+        LSR_CUDA_TRY(cudaStreamSynchronize(up));  // the unpipelined path reuses these buffers
+        return kNotPipelined;
+    }
+    const double t_plan = ms_since();
+    const lsr_host::PackSet& dset = pk.dset();
+    const lsr_host::PackSet& pset = pk.phiset();
+    int status = LSR_OK;
+    if (!mapped) status = ensure_set(dset, c->pk_d);
+    if (status == LSR_OK && !mapped && packed) status = ensure_set(pset, c->pk_phi);
+    if (status != LSR_OK) return status;
+    if (!mapped) {
+        const lsr_cuda_ctx::Packed qd = c->pk_d, qp = c->pk_phi;
+        pk.pool().post(nz, [&, qd, qp](int k) {
+            pk.gather_plane(k, dist, qd.h_vals, qd.h_desc, packed && k >= zfull ? phi : nullptr, qp.h_vals,
+                            qp.h_desc);
+            gathered[k].store(1, std::memory_order_release);
+        });
+    }
     SlParams P = make_params(g, *cfg, energy_p);
     P.halo_miss = c->d_miss;
-    // d is read only at active nodes and their axis neighbours (the centered
-    // gradient, grid.cpp:53-74): with ascending ids, the active rows of plane
-    // k span [row(first id), row(last id)], so plane k needs the d rows of
-    // planes k-1..k+1's active spans widened by one row. Ids that are not
-    // ascending are detected on the device (check_sorted below) and force
-    // the exact fallback with a full upload of d.
-    const int nx = g.dims[0], ny = g.dims[1];
-    std::vector<int> span_lo(nz, ny), span_hi(nz, -1);
-    for (int k = 0; k < nz; ++k) {
-        const int64_t a = std::lower_bound(active, active + n_active, static_cast<int64_t>(k) * nxy) - active;
-        const int64_t b = std::lower_bound(active, active + n_active, static_cast<int64_t>(k + 1) * nxy) - active;
-        if (a < b) {
-            span_lo[k] = static_cast<int>((active[a] - static_cast<int64_t>(k) * nxy) / nx);
-            span_hi[k] = static_cast<int>((active[b - 1] - static_cast<int64_t>(k) * nxy) / nx);
-        }
-    }
-    LSR_CUDA_TRY(launch_check_sorted(c->active, n_active, c->d_miss, up));
+    if (packed) P.reach = (R - 1.5) * g.dx;
     int64_t h2d = static_cast<int64_t>(sizeof(int64_t)) * n_active;
-    for (int ch = 0; ch < nch; ++ch) {  // uploads in plane order
-        const long long o = static_cast<long long>(ch) * zc * nxy;
-        const long long cnt = static_cast<long long>(std::min(nz, (ch + 1) * zc) - ch * zc) * nxy;
-        LSR_CUDA_TRY(cudaMemcpyAsync(c->phi + o, phi + o, sizeof(double) * cnt, cudaMemcpyHostToDevice, up));
-        h2d += static_cast<int64_t>(sizeof(double)) * cnt;
-        for (int k = ch * zc; k < std::min(nz, (ch + 1) * zc); ++k) {
-            int lo = ny, hi = -1;
-            for (int kk = std::max(0, k - 1); kk <= std::min(nz - 1, k + 1); ++kk) {
-                lo = std::min(lo, span_lo[kk]);
-                hi = std::max(hi, span_hi[kk]);
-            }
-            if (hi < lo) continue;
-            lo = std::max(0, lo - 1);
-            hi = std::min(ny - 1, hi + 1);
-            const long long ro = static_cast<long long>(k) * nxy + static_cast<long long>(lo) * nx;
-            LSR_CUDA_TRY(cudaMemcpyAsync(c->dist + ro, dist + ro, sizeof(double) * (hi - lo + 1) * nx,
-                                         cudaMemcpyHostToDevice, up));
-            h2d += static_cast<int64_t>(sizeof(double)) * (hi - lo + 1) * nx;
-        }
-        LSR_CUDA_TRY(cudaMemcpyAsync(c->out + o, c->phi + o, sizeof(double) * cnt, cudaMemcpyDeviceToDevice, up));
-        LSR_CUDA_TRY(cudaEventRecord(c->ev_up[ch], up));
-    }
-    for (int ch = 0; ch < nch; ++ch) {
+    int scattered = 0;  // chunks whose packed runs are in place on the device
+    int computed = 0;   // chunks whose kernel is issued
+    const auto issue_compute = [&](int ch) -> int {
         const int z0 = ch * zc, z1 = std::min(nz, (ch + 1) * zc);
-        const int need = std::min(nz, z1 + halo);           // planes that must be resident
-        const int up_ch = std::min(nch - 1, (need - 1) / zc);  // last upload chunk needed
+        const int up_ch = upload_chunk_for(ch);
         LSR_CUDA_TRY(cudaStreamWaitEvent(cmp, c->ev_up[up_ch], 0));
+        for (; !mapped && scattered <= up_ch; ++scattered) {
+            const int s0 = scattered * zc, s1 = std::min(nz, (scattered + 1) * zc);
+            LSR_CUDA_TRY(launch_scatter_runs(c->pk_d.d_vals, c->pk_d.d_desc, dset.runs_before(s0),
+                                             dset.runs_before(s1), dset.values_before(s1), c->dist, cmp));
+            if (scattered >= nfull)
+                LSR_CUDA_TRY(launch_scatter_runs(c->pk_phi.d_vals, c->pk_phi.d_desc, pset.runs_before(s0),
+                                                 pset.runs_before(s1), pset.values_before(s1), c->phi, cmp));
+        }
         P.z_base = 0;
         P.z_planes = std::min(nz, (up_ch + 1) * zc);
         P.own_lo = z0;
         P.own_hi = z1;
         const long long n = first[ch + 1] - first[ch];
         LSR_CUDA_TRY(launch_sl_step(P, cfg->interp, c->phi, c->dist, c->active + first[ch], n, c->out, c->d_bad, cmp));
+        const bool whole = ch < nfull;
+        if (!whole) LSR_CUDA_TRY(launch_gather_ids(c->out, c->active + first[ch], n, c->d_res + first[ch], cmp));
         LSR_CUDA_TRY(cudaEventRecord(c->ev_cmp[ch], cmp));
         LSR_CUDA_TRY(cudaStreamWaitEvent(down, c->ev_cmp[ch], 0));
-        const long long o = static_cast<long long>(z0) * nxy, cnt = static_cast<long long>(z1 - z0) * nxy;
-        LSR_CUDA_TRY(cudaMemcpyAsync(out + o, c->out + o, sizeof(double) * cnt, cudaMemcpyDeviceToHost, down));
+        if (!whole) {
+            if (n > 0)
+                LSR_CUDA_TRY(cudaMemcpyAsync(c->h_res + first[ch], c->d_res + first[ch], sizeof(double) * n,
+                                             cudaMemcpyDeviceToHost, down));
+            LSR_CUDA_TRY(cudaEventRecord(c->ev_down[ch], down));
+            recorded[ch].store(1, std::memory_order_release);
+        } else {
+            const long long o = chunk_off(ch), cnt = chunk_off(ch + 1) - o;
+            LSR_CUDA_TRY(cudaMemcpyAsync(out + o, c->out + o, sizeof(double) * cnt, cudaMemcpyDeviceToHost, down));
+        }
+        return LSR_OK;
+    };
+    const auto issue_upload = [&](int ch) -> int {
+        const int z0 = ch * zc, z1 = std::min(nz, (ch + 1) * zc);
+        const long long o = chunk_off(ch), cnt = chunk_off(ch + 1) - o;
+        const bool whole = ch < nfull;
+        if (whole && ch >= prefetch)
+            LSR_CUDA_TRY(cudaMemcpyAsync(c->phi + o, phi + o, sizeof(double) * cnt, cudaMemcpyHostToDevice, up));
+        if (whole) h2d += static_cast<int64_t>(sizeof(double)) * cnt;
+        if (mapped) {
+            LSR_CUDA_TRY(launch_pull_planes(nx, ny, nz, z0, z1, bmD, dist_map, c->dist, whole ? nullptr : bmB, phi_map,
+                                            c->phi, up));
+        } else {
+            for (int k = z0; k < z1; ++k)
+                while (!gathered[k].load(std::memory_order_acquire)) std::this_thread::yield();
+            if (int st = upload_set(dset, c->pk_d, z0, z1, up, &h2d)) return st;
+            if (!whole)
+                if (int st = upload_set(pset, c->pk_phi, z0, z1, up, &h2d)) return st;
+        }
+        if (whole)
+            LSR_CUDA_TRY(cudaMemcpyAsync(c->out + o, c->phi + o, sizeof(double) * cnt, cudaMemcpyDeviceToDevice, up));
+        LSR_CUDA_TRY(cudaEventRecord(c->ev_up[ch], up));
+        return LSR_OK;
+    };
+    for (int ch = 0; ch < nch && status == LSR_OK; ++ch) {  // uploads in plane order
+        status = issue_upload(ch);
+        // compute every chunk whose planes (plus the halo) are now queued
+        while (status == LSR_OK && computed < nch && upload_chunk_for(computed) <= ch)
+            status = issue_compute(computed++);
     }
+    pk.wait();
+    if (trace && status == LSR_OK) {
+        cudaEventRecord(tev[2], up);
+        cudaEventRecord(tev[3], cmp);
+    }
+    const double t_issued = ms_since();
+    if (status != LSR_OK) return status;
     unsigned long long h[2] = {0, 0};
     LSR_CUDA_TRY(cudaStreamSynchronize(down));
     LSR_CUDA_TRY(cudaStreamSynchronize(cmp));
+    if (host_copy) c->copy_pool->wait();
+    copy_joined = true;
+    if (copy_error) return set_err(LSR_ERR_CUDA, "sl_step: result download failed");
+    if (trace) {
+        float ms[3] = {0, 0, 0};
+        for (int i = 0; i < 3; ++i) cudaEventElapsedTime(&ms[i], tev[0], tev[i + 1]);
+        std::fprintf(stderr, "[lsr pipe] device: ids up %.2f ms, uploads done %.2f ms, compute done %.2f ms\n", ms[0],
+                     ms[1], ms[2]);
+        for (auto& e : tev) cudaEventDestroy(e);
+    }
+    if (trace)
+        std::fprintf(stderr,
+                     "[lsr pipe] %s, whole chunks %d/%d, threads %d+%d reach %d plan %.2f ms, issued %.2f ms, copied %.2f ms, last results "
+                     "%.2f ms, done %.2f ms; d %lld values %lld runs, phi %lld values %lld runs\n",
+                     mapped ? "zero-copy" : "host-packed", nfull, nch, std::max(1, threads - copy_threads), copy_threads, packed ? R : 0, t_plan, t_issued, t_copied,
+                     t_last_res, ms_since(),
+                     static_cast<long long>(mapped ? 0 : dset.total_values()),
+                     static_cast<long long>(mapped ? 0 : dset.total_runs()),
+                     static_cast<long long>(packed && !mapped ? pset.total_values() : 0),
+                     static_cast<long long>(packed && !mapped ? pset.total_runs() : 0));
     LSR_CUDA_TRY(cudaMemcpy(&h[0], c->d_miss, sizeof(unsigned long long), cudaMemcpyDeviceToHost));
     LSR_CUDA_TRY(cudaMemcpy(&h[1], c->d_bad, sizeof(unsigned long long), cudaMemcpyDeviceToHost));
-    c->consistent = false;
-    if (h[0] != 0) {  // rerun unpipelined with the whole of d resident
+    if (mapped) {  // values pulled over PCIe
+        unsigned long long cnt[2] = {0, 0};
+        LSR_CUDA_TRY(cudaMemcpy(cnt, c->bm + 4 * words, sizeof cnt, cudaMemcpyDeviceToHost));
+        h2d += static_cast<int64_t>(sizeof(double)) * static_cast<int64_t>(cnt[0] + cnt[1]);
+    }
+    if (h[0] != 0) {  // rerun unpipelined with phi and d whole
+        LSR_CUDA_TRY(cudaMemcpyAsync(c->phi, phi, sizeof(double) * c->n, cudaMemcpyHostToDevice, up));
         LSR_CUDA_TRY(cudaMemcpyAsync(c->dist, dist, sizeof(double) * c->n, cudaMemcpyHostToDevice, up));
-        P.halo_miss = nullptr;
-        P.z_base = 0;
-        P.z_planes = nz;
+        LSR_CUDA_TRY(cudaMemcpyAsync(c->out, c->phi, sizeof(double) * c->n, cudaMemcpyDeviceToDevice, up));
+        P = make_params(g, *cfg, energy_p);
         LSR_CUDA_TRY(cudaMemsetAsync(c->d_bad, 0xff, sizeof(unsigned long long), up));
         LSR_CUDA_TRY(launch_sl_step(P, cfg->interp, c->phi, c->dist, c->active, n_active, c->out, c->d_bad, up));
         LSR_CUDA_TRY(cudaMemcpyAsync(out, c->out, sizeof(double) * c->n, cudaMemcpyDeviceToHost, up));
         LSR_CUDA_TRY(cudaMemcpyAsync(&h[1], c->d_bad, sizeof(unsigned long long), cudaMemcpyDeviceToHost, up));
         LSR_CUDA_TRY(cudaStreamSynchronize(up));
         c->pipeline_fallbacks++;
-        h2d += static_cast<int64_t>(sizeof(double)) * c->n;
+        // the feet reach beyond the packed ball: widen it for the next calls
+        c->reach = std::min(halo, c->reach + 3);
+        h2d += 2 * static_cast<int64_t>(sizeof(double)) * c->n;
     }
     g_h2d_bytes = h2d;
-    g_d2h_bytes = static_cast<int64_t>(sizeof(double)) * c->n * (h[0] != 0 ? 2 : 1);
+    g_d2h_bytes = static_cast<int64_t>(sizeof(double)) * (n_active - first[nfull] + chunk_off(nfull)) +
+                  (h[0] != 0 ? static_cast<int64_t>(sizeof(double)) * c->n : 0);
     if (h[1] != ~0ULL) return numerical_error(g, h[1], bad_node);
+    return LSR_OK;
+}
+
+int lsr_cuda_pack_host(const lsr_grid* grid, const int64_t* active, int64_t n_active, int32_t reach,
+                       const double* dist, const double* phi, double* dist_field, double* phi_field,
+                       int64_t* counts) {
+    if (int st = check_grid(grid)) return st;
+    if (grid->dim != 3 || !dist || !dist_field || (n_active > 0 && !active) || reach < 0 ||
+        (reach > 0 && (!phi || !phi_field)))
+        return set_err(LSR_ERR_CONFIG, "pack_host: needs a 3d grid and non-null buffers");
+    lsr_host::StepPacker pk;
+    if (!pk.plan(active, n_active, grid->dims[0], grid->dims[1], grid->dims[2], reach, host_threads()))
+        return set_err(LSR_ERR_CONFIG, "pack_host: ids are not ascending inside the grid");
+    const lsr_host::PackSet& ds = pk.dset();
+    const lsr_host::PackSet& ps = pk.phiset();
+    std::vector<double> dv(ds.total_values()), pv(reach > 0 ? ps.total_values() : 0);
+    std::vector<lsr_host::RunDesc> dd(ds.total_runs()), pd(reach > 0 ? ps.total_runs() : 0);
+    for (int k = 0; k < grid->dims[2]; ++k) pk.gather_plane(k, dist, dv.data(), dd.data(), phi, pv.data(), pd.data());
+    const auto scatter = [](const std::vector<double>& v, const std::vector<lsr_host::RunDesc>& d, double* f) {
+        for (size_t r = 0; r < d.size(); ++r) {
+            const int64_t end = r + 1 < d.size() ? d[r + 1].src : static_cast<int64_t>(v.size());
+            std::memcpy(f + d[r].dst, v.data() + d[r].src, sizeof(double) * (end - d[r].src));
+        }
+    };
+    scatter(dv, dd, dist_field);
+    if (reach > 0) scatter(pv, pd, phi_field);
+    if (counts) {
+        counts[0] = ds.total_values();
+        counts[1] = ds.total_runs();
+        counts[2] = reach > 0 ? ps.total_values() : 0;
+        counts[3] = reach > 0 ? ps.total_runs() : 0;
+    }
     return LSR_OK;
 }
 

@@ -29,3 +29,12 @@ cudaError_t launch_resync(const double* phi, double* out, const int64_t* ids, lo
 
 cudaError_t launch_div_selftest(double c, double rc, unsigned long long seed, long long n,
                                 unsigned long long* mismatches);
+
+// field[desc[r].dst + l] = packed[desc[r].src + l] for the runs r in [r0, r1)
+// (desc = (dst, src) pairs; a run ends where the next begins, the last at vend)
+cudaError_t launch_scatter_runs(const double* packed, const long long* desc, long long r0, long long r1,
+                                long long vend, double* field, cudaStream_t stream);
+
+// res[t] = field[ids[t]] for t < n
+cudaError_t launch_gather_ids(const double* field, const int64_t* ids, long long n, double* res,
+                              cudaStream_t stream);

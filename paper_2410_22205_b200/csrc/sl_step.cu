@@ -10,6 +10,7 @@
 // L1 and coalesce into few sectors per warp load.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 
 #include "sl_device.cuh"
@@ -102,9 +103,47 @@ __global__ void div_selftest_kernel(double c, double rc, unsigned long long seed
     if (bad) atomicAdd(mismatches, bad);
 }
 
+// one warp per run of packed values (host_pack.h)
+__global__ void scatter_runs_kernel(const double* __restrict__ packed, const long long* __restrict__ desc,
+                                    long long r0, long long r1, long long vend, double* __restrict__ field) {
+    const long long nw = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    for (long long r = r0 + ((static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5); r < r1;
+         r += nw) {
+        const long long dst = desc[2 * r], src = desc[2 * r + 1];
+        const long long len = (r + 1 < r1 ? desc[2 * r + 3] : vend) - src;
+        for (long long l = lane; l < len; l += 32) field[dst + l] = packed[src + l];
+    }
+}
+
+// res[t] = field[ids[t]]: the updated values of one chunk, packed for the D2H
+__global__ void gather_ids_kernel(const double* __restrict__ field, const int64_t* __restrict__ ids, long long n,
+                                  double* __restrict__ res) {
+    const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t < n) res[t] = field[ids[t]];
+}
+
 }  // namespace lsr_dev
 
 using namespace lsr_dev;
+
+cudaError_t launch_gather_ids(const double* field, const int64_t* ids, long long n, double* res,
+                              cudaStream_t stream) {
+    if (n <= 0) return cudaSuccess;
+    gather_ids_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, stream>>>(field, ids, n, res);
+    lsr_note_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_scatter_runs(const double* packed, const long long* desc, long long r0, long long r1,
+                                long long vend, double* field, cudaStream_t stream) {
+    if (r1 <= r0) return cudaSuccess;
+    const long long warps = r1 - r0;
+    const unsigned blocks = static_cast<unsigned>(std::min<long long>((warps + 7) / 8, 148LL * 16));
+    scatter_runs_kernel<<<blocks, 256, 0, stream>>>(packed, desc, r0, r1, vend, field);
+    lsr_note_launch();
+    return cudaGetLastError();
+}
 
 cudaError_t launch_div_selftest(double c, double rc, unsigned long long seed, long long n,
                                 unsigned long long* mismatches) {

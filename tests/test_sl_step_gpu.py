@@ -23,8 +23,20 @@ def _cfg(lsr, rec, c):
                           interp=lsr.InterpolatorKind(int(rec["case_interp"][c])), band=bp)
 
 
-def _run(lsr, g, phi, dist, active, cfg, e):
-    out = lsr.ScalarField(g)
+def _pinned(a):
+    import torch
+
+    t = torch.empty(a.size, dtype=torch.float64 if a.dtype == np.float64 else torch.int64, pin_memory=True).numpy()
+    t[:] = a
+    return t
+
+
+def _run(lsr, g, phi, dist, active, cfg, e, pinned=False):
+    """One one-shot step; pinned=True hands over page-locked host buffers (the
+    zero-copy pull path of lsr_cuda_sl_step_host), else pageable ones."""
+    if pinned:
+        phi, dist, active = _pinned(phi), _pinned(dist), _pinned(active)
+    out = lsr.ScalarField(g, _pinned(np.zeros(g.num_nodes())) if pinned else None)
     lsr.sl_step(lsr.ScalarField(g, phi), lsr.DistanceField(lsr.ScalarField(g, dist)), lsr.BandMask(g, active=active),
                 cfg, e, out)
     return out.values
@@ -221,11 +233,13 @@ def test_full_size_sampled_subset_512(gpu, oracle):
     assert np.max(np.abs(out[band] - phi[band])) < 2 * g.dx
 
 
-@pytest.mark.parametrize("case", ["sorted", "unsorted", "far_feet"])
-def test_pipelined_host_entry_exact(gpu, oracle, case):
+@pytest.mark.parametrize("pinned", [False, True], ids=["pageable", "pinned"])
+@pytest.mark.parametrize("case", ["sorted", "unsorted", "far_feet", "scattered", "edge_planes"])
+def test_pipelined_host_entry_exact(gpu, oracle, case, pinned):
     """The one-shot host entry pipelines 3d grids over z-chunks (slab-mode
-    kernels, three streams); unsorted ids or feet beyond the upload lead must
-    fall back to the unpipelined step and stay exact."""
+    kernels, three streams) and uploads only the d values the gradients read
+    (packed row runs); unsorted ids or feet beyond the upload lead must fall
+    back to the unpipelined step and stay exact."""
     lsr = gpu
     rng = np.random.default_rng(5)
     g = lsr._api.cube_grid(96, 3)
@@ -241,8 +255,19 @@ def test_pipelined_host_entry_exact(gpu, oracle, case):
         rng.shuffle(active)
     if case == "far_feet":
         dt = 6.0 * g.dx  # displacements of several planes: beyond the pipeline's upload lead
+    if case == "scattered":  # isolated ids: one-node runs, neighbours in other rows/planes
+        active = np.sort(rng.choice(active, active.size // 9, replace=False)).astype(np.int64)
+    if case == "edge_planes":  # the band plus the grid's outer faces (one-sided gradients)
+        n = g.dims[0]
+        kk, jj, ii = np.unravel_index(np.arange(x.size), (n, n, n))
+        face = (ii == 0) | (jj == 0) | (kk == 0) | (ii == n - 1) | (jj == n - 1) | (kk == n - 1)
+        active = np.union1d(active, np.flatnonzero(face & (rng.random(x.size) < 0.3))).astype(np.int64)
     cfg = lsr.StepConfig(p=2, delta=1.0, dt=dt, band=bp)
-    got = _run(lsr, g, phi, dist, active, cfg, e)
+    got = _run(lsr, g, phi, dist, active, cfg, e, pinned)
+    if case in ("sorted", "scattered"):  # packed transfers: phi around the band in, the band's values out
+        h2d, d2h = lsr._api.last_transfer_bytes()
+        assert d2h >= 8 * active.size
+        assert case != "sorted" or (h2d < 8 * x.size and d2h < 8 * x.size)
     ref, st, _ = oracle.sl_step(dict(dim=3, dims=g.dims, origin=g.origin, dx=g.dx), phi, dist, active,
                                 dict(p=2, interp=1, delta=1.0, dt=dt, fallback_c=1e-3, fallback_alpha=1.0,
                                      gamma=bp.gamma, beta=bp.beta), e)
