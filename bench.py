@@ -474,7 +474,9 @@ def measure_e2e(lsr, g, phi, ctx, active, step, e2, args):
     lsr.lib().lsr_cuda_last_transfer_bytes(C.byref(h2d), C.byref(d2h))  # what the call actually copied
     return {"value": active.size / t, "unit": UNIT, "h2d_bytes_per_step": int(h2d.value),
             "d2h_bytes_per_step": int(d2h.value), "ms_per_step": t * 1e3,
-            "timing": "host clock around the synchronous call (pinned host buffers: phi, d, ids in; out back)",
+            "timing": "host clock around the synchronous call lsr.sl_step on pinned host buffers (phi, d, ids in, "
+                      "out back): the GPU pulls the phi/d values the step reads (zero-copy) plus 1/8 of the planes "
+                      "whole (DMA), returns the updated values, host threads copy phi to out and scatter them",
             "steps": args.e2e_steps}
 
 

@@ -4,7 +4,42 @@
 #include <algorithm>
 #include <cstring>
 
+#if defined(__SSE2__)
+#include <emmintrin.h>
+#endif
+
 namespace lsr_host {
+
+void copy_stream(void* dst, const void* src, size_t bytes) {
+#if defined(__SSE2__)
+    auto* d = static_cast<unsigned char*>(dst);
+    auto* s = static_cast<const unsigned char*>(src);
+    const size_t head = (16 - (reinterpret_cast<uintptr_t>(d) & 15)) & 15;
+    if (bytes < head + 64) {
+        std::memcpy(d, s, bytes);
+        return;
+    }
+    std::memcpy(d, s, head);
+    d += head;
+    s += head;
+    bytes -= head;
+    const size_t body = bytes & ~static_cast<size_t>(63);
+    for (size_t i = 0; i < body; i += 64) {
+        const __m128i a = _mm_loadu_si128(reinterpret_cast<const __m128i*>(s + i));
+        const __m128i b = _mm_loadu_si128(reinterpret_cast<const __m128i*>(s + i + 16));
+        const __m128i c = _mm_loadu_si128(reinterpret_cast<const __m128i*>(s + i + 32));
+        const __m128i e = _mm_loadu_si128(reinterpret_cast<const __m128i*>(s + i + 48));
+        _mm_stream_si128(reinterpret_cast<__m128i*>(d + i), a);
+        _mm_stream_si128(reinterpret_cast<__m128i*>(d + i + 16), b);
+        _mm_stream_si128(reinterpret_cast<__m128i*>(d + i + 32), c);
+        _mm_stream_si128(reinterpret_cast<__m128i*>(d + i + 48), e);
+    }
+    _mm_sfence();
+    std::memcpy(d + body, s + body, bytes - body);
+#else
+    std::memcpy(dst, src, bytes);
+#endif
+}
 
 Pool::Pool(int threads) {
     for (int t = 0; t < std::max(1, threads); ++t) workers_.emplace_back([this] { loop(); });

@@ -14,6 +14,7 @@
 
 #include <atomic>
 #include <condition_variable>
+#include <cstddef>
 #include <cstdint>
 #include <functional>
 #include <memory>
@@ -50,6 +51,11 @@ class Pool {
     uint64_t gen_ = 0;
     bool stop_ = false;
 };
+
+// dst = src for `bytes` bytes with streaming (non-temporal) stores where the
+// CPU has them: the destination is not read first and does not evict the
+// cache, which matters when host memory bandwidth is the bound
+void copy_stream(void* dst, const void* src, size_t bytes);
 
 // one run of consecutive nodes on a grid row: node ids [dst, dst + len)
 // live at packed[src, src + len). len is implied by the next run's src.

@@ -623,7 +623,7 @@ static int sl_step_host_pipelined(lsr_cuda_ctx* c, const double* phi, const doub
     // DMA engines are idle otherwise), the rest move packed values and the
     // host threads copy phi to out for them — balancing PCIe time against
     // host memory bandwidth. Unpacked: every chunk moves whole.
-    static const double full_env = std::getenv("LSR_PIPE_FULL") ? std::atof(std::getenv("LSR_PIPE_FULL")) : 0.35;
+    static const double full_env = std::getenv("LSR_PIPE_FULL") ? std::atof(std::getenv("LSR_PIPE_FULL")) : 0.125;
     const int nfull = packed ? std::max(0, std::min(nch, static_cast<int>(std::lround(full_env * nch)))) : nch;
     const int zfull = std::min(nz, nfull * zc);  // planes [0, zfull) move whole
     const int prefetch = packed ? nfull : std::min(nch, 2);
@@ -660,7 +660,7 @@ static int sl_step_host_pipelined(lsr_cuda_ctx* c, const double* phi, const doub
             if (item < nz - zfull) {
                 const int k = zfull + item;
                 const long long o = static_cast<long long>(k) * nxy;
-                std::memcpy(out + o, phi + o, sizeof(double) * nxy);
+                lsr_host::copy_stream(out + o, phi + o, sizeof(double) * nxy);
                 copied[k].store(1, std::memory_order_release);
                 if (trace && ++n_copied == nz - zfull) t_copied = ms_since();
                 return;

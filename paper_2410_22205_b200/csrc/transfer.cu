@@ -103,22 +103,36 @@ __global__ void ball_pass(Bits b, int axis, int R, const unsigned long long* __r
 }
 
 // zero-copy pull of planes [z0, z1): dst[n] = src[n] where the node's bit is
-// set (one thread per node: a warp reads consecutive x, so the PCIe reads of
-// a run coalesce); two fields at once
+// set, two fields at once. One warp per 64-node bitmap word: lane l moves
+// nodes 2l and 2l+1 with one 16-byte load when both are set, so a warp's
+// reads of a run are contiguous and wide; empty words are skipped whole.
+__device__ __forceinline__ void pull_pair(unsigned long long word, int l, const double* __restrict__ src,
+                                          double* __restrict__ dst, long long n) {
+    const unsigned pair = static_cast<unsigned>(word >> (2 * l)) & 3u;
+    if (pair == 3u && ((n & 1) == 0)) {
+        *reinterpret_cast<double2*>(dst + n) = *reinterpret_cast<const double2*>(src + n);
+    } else {
+        if (pair & 1u) dst[n] = src[n];
+        if (pair & 2u) dst[n + 1] = src[n + 1];
+    }
+}
+
 __global__ void pull_planes(Bits b, int z0, int z1, const unsigned long long* __restrict__ bm_a,
                             const double* __restrict__ src_a, double* __restrict__ dst_a,
                             const unsigned long long* __restrict__ bm_b, const double* __restrict__ src_b,
                             double* __restrict__ dst_b) {
-    const long long nxy = static_cast<long long>(b.nx) * b.ny;
-    const long long n0 = z0 * nxy, n1 = z1 * nxy;
-    for (long long n = n0 + static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; n < n1;
-         n += static_cast<long long>(gridDim.x) * blockDim.x) {
-        const long long jk = n / b.nx;
-        const int x = static_cast<int>(n - jk * b.nx);
-        const long long wi = jk * b.W + (x >> 6);
-        const unsigned long long bit = 1ULL << (x & 63);
-        if (bm_a && (bm_a[wi] & bit)) dst_a[n] = src_a[n];
-        if (bm_b && (bm_b[wi] & bit)) dst_b[n] = src_b[n];
+    const long long w0 = static_cast<long long>(z0) * b.ny * b.W, w1 = static_cast<long long>(z1) * b.ny * b.W;
+    const int l = threadIdx.x & 31;
+    const long long nw = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
+    for (long long w = w0 + ((static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5); w < w1; w += nw) {
+        const unsigned long long wa = bm_a ? bm_a[w] : 0ULL, wb = bm_b ? bm_b[w] : 0ULL;
+        if ((wa | wb) == 0ULL) continue;
+        const long long r = w / b.W;
+        const int x0 = static_cast<int>(w - r * b.W) << 6;
+        const long long n = r * b.nx + x0 + 2 * l;  // rows are unpadded in the fields
+        if (x0 + 2 * l >= b.nx) continue;
+        if (wa) pull_pair(wa, l, src_a, dst_a, n);
+        if (wb) pull_pair(wb, l, src_b, dst_b, n);
     }
 }
 
@@ -172,8 +186,8 @@ cudaError_t launch_pull_planes(int nx, int ny, int nz, int z0, int z1, const uns
                                const double* src_b, double* dst_b, cudaStream_t s) {
     if (z1 <= z0) return cudaSuccess;
     const Bits b{nx, ny, nz, (nx + 63) / 64};
-    const long long nodes = static_cast<long long>(z1 - z0) * nx * ny;
-    pull_planes<<<grid_for(nodes, 256), 256, 0, s>>>(b, z0, z1, bm_a, src_a, dst_a, bm_b, src_b, dst_b);
+    const long long warps = static_cast<long long>(z1 - z0) * ny * b.W;
+    pull_planes<<<grid_for(32 * warps, 256), 256, 0, s>>>(b, z0, z1, bm_a, src_a, dst_a, bm_b, src_b, dst_b);
     lsr_note_launch();
     return cudaGetLastError();
 }
