@@ -20,6 +20,8 @@
 
 #include <cub/cub.cuh>
 
+#include "compact.cuh"
+
 #include <cmath>
 #include <cstdint>
 #include <cstring>
@@ -124,26 +126,29 @@ __global__ void one_step(SlParams P, const double* __restrict__ prev, double* __
     const long long id = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
     bool is_zero = false, is_frozen = false;
     if (id < n) {
+        int i, j, k;
+        lsr_dev::unflatten(P, id, i, j, k);
+        // the node and its six neighbours are loaded up front (an absent
+        // neighbour reads the node itself and is skipped below), so the seven
+        // loads are in flight together
+        const bool has[6] = {i > 0, i + 1 < P.nx, j > 0, j + 1 < P.ny, P.dim == 3 && k > 0, P.dim == 3 && k + 1 < P.nz};
+        const long long st[3] = {1, P.nx, P.nxy};
+        double v[6];
+#pragma unroll
+        for (int q = 0; q < 6; ++q) v[q] = __ldg(prev + (has[q] ? id + ((q & 1) ? st[q >> 1] : -st[q >> 1]) : id));
         const double pj = __ldg(prev + id);
         double val = pj;
         if (pj == 0.0) {
             is_zero = true;
         } else {
-            int i, j, k;
-            lsr_dev::unflatten(P, id, i, j, k);
-            const int ijk[3] = {i, j, k};
-            const int nn[3] = {P.nx, P.ny, P.nz};
-            const long long st[3] = {1, P.nx, P.nxy};
             double best = -1.0;
-            for (int ax = 0; ax < P.dim; ++ax) {
-                for (int s = -1; s <= 1; s += 2) {
-                    const int c = ijk[ax] + s;
-                    if (c < 0 || c >= nn[ax]) continue;
-                    const double pk = __ldg(prev + id + s * st[ax]);
-                    if (pj * pk >= 0.0) continue;
-                    const double crossing = P.dx * fabs(pj) / (fabs(pj) + fabs(pk));
-                    best = best < 0.0 ? crossing : smin(best, crossing);
-                }
+#pragma unroll
+            for (int q = 0; q < 6; ++q) {  // axes x, y, z; -1 before +1 (reinit.cpp:30-41)
+                if (!has[q]) continue;
+                const double pk = v[q];
+                if (pj * pk >= 0.0) continue;
+                const double crossing = P.dx * fabs(pj) / (fabs(pj) + fabs(pk));
+                best = best < 0.0 ? crossing : smin(best, crossing);
             }
             if (best >= 0.0) {
                 val = pj > 0.0 ? best : -best;
@@ -160,9 +165,14 @@ __global__ void one_step(SlParams P, const double* __restrict__ prev, double* __
     }
 }
 
-struct NotFrozen {  // tube ids that were not frozen by the one-step (reinit.cpp:94-98)
+struct NotFrozen {  // tube entries t whose node was not frozen by the one-step (reinit.cpp:94-98)
     const unsigned char* frozen;
-    __device__ bool operator()(long long id) const { return !frozen[id]; }
+    const long long* tube;
+    __device__ bool operator()(long long t) const { return !frozen[tube[t]]; }
+};
+struct TubeId {
+    const long long* tube;
+    __device__ long long operator()(long long t) const { return tube[t]; }
 };
 
 // smoothed sign at entry (reinit.cpp:250-257)
@@ -355,13 +365,11 @@ int lsr_band_build(const SlParams& P, const double* phi, double gamma, BandBuffe
     lsr_note_launch();
     lsr_note_launch();
     if (P.dim == 3) lsr_note_launch();
-    cub::CountingInputIterator<long long> ids(0);
-    size_t b1 = 0, b2 = 0;
-    BR_TRY(cub::DeviceSelect::If(nullptr, b1, ids, B.active, B.counts, n, IsActive{B.state}, s));
-    BR_TRY(cub::DeviceSelect::If(nullptr, b2, ids, B.tube, B.counts + 1, n, InTube{B.state}, s));
-    if (int st = ensure_tmp(B, b1 > b2 ? b1 : b2, err)) return st;
-    BR_TRY(cub::DeviceSelect::If(B.tmp, b1, ids, B.active, B.counts, n, IsActive{B.state}, s));
-    BR_TRY(cub::DeviceSelect::If(B.tmp, b2, ids, B.tube, B.counts + 1, n, InTube{B.state}, s));
+    const size_t tb = lsr_compact::scratch_bytes(n);
+    if (int st = ensure_tmp(B, tb, err)) return st;
+    BR_TRY(lsr_compact::compact(IsActive{B.state}, lsr_compact::Identity{}, n, B.active, B.counts, B.tmp, tb, s));
+    BR_TRY(lsr_compact::compact(InTube{B.state}, lsr_compact::Identity{}, n, B.tube, B.counts + 1, B.tmp, tb, s));
+    for (int q = 0; q < 4; ++q) lsr_note_launch();
     long long h[2];
     BR_TRY(cudaMemcpyAsync(h, B.counts, sizeof h, cudaMemcpyDeviceToHost, s));
     BR_TRY(cudaStreamSynchronize(s));
@@ -446,14 +454,16 @@ int lsr_reinitialize(const SlParams& P, double** phi, double** scratch, const Ba
     // nodes = tube minus frozen, ascending (reinit.cpp:94-98)
     size_t tb = 0;
     long long* d_nn = reinterpret_cast<long long*>(W.scal + 2);
-    BR_TRY(cub::DeviceSelect::If(nullptr, tb, B.tube, W.nodes, d_nn, B.n_tube, NotFrozen{W.frozen}, s));
+    tb = lsr_compact::scratch_bytes(B.n_tube);
     if (tb > W.tmp_bytes) {
         cudaFree(W.tmp);
         W.tmp = nullptr;
         BR_TRY(cudaMalloc(&W.tmp, tb));
         W.tmp_bytes = tb;
     }
-    BR_TRY(cub::DeviceSelect::If(W.tmp, tb, B.tube, W.nodes, d_nn, B.n_tube, NotFrozen{W.frozen}, s));
+    BR_TRY(lsr_compact::compact(NotFrozen{W.frozen, B.tube}, TubeId{B.tube}, B.n_tube, W.nodes, d_nn, W.tmp, tb, s));
+    lsr_note_launch();
+    lsr_note_launch();
     long long nn = 0;
     BR_TRY(cudaMemcpyAsync(&nn, d_nn, sizeof nn, cudaMemcpyDeviceToHost, s));
     BR_TRY(cudaStreamSynchronize(s));

@@ -20,6 +20,8 @@
 
 #include <cub/cub.cuh>
 
+#include "compact.cuh"
+
 #include <cmath>
 #include <mutex>
 #include <cstdint>
@@ -162,14 +164,28 @@ __global__ void contrib_2d(SlParams P, const double* __restrict__ phi, const dou
 }
 
 // blocked_sum's in-block serial sums (parallel.hpp:31-37)
+// blocked_sum's per-block partials (parallel.hpp:39-40): one CTA per block
+// of 4096 contributions stages them through shared memory with coalesced
+// loads, then one thread adds them in index order (the reference's order)
+struct CellFlag {
+    const unsigned char* flags;
+    __device__ bool operator()(long long c) const { return flags[c] != 0; }
+};
+struct CellId {  // cell ids fit int (cub's item count, as before)
+    __device__ int operator()(long long c) const { return static_cast<int>(c); }
+};
+
 __global__ void block_partials(const double* __restrict__ contrib, long long n, double* __restrict__ partial) {
-    const long long b = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-    const long long lo = b * 4096;
-    if (lo >= n) return;
-    const long long hi = min(n, lo + 4096);
-    double s = 0.0;
-    for (long long i = lo; i < hi; ++i) s += contrib[i];
-    partial[b] = s;
+    __shared__ double buf[4096];
+    const long long lo = static_cast<long long>(blockIdx.x) * 4096;
+    const int len = static_cast<int>(min(n - lo, 4096LL));
+    for (int t = threadIdx.x; t < len; t += blockDim.x) buf[t] = contrib[lo + t];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double s = 0.0;
+        for (int t = 0; t < len; ++t) s += buf[t];
+        partial[blockIdx.x] = s;
+    }
 }
 
 }  // namespace
@@ -222,9 +238,7 @@ int lsr_prep_surface_energy(const SlParams& P, const double* phi, const double* 
     const int T = 256;
     flag_cells<<<static_cast<unsigned>((ncells + T - 1) / T), T, 0, s>>>(P, phi, ncells, W.flags);
     lsr_note_launch();
-    cub::CountingInputIterator<int> ids(0);
-    size_t tb = 0;
-    EN_TRY(cub::DeviceSelect::Flagged(nullptr, tb, ids, W.flags, W.cells, W.scal, static_cast<int>(ncells), s));
+    const size_t tb = lsr_compact::scratch_bytes(ncells) + sizeof(long long);
     if (tb > W.tmp_bytes) {
         cudaFree(W.tmp);
         W.tmp = nullptr;
@@ -232,9 +246,14 @@ int lsr_prep_surface_energy(const SlParams& P, const double* phi, const double* 
         EN_TRY(cudaMalloc(&W.tmp, tb));
         W.tmp_bytes = tb;
     }
-    EN_TRY(cub::DeviceSelect::Flagged(W.tmp, tb, ids, W.flags, W.cells, W.scal, static_cast<int>(ncells), s));
-    int nc = 0;
-    EN_TRY(cudaMemcpyAsync(&nc, W.scal, sizeof(int), cudaMemcpyDeviceToHost, s));
+    // interface cells in ascending order (metrics.cpp:150-156 visits them so)
+    long long* d_nc = static_cast<long long*>(W.tmp);
+    EN_TRY(lsr_compact::compact(CellFlag{W.flags}, CellId{}, ncells, W.cells, d_nc, d_nc + 1, tb - sizeof(long long),
+                                s));
+    lsr_note_launch();
+    lsr_note_launch();
+    long long nc = 0;
+    EN_TRY(cudaMemcpyAsync(&nc, d_nc, sizeof nc, cudaMemcpyDeviceToHost, s));
     EN_TRY(cudaStreamSynchronize(s));
     *n_cells = nc;
     double total = 0.0;
@@ -261,7 +280,7 @@ int lsr_prep_surface_energy(const SlParams& P, const double* phi, const double* 
                                                                                 W.contrib, W.scal + 1);
         }
         lsr_note_launch();
-        block_partials<<<static_cast<unsigned>((nblk + 127) / 128), 128, 0, s>>>(W.contrib, nc, W.partial);
+        block_partials<<<static_cast<unsigned>(nblk), 256, 0, s>>>(W.contrib, nc, W.partial);
         lsr_note_launch();
         EN_TRY(cudaGetLastError());
         std::vector<double> h(nblk);
