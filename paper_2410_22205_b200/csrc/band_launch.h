@@ -37,6 +37,7 @@ struct ReinitBuffers {
     unsigned char* frozen = nullptr;
     long long* nodes = nullptr;
     double* sgn = nullptr;
+    unsigned char* nbr = nullptr;  // per node: which axis neighbours exist
     unsigned long long* scal = nullptr;
     void* tmp = nullptr;
     size_t tmp_bytes = 0;

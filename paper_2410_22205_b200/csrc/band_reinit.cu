@@ -102,6 +102,58 @@ __global__ void band_pass_z(SlParams P, const unsigned char* __restrict__ u, lon
     state[id] = (c & 2) ? 1 : (d ? 2 : 0);
 }
 
+// Vector forms of the three passes for rows of a multiple of 16 nodes: the x
+// pass makes 4 nodes per thread (two 16-byte loads of phi, one 4-byte store),
+// the y/z passes 16 per thread (16-byte loads and stores, bytewise logic on
+// 32-bit lanes). Same results as the scalar passes above.
+__global__ void band_pass_x4(SlParams P, const double* __restrict__ phi, double gamma, long long n4,
+                             unsigned* __restrict__ t) {
+    const long long q = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (q >= n4) return;
+    const long long id = 4 * q;
+    const int x0 = static_cast<int>(id % P.nx);
+    const double2 a = __ldg(reinterpret_cast<const double2*>(phi + id));
+    const double2 b = __ldg(reinterpret_cast<const double2*>(phi + id) + 1);
+    const bool c0 = fabs(a.x) < gamma, c1 = fabs(a.y) < gamma, c2 = fabs(b.x) < gamma, c3 = fabs(b.y) < gamma;
+    const bool l = x0 > 0 && fabs(__ldg(phi + id - 1)) < gamma;
+    const bool r = x0 + 4 < P.nx && fabs(__ldg(phi + id + 4)) < gamma;
+    const unsigned o0 = (c0 ? 2u : 0u) | ((c0 || l || c1) ? 1u : 0u);
+    const unsigned o1 = (c1 ? 2u : 0u) | ((c1 || c0 || c2) ? 1u : 0u);
+    const unsigned o2 = (c2 ? 2u : 0u) | ((c2 || c1 || c3) ? 1u : 0u);
+    const unsigned o3 = (c3 ? 2u : 0u) | ((c3 || c2 || r) ? 1u : 0u);
+    t[q] = o0 | (o1 << 8) | (o2 << 16) | (o3 << 24);
+}
+
+__device__ __forceinline__ uint4 or4(uint4 a, uint4 b) { return make_uint4(a.x | b.x, a.y | b.y, a.z | b.z, a.w | b.w); }
+
+// per byte: core (bit 1) -> 1, else dilated (bit 0) -> 2, else 0
+__device__ __forceinline__ unsigned state_bytes(unsigned core_bits, unsigned dil_bits) {
+    const unsigned b1 = core_bits & 0x01010101u, b0 = dil_bits & 0x01010101u;
+    return b1 | ((b0 & ~b1) << 1);
+}
+
+__global__ void band_pass_yz16(SlParams P, int axis, const uint4* __restrict__ in, long long n16,
+                               uint4* __restrict__ out, uint4* __restrict__ state) {
+    const long long q = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (q >= n16) return;
+    const long long row = (16 * q) / P.nx;
+    const int j = static_cast<int>(row % P.ny), k = static_cast<int>(row / P.ny);
+    const long long st = (axis == 1 ? P.nx : P.nxy) / 16;
+    const bool has_m = axis == 1 ? j > 0 : k > 0, has_p = axis == 1 ? j < P.ny - 1 : k < P.nz - 1;
+    const uint4 c = in[q];
+    uint4 d = c;
+    if (has_m) d = or4(d, in[q - st]);
+    if (has_p) d = or4(d, in[q + st]);
+    const unsigned m = 0x01010101u;
+    if (axis == 1 && P.dim == 3) {  // keep core (bit 1) and the y-dilated bit 0 for the z pass
+        out[q] = make_uint4((c.x & (m << 1)) | (d.x & m), (c.y & (m << 1)) | (d.y & m), (c.z & (m << 1)) | (d.z & m),
+                            (c.w & (m << 1)) | (d.w & m));
+    } else {
+        state[q] = make_uint4(state_bytes(c.x >> 1, d.x), state_bytes(c.y >> 1, d.y), state_bytes(c.z >> 1, d.z),
+                              state_bytes(c.w >> 1, d.w));
+    }
+}
+
 struct IsActive {
     const unsigned char* s;
     __device__ bool operator()(long long id) const { return s[id] == 1; }
@@ -170,18 +222,30 @@ struct NotFrozen {  // tube entries t whose node was not frozen by the one-step 
     const long long* tube;
     __device__ bool operator()(long long t) const { return !frozen[tube[t]]; }
 };
+struct IsFrozen {
+    const unsigned char* frozen;
+    __device__ bool operator()(long long id) const { return frozen[id] != 0; }
+};
 struct TubeId {
     const long long* tube;
     __device__ long long operator()(long long t) const { return tube[t]; }
 };
 
-// smoothed sign at entry (reinit.cpp:250-257)
-__global__ void sign_kernel(const double* __restrict__ phi, const long long* __restrict__ nodes, long long nn,
-                            double eps2, double* __restrict__ sgn) {
+// smoothed sign at entry (reinit.cpp:250-257); also each node's neighbour
+// mask for the sweeps (bit 2*ax: the -1 neighbour along ax exists, bit
+// 2*ax+1: the +1 one), so the sweeps need no index arithmetic
+__global__ void sign_kernel(SlParams P, const double* __restrict__ phi, const long long* __restrict__ nodes,
+                            long long nn, double eps2, double* __restrict__ sgn, unsigned char* __restrict__ nbr) {
     const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (t >= nn) return;
-    const double v = __ldg(phi + nodes[t]);
+    const long long id = nodes[t];
+    const double v = __ldg(phi + id);
     sgn[t] = v / sqrt(v * v + eps2);
+    int i, j, k;
+    lsr_dev::unflatten(P, id, i, j, k);
+    unsigned m = (i > 0 ? 1u : 0u) | (i < P.nx - 1 ? 2u : 0u) | (j > 0 ? 4u : 0u) | (j < P.ny - 1 ? 8u : 0u);
+    if (P.dim == 3) m |= (k > 0 ? 16u : 0u) | (k < P.nz - 1 ? 32u : 0u);
+    nbr[t] = static_cast<unsigned char>(m);
 }
 
 // godunov_norm (reinit.cpp:63-84) on values already loaded: pc = phi at the
@@ -228,36 +292,41 @@ __device__ __forceinline__ double godunov_vals(const SlParams& P, double pc, con
 // |upd| is kept as the bits of a non-negative double (integer order = double
 // order); std::max(residual, x) never lets a NaN in, nor does `a > 0`; it is
 // reduced within each warp before one atomic per warp.
-constexpr int kJacNPT = 4;
+#ifndef LSR_JAC_NPT
+#define LSR_JAC_NPT 4
+#endif
+#ifndef LSR_JAC_MINB
+#define LSR_JAC_MINB 1
+#endif
+constexpr int kJacNPT = LSR_JAC_NPT;
 constexpr int kJacThreads = 256;
 
-__global__ void __launch_bounds__(kJacThreads) jacobi(SlParams P, const double* __restrict__ cur,
-                                                      double* __restrict__ nxt, const long long* __restrict__ nodes,
-                                                      const double* __restrict__ sgn, long long nn, double dtau,
-                                                      IterState* __restrict__ st) {
+__global__ void __launch_bounds__(kJacThreads, LSR_JAC_MINB)
+    jacobi(SlParams P, const double* __restrict__ cur, double* __restrict__ nxt, const long long* __restrict__ nodes,
+           const double* __restrict__ sgn, const unsigned char* __restrict__ nbr, long long nn, double dtau,
+           IterState* __restrict__ st) {
     if (*reinterpret_cast<volatile int*>(&st->done)) return;
     const long long base = static_cast<long long>(blockIdx.x) * (kJacThreads * kJacNPT) + threadIdx.x;
     long long id[kJacNPT];
     double sg[kJacNPT];
+    unsigned mk[kJacNPT];
 #pragma unroll
     for (int r = 0; r < kJacNPT; ++r) {
         const long long t = base + r * kJacThreads;
         id[r] = t < nn ? nodes[t] : -1;
         sg[r] = t < nn ? sgn[t] : 0.0;
+        mk[r] = t < nn ? nbr[t] : 0u;
     }
     const long long stv[3] = {1, P.nx, P.nxy};
-    const int nnv[3] = {P.nx, P.ny, P.nz};
     double pc[kJacNPT], vm[kJacNPT][3], vp[kJacNPT][3];
     bool hm[kJacNPT][3], hp[kJacNPT][3];
 #pragma unroll
     for (int r = 0; r < kJacNPT; ++r) {
-        int ijk[3] = {0, 0, 0};
-        if (id[r] >= 0) lsr_dev::unflatten(P, id[r], ijk[0], ijk[1], ijk[2]);
         pc[r] = id[r] >= 0 ? __ldg(cur + id[r]) : 0.0;
 #pragma unroll
         for (int ax = 0; ax < 3; ++ax) {
-            hm[r][ax] = id[r] >= 0 && ax < P.dim && ijk[ax] > 0;
-            hp[r][ax] = id[r] >= 0 && ax < P.dim && ijk[ax] < nnv[ax] - 1;
+            hm[r][ax] = (mk[r] >> (2 * ax)) & 1u;
+            hp[r][ax] = (mk[r] >> (2 * ax + 1)) & 1u;
             vm[r][ax] = hm[r][ax] ? __ldg(cur + id[r] - stv[ax]) : 0.0;
             vp[r][ax] = hp[r][ax] ? __ldg(cur + id[r] + stv[ax]) : 0.0;
         }
@@ -359,9 +428,21 @@ int lsr_band_build(const SlParams& P, const double* phi, double gamma, BandBuffe
     // buffers, which are only written by the compaction afterwards
     unsigned char* t = reinterpret_cast<unsigned char*>(B.active);
     unsigned char* u = reinterpret_cast<unsigned char*>(B.tube);
-    band_pass_x<<<gb, 256, 0, s>>>(P, phi, gamma, n, t);
-    band_pass_y<<<gb, 256, 0, s>>>(P, t, n, u, B.state);
-    if (P.dim == 3) band_pass_z<<<gb, 256, 0, s>>>(P, u, n, B.state);
+    if (P.nx % 16 == 0) {  // rows of whole 16-byte vectors
+        const long long n4 = n / 4, n16 = n / 16;
+        band_pass_x4<<<static_cast<unsigned>((n4 + 255) / 256), 256, 0, s>>>(P, phi, gamma, n4,
+                                                                               reinterpret_cast<unsigned*>(t));
+        const unsigned g16 = static_cast<unsigned>((n16 + 255) / 256);
+        band_pass_yz16<<<g16, 256, 0, s>>>(P, 1, reinterpret_cast<const uint4*>(t), n16, reinterpret_cast<uint4*>(u),
+                                           reinterpret_cast<uint4*>(B.state));
+        if (P.dim == 3)
+            band_pass_yz16<<<g16, 256, 0, s>>>(P, 2, reinterpret_cast<const uint4*>(u), n16, nullptr,
+                                               reinterpret_cast<uint4*>(B.state));
+    } else {
+        band_pass_x<<<gb, 256, 0, s>>>(P, phi, gamma, n, t);
+        band_pass_y<<<gb, 256, 0, s>>>(P, t, n, u, B.state);
+        if (P.dim == 3) band_pass_z<<<gb, 256, 0, s>>>(P, u, n, B.state);
+    }
     lsr_note_launch();
     lsr_note_launch();
     if (P.dim == 3) lsr_note_launch();
@@ -397,6 +478,7 @@ int ReinitBuffers::reserve(long long n, std::string* err) {
     BR_TRY(cudaMalloc(&frozen, n));
     BR_TRY(cudaMalloc(&nodes, sizeof(long long) * n));
     BR_TRY(cudaMalloc(&sgn, sizeof(double) * n));
+    BR_TRY(cudaMalloc(&nbr, n));
     BR_TRY(cudaMalloc(&scal, sizeof(unsigned long long) * 4));
     cap = n;
     return LSR_OK;
@@ -406,11 +488,13 @@ void ReinitBuffers::release() {
     cudaFree(frozen);
     cudaFree(nodes);
     cudaFree(sgn);
+    cudaFree(nbr);
     cudaFree(scal);
     cudaFree(tmp);
     frozen = nullptr;
     nodes = nullptr;
     sgn = nullptr;
+    nbr = nullptr;
     scal = nullptr;
     tmp = nullptr;
     tmp_bytes = 0;
@@ -454,12 +538,24 @@ int lsr_reinitialize(const SlParams& P, double** phi, double** scratch, const Ba
     // nodes = tube minus frozen, ascending (reinit.cpp:94-98)
     size_t tb = 0;
     long long* d_nn = reinterpret_cast<long long*>(W.scal + 2);
-    tb = lsr_compact::scratch_bytes(B.n_tube);
+    tb = lsr_compact::scratch_bytes(n > B.n_tube ? n : B.n_tube);
     if (tb > W.tmp_bytes) {
         cudaFree(W.tmp);
         W.tmp = nullptr;
         BR_TRY(cudaMalloc(&W.tmp, tb));
         W.tmp_bytes = tb;
+    }
+    // `next = phi` (reinit.cpp:259): the scratch buffer holds the pre-one-step
+    // field, which differs from phi exactly on the frozen nodes -> copy those
+    {
+        long long nf = 0;
+        BR_TRY(lsr_compact::compact(IsFrozen{W.frozen}, lsr_compact::Identity{}, n, W.nodes, d_nn, W.tmp, tb, s));
+        BR_TRY(cudaMemcpyAsync(&nf, d_nn, sizeof nf, cudaMemcpyDeviceToHost, s));
+        BR_TRY(cudaStreamSynchronize(s));
+        if (nf > 0) {
+            copy_ids<<<static_cast<unsigned>((nf + 255) / 256), 256, 0, s>>>(*phi, *scratch, W.nodes, nf);
+            lsr_note_launch();
+        }
     }
     BR_TRY(lsr_compact::compact(NotFrozen{W.frozen, B.tube}, TubeId{B.tube}, B.n_tube, W.nodes, d_nn, W.tmp, tb, s));
     lsr_note_launch();
@@ -469,12 +565,9 @@ int lsr_reinitialize(const SlParams& P, double** phi, double** scratch, const Ba
     BR_TRY(cudaStreamSynchronize(s));
     const unsigned gb = static_cast<unsigned>((nn + 255) / 256);
     if (nn > 0) {
-        sign_kernel<<<gb, 256, 0, s>>>(*phi, W.nodes, nn, R.sign_eps * R.sign_eps, W.sgn);
+        sign_kernel<<<gb, 256, 0, s>>>(P, *phi, W.nodes, nn, R.sign_eps * R.sign_eps, W.sgn, W.nbr);
         lsr_note_launch();
     }
-    // `next = phi` (reinit.cpp:259): the scratch buffer holds the pre-one-step
-    // field, which differs from phi on the frozen nodes -> one full copy
-    BR_TRY(cudaMemcpyAsync(*scratch, *phi, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
     // All max_iters sweeps are queued without host round trips: sweep k reads
     // buf[k&1] and writes buf[(k+1)&1]; a one-thread check after each sweep
     // applies the reference's stop rule (reinit.cpp:275-278) and raises a
@@ -487,7 +580,7 @@ int lsr_reinitialize(const SlParams& P, double** phi, double** scratch, const Ba
     for (int k = 0; k < R.max_iters; ++k) {
         if (nn > 0) {
             jacobi<<<static_cast<unsigned>((nn + kJacThreads * kJacNPT - 1) / (kJacThreads * kJacNPT)), kJacThreads, 0,
-                     s>>>(P, buf[k & 1], buf[(k + 1) & 1], W.nodes, W.sgn, nn, R.dtau, st);
+                     s>>>(P, buf[k & 1], buf[(k + 1) & 1], W.nodes, W.sgn, W.nbr, nn, R.dtau, st);
             lsr_note_launch();
         }
         iter_check<<<1, 1, 0, s>>>(st, tol);

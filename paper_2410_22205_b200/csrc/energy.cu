@@ -66,6 +66,42 @@ __global__ void flag_cells(SlParams P, const double* __restrict__ phi, long long
     flags[c] = (zero || (pos && neg)) ? 1 : 0;
 }
 
+// flag_cells for 3d grids with nx % 4 == 0: four consecutive cells of a row
+// per thread; the 5 x 4 corner nodes are loaded once (16-byte loads) and
+// classified once instead of 8 loads per cell
+__device__ __forceinline__ unsigned sign_class(double v) {  // bit0 pos, bit1 neg, bit2 zero (or NaN)
+    return v > 0.0 ? 1u : (v < 0.0 ? 2u : 4u);
+}
+
+__global__ void flag_cells4(SlParams P, const double* __restrict__ phi, unsigned tpr, long long nthreads,
+                            unsigned char* __restrict__ flags) {
+    const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t >= nthreads) return;
+    const unsigned cx = P.nx - 1, cy = P.ny - 1;
+    const unsigned row = static_cast<unsigned>(t / tpr);  // cell row (j, k)
+    const int i0 = 4 * static_cast<int>(t - static_cast<long long>(row) * tpr);
+    const int k = static_cast<int>(row / cy), j = static_cast<int>(row - static_cast<unsigned>(k) * cy);
+    unsigned cls[5] = {0, 0, 0, 0, 0};  // per corner column: OR of the 4 rows' classes
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+        const long long b = (static_cast<long long>(k + (r >> 1)) * P.ny + j + (r & 1)) * P.nx + i0;
+        const double2 a = __ldg(reinterpret_cast<const double2*>(phi + b));
+        const double2 c = __ldg(reinterpret_cast<const double2*>(phi + b) + 1);
+        cls[0] |= sign_class(a.x);
+        cls[1] |= sign_class(a.y);
+        cls[2] |= sign_class(c.x);
+        cls[3] |= sign_class(c.y);
+        if (i0 + 4 < P.nx) cls[4] |= sign_class(__ldg(phi + b + 4));
+    }
+    const long long c0 = static_cast<long long>(row) * cx + i0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        if (i0 + q >= static_cast<int>(cx)) break;
+        const unsigned m = cls[q] | cls[q + 1];
+        flags[c0 + q] = ((m & 4u) || (m & 3u) == 3u) ? 1 : 0;  // zero corner, or both signs
+    }
+}
+
 // energy_3d per-cell contribution (metrics.cpp:161-178)
 __global__ void contrib_3d(SlParams P, const double* __restrict__ phi, const double* __restrict__ dist,
                            const int* __restrict__ cells, long long nc, int r, double dxp, double select, int p,
@@ -236,7 +272,13 @@ int lsr_prep_surface_energy(const SlParams& P, const double* phi, const double* 
     if (!W.scal) EN_TRY(cudaMalloc(&W.scal, sizeof(int) * 2));
     EN_TRY(cudaMemsetAsync(W.scal, 0, sizeof(int) * 2, s));
     const int T = 256;
-    flag_cells<<<static_cast<unsigned>((ncells + T - 1) / T), T, 0, s>>>(P, phi, ncells, W.flags);
+    if (P.dim == 3 && P.nx % 4 == 0) {
+        const unsigned tpr = static_cast<unsigned>((P.nx - 1 + 3) / 4);
+        const long long nt = static_cast<long long>(P.ny - 1) * (P.nz - 1) * tpr;
+        flag_cells4<<<static_cast<unsigned>((nt + T - 1) / T), T, 0, s>>>(P, phi, tpr, nt, W.flags);
+    } else {
+        flag_cells<<<static_cast<unsigned>((ncells + T - 1) / T), T, 0, s>>>(P, phi, ncells, W.flags);
+    }
     lsr_note_launch();
     const size_t tb = lsr_compact::scratch_bytes(ncells) + sizeof(long long);
     if (tb > W.tmp_bytes) {
