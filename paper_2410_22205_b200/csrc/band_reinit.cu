@@ -217,6 +217,82 @@ __global__ void one_step(SlParams P, const double* __restrict__ prev, double* __
     }
 }
 
+// one_step for 3d grids with nx % 4 == 0: four consecutive nodes of a row
+// per thread, the node values and their y/z neighbours as 16-byte loads;
+// per node the same arithmetic in the same neighbour order as one_step
+__device__ __forceinline__ void one_node(const SlParams& P, double pj, const double* v, const bool* has,
+                                         double& val, bool& is_zero, bool& is_frozen) {
+    val = pj;
+    if (pj == 0.0) {
+        is_zero = true;
+        return;
+    }
+    double best = -1.0;
+#pragma unroll
+    for (int q = 0; q < 6; ++q) {
+        if (!has[q]) continue;
+        const double pk = v[q];
+        if (pj * pk >= 0.0) continue;
+        const double crossing = P.dx * fabs(pj) / (fabs(pj) + fabs(pk));
+        best = best < 0.0 ? crossing : smin(best, crossing);
+    }
+    if (best >= 0.0) {
+        val = pj > 0.0 ? best : -best;
+        is_frozen = true;
+    }
+}
+
+__device__ __forceinline__ void load4(const double* src, double* dst) {
+    const double2 a = __ldg(reinterpret_cast<const double2*>(src));
+    const double2 b = __ldg(reinterpret_cast<const double2*>(src) + 1);
+    dst[0] = a.x;
+    dst[1] = a.y;
+    dst[2] = b.x;
+    dst[3] = b.y;
+}
+
+__global__ void one_step4(SlParams P, const double* __restrict__ prev, double* __restrict__ out,
+                          unsigned* __restrict__ frozen4, long long n4, int* __restrict__ any_frozen,
+                          int* __restrict__ any_zero) {
+    const long long q = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    bool zero = false, froz = false;
+    if (q < n4) {
+        const long long id = 4 * q;
+        const long long row = id / P.nx;
+        const int x0 = static_cast<int>(id - row * P.nx);
+        const int j = static_cast<int>(row % P.ny), k = static_cast<int>(row / P.ny);
+        const bool hy[2] = {j > 0, j + 1 < P.ny}, hz[2] = {k > 0, k + 1 < P.nz};
+        double c[4], ym[4], yp[4], zm[4], zp[4];
+        load4(prev + id, c);
+        load4(prev + (hy[0] ? id - P.nx : id), ym);
+        load4(prev + (hy[1] ? id + P.nx : id), yp);
+        load4(prev + (hz[0] ? id - P.nxy : id), zm);
+        load4(prev + (hz[1] ? id + P.nxy : id), zp);
+        const double xl = x0 > 0 ? __ldg(prev + id - 1) : 0.0;
+        const double xr = x0 + 4 < P.nx ? __ldg(prev + id + 4) : 0.0;
+        double res[4];
+        unsigned fb = 0;
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const double v[6] = {r > 0 ? c[r - 1] : xl, r < 3 ? c[r + 1] : xr, ym[r], yp[r], zm[r], zp[r]};
+            const bool has[6] = {x0 + r > 0, x0 + r + 1 < P.nx, hy[0], hy[1], hz[0], hz[1]};
+            bool z = false, f = false;
+            one_node(P, c[r], v, has, res[r], z, f);
+            zero |= z;
+            froz |= f;
+            fb |= (f ? 1u : 0u) << (8 * r);
+        }
+        reinterpret_cast<double2*>(out + id)[0] = make_double2(res[0], res[1]);
+        reinterpret_cast<double2*>(out + id)[1] = make_double2(res[2], res[3]);
+        frozen4[q] = fb;
+    }
+    const unsigned zb = __ballot_sync(0xffffffffu, zero), fbal = __ballot_sync(0xffffffffu, froz);
+    if ((threadIdx.x & 31) == 0) {
+        if (zb) *any_zero = 1;
+        if (fbal) *any_frozen = 1;
+    }
+}
+
 struct NotFrozen {  // tube entries t whose node was not frozen by the one-step (reinit.cpp:94-98)
     const unsigned char* frozen;
     const long long* tube;
@@ -522,8 +598,14 @@ int lsr_reinitialize(const SlParams& P, double** phi, double** scratch, const Ba
     int* flags = reinterpret_cast<int*>(W.scal);  // [0] any_frozen, [1] any_zero
     BR_TRY(cudaMemsetAsync(W.scal, 0, sizeof(unsigned long long) * 4, s));
     // interface_one_step: *phi -> *scratch (every node), frozen flags
-    one_step<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(P, *phi, *scratch, W.frozen, n, flags,
-                                                                     flags + 1);
+    if (P.dim == 3 && P.nx % 4 == 0) {
+        const long long n4 = n / 4;
+        one_step4<<<static_cast<unsigned>((n4 + 255) / 256), 256, 0, s>>>(
+            P, *phi, *scratch, reinterpret_cast<unsigned*>(W.frozen), n4, flags, flags + 1);
+    } else {
+        one_step<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(P, *phi, *scratch, W.frozen, n, flags,
+                                                                         flags + 1);
+    }
     lsr_note_launch();
     int hf[2];
     BR_TRY(cudaMemcpyAsync(hf, flags, sizeof hf, cudaMemcpyDeviceToHost, s));
