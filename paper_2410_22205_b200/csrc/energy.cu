@@ -126,6 +126,86 @@ __global__ void contrib_3d(SlParams P, const double* __restrict__ phi, const dou
     contrib[c] = acc;
 }
 
+// contrib_3d with the per-axis work hoisted (refinement r <= 8): a sample's
+// x depends on ci only, so its cell and theta along x (locate_cell and the
+// Markstein theta, interp.cpp:63-69) are computed once per ci, likewise y and
+// z; the products wx*wy once per (ci, cj); the cell's 8 corner values of phi
+// and d are loaded once and used whenever a sample locates in the cell
+// itself (else its own corners are loaded). Every interpolant is the same
+// expression as interp_q1's, so the result is bit-identical.
+constexpr int kMaxRefine = 8;
+
+__device__ __forceinline__ double q1_corners(double w00, double w10, double w01, double w11, double uz, double tz,
+                                             const double* f) {
+    double value = 0.0;  // loop order dk, dj, di (interp.cpp:71-79); w = (wx*wy)*wz
+    value += (w00 * uz) * f[0];
+    value += (w10 * uz) * f[1];
+    value += (w01 * uz) * f[2];
+    value += (w11 * uz) * f[3];
+    value += (w00 * tz) * f[4];
+    value += (w10 * tz) * f[5];
+    value += (w01 * tz) * f[6];
+    value += (w11 * tz) * f[7];
+    return value;
+}
+
+__device__ __forceinline__ void load_corners(const SlParams& P, const double* __restrict__ f, long long b, double* v) {
+    v[0] = __ldg(f + b);
+    v[1] = __ldg(f + b + 1);
+    v[2] = __ldg(f + b + P.nx);
+    v[3] = __ldg(f + b + P.nx + 1);
+    v[4] = __ldg(f + b + P.nxy);
+    v[5] = __ldg(f + b + P.nxy + 1);
+    v[6] = __ldg(f + b + P.nxy + P.nx);
+    v[7] = __ldg(f + b + P.nxy + P.nx + 1);
+}
+
+__global__ void contrib_3d_hoisted(SlParams P, const double* __restrict__ phi, const double* __restrict__ dist,
+                                   const int* __restrict__ cells, long long nc, int r, double dxp, double select,
+                                   int p, double* __restrict__ contrib) {
+    const long long c = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (c >= nc) return;
+    const long long cid = cells[c];
+    const unsigned cx = P.nx - 1, cy = P.ny - 1;
+    const unsigned row = static_cast<unsigned>(cid) / cx;
+    const int i = static_cast<int>(static_cast<unsigned>(cid) - row * cx);
+    const int k = static_cast<int>(row / cy);
+    const int j = static_cast<int>(row - static_cast<unsigned>(k) * cy);
+    const double bx = P.ox + i * P.dx, by = P.oy + j * P.dx, bz = P.oz + k * P.dx;  // Grid::node
+    int lx[kMaxRefine], ly[kMaxRefine], lz[kMaxRefine];
+    double tx[kMaxRefine], ty[kMaxRefine], tz[kMaxRefine];
+    for (int q = 0; q < r; ++q) {
+        const double x = bx + (q + 0.5) * dxp, y = by + (q + 0.5) * dxp, z = bz + (q + 0.5) * dxp;
+        lx[q] = lsr_dev::locate_axis(P, x, P.ox, P.nx);
+        ly[q] = lsr_dev::locate_axis(P, y, P.oy, P.ny);
+        lz[q] = lsr_dev::locate_axis(P, z, P.oz, P.nz);
+        tx[q] = lsr_dev::axis_theta(P, x, P.ox, lx[q]);
+        ty[q] = lsr_dev::axis_theta(P, y, P.oy, ly[q]);
+        tz[q] = lsr_dev::axis_theta(P, z, P.oz, lz[q]);
+    }
+    const long long home = (static_cast<long long>(k) * P.ny + j) * P.nx + i;
+    double fp[8], fd[8];
+    load_corners(P, phi, home, fp);
+    load_corners(P, dist, home, fd);
+    double acc = 0.0;
+    for (int ck = 0; ck < r; ++ck)
+        for (int cj = 0; cj < r; ++cj)
+            for (int ci = 0; ci < r; ++ci) {
+                const double ux = 1.0 - tx[ci], uy = 1.0 - ty[cj], uz = 1.0 - tz[ck];
+                const double w00 = ux * uy, w10 = tx[ci] * uy, w01 = ux * ty[cj], w11 = tx[ci] * ty[cj];
+                const bool at_home = lx[ci] == i && ly[cj] == j && lz[ck] == k;
+                double gp[8], gd[8];
+                const long long b = (static_cast<long long>(lz[ck]) * P.ny + ly[cj]) * P.nx + lx[ci];
+                if (!at_home) load_corners(P, phi, b, gp);
+                const double vphi = q1_corners(w00, w10, w01, w11, uz, tz[ck], at_home ? fp : gp);
+                if (fabs(vphi) >= select) continue;
+                if (!at_home) load_corners(P, dist, b, gd);
+                const double vd = q1_corners(w00, w10, w01, w11, uz, tz[ck], at_home ? fd : gd);
+                acc += powp(fabs(vd), p) * dxp * dxp;
+            }
+    contrib[c] = acc;
+}
+
 struct Pt {
     double x, y;
 };
@@ -315,8 +395,11 @@ int lsr_prep_surface_energy(const SlParams& P, const double* phi, const double* 
             const int r = refine;
             const double dxp = P.dx / r;
             const double select = std::sqrt(3.0) / 2.0 * dxp;  // metrics.cpp:157
-            contrib_3d<<<static_cast<unsigned>((nc + 127) / 128), 128, 0, s>>>(P, phi, dist, W.cells, nc, r, dxp,
-                                                                                select, p, W.contrib);
+            const unsigned g = static_cast<unsigned>((nc + 127) / 128);
+            if (r <= kMaxRefine)
+                contrib_3d_hoisted<<<g, 128, 0, s>>>(P, phi, dist, W.cells, nc, r, dxp, select, p, W.contrib);
+            else
+                contrib_3d<<<g, 128, 0, s>>>(P, phi, dist, W.cells, nc, r, dxp, select, p, W.contrib);
         } else {
             contrib_2d<<<static_cast<unsigned>((nc + 127) / 128), 128, 0, s>>>(P, phi, dist, W.cells, nc, p,
                                                                                 W.contrib, W.scal + 1);
