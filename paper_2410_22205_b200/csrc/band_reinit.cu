@@ -154,6 +154,13 @@ __global__ void band_pass_yz16(SlParams P, int axis, const uint4* __restrict__ i
     }
 }
 
+struct StateIs1 {  // narrow_band ACTIVE
+    __device__ bool operator()(unsigned v) const { return v == 1; }
+};
+struct NonZero {  // in the tube / frozen
+    __device__ bool operator()(unsigned v) const { return v != 0; }
+};
+
 struct IsActive {
     const unsigned char* s;
     __device__ bool operator()(long long id) const { return s[id] == 1; }
@@ -524,8 +531,10 @@ int lsr_band_build(const SlParams& P, const double* phi, double gamma, BandBuffe
     if (P.dim == 3) lsr_note_launch();
     const size_t tb = lsr_compact::scratch_bytes(n);
     if (int st = ensure_tmp(B, tb, err)) return st;
-    BR_TRY(lsr_compact::compact(IsActive{B.state}, lsr_compact::Identity{}, n, B.active, B.counts, B.tmp, tb, s));
-    BR_TRY(lsr_compact::compact(InTube{B.state}, lsr_compact::Identity{}, n, B.tube, B.counts + 1, B.tmp, tb, s));
+    BR_TRY(lsr_compact::compact(lsr_compact::BytePred<StateIs1>{B.state, {}}, lsr_compact::Identity{}, n, B.active,
+                                B.counts, B.tmp, tb, s));
+    BR_TRY(lsr_compact::compact(lsr_compact::BytePred<NonZero>{B.state, {}}, lsr_compact::Identity{}, n, B.tube,
+                                B.counts + 1, B.tmp, tb, s));
     for (int q = 0; q < 4; ++q) lsr_note_launch();
     long long h[2];
     BR_TRY(cudaMemcpyAsync(h, B.counts, sizeof h, cudaMemcpyDeviceToHost, s));
@@ -631,7 +640,8 @@ int lsr_reinitialize(const SlParams& P, double** phi, double** scratch, const Ba
     // field, which differs from phi exactly on the frozen nodes -> copy those
     {
         long long nf = 0;
-        BR_TRY(lsr_compact::compact(IsFrozen{W.frozen}, lsr_compact::Identity{}, n, W.nodes, d_nn, W.tmp, tb, s));
+        BR_TRY(lsr_compact::compact(lsr_compact::BytePred<NonZero>{W.frozen, {}}, lsr_compact::Identity{}, n, W.nodes,
+                                    d_nn, W.tmp, tb, s));
         BR_TRY(cudaMemcpyAsync(&nf, d_nn, sizeof nf, cudaMemcpyDeviceToHost, s));
         BR_TRY(cudaStreamSynchronize(s));
         if (nf > 0) {

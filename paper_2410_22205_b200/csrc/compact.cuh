@@ -57,6 +57,55 @@ __global__ void __launch_bounds__(kThreads) write_tiles(Pred pred, Item item, lo
     }
 }
 
+// Byte-flag predicates (pred(i) = test(a[i])) read their 16 bytes per thread
+// with one 16-byte load; a must be 16-byte aligned.
+template <class Test>
+struct BytePred {
+    const unsigned char* a;
+    Test test;
+    __device__ __forceinline__ unsigned mask16(long long base, long long n) const {
+        unsigned m = 0;
+        if (base + kItems <= n) {
+            const uint4 v = *reinterpret_cast<const uint4*>(a + base);
+            const unsigned w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int q = 0; q < kItems; ++q) m |= (test((w[q >> 2] >> (8 * (q & 3))) & 0xffu) ? 1u : 0u) << q;
+        } else {
+            for (int q = 0; q < kItems && base + q < n; ++q) m |= (test(a[base + q]) ? 1u : 0u) << q;
+        }
+        return m;
+    }
+};
+
+template <class Test>
+__global__ void __launch_bounds__(kThreads) count_tiles_bytes(BytePred<Test> pred, long long n,
+                                                              long long* __restrict__ counts) {
+    const long long base = static_cast<long long>(blockIdx.x) * kTile + static_cast<long long>(threadIdx.x) * kItems;
+    const int c = base < n ? __popc(pred.mask16(base, n)) : 0;
+    using Reduce = cub::BlockReduce<int, kThreads>;
+    __shared__ typename Reduce::TempStorage tmp;
+    const int total = Reduce(tmp).Sum(c);
+    if (threadIdx.x == 0) counts[blockIdx.x] = total;
+}
+
+template <class Test, class Item, class Out>
+__global__ void __launch_bounds__(kThreads) write_tiles_bytes(BytePred<Test> pred, Item item, long long n,
+                                                              const long long* __restrict__ offsets,
+                                                              Out* __restrict__ out) {
+    const long long base = static_cast<long long>(blockIdx.x) * kTile + static_cast<long long>(threadIdx.x) * kItems;
+    unsigned mask = base < n ? pred.mask16(base, n) : 0u;
+    using Scan = cub::BlockScan<int, kThreads>;
+    __shared__ typename Scan::TempStorage tmp;
+    int rank;
+    Scan(tmp).ExclusiveSum(__popc(mask), rank);
+    Out* o = out + offsets[blockIdx.x] + rank;
+    while (mask) {
+        const int q = __ffs(mask) - 1;
+        mask &= mask - 1;
+        *o++ = item(base + q);
+    }
+}
+
 struct Identity {
     __device__ long long operator()(long long i) const { return i; }
 };
@@ -69,6 +118,27 @@ inline size_t scratch_bytes(long long n) {
                                   static_cast<int>(tiles + 1));
     return (2 * (tiles + 1)) * sizeof(long long) + scan + 256;
 }
+
+namespace detail {
+template <class Pred, class Item, class Out>
+void launch_count(Pred pred, Item, long long n, long long tiles, long long* counts, Out*, cudaStream_t s) {
+    count_tiles<<<static_cast<unsigned>(tiles), kThreads, 0, s>>>(pred, n, counts);
+}
+template <class Test, class Item, class Out>
+void launch_count(BytePred<Test> pred, Item, long long n, long long tiles, long long* counts, Out*, cudaStream_t s) {
+    count_tiles_bytes<<<static_cast<unsigned>(tiles), kThreads, 0, s>>>(pred, n, counts);
+}
+template <class Pred, class Item, class Out>
+void launch_write(Pred pred, Item item, long long n, long long tiles, const long long* offsets, Out* out,
+                  cudaStream_t s) {
+    write_tiles<<<static_cast<unsigned>(tiles), kThreads, 0, s>>>(pred, item, n, offsets, out);
+}
+template <class Test, class Item, class Out>
+void launch_write(BytePred<Test> pred, Item item, long long n, long long tiles, const long long* offsets, Out* out,
+                  cudaStream_t s) {
+    write_tiles_bytes<<<static_cast<unsigned>(tiles), kThreads, 0, s>>>(pred, item, n, offsets, out);
+}
+}  // namespace detail
 
 // out[0..*d_count) = item(i) for the i in [0, n) with pred(i), ascending.
 // *d_count is written on the device (stream order); scratch holds
@@ -84,10 +154,10 @@ cudaError_t compact(Pred pred, Item item, long long n, Out* out, long long* d_co
     size_t scan_bytes = scratch_size - 2 * (tiles + 1) * sizeof(long long);
     cudaError_t e = cudaMemsetAsync(counts + tiles, 0, sizeof(long long), s);
     if (e != cudaSuccess) return e;
-    count_tiles<<<static_cast<unsigned>(tiles), kThreads, 0, s>>>(pred, n, counts);
+    detail::launch_count(pred, item, n, tiles, counts, out, s);
     e = cub::DeviceScan::ExclusiveSum(scan_tmp, scan_bytes, counts, offsets, static_cast<int>(tiles + 1), s);
     if (e != cudaSuccess) return e;
-    write_tiles<<<static_cast<unsigned>(tiles), kThreads, 0, s>>>(pred, item, n, offsets, out);
+    detail::launch_write(pred, item, n, tiles, offsets, out, s);
     e = cudaMemcpyAsync(d_count, offsets + tiles, sizeof(long long), cudaMemcpyDeviceToDevice, s);
     if (e != cudaSuccess) return e;
     return cudaGetLastError();

@@ -283,6 +283,9 @@ __global__ void contrib_2d(SlParams P, const double* __restrict__ phi, const dou
 // blocked_sum's per-block partials (parallel.hpp:39-40): one CTA per block
 // of 4096 contributions stages them through shared memory with coalesced
 // loads, then one thread adds them in index order (the reference's order)
+struct FlagSet {
+    __device__ bool operator()(unsigned v) const { return v != 0; }
+};
 struct CellFlag {
     const unsigned char* flags;
     __device__ bool operator()(long long c) const { return flags[c] != 0; }
@@ -370,8 +373,8 @@ int lsr_prep_surface_energy(const SlParams& P, const double* phi, const double* 
     }
     // interface cells in ascending order (metrics.cpp:150-156 visits them so)
     long long* d_nc = static_cast<long long*>(W.tmp);
-    EN_TRY(lsr_compact::compact(CellFlag{W.flags}, CellId{}, ncells, W.cells, d_nc, d_nc + 1, tb - sizeof(long long),
-                                s));
+    EN_TRY(lsr_compact::compact(lsr_compact::BytePred<FlagSet>{W.flags, {}}, CellId{}, ncells, W.cells, d_nc, d_nc + 1,
+                                tb - sizeof(long long), s));
     lsr_note_launch();
     lsr_note_launch();
     long long nc = 0;

@@ -15,3 +15,9 @@ ncu --set full --clock-control none --import-source on -k regex:sl_step_kernel -
     -o gpurun_out/sl_full_$R $CMD > gpurun_out/ncu_full_$R.log 2>&1
 tail -2 gpurun_out/ncu_full_$R.log
 cat gpurun_out/bench_$R.json
+# 5. per-kernel DRAM bytes and durations of the loop body (band, E_p, SL, reinit)
+LOOP="python tools/loopbench.py --steps 2"
+$LOOP > gpurun_out/loop_plain_$R.log 2>&1 || exit 1
+ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
+    -k regex:"count_tiles|write_tiles|Scan|band_|flag_|contrib|block_partials|one_step|sign_|jacobi|iter_check|clamp_|sl_step|resync|copy_ids" \
+    --csv --log-file gpurun_out/loop_launches_$R.csv $LOOP > gpurun_out/ncu_loop_$R.log 2>&1
