@@ -388,11 +388,12 @@ __global__ void __launch_bounds__(kJacThreads, LSR_JAC_MINB)
     jacobi(SlParams P, const double* __restrict__ cur, double* __restrict__ nxt, const long long* __restrict__ nodes,
            const double* __restrict__ sgn, const unsigned char* __restrict__ nbr, long long nn, double dtau,
            IterState* __restrict__ st) {
-    if (*reinterpret_cast<volatile int*>(&st->done)) return;
     const long long base = static_cast<long long>(blockIdx.x) * (kJacThreads * kJacNPT) + threadIdx.x;
     long long id[kJacNPT];
     double sg[kJacNPT];
     unsigned mk[kJacNPT];
+    // the node list loads are issued before the stop flag is read, so the
+    // flag's latency overlaps them instead of preceding them
 #pragma unroll
     for (int r = 0; r < kJacNPT; ++r) {
         const long long t = base + r * kJacThreads;
@@ -400,6 +401,7 @@ __global__ void __launch_bounds__(kJacThreads, LSR_JAC_MINB)
         sg[r] = t < nn ? sgn[t] : 0.0;
         mk[r] = t < nn ? nbr[t] : 0u;
     }
+    if (*reinterpret_cast<volatile int*>(&st->done)) return;
     const long long stv[3] = {1, P.nx, P.nxy};
     double pc[kJacNPT], vm[kJacNPT][3], vp[kJacNPT][3];
     bool hm[kJacNPT][3], hp[kJacNPT][3];
@@ -433,7 +435,17 @@ __global__ void __launch_bounds__(kJacThreads, LSR_JAC_MINB)
         const unsigned long long o = __shfl_xor_sync(0xffffffffu, bitsmax, off);
         bitsmax = o > bitsmax ? o : bitsmax;
     }
-    if ((threadIdx.x & 31) == 0 && bitsmax) atomicMax(&st->residual_bits, bitsmax);
+    // one atomic per CTA: same-address atomics serialise in L2, and one per
+    // warp cost most of a sweep
+    __shared__ unsigned long long wmax[kJacThreads / 32];
+    if ((threadIdx.x & 31) == 0) wmax[threadIdx.x >> 5] = bitsmax;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long m = 0;
+#pragma unroll
+        for (int w = 0; w < kJacThreads / 32; ++w) m = wmax[w] > m ? wmax[w] : m;
+        if (m) atomicMax(&st->residual_bits, m);
+    }
 }
 
 // the stop rule after a sweep (reinit.cpp:275-278)
