@@ -170,6 +170,18 @@ struct InTube {
     __device__ bool operator()(long long id) const { return s[id] != 0; }
 };
 
+// clamp_field two nodes per thread; a node is stored only when clamping
+// changes its bits (after the first loop iteration most of the grid already
+// sits at +-gamma, so the pass is mostly reads)
+__global__ void clamp_kernel2(double2* __restrict__ f, long long n2, double gamma) {
+    const long long id = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (id >= n2) return;
+    const double2 v = f[id];
+    const double a = smin(smax(v.x, -gamma), gamma), b = smin(smax(v.y, -gamma), gamma);
+    if (__double_as_longlong(a) != __double_as_longlong(v.x) || __double_as_longlong(b) != __double_as_longlong(v.y))
+        f[id] = make_double2(a, b);
+}
+
 __global__ void clamp_kernel(double* __restrict__ f, long long n, double gamma) {
     const long long id = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (id >= n) return;
@@ -563,7 +575,11 @@ int lsr_clamp(double* f, long long n, double gamma, cudaStream_t s, std::string*
         *err = "clamp_field: gamma must be positive";  // grid.cpp:127
         return LSR_ERR_CONFIG;
     }
-    clamp_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(f, n, gamma);
+    if (n % 2 == 0 && reinterpret_cast<uintptr_t>(f) % 16 == 0)
+        clamp_kernel2<<<static_cast<unsigned>((n / 2 + 255) / 256), 256, 0, s>>>(reinterpret_cast<double2*>(f), n / 2,
+                                                                                gamma);
+    else
+        clamp_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(f, n, gamma);
     lsr_note_launch();
     BR_TRY(cudaGetLastError());
     return LSR_OK;
