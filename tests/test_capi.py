@@ -12,11 +12,15 @@ import pytest
 from conftest import ROOT, golden_grid, load_golden
 
 HEADER = os.path.join(ROOT, "include", "lsr_cuda.h")
+HEADERS = [HEADER, os.path.join(ROOT, "include", "lsr_workloads.h")]
 
 
 def declared_symbols():
-    src = open(HEADER).read()
-    return sorted(set(re.findall(r"\b(lsr_cuda_\w+)\s*\(", src)))
+    """Every function the C headers declare (lsr_cuda_* and lsr_cloud_*)."""
+    out = set()
+    for h in HEADERS:
+        out |= set(re.findall(r"\b(lsr_(?:cuda|cloud)_\w+)\s*\(", open(h).read()))
+    return sorted(out)
 
 
 def test_library_exports_every_declared_symbol(built):
