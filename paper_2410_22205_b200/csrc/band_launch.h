@@ -38,6 +38,9 @@ struct ReinitBuffers {
     long long* nodes = nullptr;
     double* sgn = nullptr;
     unsigned char* nbr = nullptr;  // per node: which axis neighbours exist
+    long long* frozen_ids = nullptr;  // nodes the one-step froze (ascending), n_frozen of them
+    long long n_frozen = 0;
+    int* clamp_outside = nullptr;  // device flag: the final clamp changed a node outside the tube
     unsigned long long* scal = nullptr;
     void* tmp = nullptr;
     size_t tmp_bytes = 0;
@@ -48,7 +51,8 @@ struct ReinitBuffers {
 
 int lsr_band_build(const lsr_dev::SlParams& P, const double* phi, double gamma, BandBuffers& B, long long* n_active,
                    long long* n_tube, cudaStream_t s, std::string* err);
-int lsr_clamp(double* f, long long n, double gamma, cudaStream_t s, std::string* err);
+int lsr_clamp(double* f, long long n, double gamma, cudaStream_t s, std::string* err,
+              const unsigned char* state = nullptr, int* outside = nullptr);
 int lsr_reinitialize(const lsr_dev::SlParams& P, double** phi, double** scratch, const BandBuffers& B, double gamma,
                      const ReinitParams& R, ReinitBuffers& W, int* iterations, int* had_interface, cudaStream_t s,
                      std::string* err);

@@ -173,19 +173,30 @@ struct InTube {
 // clamp_field two nodes per thread; a node is stored only when clamping
 // changes its bits (after the first loop iteration most of the grid already
 // sits at +-gamma, so the pass is mostly reads)
-__global__ void clamp_kernel2(double2* __restrict__ f, long long n2, double gamma) {
+// `state` (optional): the band of the previous step; a change at a node
+// outside its tube (state 0) raises *outside, telling the loop that the
+// field changed beyond the tube (else it resyncs only tube and frozen nodes)
+__global__ void clamp_kernel2(double2* __restrict__ f, long long n2, double gamma,
+                              const unsigned char* __restrict__ state, int* __restrict__ outside) {
     const long long id = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (id >= n2) return;
     const double2 v = f[id];
     const double a = smin(smax(v.x, -gamma), gamma), b = smin(smax(v.y, -gamma), gamma);
-    if (__double_as_longlong(a) != __double_as_longlong(v.x) || __double_as_longlong(b) != __double_as_longlong(v.y))
+    const bool ca = __double_as_longlong(a) != __double_as_longlong(v.x);
+    const bool cb = __double_as_longlong(b) != __double_as_longlong(v.y);
+    if (ca || cb) {
         f[id] = make_double2(a, b);
+        if (state && ((ca && !state[2 * id]) || (cb && !state[2 * id + 1]))) *outside = 1;
+    }
 }
 
-__global__ void clamp_kernel(double* __restrict__ f, long long n, double gamma) {
+__global__ void clamp_kernel(double* __restrict__ f, long long n, double gamma, const unsigned char* __restrict__ state,
+                             int* __restrict__ outside) {
     const long long id = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (id >= n) return;
-    f[id] = smin(smax(f[id], -gamma), gamma);
+    const double v = f[id], c = smin(smax(v, -gamma), gamma);
+    f[id] = c;
+    if (state && __double_as_longlong(c) != __double_as_longlong(v) && !state[id]) *outside = 1;
 }
 
 // interface_one_step (reinit.cpp:24-46); `prev` is read-only, `out` gets every
@@ -570,16 +581,17 @@ int lsr_band_build(const SlParams& P, const double* phi, double gamma, BandBuffe
     return LSR_OK;
 }
 
-int lsr_clamp(double* f, long long n, double gamma, cudaStream_t s, std::string* err) {
+int lsr_clamp(double* f, long long n, double gamma, cudaStream_t s, std::string* err, const unsigned char* state,
+              int* outside) {
     if (!(gamma > 0.0)) {
         *err = "clamp_field: gamma must be positive";  // grid.cpp:127
         return LSR_ERR_CONFIG;
     }
     if (n % 2 == 0 && reinterpret_cast<uintptr_t>(f) % 16 == 0)
         clamp_kernel2<<<static_cast<unsigned>((n / 2 + 255) / 256), 256, 0, s>>>(reinterpret_cast<double2*>(f), n / 2,
-                                                                                gamma);
+                                                                                gamma, state, outside);
     else
-        clamp_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(f, n, gamma);
+        clamp_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(f, n, gamma, state, outside);
     lsr_note_launch();
     BR_TRY(cudaGetLastError());
     return LSR_OK;
@@ -592,6 +604,8 @@ int ReinitBuffers::reserve(long long n, std::string* err) {
     BR_TRY(cudaMalloc(&nodes, sizeof(long long) * n));
     BR_TRY(cudaMalloc(&sgn, sizeof(double) * n));
     BR_TRY(cudaMalloc(&nbr, n));
+    BR_TRY(cudaMalloc(&frozen_ids, sizeof(long long) * n));
+    BR_TRY(cudaMalloc(&clamp_outside, sizeof(int)));
     BR_TRY(cudaMalloc(&scal, sizeof(unsigned long long) * 4));
     cap = n;
     return LSR_OK;
@@ -602,6 +616,10 @@ void ReinitBuffers::release() {
     cudaFree(nodes);
     cudaFree(sgn);
     cudaFree(nbr);
+    cudaFree(frozen_ids);
+    cudaFree(clamp_outside);
+    frozen_ids = nullptr;
+    clamp_outside = nullptr;
     cudaFree(scal);
     cudaFree(tmp);
     frozen = nullptr;
@@ -632,6 +650,8 @@ int lsr_reinitialize(const SlParams& P, double** phi, double** scratch, const Ba
     if (int st = W.reserve(n, err)) return st;
     *iterations = 0;
     *had_interface = 0;
+    W.n_frozen = 0;
+    BR_TRY(cudaMemsetAsync(W.clamp_outside, 0, sizeof(int), s));
     int* flags = reinterpret_cast<int*>(W.scal);  // [0] any_frozen, [1] any_zero
     BR_TRY(cudaMemsetAsync(W.scal, 0, sizeof(unsigned long long) * 4, s));
     // interface_one_step: *phi -> *scratch (every node), frozen flags
@@ -650,7 +670,8 @@ int lsr_reinitialize(const SlParams& P, double** phi, double** scratch, const Ba
     if (!hf[0] && !hf[1]) {
         // NoInterfaceError caught by reinitialize (reinit.cpp:140-142): phi is
         // left as it was (the one-step wrote nothing), then clamped
-        return lsr_clamp(*phi, n, gamma, s, err);
+        W.n_frozen = 0;
+        return lsr_clamp(*phi, n, gamma, s, err, B.state, W.clamp_outside);
     }
     std::swap(*phi, *scratch);  // *phi = one-step result
     *had_interface = 1;
@@ -668,12 +689,13 @@ int lsr_reinitialize(const SlParams& P, double** phi, double** scratch, const Ba
     // field, which differs from phi exactly on the frozen nodes -> copy those
     {
         long long nf = 0;
-        BR_TRY(lsr_compact::compact(lsr_compact::BytePred<NonZero>{W.frozen, {}}, lsr_compact::Identity{}, n, W.nodes,
-                                    d_nn, W.tmp, tb, s));
+        BR_TRY(lsr_compact::compact(lsr_compact::BytePred<NonZero>{W.frozen, {}}, lsr_compact::Identity{}, n,
+                                    W.frozen_ids, d_nn, W.tmp, tb, s));
         BR_TRY(cudaMemcpyAsync(&nf, d_nn, sizeof nf, cudaMemcpyDeviceToHost, s));
         BR_TRY(cudaStreamSynchronize(s));
+        W.n_frozen = nf;
         if (nf > 0) {
-            copy_ids<<<static_cast<unsigned>((nf + 255) / 256), 256, 0, s>>>(*phi, *scratch, W.nodes, nf);
+            copy_ids<<<static_cast<unsigned>((nf + 255) / 256), 256, 0, s>>>(*phi, *scratch, W.frozen_ids, nf);
             lsr_note_launch();
         }
     }
@@ -719,5 +741,5 @@ int lsr_reinitialize(const SlParams& P, double** phi, double** scratch, const Ba
         lsr_note_launch();
     }
     *iterations = iter;
-    return lsr_clamp(*phi, n, gamma, s, err);
+    return lsr_clamp(*phi, n, gamma, s, err, B.state, W.clamp_outside);
 }

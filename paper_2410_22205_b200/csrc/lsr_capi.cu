@@ -1118,7 +1118,29 @@ int lsr_cuda_loop_step(lsr_cuda_ctx* c, const lsr_step_cfg* cfg, const lsr_reini
     int it = 0, had = 0;
     if (int st = lsr_cuda_reinitialize(c, LSR_FIELD_OUT, cfg->gamma, rc, &it, &had)) return st;
     cudaEventRecord(ev[4], c->stream);
-    // 5. swap (driver.cpp:203)
+    // 5. swap (driver.cpp:203). phi^{n+1} differs from phi^n (the buffer that
+    // becomes `out`) only where the SL step, the one-step, the sweeps or the
+    // clamp changed it: inside the tube of phi^n (ACTIVE is in it), at the
+    // frozen nodes, or — reported by the clamp — elsewhere. Unless the clamp
+    // reported a change outside the tube, the next SL step resyncs just the
+    // tube and frozen nodes instead of copying the whole field.
+    int outside = 1;
+    LSR_CUDA_TRY(cudaMemcpyAsync(&outside, c->rb.clamp_outside, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    LSR_CUDA_TRY(cudaStreamSynchronize(c->stream));
+    const int64_t nd = c->band.n_tube + c->rb.n_frozen;
+    if (!outside) {
+        if (int st = ensure_ids(&c->dirty, &c->cap_dirty, nd)) return st;
+        if (c->band.n_tube > 0)
+            LSR_CUDA_TRY(cudaMemcpyAsync(c->dirty, c->band.tube, sizeof(int64_t) * c->band.n_tube,
+                                         cudaMemcpyDeviceToDevice, c->stream));
+        if (c->rb.n_frozen > 0)
+            LSR_CUDA_TRY(cudaMemcpyAsync(c->dirty + c->band.n_tube, c->rb.frozen_ids, sizeof(int64_t) * c->rb.n_frozen,
+                                         cudaMemcpyDeviceToDevice, c->stream));
+        c->n_dirty = nd;
+        c->consistent = true;
+    } else {
+        c->consistent = false;
+    }
     std::swap(c->phi, c->out);
     LSR_CUDA_TRY(cudaStreamSynchronize(c->stream));
     S.energy = e2;
