@@ -257,6 +257,12 @@ __device__ __forceinline__ void one_node(const SlParams& P, double pj, const dou
         is_zero = true;
         return;
     }
+    // common case first: no existing neighbour of the opposite sign (a NaN
+    // product fails the test and takes the full path below)
+    bool quiet = true;
+#pragma unroll
+    for (int q = 0; q < 6; ++q) quiet = quiet && (!has[q] || pj * v[q] >= 0.0);
+    if (quiet) return;
     double best = -1.0;
 #pragma unroll
     for (int q = 0; q < 6; ++q) {
@@ -288,9 +294,8 @@ __global__ void one_step4(SlParams P, const double* __restrict__ prev, double* _
     bool zero = false, froz = false;
     if (q < n4) {
         const long long id = 4 * q;
-        const long long row = id / P.nx;
-        const int x0 = static_cast<int>(id - row * P.nx);
-        const int j = static_cast<int>(row % P.ny), k = static_cast<int>(row / P.ny);
+        int x0, j, k;
+        lsr_dev::unflatten(P, id, x0, j, k);  // 32-bit divisions when the grid allows
         const bool hy[2] = {j > 0, j + 1 < P.ny}, hz[2] = {k > 0, k + 1 < P.nz};
         double c[4], ym[4], yp[4], zm[4], zp[4];
         load4(prev + id, c);
