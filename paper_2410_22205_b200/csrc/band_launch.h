@@ -38,6 +38,7 @@ struct ReinitBuffers {
     long long* nodes = nullptr;
     double* sgn = nullptr;
     unsigned char* nbr = nullptr;  // per node: which axis neighbours exist
+    unsigned* nodes32 = nullptr;      // the node list as 4-byte ids (grids below 2^32 nodes)
     long long* frozen_ids = nullptr;  // nodes the one-step froze (ascending), n_frozen of them
     long long n_frozen = 0;
     int* clamp_outside = nullptr;  // device flag: the final clamp changed a node outside the tube

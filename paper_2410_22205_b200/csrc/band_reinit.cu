@@ -346,10 +346,12 @@ struct TubeId {
 // mask for the sweeps (bit 2*ax: the -1 neighbour along ax exists, bit
 // 2*ax+1: the +1 one), so the sweeps need no index arithmetic
 __global__ void sign_kernel(SlParams P, const double* __restrict__ phi, const long long* __restrict__ nodes,
-                            long long nn, double eps2, double* __restrict__ sgn, unsigned char* __restrict__ nbr) {
+                            long long nn, double eps2, double* __restrict__ sgn, unsigned char* __restrict__ nbr,
+                            unsigned* __restrict__ nodes32) {
     const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (t >= nn) return;
     const long long id = nodes[t];
+    if (nodes32) nodes32[t] = static_cast<unsigned>(id);  // 4-byte ids for the sweeps when the grid allows
     const double v = __ldg(phi + id);
     sgn[t] = v / sqrt(v * v + eps2);
     int i, j, k;
@@ -412,8 +414,9 @@ __device__ __forceinline__ double godunov_vals(const SlParams& P, double pc, con
 constexpr int kJacNPT = LSR_JAC_NPT;
 constexpr int kJacThreads = 256;
 
+template <class IdT>
 __global__ void __launch_bounds__(kJacThreads, LSR_JAC_MINB)
-    jacobi(SlParams P, const double* __restrict__ cur, double* __restrict__ nxt, const long long* __restrict__ nodes,
+    jacobi(SlParams P, const double* __restrict__ cur, double* __restrict__ nxt, const IdT* __restrict__ nodes,
            const double* __restrict__ sgn, const unsigned char* __restrict__ nbr, long long nn, double dtau,
            IterState* __restrict__ st) {
     const long long base = static_cast<long long>(blockIdx.x) * (kJacThreads * kJacNPT) + threadIdx.x;
@@ -425,7 +428,7 @@ __global__ void __launch_bounds__(kJacThreads, LSR_JAC_MINB)
 #pragma unroll
     for (int r = 0; r < kJacNPT; ++r) {
         const long long t = base + r * kJacThreads;
-        id[r] = t < nn ? nodes[t] : -1;
+        id[r] = t < nn ? static_cast<long long>(nodes[t]) : -1;
         sg[r] = t < nn ? sgn[t] : 0.0;
         mk[r] = t < nn ? nbr[t] : 0u;
     }
@@ -610,6 +613,7 @@ int ReinitBuffers::reserve(long long n, std::string* err) {
     BR_TRY(cudaMalloc(&sgn, sizeof(double) * n));
     BR_TRY(cudaMalloc(&nbr, n));
     BR_TRY(cudaMalloc(&frozen_ids, sizeof(long long) * n));
+    BR_TRY(cudaMalloc(&nodes32, sizeof(unsigned) * n));
     BR_TRY(cudaMalloc(&clamp_outside, sizeof(int)));
     BR_TRY(cudaMalloc(&scal, sizeof(unsigned long long) * 4));
     cap = n;
@@ -622,6 +626,8 @@ void ReinitBuffers::release() {
     cudaFree(sgn);
     cudaFree(nbr);
     cudaFree(frozen_ids);
+    cudaFree(nodes32);
+    nodes32 = nullptr;
     cudaFree(clamp_outside);
     frozen_ids = nullptr;
     clamp_outside = nullptr;
@@ -712,7 +718,8 @@ int lsr_reinitialize(const SlParams& P, double** phi, double** scratch, const Ba
     BR_TRY(cudaStreamSynchronize(s));
     const unsigned gb = static_cast<unsigned>((nn + 255) / 256);
     if (nn > 0) {
-        sign_kernel<<<gb, 256, 0, s>>>(P, *phi, W.nodes, nn, R.sign_eps * R.sign_eps, W.sgn, W.nbr);
+        sign_kernel<<<gb, 256, 0, s>>>(P, *phi, W.nodes, nn, R.sign_eps * R.sign_eps, W.sgn, W.nbr,
+                                       n <= 0xffffffffLL ? W.nodes32 : nullptr);
         lsr_note_launch();
     }
     // All max_iters sweeps are queued without host round trips: sweep k reads
@@ -726,8 +733,13 @@ int lsr_reinitialize(const SlParams& P, double** phi, double** scratch, const Ba
     double* buf[2] = {*phi, *scratch};
     for (int k = 0; k < R.max_iters; ++k) {
         if (nn > 0) {
-            jacobi<<<static_cast<unsigned>((nn + kJacThreads * kJacNPT - 1) / (kJacThreads * kJacNPT)), kJacThreads, 0,
-                     s>>>(P, buf[k & 1], buf[(k + 1) & 1], W.nodes, W.sgn, W.nbr, nn, R.dtau, st);
+            const unsigned g = static_cast<unsigned>((nn + kJacThreads * kJacNPT - 1) / (kJacThreads * kJacNPT));
+            if (n <= 0xffffffffLL)
+                jacobi<<<g, kJacThreads, 0, s>>>(P, buf[k & 1], buf[(k + 1) & 1], W.nodes32, W.sgn, W.nbr, nn, R.dtau,
+                                                 st);
+            else
+                jacobi<<<g, kJacThreads, 0, s>>>(P, buf[k & 1], buf[(k + 1) & 1], W.nodes, W.sgn, W.nbr, nn, R.dtau,
+                                                 st);
             lsr_note_launch();
         }
         iter_check<<<1, 1, 0, s>>>(st, tol);
