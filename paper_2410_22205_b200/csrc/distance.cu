@@ -22,6 +22,8 @@
 
 #include <cub/cub.cuh>
 
+#include <cstdlib>
+
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
@@ -226,6 +228,120 @@ __global__ void sweep_plane(GridP G, int ord, int s, int k_lo, int k_cnt, double
     }
 }
 
+// Tiled wavefront form of one 3d Gauss-Seidel sweep (fast_sweep's inner
+// triple loop for one ordering, distance.cpp:80-139). In the mirrored
+// coordinates of the ordering every update reads its -1 neighbours already
+// updated and its +1 neighbours not yet updated. Tiles of kTile^3 nodes whose
+// mirrored tile coordinates sum to S run in the S-th launch (their -1 face
+// neighbours finished at S-1, their +1 ones start at S+1); inside a tile one
+// CTA walks the kTile*3-2 inner planes in order, one node per thread and
+// plane, with the tile and a one-node halo in shared memory. Every node sees
+// exactly the neighbour values the lexicographic sweep gives it, so the
+// result is bit-identical, with 3*n/kTile launches per sweep instead of 3*n.
+constexpr int kTile = 16;
+constexpr int kTH = kTile + 2;
+
+__global__ void __launch_bounds__(kTile * kTile) sweep_tiles(GridP G, int ord, int S, int nti, int ntj, int ntk,
+                                                             int tk_lo, double sentinel,
+                                                             const unsigned char* __restrict__ exact,
+                                                             double* __restrict__ d,
+                                                             unsigned long long* __restrict__ max_change) {
+    __shared__ double sd[kTH * kTH * kTH];
+    __shared__ unsigned long long wmax[kTile * kTile / 32];
+    const int tkp = tk_lo + blockIdx.x / ntj, tjp = blockIdx.x % ntj;
+    const int tip = S - tjp - tkp;
+    if (tip < 0 || tip >= nti || tkp >= ntk) return;  // uniform per CTA
+    // the tile's real box [x0, x0 + bx) etc. (mirrored tiles map to contiguous boxes)
+    const int mlo[3] = {tip * kTile, tjp * kTile, tkp * kTile};
+    const int n3[3] = {G.nx, G.ny, G.nz};
+    int lo[3], bsz[3];
+    for (int a = 0; a < 3; ++a) {
+        const int mhi = min(mlo[a] + kTile, n3[a]);
+        bsz[a] = mhi - mlo[a];
+        lo[a] = (ord >> a) & 1 ? n3[a] - mhi : mlo[a];
+    }
+    // box + halo into shared memory (outside the grid: never read)
+    for (int e = threadIdx.x; e < kTH * kTH * kTH; e += blockDim.x) {
+        const int hz = e / (kTH * kTH), hy = (e / kTH) % kTH, hx = e % kTH;
+        const int gx = lo[0] - 1 + hx, gy = lo[1] - 1 + hy, gz = lo[2] - 1 + hz;
+        if (hx <= bsz[0] + 1 && hy <= bsz[1] + 1 && hz <= bsz[2] + 1 && gx >= 0 && gx < G.nx && gy >= 0 &&
+            gy < G.ny && gz >= 0 && gz < G.nz)
+            sd[e] = d[(static_cast<long long>(gz) * G.ny + gy) * G.nx + gx];
+    }
+    __syncthreads();
+    const int ljp = threadIdx.x % kTile, lkp = threadIdx.x / kTile;  // this thread's mirrored row
+    const bool row_ok = ljp < bsz[1] && lkp < bsz[2];
+    const int lj = (ord & 2) ? bsz[1] - 1 - ljp : ljp, lk = (ord & 4) ? bsz[2] - 1 - lkp : lkp;
+    const int gj = lo[1] + lj, gk = lo[2] + lk;
+    unsigned long long cmax = 0;
+    const int planes = bsz[0] + bsz[1] + bsz[2] - 2;
+    for (int sp = 0; sp < planes; ++sp) {
+        const int lip = sp - ljp - lkp;
+        if (row_ok && lip >= 0 && lip < bsz[0]) {
+            const int li = (ord & 1) ? bsz[0] - 1 - lip : lip;
+            const int gi = lo[0] + li;
+            const long long id = (static_cast<long long>(gk) * G.ny + gj) * G.nx + gi;
+            if (!exact[id]) {
+                const int e = ((lk + 1) * kTH + lj + 1) * kTH + li + 1;
+                double a[3];
+                int m = 0;
+                {
+                    double best = sentinel;
+                    if (gi > 0) best = dmin(best, sd[e - 1]);
+                    if (gi < G.nx - 1) best = dmin(best, sd[e + 1]);
+                    if (best < sentinel) a[m++] = best;
+                }
+                {
+                    double best = sentinel;
+                    if (gj > 0) best = dmin(best, sd[e - kTH]);
+                    if (gj < G.ny - 1) best = dmin(best, sd[e + kTH]);
+                    if (best < sentinel) a[m++] = best;
+                }
+                {
+                    double best = sentinel;
+                    if (gk > 0) best = dmin(best, sd[e - kTH * kTH]);
+                    if (gk < G.nz - 1) best = dmin(best, sd[e + kTH * kTH]);
+                    if (best < sentinel) a[m++] = best;
+                }
+                if (m > 0) {
+                    if (m >= 2 && a[1] < a[0]) { const double t0 = a[0]; a[0] = a[1]; a[1] = t0; }
+                    if (m == 3) {
+                        if (a[2] < a[1]) { const double t1 = a[1]; a[1] = a[2]; a[2] = t1; }
+                        if (a[1] < a[0]) { const double t0 = a[0]; a[0] = a[1]; a[1] = t0; }
+                    }
+                    const double v = sd[e];
+                    const double cand = eikonal_update(a, m, G.dx);
+                    if (cand < v) {
+                        sd[e] = cand;
+                        const unsigned long long c =
+                            static_cast<unsigned long long>(__double_as_longlong(v - cand));
+                        cmax = c > cmax ? c : cmax;
+                    }
+                }
+            }
+        }
+        __syncthreads();
+    }
+    // write the box back
+    for (int e = threadIdx.x; e < bsz[0] * bsz[1] * bsz[2]; e += blockDim.x) {
+        const int z = e / (bsz[0] * bsz[1]), y = (e / bsz[0]) % bsz[1], x = e % bsz[0];
+        d[(static_cast<long long>(lo[2] + z) * G.ny + lo[1] + y) * G.nx + lo[0] + x] =
+            sd[((z + 1) * kTH + y + 1) * kTH + x + 1];
+    }
+    // the largest change: one atomic per CTA (max is order free)
+    for (int off = 16; off > 0; off >>= 1) {
+        const unsigned long long o = __shfl_xor_sync(0xffffffffu, cmax, off);
+        cmax = o > cmax ? o : cmax;
+    }
+    if ((threadIdx.x & 31) == 0) wmax[threadIdx.x >> 5] = cmax;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long mm = 0;
+        for (int w = 0; w < kTile * kTile / 32; ++w) mm = wmax[w] > mm ? wmax[w] : mm;
+        if (mm) atomicMax(max_change, mm);
+    }
+}
+
 // estimate_resolution's terms (cloud.cpp:473-476): the exact NN distance of
 // sampled point idx[i] to the rest of the cloud
 __global__ void sample_nn(HashP H, const double* __restrict__ pts, const int* __restrict__ starts,
@@ -374,11 +490,24 @@ int lsr_prep_build_distance(const lsr_grid* g, const double* h_pts, int64_t n, i
     const int orderings = g->dim == 3 ? 8 : 4;
     const double tol = 1e-3 * g->dx;
     const int max_rounds = 8;
+    static const bool tiled = !(std::getenv("LSR_SWEEP_TILES") && std::atoi(std::getenv("LSR_SWEEP_TILES")) == 0);
     const int smax = (G.nx - 1) + (G.ny - 1) + (G.dim == 3 ? G.nz - 1 : 0);
     int round = 0;
     for (; round < max_rounds; ++round) {
         PREP_TRY(cudaMemsetAsync(dmax, 0, sizeof(unsigned long long), s));
         for (int ord = 0; ord < orderings; ++ord) {
+            if (G.dim == 3 && tiled) {
+                const int nti = (G.nx + kTile - 1) / kTile, ntj = (G.ny + kTile - 1) / kTile,
+                          ntk = (G.nz + kTile - 1) / kTile;
+                for (int S = 0; S <= (nti - 1) + (ntj - 1) + (ntk - 1); ++S) {
+                    const int tk_lo = std::max(0, S - (nti - 1) - (ntj - 1)), tk_hi = std::min(ntk - 1, S);
+                    const unsigned ctas = static_cast<unsigned>((tk_hi - tk_lo + 1) * ntj);
+                    sweep_tiles<<<ctas, kTile * kTile, 0, s>>>(G, ord, S, nti, ntj, ntk, tk_lo, sentinel, d_exact,
+                                                               d_field, dmax);
+                    lsr_note_launch();
+                }
+                continue;
+            }
             for (int sp = 0; sp <= smax; ++sp) {
                 const int k_lo = G.dim == 3 ? std::max(0, sp - (G.nx - 1) - (G.ny - 1)) : 0;
                 const int k_hi = G.dim == 3 ? std::min(G.nz - 1, sp) : 0;
