@@ -247,6 +247,7 @@ __global__ void __launch_bounds__(kTile * kTile) sweep_tiles(GridP G, int ord, i
                                                              double* __restrict__ d,
                                                              unsigned long long* __restrict__ max_change) {
     __shared__ double sd[kTH * kTH * kTH];
+    __shared__ unsigned sx[kTile * kTile * kTile / 32];  // the box's exact flags, one bit per node
     __shared__ unsigned long long wmax[kTile * kTile / 32];
     const int tkp = tk_lo + blockIdx.x / ntj, tjp = blockIdx.x % ntj;
     const int tip = S - tjp - tkp;
@@ -268,6 +269,17 @@ __global__ void __launch_bounds__(kTile * kTile) sweep_tiles(GridP G, int ord, i
             gy < G.ny && gz >= 0 && gz < G.nz)
             sd[e] = d[(static_cast<long long>(gz) * G.ny + gy) * G.nx + gx];
     }
+    // the flags too: a global load inside the plane loop would put its
+    // latency on every one of the 3*kTile-2 dependent steps
+    for (int w = threadIdx.x; w < kTile * kTile * kTile / 32; w += blockDim.x) sx[w] = 0u;
+    __syncthreads();
+    for (int e = threadIdx.x; e < bsz[0] * bsz[1] * bsz[2]; e += blockDim.x) {
+        const int z = e / (bsz[0] * bsz[1]), y = (e / bsz[0]) % bsz[1], x = e % bsz[0];
+        if (exact[(static_cast<long long>(lo[2] + z) * G.ny + lo[1] + y) * G.nx + lo[0] + x]) {
+            const int b = (z * kTile + y) * kTile + x;
+            atomicOr(sx + (b >> 5), 1u << (b & 31));
+        }
+    }
     __syncthreads();
     const int ljp = threadIdx.x % kTile, lkp = threadIdx.x / kTile;  // this thread's mirrored row
     const bool row_ok = ljp < bsz[1] && lkp < bsz[2];
@@ -280,8 +292,8 @@ __global__ void __launch_bounds__(kTile * kTile) sweep_tiles(GridP G, int ord, i
         if (row_ok && lip >= 0 && lip < bsz[0]) {
             const int li = (ord & 1) ? bsz[0] - 1 - lip : lip;
             const int gi = lo[0] + li;
-            const long long id = (static_cast<long long>(gk) * G.ny + gj) * G.nx + gi;
-            if (!exact[id]) {
+            const int b = (lk * kTile + lj) * kTile + li;
+            if (!((sx[b >> 5] >> (b & 31)) & 1u)) {
                 const int e = ((lk + 1) * kTH + lj + 1) * kTH + li + 1;
                 double a[3];
                 int m = 0;
