@@ -238,7 +238,10 @@ __global__ void sweep_plane(GridP G, int ord, int s, int k_lo, int k_cnt, double
 // plane, with the tile and a one-node halo in shared memory. Every node sees
 // exactly the neighbour values the lexicographic sweep gives it, so the
 // result is bit-identical, with 3*n/kTile launches per sweep instead of 3*n.
-constexpr int kTile = 16;
+#ifndef LSR_SWEEP_TILE
+#define LSR_SWEEP_TILE 16
+#endif
+constexpr int kTile = LSR_SWEEP_TILE;
 constexpr int kTH = kTile + 2;
 
 __global__ void __launch_bounds__(kTile * kTile) sweep_tiles(GridP G, int ord, int S, int nti, int ntj, int ntk,
