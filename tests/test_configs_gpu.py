@@ -72,3 +72,48 @@ def test_configs_2_3_vs_live_reference(gpu, reference, config, n, steps):
     own = lsr.surface_energy(lsr.ScalarField(g, cur), lsr.DistanceField(lsr.ScalarField(g, dref)), 2, 5)
     ref_e = reference.surface_energy(gd, cur, dref, 2, 5)
     assert abs(own - ref_e) <= ULP16 * ref_e
+
+
+def test_config4_512_loop_step_and_one_shot_vs_reference(gpu, reference):
+    """Config 4 at its full size (512^3, 1 M-point bumpy sphere, WENO, p = 2,
+    delta = 1): one whole loop iteration (band, E_2, SL, reinit) against the
+    reference's own loop body on the host, bit for bit, and the one-shot
+    host entry on pinned buffers (the zero-copy pull path bench.py's e2e
+    times) against the device-resident step."""
+    import torch
+
+    lsr = gpu
+    g = lsr.cube_grid(512, 3)
+    pts = lsr.cloud_generate(4, 1_000_000, seed=2410, sigma=0.0)
+    ax = g.axes()
+    phi = (np.sqrt(ax[0][None, None, :] ** 2 + ax[1][None, :, None] ** 2 + ax[2][:, None, None] ** 2) - 0.9).ravel()
+    gd = dict(dim=3, dims=g.dims, origin=g.origin, dx=g.dx)
+    bp = lsr.default_band_params(3, g.dx)
+    cfg = lsr.StepConfig(p=2, delta=1.0, dt=0.25 * g.dx, interp=lsr.InterpolatorKind.Weno, band=bp)
+    ccfg = dict(p=2, interp=1, delta=1.0, dt=cfg.dt, fallback_c=1e-3, fallback_alpha=1.0, gamma=bp.gamma,
+                beta=bp.beta)
+    ctx = lsr.Context(g)
+    ctx.build_distance(pts)  # bit-identical to the reference's (tests/test_distance.py)
+    d = ctx.download(1)
+    # one-shot on pinned host buffers vs the device-resident step, same inputs
+    active = np.flatnonzero(np.abs(phi) < bp.gamma).astype(np.int64)
+    pin = lambda a: (lambda t: (t.__setitem__(slice(None), a), t)[1])(  # noqa: E731
+        torch.empty(a.size, dtype=torch.float64 if a.dtype == np.float64 else torch.int64, pin_memory=True).numpy())
+    hphi, hd, hact = pin(phi), pin(d), pin(active)
+    hout = pin(np.zeros(phi.size))
+    lsr.sl_step(lsr.ScalarField(g, hphi), lsr.DistanceField(lsr.ScalarField(g, hd)), lsr.BandMask(g, active=hact),
+                cfg, 1.5, lsr.ScalarField(g, hout))
+    ctx.upload(0, phi)
+    ctx.set_active(active)
+    ctx.sl_step(cfg, 1.5)
+    dev = ctx.download(2)
+    assert np.count_nonzero(bits(hout) != bits(dev)) == 0
+    # one loop iteration vs the reference's loop body
+    ctx.upload(0, phi)
+    rc = lsr.ReinitConfig.defaults(g.dx, bp.gamma)
+    ref_phi, e2, na, it, _ = reference.loop_step(gd, phi, d, ccfg)
+    s = ctx.loop_step(cfg, rc, 5, energy_override=e2)
+    assert s["n_active"] == na and s["reinit_iterations"] == it
+    got = ctx.download(0)
+    diff = np.count_nonzero(bits(got) != bits(ref_phi))
+    assert diff == 0, f"{diff} nodes differ"
