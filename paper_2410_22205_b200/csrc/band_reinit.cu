@@ -412,7 +412,10 @@ __device__ __forceinline__ double godunov_vals(const SlParams& P, double pc, con
 #define LSR_JAC_MINB 1
 #endif
 constexpr int kJacNPT = LSR_JAC_NPT;
-constexpr int kJacThreads = 256;
+#ifndef LSR_JAC_THREADS
+#define LSR_JAC_THREADS 128
+#endif
+constexpr int kJacThreads = LSR_JAC_THREADS;
 
 template <class IdT>
 __global__ void __launch_bounds__(kJacThreads, LSR_JAC_MINB)
