@@ -328,6 +328,66 @@ __global__ void one_step4(SlParams P, const double* __restrict__ prev, double* _
     }
 }
 
+// one_step4 marching along z: a thread owns 4 nodes of a row (x0.., j) for
+// kMarch consecutive planes and keeps the planes k-1, k, k+1 of its row in
+// registers, so each plane costs three row loads (z+1, y-1, y+1) instead of
+// five; same per-node arithmetic as one_step
+constexpr int kMarch = 16;
+
+__global__ void one_step_march(SlParams P, const double* __restrict__ prev, double* __restrict__ out,
+                               unsigned* __restrict__ frozen4, int* __restrict__ any_frozen,
+                               int* __restrict__ any_zero) {
+    const int qx = P.nx / 4;
+    const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const long long rows = static_cast<long long>(qx) * P.ny;  // (x-quad, j) pairs
+    bool zero = false, froz = false;
+    if (t < rows * ((P.nz + kMarch - 1) / kMarch)) {
+        const int kb = static_cast<int>(t / rows);
+        const long long r = t - kb * rows;
+        const int j = static_cast<int>(r / qx), x0 = 4 * static_cast<int>(r - static_cast<long long>(j) * qx);
+        const int k0 = kb * kMarch, k1 = min(P.nz, k0 + kMarch);
+        const bool hy[2] = {j > 0, j + 1 < P.ny};
+        long long id = (static_cast<long long>(k0) * P.ny + j) * P.nx + x0;
+        double zm[4], c[4], zp[4];
+        load4(prev + (k0 > 0 ? id - P.nxy : id), zm);
+        load4(prev + id, c);
+        for (int k = k0; k < k1; ++k, id += P.nxy) {
+            const bool hz[2] = {k > 0, k + 1 < P.nz};
+            double ym[4], yp[4];
+            load4(prev + (hz[1] ? id + P.nxy : id), zp);
+            load4(prev + (hy[0] ? id - P.nx : id), ym);
+            load4(prev + (hy[1] ? id + P.nx : id), yp);
+            const double xl = x0 > 0 ? __ldg(prev + id - 1) : 0.0;
+            const double xr = x0 + 4 < P.nx ? __ldg(prev + id + 4) : 0.0;
+            double res[4];
+            unsigned fb = 0;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const double v[6] = {q > 0 ? c[q - 1] : xl, q < 3 ? c[q + 1] : xr, ym[q], yp[q], zm[q], zp[q]};
+                const bool has[6] = {x0 + q > 0, x0 + q + 1 < P.nx, hy[0], hy[1], hz[0], hz[1]};
+                bool z = false, f = false;
+                one_node(P, c[q], v, has, res[q], z, f);
+                zero |= z;
+                froz |= f;
+                fb |= (f ? 1u : 0u) << (8 * q);
+            }
+            reinterpret_cast<double2*>(out + id)[0] = make_double2(res[0], res[1]);
+            reinterpret_cast<double2*>(out + id)[1] = make_double2(res[2], res[3]);
+            frozen4[id / 4] = fb;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                zm[q] = c[q];
+                c[q] = zp[q];
+            }
+        }
+    }
+    const unsigned zb = __ballot_sync(0xffffffffu, zero), fbal = __ballot_sync(0xffffffffu, froz);
+    if ((threadIdx.x & 31) == 0) {
+        if (zb) *any_zero = 1;
+        if (fbal) *any_frozen = 1;
+    }
+}
+
 struct NotFrozen {  // tube entries t whose node was not frozen by the one-step (reinit.cpp:94-98)
     const unsigned char* frozen;
     const long long* tube;
@@ -669,7 +729,12 @@ int lsr_reinitialize(const SlParams& P, double** phi, double** scratch, const Ba
     int* flags = reinterpret_cast<int*>(W.scal);  // [0] any_frozen, [1] any_zero
     BR_TRY(cudaMemsetAsync(W.scal, 0, sizeof(unsigned long long) * 4, s));
     // interface_one_step: *phi -> *scratch (every node), frozen flags
-    if (P.dim == 3 && P.nx % 4 == 0) {
+    static const bool march = !(std::getenv("LSR_ONE_STEP_MARCH") && std::atoi(std::getenv("LSR_ONE_STEP_MARCH")) == 0);
+    if (P.dim == 3 && P.nx % 4 == 0 && march) {
+        const long long threads = static_cast<long long>(P.nx / 4) * P.ny * ((P.nz + kMarch - 1) / kMarch);
+        one_step_march<<<static_cast<unsigned>((threads + 255) / 256), 256, 0, s>>>(
+            P, *phi, *scratch, reinterpret_cast<unsigned*>(W.frozen), flags, flags + 1);
+    } else if (P.dim == 3 && P.nx % 4 == 0) {
         const long long n4 = n / 4;
         one_step4<<<static_cast<unsigned>((n4 + 255) / 256), 256, 0, s>>>(
             P, *phi, *scratch, reinterpret_cast<unsigned*>(W.frozen), n4, flags, flags + 1);
