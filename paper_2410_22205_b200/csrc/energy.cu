@@ -20,6 +20,8 @@
 
 #include <cub/cub.cuh>
 
+#include <cstdlib>
+
 #include "compact.cuh"
 
 #include <cmath>
@@ -99,6 +101,56 @@ __global__ void flag_cells4(SlParams P, const double* __restrict__ phi, unsigned
         if (i0 + q >= static_cast<int>(cx)) break;
         const unsigned m = cls[q] | cls[q + 1];
         flags[c0 + q] = ((m & 4u) || (m & 3u) == 3u) ? 1 : 0;  // zero corner, or both signs
+    }
+}
+
+// flag_cells4 marching along z: a thread owns 4 cells of a cell row (i0..,
+// j) for kMarchCells consecutive cell planes; the classes of node rows
+// (j, k) and (j+1, k) carry over from the previous plane, so each plane
+// loads two node rows instead of four
+constexpr int kMarchCells = 16;
+
+__device__ __forceinline__ void row_classes(const SlParams& P, const double* __restrict__ phi, long long b, int i0,
+                                            unsigned* cls) {
+    const double2 a = __ldg(reinterpret_cast<const double2*>(phi + b));
+    const double2 c = __ldg(reinterpret_cast<const double2*>(phi + b) + 1);
+    cls[0] = sign_class(a.x);
+    cls[1] = sign_class(a.y);
+    cls[2] = sign_class(c.x);
+    cls[3] = sign_class(c.y);
+    cls[4] = i0 + 4 < P.nx ? sign_class(__ldg(phi + b + 4)) : 0u;
+}
+
+__global__ void flag_cells_march(SlParams P, const double* __restrict__ phi, unsigned tpr,
+                                 unsigned char* __restrict__ flags) {
+    const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int cx = P.nx - 1, cy = P.ny - 1, cz = P.nz - 1;
+    const long long rows = static_cast<long long>(tpr) * cy;  // (x-quad, j) pairs
+    if (t >= rows * ((cz + kMarchCells - 1) / kMarchCells)) return;
+    const int kb = static_cast<int>(t / rows);
+    const long long r = t - kb * rows;
+    const int j = static_cast<int>(r / tpr), i0 = 4 * static_cast<int>(r - static_cast<long long>(j) * tpr);
+    const int k0 = kb * kMarchCells, k1 = min(cz, k0 + kMarchCells);
+    unsigned lo[5], lo1[5];  // classes of node rows (j, k) and (j+1, k)
+    long long b = (static_cast<long long>(k0) * P.ny + j) * P.nx + i0;
+    row_classes(P, phi, b, i0, lo);
+    row_classes(P, phi, b + P.nx, i0, lo1);
+    for (int k = k0; k < k1; ++k, b += P.nxy) {
+        unsigned up[5], up1[5];
+        row_classes(P, phi, b + P.nxy, i0, up);
+        row_classes(P, phi, b + P.nxy + P.nx, i0, up1);
+        const long long c0 = (static_cast<long long>(k) * cy + j) * cx + i0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            if (i0 + q >= cx) break;
+            const unsigned m = lo[q] | lo[q + 1] | lo1[q] | lo1[q + 1] | up[q] | up[q + 1] | up1[q] | up1[q + 1];
+            flags[c0 + q] = ((m & 4u) || (m & 3u) == 3u) ? 1 : 0;  // zero corner, or both signs
+        }
+#pragma unroll
+        for (int q = 0; q < 5; ++q) {
+            lo[q] = up[q];
+            lo1[q] = up1[q];
+        }
     }
 }
 
@@ -355,7 +407,12 @@ int lsr_prep_surface_energy(const SlParams& P, const double* phi, const double* 
     if (!W.scal) EN_TRY(cudaMalloc(&W.scal, sizeof(int) * 2));
     EN_TRY(cudaMemsetAsync(W.scal, 0, sizeof(int) * 2, s));
     const int T = 256;
-    if (P.dim == 3 && P.nx % 4 == 0) {
+    static const bool march = !(std::getenv("LSR_FLAG_MARCH") && std::atoi(std::getenv("LSR_FLAG_MARCH")) == 0);
+    if (P.dim == 3 && P.nx % 4 == 0 && march) {
+        const unsigned tpr = static_cast<unsigned>((P.nx - 1 + 3) / 4);
+        const long long nt = static_cast<long long>(P.ny - 1) * tpr * ((P.nz - 1 + kMarchCells - 1) / kMarchCells);
+        flag_cells_march<<<static_cast<unsigned>((nt + T - 1) / T), T, 0, s>>>(P, phi, tpr, W.flags);
+    } else if (P.dim == 3 && P.nx % 4 == 0) {
         const unsigned tpr = static_cast<unsigned>((P.nx - 1 + 3) / 4);
         const long long nt = static_cast<long long>(P.ny - 1) * (P.nz - 1) * tpr;
         flag_cells4<<<static_cast<unsigned>((nt + T - 1) / T), T, 0, s>>>(P, phi, tpr, nt, W.flags);
