@@ -380,6 +380,10 @@ int lsr_prep_surface_energy(const SlParams& P, const double* phi, const double* 
         return LSR_ERR_CONFIG;
     }
     const long long ncells = static_cast<long long>(P.nx - 1) * (P.ny - 1) * (P.dim == 3 ? (P.nz - 1) : 1);
+    if (ncells > 0x7fffffffLL) {  // interface cell ids are kept as int
+        *err = "surface_energy: grids of 2^31 cells or more are not supported";
+        return LSR_ERR_CONFIG;
+    }
     // process-wide workspace, grown on demand (no per-call cudaMalloc)
     static std::mutex mu;
     static struct Work {
