@@ -18,6 +18,8 @@
 //    the other orderings) gives every node exactly the same inputs, and
 //    nodes of one hyperplane are independent. max_change is a max (order
 //    free), accumulated with an integer atomicMax on the non-negative bits.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <cub/cub.cuh>
@@ -242,16 +244,46 @@ __global__ void sweep_plane(GridP G, int ord, int s, int k_lo, int k_cnt, double
 #define LSR_SWEEP_TILE 16
 #endif
 constexpr int kTile = LSR_SWEEP_TILE;
-constexpr int kTH = kTile + 2;
+#ifndef LSR_SWEEP_TMA_FLAGS
+#define LSR_SWEEP_TMA_FLAGS 1
+#endif
+constexpr int kTH = kTile + 2;   // y and z extent of the box + halo
+constexpr int kTHX = kTile + 4;  // x extent: the box starts two nodes early so its start stays 16-byte aligned
 
-__global__ void __launch_bounds__(kTile * kTile) sweep_tiles(GridP G, int ord, int S, int nti, int ntj, int ntk,
-                                                             int tk_lo, double sentinel,
-                                                             const unsigned char* __restrict__ exact,
+// dynamic shared memory of one tile: the box + halo of d, the box's exact
+// flags, the TMA mbarrier and the per-warp maxima
+constexpr int kSdBytes = kTH * kTH * kTHX * 8;
+constexpr int kSdOff = 128;  // after the mbarrier and the per-warp maxima; TMA destinations are 128-byte aligned
+constexpr int kSxOff = kSdOff + (kSdBytes + 127) / 128 * 128;
+constexpr int kSxBytes = kTile * kTile * kTile;
+constexpr int kTileSmem = kSxOff + kSxBytes;
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+
+// With kTma the box + halo of d (kTH x kTH x kTHX doubles) and the box's
+// exact flags (kTile^3 bytes) arrive by two TMA tensor copies
+// (cp.async.bulk.tensor) on one mbarrier; otherwise by per-thread loads. A
+// TMA box must start at a non-negative coordinate whose innermost offset is
+// 16-byte aligned (an odd fp64 x start faults with an illegal instruction),
+// so along x the box starts two nodes before the tile (the tile starts at a
+// multiple of 16 when nx % 16 == 0) and along any axis where that start
+// would be negative it starts at 0 and the shared-memory index shifts (the
+// nodes before 0 are outside the grid and never read; the box then reaches
+// past the far halo, zero-filled or unused).
+template <bool kTma>
+__global__ void __launch_bounds__(kTile * kTile) sweep_tiles(const __grid_constant__ CUtensorMap tmap_d,
+                                                             const __grid_constant__ CUtensorMap tmap_x, GridP G,
+                                                             int ord, int S, int nti, int ntj, int ntk, int tk_lo,
+                                                             double sentinel, const unsigned char* __restrict__ exact,
                                                              double* __restrict__ d,
                                                              unsigned long long* __restrict__ max_change) {
-    __shared__ double sd[kTH * kTH * kTH];
-    __shared__ unsigned sx[kTile * kTile * kTile / 32];  // the box's exact flags, one bit per node
-    __shared__ unsigned long long wmax[kTile * kTile / 32];
+    extern __shared__ __align__(128) unsigned char smem[];
+    unsigned long long* mbar = reinterpret_cast<unsigned long long*>(smem);
+    unsigned long long* wmax = mbar + 1;
+    double* sd = reinterpret_cast<double*>(smem + kSdOff);
+    unsigned char* sx = smem + kSxOff;
     const int tkp = tk_lo + blockIdx.x / ntj, tjp = blockIdx.x % ntj;
     const int tip = S - tjp - tkp;
     if (tip < 0 || tip >= nti || tkp >= ntk) return;  // uniform per CTA
@@ -264,26 +296,64 @@ __global__ void __launch_bounds__(kTile * kTile) sweep_tiles(GridP G, int ord, i
         bsz[a] = mhi - mlo[a];
         lo[a] = (ord >> a) & 1 ? n3[a] - mhi : mlo[a];
     }
-    // box + halo into shared memory (outside the grid: never read)
-    for (int e = threadIdx.x; e < kTH * kTH * kTH; e += blockDim.x) {
-        const int hz = e / (kTH * kTH), hy = (e / kTH) % kTH, hx = e % kTH;
-        const int gx = lo[0] - 1 + hx, gy = lo[1] - 1 + hy, gz = lo[2] - 1 + hz;
-        if (hx <= bsz[0] + 1 && hy <= bsz[1] + 1 && hz <= bsz[2] + 1 && gx >= 0 && gx < G.nx && gy >= 0 &&
-            gy < G.ny && gz >= 0 && gz < G.nz)
-            sd[e] = d[(static_cast<long long>(gz) * G.ny + gy) * G.nx + gx];
-    }
-    // the flags too: a global load inside the plane loop would put its
-    // latency on every one of the 3*kTile-2 dependent steps
-    for (int w = threadIdx.x; w < kTile * kTile * kTile / 32; w += blockDim.x) sx[w] = 0u;
-    __syncthreads();
-    for (int e = threadIdx.x; e < bsz[0] * bsz[1] * bsz[2]; e += blockDim.x) {
-        const int z = e / (bsz[0] * bsz[1]), y = (e / bsz[0]) % bsz[1], x = e % bsz[0];
-        if (exact[(static_cast<long long>(lo[2] + z) * G.ny + lo[1] + y) * G.nx + lo[0] + x]) {
-            const int b = (z * kTile + y) * kTile + x;
-            atomicOr(sx + (b >> 5), 1u << (b & 31));
+    // box start per axis (x two nodes early, y and z one) and the shared index
+    // of the real local node (l0, l1, l2), l in [-1, kTile]
+    const int bx0 = kTma ? max(lo[0] - 2, 0) : lo[0] - 2, by0 = kTma ? max(lo[1] - 1, 0) : lo[1] - 1,
+              bz0 = kTma ? max(lo[2] - 1, 0) : lo[2] - 1;
+    const int ebase = ((lo[2] - bz0) * kTH + lo[1] - by0) * kTHX + lo[0] - bx0;
+    if (kTma) {
+        if (threadIdx.x == 0) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(mbar)));
+            asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
         }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(mbar)),
+                         "r"(kSdBytes + (LSR_SWEEP_TMA_FLAGS ? kSxBytes : 0))
+                         : "memory");
+            asm volatile(
+                "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+                "[%5];\n" ::"r"(smem_u32(sd)),
+                "l"(reinterpret_cast<unsigned long long>(&tmap_d)), "r"(bx0), "r"(by0), "r"(bz0), "r"(smem_u32(mbar))
+                : "memory");
+#if LSR_SWEEP_TMA_FLAGS
+            asm volatile(
+                "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+                "[%5];\n" ::"r"(smem_u32(sx)),
+                "l"(reinterpret_cast<unsigned long long>(&tmap_x)), "r"(lo[0]), "r"(lo[1]), "r"(lo[2]), "r"(smem_u32(mbar))
+                : "memory");
+#endif
+        }
+        asm volatile(
+            "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n @!p bra WAIT_%=;\n}\n" ::"r"(
+                smem_u32(mbar))
+            : "memory");
+#if !LSR_SWEEP_TMA_FLAGS
+        for (int e = threadIdx.x; e < bsz[0] * bsz[1] * bsz[2]; e += blockDim.x) {
+            const int z = e / (bsz[0] * bsz[1]), y = (e / bsz[0]) % bsz[1], x = e % bsz[0];
+            sx[(z * kTile + y) * kTile + x] =
+                exact[(static_cast<long long>(lo[2] + z) * G.ny + lo[1] + y) * G.nx + lo[0] + x];
+        }
+        __syncthreads();
+#endif
+    } else {
+        // box + halo into shared memory (outside the grid: never read)
+        for (int e = threadIdx.x; e < kTH * kTH * kTHX; e += blockDim.x) {
+            const int hz = e / (kTH * kTHX), hy = (e / kTHX) % kTH, hx = e % kTHX;
+            const int gx = bx0 + hx, gy = by0 + hy, gz = bz0 + hz;
+            if (hx >= 1 && hx <= bsz[0] + 2 && hy <= bsz[1] + 1 && hz <= bsz[2] + 1 && gx >= 0 && gx < G.nx &&
+                gy >= 0 && gy < G.ny && gz >= 0 && gz < G.nz)
+                sd[e] = d[(static_cast<long long>(gz) * G.ny + gy) * G.nx + gx];
+        }
+        // the flags too: a global load inside the plane loop would put its
+        // latency on every one of the 3*kTile-2 dependent steps
+        for (int e = threadIdx.x; e < bsz[0] * bsz[1] * bsz[2]; e += blockDim.x) {
+            const int z = e / (bsz[0] * bsz[1]), y = (e / bsz[0]) % bsz[1], x = e % bsz[0];
+            sx[(z * kTile + y) * kTile + x] =
+                exact[(static_cast<long long>(lo[2] + z) * G.ny + lo[1] + y) * G.nx + lo[0] + x];
+        }
+        __syncthreads();
     }
-    __syncthreads();
     const int ljp = threadIdx.x % kTile, lkp = threadIdx.x / kTile;  // this thread's mirrored row
     const bool row_ok = ljp < bsz[1] && lkp < bsz[2];
     const int lj = (ord & 2) ? bsz[1] - 1 - ljp : ljp, lk = (ord & 4) ? bsz[2] - 1 - lkp : lkp;
@@ -295,9 +365,8 @@ __global__ void __launch_bounds__(kTile * kTile) sweep_tiles(GridP G, int ord, i
         if (row_ok && lip >= 0 && lip < bsz[0]) {
             const int li = (ord & 1) ? bsz[0] - 1 - lip : lip;
             const int gi = lo[0] + li;
-            const int b = (lk * kTile + lj) * kTile + li;
-            if (!((sx[b >> 5] >> (b & 31)) & 1u)) {
-                const int e = ((lk + 1) * kTH + lj + 1) * kTH + li + 1;
+            if (!sx[(lk * kTile + lj) * kTile + li]) {
+                const int e = ebase + (lk * kTH + lj) * kTHX + li;
                 double a[3];
                 int m = 0;
                 {
@@ -308,14 +377,14 @@ __global__ void __launch_bounds__(kTile * kTile) sweep_tiles(GridP G, int ord, i
                 }
                 {
                     double best = sentinel;
-                    if (gj > 0) best = dmin(best, sd[e - kTH]);
-                    if (gj < G.ny - 1) best = dmin(best, sd[e + kTH]);
+                    if (gj > 0) best = dmin(best, sd[e - kTHX]);
+                    if (gj < G.ny - 1) best = dmin(best, sd[e + kTHX]);
                     if (best < sentinel) a[m++] = best;
                 }
                 {
                     double best = sentinel;
-                    if (gk > 0) best = dmin(best, sd[e - kTH * kTH]);
-                    if (gk < G.nz - 1) best = dmin(best, sd[e + kTH * kTH]);
+                    if (gk > 0) best = dmin(best, sd[e - kTH * kTHX]);
+                    if (gk < G.nz - 1) best = dmin(best, sd[e + kTH * kTHX]);
                     if (best < sentinel) a[m++] = best;
                 }
                 if (m > 0) {
@@ -341,7 +410,7 @@ __global__ void __launch_bounds__(kTile * kTile) sweep_tiles(GridP G, int ord, i
     for (int e = threadIdx.x; e < bsz[0] * bsz[1] * bsz[2]; e += blockDim.x) {
         const int z = e / (bsz[0] * bsz[1]), y = (e / bsz[0]) % bsz[1], x = e % bsz[0];
         d[(static_cast<long long>(lo[2] + z) * G.ny + lo[1] + y) * G.nx + lo[0] + x] =
-            sd[((z + 1) * kTH + y + 1) * kTH + x + 1];
+            sd[ebase + (z * kTH + y) * kTHX + x];
     }
     // the largest change: one atomic per CTA (max is order free)
     for (int off = 16; off > 0; off >>= 1) {
@@ -356,6 +425,42 @@ __global__ void __launch_bounds__(kTile * kTile) sweep_tiles(GridP G, int ord, i
         if (mm) atomicMax(max_change, mm);
     }
 }
+
+}  // namespace
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda
+// link dependency)
+static bool make_tile_maps(const GridP& G, double* d, unsigned char* exact, CUtensorMap* maps) {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        // the 12.0 ABI of the symbol (the typedef below), whatever the driver's default
+        if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &fn, 12000, cudaEnableDefault, &q) !=
+                cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            return static_cast<PFN_cuTensorMapEncodeTiled_v12000>(nullptr);
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }();
+    if (!encode) return false;
+    const cuuint64_t dims[3] = {static_cast<cuuint64_t>(G.nx), static_cast<cuuint64_t>(G.ny),
+                                static_cast<cuuint64_t>(G.nz)};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    const cuuint64_t sd_str[2] = {static_cast<cuuint64_t>(G.nx) * 8, static_cast<cuuint64_t>(G.nxy) * 8};
+    const cuuint32_t sd_box[3] = {kTHX, kTH, kTH};
+    const cuuint64_t sx_str[2] = {static_cast<cuuint64_t>(G.nx), static_cast<cuuint64_t>(G.nxy)};
+    const cuuint32_t sx_box[3] = {kTile, kTile, kTile};
+    if (encode(&maps[0], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, d, dims, sd_str, sd_box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return false;
+    if (encode(&maps[1], CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, exact, dims, sx_str, sx_box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return false;
+    return true;
+}
+
+namespace {
 
 // estimate_resolution's terms (cloud.cpp:473-476): the exact NN distance of
 // sampled point idx[i] to the rest of the cloud
@@ -506,6 +611,20 @@ int lsr_prep_build_distance(const lsr_grid* g, const double* h_pts, int64_t n, i
     const double tol = 1e-3 * g->dx;
     const int max_rounds = 8;
     static const bool tiled = !(std::getenv("LSR_SWEEP_TILES") && std::atoi(std::getenv("LSR_SWEEP_TILES")) == 0);
+    // TMA tensor maps of d (fp64) and the exact flags (u8) over the grid for
+    // the tiled sweep; global strides must be multiples of 16 bytes
+    CUtensorMap tmaps[2] = {};
+    bool use_tma = false;
+    if (G.dim == 3 && tiled) {
+        static const int tma_env = std::getenv("LSR_SWEEP_TMA") ? std::atoi(std::getenv("LSR_SWEEP_TMA")) : 1;
+        use_tma = tma_env != 0 && G.nx % 16 == 0 && make_tile_maps(G, d_field, d_exact, tmaps);
+        static bool attr_set = false;
+        if (!attr_set) {
+            PREP_TRY(cudaFuncSetAttribute(sweep_tiles<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTileSmem));
+            PREP_TRY(cudaFuncSetAttribute(sweep_tiles<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTileSmem));
+            attr_set = true;
+        }
+    }
     const int smax = (G.nx - 1) + (G.ny - 1) + (G.dim == 3 ? G.nz - 1 : 0);
     int round = 0;
     for (; round < max_rounds; ++round) {
@@ -517,8 +636,12 @@ int lsr_prep_build_distance(const lsr_grid* g, const double* h_pts, int64_t n, i
                 for (int S = 0; S <= (nti - 1) + (ntj - 1) + (ntk - 1); ++S) {
                     const int tk_lo = std::max(0, S - (nti - 1) - (ntj - 1)), tk_hi = std::min(ntk - 1, S);
                     const unsigned ctas = static_cast<unsigned>((tk_hi - tk_lo + 1) * ntj);
-                    sweep_tiles<<<ctas, kTile * kTile, 0, s>>>(G, ord, S, nti, ntj, ntk, tk_lo, sentinel, d_exact,
-                                                               d_field, dmax);
+                    if (use_tma)
+                        sweep_tiles<true><<<ctas, kTile * kTile, kTileSmem, s>>>(
+                            tmaps[0], tmaps[1], G, ord, S, nti, ntj, ntk, tk_lo, sentinel, d_exact, d_field, dmax);
+                    else
+                        sweep_tiles<false><<<ctas, kTile * kTile, kTileSmem, s>>>(
+                            tmaps[0], tmaps[1], G, ord, S, nti, ntj, ntk, tk_lo, sentinel, d_exact, d_field, dmax);
                     lsr_note_launch();
                 }
                 continue;
