@@ -176,6 +176,7 @@ def run_ours(args):
 
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
     halo = 0
+    table_ms = []  # z-line table fill per step (3d WENO, inside the step, outside the SL kernel)
     if world == 1:
         mine = active
         ctx.set_active(mine)
@@ -183,6 +184,7 @@ def run_ours(args):
         def one_step(i):
             ctx.sl_step(step, e2)
             ctx.swap()
+            table_ms.append(ctx.last_table_ms())
             return ctx.last_times()[0]
     else:
         # z-slabs (paper_2410_22205_b200/zslab.py): slab-sized resident buffers,
@@ -340,7 +342,10 @@ def run_ours(args):
                 "peak_source": peak_kind,
                 "algorithmic_bytes_per_update": bpu,
                 "kernel_ms_avg": kern_avg_ms,
-                "note": "reference-access bytes per node-update (SURVEY 8(d)); the kernel is fp64-pipe bound",
+                "table_fill_ms_avg": float(np.mean(table_ms[-args.steps:])) if table_ms else None,
+                "note": "reference-access bytes per node-update (SURVEY 8(d)) over the SL kernel's time; the "
+                        "kernel is fp64-pipe bound. The step (value, ms_per_step) also holds the z-line table "
+                        "fill (table_fill_ms_avg) and the sparse resync",
             },
             "gpu_launches": int(launches),
             "clocks": clk.summary(),

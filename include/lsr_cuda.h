@@ -124,6 +124,9 @@ int lsr_cuda_swap(lsr_cuda_ctx* ctx);
 /* device time (ms, CUDA events on the context stream) of the last SL kernel
  * and of the last whole sl_step (sync of out + kernel) */
 int lsr_cuda_last_times(lsr_cuda_ctx* ctx, float* kernel_ms, float* step_ms);
+/* device time (ms) of the last step's z-line table fill (3d WENO; 0 when the
+ * step did not use the table); it is part of step_ms, not of kernel_ms */
+int lsr_cuda_last_table_ms(lsr_cuda_ctx* ctx, float* table_ms);
 
 /* ---- raw device entry (slab / multi-GPU plumbing) ----
  * Fields hold global planes [z_base, z_base + z_planes) of `grid` (3d) — a

@@ -113,6 +113,7 @@ def lib() -> C.CDLL:
     L.lsr_cuda_sl_step.argtypes = [C.c_void_p, P(CStepCfg), C.c_double, P(C.c_int64)]
     L.lsr_cuda_swap.argtypes = [C.c_void_p]
     L.lsr_cuda_last_times.argtypes = [C.c_void_p, P(C.c_float), P(C.c_float)]
+    L.lsr_cuda_last_table_ms.argtypes = [C.c_void_p, P(C.c_float)]
     L.lsr_cuda_sl_step_device.argtypes = [P(CGrid), C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
                                           C.c_int64, P(CStepCfg), C.c_double, C.c_void_p, C.c_void_p, C.c_void_p,
                                           C.c_void_p]
@@ -565,3 +566,9 @@ class Context:
         k, s = C.c_float(), C.c_float()
         _check(lib().lsr_cuda_last_times(self.h, C.byref(k), C.byref(s)))
         return k.value, s.value
+
+    def last_table_ms(self) -> float:
+        """Device time of the last step's z-line table fill (part of the step)."""
+        t = C.c_float()
+        _check(lib().lsr_cuda_last_table_ms(self.h, C.byref(t)))
+        return t.value

@@ -153,8 +153,8 @@ struct lsr_cuda_ctx {
     unsigned long long* h_bad = nullptr;  // pinned
     cudaStream_t own = nullptr;
     cudaStream_t stream = nullptr;
-    cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
-    float kernel_ms = 0.f, step_ms = 0.f;
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};  // start, resynced, table filled, SL done
+    float kernel_ms = 0.f, step_ms = 0.f, table_ms = 0.f;
     int64_t n_interface_cells = 0;
     BandBuffers band;        // last narrow_band built on the device
     ReinitBuffers rb;        // reinitialisation scratch
@@ -182,6 +182,8 @@ struct lsr_cuda_ctx {
     int64_t cap_hres = 0, cap_dres = 0;
     unsigned long long* bm = nullptr;  // node bitmaps of the zero-copy pull (transfer.cu)
     int64_t cap_bm = 0;
+    ZtBuffers zt{};  // z-line table of the 3d WENO path (sl_launch.h)
+    bool zt_bricks = false;  // zt.list holds the bricks of the current active set
 };
 
 namespace {
@@ -236,7 +238,7 @@ int lsr_cuda_create(int device, const lsr_grid* grid, lsr_cuda_ctx** out) {
     if (e == cudaSuccess) e = cudaMalloc(&c->d_bad, sizeof(unsigned long long));
     if (e == cudaSuccess) e = cudaMallocHost(&c->h_bad, sizeof(unsigned long long));
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking);
-    for (int i = 0; i < 3 && e == cudaSuccess; ++i) e = cudaEventCreate(&c->ev[i]);
+    for (int i = 0; i < 4 && e == cudaSuccess; ++i) e = cudaEventCreate(&c->ev[i]);
     if (e != cudaSuccess) {
         lsr_cuda_destroy(c);
         return cuda_err(e, "lsr_cuda_create");
@@ -268,6 +270,11 @@ int lsr_cuda_destroy(lsr_cuda_ctx* c) {
     if (c->h_res) cudaFreeHost(c->h_res);
     cudaFree(c->d_res);
     cudaFree(c->bm);
+    cudaFree(c->zt.zt);
+    cudaFree(c->zt.zc);
+    cudaFree(c->zt.mark);
+    cudaFree(c->zt.list);
+    cudaFree(c->zt.count);
     for (auto& e : c->ev_down)
         if (e) cudaEventDestroy(e);
     for (auto& e : c->ev_up)
@@ -336,6 +343,7 @@ int lsr_cuda_set_active(lsr_cuda_ctx* c, const int64_t* ids, int64_t n) {
         LSR_CUDA_TRY(cudaMemcpyAsync(c->active, ids, sizeof(int64_t) * n, cudaMemcpyHostToDevice, c->stream));
     LSR_CUDA_TRY(cudaStreamSynchronize(c->stream));
     c->n_active = n;
+    c->zt_bricks = false;
     return LSR_OK;
 }
 
@@ -346,6 +354,7 @@ int lsr_cuda_set_active_device(lsr_cuda_ctx* c, const int64_t* d_ids, int64_t n)
     if (n > 0)
         LSR_CUDA_TRY(cudaMemcpyAsync(c->active, d_ids, sizeof(int64_t) * n, cudaMemcpyDeviceToDevice, c->stream));
     c->n_active = n;
+    c->zt_bricks = false;
     return LSR_OK;
 }
 
@@ -354,7 +363,7 @@ int lsr_cuda_sl_step(lsr_cuda_ctx* c, const lsr_step_cfg* cfg, double energy_p, 
     if (!c) return set_err(LSR_ERR_CONFIG, "null context");
     if (int st = check_cfg(cfg, energy_p)) return st;
     LSR_CUDA_TRY(cudaSetDevice(c->device));
-    const SlParams P = make_params(c->grid, *cfg, energy_p);
+    SlParams P = make_params(c->grid, *cfg, energy_p);
     cudaStream_t s = c->stream;
     LSR_CUDA_TRY(cudaEventRecord(c->ev[0], s));
     // "non-active nodes carry phi over" (evolve.cpp:50) without the O(N) copy
@@ -366,8 +375,29 @@ int lsr_cuda_sl_step(lsr_cuda_ctx* c, const lsr_step_cfg* cfg, double energy_p, 
     }
     LSR_CUDA_TRY(cudaMemsetAsync(c->d_bad, 0xff, sizeof(unsigned long long), s));
     LSR_CUDA_TRY(cudaEventRecord(c->ev[1], s));
-    LSR_CUDA_TRY(launch_sl_step(P, cfg->interp, c->phi, c->dist, c->active, c->n_active, c->out, c->d_bad, s));
+    // 3d WENO: the z-line table of phi on the bricks around the active set
+    // (sl_step.cu); the brick list depends on the ids only and is kept until
+    // the active set changes
+    const bool use_table = LSR_ZTAB && c->grid.dim == 3 && cfg->interp == 1 && P.fast_weno && c->grid.dims[2] >= 4;
+    if (use_table) {
+        if (!c->zt.zt) {
+            const long long nb = zt_num_bricks(c->grid.dims);
+            LSR_CUDA_TRY(cudaMalloc(&c->zt.zt, sizeof(double) * 4 * static_cast<size_t>(c->n)));
+            LSR_CUDA_TRY(cudaMalloc(&c->zt.zc, sizeof(double) * 2 * static_cast<size_t>(c->n)));
+            LSR_CUDA_TRY(cudaMalloc(&c->zt.mark, static_cast<size_t>(nb)));
+            LSR_CUDA_TRY(cudaMalloc(&c->zt.list, sizeof(unsigned) * static_cast<size_t>(nb)));
+            LSR_CUDA_TRY(cudaMalloc(&c->zt.count, 2 * sizeof(unsigned)));
+        }
+        if (!c->zt_bricks) LSR_CUDA_TRY(launch_zt_bricks(P, c->active, c->n_active, c->zt, s));
+        c->zt_bricks = true;
+        LSR_CUDA_TRY(launch_zt_fill(P, c->phi, c->zt, s));
+        P.ztab = c->zt.zt;
+        P.zcoef = c->zt.zc;
+        P.ztab_bad = c->zt.count + 1;
+    }
     LSR_CUDA_TRY(cudaEventRecord(c->ev[2], s));
+    LSR_CUDA_TRY(launch_sl_step(P, cfg->interp, c->phi, c->dist, c->active, c->n_active, c->out, c->d_bad, s));
+    LSR_CUDA_TRY(cudaEventRecord(c->ev[3], s));
     if (int st = ensure_ids(&c->dirty, &c->cap_dirty, c->n_active)) return st;
     if (c->n_active > 0)
         LSR_CUDA_TRY(cudaMemcpyAsync(c->dirty, c->active, sizeof(int64_t) * c->n_active, cudaMemcpyDeviceToDevice, s));
@@ -375,8 +405,10 @@ int lsr_cuda_sl_step(lsr_cuda_ctx* c, const lsr_step_cfg* cfg, double energy_p, 
     c->consistent = true;
     LSR_CUDA_TRY(cudaMemcpyAsync(c->h_bad, c->d_bad, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
     LSR_CUDA_TRY(cudaStreamSynchronize(s));
-    cudaEventElapsedTime(&c->kernel_ms, c->ev[1], c->ev[2]);
-    cudaEventElapsedTime(&c->step_ms, c->ev[0], c->ev[2]);
+    cudaEventElapsedTime(&c->kernel_ms, c->ev[2], c->ev[3]);
+    cudaEventElapsedTime(&c->step_ms, c->ev[0], c->ev[3]);
+    c->table_ms = 0.f;
+    if (use_table) cudaEventElapsedTime(&c->table_ms, c->ev[1], c->ev[2]);
     if (*c->h_bad != ~0ULL) return numerical_error(c->grid, *c->h_bad, bad_node);
     return LSR_OK;
 }
@@ -384,6 +416,12 @@ int lsr_cuda_sl_step(lsr_cuda_ctx* c, const lsr_step_cfg* cfg, double energy_p, 
 int lsr_cuda_swap(lsr_cuda_ctx* c) {
     if (!c) return set_err(LSR_ERR_CONFIG, "null context");
     std::swap(c->phi, c->out);  // out and phi still differ only at `dirty`
+    return LSR_OK;
+}
+
+int lsr_cuda_last_table_ms(lsr_cuda_ctx* c, float* table_ms) {
+    if (!c || !table_ms) return set_err(LSR_ERR_CONFIG, "null argument");
+    *table_ms = c->table_ms;
     return LSR_OK;
 }
 
@@ -630,6 +668,7 @@ static int sl_step_host_pipelined(lsr_cuda_ctx* c, const double* phi, const doub
     if (prefetch)
         LSR_CUDA_TRY(cudaMemcpyAsync(c->phi, phi, sizeof(double) * chunk_off(prefetch), cudaMemcpyHostToDevice, up));
     c->n_active = n_active;
+    c->zt_bricks = false;
     c->consistent = false;
     // per-chunk ranges of the (ascending) ids
     std::vector<int64_t> first(nch + 1);
@@ -920,6 +959,7 @@ int lsr_cuda_sl_step_host(const lsr_grid* grid, const double* phi, const double*
     if (n_active > 0)
         LSR_CUDA_TRY(cudaMemcpyAsync(c->active, active, sizeof(int64_t) * n_active, cudaMemcpyHostToDevice, s));
     c->n_active = n_active;
+    c->zt_bricks = false;
     c->consistent = false;
     int64_t bad = -1;
     const int st = lsr_cuda_sl_step(c, cfg, energy_p, &bad);
@@ -1021,6 +1061,7 @@ int lsr_cuda_narrow_band(lsr_cuda_ctx* c, int which, double gamma, int64_t* n_ac
         LSR_CUDA_TRY(cudaMemcpyAsync(c->active, c->band.active, sizeof(int64_t) * na, cudaMemcpyDeviceToDevice,
                                      c->stream));
     c->n_active = na;
+    c->zt_bricks = false;
     if (n_active) *n_active = na;
     if (n_tube) *n_tube = nt;
     return LSR_OK;

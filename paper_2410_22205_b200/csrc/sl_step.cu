@@ -39,12 +39,13 @@ __global__ void __launch_bounds__(kSlThreads, kSlMinBlocks) sl_step_kernel(SlPar
         j = static_cast<int>((id / P.nx) % P.ny);
         k = static_cast<int>(id / P.nxy);
     }
+    const bool use_zt = LSR_ZTAB && DIM == 3 && KIND == 1 && P.ztab != nullptr && __ldg(P.ztab_bad) == 0u;
     double* sb = nullptr;
     if (LSR_SMEM_FEET && DIM == 3 && KIND == 1) {  // per-thread double-buffered stencil columns
         __shared__ double sbuf[2 * 16 * kSlThreads];
         sb = sbuf + threadIdx.x;
     }
-    const double next = sl_node<DIM, KIND, kSlThreads>(P, phi, dist, id, i, j, k, sb);
+    const double next = sl_node<DIM, KIND, kSlThreads>(P, phi, dist, id, i, j, k, sb, use_zt);
     if (!isfinite(next)) atomicMin(bad, static_cast<unsigned long long>(id));
     out[id] = next;
     // fused halo exchange: the neighbours read these planes next step, so the
@@ -60,6 +61,112 @@ __global__ void __launch_bounds__(kSlThreads, kSlMinBlocks) sl_step_kernel(SlPar
         pushed = true;
     }
     if (pushed) __threadfence_system();
+}
+
+// The z-line table of the 3d WENO fast path. For node n = (i, j, k),
+// 1 <= k <= nz - 2, it holds the terms of weno1_fast that depend only on the
+// z-line data (interp.cpp:11-33), computed once per node instead of once per
+// z-line per foot (a node's z data is read by ~50 z-lines of nearby feet):
+//   zt[n] = {sd, S, Y, phi}: sd = phi(k-1) - 2 phi(k) + phi(k+1), the second
+//           difference of the lines whose v0 (sdl) or vp (sdr) is n;
+//           S = (sd^2/dx^2 + dx^2)^2 (the alpha denominator), Y = recip_seq(S)
+//   zc[n] = {c1, e2}: c1 = phi(k+1) - phi(k-1) (d1), e2 = -3 phi(k) +
+//           4 phi(k+1) - phi(k+2) (d2), for the line whose v0 is n
+// Same operations and operands as weno1_fast => same bits. A node outside
+// weno1_fast's range argument (square_in_range of sd^2, halvable c1/e2)
+// sets *bad, which switches the step back to the per-line arithmetic.
+//
+// The table is dense (indexed by node id) but written only on bricks of
+// kZtBrick^3 nodes: those holding an active node and their 26 neighbours,
+// which covers every stencil whose foot cell lies within kZtReach... of its
+// node (zt_cells_ok in sl_device.cuh); other feet take the per-line path.
+
+__device__ __forceinline__ long long brick_of(const SlParams& P, int i, int j, int k, int nbx, int nby) {
+    return (static_cast<long long>(k / kZtBrick) * nby + j / kZtBrick) * nbx + i / kZtBrick;
+}
+
+// mark[brick] = 1 for the brick of every active node
+__global__ void zt_mark_kernel(SlParams P, const int64_t* __restrict__ active, long long n, int nbx, int nby,
+                               unsigned char* __restrict__ mark) {
+    const long long a = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    long long b = -1;
+    if (a < n) {
+        int i, j, k;
+        unflatten(P, __ldg(active + a), i, j, k);
+        b = brick_of(P, i, j, k, nbx, nby);
+    }
+    const long long prev = __shfl_up_sync(0xffffffffu, b, 1);
+    if (b >= 0 && ((threadIdx.x & 31) == 0 || prev != b)) mark[b] = 1;  // same value: races are benign
+}
+
+// list = bricks with a marked brick in their 3x3x3 neighbourhood (any order)
+__global__ void zt_list_kernel(const unsigned char* __restrict__ mark, int nbx, int nby, int nbz,
+                               unsigned* __restrict__ list, unsigned* __restrict__ count) {
+    const long long b = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    bool hit = false;
+    if (b < static_cast<long long>(nbx) * nby * nbz) {
+        const int bi = static_cast<int>(b % nbx), bj = static_cast<int>((b / nbx) % nby),
+                  bk = static_cast<int>(b / (static_cast<long long>(nbx) * nby));
+        for (int dk = -1; dk <= 1 && !hit; ++dk)
+            for (int dj = -1; dj <= 1 && !hit; ++dj)
+                for (int di = -1; di <= 1 && !hit; ++di) {
+                    const int x = bi + di, y = bj + dj, z = bk + dk;
+                    if (x < 0 || y < 0 || z < 0 || x >= nbx || y >= nby || z >= nbz) continue;
+                    hit = mark[(static_cast<long long>(z) * nby + y) * nbx + x] != 0;
+                }
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, hit);
+    if (!m) return;
+    const int lane = threadIdx.x & 31;
+    unsigned base = 0;
+    if (lane == 0) base = atomicAdd(count, static_cast<unsigned>(__popc(m)));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (hit) list[base + __popc(m & ((1u << lane) - 1u))] = static_cast<unsigned>(b);
+}
+
+// the table entries of the listed bricks: one thread per (x, y) column of a
+// brick, marching up its kZtBrick planes with a sliding window of phi
+__global__ void __launch_bounds__(256) zt_fill_kernel(SlParams P, const double* __restrict__ phi,
+                                                      const unsigned* __restrict__ list,
+                                                      const unsigned* __restrict__ count, int nbx, int nby,
+                                                      double* __restrict__ zt, double* __restrict__ zc,
+                                                      unsigned* __restrict__ bad) {
+    constexpr int kCols = kZtBrick * kZtBrick;
+    const unsigned nb = *count;
+    const unsigned per_cta = blockDim.x / kCols;
+    const int c = threadIdx.x % kCols;
+    bool ok = true;
+    for (unsigned q = blockIdx.x * per_cta + threadIdx.x / kCols; q < nb; q += gridDim.x * per_cta) {
+        const unsigned b = __ldg(list + q);
+        const int bi = static_cast<int>(b % nbx), bj = static_cast<int>((b / nbx) % nby),
+                  bk = static_cast<int>(b / (static_cast<unsigned>(nbx) * nby));
+        const int i = bi * kZtBrick + c % kZtBrick, j = bj * kZtBrick + c / kZtBrick;
+        if (i >= P.nx || j >= P.ny) continue;
+        const int k0 = max(bk * kZtBrick, 1), k1 = min(bk * kZtBrick + kZtBrick, P.nz - 1);  // planes [k0, k1)
+        if (k0 >= k1) continue;
+        long long id = (static_cast<long long>(k0) * P.ny + j) * P.nx + i;
+        double vm = __ldg(phi + id - P.nxy), v0 = __ldg(phi + id), vp = __ldg(phi + id + P.nxy);
+        for (int k = k0; k < k1; ++k, id += P.nxy) {
+            const double vpp = k + 2 < P.nz ? __ldg(phi + id + 2 * P.nxy) : 0.0;
+            const double sd = vm - 2.0 * v0 + vp;  // weno1_fast's sdl / sdr
+            const double a = sqr(sd);
+            bool good = square_in_range(a);
+            double il = a * P.rdx2;
+            il = __fma_rn(__fma_rn(-il, P.dx2, a), P.rdx2, il);
+            const double S = sqr(il + P.dx2);
+            const double Y = recip_seq(S);
+            const double c1 = vp - vm;                      // d1
+            const double e2 = -3.0 * v0 + 4.0 * vp - vpp;  // d2
+            if (k + 2 < P.nz) good = good & halvable(c1) & halvable(e2);
+            ok = ok & good;
+            reinterpret_cast<double4*>(zt)[id] = make_double4(sd, S, Y, v0);
+            reinterpret_cast<double2*>(zc)[id] = make_double2(c1, e2);
+            vm = v0;
+            v0 = vp;
+            vp = vpp;
+        }
+    }
+    if (__any_sync(0xffffffffu, !ok) && (threadIdx.x & 31) == 0) atomicOr(bad, 1u);
 }
 
 // out[ids] = phi[ids]: re-establishes "out equals phi off the active set"
@@ -164,6 +271,32 @@ cudaError_t launch_sl_step(const SlParams& P, int kind, const double* phi, const
         if (kind == 0) sl_step_kernel<3, 0><<<blocks, kSlThreads, 0, stream>>>(P, phi, dist, active, n_active, out, bad);
         else sl_step_kernel<3, 1><<<blocks, kSlThreads, 0, stream>>>(P, phi, dist, active, n_active, out, bad);
     }
+    lsr_note_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_zt_bricks(const SlParams& P, const int64_t* active, long long n_active, const ZtBuffers& Z,
+                             cudaStream_t stream) {
+    const int nbx = (P.nx + kZtBrick - 1) / kZtBrick, nby = (P.ny + kZtBrick - 1) / kZtBrick,
+              nbz = (P.nz + kZtBrick - 1) / kZtBrick;
+    const long long nbricks = static_cast<long long>(nbx) * nby * nbz;
+    cudaError_t e = cudaMemsetAsync(Z.mark, 0, static_cast<size_t>(nbricks), stream);
+    if (e == cudaSuccess) e = cudaMemsetAsync(Z.count, 0, sizeof(unsigned), stream);
+    if (e != cudaSuccess || n_active <= 0) return e;
+    zt_mark_kernel<<<static_cast<unsigned>((n_active + 255) / 256), 256, 0, stream>>>(P, active, n_active, nbx, nby,
+                                                                                     Z.mark);
+    zt_list_kernel<<<static_cast<unsigned>((nbricks + 255) / 256), 256, 0, stream>>>(Z.mark, nbx, nby, nbz, Z.list,
+                                                                                    Z.count);
+    lsr_note_launch();
+    lsr_note_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_zt_fill(const SlParams& P, const double* phi, const ZtBuffers& Z, cudaStream_t stream) {
+    const int nbx = (P.nx + kZtBrick - 1) / kZtBrick, nby = (P.ny + kZtBrick - 1) / kZtBrick;
+    cudaError_t e = cudaMemsetAsync(Z.count + 1, 0, sizeof(unsigned), stream);
+    if (e != cudaSuccess) return e;
+    zt_fill_kernel<<<148 * 8, 256, 0, stream>>>(P, phi, Z.list, Z.count, nbx, nby, Z.zt, Z.zc, Z.count + 1);
     lsr_note_launch();
     return cudaGetLastError();
 }

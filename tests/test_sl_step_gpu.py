@@ -273,3 +273,90 @@ def test_pipelined_host_entry_exact(gpu, oracle, case, pinned):
                                      gamma=bp.gamma, beta=bp.beta), e)
     assert st == 0
     assert np.count_nonzero(bits(got) != bits(ref)) == 0
+
+
+# ---- z-line table of the 3d WENO path (sl_step.cu: zt_fill_kernel) ----------
+
+def _ctx_step(lsr, g, phi, dist, active, cfg, e):
+    ctx = lsr.Context(g)
+    try:
+        ctx.upload(0, phi)
+        ctx.upload(1, dist)
+        ctx.set_active(active)
+        ctx.sl_step(cfg, e)
+        return ctx.download(2), ctx.last_table_ms()
+    finally:
+        ctx.close()
+
+
+def _oracle_step(oracle, g, phi, dist, active, cfg, p, delta, e):
+    ref, st, _ = oracle.sl_step(dict(dim=3, dims=g.dims, origin=g.origin, dx=g.dx), phi, dist, active,
+                                dict(p=p, interp=1, delta=delta, dt=cfg.dt, fallback_c=1e-3, fallback_alpha=1.0,
+                                     gamma=cfg.band.gamma, beta=cfg.band.beta), e, nthreads=0)
+    assert st == 0
+    return ref
+
+
+@pytest.mark.parametrize("dt_dx,delta", [(0.25, 1.0), (3.0, 1.0), (12.0, 1.0)])
+def test_ztab_context_far_feet_exact(gpu, oracle, dt_dx, delta):
+    """Device-resident step with the z-line table: feet within the table's
+    brick coverage read it, farther feet (large dt) take the per-line
+    arithmetic; every node bit-identical to the reference either way."""
+    lsr = gpu
+    rng = np.random.default_rng(21)
+    g = lsr._api.cube_grid(72, 3)
+    x, y, z = (a.ravel() for a in g.mesh())
+    r = np.sqrt(x * x + y * y + z * z)
+    phi = r - 0.55 + 0.2 * g.dx * rng.standard_normal(x.size)
+    dist = np.abs(r - 0.3) + 0.02 * rng.random(x.size)
+    bp = lsr.default_band_params(3, g.dx)
+    active = np.flatnonzero(np.abs(phi) < bp.gamma).astype(np.int64)
+    cfg = lsr.StepConfig(p=2, delta=delta, dt=dt_dx * g.dx, interp=lsr.InterpolatorKind.Weno, band=bp)
+    got, tms = _ctx_step(lsr, g, phi, dist, active, cfg, 0.4)
+    assert tms > 0.0  # the table was built
+    ref = _oracle_step(oracle, g, phi, dist, active, cfg, 2, delta, 0.4)
+    assert np.count_nonzero(bits(got) != bits(ref)) == 0
+
+
+def test_ztab_out_of_range_data_falls_back_exact(gpu, oracle):
+    """Second differences whose squares fall below weno1_fast's range
+    (nonzero, < 2^-700) flag the table; the step takes the guarded per-line
+    path and stays bit-identical."""
+    lsr = gpu
+    rng = np.random.default_rng(5)
+    g = lsr._api.cube_grid(40, 3)
+    x, y, z = (a.ravel() for a in g.mesh())
+    r = np.sqrt(x * x + y * y + z * z)
+    phi = r - 0.5
+    tiny = np.flatnonzero(np.abs(z) < 0.3)
+    phi[tiny] = 1e-140 * (1.0 + rng.random(tiny.size))  # a slab of near-zero values
+    dist = np.abs(r - 0.3) + 0.01
+    bp = lsr.default_band_params(3, g.dx)
+    active = np.flatnonzero(np.abs(phi) < bp.gamma).astype(np.int64)
+    cfg = lsr.StepConfig(p=2, delta=1.0, dt=0.25 * g.dx, interp=lsr.InterpolatorKind.Weno, band=bp)
+    got, _ = _ctx_step(lsr, g, phi, dist, active, cfg, 0.6)
+    ref = _oracle_step(oracle, g, phi, dist, active, cfg, 2, 1.0, 0.6)
+    assert np.count_nonzero(bits(got) != bits(ref)) == 0
+
+
+def test_ztab_context_full_size_sampled_512(gpu, oracle):
+    """Config-4 size through the device-resident context (table path): a
+    random subset of the band vs the oracle, then the whole band against the
+    one-shot host path (which does not use the table), bit for bit."""
+    lsr = gpu
+    rng = np.random.default_rng(17)
+    g = lsr._api.cube_grid(512, 3)
+    ax = g.axes()
+    r = np.sqrt(ax[0][None, None, :] ** 2 + ax[1][None, :, None] ** 2 + ax[2][:, None, None] ** 2).ravel()
+    phi = r - 0.9
+    dist = np.abs(r - 0.5) + 1e-3 * np.cos(9 * r)
+    bp = lsr.default_band_params(3, g.dx)
+    band = np.flatnonzero(np.abs(phi) < bp.gamma).astype(np.int64)
+    sub = np.sort(rng.choice(band, 20000, replace=False)).astype(np.int64)
+    cfg = lsr.StepConfig(p=2, delta=1.0, dt=0.25 * g.dx, interp=lsr.InterpolatorKind.Weno, band=bp)
+    got, _ = _ctx_step(lsr, g, phi, dist, sub, cfg, 1.3)
+    ref = _oracle_step(oracle, g, phi, dist, sub, cfg, 2, 1.0, 1.3)
+    assert np.array_equal(bits(got[sub]), bits(ref[sub]))
+    whole, _ = _ctx_step(lsr, g, phi, dist, band, cfg, 1.3)
+    host = _run(lsr, g, phi, dist, band, cfg, 1.3)
+    assert np.array_equal(bits(whole), bits(host))
