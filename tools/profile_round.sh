@@ -9,8 +9,8 @@ R=${1:-r01}
 python bench.py > gpurun_out/bench_$R.json 2> gpurun_out/bench_$R.err
 CMD="python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu-baseline"
 $CMD > gpurun_out/plain_$R.log 2>&1 || exit 1
-ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"sl_step_kernel|resync_kernel|FillFunctor" \
-    -c 40 --csv --log-file gpurun_out/launches_$R.csv $CMD > gpurun_out/ncu_launch_$R.log 2>&1
+ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"sl_step_kernel|resync_kernel|zt_|FillFunctor" \
+    -c 60 --csv --log-file gpurun_out/launches_$R.csv $CMD > gpurun_out/ncu_launch_$R.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:sl_step_kernel -s 4 -c 1 \
     -o gpurun_out/sl_full_$R $CMD > gpurun_out/ncu_full_$R.log 2>&1
 tail -2 gpurun_out/ncu_full_$R.log
@@ -19,5 +19,5 @@ cat gpurun_out/bench_$R.json
 LOOP="python tools/loopbench.py --steps 2"
 $LOOP > gpurun_out/loop_plain_$R.log 2>&1 || exit 1
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
-    -k regex:"count_tiles|write_tiles|Scan|band_|flag_|contrib|block_partials|one_step|sign_|jacobi|iter_check|clamp_|sl_step|resync|copy_ids" \
+    -k regex:"count_tiles|write_tiles|Scan|band_|flag_|contrib|block_partials|one_step|sign_|jacobi|iter_check|clamp_|sl_step|resync|copy_ids|zt_" \
     --csv --log-file gpurun_out/loop_launches_$R.csv $LOOP > gpurun_out/ncu_loop_$R.log 2>&1
