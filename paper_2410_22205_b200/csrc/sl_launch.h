@@ -13,7 +13,11 @@
 #ifndef LSR_SL_MIN_BLOCKS
 #define LSR_SL_MIN_BLOCKS 7
 #endif
+#ifndef LSR_SL_MIN_BLOCKS_ZT
+#define LSR_SL_MIN_BLOCKS_ZT 9
+#endif
 constexpr int kSlThreads = LSR_SL_THREADS;
+constexpr int kSlMinBlocksZt = LSR_SL_MIN_BLOCKS_ZT;  // the same for the z-line-table kernel
 constexpr int kSlMinBlocks = LSR_SL_MIN_BLOCKS;  // resident CTAs per SM the register budget must allow
 
 // bumps the process-wide launch counter (lsr_cuda_kernel_launches)
