@@ -432,6 +432,73 @@ int lsr_cuda_last_times(lsr_cuda_ctx* c, float* kernel_ms, float* step_ms) {
     return LSR_OK;
 }
 
+namespace {
+
+// z-line table buffers of the stateless device entries (slab mode), one set
+// per host thread, device and stream (launches on one stream are ordered, so
+// reusing the set is safe), grown on demand; the brick list is rebuilt every
+// call since the caller's ids may change between calls
+struct SlabTable {
+    int device = -1;
+    cudaStream_t stream = nullptr;
+    long long nodes = 0, bricks = 0;
+    ZtBuffers Z{};
+    void release() {
+        cudaFree(Z.zt);
+        cudaFree(Z.zc);
+        cudaFree(Z.mark);
+        cudaFree(Z.list);
+        cudaFree(Z.count);
+        Z = ZtBuffers{};
+        nodes = bricks = 0;
+    }
+    ~SlabTable() { release(); }
+};
+thread_local std::vector<std::unique_ptr<SlabTable>> g_slab_tables;
+
+// attaches a z-line table of the resident planes to P (3d WENO only);
+// P.z_base/z_planes must be set, phi_g is the global-id-shifted phi
+int attach_slab_table(SlParams& P, const lsr_grid& g, int interp, const double* phi_g, const int64_t* d_active,
+                      int64_t n_active, cudaStream_t s) {
+    if (!(LSR_ZTAB && g.dim == 3 && interp == 1 && P.fast_weno && P.z_planes >= 4 && n_active > 0)) return LSR_OK;
+    int dev = 0;
+    LSR_CUDA_TRY(cudaGetDevice(&dev));
+    SlabTable* tp = nullptr;
+    for (auto& t : g_slab_tables)
+        if (t->device == dev && t->stream == s) tp = t.get();
+    if (!tp) {
+        g_slab_tables.push_back(std::make_unique<SlabTable>());
+        tp = g_slab_tables.back().get();
+        tp->device = dev;
+        tp->stream = s;
+    }
+    SlabTable& T = *tp;
+    const long long nodes = static_cast<long long>(P.z_planes) * P.nxy;
+    const long long bricks = zt_num_bricks(g.dims);
+    if (T.nodes < nodes || T.bricks < bricks) {
+        T.release();
+        LSR_CUDA_TRY(cudaMalloc(&T.Z.zt, sizeof(double) * 4 * static_cast<size_t>(nodes)));
+        LSR_CUDA_TRY(cudaMalloc(&T.Z.zc, sizeof(double) * 2 * static_cast<size_t>(nodes)));
+        LSR_CUDA_TRY(cudaMalloc(&T.Z.mark, static_cast<size_t>(bricks)));
+        LSR_CUDA_TRY(cudaMalloc(&T.Z.list, sizeof(unsigned) * static_cast<size_t>(bricks)));
+        LSR_CUDA_TRY(cudaMalloc(&T.Z.count, 2 * sizeof(unsigned)));
+        T.nodes = nodes;
+        T.bricks = bricks;
+    }
+    const long long shift = static_cast<long long>(P.z_base) * P.nxy;
+    ZtBuffers Zg = T.Z;  // indexed by global node id
+    Zg.zt -= 4 * shift;
+    Zg.zc -= 2 * shift;
+    LSR_CUDA_TRY(launch_zt_bricks(P, d_active, n_active, Zg, s));
+    LSR_CUDA_TRY(launch_zt_fill(P, phi_g, Zg, s));
+    P.ztab = Zg.zt;
+    P.zcoef = Zg.zc;
+    P.ztab_bad = T.Z.count + 1;
+    return LSR_OK;
+}
+
+}  // namespace
+
 int lsr_cuda_sl_step_device(const lsr_grid* grid, int32_t z_base, int32_t z_planes, const double* d_phi,
                             const double* d_dist, const int64_t* d_active, int64_t n_active,
                             const lsr_step_cfg* cfg, double energy_p, double* d_out, int64_t* d_bad_node,
@@ -449,6 +516,9 @@ int lsr_cuda_sl_step_device(const lsr_grid* grid, int32_t z_base, int32_t z_plan
     // the resident planes start at global plane z_base: shift the bases so
     // that global ids index them directly
     const long long shift = static_cast<long long>(z_base) * grid->dims[0] * grid->dims[1];
+    if (int st = attach_slab_table(P, *grid, cfg->interp, d_phi - shift, d_active, n_active,
+                                   static_cast<cudaStream_t>(stream)))
+        return st;
     LSR_CUDA_TRY(launch_sl_step(P, cfg->interp, d_phi - shift, d_dist - shift, d_active, n_active, d_out - shift,
                                 reinterpret_cast<unsigned long long*>(d_bad_node), static_cast<cudaStream_t>(stream)));
     return LSR_OK;
@@ -478,6 +548,9 @@ int lsr_cuda_sl_step_device_fused(const lsr_grid* grid, int32_t z_base, int32_t 
     P.push_lo_below = own_lo + push_lo_planes;
     P.push_hi_from = own_hi - push_hi_planes;
     const long long shift = static_cast<long long>(z_base) * nxy;
+    if (int st = attach_slab_table(P, *grid, cfg->interp, d_phi - shift, d_active, n_active,
+                                   static_cast<cudaStream_t>(stream)))
+        return st;
     LSR_CUDA_TRY(launch_sl_step(P, cfg->interp, d_phi - shift, d_dist - shift, d_active, n_active, d_out - shift,
                                 reinterpret_cast<unsigned long long*>(d_bad_node), static_cast<cudaStream_t>(stream)));
     return LSR_OK;

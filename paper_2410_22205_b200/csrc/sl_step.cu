@@ -144,12 +144,15 @@ __global__ void __launch_bounds__(256) zt_fill_kernel(SlParams P, const double* 
                   bk = static_cast<int>(b / (static_cast<unsigned>(nbx) * nby));
         const int i = bi * kZtBrick + c % kZtBrick, j = bj * kZtBrick + c / kZtBrick;
         if (i >= P.nx || j >= P.ny) continue;
-        const int k0 = max(bk * kZtBrick, 1), k1 = min(bk * kZtBrick + kZtBrick, P.nz - 1);  // planes [k0, k1)
+        // planes [k0, k1): interior planes whose z neighbours are resident
+        // (whole grid: 1 .. nz-2; slab mode: z_base+1 .. z_base+z_planes-2)
+        const int top = P.z_base + P.z_planes;
+        const int k0 = max(bk * kZtBrick, P.z_base + 1), k1 = min(bk * kZtBrick + kZtBrick, top - 1);
         if (k0 >= k1) continue;
         long long id = (static_cast<long long>(k0) * P.ny + j) * P.nx + i;
         double vm = __ldg(phi + id - P.nxy), v0 = __ldg(phi + id), vp = __ldg(phi + id + P.nxy);
         for (int k = k0; k < k1; ++k, id += P.nxy) {
-            const double vpp = k + 2 < P.nz ? __ldg(phi + id + 2 * P.nxy) : 0.0;
+            const double vpp = k + 2 < top ? __ldg(phi + id + 2 * P.nxy) : 0.0;
             const double sd = vm - 2.0 * v0 + vp;  // weno1_fast's sdl / sdr
             const double a = sqr(sd);
             bool good = square_in_range(a);
@@ -159,7 +162,7 @@ __global__ void __launch_bounds__(256) zt_fill_kernel(SlParams P, const double* 
             const double Y = recip_seq(S);
             const double c1 = vp - vm;                      // d1
             const double e2 = -3.0 * v0 + 4.0 * vp - vpp;  // d2
-            if (k + 2 < P.nz) good = good & halvable(c1) & halvable(e2);
+            if (k + 2 < top) good = good & halvable(c1) & halvable(e2);  // else e2 is never read (no stencil has K = k)
             ok = ok & good;
             reinterpret_cast<double4*>(zt)[id] = make_double4(sd, S, Y, v0);
             reinterpret_cast<double2*>(zc)[id] = make_double2(c1, e2);
