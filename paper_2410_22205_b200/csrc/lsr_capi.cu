@@ -121,6 +121,16 @@ SlParams make_params(const lsr_grid& g, const lsr_step_cfg& c, double energy_p) 
     return P;
 }
 
+// points the SL kernel at a filled z-line table
+void zt_attach(SlParams& P, const ZtBuffers& Z) {
+    P.ztab = Z.zt;
+    P.zcoef = Z.zc;
+    P.ztab_bad = Z.count + 1;
+    P.zt_cover = Z.mark;
+    P.zt_nbx = (P.nx + kZtBrick - 1) / kZtBrick;
+    P.zt_nby = (P.ny + kZtBrick - 1) / kZtBrick;
+}
+
 int numerical_error(const lsr_grid& g, unsigned long long bad, int64_t* bad_node) {
     if (bad_node) *bad_node = static_cast<int64_t>(bad);
     const int64_t id = static_cast<int64_t>(bad);
@@ -153,7 +163,7 @@ struct lsr_cuda_ctx {
     unsigned long long* h_bad = nullptr;  // pinned
     cudaStream_t own = nullptr;
     cudaStream_t stream = nullptr;
-    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};  // start, resynced, table filled, SL done
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};  // start, table filled, SL start, SL done
     float kernel_ms = 0.f, step_ms = 0.f, table_ms = 0.f;
     int64_t n_interface_cells = 0;
     BandBuffers band;        // last narrow_band built on the device
@@ -183,7 +193,10 @@ struct lsr_cuda_ctx {
     unsigned long long* bm = nullptr;  // node bitmaps of the zero-copy pull (transfer.cu)
     int64_t cap_bm = 0;
     ZtBuffers zt{};  // z-line table of the 3d WENO path (sl_launch.h)
-    bool zt_bricks = false;  // zt.list holds the bricks of the current active set
+    bool zt_bricks = false;  // zt.list holds the covered bricks of the current active set ...
+    double zt_key[4] = {0, 0, 0, 0};  // ... for this (E, dt, delta, p) (and the current d)
+    cudaStream_t s_aux = nullptr;  // resync beside the table fill
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 };
 
 namespace {
@@ -273,6 +286,7 @@ int lsr_cuda_destroy(lsr_cuda_ctx* c) {
     cudaFree(c->zt.zt);
     cudaFree(c->zt.zc);
     cudaFree(c->zt.mark);
+    cudaFree(c->zt.reach);
     cudaFree(c->zt.list);
     cudaFree(c->zt.count);
     for (auto& e : c->ev_down)
@@ -282,6 +296,9 @@ int lsr_cuda_destroy(lsr_cuda_ctx* c) {
     for (auto& e : c->ev_cmp)
         if (e) cudaEventDestroy(e);
     if (c->s_cmp) cudaStreamDestroy(c->s_cmp);
+    if (c->s_aux) cudaStreamDestroy(c->s_aux);
+    if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+    if (c->ev_join) cudaEventDestroy(c->ev_join);
     if (c->s_down) cudaStreamDestroy(c->s_down);
     cudaFree(c->active);
     cudaFree(c->dirty);
@@ -308,6 +325,7 @@ int lsr_cuda_upload_field(lsr_cuda_ctx* c, int which, const double* host) {
     LSR_CUDA_TRY(cudaMemcpyAsync(*slot, host, sizeof(double) * c->n, cudaMemcpyHostToDevice, c->stream));
     LSR_CUDA_TRY(cudaStreamSynchronize(c->stream));
     if (which != LSR_FIELD_DIST) c->consistent = false;
+    else c->zt_bricks = false;  // the covered bricks depend on d
     return LSR_OK;
 }
 
@@ -332,6 +350,7 @@ int lsr_cuda_field_ptr(lsr_cuda_ctx* c, int which, double** dptr) {
 int lsr_cuda_mark_dirty(lsr_cuda_ctx* c, int which) {
     if (!c) return set_err(LSR_ERR_CONFIG, "null context");
     if (which != LSR_FIELD_DIST) c->consistent = false;
+    else c->zt_bricks = false;
     return LSR_OK;
 }
 
@@ -365,35 +384,53 @@ int lsr_cuda_sl_step(lsr_cuda_ctx* c, const lsr_step_cfg* cfg, double energy_p, 
     LSR_CUDA_TRY(cudaSetDevice(c->device));
     SlParams P = make_params(c->grid, *cfg, energy_p);
     cudaStream_t s = c->stream;
+    const bool use_table = LSR_ZTAB && c->grid.dim == 3 && cfg->interp == 1 && P.fast_weno && c->grid.dims[2] >= 4;
+    if (use_table && !c->s_aux) {
+        LSR_CUDA_TRY(cudaStreamCreateWithFlags(&c->s_aux, cudaStreamNonBlocking));
+        LSR_CUDA_TRY(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+        LSR_CUDA_TRY(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+    }
+    // the resync runs beside the table fill (different buffers) on s_aux
+    cudaStream_t sr = use_table ? c->s_aux : s;
     LSR_CUDA_TRY(cudaEventRecord(c->ev[0], s));
+    if (use_table) {
+        LSR_CUDA_TRY(cudaEventRecord(c->ev_fork, s));
+        LSR_CUDA_TRY(cudaStreamWaitEvent(sr, c->ev_fork, 0));
+    }
     // "non-active nodes carry phi over" (evolve.cpp:50) without the O(N) copy
     // when out is known to equal phi except at the previous step's ids.
     if (!c->consistent) {
-        LSR_CUDA_TRY(cudaMemcpyAsync(c->out, c->phi, sizeof(double) * c->n, cudaMemcpyDeviceToDevice, s));
+        LSR_CUDA_TRY(cudaMemcpyAsync(c->out, c->phi, sizeof(double) * c->n, cudaMemcpyDeviceToDevice, sr));
     } else {
-        LSR_CUDA_TRY(launch_resync(c->phi, c->out, c->dirty, c->n_dirty, s));
+        LSR_CUDA_TRY(launch_resync(c->phi, c->out, c->dirty, c->n_dirty, sr));
     }
-    LSR_CUDA_TRY(cudaMemsetAsync(c->d_bad, 0xff, sizeof(unsigned long long), s));
-    LSR_CUDA_TRY(cudaEventRecord(c->ev[1], s));
+    LSR_CUDA_TRY(cudaMemsetAsync(c->d_bad, 0xff, sizeof(unsigned long long), sr));
     // 3d WENO: the z-line table of phi on the bricks around the active set
     // (sl_step.cu); the brick list depends on the ids only and is kept until
     // the active set changes
-    const bool use_table = LSR_ZTAB && c->grid.dim == 3 && cfg->interp == 1 && P.fast_weno && c->grid.dims[2] >= 4;
     if (use_table) {
         if (!c->zt.zt) {
             const long long nb = zt_num_bricks(c->grid.dims);
             LSR_CUDA_TRY(cudaMalloc(&c->zt.zt, sizeof(double) * 4 * static_cast<size_t>(c->n)));
             LSR_CUDA_TRY(cudaMalloc(&c->zt.zc, sizeof(double) * 2 * static_cast<size_t>(c->n)));
             LSR_CUDA_TRY(cudaMalloc(&c->zt.mark, static_cast<size_t>(nb)));
+            LSR_CUDA_TRY(cudaMalloc(&c->zt.reach, sizeof(unsigned) * static_cast<size_t>(nb)));
             LSR_CUDA_TRY(cudaMalloc(&c->zt.list, sizeof(unsigned) * static_cast<size_t>(nb)));
             LSR_CUDA_TRY(cudaMalloc(&c->zt.count, 2 * sizeof(unsigned)));
         }
-        if (!c->zt_bricks) LSR_CUDA_TRY(launch_zt_bricks(P, c->active, c->n_active, c->zt, s));
-        c->zt_bricks = true;
+        const double key[4] = {energy_p, cfg->dt, cfg->delta, static_cast<double>(cfg->p)};
+        if (!c->zt_bricks || std::memcmp(key, c->zt_key, sizeof key) != 0) {
+            LSR_CUDA_TRY(launch_zt_bricks(P, c->dist, c->active, c->n_active, c->zt, s));
+            std::memcpy(c->zt_key, key, sizeof key);
+            c->zt_bricks = true;
+        }
         LSR_CUDA_TRY(launch_zt_fill(P, c->phi, c->zt, s));
-        P.ztab = c->zt.zt;
-        P.zcoef = c->zt.zc;
-        P.ztab_bad = c->zt.count + 1;
+        zt_attach(P, c->zt);
+    }
+    LSR_CUDA_TRY(cudaEventRecord(c->ev[1], s));
+    if (use_table) {
+        LSR_CUDA_TRY(cudaEventRecord(c->ev_join, sr));
+        LSR_CUDA_TRY(cudaStreamWaitEvent(s, c->ev_join, 0));
     }
     LSR_CUDA_TRY(cudaEventRecord(c->ev[2], s));
     LSR_CUDA_TRY(launch_sl_step(P, cfg->interp, c->phi, c->dist, c->active, c->n_active, c->out, c->d_bad, s));
@@ -408,7 +445,7 @@ int lsr_cuda_sl_step(lsr_cuda_ctx* c, const lsr_step_cfg* cfg, double energy_p, 
     cudaEventElapsedTime(&c->kernel_ms, c->ev[2], c->ev[3]);
     cudaEventElapsedTime(&c->step_ms, c->ev[0], c->ev[3]);
     c->table_ms = 0.f;
-    if (use_table) cudaEventElapsedTime(&c->table_ms, c->ev[1], c->ev[2]);
+    if (use_table) cudaEventElapsedTime(&c->table_ms, c->ev[0], c->ev[1]);
     if (*c->h_bad != ~0ULL) return numerical_error(c->grid, *c->h_bad, bad_node);
     return LSR_OK;
 }
@@ -447,6 +484,7 @@ struct SlabTable {
         cudaFree(Z.zt);
         cudaFree(Z.zc);
         cudaFree(Z.mark);
+        cudaFree(Z.reach);
         cudaFree(Z.list);
         cudaFree(Z.count);
         Z = ZtBuffers{};
@@ -458,8 +496,8 @@ thread_local std::vector<std::unique_ptr<SlabTable>> g_slab_tables;
 
 // attaches a z-line table of the resident planes to P (3d WENO only);
 // P.z_base/z_planes must be set, phi_g is the global-id-shifted phi
-int attach_slab_table(SlParams& P, const lsr_grid& g, int interp, const double* phi_g, const int64_t* d_active,
-                      int64_t n_active, cudaStream_t s) {
+int attach_slab_table(SlParams& P, const lsr_grid& g, int interp, const double* phi_g, const double* dist_g,
+                      const int64_t* d_active, int64_t n_active, cudaStream_t s) {
     if (!(LSR_ZTAB && g.dim == 3 && interp == 1 && P.fast_weno && P.z_planes >= 4 && n_active > 0)) return LSR_OK;
     int dev = 0;
     LSR_CUDA_TRY(cudaGetDevice(&dev));
@@ -480,6 +518,7 @@ int attach_slab_table(SlParams& P, const lsr_grid& g, int interp, const double* 
         LSR_CUDA_TRY(cudaMalloc(&T.Z.zt, sizeof(double) * 4 * static_cast<size_t>(nodes)));
         LSR_CUDA_TRY(cudaMalloc(&T.Z.zc, sizeof(double) * 2 * static_cast<size_t>(nodes)));
         LSR_CUDA_TRY(cudaMalloc(&T.Z.mark, static_cast<size_t>(bricks)));
+        LSR_CUDA_TRY(cudaMalloc(&T.Z.reach, sizeof(unsigned) * static_cast<size_t>(bricks)));
         LSR_CUDA_TRY(cudaMalloc(&T.Z.list, sizeof(unsigned) * static_cast<size_t>(bricks)));
         LSR_CUDA_TRY(cudaMalloc(&T.Z.count, 2 * sizeof(unsigned)));
         T.nodes = nodes;
@@ -489,11 +528,9 @@ int attach_slab_table(SlParams& P, const lsr_grid& g, int interp, const double* 
     ZtBuffers Zg = T.Z;  // indexed by global node id
     Zg.zt -= 4 * shift;
     Zg.zc -= 2 * shift;
-    LSR_CUDA_TRY(launch_zt_bricks(P, d_active, n_active, Zg, s));
+    LSR_CUDA_TRY(launch_zt_bricks(P, dist_g, d_active, n_active, Zg, s));
     LSR_CUDA_TRY(launch_zt_fill(P, phi_g, Zg, s));
-    P.ztab = Zg.zt;
-    P.zcoef = Zg.zc;
-    P.ztab_bad = T.Z.count + 1;
+    zt_attach(P, Zg);
     return LSR_OK;
 }
 
@@ -516,7 +553,7 @@ int lsr_cuda_sl_step_device(const lsr_grid* grid, int32_t z_base, int32_t z_plan
     // the resident planes start at global plane z_base: shift the bases so
     // that global ids index them directly
     const long long shift = static_cast<long long>(z_base) * grid->dims[0] * grid->dims[1];
-    if (int st = attach_slab_table(P, *grid, cfg->interp, d_phi - shift, d_active, n_active,
+    if (int st = attach_slab_table(P, *grid, cfg->interp, d_phi - shift, d_dist - shift, d_active, n_active,
                                    static_cast<cudaStream_t>(stream)))
         return st;
     LSR_CUDA_TRY(launch_sl_step(P, cfg->interp, d_phi - shift, d_dist - shift, d_active, n_active, d_out - shift,
@@ -548,7 +585,7 @@ int lsr_cuda_sl_step_device_fused(const lsr_grid* grid, int32_t z_base, int32_t 
     P.push_lo_below = own_lo + push_lo_planes;
     P.push_hi_from = own_hi - push_hi_planes;
     const long long shift = static_cast<long long>(z_base) * nxy;
-    if (int st = attach_slab_table(P, *grid, cfg->interp, d_phi - shift, d_active, n_active,
+    if (int st = attach_slab_table(P, *grid, cfg->interp, d_phi - shift, d_dist - shift, d_active, n_active,
                                    static_cast<cudaStream_t>(stream)))
         return st;
     LSR_CUDA_TRY(launch_sl_step(P, cfg->interp, d_phi - shift, d_dist - shift, d_active, n_active, d_out - shift,
@@ -1053,6 +1090,7 @@ int lsr_cuda_ctx_build_distance(lsr_cuda_ctx* c, const double* pts, int64_t n, i
     if (!c || (n > 0 && !pts)) return set_err(LSR_ERR_CONFIG, "build_distance: null argument");
     LSR_CUDA_TRY(cudaSetDevice(c->device));
     if (!c->exact) LSR_CUDA_TRY(cudaMalloc(&c->exact, static_cast<size_t>(c->n)));
+    c->zt_bricks = false;  // the covered bricks depend on d
     std::string err;
     double sent = 0.0;
     int r = 0;
@@ -1163,6 +1201,7 @@ int lsr_cuda_clamp_field(lsr_cuda_ctx* c, int which, double gamma) {
     if (int st = lsr_clamp(*slot, c->n, gamma, c->stream, &err)) return set_err(st, err);
     LSR_CUDA_TRY(cudaStreamSynchronize(c->stream));
     if (which != LSR_FIELD_DIST) c->consistent = false;
+    else c->zt_bricks = false;  // the covered bricks depend on d
     return LSR_OK;
 }
 

@@ -28,13 +28,15 @@ cudaError_t launch_sl_step(const lsr_dev::SlParams& P, int kind, const double* p
                            cudaStream_t stream);
 
 // the z-line table of the 3d WENO fast path (sl_step.cu): dense zt (4
-// doubles per node) and zc (2 per node), written on the bricks around the
-// active nodes; mark = one byte per brick, list = one unsigned per brick,
-// count[0] = listed bricks, count[1] = range-check failures (SlParams::ztab_bad)
+// doubles per node) and zc (2 per node), written on the covered bricks;
+// reach = foot reach per brick (cells), mark = covered bricks (the SL
+// kernel's coverage map), list = covered brick ids, count[0] = listed
+// bricks, count[1] = range-check failures (SlParams::ztab_bad)
 struct ZtBuffers {
     double* zt;
     double* zc;
     unsigned char* mark;
+    unsigned* reach;
     unsigned* list;
     unsigned* count;
 };
@@ -42,9 +44,10 @@ inline long long zt_num_bricks(const int dims[3]) {
     return static_cast<long long>((dims[0] + kZtBrick - 1) / kZtBrick) * ((dims[1] + kZtBrick - 1) / kZtBrick) *
            ((dims[2] + kZtBrick - 1) / kZtBrick);
 }
-// brick list of an active set (depends on the ids only; cached by the context)
-cudaError_t launch_zt_bricks(const lsr_dev::SlParams& P, const int64_t* active, long long n_active, const ZtBuffers& Z,
-                             cudaStream_t stream);
+// covered bricks of an active set: depends on the ids, d, E and the step
+// config (P.energy, dt, delta, p), not on phi — the context caches it
+cudaError_t launch_zt_bricks(const lsr_dev::SlParams& P, const double* dist, const int64_t* active, long long n_active,
+                             const ZtBuffers& Z, cudaStream_t stream);
 // table entries of the listed bricks from phi (every step)
 cudaError_t launch_zt_fill(const lsr_dev::SlParams& P, const double* phi, const ZtBuffers& Z, cudaStream_t stream);
 

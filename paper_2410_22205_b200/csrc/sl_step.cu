@@ -79,44 +79,94 @@ __global__ void __launch_bounds__(kSlThreads, ZT ? kSlMinBlocksZt : kSlMinBlocks
 // sets *bad, which switches the step back to the per-line arithmetic.
 //
 // The table is dense (indexed by node id) but written only on bricks of
-// kZtBrick^3 nodes: those holding an active node and their 26 neighbours,
-// which covers every stencil whose foot cell lies within kZtReach... of its
-// node (zt_cells_ok in sl_device.cuh); other feet take the per-line path.
+// kZtBrick^3 nodes that some foot stencil may read: every active node bounds
+// how far its feet can land (zt_reach_kernel: from d, grad d, E and the step
+// config, evolve.cpp:83-101, with |nu1|, |nu2| <= 1), its brick keeps the
+// maximum, and each such brick covers the bricks its reach spans
+// (zt_cover_kernel). The SL kernel still checks, per foot, that the bricks
+// of the stencil's table nodes are covered (zt_covered in sl_device.cuh), so
+// the bound only decides speed, never the result: an uncovered foot takes
+// the per-line arithmetic, which gives the same bits.
 
-__device__ __forceinline__ long long brick_of(const SlParams& P, int i, int j, int k, int nbx, int nby) {
+__device__ __forceinline__ long long brick_of(int i, int j, int k, int nbx, int nby) {
     return (static_cast<long long>(k / kZtBrick) * nby + j / kZtBrick) * nbx + i / kZtBrick;
 }
 
-// mark[brick] = 1 for the brick of every active node
-__global__ void zt_mark_kernel(SlParams P, const int64_t* __restrict__ active, long long n, int nbx, int nby,
-                               unsigned char* __restrict__ mark) {
+// reach[brick] = max over its active nodes of the foot reach: with D the
+// bound on a foot's displacement in cells along any axis, a foot cell lies in
+// [i - ceil(D), i + floor(D)]; packed as ceil(D) << 8 | floor(D) (monotone in
+// D, so atomicMax keeps the largest), D capped at kZtMaxReach
+__global__ void zt_reach_kernel(SlParams P, const double* __restrict__ dist, const int64_t* __restrict__ active,
+                                long long n, int nbx, int nby, unsigned* __restrict__ reach) {
     const long long a = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
     long long b = -1;
+    unsigned r = 0;
     if (a < n) {
+        const long long id = __ldg(active + a);
         int i, j, k;
-        unflatten(P, __ldg(active + a), i, j, k);
-        b = brick_of(P, i, j, k, nbx, nby);
+        unflatten(P, id, i, j, k);
+        b = brick_of(i, j, k, nbx, nby);
+        const double d_j = __ldg(dist + id);
+        const double c_j = P.p == 1 ? 1.0 : d_j / P.energy;  // scale_factor (evolve.cpp:32-38)
+        const double s = c_j * P.dt;
+        const double spread = sqrt(fmax(0.0, c_j * P.delta * d_j * P.dt / P.pd));
+        double m = fabs(s * grad_axis(P, dist, id, i, P.nx, 1));
+        m = fmax(m, fabs(s * grad_axis(P, dist, id, j, P.ny, P.nx)));
+        if (P.dim == 3) m = fmax(m, fabs(s * grad_axis(P, dist, id, k, P.nz, P.nxy)));
+        // feet = base +- spread nu1 +- spread nu2 (evolve.cpp:96-101); per axis
+        // |nu1_x| + |nu2_x| <= sqrt(2) for orthonormal nu1, nu2
+        const double cells = (m + 1.4143 * spread) / P.dx;
+        if (cells < static_cast<double>(kZtMaxReach)) {
+            const unsigned fl = static_cast<unsigned>(floor(cells)), ce = static_cast<unsigned>(ceil(cells));
+            r = (ce << 8) | fl;
+        } else {
+            r = (kZtMaxReach << 8) | kZtMaxReach;
+        }
+        r = r ? r : 1u;  // a brick with an active node is nonzero
     }
-    const long long prev = __shfl_up_sync(0xffffffffu, b, 1);
-    if (b >= 0 && ((threadIdx.x & 31) == 0 || prev != b)) mark[b] = 1;  // same value: races are benign
+    // one atomic per (warp, brick): consecutive ids share bricks
+    const unsigned same = __match_any_sync(0xffffffffu, b);
+    const unsigned rmax = __reduce_max_sync(same, r);
+    if (b >= 0 && (threadIdx.x & 31) == static_cast<unsigned>(__ffs(same) - 1)) atomicMax(reach + b, rmax);
 }
 
-// list = bricks with a marked brick in their 3x3x3 neighbourhood (any order)
-__global__ void zt_list_kernel(const unsigned char* __restrict__ mark, int nbx, int nby, int nbz,
+__device__ __forceinline__ int floor_div(int a, int b) { return a >= 0 ? a / b : -((-a + b - 1) / b); }
+
+// a brick b0 whose feet reach [i - rn, i + rp] reads table nodes x, y in
+// [b0 - rn - 1, b0 + B - 1 + rp + 2] and z in [b0 - rn, b0 + B - 1 + rp + 1]
+// (stencil cell-1 .. cell+2; table at z = cell, cell+1); cover[] = 1 on the
+// bricks overlapping them (benign same-value races)
+__global__ void zt_cover_kernel(const unsigned* __restrict__ reach, int nbx, int nby, int nbz,
+                                unsigned char* __restrict__ cover) {
+    const long long b = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (b >= static_cast<long long>(nbx) * nby * nbz) return;
+    const unsigned r = reach[b];
+    if (r == 0) return;
+    const int rn = static_cast<int>(r >> 8), rp = static_cast<int>(r & 0xffu);
+    const int bi = static_cast<int>(b % nbx), bj = static_cast<int>((b / nbx) % nby),
+              bk = static_cast<int>(b / (static_cast<long long>(nbx) * nby));
+    const int lo = floor_div(-rn - 1, kZtBrick), hi = floor_div(kZtBrick + 1 + rp, kZtBrick);
+    const int loz = floor_div(-rn, kZtBrick), hiz = floor_div(kZtBrick + rp, kZtBrick);
+    for (int dk = loz; dk <= hiz; ++dk) {
+        const int z = bk + dk;
+        if (z < 0 || z >= nbz) continue;
+        for (int dj = lo; dj <= hi; ++dj) {
+            const int y = bj + dj;
+            if (y < 0 || y >= nby) continue;
+            for (int di = lo; di <= hi; ++di) {
+                const int x = bi + di;
+                if (x < 0 || x >= nbx) continue;
+                cover[(static_cast<long long>(z) * nby + y) * nbx + x] = 1;
+            }
+        }
+    }
+}
+
+// list = the covered bricks (any order)
+__global__ void zt_list_kernel(const unsigned char* __restrict__ cover, long long nbricks,
                                unsigned* __restrict__ list, unsigned* __restrict__ count) {
     const long long b = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-    bool hit = false;
-    if (b < static_cast<long long>(nbx) * nby * nbz) {
-        const int bi = static_cast<int>(b % nbx), bj = static_cast<int>((b / nbx) % nby),
-                  bk = static_cast<int>(b / (static_cast<long long>(nbx) * nby));
-        for (int dk = -1; dk <= 1 && !hit; ++dk)
-            for (int dj = -1; dj <= 1 && !hit; ++dj)
-                for (int di = -1; di <= 1 && !hit; ++di) {
-                    const int x = bi + di, y = bj + dj, z = bk + dk;
-                    if (x < 0 || y < 0 || z < 0 || x >= nbx || y >= nby || z >= nbz) continue;
-                    hit = mark[(static_cast<long long>(z) * nby + y) * nbx + x] != 0;
-                }
-    }
+    const bool hit = b < nbricks && cover[b] != 0;
     const unsigned m = __ballot_sync(0xffffffffu, hit);
     if (!m) return;
     const int lane = threadIdx.x & 31;
@@ -282,20 +332,21 @@ cudaError_t launch_sl_step(const SlParams& P, int kind, const double* phi, const
     return cudaGetLastError();
 }
 
-cudaError_t launch_zt_bricks(const SlParams& P, const int64_t* active, long long n_active, const ZtBuffers& Z,
-                             cudaStream_t stream) {
+cudaError_t launch_zt_bricks(const SlParams& P, const double* dist, const int64_t* active, long long n_active,
+                             const ZtBuffers& Z, cudaStream_t stream) {
     const int nbx = (P.nx + kZtBrick - 1) / kZtBrick, nby = (P.ny + kZtBrick - 1) / kZtBrick,
               nbz = (P.nz + kZtBrick - 1) / kZtBrick;
     const long long nbricks = static_cast<long long>(nbx) * nby * nbz;
     cudaError_t e = cudaMemsetAsync(Z.mark, 0, static_cast<size_t>(nbricks), stream);
+    if (e == cudaSuccess) e = cudaMemsetAsync(Z.reach, 0, sizeof(unsigned) * static_cast<size_t>(nbricks), stream);
     if (e == cudaSuccess) e = cudaMemsetAsync(Z.count, 0, sizeof(unsigned), stream);
     if (e != cudaSuccess || n_active <= 0) return e;
-    zt_mark_kernel<<<static_cast<unsigned>((n_active + 255) / 256), 256, 0, stream>>>(P, active, n_active, nbx, nby,
-                                                                                     Z.mark);
-    zt_list_kernel<<<static_cast<unsigned>((nbricks + 255) / 256), 256, 0, stream>>>(Z.mark, nbx, nby, nbz, Z.list,
-                                                                                    Z.count);
-    lsr_note_launch();
-    lsr_note_launch();
+    const unsigned gb = static_cast<unsigned>((nbricks + 255) / 256);
+    zt_reach_kernel<<<static_cast<unsigned>((n_active + 255) / 256), 256, 0, stream>>>(P, dist, active, n_active, nbx,
+                                                                                      nby, Z.reach);
+    zt_cover_kernel<<<gb, 256, 0, stream>>>(Z.reach, nbx, nby, nbz, Z.mark);
+    zt_list_kernel<<<gb, 256, 0, stream>>>(Z.mark, nbricks, Z.list, Z.count);
+    for (int r = 0; r < 3; ++r) lsr_note_launch();
     return cudaGetLastError();
 }
 
