@@ -117,3 +117,46 @@ def test_config4_512_loop_step_and_one_shot_vs_reference(gpu, reference):
     got = ctx.download(0)
     diff = np.count_nonzero(bits(got) != bits(ref_phi))
     assert diff == 0, f"{diff} nodes differ"
+
+
+def test_config5_1024_sampled_subset_vs_oracle(gpu, oracle):
+    """Config 5 at its full size (1024^3, 4 M-point union of three tori with
+    two holes, WENO, p = 2, delta = 1) through the device-resident context
+    (z-line table path, where feet reach up to ~6 cells at the poles):
+    a random subset of the band (sl_step reads only mask.active) against the
+    oracle, bit for bit, plus whole-band properties."""
+    lsr = gpu
+    rng = np.random.default_rng(55)
+    g = lsr.cube_grid(1024, 3)
+    pts = lsr.cloud_generate(5, 4_000_000, seed=2410, sigma=0.25 * g.dx)
+    ax = g.axes()
+    phi = (np.sqrt(ax[0][None, None, :] ** 2 + ax[1][None, :, None] ** 2 + ax[2][:, None, None] ** 2) - 0.95).ravel()
+    bp = lsr.default_band_params(3, g.dx)
+    band = np.flatnonzero(np.abs(phi) < bp.gamma).astype(np.int64)
+    sub = np.sort(rng.choice(band, 30000, replace=False)).astype(np.int64)
+    cfg = lsr.StepConfig(p=2, delta=1.0, dt=0.25 * g.dx, interp=lsr.InterpolatorKind.Weno, band=bp)
+    ctx = lsr.Context(g)
+    try:
+        ctx.build_distance(pts)
+        d = ctx.download(1)
+        ctx.upload(0, phi)
+        ctx.set_active(sub)
+        ctx.sl_step(cfg, 2.4)
+        assert ctx.last_table_ms() > 0.0
+        got = ctx.download(2)
+        ref, st, _ = oracle.sl_step(dict(dim=3, dims=g.dims, origin=g.origin, dx=g.dx), phi, d, sub,
+                                    dict(p=2, interp=1, delta=1.0, dt=cfg.dt, fallback_c=1e-3, fallback_alpha=1.0,
+                                         gamma=bp.gamma, beta=bp.beta), 2.4, nthreads=0)
+        assert st == 0
+        assert np.array_equal(bits(got[sub]), bits(ref[sub]))
+        del got, ref
+        # whole band: finite, off-band untouched, bounded update
+        ctx.set_active(band)
+        ctx.sl_step(cfg, 2.4)
+        out = ctx.download(2)
+        assert np.all(np.isfinite(out[band]))
+        changed = np.flatnonzero(out.view(np.int64) != phi.view(np.int64))
+        assert np.all(np.isin(changed, band, assume_unique=True))  # off-band nodes carry phi over
+        assert np.max(np.abs(out[band] - phi[band])) < 4 * g.dx
+    finally:
+        ctx.close()
