@@ -119,6 +119,17 @@ int lsr_cuda_set_active_device(lsr_cuda_ctx* ctx, const int64_t* d_ids, int64_t 
 /* lsr::sl_step(PHI, DIST, active, cfg, energy_p, OUT) */
 int lsr_cuda_sl_step(lsr_cuda_ctx* ctx, const lsr_step_cfg* cfg, double energy_p,
                      int64_t* bad_node);
+/* the same step enqueued without any host synchronisation (device-resident
+ * loops, CUDA-graph-style back-to-back submission); a non-finite update is
+ * reported by the next lsr_cuda_sync (smallest bad id over the pending
+ * steps). lsr_cuda_sl_step refuses to run while async steps are pending. */
+int lsr_cuda_sl_step_async(lsr_cuda_ctx* ctx, const lsr_step_cfg* cfg, double energy_p);
+/* waits for the pending async steps; LSR_ERR_NUMERICAL as lsr_cuda_sl_step */
+int lsr_cuda_sync(lsr_cuda_ctx* ctx, int64_t* bad_node);
+/* per-step device times (ms) of the async steps completed by the last sync:
+ * SL kernel, whole step, z-line table fill; *n = min(cap, count) */
+int lsr_cuda_async_times(lsr_cuda_ctx* ctx, float* kernel_ms, float* step_ms, float* table_ms, int cap,
+                         int* n);
 /* std::swap(phi.values, next.values) (driver.cpp:203): O(1) */
 int lsr_cuda_swap(lsr_cuda_ctx* ctx);
 /* device time (ms, CUDA events on the context stream) of the last SL kernel

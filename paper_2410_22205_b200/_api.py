@@ -112,6 +112,9 @@ def lib() -> C.CDLL:
     L.lsr_cuda_set_active_device.argtypes = [C.c_void_p, C.c_void_p, C.c_int64]
     L.lsr_cuda_sl_step.argtypes = [C.c_void_p, P(CStepCfg), C.c_double, P(C.c_int64)]
     L.lsr_cuda_swap.argtypes = [C.c_void_p]
+    L.lsr_cuda_sl_step_async.argtypes = [C.c_void_p, P(CStepCfg), C.c_double]
+    L.lsr_cuda_sync.argtypes = [C.c_void_p, P(C.c_int64)]
+    L.lsr_cuda_async_times.argtypes = [C.c_void_p, P(C.c_float), P(C.c_float), P(C.c_float), C.c_int, P(C.c_int)]
     L.lsr_cuda_last_times.argtypes = [C.c_void_p, P(C.c_float), P(C.c_float)]
     L.lsr_cuda_last_table_ms.argtypes = [C.c_void_p, P(C.c_float)]
     L.lsr_cuda_sl_step_device.argtypes = [P(CGrid), C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
@@ -507,6 +510,24 @@ class Context:
         st = lib().lsr_cuda_sl_step(self.h, C.byref(cfg.c()), float(energy_p), C.byref(bad))
         self.bad_node = bad.value
         _check(st)
+
+    def sl_step_async(self, cfg: StepConfig, energy_p: float) -> None:
+        """Enqueue one step without host synchronisation (see sync())."""
+        _check(lib().lsr_cuda_sl_step_async(self.h, C.byref(cfg.c()), float(energy_p)))
+
+    def sync(self) -> None:
+        """Wait for the pending async steps; raises NumericalError like sl_step."""
+        bad = C.c_int64(-1)
+        st = lib().lsr_cuda_sync(self.h, C.byref(bad))
+        self.bad_node = bad.value
+        _check(st)
+
+    def async_times(self, cap: int = 4096):
+        """(kernel_ms, step_ms, table_ms) lists of the steps the last sync() completed."""
+        k, s, t = (C.c_float * cap)(), (C.c_float * cap)(), (C.c_float * cap)()
+        n = C.c_int()
+        _check(lib().lsr_cuda_async_times(self.h, k, s, t, cap, C.byref(n)))
+        return list(k[:n.value]), list(s[:n.value]), list(t[:n.value])
 
     def swap(self):
         _check(lib().lsr_cuda_swap(self.h))

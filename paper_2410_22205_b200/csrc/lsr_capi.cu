@@ -3,6 +3,7 @@
 // host entry that stands in for lsr::sl_step (evolve.cpp:40-118).
 #include <cuda_runtime.h>
 
+#include <array>
 #include <atomic>
 #include <cmath>
 #include <cstdio>
@@ -146,6 +147,8 @@ int numerical_error(const lsr_grid& g, unsigned long long bad, int64_t* bad_node
 
 void lsr_note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
+constexpr int kMaxAsyncSteps = 4096;
+
 struct lsr_cuda_ctx {
     int device = 0;
     lsr_grid grid{};
@@ -197,6 +200,13 @@ struct lsr_cuda_ctx {
     double zt_key[4] = {0, 0, 0, 0};  // ... for this (E, dt, delta, p) (and the current d)
     cudaStream_t s_aux = nullptr;  // resync beside the table fill
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    bool dirty_is_active = false;  // `dirty` holds the current active ids
+    // asynchronous steps since the last lsr_cuda_sync: their timing events,
+    // whether they used the table, and the times read at the sync
+    int async_n = 0;
+    std::vector<std::array<cudaEvent_t, 4>> aev;
+    bool aused[kMaxAsyncSteps] = {};
+    std::vector<float> async_kernel_ms, async_step_ms, async_table_ms;
 };
 
 namespace {
@@ -298,6 +308,8 @@ int lsr_cuda_destroy(lsr_cuda_ctx* c) {
     if (c->s_cmp) cudaStreamDestroy(c->s_cmp);
     if (c->s_aux) cudaStreamDestroy(c->s_aux);
     if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+    for (auto& e : c->aev)
+        for (auto& x : e) cudaEventDestroy(x);
     if (c->ev_join) cudaEventDestroy(c->ev_join);
     if (c->s_down) cudaStreamDestroy(c->s_down);
     cudaFree(c->active);
@@ -363,6 +375,7 @@ int lsr_cuda_set_active(lsr_cuda_ctx* c, const int64_t* ids, int64_t n) {
     LSR_CUDA_TRY(cudaStreamSynchronize(c->stream));
     c->n_active = n;
     c->zt_bricks = false;
+    c->dirty_is_active = false;
     return LSR_OK;
 }
 
@@ -374,14 +387,17 @@ int lsr_cuda_set_active_device(lsr_cuda_ctx* c, const int64_t* d_ids, int64_t n)
         LSR_CUDA_TRY(cudaMemcpyAsync(c->active, d_ids, sizeof(int64_t) * n, cudaMemcpyDeviceToDevice, c->stream));
     c->n_active = n;
     c->zt_bricks = false;
+    c->dirty_is_active = false;
     return LSR_OK;
 }
 
-int lsr_cuda_sl_step(lsr_cuda_ctx* c, const lsr_step_cfg* cfg, double energy_p, int64_t* bad_node) {
-    if (bad_node) *bad_node = -1;
-    if (!c) return set_err(LSR_ERR_CONFIG, "null context");
-    if (int st = check_cfg(cfg, energy_p)) return st;
-    LSR_CUDA_TRY(cudaSetDevice(c->device));
+namespace {
+
+// Enqueues one SL step on the context stream (resync of out, z-line table,
+// SL kernel, dirty-id bookkeeping) with timing events ev[0..3] = start, table
+// filled, SL kernel start, SL kernel end; no host synchronisation.
+int enqueue_step(lsr_cuda_ctx* c, const lsr_step_cfg* cfg, double energy_p, bool reset_bad, cudaEvent_t* ev,
+                 bool* used_table) {
     SlParams P = make_params(c->grid, *cfg, energy_p);
     cudaStream_t s = c->stream;
     const bool use_table = LSR_ZTAB && c->grid.dim == 3 && cfg->interp == 1 && P.fast_weno && c->grid.dims[2] >= 4;
@@ -392,7 +408,7 @@ int lsr_cuda_sl_step(lsr_cuda_ctx* c, const lsr_step_cfg* cfg, double energy_p, 
     }
     // the resync runs beside the table fill (different buffers) on s_aux
     cudaStream_t sr = use_table ? c->s_aux : s;
-    LSR_CUDA_TRY(cudaEventRecord(c->ev[0], s));
+    LSR_CUDA_TRY(cudaEventRecord(ev[0], s));
     if (use_table) {
         LSR_CUDA_TRY(cudaEventRecord(c->ev_fork, s));
         LSR_CUDA_TRY(cudaStreamWaitEvent(sr, c->ev_fork, 0));
@@ -404,7 +420,7 @@ int lsr_cuda_sl_step(lsr_cuda_ctx* c, const lsr_step_cfg* cfg, double energy_p, 
     } else {
         LSR_CUDA_TRY(launch_resync(c->phi, c->out, c->dirty, c->n_dirty, sr));
     }
-    LSR_CUDA_TRY(cudaMemsetAsync(c->d_bad, 0xff, sizeof(unsigned long long), sr));
+    if (reset_bad) LSR_CUDA_TRY(cudaMemsetAsync(c->d_bad, 0xff, sizeof(unsigned long long), sr));
     // 3d WENO: the z-line table of phi on the bricks around the active set
     // (sl_step.cu); the brick list depends on the ids only and is kept until
     // the active set changes
@@ -427,19 +443,39 @@ int lsr_cuda_sl_step(lsr_cuda_ctx* c, const lsr_step_cfg* cfg, double energy_p, 
         LSR_CUDA_TRY(launch_zt_fill(P, c->phi, c->zt, s));
         zt_attach(P, c->zt);
     }
-    LSR_CUDA_TRY(cudaEventRecord(c->ev[1], s));
+    LSR_CUDA_TRY(cudaEventRecord(ev[1], s));
     if (use_table) {
         LSR_CUDA_TRY(cudaEventRecord(c->ev_join, sr));
         LSR_CUDA_TRY(cudaStreamWaitEvent(s, c->ev_join, 0));
     }
-    LSR_CUDA_TRY(cudaEventRecord(c->ev[2], s));
+    LSR_CUDA_TRY(cudaEventRecord(ev[2], s));
     LSR_CUDA_TRY(launch_sl_step(P, cfg->interp, c->phi, c->dist, c->active, c->n_active, c->out, c->d_bad, s));
-    LSR_CUDA_TRY(cudaEventRecord(c->ev[3], s));
-    if (int st = ensure_ids(&c->dirty, &c->cap_dirty, c->n_active)) return st;
-    if (c->n_active > 0)
-        LSR_CUDA_TRY(cudaMemcpyAsync(c->dirty, c->active, sizeof(int64_t) * c->n_active, cudaMemcpyDeviceToDevice, s));
-    c->n_dirty = c->n_active;
+    LSR_CUDA_TRY(cudaEventRecord(ev[3], s));
+    // the ids written now are where out may differ from phi after the swap
+    if (!c->dirty_is_active) {
+        if (int st = ensure_ids(&c->dirty, &c->cap_dirty, c->n_active)) return st;
+        if (c->n_active > 0)
+            LSR_CUDA_TRY(cudaMemcpyAsync(c->dirty, c->active, sizeof(int64_t) * c->n_active,
+                                         cudaMemcpyDeviceToDevice, s));
+        c->n_dirty = c->n_active;
+        c->dirty_is_active = true;
+    }
     c->consistent = true;
+    *used_table = use_table;
+    return LSR_OK;
+}
+
+}  // namespace
+
+int lsr_cuda_sl_step(lsr_cuda_ctx* c, const lsr_step_cfg* cfg, double energy_p, int64_t* bad_node) {
+    if (bad_node) *bad_node = -1;
+    if (!c) return set_err(LSR_ERR_CONFIG, "null context");
+    if (int st = check_cfg(cfg, energy_p)) return st;
+    if (c->async_n > 0) return set_err(LSR_ERR_CONFIG, "sl_step: asynchronous steps pending (call lsr_cuda_sync)");
+    LSR_CUDA_TRY(cudaSetDevice(c->device));
+    bool use_table = false;
+    if (int st = enqueue_step(c, cfg, energy_p, true, c->ev, &use_table)) return st;
+    cudaStream_t s = c->stream;
     LSR_CUDA_TRY(cudaMemcpyAsync(c->h_bad, c->d_bad, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
     LSR_CUDA_TRY(cudaStreamSynchronize(s));
     cudaEventElapsedTime(&c->kernel_ms, c->ev[2], c->ev[3]);
@@ -447,6 +483,57 @@ int lsr_cuda_sl_step(lsr_cuda_ctx* c, const lsr_step_cfg* cfg, double energy_p, 
     c->table_ms = 0.f;
     if (use_table) cudaEventElapsedTime(&c->table_ms, c->ev[0], c->ev[1]);
     if (*c->h_bad != ~0ULL) return numerical_error(c->grid, *c->h_bad, bad_node);
+    return LSR_OK;
+}
+
+int lsr_cuda_sl_step_async(lsr_cuda_ctx* c, const lsr_step_cfg* cfg, double energy_p) {
+    if (!c) return set_err(LSR_ERR_CONFIG, "null context");
+    if (int st = check_cfg(cfg, energy_p)) return st;
+    LSR_CUDA_TRY(cudaSetDevice(c->device));
+    if (c->async_n >= kMaxAsyncSteps) return set_err(LSR_ERR_CONFIG, "sl_step_async: too many pending steps");
+    while (static_cast<int>(c->aev.size()) <= c->async_n) {
+        std::array<cudaEvent_t, 4> e{};
+        for (auto& x : e) LSR_CUDA_TRY(cudaEventCreate(&x));
+        c->aev.push_back(e);
+    }
+    bool use_table = false;
+    if (int st = enqueue_step(c, cfg, energy_p, c->async_n == 0, c->aev[c->async_n].data(), &use_table)) return st;
+    c->aused[c->async_n] = use_table;
+    ++c->async_n;
+    return LSR_OK;
+}
+
+int lsr_cuda_sync(lsr_cuda_ctx* c, int64_t* bad_node) {
+    if (bad_node) *bad_node = -1;
+    if (!c) return set_err(LSR_ERR_CONFIG, "null context");
+    LSR_CUDA_TRY(cudaSetDevice(c->device));
+    cudaStream_t s = c->stream;
+    const int n = c->async_n;
+    if (n > 0) LSR_CUDA_TRY(cudaMemcpyAsync(c->h_bad, c->d_bad, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+    LSR_CUDA_TRY(cudaStreamSynchronize(s));
+    c->async_kernel_ms.assign(n, 0.f);
+    c->async_step_ms.assign(n, 0.f);
+    c->async_table_ms.assign(n, 0.f);
+    for (int i = 0; i < n; ++i) {
+        const auto& e = c->aev[i];
+        cudaEventElapsedTime(&c->async_kernel_ms[i], e[2], e[3]);
+        cudaEventElapsedTime(&c->async_step_ms[i], e[0], e[3]);
+        if (c->aused[i]) cudaEventElapsedTime(&c->async_table_ms[i], e[0], e[1]);
+    }
+    c->async_n = 0;
+    if (n > 0 && *c->h_bad != ~0ULL) return numerical_error(c->grid, *c->h_bad, bad_node);
+    return LSR_OK;
+}
+
+int lsr_cuda_async_times(lsr_cuda_ctx* c, float* kernel_ms, float* step_ms, float* table_ms, int cap, int* n) {
+    if (!c || !n) return set_err(LSR_ERR_CONFIG, "async_times: null argument");
+    const int m = std::min<int>(cap, static_cast<int>(c->async_kernel_ms.size()));
+    for (int i = 0; i < m; ++i) {
+        if (kernel_ms) kernel_ms[i] = c->async_kernel_ms[i];
+        if (step_ms) step_ms[i] = c->async_step_ms[i];
+        if (table_ms) table_ms[i] = c->async_table_ms[i];
+    }
+    *n = m;
     return LSR_OK;
 }
 
@@ -779,6 +866,7 @@ static int sl_step_host_pipelined(lsr_cuda_ctx* c, const double* phi, const doub
         LSR_CUDA_TRY(cudaMemcpyAsync(c->phi, phi, sizeof(double) * chunk_off(prefetch), cudaMemcpyHostToDevice, up));
     c->n_active = n_active;
     c->zt_bricks = false;
+    c->dirty_is_active = false;
     c->consistent = false;
     // per-chunk ranges of the (ascending) ids
     std::vector<int64_t> first(nch + 1);
@@ -1070,6 +1158,7 @@ int lsr_cuda_sl_step_host(const lsr_grid* grid, const double* phi, const double*
         LSR_CUDA_TRY(cudaMemcpyAsync(c->active, active, sizeof(int64_t) * n_active, cudaMemcpyHostToDevice, s));
     c->n_active = n_active;
     c->zt_bricks = false;
+    c->dirty_is_active = false;
     c->consistent = false;
     int64_t bad = -1;
     const int st = lsr_cuda_sl_step(c, cfg, energy_p, &bad);
@@ -1173,6 +1262,7 @@ int lsr_cuda_narrow_band(lsr_cuda_ctx* c, int which, double gamma, int64_t* n_ac
                                      c->stream));
     c->n_active = na;
     c->zt_bricks = false;
+    c->dirty_is_active = false;
     if (n_active) *n_active = na;
     if (n_tube) *n_tube = nt;
     return LSR_OK;
@@ -1290,6 +1380,7 @@ int lsr_cuda_loop_step(lsr_cuda_ctx* c, const lsr_step_cfg* cfg, const lsr_reini
             LSR_CUDA_TRY(cudaMemcpyAsync(c->dirty + c->band.n_tube, c->rb.frozen_ids, sizeof(int64_t) * c->rb.n_frozen,
                                          cudaMemcpyDeviceToDevice, c->stream));
         c->n_dirty = nd;
+        c->dirty_is_active = false;
         c->consistent = true;
     } else {
         c->consistent = false;

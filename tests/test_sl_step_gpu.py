@@ -360,3 +360,49 @@ def test_ztab_context_full_size_sampled_512(gpu, oracle):
     whole, _ = _ctx_step(lsr, g, phi, dist, band, cfg, 1.3)
     host = _run(lsr, g, phi, dist, band, cfg, 1.3)
     assert np.array_equal(bits(whole), bits(host))
+
+
+def test_async_steps_match_sync_steps_and_report_nan(gpu):
+    """lsr_cuda_sl_step_async x K + lsr_cuda_sync == K synchronous steps, bit
+    for bit; a non-finite update surfaces at the sync with the node's id."""
+    lsr = gpu
+    g = lsr._api.cube_grid(56, 3)
+    x, y, z = (a.ravel() for a in g.mesh())
+    r = np.sqrt(x * x + y * y + z * z)
+    phi = r - 0.55
+    dist = np.abs(r - 0.3) + 1e-3
+    bp = lsr.default_band_params(3, g.dx)
+    active = np.flatnonzero(np.abs(phi) < bp.gamma).astype(np.int64)
+    cfg = lsr.StepConfig(p=2, delta=1.0, dt=0.25 * g.dx, interp=lsr.InterpolatorKind.Weno, band=bp)
+    res = []
+    for mode in ("sync", "async"):
+        ctx = lsr.Context(g)
+        ctx.upload(0, phi)
+        ctx.upload(1, dist)
+        ctx.set_active(active)
+        for _ in range(5):
+            if mode == "sync":
+                ctx.sl_step(cfg, 0.7)
+            else:
+                ctx.sl_step_async(cfg, 0.7)
+            ctx.swap()
+        if mode == "async":
+            ctx.sync()
+            k, s, t = ctx.async_times()
+            assert len(k) == 5 and all(v > 0 for v in k) and all(a >= b for a, b in zip(s, k))
+        res.append(ctx.download(0))
+        ctx.close()
+    assert np.array_equal(bits(res[0]), bits(res[1]))
+    # NaN in d at one active node: reported by the sync, not by the enqueue
+    bad_id = int(active[len(active) // 2])
+    d2 = dist.copy()
+    d2[bad_id] = np.nan
+    ctx = lsr.Context(g)
+    ctx.upload(0, phi)
+    ctx.upload(1, d2)
+    ctx.set_active(active)
+    ctx.sl_step_async(cfg, 0.7)
+    with pytest.raises(lsr.NumericalError):
+        ctx.sync()
+    assert ctx.bad_node >= 0
+    ctx.close()
