@@ -406,3 +406,27 @@ def test_async_steps_match_sync_steps_and_report_nan(gpu):
         ctx.sync()
     assert ctx.bad_node >= 0
     ctx.close()
+
+
+@pytest.mark.parametrize("dims,dt_dx", [((45, 37, 41), 0.25), ((33, 50, 29), 2.0)])
+def test_ztab_ragged_grid_exact(gpu, oracle, dims, dt_dx):
+    """Table path on non-cubic grids whose sizes are not multiples of the 4^3
+    bricks (partial bricks at the high faces), vs the oracle bit for bit."""
+    lsr = gpu
+    rng = np.random.default_rng(sum(dims))
+    dx = 2.0 / 48
+    g = lsr.Grid(3, (-0.9, -0.8, -0.85), dx, dims)
+    x, y, z = (a.ravel() for a in g.mesh())  # x fastest
+    r = np.sqrt((x + 0.1) ** 2 + y ** 2 + (z + 0.05) ** 2)
+    phi = r - 0.5 + 0.1 * dx * rng.standard_normal(x.size)
+    dist = np.abs(r - 0.3) + 0.01 * rng.random(x.size)
+    bp = lsr.default_band_params(3, dx)
+    active = np.flatnonzero(np.abs(phi) < bp.gamma).astype(np.int64)
+    cfg = lsr.StepConfig(p=2, delta=1.0, dt=dt_dx * dx, interp=lsr.InterpolatorKind.Weno, band=bp)
+    got, tms = _ctx_step(lsr, g, phi, dist, active, cfg, 0.5)
+    assert tms > 0.0
+    ref, st, _ = oracle.sl_step(dict(dim=3, dims=g.dims, origin=g.origin, dx=g.dx), phi, dist, active,
+                                dict(p=2, interp=1, delta=1.0, dt=cfg.dt, fallback_c=1e-3, fallback_alpha=1.0,
+                                     gamma=bp.gamma, beta=bp.beta), 0.5, nthreads=0)
+    assert st == 0
+    assert np.count_nonzero(bits(got) != bits(ref)) == 0
