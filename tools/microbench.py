@@ -20,6 +20,7 @@ def main():
     ap.add_argument("--interp", type=int, default=1)
     ap.add_argument("--radius", type=float, default=0.9)
     ap.add_argument("--delta", type=float, default=1.0)
+    ap.add_argument("--zslab", type=int, nargs=2, default=None, help="only band nodes with k in [lo, hi)")
     ap.add_argument("--order", default="id", help="thread order of the active ids: id or bXYZ (brick extents)")
     a = ap.parse_args()
     g = lsr._api.cube_grid(a.n, 3)
@@ -29,6 +30,9 @@ def main():
     dist = np.abs(r - 0.5) + 1e-3 * np.cos(40 * r)
     bp = lsr.default_band_params(3, g.dx)
     band = np.flatnonzero(np.abs(phi) < bp.gamma).astype(np.int64)
+    if a.zslab:
+        kk = band // (a.n * a.n)
+        band = band[(kk >= a.zslab[0]) & (kk < a.zslab[1])]
     if a.order != "id":  # process the ids brick by brick (the step does not depend on the order)
         bx, by, bz = (int(c) for c in a.order[1:4])
         i, j, k = band % a.n, (band // a.n) % a.n, band // (a.n * a.n)
