@@ -334,7 +334,10 @@ __global__ void one_step4(SlParams P, const double* __restrict__ prev, double* _
 // five; same per-node arithmetic as one_step
 constexpr int kMarch = 16;
 
-__global__ void one_step_march(SlParams P, const double* __restrict__ prev, double* __restrict__ out,
+#ifndef LSR_MARCH_MINB
+#define LSR_MARCH_MINB 4  // 64 registers: occupancy beats the few spills (reinit 4.82 -> 4.71 ms at 512^3)
+#endif
+__global__ void __launch_bounds__(256, LSR_MARCH_MINB) one_step_march(SlParams P, const double* __restrict__ prev, double* __restrict__ out,
                                unsigned* __restrict__ frozen4, int* __restrict__ any_frozen,
                                int* __restrict__ any_zero) {
     const int qx = P.nx / 4;
