@@ -86,8 +86,19 @@ class ClockSampler:
 
     def __init__(self, index: int):
         self.index = index
-        self.rows = []
+        self.rows = []  # (host time of arrival, fields)
         self.proc = None
+        self.t0 = self.t1 = None
+
+    # the sampler is started before the warm-up (nvidia-smi takes ~0.1 s to
+    # come up); only rows that arrive inside [begin, end] describe the timed
+    # region
+    def begin(self):
+        self.t0 = time.perf_counter()
+
+    def end(self):
+        time.sleep(0.03)  # one more sampling period covers the region's tail
+        self.t1 = time.perf_counter()
 
     def __enter__(self):
         try:
@@ -102,7 +113,7 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.rows.append([c.strip() for c in line.split(",")])
+            self.rows.append((time.perf_counter(), [c.strip() for c in line.split(",")]))
 
     def __exit__(self, *a):
         if self.proc:
@@ -114,15 +125,18 @@ class ClockSampler:
             self.thread.join(timeout=2)
 
     def summary(self):
-        if not self.rows:
+        rows = [r for t, r in self.rows if self.t0 is None or (self.t0 <= t <= (self.t1 or t))]
+        if not rows and self.t0 is not None:  # a region shorter than one period: the next sample
+            rows = [r for t, r in self.rows if t >= self.t0][:1]
+        if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 4 + i and r[4 + i] == "Active"})
-        pw = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        reasons = sorted({names[i] for r in rows for i in range(4) if len(r) > 4 + i and r[4 + i] == "Active"})
+        pw = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows), "power_w_max": max(pw) if pw else None}
+                "reasons": reasons, "samples": len(rows), "power_w_max": max(pw) if pw else None}
 
 
 # ---------------------------------------------------------------------------
@@ -261,6 +275,7 @@ def run_ours(args):
             torch.cuda.current_stream().synchronize()
             return kev[0].elapsed_time(kev[1])
 
+    clk = ClockSampler(local).__enter__()
     for i in range(args.warmup):
         one_step(i)
     if world == 1:
@@ -273,7 +288,8 @@ def run_ours(args):
     kernel_ms, step_ms = [], []
     n0 = lsr.kernel_launches()
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    with ClockSampler(local) as clk:
+    clk.begin()
+    try:
         for i in range(args.steps):
             flush.fill_(float(i))  # evict L2 between timed steps (outside the step's events)
             evs[i][0].record(stream)
@@ -285,6 +301,9 @@ def run_ours(args):
             ctx.sync()  # raises NumericalError if any timed step went non-finite
             kernel_ms, _, table_ms = ctx.async_times()
         step_ms = [a.elapsed_time(b) for a, b in evs]
+    finally:
+        clk.end()
+        clk.__exit__()
     torch.cuda.synchronize()
     launches = lsr.kernel_launches() - n0
     if world > 1:
@@ -621,7 +640,7 @@ def run_reference(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=40)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", type=int, default=4, choices=sorted(CONFIGS))
