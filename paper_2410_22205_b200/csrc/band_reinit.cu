@@ -462,12 +462,42 @@ __device__ __forceinline__ double godunov_vals(const SlParams& P, double pc, con
     return sqrt(acc);
 }
 
+// godunov_norm of a node with all six neighbours (3d). Per axis only the
+// larger-magnitude candidate is divided: with u = max(dm, 0), v = min(dp, 0)
+// (or the mirrored pair for sgn <= 0), the reference's
+// max(RN(u/dx)^2, RN(v/dx)^2) equals RN(RN(c/dx)^2) for c the one of u, v of
+// larger magnitude, because x -> RN(RN(|x|/dx)^2) is non-decreasing and
+// RN(+-x/dx) = +-RN(x/dx); ties give equal values, a zero's sign vanishes in
+// the square, and a NaN u (v) is selected exactly when the reference's max
+// returns its NaN (finite) term. Returns false (the caller takes
+// godunov_vals) when a selected c is outside div_const's Markstein range.
+__device__ __forceinline__ bool godunov_interior(const SlParams& P, double pc, const double* vm, const double* vp,
+                                                 double sgn, double& gn) {
+    double acc = 0.0;
+    bool ok = P.fast_div != 0;
+#pragma unroll
+    for (int ax = 0; ax < 3; ++ax) {
+        const double dm = pc - vm[ax], dp = vp[ax] - pc;
+        const double u = sgn > 0.0 ? smax(dm, 0.0) : smin(dm, 0.0);
+        const double v = sgn > 0.0 ? smin(dp, 0.0) : smax(dp, 0.0);
+        const double c = fabs(u) < fabs(v) ? v : u;
+        ok = ok & markstein_ok(c);
+        const double q = markstein(c, P.dx, P.rdx);
+        acc += q * q;
+    }
+    gn = sqrt(acc);
+    return ok;
+}
+
 // one Jacobi iteration (reinit.cpp:111-124). Memory-latency bound (one id
 // load, then 7 dependent gathers per node), so each thread takes kJacNPT
 // nodes and issues all their loads before any arithmetic. The running max of
 // |upd| is kept as the bits of a non-negative double (integer order = double
 // order); std::max(residual, x) never lets a NaN in, nor does `a > 0`; it is
 // reduced within each warp before one atomic per warp.
+#ifndef LSR_JAC_INTERIOR
+#define LSR_JAC_INTERIOR 1  // godunov_interior for nodes with all six neighbours
+#endif
 #ifndef LSR_JAC_NPT
 #define LSR_JAC_NPT 4
 #endif
@@ -518,7 +548,9 @@ __global__ void __launch_bounds__(kJacThreads, LSR_JAC_MINB)
     for (int r = 0; r < kJacNPT; ++r) {
         if (id[r] < 0) continue;
         const double s = sg[r];
-        const double gn = godunov_vals(P, pc[r], vm[r], vp[r], hm[r], hp[r], s);
+        double gn;
+        if (!(LSR_JAC_INTERIOR && P.dim == 3 && mk[r] == 63u && godunov_interior(P, pc[r], vm[r], vp[r], s, gn)))
+            gn = godunov_vals(P, pc[r], vm[r], vp[r], hm[r], hp[r], s);
         const double upd = -dtau * s * (gn - 1.0);
         nxt[id[r]] = pc[r] + upd;
         const double a = fabs(upd);
