@@ -320,7 +320,7 @@ def run_ours(args):
     hbm_peak, peak_kind = peaks()
     bpu = BYTES_PER_UPDATE[("weno" if cfg["interp"] == 1 else "q1", cfg["dim"])]
     achieved = mine.size * bpu / (kern_avg_ms * 1e-3) / 1e9
-    traffic_pu, _ = traffic_per_update()
+    traffic_pu, traffic_info = traffic_per_update()
 
     e2e = None
     cpu = None
@@ -372,9 +372,12 @@ def run_ours(args):
                 "algorithmic_bytes_per_update": bpu,
                 "kernel_ms_avg": kern_avg_ms,
                 "table_fill_ms_avg": float(np.mean(table_ms[-args.steps:])) if table_ms else None,
+                "ncu": ({k: traffic_info[k] for k in ("fp64_pipe_active", "l1_hit", "l2_hit", "source")
+                         if k in traffic_info} if traffic_info else None),
                 "note": "reference-access bytes per node-update (SURVEY 8(d)) over the SL kernel's time; the "
-                        "kernel is fp64-pipe bound. The step (value, ms_per_step) also holds the z-line table "
-                        "fill (table_fill_ms_avg) and the sparse resync",
+                        "kernel is bound by fp64 issue and load latency, not by DRAM (ncu: fp64 pipe active, "
+                        "L1/L2 hit rates of the committed capture). The step (value, ms_per_step) also holds "
+                        "the z-line table fill (table_fill_ms_avg) and the sparse resync",
             },
             "gpu_launches": int(launches),
             "clocks": clk.summary(),
