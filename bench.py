@@ -545,6 +545,18 @@ def measure_loop(lsr, g, phi, ctx, step, steps=4, cpu_too=True):
     return out
 
 
+def cpu_model():
+    """The host CPU's model name (/proc/cpuinfo), for the baseline's record."""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 def cpu_baseline(g, phi, ctx, active, step, e2, lsr, reps=3):
     """The reference's lsr::sl_step (OpenMP, all host threads) on the same
     inputs (oracle/_ref; the oracle restatement when _ref is absent)."""
@@ -571,7 +583,7 @@ def cpu_baseline(g, phi, ctx, active, step, e2, lsr, reps=3):
             secs.append(time.perf_counter() - t0)
         kind = "port"
     best = min(secs)
-    return {"value": active.size / best, "unit": UNIT, "cores": threads, "kind": kind,
+    return {"value": active.size / best, "unit": UNIT, "cores": threads, "cpu_model": cpu_model(), "kind": kind,
             "sample": f"full band ({active.size} active nodes) of the same workload, best of {reps} calls of "
                       f"lsr::sl_step incl. its internal O(N) copy", "seconds": secs}
 
@@ -635,7 +647,8 @@ def run_reference(args):
         "config": {"workload": cfg["name"], "grid": list(g.dims), "cloud_points": cfg["points"],
                    "active_nodes": int(act_ref.size), "energy_e2": e2, "dist_sweep_rounds": rounds,
                    "setup_build_distance_s": t_dist},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind, "sample": sample},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "cpu_model": cpu_model(), "kind": kind,
+                         "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
 
