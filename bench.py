@@ -40,13 +40,13 @@ BYTES_PER_UPDATE = {("weno", 3): 2176, ("q1", 3): 384, ("weno", 2): 352, ("q1", 
 CONFIGS = {
     # id: (n, dim, cloud config, points, sigma in dx, interp, phi0 radius, p, delta)
     4: dict(n=512, dim=3, cloud=4, points=1_000_000, sigma=0.0, interp=1, r0=0.9, p=2, delta=1.0,
-            name="bumpy-sphere-512"),
+            name="bumpy-sphere-512", shape="bumpy-sphere cloud"),
     3: dict(n=256, dim=3, cloud=3, points=100_000, sigma=0.5, interp=1, r0=0.9, p=2, delta=1.0,
-            name="torus-256"),
+            name="torus-256", shape="noisy torus cloud"),
     5: dict(n=1024, dim=3, cloud=5, points=4_000_000, sigma=0.25, interp=1, r0=0.95, p=2, delta=1.0,
-            name="three-tori-1024"),
+            name="three-tori-1024", shape="three-tori cloud with two holes"),
     2: dict(n=128, dim=3, cloud=2, points=20_000, sigma=0.0, interp=0, r0=0.9, p=2, delta=1.0,
-            name="sphere-128"),
+            name="sphere-128", shape="sphere cloud"),
 }
 
 
@@ -347,7 +347,7 @@ def run_ours(args):
             "scaling": "strong",
             "vs_baseline": None,
             "dtype": "f64",
-            "data": "synthetic (seeded bumpy-sphere cloud, BASELINE config 4 shapes/sizes)",
+            "data": f"synthetic (seeded {cfg['shape']}, BASELINE config {args.config} shapes/sizes)",
             "config": {
                 "workload": cfg["name"],
                 "grid": list(g.dims),
@@ -643,7 +643,8 @@ def run_reference(args):
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps, "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded bumpy-sphere cloud, BASELINE config 4)",
+        "vs_baseline": None, "dtype": "f64",
+        "data": f"synthetic (seeded {cfg['shape']}, BASELINE config {args.config} shapes/sizes)",
         "config": {"workload": cfg["name"], "grid": list(g.dims), "cloud_points": cfg["points"],
                    "active_nodes": int(act_ref.size), "energy_e2": e2, "dist_sweep_rounds": rounds,
                    "setup_build_distance_s": t_dist},
