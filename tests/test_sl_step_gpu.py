@@ -430,3 +430,56 @@ def test_ztab_ragged_grid_exact(gpu, oracle, dims, dt_dx):
                                      gamma=bp.gamma, beta=bp.beta), 0.5, nthreads=0)
     assert st == 0
     assert np.count_nonzero(bits(got) != bits(ref)) == 0
+
+
+@pytest.mark.parametrize("dim,interp", [(2, 0), (3, 0), (3, 1)])
+def test_empty_active_set_copies_phi(gpu, dim, interp):
+    """An empty BandMask::active: out = phi everywhere (evolve.cpp:50), through
+    the one-shot call, the synchronous context step and the async one."""
+    lsr = gpu
+    g = lsr._api.cube_grid(20 if dim == 3 else 64, dim)
+    x, y, z = (a.ravel() for a in g.mesh())
+    phi = np.sqrt(x * x + y * y + z * z) - 0.5
+    dist = np.abs(phi) + 0.01
+    bp = lsr.default_band_params(dim, g.dx)
+    cfg = lsr.StepConfig(p=2, delta=1.0, dt=0.25 * g.dx, interp=lsr.InterpolatorKind(interp), band=bp)
+    none = np.zeros(0, np.int64)
+    assert np.array_equal(bits(_run(lsr, g, phi, dist, none, cfg, 0.5)), bits(phi))
+    ctx = lsr.Context(g)
+    try:
+        ctx.upload(0, phi)
+        ctx.upload(1, dist)
+        ctx.set_active(none)
+        ctx.sl_step(cfg, 0.5)
+        assert np.array_equal(bits(ctx.download(2)), bits(phi))
+        ctx.sl_step_async(cfg, 0.5)
+        ctx.sync()
+        assert np.array_equal(bits(ctx.download(2)), bits(phi))
+    finally:
+        ctx.close()
+
+
+def test_async_rejects_bad_config_before_any_work(gpu):
+    """sl_step_async validates like sl_step (evolve.hpp:25-30, evolve.cpp:45-46)
+    and refuses a synchronous step while async steps are pending."""
+    lsr = gpu
+    g = lsr._api.cube_grid(16, 3)
+    phi = np.zeros(g.num_nodes()) + 0.1
+    ctx = lsr.Context(g)
+    try:
+        ctx.upload(0, phi)
+        ctx.upload(1, phi)
+        ctx.set_active(np.arange(10, dtype=np.int64))
+        bp = lsr.default_band_params(3, g.dx)
+        with pytest.raises(lsr.ConfigError):
+            ctx.sl_step_async(lsr.StepConfig(p=2, delta=1.0, dt=0.0, band=bp), 0.5)
+        with pytest.raises(lsr.Error):
+            ctx.sl_step_async(lsr.StepConfig(p=2, delta=1.0, dt=0.1 * g.dx, band=bp), 0.0)  # E <= 0 with p > 1
+        good = lsr.StepConfig(p=2, delta=1.0, dt=0.1 * g.dx, band=bp)
+        ctx.sl_step_async(good, 0.5)
+        with pytest.raises(lsr.ConfigError):
+            ctx.sl_step(good, 0.5)
+        ctx.sync()
+        ctx.sl_step(good, 0.5)
+    finally:
+        ctx.close()
