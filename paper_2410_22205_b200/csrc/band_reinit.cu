@@ -161,14 +161,6 @@ struct NonZero {  // in the tube / frozen
     __device__ bool operator()(unsigned v) const { return v != 0; }
 };
 
-struct IsActive {
-    const unsigned char* s;
-    __device__ bool operator()(long long id) const { return s[id] == 1; }
-};
-struct InTube {
-    const unsigned char* s;
-    __device__ bool operator()(long long id) const { return s[id] != 0; }
-};
 
 // clamp_field two nodes per thread; a node is stored only when clamping
 // changes its bits (after the first loop iteration most of the grid already
@@ -395,10 +387,6 @@ struct NotFrozen {  // tube entries t whose node was not frozen by the one-step 
     const unsigned char* frozen;
     const long long* tube;
     __device__ bool operator()(long long t) const { return !frozen[tube[t]]; }
-};
-struct IsFrozen {
-    const unsigned char* frozen;
-    __device__ bool operator()(long long id) const { return frozen[id] != 0; }
 };
 struct TubeId {
     const long long* tube;

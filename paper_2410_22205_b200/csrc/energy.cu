@@ -338,10 +338,6 @@ __global__ void contrib_2d(SlParams P, const double* __restrict__ phi, const dou
 struct FlagSet {
     __device__ bool operator()(unsigned v) const { return v != 0; }
 };
-struct CellFlag {
-    const unsigned char* flags;
-    __device__ bool operator()(long long c) const { return flags[c] != 0; }
-};
 struct CellId {  // cell ids fit int (cub's item count, as before)
     __device__ int operator()(long long c) const { return static_cast<int>(c); }
 };
