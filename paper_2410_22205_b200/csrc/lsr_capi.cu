@@ -400,7 +400,10 @@ int enqueue_step(lsr_cuda_ctx* c, const lsr_step_cfg* cfg, double energy_p, bool
                  bool* used_table) {
     SlParams P = make_params(c->grid, *cfg, energy_p);
     cudaStream_t s = c->stream;
-    const bool use_table = LSR_ZTAB && c->grid.dim == 3 && cfg->interp == 1 && P.fast_weno && c->grid.dims[2] >= 4;
+    // delta = 0: the four feet coincide and one interpolation per node does
+    // not amortise the fill (1.31 vs 1.27 ms at 512^3), so no table
+    const bool use_table = LSR_ZTAB && c->grid.dim == 3 && cfg->interp == 1 && P.fast_weno && c->grid.dims[2] >= 4 &&
+                           cfg->delta > 0.0;
     if (use_table && !c->s_aux) {
         LSR_CUDA_TRY(cudaStreamCreateWithFlags(&c->s_aux, cudaStreamNonBlocking));
         LSR_CUDA_TRY(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
@@ -585,7 +588,8 @@ thread_local std::vector<std::unique_ptr<SlabTable>> g_slab_tables;
 // P.z_base/z_planes must be set, phi_g is the global-id-shifted phi
 int attach_slab_table(SlParams& P, const lsr_grid& g, int interp, const double* phi_g, const double* dist_g,
                       const int64_t* d_active, int64_t n_active, cudaStream_t s) {
-    if (!(LSR_ZTAB && g.dim == 3 && interp == 1 && P.fast_weno && P.z_planes >= 4 && n_active > 0)) return LSR_OK;
+    if (!(LSR_ZTAB && g.dim == 3 && interp == 1 && P.fast_weno && P.z_planes >= 4 && n_active > 0 && P.delta > 0.0))
+        return LSR_OK;
     int dev = 0;
     LSR_CUDA_TRY(cudaGetDevice(&dev));
     SlabTable* tp = nullptr;
