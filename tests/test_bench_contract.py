@@ -31,3 +31,29 @@ def test_reference_arm_json_line(built):
     assert d["cpu_baseline"]["value"] == d["value"]
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
     assert d["config"]["workload"] == "sphere-128"
+
+
+@pytest.mark.gpu
+def test_our_arm_json_line(gpu):
+    """bench.py's own arm (N = 1) on the smallest 3d config: one JSON line
+    with every key of the driver's contract and this tier's additions."""
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--config", "3", "--steps", "5",
+                        "--warmup", "3", "--e2e-steps", "2"], capture_output=True, text=True, cwd=ROOT, timeout=900)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+              "vs_baseline", "dtype", "data", "config", "roofline", "cpu_baseline", "e2e", "gpu_launches", "clocks"):
+        assert k in d, k
+    assert d["n_gpus"] == 1 and d["steps"] == 5 and d["value"] > 0 and d["dtype"] == "f64"
+    assert d["config"]["workload"] == "torus-256"
+    rf = d["roofline"]
+    for k in ("bound", "achieved", "peak", "unit", "frac", "traffic"):
+        assert k in rf, k
+    assert 0 < rf["frac"] < 2 and rf["unit"] == "GB/s"
+    e = d["e2e"]
+    assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
+    assert d["cpu_baseline"]["kind"] in ("reference", "port") and d["cpu_baseline"]["cores"] >= 1
+    assert d["gpu_launches"] >= d["steps"]  # at least the SL kernel per step
+    assert "sm_mhz" in d["clocks"] and "reasons" in d["clocks"]
