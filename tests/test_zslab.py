@@ -117,6 +117,32 @@ def test_plan_cuts_balance_and_thickness():
         zslab.plan_cuts(active, N * N, N, 20, min_planes=5)
 
 
+def test_plan_cuts_edge_cases_and_ownership():
+    """Empty bands, a band in one plane, and 8 ranks: the cuts tile [0, nz)
+    with slabs of at least min_planes, every active id is owned by exactly
+    one rank, and the resident planes of a slab cover its owned planes plus
+    the halo (clipped to the grid)."""
+    from paper_2410_22205_b200 import zslab
+
+    nxy, nz = 16 * 16, 64
+    rng = np.random.default_rng(3)
+    cases = [np.zeros(0, np.int64),
+             np.sort(rng.choice(nxy, 50, replace=False)).astype(np.int64) + 30 * nxy,
+             np.sort(rng.choice(nxy * nz, 5000, replace=False)).astype(np.int64)]
+    for active in cases:
+        for world in (1, 2, 8):
+            cuts = zslab.plan_cuts(active, nxy, nz, world, min_planes=4)
+            assert cuts[0] == 0 and cuts[-1] == nz and np.all(np.diff(cuts) >= 4)
+            owned = [zslab.owned_ids(active, zslab.make_slab(cuts, r, 4, nxy, nz)) for r in range(world)]
+            allown = np.concatenate(owned) if owned else np.zeros(0, np.int64)
+            assert np.array_equal(np.sort(allown), active)
+            for r in range(world):
+                sl = zslab.make_slab(cuts, r, 4, nxy, nz)
+                assert sl.lo == cuts[r] and sl.hi == cuts[r + 1]
+                assert sl.z_base == max(0, sl.lo - 4) and sl.z_base + sl.z_planes == min(nz, sl.hi + 4)
+                assert np.all((owned[r] // nxy >= sl.lo) & (owned[r] // nxy < sl.hi))
+
+
 @pytest.mark.gpu
 def test_fused_peer_push_two_slabs_one_gpu(gpu):
     """The fused SL + halo-push kernel, two slabs emulated on one GPU: the
