@@ -13,11 +13,16 @@
 #ifndef LSR_SL_MIN_BLOCKS
 #define LSR_SL_MIN_BLOCKS 7
 #endif
+#ifndef LSR_SL_THREADS_ZT
+#define LSR_SL_THREADS_ZT 192
+#endif
 #ifndef LSR_SL_MIN_BLOCKS_ZT
-#define LSR_SL_MIN_BLOCKS_ZT 9
+#define LSR_SL_MIN_BLOCKS_ZT 6
 #endif
 constexpr int kSlThreads = LSR_SL_THREADS;
-constexpr int kSlMinBlocksZt = LSR_SL_MIN_BLOCKS_ZT;  // the same for the z-line-table kernel
+// the z-line-table kernel: 6 x 192 threads (36 warps) at 56 registers
+constexpr int kSlThreadsZt = LSR_SL_THREADS_ZT;
+constexpr int kSlMinBlocksZt = LSR_SL_MIN_BLOCKS_ZT;
 constexpr int kSlMinBlocks = LSR_SL_MIN_BLOCKS;  // resident CTAs per SM the register budget must allow
 
 // bumps the process-wide launch counter (lsr_cuda_kernel_launches)

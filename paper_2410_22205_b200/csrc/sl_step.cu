@@ -21,7 +21,7 @@ namespace lsr_dev {
 // ZT: 3d WENO launches that read the z-line table; their per-line chains are
 // shorter, so they trade registers for a 9th resident CTA per SM
 template <int DIM, int KIND, bool ZT = false>
-__global__ void __launch_bounds__(kSlThreads, ZT ? kSlMinBlocksZt : kSlMinBlocks) sl_step_kernel(SlParams P, const double* __restrict__ phi,
+__global__ void __launch_bounds__(ZT ? kSlThreadsZt : kSlThreads, ZT ? kSlMinBlocksZt : kSlMinBlocks) sl_step_kernel(SlParams P, const double* __restrict__ phi,
                                                              const double* __restrict__ dist,
                                                              const int64_t* __restrict__ active,
                                                              long long n_active, double* __restrict__ out,
@@ -43,7 +43,7 @@ __global__ void __launch_bounds__(kSlThreads, ZT ? kSlMinBlocksZt : kSlMinBlocks
     }
     const bool use_zt = ZT && __ldg(P.ztab_bad) == 0u;
     double* sb = nullptr;
-    if (LSR_SMEM_FEET && DIM == 3 && KIND == 1) {  // per-thread double-buffered stencil columns
+    if (LSR_SMEM_FEET && DIM == 3 && KIND == 1 && !ZT) {  // per-thread stencil columns (kSlThreads-thread CTAs)
         __shared__ double sbuf[2 * 16 * kSlThreads];
         sb = sbuf + threadIdx.x;
     }
@@ -325,7 +325,8 @@ cudaError_t launch_sl_step(const SlParams& P, int kind, const double* phi, const
     } else {
         if (kind == 0) sl_step_kernel<3, 0><<<blocks, kSlThreads, 0, stream>>>(P, phi, dist, active, n_active, out, bad);
         else if (LSR_ZTAB && P.ztab != nullptr)
-            sl_step_kernel<3, 1, true><<<blocks, kSlThreads, 0, stream>>>(P, phi, dist, active, n_active, out, bad);
+            sl_step_kernel<3, 1, true><<<static_cast<unsigned>((n_active + kSlThreadsZt - 1) / kSlThreadsZt),
+                                         kSlThreadsZt, 0, stream>>>(P, phi, dist, active, n_active, out, bad);
         else sl_step_kernel<3, 1><<<blocks, kSlThreads, 0, stream>>>(P, phi, dist, active, n_active, out, bad);
     }
     lsr_note_launch();
