@@ -76,8 +76,8 @@ def test_configs_2_3_vs_live_reference(gpu, reference, config, n, steps):
 
 def test_config4_512_loop_step_and_one_shot_vs_reference(gpu, reference):
     """Config 4 at its full size (512^3, 1 M-point bumpy sphere, WENO, p = 2,
-    delta = 1): one whole loop iteration (band, E_2, SL, reinit) against the
-    reference's own loop body on the host, bit for bit, and the one-shot
+    delta = 1): three whole loop iterations (band, E_2, SL, reinit) against
+    the reference's own loop body on the host, bit for bit, and the one-shot
     host entry on pinned buffers (the zero-copy pull path bench.py's e2e
     times) against the device-resident step."""
     import torch
@@ -108,15 +108,18 @@ def test_config4_512_loop_step_and_one_shot_vs_reference(gpu, reference):
     ctx.sl_step(cfg, 1.5)
     dev = ctx.download(2)
     assert np.count_nonzero(bits(hout) != bits(dev)) == 0
-    # one loop iteration vs the reference's loop body
+    # three loop iterations vs the reference's loop body (band, E_2, SL with
+    # the z-line table, reinit), the GPU fed the reference's E_2 (glibc pow)
     ctx.upload(0, phi)
     rc = lsr.ReinitConfig.defaults(g.dx, bp.gamma)
-    ref_phi, e2, na, it, _ = reference.loop_step(gd, phi, d, ccfg)
-    s = ctx.loop_step(cfg, rc, 5, energy_override=e2)
-    assert s["n_active"] == na and s["reinit_iterations"] == it
-    got = ctx.download(0)
-    diff = np.count_nonzero(bits(got) != bits(ref_phi))
-    assert diff == 0, f"{diff} nodes differ"
+    ref_phi = phi
+    for step in range(3):
+        ref_phi, e2, na, it, _ = reference.loop_step(gd, ref_phi, d, ccfg)
+        s = ctx.loop_step(cfg, rc, 5, energy_override=e2)
+        assert s["n_active"] == na and s["reinit_iterations"] == it, step
+        got = ctx.download(0)
+        diff = np.count_nonzero(bits(got) != bits(ref_phi))
+        assert diff == 0, f"iteration {step}: {diff} nodes differ"
 
 
 def test_config5_1024_sampled_subset_vs_oracle(gpu, oracle):
