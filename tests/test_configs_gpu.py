@@ -163,3 +163,34 @@ def test_config5_1024_sampled_subset_vs_oracle(gpu, oracle):
         assert np.max(np.abs(out[band] - phi[band])) < 4 * g.dx
     finally:
         ctx.close()
+
+
+def test_config5_1024_loop_iteration_vs_reference(gpu, reference):
+    """Config 5 at its full size (1024^3, 4 M points): one whole loop
+    iteration (band, E_2, SL with the z-line table, reinit) on the GPU
+    against the reference's own loop body on the host, bit for bit (the GPU
+    fed the reference's E_2)."""
+    lsr = gpu
+    g = lsr.cube_grid(1024, 3)
+    pts = lsr.cloud_generate(5, 4_000_000, seed=2410, sigma=0.25 * g.dx)
+    ax = g.axes()
+    phi = (np.sqrt(ax[0][None, None, :] ** 2 + ax[1][None, :, None] ** 2 + ax[2][:, None, None] ** 2) - 0.95).ravel()
+    gd = dict(dim=3, dims=g.dims, origin=g.origin, dx=g.dx)
+    bp = lsr.default_band_params(3, g.dx)
+    cfg = lsr.StepConfig(p=2, delta=1.0, dt=0.25 * g.dx, interp=lsr.InterpolatorKind.Weno, band=bp)
+    ccfg = dict(p=2, interp=1, delta=1.0, dt=cfg.dt, fallback_c=1e-3, fallback_alpha=1.0, gamma=bp.gamma,
+                beta=bp.beta)
+    ctx = lsr.Context(g)
+    try:
+        ctx.build_distance(pts)
+        d = ctx.download(1)
+        ctx.upload(0, phi)
+        ref_phi, e2, na, it, _ = reference.loop_step(gd, phi, d, ccfg)
+        del phi
+        s = ctx.loop_step(cfg, lsr.ReinitConfig.defaults(g.dx, bp.gamma), 5, energy_override=e2)
+        assert s["n_active"] == na and s["reinit_iterations"] == it
+        got = ctx.download(0)
+        diff = np.count_nonzero(got.view(np.int64) != ref_phi.view(np.int64))
+        assert diff == 0, f"{diff} nodes differ"
+    finally:
+        ctx.close()
