@@ -194,3 +194,41 @@ def test_config5_1024_loop_iteration_vs_reference(gpu, reference):
         assert diff == 0, f"{diff} nodes differ"
     finally:
         ctx.close()
+
+
+@pytest.mark.parametrize("config,n,steps", [(2, 128, 8), (3, 256, 3)])
+def test_configs_own_energy_within_tolerance(gpu, reference, config, n, steps):
+    """The GPU loop with its own E_2 (few-ulp from the reference's glibc-pow
+    sum) against the reference loop: the north star's fp64
+    tolerance, normwise — max |phi_gpu - phi_ref| <= 1e-12 * gamma (the
+    field's scale) — and pointwise relative 1e-12 where |phi| >= dx."""
+    lsr = gpu
+    g = lsr.cube_grid(n, 3)
+    npts = {2: 20_000, 3: 100_000}[config]
+    sigma = {2: 0.0, 3: 0.5 * g.dx}[config]
+    interp = {2: lsr.InterpolatorKind.Q1, 3: lsr.InterpolatorKind.Weno}[config]
+    pts = lsr.cloud_generate(config, npts, seed=2410, sigma=sigma)
+    ax = g.axes()
+    phi = (np.sqrt(ax[0][None, None, :] ** 2 + ax[1][None, :, None] ** 2 + ax[2][:, None, None] ** 2) - 0.9).ravel()
+    gd = dict(dim=3, dims=g.dims, origin=g.origin, dx=g.dx)
+    bp = lsr.default_band_params(3, g.dx)
+    cfg = lsr.StepConfig(p=2, delta=1.0, dt=0.25 * g.dx, interp=interp, band=bp)
+    ccfg = dict(p=2, interp=int(interp), delta=1.0, dt=cfg.dt, fallback_c=1e-3, fallback_alpha=1.0, gamma=bp.gamma,
+                beta=bp.beta)
+    ctx = lsr.Context(g)
+    try:
+        ctx.build_distance(pts)
+        d = ctx.download(1)
+        ctx.upload(0, phi)
+        rc = lsr.ReinitConfig.defaults(g.dx, bp.gamma)
+        cur = phi
+        for _ in range(steps):
+            cur, _, _, _, _ = reference.loop_step(gd, cur, d, ccfg)
+            ctx.loop_step(cfg, rc, 5)  # the GPU's own E_2
+        got = ctx.download(0)
+        err = np.abs(got - cur)
+        assert np.max(err) <= 1e-12 * bp.gamma, np.max(err) / bp.gamma
+        big = np.abs(cur) >= g.dx
+        assert np.all(err[big] <= 1e-12 * np.abs(cur[big]))
+    finally:
+        ctx.close()
