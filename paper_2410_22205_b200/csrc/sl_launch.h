@@ -7,11 +7,14 @@
 
 #include "sl_device.cuh"
 
+// per-line kernels (Q1, 2d, 3d WENO without the z-line table): 4 CTAs of 256
+// threads at 64 registers (delta = 0 WENO 1.19 -> 1.10 ms, Q1 0.58 -> 0.56 ms
+// at 512^3 against 7 x 128)
 #ifndef LSR_SL_THREADS
-#define LSR_SL_THREADS 128
+#define LSR_SL_THREADS 256
 #endif
 #ifndef LSR_SL_MIN_BLOCKS
-#define LSR_SL_MIN_BLOCKS 7
+#define LSR_SL_MIN_BLOCKS 4
 #endif
 #ifndef LSR_SL_THREADS_ZT
 #define LSR_SL_THREADS_ZT 192
