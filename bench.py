@@ -5,24 +5,30 @@ r(t,p) = 0.5(1 + 0.1 sin 5t cos 4p), 1,000,000 seeded points, 10x denser at
 the poles; grid 512^3 on [-1,1]^3 (dx = 2/511); d = lsr::build_distance_field
 of the cloud (computed on the GPU, bit-identical to the reference's);
 phi^0 = |x| - 0.9; band = |phi| < gamma = 6dx; E_2 = lsr::surface_energy
-(GPU); p = 2, delta = 1 (Table 1 run r >= 3), WENO, dt = dx/4.
+(GPU); p = 2, delta = 1 (Table 1 run r >= 3), WENO, dt = dx/4. `--config N`
+runs BASELINE config N (1: 257^2 circle, Q1; 2: 128^3 sphere, Q1; 3: 256^3
+torus, WENO; 5: 1024^3 three tori, WENO) with the same recipe.
 
 One step = one lsr::sl_step over the whole band (resync of the double
-buffer + the SL kernel), inputs resident in HBM; successive steps ping-pong
-phi <-> out on the same band. L2 (126 MB) is flushed by a 256 MB write
-between timed steps. Units = active node-updates.
+buffer + the z-line table fill + the SL kernel), inputs resident in HBM;
+successive steps ping-pong phi <-> out on the same band. L2 (126 MB) is
+flushed by a 256 MB write between timed steps. Units = active node-updates.
+`moving_band` reports the same metric inside the real loop, where the band
+is rebuilt every iteration (so the covered-brick list is rebuilt too).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C]
 
-N > 1 (torchrun): z-slab decomposition — each rank owns a band-balanced
-range of z-planes, updates only its active nodes, and exchanges halo planes
-of phi^{n+1} with its neighbours over NCCL after every step.
+N > 1: one rank per GPU (bench.py relaunches itself under torch.distributed.run
+when WORLD_SIZE is unset); z-slab decomposition — each rank owns a
+band-balanced range of z-planes, updates only its active nodes, and the halo
+planes reach the neighbours through the fused peer push (or NCCL).
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
 import subprocess
 import sys
 import threading
@@ -33,21 +39,30 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-METRIC = "SL narrow-band node-updates/s (WENO, 512^3, fp64)"
 UNIT = "node-updates/s"
 BYTES_PER_UPDATE = {("weno", 3): 2176, ("q1", 3): 384, ("weno", 2): 352, ("q1", 2): 160}
+COMPULSORY_BYTES = 32  # phi_j, d_j, out, id (SURVEY §8(d) "A")
+SEED = 2410
 
 CONFIGS = {
-    # id: (n, dim, cloud config, points, sigma in dx, interp, phi0 radius, p, delta)
-    4: dict(n=512, dim=3, cloud=4, points=1_000_000, sigma=0.0, interp=1, r0=0.9, p=2, delta=1.0,
-            name="bumpy-sphere-512", shape="bumpy-sphere cloud"),
-    3: dict(n=256, dim=3, cloud=3, points=100_000, sigma=0.5, interp=1, r0=0.9, p=2, delta=1.0,
-            name="torus-256", shape="noisy torus cloud"),
-    5: dict(n=1024, dim=3, cloud=5, points=4_000_000, sigma=0.25, interp=1, r0=0.95, p=2, delta=1.0,
-            name="three-tori-1024", shape="three-tori cloud with two holes"),
+    # id: grid nodes per axis, dim, cloud generator id, points, noise (in dx), interp (0 Q1, 1 WENO),
+    #     phi^0 sphere radius, p, delta
+    1: dict(n=257, dim=2, cloud=1, points=200, sigma=0.0, interp=0, r0=0.9, p=1, delta=0.0,
+            name="circle-257", shape="circle cloud"),
     2: dict(n=128, dim=3, cloud=2, points=20_000, sigma=0.0, interp=0, r0=0.9, p=2, delta=1.0,
             name="sphere-128", shape="sphere cloud"),
+    3: dict(n=256, dim=3, cloud=3, points=100_000, sigma=0.5, interp=1, r0=0.9, p=2, delta=1.0,
+            name="torus-256", shape="noisy torus cloud"),
+    4: dict(n=512, dim=3, cloud=4, points=1_000_000, sigma=0.0, interp=1, r0=0.9, p=2, delta=1.0,
+            name="bumpy-sphere-512", shape="bumpy-sphere cloud"),
+    5: dict(n=1024, dim=3, cloud=5, points=4_000_000, sigma=0.25, interp=1, r0=0.95, p=2, delta=1.0,
+            name="three-tori-1024", shape="three-tori cloud with two holes"),
 }
+
+
+def metric_name(cfg) -> str:
+    grid = f"{cfg['n']}^{cfg['dim']}"
+    return f"SL narrow-band node-updates/s ({'WENO' if cfg['interp'] == 1 else 'Q1'}, {grid}, fp64)"
 
 
 def dist_env():
@@ -57,24 +72,37 @@ def dist_env():
     return world, rank, local
 
 
-def peaks():
+def _json(path):
     try:
-        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
-            p = json.load(f)
-        return float(p["hbm_gbs"]), "measured"
+        with open(os.path.join(ROOT, path)) as f:
+            return json.load(f)
     except Exception:
-        return 6650.0, "fallback"
+        return None
+
+
+def peaks():
+    p = _json("MEASURED_PEAKS.json")
+    if p and "hbm_gbs" in p:
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def fp64_peak():
+    """Measured DFMA thread-instruction rate of this B200 model
+    (tools/fp64_peak.cu, profiles/fp64_peak.json)."""
+    p = _json(os.path.join("profiles", "fp64_peak.json"))
+    if p and p.get("dfma_per_s"):
+        return float(p["dfma_per_s"]), p.get("source")
+    return None, None
 
 
 def traffic_per_update():
-    """DRAM bytes per node-update of the SL kernel from the committed ncu
-    capture (profiles/sl_step_traffic.json), or None."""
-    try:
-        with open(os.path.join(ROOT, "profiles", "sl_step_traffic.json")) as f:
-            t = json.load(f)
-        return float(t["dram_bytes_per_update"]), t
-    except Exception:
+    """DRAM bytes and fp64 instructions per node-update of the SL kernel from
+    the committed ncu capture (profiles/sl_step_traffic.json), or None."""
+    t = _json(os.path.join("profiles", "sl_step_traffic.json"))
+    if not t:
         return None, None
+    return float(t["dram_bytes_per_update"]), t
 
 
 class ClockSampler:
@@ -139,24 +167,56 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(rows), "power_w_max": max(pw) if pw else None}
 
 
+
 # ---------------------------------------------------------------------------
 # workload construction
 
 
-def make_inputs(lsr, cfg, seed=2410):
-    g = lsr.cube_grid(cfg["n"], cfg["dim"])
-    pts = lsr.cloud_generate(cfg["cloud"], cfg["points"], seed=seed, sigma=cfg["sigma"] * g.dx)
-    ax = g.axes()
-    if cfg["dim"] == 3:
+def workload(cfg, cloud_fn, seed=SEED):
+    """The config's inputs, shared by both arms (numpy only, no product code):
+    the grid (n nodes per axis on [-1, 1]^dim, dx = 2/(n-1)), the seeded
+    cloud (cloud_fn = the generator of include/lsr_workloads.h, linked into
+    the product library for our arm and into oracle/_ref for the reference
+    arm), phi^0 = |x| - r0, narrow_band's ACTIVE set |phi| < gamma
+    (grid.cpp:85-88) and the step parameters (dt = dx/4, driver.hpp:27;
+    default_band_params, grid.cpp:49-51)."""
+    n, dim = cfg["n"], cfg["dim"]
+    dx = 2.0 / (n - 1)
+    gd = dict(dim=dim, dims=(n, n, n) if dim == 3 else (n, n, 1), origin=(-1.0, -1.0, -1.0 if dim == 3 else 0.0),
+              dx=dx)
+    pts = cloud_fn(cfg["cloud"], cfg["points"], seed=seed, sigma=cfg["sigma"] * dx)
+    ax = [gd["origin"][d] + np.arange(gd["dims"][d], dtype=np.float64) * dx for d in range(3)]  # Grid::node
+    if dim == 3:
         r = np.sqrt(ax[0][None, None, :] ** 2 + ax[1][None, :, None] ** 2 + ax[2][:, None, None] ** 2)
     else:
         r = np.sqrt(ax[0][None, :] ** 2 + ax[1][:, None] ** 2)
     phi = (r - cfg["r0"]).reshape(-1)
-    bp = lsr.default_band_params(cfg["dim"], g.dx)
-    active = np.flatnonzero(np.abs(phi) < bp.gamma).astype(np.int64)  # narrow_band's ACTIVE set (grid.cpp:85-88)
-    step = lsr.StepConfig(p=cfg["p"], delta=cfg["delta"], dt=0.25 * g.dx, interp=lsr.InterpolatorKind(cfg["interp"]),
-                          band=bp)
-    return g, pts, phi, active, step
+    gamma, beta = (6.0 * dx, 3.0 * dx) if dim == 3 else (4.0 * dx, 2.0 * dx)
+    active = np.flatnonzero(np.abs(phi) < gamma).astype(np.int64)
+    step = dict(p=cfg["p"], interp=cfg["interp"], delta=cfg["delta"], dt=0.25 * dx, fallback_c=1e-3,
+                fallback_alpha=1.0, gamma=gamma, beta=beta)
+    return dict(grid=gd, pts=pts, phi=phi, active=active, step=step)
+
+
+def config_block(cfg, w):
+    """The JSON line's `config`: the workload only, identical in both arms."""
+    st = w["step"]
+    return {"workload": cfg["name"], "grid": list(w["grid"]["dims"]), "cloud_points": cfg["points"],
+            "cloud_seed": SEED, "phi0": f"|x| - {cfg['r0']}", "active_nodes": int(w["active"].size),
+            "interp": "weno" if cfg["interp"] == 1 else "q1", "p": st["p"], "delta": st["delta"], "dt": st["dt"],
+            "gamma": st["gamma"], "beta": st["beta"],
+            "l2": "the GPU arm flushes L2 (256 MB write) between timed steps"}
+
+
+def make_inputs(lsr, cfg):
+    """workload() in the product's host types."""
+    w = workload(cfg, lsr.cloud_generate)
+    gd = w["grid"]
+    g = lsr.Grid(gd["dim"], tuple(gd["origin"]), gd["dx"], tuple(gd["dims"]))
+    st = w["step"]
+    step = lsr.StepConfig(p=st["p"], delta=st["delta"], dt=st["dt"], interp=lsr.InterpolatorKind(st["interp"]),
+                          band=lsr.BandParams(st["gamma"], st["beta"]))
+    return g, w, step
 
 
 # ---------------------------------------------------------------------------
@@ -175,7 +235,8 @@ def run_ours(args):
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     cfg = CONFIGS[args.config]
-    g, pts, phi, active, step = make_inputs(lsr, cfg)
+    g, w, step = make_inputs(lsr, cfg)
+    pts, phi, active = w["pts"], w["phi"], w["active"]
     nxy = g.dims[0] * g.dims[1]
     # one explicit (non-legacy) stream for everything: the context's kernels,
     # the L2 flush and the timing events are then ordered on it
@@ -319,8 +380,13 @@ def run_ours(args):
     kern_avg_ms = float(np.mean(kernel_ms))
     hbm_peak, peak_kind = peaks()
     bpu = BYTES_PER_UPDATE[("weno" if cfg["interp"] == 1 else "q1", cfg["dim"])]
-    achieved = mine.size * bpu / (kern_avg_ms * 1e-3) / 1e9
+    kernel_rate = mine.size / (kern_avg_ms * 1e-3)  # this rank's node-updates per second of SL kernel
+    achieved = kernel_rate * bpu / 1e9
     traffic_pu, traffic_info = traffic_per_update()
+    f64_peak, f64_src = fp64_peak()
+    # the committed capture describes the headline kernel (config 4, WENO-3D table path) only
+    capture_applies = bool(traffic_info) and traffic_info.get("config") == args.config
+    f64_pu = traffic_info.get("fp64_inst_per_update") if capture_applies else None
 
     e2e = None
     cpu = None
@@ -336,7 +402,7 @@ def run_ours(args):
 
     if rank == 0:
         line = {
-            "metric": METRIC,
+            "metric": metric_name(cfg),
             "value": value,
             "unit": UNIT,
             "n_gpus": world,
@@ -348,18 +414,14 @@ def run_ours(args):
             "vs_baseline": None,
             "dtype": "f64",
             "data": f"synthetic (seeded {cfg['shape']}, BASELINE config {args.config} shapes/sizes)",
-            "config": {
-                "workload": cfg["name"],
-                "grid": list(g.dims),
-                "cloud_points": cfg["points"],
-                "active_nodes": int(active.size),
-                "interp": "weno" if cfg["interp"] == 1 else "q1",
-                "p": cfg["p"], "delta": cfg["delta"], "dt": step.dt, "gamma": step.band.gamma,
+            "config": config_block(cfg, w),
+            "run": {
                 "energy_e2": e2, "dist_sweep_rounds": rounds,
-                "l2": "flushed (256 MB write) between timed steps",
                 "parallelism": f"z-slab x{world}" if world > 1 else "single GPU",
                 "halo_exchange": exchange_mode if world > 1 else None,
                 "halo_planes": halo,
+                "step": "resync + z-line table fill + SL kernel" if (cfg["interp"] == 1 and cfg["dim"] == 3
+                                                                      and cfg["delta"] > 0) else "resync + SL kernel",
             },
             "roofline": {
                 "bound": "hbm",
@@ -367,22 +429,32 @@ def run_ours(args):
                 "peak": hbm_peak,
                 "unit": "GB/s",
                 "frac": achieved / hbm_peak,
-                "traffic": (traffic_pu * mine.size) if traffic_pu else None,
+                "traffic": (traffic_pu * mine.size) if (traffic_pu and capture_applies) else None,
                 "peak_source": peak_kind,
                 "algorithmic_bytes_per_update": bpu,
                 "kernel_ms_avg": kern_avg_ms,
                 "table_fill_ms_avg": float(np.mean(table_ms[-args.steps:])) if table_ms else None,
+                # the compulsory-byte fraction and the measured fp64-peak fraction
+                "compulsory_bytes_per_update": COMPULSORY_BYTES,
+                "compulsory_frac": kernel_rate * COMPULSORY_BYTES / 1e9 / hbm_peak,
+                "fp64_inst_per_update": f64_pu,
+                "fp64_peak_inst_per_s": f64_peak,
+                "fp64_peak_source": f64_src,
+                "fp64_frac": (f64_pu * kernel_rate / f64_peak) if (f64_pu and f64_peak) else None,
                 "ncu": ({k: traffic_info[k] for k in ("fp64_pipe_active", "l1_hit", "l2_hit", "source")
-                         if k in traffic_info} if traffic_info else None),
-                "note": "reference-access bytes per node-update (SURVEY 8(d)) over the SL kernel's time; the "
-                        "kernel is bound by fp64 issue and load latency, not by DRAM (ncu: fp64 pipe active, "
-                        "L1/L2 hit rates of the committed capture). The step (value, ms_per_step) also holds "
-                        "the z-line table fill (table_fill_ms_avg) and the sparse resync",
+                         if k in traffic_info} if capture_applies else None),
+                "note": "achieved = reference-access bytes per node-update (SURVEY 8(d)) over the SL kernel's "
+                        "time; the kernel is bound by fp64 issue and load latency, not by DRAM: fp64_frac = fp64 "
+                        "instructions per update (ncu capture) x kernel rate / measured DFMA rate; "
+                        "compulsory_frac = 32 B per update at the kernel rate. The step (value, ms_per_step) "
+                        "also holds the z-line table fill (table_fill_ms_avg) and the sparse resync",
             },
             "gpu_launches": int(launches),
             "clocks": clk.summary(),
             "setup_s": {"build_distance": t_dist, "surface_energy": t_energy},
         }
+        if loop and loop.get("moving_band"):
+            line["moving_band"] = loop["moving_band"]
         if e2e:
             line["e2e"] = e2e
         if cpu:
@@ -517,17 +589,25 @@ def measure_e2e(lsr, g, phi, ctx, active, step, e2, args):
             "steps": args.e2e_steps}
 
 
-def measure_loop(lsr, g, phi, ctx, step, steps=4, cpu_too=True):
+def measure_loop(lsr, g, phi, ctx, step, steps=6, cpu_too=True):
     """The whole driver iteration (driver.cpp:187-203: band, E_2, SL,
     reinit, swap) from phi^0 on the device, per-phase device ms, next to one
-    iteration of the reference's own loop body on the host cores."""
+    iteration of the reference's own loop body on the host cores. Its SL
+    phase gives `moving_band`: the headline metric when the band (and so the
+    z-line table's covered-brick list) is rebuilt every iteration."""
     ctx.upload(lsr._api.FIELD_PHI, phi)
     rc = lsr.ReinitConfig.defaults(g.dx, step.band.gamma)
     stats = [ctx.loop_step(step, rc, 5) for _ in range(steps)]
     ms = np.array([s["ms"] for s in stats[1:]])  # first iteration includes workspace allocation
+    na = np.array([s["n_active"] for s in stats[1:]], dtype=np.float64)
     out = {"gpu_ms_per_step": dict(zip(("band", "energy", "sl", "reinit"), map(float, ms.mean(0)))),
            "gpu_total_ms_per_step": float(ms.sum(1).mean()), "steps": steps,
            "reinit_iterations": [s["reinit_iterations"] for s in stats]}
+    out["moving_band"] = {
+        "value": float(na.sum() / (ms[:, 2].sum() * 1e-3)), "unit": UNIT,
+        "sl_ms_per_step": float(ms[:, 2].mean()), "active_nodes_mean": float(na.mean()), "iterations": steps - 1,
+        "what": "SL phase of the device loop (band rebuilt every iteration: covered-brick list, z-line table "
+                "fill, sparse resync, SL kernel), CUDA events; loop iterations 2..N from phi^0"}
     if cpu_too:
         from oracle import bindings
 
@@ -594,35 +674,34 @@ def cpu_baseline(g, phi, ctx, active, step, e2, lsr, reps=3):
 def run_reference(args):
     """--impl reference: the reference's own CPU lsr::sl_step (oracle/_ref,
     built from the reference sources; OpenMP over all host cores) on the same
-    workload, inputs produced by the reference's own functions."""
+    workload, inputs produced by the reference's own functions. Nothing of
+    the product is imported or loaded here: the cloud generator is linked
+    into oracle/_ref as well."""
     world, rank, local = dist_env()
     if rank != 0:
         return
     from oracle import bindings
 
-    import paper_2410_22205_b200 as lsr  # host-side types and the seeded cloud generator only
-
     cfg = CONFIGS[args.config]
-    g, pts, phi, active, step = make_inputs(lsr, cfg)
-    gd = dict(dim=g.dim, dims=g.dims, origin=g.origin, dx=g.dx)
     threads = os.cpu_count() or 1
-    if bindings.reference_available():
-        R = bindings.Reference()
-        R.set_threads(threads)
-        kind = "reference"
-    else:
+    if not bindings.reference_available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built on this machine"}))
         return
+    R = bindings.Reference()
+    R.set_threads(threads)
+    kind = "reference"
+    w = workload(cfg, R.cloud_generate)
+    gd, phi, step = w["grid"], w["phi"], w["step"]
     t0 = time.perf_counter()
-    d, _, _, rounds = R.build_distance(gd, pts, cfg["dim"])  # lsr::build_distance_field
+    d, _, _, rounds = R.build_distance(gd, w["pts"], cfg["dim"])  # lsr::build_distance_field
     t_dist = time.perf_counter() - t0
     e2 = R.surface_energy(gd, phi, d, 2, 5)
-    _, act_ref, _ = R.narrow_band(gd, phi, step.band.gamma)
-    cc = dict(p=step.p, interp=int(step.interp), delta=step.delta, dt=step.dt, fallback_c=step.fallback_c,
-              fallback_alpha=step.fallback_alpha, gamma=step.band.gamma, beta=step.band.beta)
+    _, act_ref, _ = R.narrow_band(gd, phi, step["gamma"])
+    if not np.array_equal(act_ref, w["active"]):
+        raise RuntimeError("the reference's narrow_band differs from the workload's active set")
     h = R.ctx(gd, phi, d, act_ref)
     # bound the run to a few minutes: sample a contiguous share of the band per step if needed
-    probe = R.ctx_sl_step(h, cc, e2)
+    probe = R.ctx_sl_step(h, step, e2)
     budget = 150.0
     frac = min(1.0, budget / max(1e-9, probe * (args.steps + args.warmup)))
     if frac < 1.0:
@@ -633,25 +712,36 @@ def run_reference(args):
     else:
         units = act_ref.size
     for _ in range(args.warmup):
-        R.ctx_sl_step(h, cc, e2)
-    secs = [R.ctx_sl_step(h, cc, e2) for _ in range(args.steps)]
+        R.ctx_sl_step(h, step, e2)
+    secs = [R.ctx_sl_step(h, step, e2) for _ in range(args.steps)]
     R.ctx_free(h)
     t = float(np.sum(secs))
     value = units * args.steps / t
     sample = (f"{units} of {act_ref.size} active nodes per step (lsr::sl_step incl. its O(N) copy), "
               f"OpenMP {threads} threads")
     print(json.dumps({
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps, "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "f64",
+        "impl": "reference", "metric": metric_name(cfg), "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": f"synthetic (seeded {cfg['shape']}, BASELINE config {args.config} shapes/sizes)",
-        "config": {"workload": cfg["name"], "grid": list(g.dims), "cloud_points": cfg["points"],
-                   "active_nodes": int(act_ref.size), "energy_e2": e2, "dist_sweep_rounds": rounds,
-                   "setup_build_distance_s": t_dist},
+        "config": config_block(cfg, w),
+        "run": {"energy_e2": e2, "dist_sweep_rounds": rounds, "setup_build_distance_s": t_dist,
+                "parallelism": f"OpenMP, {threads} host threads"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "cpu_model": cpu_model(), "kind": kind,
                          "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
+
+
+def relaunch_under_torchrun(args) -> int:
+    """`bench.py --gpus N` without a torch.distributed launcher: start N ranks
+    (one per GPU) on this node and pass their output through."""
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
 
 
 def main():
@@ -670,6 +760,8 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch_under_torchrun(args))
     if args.impl == "reference":
         run_reference(args)
     else:

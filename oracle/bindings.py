@@ -188,8 +188,11 @@ class Reference:
                                            C.POINTER(C.c_double), C.POINTER(C.c_double), _dp]
         L.lsrref_loop_step.argtypes = [C.POINTER(CGrid), _dp, _dp, C.POINTER(CCfg), C.c_int, C.POINTER(C.c_double),
                                        C.POINTER(C.c_int64), C.POINTER(C.c_int), _dp]
+        L.lsrref_loop_run.argtypes = [C.POINTER(CGrid), _dp, _dp, C.POINTER(CCfg), C.c_int, C.c_int, _dp, _ip,
+                                      _i32p]
         L.lsrref_set_threads.argtypes = [C.c_int]
         L.lsrref_max_threads.restype = C.c_int
+        L.lsr_cloud_generate.argtypes = [C.c_int, C.c_int64, C.c_uint64, C.c_double, _dp]
 
     def _err(self, st):
         if st:
@@ -335,6 +338,25 @@ class Reference:
                                             C.byref(ccfg(cfg)), int(refine), C.byref(e2), C.byref(na), C.byref(it),
                                             sec))
         return phi, e2.value, na.value, it.value, sec
+
+    def loop_run(self, grid, phi, dist, cfg, iters, refine=5):
+        """iters loop iterations; returns (phi, e2 per iteration, |active| per
+        iteration, reinit iterations per iteration)."""
+        phi = np.array(phi, dtype=np.float64).ravel()
+        e2 = np.zeros(iters)
+        na = np.zeros(iters, np.int64)
+        it = np.zeros(iters, np.int32)
+        self._err(self.lib.lsrref_loop_run(C.byref(cgrid(grid)), phi, np.ascontiguousarray(dist, np.float64).ravel(),
+                                           C.byref(ccfg(cfg)), int(refine), int(iters), e2, na, it))
+        return phi, e2, na, it
+
+    def cloud_generate(self, config, n, seed=0, sigma=0.0):
+        """The seeded BASELINE cloud (paper_2410_22205_b200/csrc/workloads.cpp,
+        compiled into this library), shape (n, 3)."""
+        pts = np.zeros((int(n), 3))
+        if self.lib.lsr_cloud_generate(int(config), int(n), int(seed), float(sigma), pts.reshape(-1)) != 0:
+            raise OracleError(1, f"unknown cloud config {config}")
+        return pts
 
     # bench helpers -------------------------------------------------------
     def ctx(self, grid, phi, dist, active):

@@ -397,4 +397,32 @@ int lsrref_loop_step(const RGrid* rg, double* phi, const double* dist, const RCf
     });
 }
 
+// K iterations of the same loop body without leaving the library (the long
+// end-to-end parity runs): per iteration the E2, |active| and reinit
+// iteration count it used. phi is updated in place.
+int lsrref_loop_run(const RGrid* rg, double* phi, const double* dist, const RCfg* rc, int energy_refine,
+                    int iters, double* e2s, int64_t* n_active, int* reinit_iters) {
+    return guarded([&] {
+        const lsr::Grid g = to_grid(rg);
+        lsr::ScalarField f = to_field(g, phi);
+        lsr::DistanceField d;
+        d.field = to_field(g, dist);
+        const lsr::StepConfig step = to_cfg(rc);
+        const lsr::ReinitConfig rcfg = lsr::ReinitConfig::defaults(g.dx, step.band.gamma);
+        lsr::ScalarField next(g);
+        for (int it = 0; it < iters; ++it) {
+            const lsr::BandMask band = lsr::narrow_band(f, step.band.gamma);
+            const double e2 = lsr::surface_energy(f, d, 2, energy_refine);
+            if (step.p > 1 && e2 == 0.0) next.values = f.values;
+            else lsr::sl_step(f, d, band, step, e2, next);
+            const lsr::ReinitResult rr = lsr::reinitialize(next, band, step.band.gamma, rcfg);
+            e2s[it] = e2;
+            n_active[it] = static_cast<int64_t>(band.active.size());
+            reinit_iters[it] = rr.iterations;
+            std::swap(f.values, next.values);
+        }
+        std::memcpy(phi, f.values.data(), sizeof(double) * f.values.size());
+    });
+}
+
 }  // extern "C"
