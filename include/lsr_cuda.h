@@ -255,6 +255,13 @@ int lsr_cuda_loop_step(lsr_cuda_ctx* ctx, const lsr_step_cfg* cfg, const lsr_rei
  * division and with the hardware IEEE division; *mismatches = how many
  * quotients differ in any bit (must be 0). */
 int lsr_cuda_selftest_div_const(double c, int64_t n, uint64_t seed, int64_t* mismatches);
+/* Differential test of the exact fast WENO forms (weno1_fast, and weno1_zt
+ * fed the z-line table's terms) against weno_1d with the plain IEEE
+ * operators, over n pseudo-random stencils and abscissae (smooth lines, raw
+ * bit patterns, lines at the range/halving guards, tiny differences) at this
+ * dx (in [2^-30, 1]). counts[4] = fast path taken, fast mismatches, table
+ * path taken, table mismatches; both mismatch counts must be 0. */
+int lsr_cuda_selftest_weno(double dx, int64_t n, uint64_t seed, int64_t* counts);
 
 #ifdef __cplusplus
 }

@@ -339,10 +339,13 @@ class Reference:
                                             sec))
         return phi, e2.value, na.value, it.value, sec
 
-    def loop_run(self, grid, phi, dist, cfg, iters, refine=5):
+    def loop_run(self, grid, phi, dist, cfg, iters, refine=5, inplace=False):
         """iters loop iterations; returns (phi, e2 per iteration, |active| per
-        iteration, reinit iterations per iteration)."""
-        phi = np.array(phi, dtype=np.float64).ravel()
+        iteration, reinit iterations per iteration). inplace: phi (contiguous
+        float64) is overwritten instead of copied."""
+        if not (inplace and isinstance(phi, np.ndarray) and phi.dtype == np.float64 and phi.flags.c_contiguous):
+            phi = np.array(phi, dtype=np.float64)
+        phi = phi.reshape(-1)
         e2 = np.zeros(iters)
         na = np.zeros(iters, np.int64)
         it = np.zeros(iters, np.int32)

@@ -121,6 +121,7 @@ def lib() -> C.CDLL:
                                           C.c_int64, P(CStepCfg), C.c_double, C.c_void_p, C.c_void_p, C.c_void_p,
                                           C.c_void_p]
     L.lsr_cuda_selftest_div_const.argtypes = [C.c_double, C.c_int64, C.c_uint64, P(C.c_int64)]
+    L.lsr_cuda_selftest_weno.argtypes = [C.c_double, C.c_int64, C.c_uint64, P(C.c_int64)]
     L.lsr_cuda_build_distance.argtypes = [P(CGrid), _dp, C.c_int64, C.c_int, C.c_int, C.c_void_p, C.c_void_p,
                                           P(C.c_double), P(C.c_int)]
     L.lsr_cuda_ctx_build_distance.argtypes = [C.c_void_p, _dp, C.c_int64, C.c_int, C.c_int, P(C.c_double),
@@ -275,6 +276,14 @@ def selftest_div_const(c: float, n: int, seed: int = 1) -> int:
     m = C.c_int64()
     _check(lib().lsr_cuda_selftest_div_const(float(c), int(n), int(seed), C.byref(m)))
     return int(m.value)
+
+
+def selftest_weno(dx: float, n: int, seed: int = 1) -> dict:
+    """GPU differential test of the fast exact WENO forms against the plain
+    IEEE weno_1d (lsr_cuda_selftest_weno)."""
+    c = (C.c_int64 * 4)()
+    _check(lib().lsr_cuda_selftest_weno(float(dx), int(n), int(seed), c))
+    return dict(fast_taken=int(c[0]), fast_mismatch=int(c[1]), table_taken=int(c[2]), table_mismatch=int(c[3]))
 
 
 def _check(status: int) -> None:

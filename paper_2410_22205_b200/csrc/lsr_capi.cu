@@ -1427,4 +1427,29 @@ int lsr_cuda_selftest_div_const(double c, int64_t n, uint64_t seed, int64_t* mis
     return LSR_OK;
 }
 
+int lsr_cuda_selftest_weno(double dx, int64_t n, uint64_t seed, int64_t* counts) {
+    if (!counts || n < 0) return set_err(LSR_ERR_CONFIG, "selftest_weno: bad arguments");
+    lsr_grid g{};
+    g.dim = 3;
+    g.dims[0] = g.dims[1] = g.dims[2] = 8;
+    g.dx = dx;
+    lsr_step_cfg c{};
+    c.p = 1;
+    c.interp = LSR_INTERP_WENO;
+    c.dt = dx;
+    c.gamma = 2.0;
+    c.beta = 1.0;
+    const SlParams P = make_params(g, c, 1.0);
+    if (!P.fast_weno) return set_err(LSR_ERR_CONFIG, "selftest_weno: dx outside the fast path's range [2^-30, 1]");
+    unsigned long long* d = nullptr;
+    LSR_CUDA_TRY(cudaMalloc(&d, 4 * sizeof(unsigned long long)));
+    LSR_CUDA_TRY(cudaMemset(d, 0, 4 * sizeof(unsigned long long)));
+    LSR_CUDA_TRY(launch_weno_selftest(P, seed, n, d));
+    unsigned long long h[4] = {0, 0, 0, 0};
+    LSR_CUDA_TRY(cudaMemcpy(h, d, sizeof h, cudaMemcpyDeviceToHost));
+    cudaFree(d);
+    for (int q = 0; q < 4; ++q) counts[q] = static_cast<int64_t>(h[q]);
+    return LSR_OK;
+}
+
 }  // extern "C"

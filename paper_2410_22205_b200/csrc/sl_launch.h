@@ -63,6 +63,9 @@ cudaError_t launch_check_sorted(const int64_t* ids, long long n, unsigned long l
 
 cudaError_t launch_resync(const double* phi, double* out, const int64_t* ids, long long n, cudaStream_t stream);
 
+cudaError_t launch_weno_selftest(const lsr_dev::SlParams& P, unsigned long long seed, long long n,
+                                 unsigned long long* counts);
+
 cudaError_t launch_div_selftest(double c, double rc, unsigned long long seed, long long n,
                                 unsigned long long* mismatches);
 

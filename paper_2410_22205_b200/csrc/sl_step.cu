@@ -203,13 +203,8 @@ __global__ void __launch_bounds__(256) zt_fill_kernel(SlParams P, const double* 
         double vm = __ldg(phi + id - P.nxy), v0 = __ldg(phi + id), vp = __ldg(phi + id + P.nxy);
         for (int k = k0; k < k1; ++k, id += P.nxy) {
             const double vpp = k + 2 < top ? __ldg(phi + id + 2 * P.nxy) : 0.0;
-            const double sd = vm - 2.0 * v0 + vp;  // weno1_fast's sdl / sdr
-            const double a = sqr(sd);
-            bool good = square_in_range(a);
-            double il = a * P.rdx2;
-            il = __fma_rn(__fma_rn(-il, P.dx2, a), P.rdx2, il);
-            const double S = sqr(il + P.dx2);
-            const double Y = recip_seq(S);
+            double sd, S, Y;  // weno1_fast's sdl / sdr and its alpha denominator
+            bool good = zt_node_terms(P, vm, v0, vp, sd, S, Y);
             const double c1 = vp - vm;                      // d1
             const double e2 = -3.0 * v0 + 4.0 * vp - vpp;  // d2
             if (k + 2 < top) good = good & halvable(c1) & halvable(e2);  // else e2 is never read (no stencil has K = k)
@@ -265,6 +260,108 @@ __global__ void div_selftest_kernel(double c, double rc, unsigned long long seed
     if (bad) atomicAdd(mismatches, bad);
 }
 
+// Differential self-test of the exact fast WENO forms against weno1 (the
+// plain IEEE operators, interp.cpp:16-33): for n pseudo-random stencils
+// (vm, v0, vp, vpp) and abscissae theta, weno1_fast must return weno1's bits
+// whenever its guards pass (theta_in_range and the in-function checks), and
+// weno1_zt fed the table terms zt_fill_kernel would store (zt_node_terms of
+// K = v0 and K + 1 = vp, d1, d2) must too whenever the fill's checks and
+// theta_in_range pass. Sample classes (i mod 4): 0 smooth lines at random
+// scales 2^-60..2^20; 1 raw random bit patterns (every exponent, zeros,
+// subnormals, inf, NaN); 2 lines whose squared second differences sit at the
+// range guards 2^-700 / 2^200 (+-few ulp) and differences at the halving
+// guard 2^-1021; 3 tiny/subnormal/zero differences. theta is drawn from
+// [-0.7, 1.7] or, one sample in four, from the guard values -1/2, 0, -0, 3/2,
+// +-2^-510, +-2^-511 and their neighbours.
+// counts: [0] fast taken, [1] fast mismatches, [2] table taken, [3] table
+// mismatches.
+__device__ __forceinline__ unsigned long long mix64(unsigned long long z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+
+__device__ __forceinline__ double unit01(unsigned long long z) { return static_cast<double>(z >> 11) * 0x1.0p-53; }
+
+__device__ __forceinline__ double nudge(double x, int ulps) {  // x moved by `ulps` units in the last place
+    return __longlong_as_double(__double_as_longlong(x) + ulps);
+}
+
+__global__ void weno_selftest_kernel(SlParams P, unsigned long long seed, long long n,
+                                     unsigned long long* __restrict__ counts) {
+    unsigned long long c[4] = {0, 0, 0, 0};
+    const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+    for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+        unsigned long long z = seed + 0x9E3779B97F4A7C15ULL * static_cast<unsigned long long>(i + 1);
+        auto next = [&z]() {
+            z += 0x9E3779B97F4A7C15ULL;
+            return mix64(z);
+        };
+        double v[4];
+        const int cls = static_cast<int>(i & 3);
+        if (cls == 0) {  // smooth: quadratic + small noise, random scale
+            const double sc = ldexp(1.0, static_cast<int>(next() % 81) - 60);
+            const double a0 = unit01(next()) - 0.5, a1 = unit01(next()) - 0.5, a2 = (unit01(next()) - 0.5) * 0.1;
+            for (int q = 0; q < 4; ++q)
+                v[q] = sc * (a0 + a1 * (q - 1) + a2 * (q - 1) * (q - 1) + 1e-6 * (unit01(next()) - 0.5));
+        } else if (cls == 1) {  // raw bit patterns
+            for (int q = 0; q < 4; ++q) v[q] = __longlong_as_double(static_cast<long long>(next()));
+        } else if (cls == 2) {  // at the guards
+            const unsigned long long r = next();
+            const int ulps = static_cast<int>(r % 9) - 4;
+            const int which = static_cast<int>((r >> 8) % 6);
+            const double s = (r >> 16) & 1 ? -1.0 : 1.0;
+            for (int q = 0; q < 4; ++q) v[q] = 0.0;
+            // sd^2 = 2^-700 <=> |sd| = 2^-350; sd^2 = 2^200 <=> |sd| = 2^100; d/2 exact down to 2^-1021
+            const double mag = which == 0 ? 0x1.0p-350 : which == 1 ? 0x1.0p100 : which == 2 ? 0x1.0p-1021 : which == 3
+                ? 0x1.6a09e667f3bcdp-351 /* sqrt(2^-701) */ : which == 4 ? 0x1.6a09e667f3bcdp+99 : 0x1.0p-1022;
+            const int slot = static_cast<int>((r >> 20) & 3);
+            v[slot] = s * nudge(mag, ulps);
+            if ((r >> 24) & 1) v[(slot + 1) & 3] = 0.5 * v[slot];
+        } else {  // tiny / subnormal / zero differences around a base value
+            const double base = unit01(next()) - 0.5;
+            for (int q = 0; q < 4; ++q) {
+                const unsigned long long r = next();
+                v[q] = (r & 3) == 0 ? base : (r & 3) == 1 ? 0.0 : (r & 3) == 2 ? nudge(base, static_cast<int>(r % 5) - 2)
+                                                                               : __longlong_as_double(static_cast<long long>(r >> 12));
+            }
+        }
+        double t;
+        {
+            const unsigned long long r = next();
+            if ((r & 3) != 0) {
+                t = -0.7 + 2.4 * unit01(next());
+            } else {
+                const double special[8] = {-0.5, 0.0, -0.0, 1.5, 0x1.0p-510, -0x1.0p-510, 0x1.0p-511, -0x1.0p-511};
+                t = special[(r >> 2) & 7];
+                if ((r >> 5) & 1) t = nudge(t, ((r >> 6) & 1) ? 1 : -1);
+                if (t == 0.0 && ((r >> 7) & 1)) t = __longlong_as_double(static_cast<long long>((r >> 8) & 0xfffff));
+            }
+        }
+        const AxisW w = axis_weights(P, t);
+        const double ref = weno1(P, w, v[0], v[1], v[2], v[3]);
+        bool ok = theta_in_range(t);
+        const double fast = weno1_fast(P, w, v[0], v[1], v[2], v[3], ok);
+        if (ok) {
+            ++c[0];
+            if (__double_as_longlong(fast) != __double_as_longlong(ref)) ++c[1];
+        }
+        double sdK, SK, YK, sdK1, SK1, YK1;
+        bool good = zt_node_terms(P, v[0], v[1], v[2], sdK, SK, YK);
+        good = good & zt_node_terms(P, v[1], v[2], v[3], sdK1, SK1, YK1);
+        const double c1 = v[2] - v[0], e2 = -3.0 * v[1] + 4.0 * v[2] - v[3];
+        good = good & halvable(c1) & halvable(e2) & theta_in_range(t);
+        if (good) {
+            ++c[2];
+            const double zt = weno1_zt(w, make_double4(sdK, SK, YK, v[1]), make_double4(sdK1, SK1, YK1, v[2]),
+                                       make_double2(c1, e2));
+            if (__double_as_longlong(zt) != __double_as_longlong(ref)) ++c[3];
+        }
+    }
+    for (int q = 0; q < 4; ++q)
+        if (c[q]) atomicAdd(counts + q, c[q]);
+}
+
 // one warp per run of packed values (host_pack.h)
 __global__ void scatter_runs_kernel(const double* __restrict__ packed, const long long* __restrict__ desc,
                                     long long r0, long long r1, long long vend, double* __restrict__ field) {
@@ -310,6 +407,12 @@ cudaError_t launch_scatter_runs(const double* packed, const long long* desc, lon
 cudaError_t launch_div_selftest(double c, double rc, unsigned long long seed, long long n,
                                 unsigned long long* mismatches) {
     div_selftest_kernel<<<148 * 8, 256>>>(c, rc, seed, n, mismatches);
+    lsr_note_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_weno_selftest(const SlParams& P, unsigned long long seed, long long n, unsigned long long* counts) {
+    weno_selftest_kernel<<<148 * 8, 256>>>(P, seed, n, counts);
     lsr_note_launch();
     return cudaGetLastError();
 }

@@ -177,6 +177,22 @@ def test_constant_divisor_division_is_ieee(gpu, c):
         assert lsr._api.selftest_div_const(d, 1 << 26, seed=int(d * 1e9) + 1) == 0, d
 
 
+@pytest.mark.parametrize("dx", [2.0 / 511, 2.0 / 1023, 2.0 / 127, 2.0 / 255, 2.0 ** -7, 1.0, 2.0 ** -30])
+def test_weno_fast_forms_selftest(gpu, dx):
+    """weno1_fast and weno1_zt (the exact fast divisions the SL kernels use)
+    against weno_1d with the plain IEEE operators on the GPU, 2^26 samples per
+    dx: smooth lines, raw bit patterns, lines at the range guards (squared
+    second differences at 2^-700 and 2^200, differences at 2^-1021), tiny and
+    subnormal differences; theta uniform in [-0.7, 1.7] and at the guards
+    (-1/2, 0, -0, 3/2, +-2^-510, +-2^-511 and neighbours). Whenever a fast
+    form's guards pass, its bits must equal weno_1d's."""
+    lsr = gpu
+    c = lsr._api.selftest_weno(dx, 1 << 26, seed=int(1e6 * dx) + 7)
+    assert c["fast_mismatch"] == 0 and c["table_mismatch"] == 0, c
+    # the guards must not reject the common case: most samples take the fast path
+    assert c["fast_taken"] > (1 << 26) // 10 and c["table_taken"] > (1 << 26) // 10, c
+
+
 def test_context_multistep_swap_matches_oracle(gpu, oracle):
     """Device-resident loop: K ping-pong steps with changing active sets; the
     sparse resync must reproduce the reference's full copy (evolve.cpp:50)."""
