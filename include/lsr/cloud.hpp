@@ -1,4 +1,4 @@
-// Forwarding header: the reference include path `lsr/types.hpp` resolves to the
+// Forwarding header: the reference include path `lsr/cloud.hpp` resolves to the
 // B200 API, which declares everything the reference header declares
 // (see lsr_b200.hpp for the file:line map and which definitions the GPU
 // library provides).

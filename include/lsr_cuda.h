@@ -188,6 +188,14 @@ int lsr_cuda_build_distance(const lsr_grid* grid, const double* pts, int64_t n, 
 int lsr_cuda_ctx_build_distance(lsr_cuda_ctx* ctx, const double* pts, int64_t n, int dim, int seed_only,
                                 double* sentinel, int* rounds);
 
+/* lsr::fast_sweep (distance.cpp:72-142) of the context's DIST field in
+ * place, bit-identical: exact (num_nodes bytes, host; NULL = the flags of
+ * the last lsr_cuda_ctx_build_distance) marks the nodes never modified,
+ * values >= sentinel are unseeded. *rounds = fast_sweep's return value.
+ * lsr_cuda_download_exact copies the context's exact flags to the host. */
+int lsr_cuda_fast_sweep(lsr_cuda_ctx* ctx, const uint8_t* exact, double sentinel, int* rounds);
+int lsr_cuda_download_exact(lsr_cuda_ctx* ctx, uint8_t* exact);
+
 /* lsr::compute_stats (cloud.cpp:480-489; cloud.hpp:52-53): h_S =
  * estimate_resolution (mean exact nearest-neighbour distance over a seeded
  * Fisher-Yates sample of round(fraction*n) points, blocked_sum order),
@@ -231,6 +239,22 @@ typedef struct lsr_reinit_cfg {
 } lsr_reinit_cfg;
 int lsr_cuda_reinitialize(lsr_cuda_ctx* ctx, int which, double gamma, const lsr_reinit_cfg* cfg, int* iterations,
                           int* had_interface);
+/* A host BandMask (grid.hpp:79-84) as the context's band: state (num_nodes
+ * bytes), ascending ACTIVE and tube ids; the ACTIVE list also becomes the
+ * active set. (lsr_cuda_narrow_band builds the band on the device instead.) */
+int lsr_cuda_set_band(lsr_cuda_ctx* ctx, const uint8_t* state, const int64_t* active, int64_t n_active,
+                      const int64_t* tube, int64_t n_tube);
+/* lsr::interface_one_step (reinit.cpp:18-59) of field `which` in place;
+ * frozen (num_nodes bytes, may be NULL) receives the flags, which also stay
+ * on the device for lsr_cuda_reinit_iterate. A field without sign change or
+ * zero is left unchanged and LSR_ERR_NO_INTERFACE is returned (the
+ * reference's NoInterfaceError). */
+int lsr_cuda_interface_one_step(lsr_cuda_ctx* ctx, int which, uint8_t* frozen, int* had_interface);
+/* lsr::reinit_iterate (reinit.cpp:88-131) of field `which` in place on the
+ * context's band tube minus the frozen nodes (host flags, or NULL = those of
+ * the last lsr_cuda_interface_one_step); *iterations = its return value. */
+int lsr_cuda_reinit_iterate(lsr_cuda_ctx* ctx, int which, const uint8_t* frozen, const lsr_reinit_cfg* cfg,
+                            int* iterations);
 /* ReinitConfig::defaults(dx, gamma) (reinit.cpp:8-16) */
 void lsr_cuda_reinit_defaults(double dx, double gamma, lsr_reinit_cfg* cfg);
 

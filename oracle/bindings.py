@@ -72,6 +72,10 @@ def build(ref: bool = True) -> None:
     subprocess.run(["make", "-s", "-C", HERE, "liblsr_oracle.so"], check=True)
     if ref and os.path.isdir(REF_SRC):
         subprocess.run(["make", "-s", "-C", HERE, "ref", f"REF={REF_SRC}"], check=True)
+        # the reference's run_schedule built three ways; needs the product library
+        if os.path.exists(os.path.join(HERE, "..", "paper_2410_22205_b200", "liblsr_b200.so")):
+            subprocess.run(["make", "-s", "-C", HERE, "integration", f"REF={REF_SRC}"], check=True,
+                           stdout=subprocess.DEVNULL)
 
 
 class OracleError(RuntimeError):

@@ -54,6 +54,11 @@ int lsr_band_build(const lsr_dev::SlParams& P, const double* phi, double gamma, 
                    long long* n_tube, cudaStream_t s, std::string* err);
 int lsr_clamp(double* f, long long n, double gamma, cudaStream_t s, std::string* err,
               const unsigned char* state = nullptr, int* outside = nullptr);
+int lsr_reinit_one_step(const lsr_dev::SlParams& P, double** phi, double** scratch, ReinitBuffers& W,
+                        int* had_interface, cudaStream_t s, std::string* err);
+int lsr_reinit_iterate(const lsr_dev::SlParams& P, double** phi, double** scratch, const long long* tube,
+                       long long n_tube, const ReinitParams& R, ReinitBuffers& W, bool scratch_differs_on_frozen,
+                       int* iterations, cudaStream_t s, std::string* err);
 int lsr_reinitialize(const lsr_dev::SlParams& P, double** phi, double** scratch, const BandBuffers& B, double gamma,
                      const ReinitParams& R, ReinitBuffers& W, int* iterations, int* had_interface, cudaStream_t s,
                      std::string* err);

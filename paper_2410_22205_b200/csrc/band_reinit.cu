@@ -302,48 +302,7 @@ __device__ __forceinline__ void load4(const double* src, double* dst) {
     dst[3] = b.y;
 }
 
-__global__ void one_step4(SlParams P, const double* __restrict__ prev, double* __restrict__ out,
-                          unsigned* __restrict__ frozen4, long long n4, int* __restrict__ any_frozen,
-                          int* __restrict__ any_zero) {
-    const long long q = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-    bool zero = false, froz = false;
-    if (q < n4) {
-        const long long id = 4 * q;
-        int x0, j, k;
-        lsr_dev::unflatten(P, id, x0, j, k);  // 32-bit divisions when the grid allows
-        const bool hy[2] = {j > 0, j + 1 < P.ny}, hz[2] = {k > 0, k + 1 < P.nz};
-        double c[4], ym[4], yp[4], zm[4], zp[4];
-        load4(prev + id, c);
-        load4(prev + (hy[0] ? id - P.nx : id), ym);
-        load4(prev + (hy[1] ? id + P.nx : id), yp);
-        load4(prev + (hz[0] ? id - P.nxy : id), zm);
-        load4(prev + (hz[1] ? id + P.nxy : id), zp);
-        const double xl = x0 > 0 ? __ldg(prev + id - 1) : 0.0;
-        const double xr = x0 + 4 < P.nx ? __ldg(prev + id + 4) : 0.0;
-        double res[4];
-        unsigned fb = 0;
-#pragma unroll
-        for (int r = 0; r < 4; ++r) {
-            const double v[6] = {r > 0 ? c[r - 1] : xl, r < 3 ? c[r + 1] : xr, ym[r], yp[r], zm[r], zp[r]};
-            const bool has[6] = {x0 + r > 0, x0 + r + 1 < P.nx, hy[0], hy[1], hz[0], hz[1]};
-            bool z = false, f = false;
-            one_node(P, c[r], v, has, res[r], z, f);
-            zero |= z;
-            froz |= f;
-            fb |= (f ? 1u : 0u) << (8 * r);
-        }
-        reinterpret_cast<double2*>(out + id)[0] = make_double2(res[0], res[1]);
-        reinterpret_cast<double2*>(out + id)[1] = make_double2(res[2], res[3]);
-        frozen4[q] = fb;
-    }
-    const unsigned zb = __ballot_sync(0xffffffffu, zero), fbal = __ballot_sync(0xffffffffu, froz);
-    if ((threadIdx.x & 31) == 0) {
-        if (zb) *any_zero = 1;
-        if (fbal) *any_frozen = 1;
-    }
-}
-
-// one_step4 marching along z: a thread owns 4 nodes of a row (x0.., j) for
+// one_step marching along z: a thread owns 4 nodes of a row (x0.., j) for
 // kMarch consecutive planes and keeps the planes k-1, k, k+1 of its row in
 // registers, so each plane costs three row loads (z+1, y-1, y+1) instead of
 // five; same per-node arithmetic as one_step
@@ -758,11 +717,47 @@ void ReinitBuffers::release() {
 // reinitialize (reinit.cpp:133-145) of the field in *phi (device), on the
 // band B (tube list + state of the band field). *phi and *scratch are two
 // full-grid buffers; on return *phi holds the result (pointers may swap).
-int lsr_reinitialize(const SlParams& P, double** phi, double** scratch, const BandBuffers& B, double gamma,
-                     const ReinitParams& R, ReinitBuffers& W, int* iterations, int* had_interface, cudaStream_t s,
-                     std::string* err) {
+// interface_one_step (reinit.cpp:18-59): *phi -> *scratch on every node,
+// frozen flags in W.frozen. With an interface the buffers are swapped (*phi
+// = the one-step result, *scratch = the field before it) and *had = 1; a
+// field with no sign change and no zero is left as it was, *had = 0 (the
+// reference's NoInterfaceError).
+int lsr_reinit_one_step(const SlParams& P, double** phi, double** scratch, ReinitBuffers& W, int* had_interface,
+                        cudaStream_t s, std::string* err) {
+    const long long n = P.nxy * P.nz;
+    if (int st = W.reserve(n, err)) return st;
+    *had_interface = 0;
+    W.n_frozen = 0;
+    int* flags = reinterpret_cast<int*>(W.scal);  // [0] any_frozen, [1] any_zero
+    BR_TRY(cudaMemsetAsync(W.scal, 0, sizeof(unsigned long long) * 4, s));
+    if (P.dim == 3 && P.nx % 4 == 0) {
+        const long long threads = static_cast<long long>(P.nx / 4) * P.ny * ((P.nz + kMarch - 1) / kMarch);
+        one_step_march<<<static_cast<unsigned>((threads + 255) / 256), 256, 0, s>>>(
+            P, *phi, *scratch, reinterpret_cast<unsigned*>(W.frozen), flags, flags + 1);
+    } else {
+        one_step<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(P, *phi, *scratch, W.frozen, n, flags,
+                                                                         flags + 1);
+    }
+    lsr_note_launch();
+    int hf[2];
+    BR_TRY(cudaMemcpyAsync(hf, flags, sizeof hf, cudaMemcpyDeviceToHost, s));
+    BR_TRY(cudaStreamSynchronize(s));
+    if (!hf[0] && !hf[1]) return LSR_OK;
+    std::swap(*phi, *scratch);
+    *had_interface = 1;
+    return LSR_OK;
+}
+
+// reinit_iterate (reinit.cpp:88-131) on the tube minus the nodes flagged in
+// W.frozen. On entry *scratch must equal *phi except possibly on the frozen
+// nodes (scratch_differs_on_frozen: right after lsr_reinit_one_step), or
+// anywhere (otherwise: it is refreshed whole). On return *phi holds the
+// result and *scratch equals it on the iterated nodes.
+int lsr_reinit_iterate(const SlParams& P, double** phi, double** scratch, const long long* tube, long long n_tube,
+                       const ReinitParams& R, ReinitBuffers& W, bool scratch_differs_on_frozen, int* iterations,
+                       cudaStream_t s, std::string* err) {
     if (!(R.dtau > 0.0)) {
-        *err = "reinit: dtau must be positive";  // reinit.hpp:46-47
+        *err = "reinit: dtau must be positive";  // reinit.hpp:14-17
         return LSR_ERR_CONFIG;
     }
     if (R.max_iters < 1) {
@@ -772,50 +767,18 @@ int lsr_reinitialize(const SlParams& P, double** phi, double** scratch, const Ba
     const long long n = P.nxy * P.nz;
     if (int st = W.reserve(n, err)) return st;
     *iterations = 0;
-    *had_interface = 0;
-    W.n_frozen = 0;
-    BR_TRY(cudaMemsetAsync(W.clamp_outside, 0, sizeof(int), s));
-    int* flags = reinterpret_cast<int*>(W.scal);  // [0] any_frozen, [1] any_zero
-    BR_TRY(cudaMemsetAsync(W.scal, 0, sizeof(unsigned long long) * 4, s));
-    // interface_one_step: *phi -> *scratch (every node), frozen flags
-    static const bool march = !(std::getenv("LSR_ONE_STEP_MARCH") && std::atoi(std::getenv("LSR_ONE_STEP_MARCH")) == 0);
-    if (P.dim == 3 && P.nx % 4 == 0 && march) {
-        const long long threads = static_cast<long long>(P.nx / 4) * P.ny * ((P.nz + kMarch - 1) / kMarch);
-        one_step_march<<<static_cast<unsigned>((threads + 255) / 256), 256, 0, s>>>(
-            P, *phi, *scratch, reinterpret_cast<unsigned*>(W.frozen), flags, flags + 1);
-    } else if (P.dim == 3 && P.nx % 4 == 0) {
-        const long long n4 = n / 4;
-        one_step4<<<static_cast<unsigned>((n4 + 255) / 256), 256, 0, s>>>(
-            P, *phi, *scratch, reinterpret_cast<unsigned*>(W.frozen), n4, flags, flags + 1);
-    } else {
-        one_step<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(P, *phi, *scratch, W.frozen, n, flags,
-                                                                         flags + 1);
-    }
-    lsr_note_launch();
-    int hf[2];
-    BR_TRY(cudaMemcpyAsync(hf, flags, sizeof hf, cudaMemcpyDeviceToHost, s));
-    BR_TRY(cudaStreamSynchronize(s));
-    if (!hf[0] && !hf[1]) {
-        // NoInterfaceError caught by reinitialize (reinit.cpp:140-142): phi is
-        // left as it was (the one-step wrote nothing), then clamped
-        W.n_frozen = 0;
-        return lsr_clamp(*phi, n, gamma, s, err, B.state, W.clamp_outside);
-    }
-    std::swap(*phi, *scratch);  // *phi = one-step result
-    *had_interface = 1;
-    // nodes = tube minus frozen, ascending (reinit.cpp:94-98)
-    size_t tb = 0;
     long long* d_nn = reinterpret_cast<long long*>(W.scal + 2);
-    tb = lsr_compact::scratch_bytes(n > B.n_tube ? n : B.n_tube);
+    const size_t tb = lsr_compact::scratch_bytes(n > n_tube ? n : n_tube);
     if (tb > W.tmp_bytes) {
         cudaFree(W.tmp);
         W.tmp = nullptr;
         BR_TRY(cudaMalloc(&W.tmp, tb));
         W.tmp_bytes = tb;
     }
-    // `next = phi` (reinit.cpp:259): the scratch buffer holds the pre-one-step
-    // field, which differs from phi exactly on the frozen nodes -> copy those
-    {
+    // `ScalarField next = phi` (reinit.cpp:109): after the one-step the two
+    // buffers differ exactly on the frozen nodes -> copy those; otherwise copy
+    // the field
+    if (scratch_differs_on_frozen) {
         long long nf = 0;
         BR_TRY(lsr_compact::compact(lsr_compact::BytePred<NonZero>{W.frozen, {}}, lsr_compact::Identity{}, n,
                                     W.frozen_ids, d_nn, W.tmp, tb, s));
@@ -826,8 +789,11 @@ int lsr_reinitialize(const SlParams& P, double** phi, double** scratch, const Ba
             copy_ids<<<static_cast<unsigned>((nf + 255) / 256), 256, 0, s>>>(*phi, *scratch, W.frozen_ids, nf);
             lsr_note_launch();
         }
+    } else {
+        BR_TRY(cudaMemcpyAsync(*scratch, *phi, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
     }
-    BR_TRY(lsr_compact::compact(NotFrozen{W.frozen, B.tube}, TubeId{B.tube}, B.n_tube, W.nodes, d_nn, W.tmp, tb, s));
+    // nodes = tube minus frozen, ascending (reinit.cpp:94-98)
+    BR_TRY(lsr_compact::compact(NotFrozen{W.frozen, tube}, TubeId{tube}, n_tube, W.nodes, d_nn, W.tmp, tb, s));
     lsr_note_launch();
     lsr_note_launch();
     long long nn = 0;
@@ -841,7 +807,7 @@ int lsr_reinitialize(const SlParams& P, double** phi, double** scratch, const Ba
     }
     // All max_iters sweeps are queued without host round trips: sweep k reads
     // buf[k&1] and writes buf[(k+1)&1]; a one-thread check after each sweep
-    // applies the reference's stop rule (reinit.cpp:275-278) and raises a
+    // applies the reference's stop rule (reinit.cpp:125-128) and raises a
     // device flag that turns the remaining sweeps into no-ops. The number of
     // sweeps done tells which buffer holds the result.
     const double tol = R.residual_tol * P.dx;
@@ -875,5 +841,28 @@ int lsr_reinitialize(const SlParams& P, double** phi, double** scratch, const Ba
         lsr_note_launch();
     }
     *iterations = iter;
+    return LSR_OK;
+}
+
+int lsr_reinitialize(const SlParams& P, double** phi, double** scratch, const BandBuffers& B, double gamma,
+                     const ReinitParams& R, ReinitBuffers& W, int* iterations, int* had_interface, cudaStream_t s,
+                     std::string* err) {
+    if (!(R.dtau > 0.0)) {
+        *err = "reinit: dtau must be positive";  // reinit.hpp:14-17
+        return LSR_ERR_CONFIG;
+    }
+    if (R.max_iters < 1) {
+        *err = "reinit: max_iters must be >= 1";
+        return LSR_ERR_CONFIG;
+    }
+    const long long n = P.nxy * P.nz;
+    if (int st = W.reserve(n, err)) return st;
+    *iterations = 0;
+    BR_TRY(cudaMemsetAsync(W.clamp_outside, 0, sizeof(int), s));
+    if (int st = lsr_reinit_one_step(P, phi, scratch, W, had_interface, s, err)) return st;
+    // NoInterfaceError is caught by reinitialize (reinit.cpp:140-142): phi is
+    // left as it was, then clamped
+    if (*had_interface)
+        if (int st = lsr_reinit_iterate(P, phi, scratch, B.tube, B.n_tube, R, W, true, iterations, s, err)) return st;
     return lsr_clamp(*phi, n, gamma, s, err, B.state, W.clamp_outside);
 }

@@ -22,6 +22,8 @@
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
+#include <atomic>
+
 #include <cub/cub.cuh>
 
 #include <cstdlib>
@@ -430,7 +432,7 @@ __global__ void __launch_bounds__(kTile * kTile) sweep_tiles(const __grid_consta
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda
 // link dependency)
-static bool make_tile_maps(const GridP& G, double* d, unsigned char* exact, CUtensorMap* maps) {
+static bool make_tile_maps(const GridP& G, double* d, const unsigned char* exact, CUtensorMap* maps) {
     static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
         void* fn = nullptr;
         cudaDriverEntryPointQueryResult q{};
@@ -453,7 +455,7 @@ static bool make_tile_maps(const GridP& G, double* d, unsigned char* exact, CUte
                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
         return false;
-    if (encode(&maps[1], CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, exact, dims, sx_str, sx_box, estr,
+    if (encode(&maps[1], CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<unsigned char*>(exact), dims, sx_str, sx_box, estr,
                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
         return false;
@@ -488,6 +490,115 @@ __global__ void block_sums(const double* __restrict__ term, long long n, double*
 }  // namespace
 
 // ---------------------------------------------------------------------------
+
+// fast_sweep (distance.cpp:72-142) of the device field d_field with the
+// exact flags d_exact and the sentinel (values >= sentinel are unseeded):
+// Gauss-Seidel over the 2^dim orderings as tiled wavefronts, until the
+// largest change of a round is below 1e-3 dx or after 8 rounds.
+int lsr_prep_fast_sweep(const lsr_grid* g, double* d_field, const unsigned char* d_exact, double sentinel,
+                        int* rounds_out, cudaStream_t s, std::string* err) {
+    auto fail = [&](int code, const char* m) {
+        *err = m;
+        return code;
+    };
+#define PREP_TRY(x)                                         \
+    do {                                                    \
+        cudaError_t e_ = (x);                               \
+        if (e_ != cudaSuccess) {                            \
+            *err = std::string(#x) + ": " + cudaGetErrorString(e_); \
+            return LSR_ERR_CUDA;                            \
+        }                                                   \
+    } while (0)
+    GridP G{g->dim, g->dims[0], g->dims[1], g->dims[2], static_cast<long long>(g->dims[0]) * g->dims[1],
+            g->origin[0], g->origin[1], g->origin[2], g->dx};
+    const long long N = G.nxy * G.nz;
+    const int T = 256;
+    int* flag = nullptr;
+    unsigned long long* dmax = nullptr;
+    struct Guard {
+        int*& f;
+        unsigned long long*& m;
+        ~Guard() {
+            cudaFree(f);
+            cudaFree(m);
+        }
+    } guard{flag, dmax};
+    PREP_TRY(cudaMalloc(&flag, sizeof(int)));
+    PREP_TRY(cudaMalloc(&dmax, sizeof(unsigned long long)));
+    int h_flag = 0;
+    PREP_TRY(cudaMemsetAsync(flag, 0, sizeof(int), s));
+    any_below<<<148 * 4, 256, 0, s>>>(d_field, N, sentinel, flag);
+    lsr_note_launch();
+    PREP_TRY(cudaMemcpyAsync(&h_flag, flag, sizeof(int), cudaMemcpyDeviceToHost, s));
+    PREP_TRY(cudaStreamSynchronize(s));
+    if (!h_flag) return fail(LSR_ERR, "fast_sweep: no finite seed value");
+    const int orderings = g->dim == 3 ? 8 : 4;
+    const double tol = 1e-3 * g->dx;
+    const int max_rounds = 8;
+    static const bool tiled = !(std::getenv("LSR_SWEEP_TILES") && std::atoi(std::getenv("LSR_SWEEP_TILES")) == 0);
+    // TMA tensor maps of d (fp64) and the exact flags (u8) over the grid for
+    // the tiled sweep; global strides must be multiples of 16 bytes
+    CUtensorMap tmaps[2] = {};
+    bool use_tma = false;
+    if (G.dim == 3 && tiled) {
+        static const int tma_env = std::getenv("LSR_SWEEP_TMA") ? std::atoi(std::getenv("LSR_SWEEP_TMA")) : 1;
+        use_tma = tma_env != 0 && G.nx % 16 == 0 && make_tile_maps(G, d_field, d_exact, tmaps);
+        // the dynamic shared-memory limit is a per-device function attribute
+        static std::atomic<unsigned long long> attr_set{0};
+        int dev = 0;
+        PREP_TRY(cudaGetDevice(&dev));
+        if (dev >= 64 || !(attr_set.load() >> dev & 1ULL)) {
+            PREP_TRY(cudaFuncSetAttribute(sweep_tiles<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTileSmem));
+            PREP_TRY(cudaFuncSetAttribute(sweep_tiles<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTileSmem));
+            if (dev < 64) attr_set.fetch_or(1ULL << dev);
+        }
+    }
+    const int smax = (G.nx - 1) + (G.ny - 1) + (G.dim == 3 ? G.nz - 1 : 0);
+    int round = 0;
+    for (; round < max_rounds; ++round) {
+        PREP_TRY(cudaMemsetAsync(dmax, 0, sizeof(unsigned long long), s));
+        for (int ord = 0; ord < orderings; ++ord) {
+            if (G.dim == 3 && tiled) {
+                const int nti = (G.nx + kTile - 1) / kTile, ntj = (G.ny + kTile - 1) / kTile,
+                          ntk = (G.nz + kTile - 1) / kTile;
+                for (int S = 0; S <= (nti - 1) + (ntj - 1) + (ntk - 1); ++S) {
+                    const int tk_lo = std::max(0, S - (nti - 1) - (ntj - 1)), tk_hi = std::min(ntk - 1, S);
+                    const unsigned ctas = static_cast<unsigned>((tk_hi - tk_lo + 1) * ntj);
+                    if (use_tma)
+                        sweep_tiles<true><<<ctas, kTile * kTile, kTileSmem, s>>>(
+                            tmaps[0], tmaps[1], G, ord, S, nti, ntj, ntk, tk_lo, sentinel, d_exact, d_field, dmax);
+                    else
+                        sweep_tiles<false><<<ctas, kTile * kTile, kTileSmem, s>>>(
+                            tmaps[0], tmaps[1], G, ord, S, nti, ntj, ntk, tk_lo, sentinel, d_exact, d_field, dmax);
+                    lsr_note_launch();
+                }
+                continue;
+            }
+            for (int sp = 0; sp <= smax; ++sp) {
+                const int k_lo = G.dim == 3 ? std::max(0, sp - (G.nx - 1) - (G.ny - 1)) : 0;
+                const int k_hi = G.dim == 3 ? std::min(G.nz - 1, sp) : 0;
+                const int k_cnt = k_hi - k_lo + 1;
+                const long long threads = static_cast<long long>(k_cnt) * G.ny;
+                sweep_plane<<<static_cast<unsigned>((threads + T - 1) / T), T, 0, s>>>(G, ord, sp, k_lo, k_cnt,
+                                                                                      sentinel, d_exact, d_field, dmax);
+                lsr_note_launch();
+            }
+        }
+        PREP_TRY(cudaGetLastError());
+        unsigned long long h_max = 0;
+        PREP_TRY(cudaMemcpyAsync(&h_max, dmax, sizeof h_max, cudaMemcpyDeviceToHost, s));
+        PREP_TRY(cudaStreamSynchronize(s));
+        double max_change;
+        std::memcpy(&max_change, &h_max, sizeof max_change);
+        if (max_change < tol) {
+            ++round;
+            break;
+        }
+    }
+    *rounds_out = round;
+    return LSR_OK;
+#undef PREP_TRY
+}
 
 int lsr_prep_build_distance(const lsr_grid* g, const double* h_pts, int64_t n, int dim, int seed_only,
                             double* d_field, unsigned char* d_exact, double* sentinel_out, int* rounds_out,
@@ -548,19 +659,16 @@ int lsr_prep_build_distance(const lsr_grid* g, const double* h_pts, int64_t n, i
     const long long N = G.nxy * G.nz;
 
     double* pts = nullptr;
-    int *counts = nullptr, *starts = nullptr, *bin_id = nullptr, *entries = nullptr, *flag = nullptr;
+    int *counts = nullptr, *starts = nullptr, *bin_id = nullptr, *entries = nullptr;
     void* tmp = nullptr;
     size_t tmp_bytes = 0;
-    unsigned long long* dmax = nullptr;
     auto cleanup = [&] {
         cudaFree(pts);
         cudaFree(counts);
         cudaFree(starts);
         cudaFree(bin_id);
         cudaFree(entries);
-        cudaFree(flag);
         cudaFree(tmp);
-        cudaFree(dmax);
     };
     struct Guard {
         decltype(cleanup)& f;
@@ -571,8 +679,6 @@ int lsr_prep_build_distance(const lsr_grid* g, const double* h_pts, int64_t n, i
     PREP_TRY(cudaMalloc(&starts, sizeof(int) * (nbins + 1)));
     PREP_TRY(cudaMalloc(&bin_id, sizeof(int) * n));
     PREP_TRY(cudaMalloc(&entries, sizeof(int) * n));
-    PREP_TRY(cudaMalloc(&flag, sizeof(int)));
-    PREP_TRY(cudaMalloc(&dmax, sizeof(unsigned long long)));
     PREP_TRY(cudaMemcpyAsync(pts, h_pts, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, s));
     PREP_TRY(cudaMemsetAsync(counts, 0, sizeof(int) * (nbins + 1), s));
     const int T = 256;
@@ -599,76 +705,7 @@ int lsr_prep_build_distance(const lsr_grid* g, const double* h_pts, int64_t n, i
         return LSR_OK;
     }
 
-    // fast_sweep (distance.cpp:72-142)
-    int h_flag = 0;
-    PREP_TRY(cudaMemsetAsync(flag, 0, sizeof(int), s));
-    any_below<<<148 * 4, 256, 0, s>>>(d_field, N, sentinel, flag);
-    lsr_note_launch();
-    PREP_TRY(cudaMemcpyAsync(&h_flag, flag, sizeof(int), cudaMemcpyDeviceToHost, s));
-    PREP_TRY(cudaStreamSynchronize(s));
-    if (!h_flag) return fail(LSR_ERR, "fast_sweep: no finite seed value");
-    const int orderings = g->dim == 3 ? 8 : 4;
-    const double tol = 1e-3 * g->dx;
-    const int max_rounds = 8;
-    static const bool tiled = !(std::getenv("LSR_SWEEP_TILES") && std::atoi(std::getenv("LSR_SWEEP_TILES")) == 0);
-    // TMA tensor maps of d (fp64) and the exact flags (u8) over the grid for
-    // the tiled sweep; global strides must be multiples of 16 bytes
-    CUtensorMap tmaps[2] = {};
-    bool use_tma = false;
-    if (G.dim == 3 && tiled) {
-        static const int tma_env = std::getenv("LSR_SWEEP_TMA") ? std::atoi(std::getenv("LSR_SWEEP_TMA")) : 1;
-        use_tma = tma_env != 0 && G.nx % 16 == 0 && make_tile_maps(G, d_field, d_exact, tmaps);
-        static bool attr_set = false;
-        if (!attr_set) {
-            PREP_TRY(cudaFuncSetAttribute(sweep_tiles<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTileSmem));
-            PREP_TRY(cudaFuncSetAttribute(sweep_tiles<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTileSmem));
-            attr_set = true;
-        }
-    }
-    const int smax = (G.nx - 1) + (G.ny - 1) + (G.dim == 3 ? G.nz - 1 : 0);
-    int round = 0;
-    for (; round < max_rounds; ++round) {
-        PREP_TRY(cudaMemsetAsync(dmax, 0, sizeof(unsigned long long), s));
-        for (int ord = 0; ord < orderings; ++ord) {
-            if (G.dim == 3 && tiled) {
-                const int nti = (G.nx + kTile - 1) / kTile, ntj = (G.ny + kTile - 1) / kTile,
-                          ntk = (G.nz + kTile - 1) / kTile;
-                for (int S = 0; S <= (nti - 1) + (ntj - 1) + (ntk - 1); ++S) {
-                    const int tk_lo = std::max(0, S - (nti - 1) - (ntj - 1)), tk_hi = std::min(ntk - 1, S);
-                    const unsigned ctas = static_cast<unsigned>((tk_hi - tk_lo + 1) * ntj);
-                    if (use_tma)
-                        sweep_tiles<true><<<ctas, kTile * kTile, kTileSmem, s>>>(
-                            tmaps[0], tmaps[1], G, ord, S, nti, ntj, ntk, tk_lo, sentinel, d_exact, d_field, dmax);
-                    else
-                        sweep_tiles<false><<<ctas, kTile * kTile, kTileSmem, s>>>(
-                            tmaps[0], tmaps[1], G, ord, S, nti, ntj, ntk, tk_lo, sentinel, d_exact, d_field, dmax);
-                    lsr_note_launch();
-                }
-                continue;
-            }
-            for (int sp = 0; sp <= smax; ++sp) {
-                const int k_lo = G.dim == 3 ? std::max(0, sp - (G.nx - 1) - (G.ny - 1)) : 0;
-                const int k_hi = G.dim == 3 ? std::min(G.nz - 1, sp) : 0;
-                const int k_cnt = k_hi - k_lo + 1;
-                const long long threads = static_cast<long long>(k_cnt) * G.ny;
-                sweep_plane<<<static_cast<unsigned>((threads + T - 1) / T), T, 0, s>>>(G, ord, sp, k_lo, k_cnt,
-                                                                                      sentinel, d_exact, d_field, dmax);
-                lsr_note_launch();
-            }
-        }
-        PREP_TRY(cudaGetLastError());
-        unsigned long long h_max = 0;
-        PREP_TRY(cudaMemcpyAsync(&h_max, dmax, sizeof h_max, cudaMemcpyDeviceToHost, s));
-        PREP_TRY(cudaStreamSynchronize(s));
-        double max_change;
-        std::memcpy(&max_change, &h_max, sizeof max_change);
-        if (max_change < tol) {
-            ++round;
-            break;
-        }
-    }
-    *rounds_out = round;
-    return LSR_OK;
+    return lsr_prep_fast_sweep(g, d_field, d_exact, sentinel, rounds_out, s, err);
 #undef PREP_TRY
 }
 

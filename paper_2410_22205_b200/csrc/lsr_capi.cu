@@ -1320,6 +1320,105 @@ int lsr_cuda_reinitialize(lsr_cuda_ctx* c, int which, double gamma, const lsr_re
     return LSR_OK;
 }
 
+int lsr_cuda_set_band(lsr_cuda_ctx* c, const uint8_t* state, const int64_t* active, int64_t n_active,
+                      const int64_t* tube, int64_t n_tube) {
+    if (!c || !state || (n_active > 0 && !active) || (n_tube > 0 && !tube))
+        return set_err(LSR_ERR_CONFIG, "set_band: null argument");
+    if (n_active < 0 || n_tube < 0 || n_active > c->n || n_tube > c->n)
+        return set_err(LSR_ERR_CONFIG, "set_band: bad list sizes");
+    LSR_CUDA_TRY(cudaSetDevice(c->device));
+    std::string err;
+    if (int st = c->band.reserve(c->n, &err)) return set_err(st, err);
+    cudaStream_t s = c->stream;
+    LSR_CUDA_TRY(cudaMemcpyAsync(c->band.state, state, static_cast<size_t>(c->n), cudaMemcpyHostToDevice, s));
+    if (n_active > 0)
+        LSR_CUDA_TRY(cudaMemcpyAsync(c->band.active, active, sizeof(int64_t) * n_active, cudaMemcpyHostToDevice, s));
+    if (n_tube > 0)
+        LSR_CUDA_TRY(cudaMemcpyAsync(c->band.tube, tube, sizeof(int64_t) * n_tube, cudaMemcpyHostToDevice, s));
+    c->band.n_active = n_active;
+    c->band.n_tube = n_tube;
+    // the band's ACTIVE list becomes the context's active set (as narrow_band)
+    if (int st = ensure_ids(&c->active, &c->cap_active, n_active)) return st;
+    if (n_active > 0)
+        LSR_CUDA_TRY(cudaMemcpyAsync(c->active, active, sizeof(int64_t) * n_active, cudaMemcpyHostToDevice, s));
+    c->n_active = n_active;
+    c->zt_bricks = false;
+    c->dirty_is_active = false;
+    LSR_CUDA_TRY(cudaStreamSynchronize(s));
+    return LSR_OK;
+}
+
+int lsr_cuda_interface_one_step(lsr_cuda_ctx* c, int which, uint8_t* frozen, int* had_interface) {
+    if (!c) return set_err(LSR_ERR_CONFIG, "null context");
+    double** slot = field_slot(c, which);
+    if (!slot || which == LSR_FIELD_DIST) return set_err(LSR_ERR_CONFIG, "interface_one_step: phi must be PHI or OUT");
+    LSR_CUDA_TRY(cudaSetDevice(c->device));
+    if (!c->scratch) LSR_CUDA_TRY(cudaMalloc(&c->scratch, sizeof(double) * c->n));
+    std::string err;
+    int had = 0;
+    if (int st = lsr_reinit_one_step(grid_params(c->grid), slot, &c->scratch, c->rb, &had, c->stream, &err))
+        return set_err(st, err);
+    if (had_interface) *had_interface = had;
+    if (frozen) {
+        LSR_CUDA_TRY(cudaMemcpyAsync(frozen, c->rb.frozen, static_cast<size_t>(c->n), cudaMemcpyDeviceToHost, c->stream));
+        LSR_CUDA_TRY(cudaStreamSynchronize(c->stream));
+    }
+    c->consistent = false;
+    if (!had) return set_err(LSR_ERR_NO_INTERFACE, "interface_one_step: phi has no sign change");  // reinit.cpp:56
+    return LSR_OK;
+}
+
+int lsr_cuda_reinit_iterate(lsr_cuda_ctx* c, int which, const uint8_t* frozen, const lsr_reinit_cfg* rc,
+                            int* iterations) {
+    if (!c || !rc) return set_err(LSR_ERR_CONFIG, "reinit_iterate: null argument");
+    double** slot = field_slot(c, which);
+    if (!slot || which == LSR_FIELD_DIST) return set_err(LSR_ERR_CONFIG, "reinit_iterate: phi must be PHI or OUT");
+    if (!c->band.state) return set_err(LSR_ERR_CONFIG, "reinit_iterate: no band (lsr_cuda_narrow_band / set_band)");
+    LSR_CUDA_TRY(cudaSetDevice(c->device));
+    if (!c->scratch) LSR_CUDA_TRY(cudaMalloc(&c->scratch, sizeof(double) * c->n));
+    std::string err;
+    if (int st = c->rb.reserve(c->n, &err)) return set_err(st, err);
+    if (frozen)
+        LSR_CUDA_TRY(cudaMemcpyAsync(c->rb.frozen, frozen, static_cast<size_t>(c->n), cudaMemcpyHostToDevice, c->stream));
+    const ReinitParams R{rc->dtau, rc->max_iters, rc->residual_tol, rc->sign_eps};
+    int it = 0;
+    if (int st = lsr_reinit_iterate(grid_params(c->grid), slot, &c->scratch, c->band.tube, c->band.n_tube, R, c->rb,
+                                    false, &it, c->stream, &err))
+        return set_err(st, err);
+    LSR_CUDA_TRY(cudaStreamSynchronize(c->stream));
+    c->consistent = false;
+    if (iterations) *iterations = it;
+    return LSR_OK;
+}
+
+int lsr_cuda_fast_sweep(lsr_cuda_ctx* c, const uint8_t* exact, double sentinel, int* rounds) {
+    if (!c) return set_err(LSR_ERR_CONFIG, "null context");
+    LSR_CUDA_TRY(cudaSetDevice(c->device));
+    if (!c->exact) {
+        if (!exact) return set_err(LSR_ERR_CONFIG, "fast_sweep: no exact flags");
+        LSR_CUDA_TRY(cudaMalloc(&c->exact, static_cast<size_t>(c->n)));
+    }
+    if (exact)
+        LSR_CUDA_TRY(cudaMemcpyAsync(c->exact, exact, static_cast<size_t>(c->n), cudaMemcpyHostToDevice, c->stream));
+    std::string err;
+    int r = 0;
+    if (int st = lsr_prep_fast_sweep(&c->grid, c->dist, c->exact, sentinel, &r, c->stream, &err))
+        return set_err(st, err);
+    LSR_CUDA_TRY(cudaStreamSynchronize(c->stream));
+    c->zt_bricks = false;  // the covered bricks depend on d
+    if (rounds) *rounds = r;
+    return LSR_OK;
+}
+
+int lsr_cuda_download_exact(lsr_cuda_ctx* c, uint8_t* exact) {
+    if (!c || !exact) return set_err(LSR_ERR_CONFIG, "download_exact: null argument");
+    if (!c->exact) return set_err(LSR_ERR_CONFIG, "download_exact: no distance field built");
+    LSR_CUDA_TRY(cudaSetDevice(c->device));
+    LSR_CUDA_TRY(cudaMemcpyAsync(exact, c->exact, static_cast<size_t>(c->n), cudaMemcpyDeviceToHost, c->stream));
+    LSR_CUDA_TRY(cudaStreamSynchronize(c->stream));
+    return LSR_OK;
+}
+
 void lsr_cuda_reinit_defaults(double dx, double gamma, lsr_reinit_cfg* rc) {  // ReinitConfig::defaults (reinit.cpp:8-16)
     rc->dtau = 0.5 * dx;
     rc->max_iters = 4 * static_cast<int>(std::ceil(gamma / dx));

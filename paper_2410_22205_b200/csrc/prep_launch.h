@@ -17,6 +17,10 @@ int lsr_prep_build_distance(const lsr_grid* g, const double* h_pts, int64_t n, i
                             double* d_field, unsigned char* d_exact, double* sentinel_out, int* rounds_out,
                             cudaStream_t s, std::string* err);
 
+// lsr::fast_sweep (distance.cpp:72-142) of a device field in place.
+int lsr_prep_fast_sweep(const lsr_grid* g, double* d_field, const unsigned char* d_exact, double sentinel,
+                        int* rounds_out, cudaStream_t s, std::string* err);
+
 // lsr::surface_energy on device fields (energy.cu); synchronous.
 int lsr_prep_surface_energy(const lsr_dev::SlParams& P, const double* phi, const double* dist, int p, int refine,
                             double* energy, int64_t* n_cells, cudaStream_t s, std::string* err);

@@ -287,57 +287,61 @@ __device__ __forceinline__ double nudge(double x, int ulps) {  // x moved by `ul
     return __longlong_as_double(__double_as_longlong(x) + ulps);
 }
 
+// sample i of the self-test stream: a stencil v[4] and an abscissa t
+__device__ __forceinline__ void weno_sample(unsigned long long seed, long long i, double* v, double& t) {
+    unsigned long long z = seed + 0x9E3779B97F4A7C15ULL * static_cast<unsigned long long>(i + 1);
+    auto next = [&z]() {
+        z += 0x9E3779B97F4A7C15ULL;
+        return mix64(z);
+    };
+    const int cls = static_cast<int>(i & 3);
+    if (cls == 0) {  // smooth: quadratic + small noise, random scale
+        const double sc = ldexp(1.0, static_cast<int>(next() % 81) - 60);
+        const double a0 = unit01(next()) - 0.5, a1 = unit01(next()) - 0.5, a2 = (unit01(next()) - 0.5) * 0.1;
+        for (int q = 0; q < 4; ++q)
+            v[q] = sc * (a0 + a1 * (q - 1) + a2 * (q - 1) * (q - 1) + 1e-6 * (unit01(next()) - 0.5));
+    } else if (cls == 1) {  // raw bit patterns
+        for (int q = 0; q < 4; ++q) v[q] = __longlong_as_double(static_cast<long long>(next()));
+    } else if (cls == 2) {  // at the guards
+        const unsigned long long r = next();
+        const int ulps = static_cast<int>(r % 9) - 4;
+        const int which = static_cast<int>((r >> 8) % 6);
+        const double s = (r >> 16) & 1 ? -1.0 : 1.0;
+        for (int q = 0; q < 4; ++q) v[q] = 0.0;
+        // sd^2 = 2^-700 <=> |sd| = 2^-350; sd^2 = 2^200 <=> |sd| = 2^100; d/2 exact down to 2^-1021
+        const double mag = which == 0 ? 0x1.0p-350 : which == 1 ? 0x1.0p100 : which == 2 ? 0x1.0p-1021 : which == 3
+            ? 0x1.6a09e667f3bcdp-351 /* sqrt(2^-701) */ : which == 4 ? 0x1.6a09e667f3bcdp+99 : 0x1.0p-1022;
+        const int slot = static_cast<int>((r >> 20) & 3);
+        v[slot] = s * nudge(mag, ulps);
+        if ((r >> 24) & 1) v[(slot + 1) & 3] = 0.5 * v[slot];
+    } else {  // tiny / subnormal / zero differences around a base value
+        const double base = unit01(next()) - 0.5;
+        for (int q = 0; q < 4; ++q) {
+            const unsigned long long r = next();
+            v[q] = (r & 3) == 0 ? base : (r & 3) == 1 ? 0.0 : (r & 3) == 2 ? nudge(base, static_cast<int>(r % 5) - 2)
+                                                                           : __longlong_as_double(static_cast<long long>(r >> 12));
+        }
+    }
+    {
+        const unsigned long long r = next();
+        if ((r & 3) != 0) {
+            t = -0.7 + 2.4 * unit01(next());
+        } else {
+            const double special[8] = {-0.5, 0.0, -0.0, 1.5, 0x1.0p-510, -0x1.0p-510, 0x1.0p-511, -0x1.0p-511};
+            t = special[(r >> 2) & 7];
+            if ((r >> 5) & 1) t = nudge(t, ((r >> 6) & 1) ? 1 : -1);
+            if (t == 0.0 && ((r >> 7) & 1)) t = __longlong_as_double(static_cast<long long>((r >> 8) & 0xfffff));
+        }
+    }
+}
+
 __global__ void weno_selftest_kernel(SlParams P, unsigned long long seed, long long n,
                                      unsigned long long* __restrict__ counts) {
     unsigned long long c[4] = {0, 0, 0, 0};
     const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
     for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
-        unsigned long long z = seed + 0x9E3779B97F4A7C15ULL * static_cast<unsigned long long>(i + 1);
-        auto next = [&z]() {
-            z += 0x9E3779B97F4A7C15ULL;
-            return mix64(z);
-        };
-        double v[4];
-        const int cls = static_cast<int>(i & 3);
-        if (cls == 0) {  // smooth: quadratic + small noise, random scale
-            const double sc = ldexp(1.0, static_cast<int>(next() % 81) - 60);
-            const double a0 = unit01(next()) - 0.5, a1 = unit01(next()) - 0.5, a2 = (unit01(next()) - 0.5) * 0.1;
-            for (int q = 0; q < 4; ++q)
-                v[q] = sc * (a0 + a1 * (q - 1) + a2 * (q - 1) * (q - 1) + 1e-6 * (unit01(next()) - 0.5));
-        } else if (cls == 1) {  // raw bit patterns
-            for (int q = 0; q < 4; ++q) v[q] = __longlong_as_double(static_cast<long long>(next()));
-        } else if (cls == 2) {  // at the guards
-            const unsigned long long r = next();
-            const int ulps = static_cast<int>(r % 9) - 4;
-            const int which = static_cast<int>((r >> 8) % 6);
-            const double s = (r >> 16) & 1 ? -1.0 : 1.0;
-            for (int q = 0; q < 4; ++q) v[q] = 0.0;
-            // sd^2 = 2^-700 <=> |sd| = 2^-350; sd^2 = 2^200 <=> |sd| = 2^100; d/2 exact down to 2^-1021
-            const double mag = which == 0 ? 0x1.0p-350 : which == 1 ? 0x1.0p100 : which == 2 ? 0x1.0p-1021 : which == 3
-                ? 0x1.6a09e667f3bcdp-351 /* sqrt(2^-701) */ : which == 4 ? 0x1.6a09e667f3bcdp+99 : 0x1.0p-1022;
-            const int slot = static_cast<int>((r >> 20) & 3);
-            v[slot] = s * nudge(mag, ulps);
-            if ((r >> 24) & 1) v[(slot + 1) & 3] = 0.5 * v[slot];
-        } else {  // tiny / subnormal / zero differences around a base value
-            const double base = unit01(next()) - 0.5;
-            for (int q = 0; q < 4; ++q) {
-                const unsigned long long r = next();
-                v[q] = (r & 3) == 0 ? base : (r & 3) == 1 ? 0.0 : (r & 3) == 2 ? nudge(base, static_cast<int>(r % 5) - 2)
-                                                                               : __longlong_as_double(static_cast<long long>(r >> 12));
-            }
-        }
-        double t;
-        {
-            const unsigned long long r = next();
-            if ((r & 3) != 0) {
-                t = -0.7 + 2.4 * unit01(next());
-            } else {
-                const double special[8] = {-0.5, 0.0, -0.0, 1.5, 0x1.0p-510, -0x1.0p-510, 0x1.0p-511, -0x1.0p-511};
-                t = special[(r >> 2) & 7];
-                if ((r >> 5) & 1) t = nudge(t, ((r >> 6) & 1) ? 1 : -1);
-                if (t == 0.0 && ((r >> 7) & 1)) t = __longlong_as_double(static_cast<long long>((r >> 8) & 0xfffff));
-            }
-        }
+        double v[4], t;
+        weno_sample(seed, i, v, t);
         const AxisW w = axis_weights(P, t);
         const double ref = weno1(P, w, v[0], v[1], v[2], v[3]);
         bool ok = theta_in_range(t);
