@@ -456,6 +456,11 @@ def sl_step(phi: ScalarField, dist: DistanceField, mask: BandMask, cfg: StepConf
     if not (out.grid == g) or out.values.size != g.num_nodes():
         out.grid = g
         out.values = np.zeros(g.num_nodes(), dtype=np.float64)
+    n = g.num_nodes()
+    if phi.values.size != n or dist.field.values.size != n:  # native code reads num_nodes() values of each
+        raise ConfigError("sl_step: phi and dist must hold grid.num_nodes() values")
+    if out.values.dtype != np.float64 or not out.values.flags.c_contiguous:
+        out.values = np.ascontiguousarray(out.values, dtype=np.float64)
     active = np.ascontiguousarray(mask.active, dtype=np.int64)
     bad = C.c_int64(-1)
     st = lib().lsr_cuda_sl_step_host(C.byref(g.c()), phi.values, np.ascontiguousarray(dist.field.values), _ids_ptr(active),

@@ -186,6 +186,7 @@ __global__ void contrib_3d(SlParams P, const double* __restrict__ phi, const dou
 // itself (else its own corners are loaded). Every interpolant is the same
 // expression as interp_q1's, so the result is bit-identical.
 constexpr int kMaxRefine = 8;
+constexpr int kEnergyMaxDevices = 64;
 
 __device__ __forceinline__ double q1_corners(double w00, double w10, double w01, double w11, double uz, double tz,
                                              const double* f) {
@@ -386,9 +387,10 @@ int lsr_prep_surface_energy(const SlParams& P, const double* phi, const double* 
         *err = "surface_energy: grids of 2^31 cells or more are not supported";
         return LSR_ERR_CONFIG;
     }
-    // process-wide workspace, grown on demand (no per-call cudaMalloc)
+    // workspace per device, grown on demand (no per-call cudaMalloc); one
+    // process may drive several devices (one context each)
     static std::mutex mu;
-    static struct Work {
+    struct Work {
         unsigned char* flags = nullptr;
         int* cells = nullptr;
         int* scal = nullptr;  // [0] selected count, [1] out-of-domain flag
@@ -398,7 +400,15 @@ int lsr_prep_surface_energy(const SlParams& P, const double* phi, const double* 
         double* contrib = nullptr;
         double* partial = nullptr;
         long long ccap = 0;
-    } W;
+    };
+    static Work works[kEnergyMaxDevices];
+    int dev = 0;
+    EN_TRY(cudaGetDevice(&dev));
+    if (dev < 0 || dev >= kEnergyMaxDevices) {
+        *err = "surface_energy: device ordinal out of range";
+        return LSR_ERR_CONFIG;
+    }
+    Work& W = works[dev];
     std::lock_guard<std::mutex> lock(mu);
     if (ncells > W.cap) {
         cudaFree(W.flags);

@@ -222,6 +222,29 @@ int ensure_ids(int64_t** buf, int64_t* cap, int64_t n) {
     return LSR_OK;
 }
 
+// every id a node of the grid (0 <= id < n)? Active ids are dereferenced
+// by the kernels and by the host scatter, so they are checked before any of
+// that (the reference's BandMask holds node ids by construction,
+// grid.hpp:79-84). Large lists are scanned by several threads.
+bool ids_in_grid(const int64_t* ids, int64_t n, int64_t n_nodes) {
+    const auto scan = [=](int64_t t0, int64_t t1) {
+        bool ok = true;
+        for (int64_t t = t0; t < t1; ++t) ok &= static_cast<uint64_t>(ids[t]) < static_cast<uint64_t>(n_nodes);
+        return ok;
+    };
+    const int64_t kSerial = 1 << 20;
+    if (n <= kSerial) return scan(0, n);
+    const int nt = static_cast<int>(std::min<int64_t>(8, n / kSerial + 1));
+    std::vector<std::thread> th;
+    std::vector<char> ok(nt, 1);
+    for (int q = 0; q < nt; ++q)
+        th.emplace_back([&, q] { ok[q] = scan(n * q / nt, n * (q + 1) / nt); });
+    for (auto& t : th) t.join();
+    for (char v : ok)
+        if (!v) return false;
+    return true;
+}
+
 double** field_slot(lsr_cuda_ctx* c, int which) {
     switch (which) {
         case LSR_FIELD_PHI: return &c->phi;
@@ -368,6 +391,7 @@ int lsr_cuda_mark_dirty(lsr_cuda_ctx* c, int which) {
 
 int lsr_cuda_set_active(lsr_cuda_ctx* c, const int64_t* ids, int64_t n) {
     if (!c || (n > 0 && !ids) || n < 0) return set_err(LSR_ERR_CONFIG, "set_active: bad argument");
+    if (!ids_in_grid(ids, n, c->n)) return set_err(LSR_ERR_CONFIG, "set_active: ids must be node ids of the grid");
     LSR_CUDA_TRY(cudaSetDevice(c->device));
     if (int st = ensure_ids(&c->active, &c->cap_active, n)) return st;
     if (n > 0)
@@ -383,8 +407,19 @@ int lsr_cuda_set_active_device(lsr_cuda_ctx* c, const int64_t* d_ids, int64_t n)
     if (!c || (n > 0 && !d_ids) || n < 0) return set_err(LSR_ERR_CONFIG, "set_active_device: bad argument");
     LSR_CUDA_TRY(cudaSetDevice(c->device));
     if (int st = ensure_ids(&c->active, &c->cap_active, n)) return st;
-    if (n > 0)
+    if (n > 0) {
         LSR_CUDA_TRY(cudaMemcpyAsync(c->active, d_ids, sizeof(int64_t) * n, cudaMemcpyDeviceToDevice, c->stream));
+        // the range check before any kernel dereferences them
+        LSR_CUDA_TRY(cudaMemsetAsync(c->d_bad, 0, sizeof(unsigned long long), c->stream));
+        LSR_CUDA_TRY(launch_check_ids(c->active, n, c->n, c->d_bad, c->stream));
+        LSR_CUDA_TRY(cudaMemcpyAsync(c->h_bad, c->d_bad, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                                     c->stream));
+        LSR_CUDA_TRY(cudaStreamSynchronize(c->stream));
+        if (*c->h_bad != 0) {
+            c->n_active = 0;
+            return set_err(LSR_ERR_CONFIG, "set_active_device: ids must be node ids of the grid");
+        }
+    }
     c->n_active = n;
     c->zt_bricks = false;
     c->dirty_is_active = false;
@@ -640,6 +675,8 @@ int lsr_cuda_sl_step_device(const lsr_grid* grid, int32_t z_base, int32_t z_plan
     SlParams P = make_params(*grid, *cfg, energy_p);
     P.z_base = z_base;
     P.z_planes = z_planes;
+    P.own_lo = z_base;  // ids outside the resident planes are counted, never read or written
+    P.own_hi = z_base + z_planes;
     P.halo_miss = slab ? reinterpret_cast<unsigned long long*>(d_halo_miss) : nullptr;
     // the resident planes start at global plane z_base: shift the bases so
     // that global ids index them directly
@@ -1135,6 +1172,10 @@ int lsr_cuda_sl_step_host(const lsr_grid* grid, const double* phi, const double*
     if (int st = check_cfg(cfg, energy_p)) return st;
     if (!phi || !dist || !out || (n_active > 0 && !active)) return set_err(LSR_ERR_CONFIG, "sl_step: null argument");
     if (out == phi) return set_err(LSR_ERR_CONFIG, "sl_step: out must not alias phi");
+    {
+        const int64_t nodes = static_cast<int64_t>(grid->dims[0]) * grid->dims[1] * grid->dims[2];
+        if (!ids_in_grid(active, n_active, nodes)) return set_err(LSR_ERR_CONFIG, "sl_step: ids must be node ids of the grid");
+    }
     struct Cache {
         lsr_cuda_ctx* ctx = nullptr;
         ~Cache() { lsr_cuda_destroy(ctx); }

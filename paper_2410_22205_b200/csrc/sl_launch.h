@@ -16,16 +16,18 @@
 #ifndef LSR_SL_MIN_BLOCKS
 #define LSR_SL_MIN_BLOCKS 4
 #endif
-#ifndef LSR_SL_THREADS_ZT
-#define LSR_SL_THREADS_ZT 192
+// 3d WENO (sl_step_w3_kernel, z-line table or per-line): 6 CTAs of 192
+// threads at 56 registers (36 warps/SM; 7 x 192, 10 x 128, 5 x 256, 8 x 128,
+// 12 x 96 measured 3-33 % slower at 512^3)
+#ifndef LSR_SL_THREADS_W3
+#define LSR_SL_THREADS_W3 192
 #endif
-#ifndef LSR_SL_MIN_BLOCKS_ZT
-#define LSR_SL_MIN_BLOCKS_ZT 6
+#ifndef LSR_SL_MIN_BLOCKS_W3
+#define LSR_SL_MIN_BLOCKS_W3 6
 #endif
 constexpr int kSlThreads = LSR_SL_THREADS;
-// the z-line-table kernel: 6 x 192 threads (36 warps) at 56 registers
-constexpr int kSlThreadsZt = LSR_SL_THREADS_ZT;
-constexpr int kSlMinBlocksZt = LSR_SL_MIN_BLOCKS_ZT;
+constexpr int kSlThreadsW3 = LSR_SL_THREADS_W3;
+constexpr int kSlMinBlocksW3 = LSR_SL_MIN_BLOCKS_W3;
 constexpr int kSlMinBlocks = LSR_SL_MIN_BLOCKS;  // resident CTAs per SM the register budget must allow
 
 // bumps the process-wide launch counter (lsr_cuda_kernel_launches)
@@ -60,6 +62,8 @@ cudaError_t launch_zt_bricks(const lsr_dev::SlParams& P, const double* dist, con
 cudaError_t launch_zt_fill(const lsr_dev::SlParams& P, const double* phi, const ZtBuffers& Z, cudaStream_t stream);
 
 cudaError_t launch_check_sorted(const int64_t* ids, long long n, unsigned long long* bad, cudaStream_t stream);
+cudaError_t launch_check_ids(const int64_t* ids, long long n, long long n_nodes, unsigned long long* bad,
+                             cudaStream_t stream);
 
 cudaError_t launch_resync(const double* phi, double* out, const int64_t* ids, long long n, cudaStream_t stream);
 

@@ -20,16 +20,7 @@ namespace lsr_dev {
 
 // ZT: 3d WENO launches that read the z-line table; their per-line chains are
 // shorter, so they trade registers for a 9th resident CTA per SM
-template <int DIM, int KIND, bool ZT = false>
-__global__ void __launch_bounds__(ZT ? kSlThreadsZt : kSlThreads, ZT ? kSlMinBlocksZt : kSlMinBlocks) sl_step_kernel(SlParams P, const double* __restrict__ phi,
-                                                             const double* __restrict__ dist,
-                                                             const int64_t* __restrict__ active,
-                                                             long long n_active, double* __restrict__ out,
-                                                             unsigned long long* __restrict__ bad) {
-    const long long a = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (a >= n_active) return;
-    const long long id = __ldg(active + a);
-    int i, j, k;
+__device__ __forceinline__ void node_ijk(const SlParams& P, long long id, int& i, int& j, int& k) {
     if (P.nxy * P.nz < (1LL << 31)) {  // Grid::unflatten (grid.hpp:22-27) in 32 bits when it fits
         const unsigned u = static_cast<unsigned>(id);
         const unsigned row = u / static_cast<unsigned>(P.nx);
@@ -41,18 +32,17 @@ __global__ void __launch_bounds__(ZT ? kSlThreadsZt : kSlThreads, ZT ? kSlMinBlo
         j = static_cast<int>((id / P.nx) % P.ny);
         k = static_cast<int>(id / P.nxy);
     }
-    const bool use_zt = ZT && __ldg(P.ztab_bad) == 0u;
-    double* sb = nullptr;
-    if (LSR_SMEM_FEET && DIM == 3 && KIND == 1 && !ZT) {  // per-thread stencil columns (kSlThreads-thread CTAs)
-        __shared__ double sbuf[2 * 16 * kSlThreads];
-        sb = sbuf + threadIdx.x;
-    }
-    const double next = sl_node<DIM, KIND, kSlThreads>(P, phi, dist, id, i, j, k, sb, use_zt);
+}
+
+// the write of one update (evolve.cpp:107-117): out, the smallest
+// non-finite id, and the fused halo exchange — the neighbours read these
+// planes next step, so the update goes straight into their resident buffers
+// over NVLink (peer mapped) instead of a separate plane exchange after the
+// kernel
+__device__ __forceinline__ void store_update(const SlParams& P, long long id, int k, double next, double* out,
+                                             unsigned long long* bad) {
     if (!isfinite(next)) atomicMin(bad, static_cast<unsigned long long>(id));
     out[id] = next;
-    // fused halo exchange: the neighbours read these planes next step, so the
-    // update goes straight into their resident buffers over NVLink (peer
-    // mapped) instead of a separate plane exchange after the kernel
     bool pushed = false;
     if (P.peer_lo != nullptr && k < P.push_lo_below) {
         P.peer_lo[id] = next;
@@ -63,6 +53,46 @@ __global__ void __launch_bounds__(ZT ? kSlThreadsZt : kSlThreads, ZT ? kSlMinBlo
         pushed = true;
     }
     if (pushed) __threadfence_system();
+}
+
+// one thread per active node (Q1, 2d)
+template <int DIM, int KIND>
+__global__ void __launch_bounds__(kSlThreads, kSlMinBlocks) sl_step_kernel(SlParams P, const double* __restrict__ phi,
+                                                                           const double* __restrict__ dist,
+                                                                           const int64_t* __restrict__ active,
+                                                                           long long n_active, double* __restrict__ out,
+                                                                           unsigned long long* __restrict__ bad) {
+    const long long a = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (a >= n_active) return;
+    const long long id = __ldg(active + a);
+    int i, j, k;
+    node_ijk(P, id, i, j, k);
+    if (slab_node_miss(P, k)) {  // nothing of a non-resident node is read or written
+        atomicAdd(P.halo_miss, 1ULL);
+        return;
+    }
+    store_update(P, id, k, sl_node<DIM, KIND>(P, phi, dist, id, i, j, k), out, bad);
+}
+
+// 3d WENO with the z-line table, one thread per active node (its own launch
+// shape; the per-line kernel above runs Q1, 2d and table-less WENO). (Splitting a node's four feet over 2 or 4 lanes, each lane
+// recomputing the node's gradients and basis, measured slower: 3.77 / 4.22
+// ms against 2.93 ms at 512^3 — the feet of a warp's nodes then touch 2-4x
+// as many L1 lines per table load, and L1 wavefronts are the busiest unit.)
+__global__ void __launch_bounds__(kSlThreadsW3, kSlMinBlocksW3) sl_step_zt_kernel(
+    SlParams P, const double* __restrict__ phi, const double* __restrict__ dist, const int64_t* __restrict__ active,
+    long long n_active, double* __restrict__ out, unsigned long long* __restrict__ bad) {
+    const long long a = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (a >= n_active) return;
+    const long long id = __ldg(active + a);
+    int i, j, k;
+    node_ijk(P, id, i, j, k);
+    if (slab_node_miss(P, k)) {
+        atomicAdd(P.halo_miss, 1ULL);
+        return;
+    }
+    const bool use_zt = __ldg(P.ztab_bad) == 0u;
+    store_update(P, id, k, sl_node<3, 1>(P, phi, dist, id, i, j, k, use_zt), out, bad);
 }
 
 // The z-line table of the 3d WENO fast path. For node n = (i, j, k),
@@ -101,10 +131,13 @@ __global__ void zt_reach_kernel(SlParams P, const double* __restrict__ dist, con
     const long long a = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
     long long b = -1;
     unsigned r = 0;
+    long long id = 0;
+    int i = 0, j = 0, k = 0;
     if (a < n) {
-        const long long id = __ldg(active + a);
-        int i, j, k;
+        id = __ldg(active + a);
         unflatten(P, id, i, j, k);
+    }
+    if (a < n && !slab_node_miss(P, k)) {  // (a non-resident node is counted by the SL kernel)
         b = brick_of(i, j, k, nbx, nby);
         const double d_j = __ldg(dist + id);
         const double c_j = P.p == 1 ? 1.0 : d_j / P.energy;  // scale_factor (evolve.cpp:32-38)
@@ -227,6 +260,15 @@ __global__ void resync_kernel(const double* __restrict__ phi, double* __restrict
     if (a >= n) return;
     const long long id = __ldg(ids + a);
     out[id] = __ldg(phi + id);
+}
+
+// counts ids outside [0, n_nodes)
+__global__ void check_ids_kernel(const int64_t* __restrict__ ids, long long n, long long n_nodes,
+                                 unsigned long long* __restrict__ bad) {
+    const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const bool wrong = i < n && static_cast<unsigned long long>(__ldg(ids + i)) >= static_cast<unsigned long long>(n_nodes);
+    const unsigned b = __ballot_sync(0xffffffffu, wrong);
+    if ((threadIdx.x & 31) == 0 && b) atomicAdd(bad, static_cast<unsigned long long>(__popc(b)));
 }
 
 // counts positions where the id list is not strictly ascending
@@ -426,15 +468,16 @@ cudaError_t launch_sl_step(const SlParams& P, int kind, const double* phi, const
                            cudaStream_t stream) {
     if (n_active <= 0) return cudaSuccess;
     const unsigned blocks = static_cast<unsigned>((n_active + kSlThreads - 1) / kSlThreads);
+    const unsigned blocks_w3 = static_cast<unsigned>((n_active + kSlThreadsW3 - 1) / kSlThreadsW3);
     if (P.dim == 2) {
         if (kind == 0) sl_step_kernel<2, 0><<<blocks, kSlThreads, 0, stream>>>(P, phi, dist, active, n_active, out, bad);
         else sl_step_kernel<2, 1><<<blocks, kSlThreads, 0, stream>>>(P, phi, dist, active, n_active, out, bad);
+    } else if (kind == 0) {
+        sl_step_kernel<3, 0><<<blocks, kSlThreads, 0, stream>>>(P, phi, dist, active, n_active, out, bad);
+    } else if (LSR_ZTAB && P.ztab != nullptr) {
+        sl_step_zt_kernel<<<blocks_w3, kSlThreadsW3, 0, stream>>>(P, phi, dist, active, n_active, out, bad);
     } else {
-        if (kind == 0) sl_step_kernel<3, 0><<<blocks, kSlThreads, 0, stream>>>(P, phi, dist, active, n_active, out, bad);
-        else if (LSR_ZTAB && P.ztab != nullptr)
-            sl_step_kernel<3, 1, true><<<static_cast<unsigned>((n_active + kSlThreadsZt - 1) / kSlThreadsZt),
-                                         kSlThreadsZt, 0, stream>>>(P, phi, dist, active, n_active, out, bad);
-        else sl_step_kernel<3, 1><<<blocks, kSlThreads, 0, stream>>>(P, phi, dist, active, n_active, out, bad);
+        sl_step_kernel<3, 1><<<blocks, kSlThreads, 0, stream>>>(P, phi, dist, active, n_active, out, bad);
     }
     lsr_note_launch();
     return cudaGetLastError();
@@ -470,6 +513,14 @@ cudaError_t launch_zt_fill(const SlParams& P, const double* phi, const ZtBuffers
 cudaError_t launch_check_sorted(const int64_t* ids, long long n, unsigned long long* bad, cudaStream_t stream) {
     if (n <= 1) return cudaSuccess;
     check_sorted_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, stream>>>(ids, n, bad);
+    lsr_note_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_check_ids(const int64_t* ids, long long n, long long n_nodes, unsigned long long* bad,
+                             cudaStream_t stream) {
+    if (n <= 0) return cudaSuccess;
+    check_ids_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, stream>>>(ids, n, n_nodes, bad);
     lsr_note_launch();
     return cudaGetLastError();
 }

@@ -110,3 +110,20 @@ def test_golden_fixture_coverage():
     g = golden_grid(rec)
     k = rec["active"] // (g["dims"][0] * g["dims"][1])
     assert np.count_nonzero((k <= 1) | (k >= g["dims"][2] - 2)) > 100
+
+
+@pytest.mark.parametrize("ids", [[-1], [10**9], [0, 5, 1 << 40]])
+def test_out_of_grid_ids_are_config_error_before_device_work(built, ids):
+    lsr, g, phi, d, m = _args()
+    cfg = lsr.StepConfig(p=1, delta=0.0, dt=0.1, band=lsr.BandParams(0.4, 0.2))
+    bad = lsr.BandMask(g, active=np.asarray(ids, dtype=np.int64))
+    with pytest.raises(lsr.ConfigError, match="node ids"):
+        lsr.sl_step(phi, d, bad, cfg, 1.0, lsr.ScalarField(g))
+
+
+def test_short_host_arrays_are_config_error(built):
+    lsr, g, phi, d, m = _args()
+    cfg = lsr.StepConfig(p=1, delta=0.0, dt=0.1, band=lsr.BandParams(0.4, 0.2))
+    short = lsr.ScalarField(g, np.zeros(g.num_nodes() - 1))
+    with pytest.raises(lsr.ConfigError):
+        lsr.sl_step(short, d, m, cfg, 1.0, lsr.ScalarField(g))

@@ -520,3 +520,21 @@ def test_ztab_context_seeded_vs_oracle(gpu, oracle, n, p, delta, seed):
     assert (tms > 0.0) == (delta > 0.0)  # delta = 0 (coinciding feet) runs without the table
     ref = _oracle_step(oracle, g, phi, dist, active, cfg, p, delta, 0.7)
     assert np.count_nonzero(bits(got) != bits(ref)) == 0
+
+
+def test_context_rejects_out_of_grid_ids(gpu):
+    """Active ids are node ids (grid.hpp:79-84): host and device id lists
+    outside the grid are ConfigErrors before any kernel dereferences them."""
+    import torch
+
+    lsr = gpu
+    g = lsr._api.cube_grid(12, 3)
+    ctx = lsr.Context(g)
+    with pytest.raises(lsr.ConfigError, match="node ids"):
+        ctx.set_active(np.array([0, g.num_nodes()], dtype=np.int64))
+    bad = torch.tensor([3, -2, 5], dtype=torch.int64, device="cuda")
+    with pytest.raises(lsr.ConfigError, match="node ids"):
+        ctx.set_active_device(bad.data_ptr(), bad.numel())
+    ok = torch.arange(10, dtype=torch.int64, device="cuda")
+    ctx.set_active_device(ok.data_ptr(), ok.numel())
+    ctx.close()
