@@ -53,6 +53,7 @@ extern "C" {
 #define LSR_FIELD_PHI 0  /* phi^n (input of the step) */
 #define LSR_FIELD_DIST 1 /* unsigned distance d (DistanceField::field) */
 #define LSR_FIELD_OUT 2  /* phi^{n+1} (the double buffer `out`) */
+#define LSR_FIELD_SCRATCH 3 /* reinitialisation double buffer (z-slab contexts) */
 
 /* lsr::Grid (grid.hpp:10-52). dims[2] == 1 and origin[2] == 0 in 2d. */
 typedef struct lsr_grid {
@@ -273,6 +274,52 @@ typedef struct lsr_loop_stats {
 } lsr_loop_stats;
 int lsr_cuda_loop_step(lsr_cuda_ctx* ctx, const lsr_step_cfg* cfg, const lsr_reinit_cfg* rcfg, int energy_refine,
                        double energy_override, lsr_loop_stats* stats);
+
+/* ---- z-slab loop (driver.cpp:185-203 split over ranks) ----
+ * A slab context holds the resident planes [win_lo, win_hi) of the global
+ * grid (fields of (win_hi - win_lo) * nx * ny values; upload / download /
+ * field_ptr move whole windows) and works on the owned planes
+ * [own_lo, own_hi), win_lo <= max(own_lo - 1, 0), min(own_hi + 1, nz) <=
+ * win_hi. Node ids (active / tube lists, bad_node) are global. Between the
+ * phases the caller exchanges halo planes (lsr_cuda_slab_copy_planes) and
+ * reduces over the ranks; every phase gives the owned nodes the bits the
+ * whole-grid function gives them (paper_2410_22205_b200/zslab.py drives it). */
+int lsr_cuda_slab_create(int device, const lsr_grid* grid, int32_t win_lo, int32_t win_hi, int32_t own_lo,
+                         int32_t own_hi, lsr_cuda_ctx** ctx);
+/* planes [plane0, plane0 + nplanes) of field `which` to (to_field = 0) or
+ * from (1) nplanes * nx * ny doubles of device memory at dev */
+int lsr_cuda_slab_copy_planes(lsr_cuda_ctx* ctx, int which, int32_t plane0, int32_t nplanes, void* dev,
+                              int32_t to_field);
+/* narrow_band (grid.cpp:76-124) of the owned planes; needs `which` valid on
+ * the owned planes +- 1; the ACTIVE list becomes the active set */
+int lsr_cuda_slab_band(lsr_cuda_ctx* ctx, int which, double gamma, int64_t* n_active, int64_t* n_tube);
+/* surface_energy's interface cells of the owned cell planes and their
+ * contributions (metrics.cpp:145-184); then, given the global position of
+ * this rank's first contribution (the sum of the lower ranks' counts), its
+ * pieces of blocked_sum (parallel.hpp:26-42): the sums of the 4096-blocks
+ * wholly inside its range, and the raw contributions before its first
+ * (head, < 4096) and after its last (tail, < 4096) block boundary. blocks
+ * holds n_cells / 4096 + 1 values. */
+int lsr_cuda_slab_energy_cells(lsr_cuda_ctx* ctx, int which, int p, int refine, int64_t* n_cells);
+int lsr_cuda_slab_energy_pieces(lsr_cuda_ctx* ctx, int64_t offset, double* blocks, int64_t* n_blocks, double* head,
+                                int64_t* n_head, double* tail, int64_t* n_tail);
+/* largest foot displacement bound (cells) over the owned active nodes: the
+ * halo must exceed it by the stencil radius + 1 (2 + 1 for WENO) */
+int lsr_cuda_slab_max_reach(lsr_cuda_ctx* ctx, const lsr_step_cfg* cfg, double energy_p, double* cells);
+/* sl_step on the owned active nodes: OUT = PHI on the window, then the
+ * updates; *halo_miss = stencils that left the resident planes (then the
+ * result is void: widen the halo and redo) */
+int lsr_cuda_slab_sl_step(lsr_cuda_ctx* ctx, const lsr_step_cfg* cfg, double energy_p, int64_t* bad_node,
+                          int64_t* halo_miss);
+/* reinitialize (reinit.cpp:133-145) in phases: interface_one_step OUT ->
+ * SCRATCH on the owned planes (OUT valid on owned +- 1); reinit_begin after
+ * SCRATCH's halo planes are exchanged; sweep k reads buf[k & 1] and writes
+ * buf[(k + 1) & 1], buf = {SCRATCH, OUT}, returning the owned max |upd|;
+ * reinit_end clamps the result field's owned planes and makes it OUT */
+int lsr_cuda_slab_one_step(lsr_cuda_ctx* ctx, int* any_frozen, int* any_zero);
+int lsr_cuda_slab_reinit_begin(lsr_cuda_ctx* ctx, const lsr_reinit_cfg* rcfg, int64_t* n_nodes);
+int lsr_cuda_slab_reinit_sweep(lsr_cuda_ctx* ctx, const lsr_reinit_cfg* rcfg, int32_t k, double* residual);
+int lsr_cuda_slab_reinit_end(lsr_cuda_ctx* ctx, int which, double gamma);
 
 /* ---- self-test hook ----
  * Divides n pseudo-random doubles by c with the kernels' constant-divisor

@@ -27,6 +27,7 @@ from ._api import (  # noqa: F401
     OutOfDomainError,
     ReinitConfig,
     ScalarField,
+    SlabContext,
     StepConfig,
     build_distance_field,
     compute_stats,

@@ -62,7 +62,7 @@ _EXC = {
     LSR_ERR_CUDA: CudaError,
     LSR_ERR_NO_INTERFACE: NoInterfaceError,
 }
-FIELD_PHI, FIELD_DIST, FIELD_OUT = 0, 1, 2
+FIELD_PHI, FIELD_DIST, FIELD_OUT, FIELD_SCRATCH = 0, 1, 2, 3
 
 
 class CGrid(C.Structure):
@@ -151,6 +151,19 @@ def lib() -> C.CDLL:
     L.lsr_cuda_ipc_close.argtypes = [C.c_void_p]
     L.lsr_cuda_compute_stats.argtypes = [_dp, C.c_int64, C.c_int, C.c_double, C.c_double, C.c_uint64, P(C.c_double),
                                          P(C.c_double), _dp]
+    L.lsr_cuda_slab_create.argtypes = [C.c_int, P(CGrid), C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+                                       P(C.c_void_p)]
+    L.lsr_cuda_slab_copy_planes.argtypes = [C.c_void_p, C.c_int, C.c_int32, C.c_int32, C.c_void_p, C.c_int32]
+    L.lsr_cuda_slab_band.argtypes = [C.c_void_p, C.c_int, C.c_double, P(C.c_int64), P(C.c_int64)]
+    L.lsr_cuda_slab_energy_cells.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, P(C.c_int64)]
+    L.lsr_cuda_slab_energy_pieces.argtypes = [C.c_void_p, C.c_int64, _dp, P(C.c_int64), _dp, P(C.c_int64), _dp,
+                                              P(C.c_int64)]
+    L.lsr_cuda_slab_max_reach.argtypes = [C.c_void_p, P(CStepCfg), C.c_double, P(C.c_double)]
+    L.lsr_cuda_slab_sl_step.argtypes = [C.c_void_p, P(CStepCfg), C.c_double, P(C.c_int64), P(C.c_int64)]
+    L.lsr_cuda_slab_one_step.argtypes = [C.c_void_p, P(C.c_int), P(C.c_int)]
+    L.lsr_cuda_slab_reinit_begin.argtypes = [C.c_void_p, P(CReinitCfg), P(C.c_int64)]
+    L.lsr_cuda_slab_reinit_sweep.argtypes = [C.c_void_p, P(CReinitCfg), C.c_int32, P(C.c_double)]
+    L.lsr_cuda_slab_reinit_end.argtypes = [C.c_void_p, C.c_int, C.c_double]
     _lib = L
     return L
 
@@ -607,3 +620,114 @@ class Context:
         t = C.c_float()
         _check(lib().lsr_cuda_last_table_ms(self.h, C.byref(t)))
         return t.value
+
+
+
+class SlabContext:
+    """One rank's z-slab of the loop (lsr_cuda_slab_*): fields hold the
+    resident planes [win_lo, win_hi) of the global grid, the phases work on
+    the owned planes [own_lo, own_hi). Node ids are global. See
+    paper_2410_22205_b200.zslab.SlabLoop for the driver."""
+
+    def __init__(self, grid: Grid, win_lo: int, win_hi: int, own_lo: int, own_hi: int, device: int = 0):
+        self.grid = grid
+        self.win_lo, self.win_hi, self.own_lo, self.own_hi = int(win_lo), int(win_hi), int(own_lo), int(own_hi)
+        self.nxy = grid.dims[0] * grid.dims[1]
+        self.h = C.c_void_p()
+        _check(lib().lsr_cuda_slab_create(int(device), C.byref(grid.c()), self.win_lo, self.win_hi, self.own_lo,
+                                          self.own_hi, C.byref(self.h)))
+
+    @property
+    def n_resident(self) -> int:
+        return (self.win_hi - self.win_lo) * self.nxy
+
+    def close(self):
+        if self.h:
+            lib().lsr_cuda_destroy(self.h)
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def upload(self, which: int, values: np.ndarray):
+        v = np.ascontiguousarray(values, dtype=np.float64).reshape(-1)
+        if v.size != self.n_resident:
+            raise ConfigError("slab upload: need the resident planes' values")
+        _check(lib().lsr_cuda_upload_field(self.h, which, v.ctypes.data_as(C.c_void_p)))
+
+    def download(self, which: int) -> np.ndarray:
+        out = np.empty(self.n_resident, dtype=np.float64)
+        _check(lib().lsr_cuda_download_field(self.h, which, out.ctypes.data_as(C.c_void_p)))
+        return out
+
+    def field_ptr(self, which: int) -> int:
+        p = C.c_void_p()
+        _check(lib().lsr_cuda_field_ptr(self.h, which, C.byref(p)))
+        return int(p.value)
+
+    def plane_ptr(self, which: int, plane: int) -> int:
+        """Device address of global plane `plane` of field `which`."""
+        assert self.win_lo <= plane <= self.win_hi
+        return self.field_ptr(which) + 8 * (plane - self.win_lo) * self.nxy
+
+    def copy_planes(self, which: int, plane0: int, nplanes: int, dev_ptr: int, to_field: bool):
+        _check(lib().lsr_cuda_slab_copy_planes(self.h, int(which), int(plane0), int(nplanes), C.c_void_p(dev_ptr),
+                                               int(bool(to_field))))
+
+    def swap(self):
+        _check(lib().lsr_cuda_swap(self.h))
+
+    def band(self, gamma: float, which: int = FIELD_PHI):
+        na, nt = C.c_int64(), C.c_int64()
+        _check(lib().lsr_cuda_slab_band(self.h, int(which), float(gamma), C.byref(na), C.byref(nt)))
+        self.n_active, self.n_tube = na.value, nt.value
+        return na.value, nt.value
+
+    def energy_cells(self, which: int = FIELD_PHI, p: int = 2, refine: int = 5) -> int:
+        n = C.c_int64()
+        _check(lib().lsr_cuda_slab_energy_cells(self.h, int(which), int(p), int(refine), C.byref(n)))
+        self.n_cells = n.value
+        return n.value
+
+    def energy_pieces(self, offset: int):
+        """(block sums, head, tail) of blocked_sum for this rank at global offset."""
+        nb_cap = self.n_cells // 4096 + 1
+        blocks, head, tail = np.empty(nb_cap), np.empty(4096), np.empty(4096)
+        nb, nh, nt = C.c_int64(), C.c_int64(), C.c_int64()
+        _check(lib().lsr_cuda_slab_energy_pieces(self.h, int(offset), blocks, C.byref(nb), head, C.byref(nh), tail,
+                                                 C.byref(nt)))
+        return blocks[:nb.value].copy(), head[:nh.value].copy(), tail[:nt.value].copy()
+
+    def max_reach(self, cfg: StepConfig, energy_p: float) -> float:
+        c = C.c_double()
+        _check(lib().lsr_cuda_slab_max_reach(self.h, C.byref(cfg.c()), float(energy_p), C.byref(c)))
+        return c.value
+
+    def sl_step(self, cfg: StepConfig, energy_p: float) -> int:
+        """Returns the halo-miss count (0: the step is valid)."""
+        bad, miss = C.c_int64(-1), C.c_int64(0)
+        st = lib().lsr_cuda_slab_sl_step(self.h, C.byref(cfg.c()), float(energy_p), C.byref(bad), C.byref(miss))
+        self.bad_node = bad.value
+        _check(st)
+        return miss.value
+
+    def one_step(self):
+        f, z = C.c_int(), C.c_int()
+        _check(lib().lsr_cuda_slab_one_step(self.h, C.byref(f), C.byref(z)))
+        return bool(f.value), bool(z.value)
+
+    def reinit_begin(self, rcfg: "ReinitConfig") -> int:
+        n = C.c_int64()
+        _check(lib().lsr_cuda_slab_reinit_begin(self.h, C.byref(rcfg.c()), C.byref(n)))
+        return n.value
+
+    def reinit_sweep(self, rcfg: "ReinitConfig", k: int) -> float:
+        r = C.c_double()
+        _check(lib().lsr_cuda_slab_reinit_sweep(self.h, C.byref(rcfg.c()), int(k), C.byref(r)))
+        return r.value
+
+    def reinit_end(self, which: int, gamma: float):
+        _check(lib().lsr_cuda_slab_reinit_end(self.h, int(which), float(gamma)))

@@ -62,3 +62,17 @@ int lsr_reinit_iterate(const lsr_dev::SlParams& P, double** phi, double** scratc
 int lsr_reinitialize(const lsr_dev::SlParams& P, double** phi, double** scratch, const BandBuffers& B, double gamma,
                      const ReinitParams& R, ReinitBuffers& W, int* iterations, int* had_interface, cudaStream_t s,
                      std::string* err);
+
+// z-slab forms (band_reinit.cu): owned planes [own_lo, own_hi) of buffers
+// resident on [win_lo, win_hi), passed shifted to global node ids
+int lsr_band_build_slab(const lsr_dev::SlParams& P, const double* phi_g, double gamma, BandBuffers& B, int win_lo,
+                        int win_hi, int own_lo, int own_hi, long long* n_active, long long* n_tube, cudaStream_t s,
+                        std::string* err);
+int lsr_reinit_one_step_slab(const lsr_dev::SlParams& P, const double* prev_g, double* out_g, ReinitBuffers& W,
+                             int win_lo, int win_hi, int own_lo, int own_hi, int* any_frozen, int* any_zero,
+                             cudaStream_t s, std::string* err);
+int lsr_reinit_slab_begin(const lsr_dev::SlParams& P, const double* cur_g, double* nxt_g, const long long* tube,
+                          long long n_tube, const ReinitParams& R, ReinitBuffers& W, int win_lo, int win_hi,
+                          long long* n_nodes, cudaStream_t s, std::string* err);
+int lsr_reinit_slab_sweep(const lsr_dev::SlParams& P, const double* cur_g, double* nxt_g, ReinitBuffers& W,
+                          long long nn, double dtau, double* residual, cudaStream_t s, std::string* err);

@@ -61,10 +61,11 @@ struct IterState {  // device-side control of the Jacobi sweeps
 // max-dilation of the ACTIVE indicator: dilate along x (pass 1, which also
 // evaluates |phi| < gamma), then y (pass 2), then z (pass 3). Per node:
 // bit 0 = dilated indicator, bit 1 = the node itself is ACTIVE.
-__global__ void band_pass_x(SlParams P, const double* __restrict__ phi, double gamma, long long n,
+// (all passes take node ids [base, end); buffers are indexed by global id)
+__global__ void band_pass_x(SlParams P, const double* __restrict__ phi, double gamma, long long base, long long end,
                             unsigned char* __restrict__ t) {
-    const long long id = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (id >= n) return;
+    const long long id = base + static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (id >= end) return;
     int i, j, k;
     lsr_dev::unflatten(P, id, i, j, k);
     const bool c = fabs(__ldg(phi + id)) < gamma;
@@ -74,10 +75,10 @@ __global__ void band_pass_x(SlParams P, const double* __restrict__ phi, double g
     t[id] = static_cast<unsigned char>((c ? 2 : 0) | (d ? 1 : 0));
 }
 
-__global__ void band_pass_y(SlParams P, const unsigned char* __restrict__ t, long long n,
+__global__ void band_pass_y(SlParams P, const unsigned char* __restrict__ t, long long base, long long end,
                             unsigned char* __restrict__ u, unsigned char* __restrict__ state) {
-    const long long id = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (id >= n) return;
+    const long long id = base + static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (id >= end) return;
     int i, j, k;
     lsr_dev::unflatten(P, id, i, j, k);
     const unsigned char c = t[id];
@@ -89,10 +90,10 @@ __global__ void band_pass_y(SlParams P, const unsigned char* __restrict__ t, lon
     else u[id] = v;
 }
 
-__global__ void band_pass_z(SlParams P, const unsigned char* __restrict__ u, long long n,
+__global__ void band_pass_z(SlParams P, const unsigned char* __restrict__ u, long long base, long long end,
                             unsigned char* __restrict__ state) {
-    const long long id = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (id >= n) return;
+    const long long id = base + static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (id >= end) return;
     int i, j, k;
     lsr_dev::unflatten(P, id, i, j, k);
     const unsigned char c = u[id];
@@ -106,10 +107,10 @@ __global__ void band_pass_z(SlParams P, const unsigned char* __restrict__ u, lon
 // pass makes 4 nodes per thread (two 16-byte loads of phi, one 4-byte store),
 // the y/z passes 16 per thread (16-byte loads and stores, bytewise logic on
 // 32-bit lanes). Same results as the scalar passes above.
-__global__ void band_pass_x4(SlParams P, const double* __restrict__ phi, double gamma, long long n4,
+__global__ void band_pass_x4(SlParams P, const double* __restrict__ phi, double gamma, long long base4, long long end4,
                              unsigned* __restrict__ t) {
-    const long long q = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (q >= n4) return;
+    const long long q = base4 + static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (q >= end4) return;
     const long long id = 4 * q;
     const int x0 = static_cast<int>(id % P.nx);
     const double2 a = __ldg(reinterpret_cast<const double2*>(phi + id));
@@ -132,10 +133,10 @@ __device__ __forceinline__ unsigned state_bytes(unsigned core_bits, unsigned dil
     return b1 | ((b0 & ~b1) << 1);
 }
 
-__global__ void band_pass_yz16(SlParams P, int axis, const uint4* __restrict__ in, long long n16,
+__global__ void band_pass_yz16(SlParams P, int axis, const uint4* __restrict__ in, long long base16, long long end16,
                                uint4* __restrict__ out, uint4* __restrict__ state) {
-    const long long q = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (q >= n16) return;
+    const long long q = base16 + static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (q >= end16) return;
     const long long row = (16 * q) / P.nx;
     const int j = static_cast<int>(row % P.ny), k = static_cast<int>(row / P.ny);
     const long long st = (axis == 1 ? P.nx : P.nxy) / 16;
@@ -217,12 +218,17 @@ __global__ void clamp_kernel(double* __restrict__ f, long long n, double gamma, 
 // interface_one_step (reinit.cpp:24-46); `prev` is read-only, `out` gets every
 // node. The two "any" flags are raised once per warp (a single-address store
 // from every frozen node serialises in L2).
+// (prev, out, frozen point at node `base`, items [0, n): a z-slab's owned ids)
 __global__ void one_step(SlParams P, const double* __restrict__ prev, double* __restrict__ out,
                          unsigned char* __restrict__ frozen, long long n, int* __restrict__ any_frozen,
-                         int* __restrict__ any_zero) {
-    const long long id = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+                         int* __restrict__ any_zero, long long base) {
+    const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
     bool is_zero = false, is_frozen = false;
-    if (id < n) {
+    if (t < n) {
+        const long long id = base + t;
+        prev -= base;
+        out -= base;
+        frozen -= base;
         int i, j, k;
         lsr_dev::unflatten(P, id, i, j, k);
         // the node and its six neighbours are loaded up front (an absent
@@ -311,18 +317,19 @@ constexpr int kMarch = 16;
 #ifndef LSR_MARCH_MINB
 #define LSR_MARCH_MINB 4  // 64 registers: occupancy beats the few spills (reinit 4.82 -> 4.71 ms at 512^3)
 #endif
+// planes [k_lo, k_hi) (the whole grid: 0, nz; a z-slab: its owned planes)
 __global__ void __launch_bounds__(256, LSR_MARCH_MINB) one_step_march(SlParams P, const double* __restrict__ prev, double* __restrict__ out,
                                unsigned* __restrict__ frozen4, int* __restrict__ any_frozen,
-                               int* __restrict__ any_zero) {
+                               int* __restrict__ any_zero, int k_lo, int k_hi) {
     const int qx = P.nx / 4;
     const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
     const long long rows = static_cast<long long>(qx) * P.ny;  // (x-quad, j) pairs
     bool zero = false, froz = false;
-    if (t < rows * ((P.nz + kMarch - 1) / kMarch)) {
+    if (t < rows * ((k_hi - k_lo + kMarch - 1) / kMarch)) {
         const int kb = static_cast<int>(t / rows);
         const long long r = t - kb * rows;
         const int j = static_cast<int>(r / qx), x0 = 4 * static_cast<int>(r - static_cast<long long>(j) * qx);
-        const int k0 = kb * kMarch, k1 = min(P.nz, k0 + kMarch);
+        const int k0 = k_lo + kb * kMarch, k1 = min(k_hi, k0 + kMarch);
         const bool hy[2] = {j > 0, j + 1 < P.ny};
         long long id = (static_cast<long long>(k0) * P.ny + j) * P.nx + x0;
         double zm[4], c[4], zp[4];
@@ -609,6 +616,39 @@ static int ensure_tmp(BandBuffers& B, size_t bytes, std::string* err) {
     return LSR_OK;
 }
 
+// the three dilation passes: x and y over node ids [a0, a1), z (the state)
+// over [b0, b1) within [a0, a1); every buffer indexed by global node id. A
+// z-slab passes its owned ids as [b0, b1) and one plane more on each side as
+// [a0, a1) (the z pass reads the y-dilated planes next to its own).
+static void band_passes(const SlParams& P, const double* phi, double gamma, long long a0, long long a1, long long b0,
+                        long long b1, unsigned char* t, unsigned char* u, unsigned char* state, cudaStream_t s) {
+    const auto grid = [](long long items) { return static_cast<unsigned>((items + 255) / 256); };
+    if (P.nx % 16 == 0) {  // rows of whole 16-byte vectors
+        band_pass_x4<<<grid((a1 - a0) / 4), 256, 0, s>>>(P, phi, gamma, a0 / 4, a1 / 4, reinterpret_cast<unsigned*>(t));
+        const uint4* t16 = reinterpret_cast<const uint4*>(t);
+        const uint4* u16c = reinterpret_cast<const uint4*>(u);
+        uint4* u16 = reinterpret_cast<uint4*>(u);
+        uint4* st16 = reinterpret_cast<uint4*>(state);
+        if (P.dim == 3) {
+            band_pass_yz16<<<grid((a1 - a0) / 16), 256, 0, s>>>(P, 1, t16, a0 / 16, a1 / 16, u16, st16);
+            band_pass_yz16<<<grid((b1 - b0) / 16), 256, 0, s>>>(P, 2, u16c, b0 / 16, b1 / 16, nullptr, st16);
+        } else {
+            band_pass_yz16<<<grid((b1 - b0) / 16), 256, 0, s>>>(P, 1, t16, b0 / 16, b1 / 16, u16, st16);
+        }
+    } else {
+        band_pass_x<<<grid(a1 - a0), 256, 0, s>>>(P, phi, gamma, a0, a1, t);
+        if (P.dim == 3) {
+            band_pass_y<<<grid(a1 - a0), 256, 0, s>>>(P, t, a0, a1, u, state);
+            band_pass_z<<<grid(b1 - b0), 256, 0, s>>>(P, u, b0, b1, state);
+        } else {
+            band_pass_y<<<grid(b1 - b0), 256, 0, s>>>(P, t, b0, b1, u, state);
+        }
+    }
+    lsr_note_launch();
+    lsr_note_launch();
+    if (P.dim == 3) lsr_note_launch();
+}
+
 int lsr_band_build(const SlParams& P, const double* phi, double gamma, BandBuffers& B, long long* n_active,
                    long long* n_tube, cudaStream_t s, std::string* err) {
     if (!(gamma > 0.0)) {
@@ -617,29 +657,11 @@ int lsr_band_build(const SlParams& P, const double* phi, double gamma, BandBuffe
     }
     const long long n = P.nxy * P.nz;
     if (int st = B.reserve(n, err)) return st;
-    const unsigned gb = static_cast<unsigned>((n + 255) / 256);
     // scratch bytes for the two dilation passes live in the active/tube id
     // buffers, which are only written by the compaction afterwards
     unsigned char* t = reinterpret_cast<unsigned char*>(B.active);
     unsigned char* u = reinterpret_cast<unsigned char*>(B.tube);
-    if (P.nx % 16 == 0) {  // rows of whole 16-byte vectors
-        const long long n4 = n / 4, n16 = n / 16;
-        band_pass_x4<<<static_cast<unsigned>((n4 + 255) / 256), 256, 0, s>>>(P, phi, gamma, n4,
-                                                                               reinterpret_cast<unsigned*>(t));
-        const unsigned g16 = static_cast<unsigned>((n16 + 255) / 256);
-        band_pass_yz16<<<g16, 256, 0, s>>>(P, 1, reinterpret_cast<const uint4*>(t), n16, reinterpret_cast<uint4*>(u),
-                                           reinterpret_cast<uint4*>(B.state));
-        if (P.dim == 3)
-            band_pass_yz16<<<g16, 256, 0, s>>>(P, 2, reinterpret_cast<const uint4*>(u), n16, nullptr,
-                                               reinterpret_cast<uint4*>(B.state));
-    } else {
-        band_pass_x<<<gb, 256, 0, s>>>(P, phi, gamma, n, t);
-        band_pass_y<<<gb, 256, 0, s>>>(P, t, n, u, B.state);
-        if (P.dim == 3) band_pass_z<<<gb, 256, 0, s>>>(P, u, n, B.state);
-    }
-    lsr_note_launch();
-    lsr_note_launch();
-    if (P.dim == 3) lsr_note_launch();
+    band_passes(P, phi, gamma, 0, n, 0, n, t, u, B.state, s);
     const size_t tb = lsr_compact::scratch_bytes(n);
     if (int st = ensure_tmp(B, tb, err)) return st;
     BR_TRY(lsr_compact::compact(lsr_compact::BytePred<StateIs1>{B.state, {}}, lsr_compact::Identity{}, n, B.active,
@@ -733,10 +755,10 @@ int lsr_reinit_one_step(const SlParams& P, double** phi, double** scratch, Reini
     if (P.dim == 3 && P.nx % 4 == 0) {
         const long long threads = static_cast<long long>(P.nx / 4) * P.ny * ((P.nz + kMarch - 1) / kMarch);
         one_step_march<<<static_cast<unsigned>((threads + 255) / 256), 256, 0, s>>>(
-            P, *phi, *scratch, reinterpret_cast<unsigned*>(W.frozen), flags, flags + 1);
+            P, *phi, *scratch, reinterpret_cast<unsigned*>(W.frozen), flags, flags + 1, 0, P.nz);
     } else {
         one_step<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(P, *phi, *scratch, W.frozen, n, flags,
-                                                                         flags + 1);
+                                                                         flags + 1, 0);
     }
     lsr_note_launch();
     int hf[2];
@@ -865,4 +887,138 @@ int lsr_reinitialize(const SlParams& P, double** phi, double** scratch, const Ba
     if (*had_interface)
         if (int st = lsr_reinit_iterate(P, phi, scratch, B.tube, B.n_tube, R, W, true, iterations, s, err)) return st;
     return lsr_clamp(*phi, n, gamma, s, err, B.state, W.clamp_outside);
+}
+
+// ---------------------------------------------------------------------------
+// z-slab forms: the same kernels on the owned planes
+// [own_lo, own_hi) of a rank whose buffers hold the resident planes
+// [win_lo, win_hi) and are passed shifted to global node ids (phi_g[id] is
+// node id's value for any resident id). Boundary tests stay those of the
+// global grid; a node's stencil (one plane up and down) must be resident,
+// i.e. win_lo <= max(own_lo - 1, 0) and min(own_hi + 1, nz) <= win_hi.
+
+namespace {
+struct OffsetId {  // compaction item: the index shifted to a global id
+    long long base;
+    __device__ long long operator()(long long i) const { return base + i; }
+};
+}  // namespace
+
+int lsr_band_build_slab(const SlParams& P, const double* phi_g, double gamma, BandBuffers& B, int win_lo, int win_hi,
+                        int own_lo, int own_hi, long long* n_active, long long* n_tube, cudaStream_t s,
+                        std::string* err) {
+    if (!(gamma > 0.0)) {
+        *err = "narrow_band: gamma must be positive";  // grid.cpp:77
+        return LSR_ERR_CONFIG;
+    }
+    const long long nw = static_cast<long long>(win_hi - win_lo) * P.nxy, off = static_cast<long long>(win_lo) * P.nxy;
+    if (int st = B.reserve(nw, err)) return st;
+    unsigned char* t = reinterpret_cast<unsigned char*>(B.active) - off;  // scratch bytes (see lsr_band_build)
+    unsigned char* u = reinterpret_cast<unsigned char*>(B.tube) - off;
+    unsigned char* state = B.state - off;
+    const long long a0 = static_cast<long long>(max(own_lo - 1, win_lo)) * P.nxy;
+    const long long a1 = static_cast<long long>(min(own_hi + 1, win_hi)) * P.nxy;
+    const long long b0 = static_cast<long long>(own_lo) * P.nxy, b1 = static_cast<long long>(own_hi) * P.nxy;
+    band_passes(P, phi_g, gamma, a0, a1, b0, b1, t, u, state, s);
+    const size_t tb = lsr_compact::scratch_bytes(b1 - b0);
+    if (int st = ensure_tmp(B, tb, err)) return st;
+    BR_TRY(lsr_compact::compact(lsr_compact::BytePred<StateIs1>{state + b0, {}}, OffsetId{b0}, b1 - b0, B.active,
+                                B.counts, B.tmp, tb, s));
+    BR_TRY(lsr_compact::compact(lsr_compact::BytePred<NonZero>{state + b0, {}}, OffsetId{b0}, b1 - b0, B.tube,
+                                B.counts + 1, B.tmp, tb, s));
+    for (int q = 0; q < 4; ++q) lsr_note_launch();
+    long long h[2];
+    BR_TRY(cudaMemcpyAsync(h, B.counts, sizeof h, cudaMemcpyDeviceToHost, s));
+    BR_TRY(cudaStreamSynchronize(s));
+    *n_active = B.n_active = h[0];
+    *n_tube = B.n_tube = h[1];
+    return LSR_OK;
+}
+
+// interface_one_step (reinit.cpp:24-46) on the owned planes: prev_g -> out_g,
+// frozen flags; any_frozen / any_zero of the owned nodes (the caller ORs them
+// over the ranks: NoInterfaceError is a global verdict)
+int lsr_reinit_one_step_slab(const SlParams& P, const double* prev_g, double* out_g, ReinitBuffers& W, int win_lo,
+                             int win_hi, int own_lo, int own_hi, int* any_frozen, int* any_zero, cudaStream_t s,
+                             std::string* err) {
+    const long long nw = static_cast<long long>(win_hi - win_lo) * P.nxy, off = static_cast<long long>(win_lo) * P.nxy;
+    if (int st = W.reserve(nw, err)) return st;
+    int* flags = reinterpret_cast<int*>(W.scal);
+    BR_TRY(cudaMemsetAsync(W.scal, 0, sizeof(unsigned long long) * 4, s));
+    BR_TRY(cudaMemsetAsync(W.frozen, 0, static_cast<size_t>(nw), s));
+    unsigned char* frozen_g = W.frozen - off;
+    if (P.nx % 4 == 0) {
+        const long long threads = static_cast<long long>(P.nx / 4) * P.ny * ((own_hi - own_lo + kMarch - 1) / kMarch);
+        one_step_march<<<static_cast<unsigned>((threads + 255) / 256), 256, 0, s>>>(
+            P, prev_g, out_g, reinterpret_cast<unsigned*>(frozen_g), flags, flags + 1, own_lo, own_hi);
+    } else {
+        const long long b0 = static_cast<long long>(own_lo) * P.nxy, n = static_cast<long long>(own_hi - own_lo) * P.nxy;
+        one_step<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(P, prev_g + b0, out_g + b0, frozen_g + b0, n,
+                                                                         flags, flags + 1, b0);
+    }
+    lsr_note_launch();
+    int hf[2];
+    BR_TRY(cudaMemcpyAsync(hf, flags, sizeof hf, cudaMemcpyDeviceToHost, s));
+    BR_TRY(cudaStreamSynchronize(s));
+    *any_frozen = hf[0];
+    *any_zero = hf[1];
+    return LSR_OK;
+}
+
+// reinit_iterate's set-up (reinit.cpp:94-109) on the owned planes: `cur_g`
+// holds the one-step result on every resident plane (halo exchanged);
+// `nxt_g` becomes a copy of it (next = phi), the node list is the owned tube
+// minus the frozen nodes (ascending), and the signs / neighbour masks
+// (sign_kernel) are taken from cur. Returns the node count.
+int lsr_reinit_slab_begin(const SlParams& P, const double* cur_g, double* nxt_g, const long long* tube,
+                          long long n_tube, const ReinitParams& R, ReinitBuffers& W, int win_lo, int win_hi,
+                          long long* n_nodes, cudaStream_t s, std::string* err) {
+    const long long nw = static_cast<long long>(win_hi - win_lo) * P.nxy, off = static_cast<long long>(win_lo) * P.nxy;
+    if (int st = W.reserve(nw, err)) return st;
+    BR_TRY(cudaMemcpyAsync(nxt_g + off, cur_g + off, sizeof(double) * nw, cudaMemcpyDeviceToDevice, s));
+    long long* d_nn = reinterpret_cast<long long*>(W.scal + 2);
+    const size_t tb = lsr_compact::scratch_bytes(n_tube > 0 ? n_tube : 1);
+    if (tb > W.tmp_bytes) {
+        cudaFree(W.tmp);
+        W.tmp = nullptr;
+        BR_TRY(cudaMalloc(&W.tmp, tb));
+        W.tmp_bytes = tb;
+    }
+    BR_TRY(lsr_compact::compact(NotFrozen{W.frozen - off, tube}, TubeId{tube}, n_tube, W.nodes, d_nn, W.tmp, tb, s));
+    lsr_note_launch();
+    lsr_note_launch();
+    long long nn = 0;
+    BR_TRY(cudaMemcpyAsync(&nn, d_nn, sizeof nn, cudaMemcpyDeviceToHost, s));
+    BR_TRY(cudaStreamSynchronize(s));
+    if (nn > 0) {
+        const bool small = static_cast<long long>(P.nxy) * P.nz <= 0xffffffffLL;
+        sign_kernel<<<static_cast<unsigned>((nn + 255) / 256), 256, 0, s>>>(P, cur_g, W.nodes, nn,
+                                                                             R.sign_eps * R.sign_eps, W.sgn, W.nbr,
+                                                                             small ? W.nodes32 : nullptr);
+        lsr_note_launch();
+    }
+    *n_nodes = nn;
+    return LSR_OK;
+}
+
+// one Jacobi sweep (reinit.cpp:111-124) cur_g -> nxt_g on the node list of
+// lsr_reinit_slab_begin; *residual = max |upd| over the owned nodes (the
+// caller takes the max over the ranks for the stop rule, reinit.cpp:125-128)
+int lsr_reinit_slab_sweep(const SlParams& P, const double* cur_g, double* nxt_g, ReinitBuffers& W, long long nn,
+                          double dtau, double* residual, cudaStream_t s, std::string* err) {
+    IterState* st = reinterpret_cast<IterState*>(W.scal);
+    BR_TRY(cudaMemsetAsync(st, 0, sizeof(IterState), s));
+    if (nn > 0) {
+        const unsigned g = static_cast<unsigned>((nn + kJacThreads * kJacNPT - 1) / (kJacThreads * kJacNPT));
+        if (static_cast<long long>(P.nxy) * P.nz <= 0xffffffffLL)
+            jacobi<<<g, kJacThreads, 0, s>>>(P, cur_g, nxt_g, W.nodes32, W.sgn, W.nbr, nn, dtau, st);
+        else
+            jacobi<<<g, kJacThreads, 0, s>>>(P, cur_g, nxt_g, W.nodes, W.sgn, W.nbr, nn, dtau, st);
+        lsr_note_launch();
+    }
+    unsigned long long bits = 0;
+    BR_TRY(cudaMemcpyAsync(&bits, &st->residual_bits, sizeof bits, cudaMemcpyDeviceToHost, s));
+    BR_TRY(cudaStreamSynchronize(s));
+    std::memcpy(residual, &bits, sizeof bits);
+    return LSR_OK;
 }

@@ -45,10 +45,11 @@ __device__ __forceinline__ double powp(double a, int p) {
 }
 
 // interface_cells' corner test (metrics.cpp:23-31, 40-52)
-__global__ void flag_cells(SlParams P, const double* __restrict__ phi, long long ncells,
+// cells [base, end); flags indexed by global cell id
+__global__ void flag_cells(SlParams P, const double* __restrict__ phi, long long base, long long end,
                            unsigned char* __restrict__ flags) {
-    const long long c = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (c >= ncells) return;
+    const long long c = base + static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (c >= end) return;
     const unsigned cx = P.nx - 1, cy = P.ny - 1;  // cells < 2^31 (cub's int item count)
     const unsigned row = static_cast<unsigned>(c) / cx;
     const int i = static_cast<int>(static_cast<unsigned>(c) - row * cx);
@@ -121,16 +122,17 @@ __device__ __forceinline__ void row_classes(const SlParams& P, const double* __r
     cls[4] = i0 + 4 < P.nx ? sign_class(__ldg(phi + b + 4)) : 0u;
 }
 
+// cell planes [k_lo, k_hi) (whole grid: 0, nz - 1); flags indexed by global cell id
 __global__ void flag_cells_march(SlParams P, const double* __restrict__ phi, unsigned tpr,
-                                 unsigned char* __restrict__ flags) {
+                                 unsigned char* __restrict__ flags, int k_lo, int k_hi) {
     const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-    const int cx = P.nx - 1, cy = P.ny - 1, cz = P.nz - 1;
+    const int cx = P.nx - 1, cy = P.ny - 1;
     const long long rows = static_cast<long long>(tpr) * cy;  // (x-quad, j) pairs
-    if (t >= rows * ((cz + kMarchCells - 1) / kMarchCells)) return;
+    if (t >= rows * ((k_hi - k_lo + kMarchCells - 1) / kMarchCells)) return;
     const int kb = static_cast<int>(t / rows);
     const long long r = t - kb * rows;
     const int j = static_cast<int>(r / tpr), i0 = 4 * static_cast<int>(r - static_cast<long long>(j) * tpr);
-    const int k0 = kb * kMarchCells, k1 = min(cz, k0 + kMarchCells);
+    const int k0 = k_lo + kb * kMarchCells, k1 = min(k_hi, k0 + kMarchCells);
     unsigned lo[5], lo1[5];  // classes of node rows (j, k) and (j+1, k)
     long long b = (static_cast<long long>(k0) * P.ny + j) * P.nx + i0;
     row_classes(P, phi, b, i0, lo);
@@ -348,6 +350,10 @@ struct FlagSet {
 struct CellId {  // cell ids fit int (cub's item count, as before)
     __device__ int operator()(long long c) const { return static_cast<int>(c); }
 };
+struct CellIdFrom {  // a z-slab's cells: index i of its range is global cell base + i
+    long long base;
+    __device__ int operator()(long long c) const { return static_cast<int>(base + c); }
+};
 
 __global__ void block_partials(const double* __restrict__ contrib, long long n, double* __restrict__ partial) {
     __shared__ double buf[4096];
@@ -427,13 +433,13 @@ int lsr_prep_surface_energy(const SlParams& P, const double* phi, const double* 
     if (P.dim == 3 && P.nx % 4 == 0 && march) {
         const unsigned tpr = static_cast<unsigned>((P.nx - 1 + 3) / 4);
         const long long nt = static_cast<long long>(P.ny - 1) * tpr * ((P.nz - 1 + kMarchCells - 1) / kMarchCells);
-        flag_cells_march<<<static_cast<unsigned>((nt + T - 1) / T), T, 0, s>>>(P, phi, tpr, W.flags);
+        flag_cells_march<<<static_cast<unsigned>((nt + T - 1) / T), T, 0, s>>>(P, phi, tpr, W.flags, 0, P.nz - 1);
     } else if (P.dim == 3 && P.nx % 4 == 0) {
         const unsigned tpr = static_cast<unsigned>((P.nx - 1 + 3) / 4);
         const long long nt = static_cast<long long>(P.ny - 1) * (P.nz - 1) * tpr;
         flag_cells4<<<static_cast<unsigned>((nt + T - 1) / T), T, 0, s>>>(P, phi, tpr, nt, W.flags);
     } else {
-        flag_cells<<<static_cast<unsigned>((ncells + T - 1) / T), T, 0, s>>>(P, phi, ncells, W.flags);
+        flag_cells<<<static_cast<unsigned>((ncells + T - 1) / T), T, 0, s>>>(P, phi, 0, ncells, W.flags);
     }
     lsr_note_launch();
     const size_t tb = lsr_compact::scratch_bytes(ncells) + sizeof(long long);
@@ -499,4 +505,131 @@ int lsr_prep_surface_energy(const SlParams& P, const double* phi, const double* 
     *energy = std::pow(total, 1.0 / p);  // metrics.cpp:142,183
     return LSR_OK;
 #undef EN_TRY
+}
+
+// ---------------------------------------------------------------------------
+// z-slab E_p: the interface cells of the owned cell planes
+// [k_lo, k_hi) and their contributions (ascending global cell order), then
+// the pieces of blocked_sum (parallel.hpp:26-42) this rank can form on its
+// own given the global position `offset` of its first contribution: the
+// sums of the 4096-blocks that lie wholly in its range, and the raw
+// contributions before its first and after its last block boundary. The
+// ranks' pieces, laid end to end, give the reference's block partials bit for
+// bit (the host adds the split blocks serially and then the partials in
+// block order, and applies pow).
+int lsr_energy_slab_cells(const SlParams& P, const double* phi_g, const double* dist_g, int p, int refine, int k_lo,
+                          int k_hi, EnergySlabWork& W, long long* n_cells, cudaStream_t s, std::string* err) {
+#define ES_TRY(x)                                                   \
+    do {                                                            \
+        cudaError_t e_ = (x);                                       \
+        if (e_ != cudaSuccess) {                                    \
+            *err = std::string(#x) + ": " + cudaGetErrorString(e_); \
+            return LSR_ERR_CUDA;                                    \
+        }                                                           \
+    } while (0)
+    if (P.dim != 3 || p < 1 || refine < 1) {
+        *err = "energy slab: 3d grids, p >= 1 and refinement >= 1";
+        return LSR_ERR_CONFIG;
+    }
+    const long long cx = P.nx - 1, cy = P.ny - 1;
+    const long long c0 = static_cast<long long>(k_lo) * cy * cx, c1 = static_cast<long long>(k_hi) * cy * cx;
+    const long long nrange = c1 > c0 ? c1 - c0 : 0;
+    if (c1 > 0x7fffffffLL) {
+        *err = "surface_energy: grids of 2^31 cells or more are not supported";
+        return LSR_ERR_CONFIG;
+    }
+    if (nrange > W.cap) {
+        cudaFree(W.flags);
+        cudaFree(W.cells);
+        cudaFree(W.contrib);
+        W.flags = nullptr;
+        W.cells = nullptr;
+        W.contrib = nullptr;
+        W.cap = 0;
+        ES_TRY(cudaMalloc(&W.flags, nrange + 16));
+        ES_TRY(cudaMalloc(&W.cells, sizeof(int) * nrange));
+        ES_TRY(cudaMalloc(&W.contrib, sizeof(double) * nrange));
+        W.cap = nrange;
+    }
+    const size_t tb = lsr_compact::scratch_bytes(nrange > 0 ? nrange : 1) + sizeof(long long);
+    if (tb > W.tmp_bytes) {
+        cudaFree(W.tmp);
+        W.tmp = nullptr;
+        ES_TRY(cudaMalloc(&W.tmp, tb));
+        W.tmp_bytes = tb;
+    }
+    W.nc = 0;
+    *n_cells = 0;
+    if (nrange == 0) return LSR_OK;
+    unsigned char* flags_g = W.flags - c0;
+    const int T = 256;
+    if (P.nx % 4 == 0) {
+        const unsigned tpr = static_cast<unsigned>((P.nx - 1 + 3) / 4);
+        const long long nt = cy * tpr * ((k_hi - k_lo + kMarchCells - 1) / kMarchCells);
+        flag_cells_march<<<static_cast<unsigned>((nt + T - 1) / T), T, 0, s>>>(P, phi_g, tpr, flags_g, k_lo, k_hi);
+    } else {
+        flag_cells<<<static_cast<unsigned>((nrange + T - 1) / T), T, 0, s>>>(P, phi_g, c0, c1, flags_g);
+    }
+    lsr_note_launch();
+    long long* d_nc = static_cast<long long*>(W.tmp);
+    ES_TRY(lsr_compact::compact(lsr_compact::BytePred<FlagSet>{W.flags, {}}, CellIdFrom{c0}, nrange, W.cells, d_nc,
+                                d_nc + 1, tb - sizeof(long long), s));
+    lsr_note_launch();
+    lsr_note_launch();
+    long long nc = 0;
+    ES_TRY(cudaMemcpyAsync(&nc, d_nc, sizeof nc, cudaMemcpyDeviceToHost, s));
+    ES_TRY(cudaStreamSynchronize(s));
+    if (nc > 0) {
+        const double dxp = P.dx / refine;
+        const double select = std::sqrt(3.0) / 2.0 * dxp;  // metrics.cpp:157
+        if (refine <= kMaxRefine)
+            contrib_3d_hoisted<<<static_cast<unsigned>((nc + LSR_EN_THREADS - 1) / LSR_EN_THREADS), LSR_EN_THREADS, 0,
+                                 s>>>(P, phi_g, dist_g, W.cells, nc, refine, dxp, select, p, W.contrib);
+        else
+            contrib_3d<<<static_cast<unsigned>((nc + 127) / 128), 128, 0, s>>>(P, phi_g, dist_g, W.cells, nc, refine,
+                                                                               dxp, select, p, W.contrib);
+        lsr_note_launch();
+        ES_TRY(cudaGetLastError());
+    }
+    W.nc = nc;
+    *n_cells = nc;
+    return LSR_OK;
+}
+
+int lsr_energy_slab_pieces(EnergySlabWork& W, long long offset, double* h_blocks, long long* n_blocks, double* h_head,
+                           long long* n_head, double* h_tail, long long* n_tail, cudaStream_t s, std::string* err) {
+    const long long nc = W.nc;
+    const long long s0 = (4096 - offset % 4096) % 4096;  // first local index on a block boundary
+    long long head = nc < s0 ? nc : s0, full = 0;
+    if (nc > s0) full = (nc - s0) / 4096;
+    const long long tail0 = head + 4096 * full;
+    *n_head = head;
+    *n_blocks = full;
+    *n_tail = nc - tail0;
+    if (full > 0) {
+        if (full > W.pcap) {
+            cudaFree(W.partial);
+            W.partial = nullptr;
+            ES_TRY(cudaMalloc(&W.partial, sizeof(double) * full));
+            W.pcap = full;
+        }
+        block_partials<<<static_cast<unsigned>(full), 256, 0, s>>>(W.contrib + s0, 4096 * full, W.partial);
+        lsr_note_launch();
+        ES_TRY(cudaMemcpyAsync(h_blocks, W.partial, sizeof(double) * full, cudaMemcpyDeviceToHost, s));
+    }
+    if (head > 0) ES_TRY(cudaMemcpyAsync(h_head, W.contrib, sizeof(double) * head, cudaMemcpyDeviceToHost, s));
+    if (nc - tail0 > 0)
+        ES_TRY(cudaMemcpyAsync(h_tail, W.contrib + tail0, sizeof(double) * (nc - tail0), cudaMemcpyDeviceToHost, s));
+    ES_TRY(cudaStreamSynchronize(s));
+    return LSR_OK;
+#undef ES_TRY
+}
+
+void EnergySlabWork::release() {
+    cudaFree(flags);
+    cudaFree(cells);
+    cudaFree(contrib);
+    cudaFree(partial);
+    cudaFree(tmp);
+    *this = EnergySlabWork{};
 }

@@ -172,6 +172,14 @@ struct lsr_cuda_ctx {
     BandBuffers band;        // last narrow_band built on the device
     ReinitBuffers rb;        // reinitialisation scratch
     double* scratch = nullptr;  // third full-grid field (reinit double buffer)
+    // z-slab context (lsr_cuda_slab_create): fields hold the resident planes
+    // [win_lo, win_hi) of the global grid `grid`; work is done on the owned
+    // planes [own_lo, own_hi); n = resident nodes
+    bool slab = false;
+    int win_lo = 0, win_hi = 0, own_lo = 0, own_hi = 0;
+    EnergySlabWork ew;
+    long long reinit_nn = 0;
+    unsigned long long* d_aux = nullptr;  // [0] halo misses, [1] reach bits
     // pipelined host entry: compute / D2H streams, per-chunk events, miss counter
     cudaStream_t s_cmp = nullptr, s_down = nullptr;
     cudaEvent_t ev_up[32] = {}, ev_cmp[32] = {};
@@ -250,6 +258,7 @@ double** field_slot(lsr_cuda_ctx* c, int which) {
         case LSR_FIELD_PHI: return &c->phi;
         case LSR_FIELD_DIST: return &c->dist;
         case LSR_FIELD_OUT: return &c->out;
+        case LSR_FIELD_SCRATCH: return c->scratch ? &c->scratch : nullptr;  // once allocated
     }
     return nullptr;
 }
@@ -303,6 +312,8 @@ int lsr_cuda_destroy(lsr_cuda_ctx* c) {
     cudaFree(c->dist);
     cudaFree(c->exact);
     cudaFree(c->scratch);
+    c->ew.release();
+    cudaFree(c->d_aux);
     c->band.release();
     c->rb.release();
     cudaFree(c->d_miss);
@@ -1589,6 +1600,246 @@ int lsr_cuda_selftest_weno(double dx, int64_t n, uint64_t seed, int64_t* counts)
     LSR_CUDA_TRY(cudaMemcpy(h, d, sizeof h, cudaMemcpyDeviceToHost));
     cudaFree(d);
     for (int q = 0; q < 4; ++q) counts[q] = static_cast<int64_t>(h[q]);
+    return LSR_OK;
+}
+
+
+// ---------------------------------------------------------------------------
+// z-slab loop: one rank's share of driver.cpp:185-203 on its
+// owned planes; the caller (paper_2410_22205_b200/zslab.py) does the plane
+// exchanges and the reductions between the phases.
+
+static int slab_check(lsr_cuda_ctx* c) {
+    if (!c) return set_err(LSR_ERR_CONFIG, "null context");
+    if (!c->slab) return set_err(LSR_ERR_CONFIG, "slab: not a slab context (lsr_cuda_slab_create)");
+    return LSR_OK;
+}
+
+static long long slab_off(const lsr_cuda_ctx* c) {
+    return static_cast<long long>(c->win_lo) * c->grid.dims[0] * c->grid.dims[1];
+}
+
+int lsr_cuda_slab_create(int device, const lsr_grid* grid, int32_t win_lo, int32_t win_hi, int32_t own_lo,
+                         int32_t own_hi, lsr_cuda_ctx** out) {
+    if (!out) return set_err(LSR_ERR_CONFIG, "slab_create: null out");
+    *out = nullptr;
+    if (int st = check_grid(grid)) return st;
+    const int nz = grid->dims[2];
+    if (grid->dim != 3 || own_lo < 0 || own_hi > nz || own_lo >= own_hi || win_lo > std::max(own_lo - 1, 0) ||
+        win_hi < std::min(own_hi + 1, nz) || win_lo < 0 || win_hi > nz)
+        return set_err(LSR_ERR_CONFIG,
+                       "slab_create: need a 3d grid and 0 <= win_lo <= own_lo - 1 < own_hi + 1 <= win_hi <= nz");
+    const long long nxy = static_cast<long long>(grid->dims[0]) * grid->dims[1];
+    if (nxy % 16 != 0) return set_err(LSR_ERR_CONFIG, "slab_create: planes must hold a multiple of 16 nodes");
+    LSR_CUDA_TRY(cudaSetDevice(device));
+    auto* c = new lsr_cuda_ctx;
+    c->device = device;
+    c->grid = *grid;
+    c->slab = true;
+    c->win_lo = win_lo;
+    c->win_hi = win_hi;
+    c->own_lo = own_lo;
+    c->own_hi = own_hi;
+    c->n = static_cast<int64_t>(win_hi - win_lo) * nxy;
+    const size_t bytes = sizeof(double) * static_cast<size_t>(c->n);
+    cudaError_t e = cudaSuccess;
+    if (e == cudaSuccess) e = cudaMalloc(&c->phi, bytes);
+    if (e == cudaSuccess) e = cudaMalloc(&c->out, bytes);
+    if (e == cudaSuccess) e = cudaMalloc(&c->dist, bytes);
+    if (e == cudaSuccess) e = cudaMalloc(&c->scratch, bytes);
+    if (e == cudaSuccess) e = cudaMalloc(&c->d_bad, sizeof(unsigned long long));
+    if (e == cudaSuccess) e = cudaMalloc(&c->d_aux, 2 * sizeof(unsigned long long));
+    if (e == cudaSuccess) e = cudaMallocHost(&c->h_bad, sizeof(unsigned long long));
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking);
+    for (int i = 0; i < 4 && e == cudaSuccess; ++i) e = cudaEventCreate(&c->ev[i]);
+    if (e != cudaSuccess) {
+        lsr_cuda_destroy(c);
+        return cuda_err(e, "lsr_cuda_slab_create");
+    }
+    c->stream = c->own;
+    *out = c;
+    return LSR_OK;
+}
+
+int lsr_cuda_slab_copy_planes(lsr_cuda_ctx* c, int which, int32_t plane0, int32_t nplanes, void* dev,
+                              int32_t to_field) {
+    if (int st = slab_check(c)) return st;
+    double** slot = field_slot(c, which);
+    if (!slot || !dev || nplanes < 0 || plane0 < c->win_lo || plane0 + nplanes > c->win_hi)
+        return set_err(LSR_ERR_CONFIG, "slab_copy_planes: bad field or planes outside the resident window");
+    LSR_CUDA_TRY(cudaSetDevice(c->device));
+    const long long nxy = static_cast<long long>(c->grid.dims[0]) * c->grid.dims[1];
+    double* f = *slot + (static_cast<long long>(plane0) - c->win_lo) * nxy;
+    const size_t bytes = sizeof(double) * static_cast<size_t>(nplanes) * nxy;
+    if (bytes == 0) return LSR_OK;
+    if (to_field) LSR_CUDA_TRY(cudaMemcpyAsync(f, dev, bytes, cudaMemcpyDeviceToDevice, c->stream));
+    else LSR_CUDA_TRY(cudaMemcpyAsync(dev, f, bytes, cudaMemcpyDeviceToDevice, c->stream));
+    LSR_CUDA_TRY(cudaStreamSynchronize(c->stream));
+    if (to_field && which != LSR_FIELD_DIST) c->consistent = false;
+    return LSR_OK;
+}
+
+int lsr_cuda_slab_band(lsr_cuda_ctx* c, int which, double gamma, int64_t* n_active, int64_t* n_tube) {
+    if (int st = slab_check(c)) return st;
+    double** slot = field_slot(c, which);
+    if (!slot || which == LSR_FIELD_DIST) return set_err(LSR_ERR_CONFIG, "slab_band: phi must be PHI or OUT");
+    LSR_CUDA_TRY(cudaSetDevice(c->device));
+    std::string err;
+    long long na = 0, nt = 0;
+    if (int st = lsr_band_build_slab(grid_params(c->grid), *slot - slab_off(c), gamma, c->band, c->win_lo, c->win_hi,
+                                     c->own_lo, c->own_hi, &na, &nt, c->stream, &err))
+        return set_err(st, err);
+    if (int st = ensure_ids(&c->active, &c->cap_active, na)) return st;
+    if (na > 0)
+        LSR_CUDA_TRY(cudaMemcpyAsync(c->active, c->band.active, sizeof(int64_t) * na, cudaMemcpyDeviceToDevice,
+                                     c->stream));
+    c->n_active = na;
+    if (n_active) *n_active = na;
+    if (n_tube) *n_tube = nt;
+    return LSR_OK;
+}
+
+int lsr_cuda_slab_energy_cells(lsr_cuda_ctx* c, int which, int p, int refine, int64_t* n_cells) {
+    if (int st = slab_check(c)) return st;
+    double** slot = field_slot(c, which);
+    if (!slot || which == LSR_FIELD_DIST) return set_err(LSR_ERR_CONFIG, "slab_energy: phi must be PHI or OUT");
+    LSR_CUDA_TRY(cudaSetDevice(c->device));
+    std::string err;
+    long long nc = 0;
+    const int k_hi = std::min(c->own_hi, c->grid.dims[2] - 1);  // cells (k, k+1) of the owned planes
+    const long long off = slab_off(c);
+    if (int st = lsr_energy_slab_cells(grid_params(c->grid), *slot - off, c->dist - off, p, refine, c->own_lo,
+                                       std::max(k_hi, c->own_lo), c->ew, &nc, c->stream, &err))
+        return set_err(st, err);
+    if (n_cells) *n_cells = nc;
+    return LSR_OK;
+}
+
+int lsr_cuda_slab_energy_pieces(lsr_cuda_ctx* c, int64_t offset, double* blocks, int64_t* n_blocks, double* head,
+                                int64_t* n_head, double* tail, int64_t* n_tail) {
+    if (int st = slab_check(c)) return st;
+    if (!blocks || !head || !tail || !n_blocks || !n_head || !n_tail || offset < 0)
+        return set_err(LSR_ERR_CONFIG, "slab_energy_pieces: null argument");
+    LSR_CUDA_TRY(cudaSetDevice(c->device));
+    std::string err;
+    long long nb = 0, nh = 0, nt = 0;
+    if (int st = lsr_energy_slab_pieces(c->ew, offset, blocks, &nb, head, &nh, tail, &nt, c->stream, &err))
+        return set_err(st, err);
+    *n_blocks = nb;
+    *n_head = nh;
+    *n_tail = nt;
+    return LSR_OK;
+}
+
+int lsr_cuda_slab_max_reach(lsr_cuda_ctx* c, const lsr_step_cfg* cfg, double energy_p, double* cells) {
+    if (int st = slab_check(c)) return st;
+    if (int st = check_cfg(cfg, energy_p)) return st;
+    if (!cells) return set_err(LSR_ERR_CONFIG, "slab_max_reach: null argument");
+    LSR_CUDA_TRY(cudaSetDevice(c->device));
+    SlParams P = make_params(c->grid, *cfg, energy_p);
+    LSR_CUDA_TRY(cudaMemsetAsync(c->d_aux + 1, 0, sizeof(unsigned long long), c->stream));
+    LSR_CUDA_TRY(launch_reach_max(P, c->dist - slab_off(c), c->active, c->n_active, c->d_aux + 1, c->stream));
+    unsigned long long bits = 0;
+    LSR_CUDA_TRY(cudaMemcpyAsync(&bits, c->d_aux + 1, sizeof bits, cudaMemcpyDeviceToHost, c->stream));
+    LSR_CUDA_TRY(cudaStreamSynchronize(c->stream));
+    std::memcpy(cells, &bits, sizeof bits);
+    return LSR_OK;
+}
+
+int lsr_cuda_slab_sl_step(lsr_cuda_ctx* c, const lsr_step_cfg* cfg, double energy_p, int64_t* bad_node,
+                          int64_t* halo_miss) {
+    if (bad_node) *bad_node = -1;
+    if (halo_miss) *halo_miss = 0;
+    if (int st = slab_check(c)) return st;
+    if (int st = check_cfg(cfg, energy_p)) return st;
+    LSR_CUDA_TRY(cudaSetDevice(c->device));
+    cudaStream_t s = c->stream;
+    // out = phi on every resident node (evolve.cpp:50), then the owned active updates
+    LSR_CUDA_TRY(cudaMemcpyAsync(c->out, c->phi, sizeof(double) * c->n, cudaMemcpyDeviceToDevice, s));
+    LSR_CUDA_TRY(cudaMemsetAsync(c->d_bad, 0xff, sizeof(unsigned long long), s));
+    LSR_CUDA_TRY(cudaMemsetAsync(c->d_aux, 0, sizeof(unsigned long long), s));
+    if (!(cfg->p > 1 && energy_p == 0.0) && c->n_active > 0) {  // driver.cpp:191-195
+        SlParams P = make_params(c->grid, *cfg, energy_p);
+        P.z_base = c->win_lo;
+        P.z_planes = c->win_hi - c->win_lo;
+        P.own_lo = c->own_lo;
+        P.own_hi = c->own_hi;
+        P.halo_miss = c->d_aux;
+        const long long off = slab_off(c);
+        if (int st = attach_slab_table(P, c->grid, cfg->interp, c->phi - off, c->dist - off, c->active, c->n_active, s))
+            return st;
+        LSR_CUDA_TRY(launch_sl_step(P, cfg->interp, c->phi - off, c->dist - off, c->active, c->n_active, c->out - off,
+                                    c->d_bad, s));
+    }
+    unsigned long long h[2] = {0, 0};
+    LSR_CUDA_TRY(cudaMemcpyAsync(&h[0], c->d_bad, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+    LSR_CUDA_TRY(cudaMemcpyAsync(&h[1], c->d_aux, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+    LSR_CUDA_TRY(cudaStreamSynchronize(s));
+    c->consistent = false;
+    if (halo_miss) *halo_miss = static_cast<int64_t>(h[1]);
+    if (h[0] != ~0ULL) return numerical_error(c->grid, h[0], bad_node);
+    return LSR_OK;
+}
+
+int lsr_cuda_slab_one_step(lsr_cuda_ctx* c, int* any_frozen, int* any_zero) {
+    if (int st = slab_check(c)) return st;
+    if (!any_frozen || !any_zero) return set_err(LSR_ERR_CONFIG, "slab_one_step: null argument");
+    LSR_CUDA_TRY(cudaSetDevice(c->device));
+    std::string err;
+    const long long off = slab_off(c);
+    if (int st = lsr_reinit_one_step_slab(grid_params(c->grid), c->out - off, c->scratch - off, c->rb, c->win_lo,
+                                          c->win_hi, c->own_lo, c->own_hi, any_frozen, any_zero, c->stream, &err))
+        return set_err(st, err);
+    return LSR_OK;
+}
+
+int lsr_cuda_slab_reinit_begin(lsr_cuda_ctx* c, const lsr_reinit_cfg* rc, int64_t* n_nodes) {
+    if (int st = slab_check(c)) return st;
+    if (!rc || !n_nodes) return set_err(LSR_ERR_CONFIG, "slab_reinit_begin: null argument");
+    if (!c->band.state) return set_err(LSR_ERR_CONFIG, "slab_reinit_begin: build the band first (lsr_cuda_slab_band)");
+    if (!(rc->dtau > 0.0) || rc->max_iters < 1) return set_err(LSR_ERR_CONFIG, "reinit: bad configuration");
+    LSR_CUDA_TRY(cudaSetDevice(c->device));
+    std::string err;
+    const ReinitParams R{rc->dtau, rc->max_iters, rc->residual_tol, rc->sign_eps};
+    const long long off = slab_off(c);
+    long long nn = 0;
+    if (int st = lsr_reinit_slab_begin(grid_params(c->grid), c->scratch - off, c->out - off, c->band.tube,
+                                       c->band.n_tube, R, c->rb, c->win_lo, c->win_hi, &nn, c->stream, &err))
+        return set_err(st, err);
+    c->reinit_nn = nn;
+    *n_nodes = nn;
+    return LSR_OK;
+}
+
+// sweep k reads buf[k & 1] and writes buf[(k + 1) & 1], buf = {SCRATCH, OUT}
+int lsr_cuda_slab_reinit_sweep(lsr_cuda_ctx* c, const lsr_reinit_cfg* rc, int32_t k, double* residual) {
+    if (int st = slab_check(c)) return st;
+    if (!rc || !residual || k < 0) return set_err(LSR_ERR_CONFIG, "slab_reinit_sweep: bad argument");
+    LSR_CUDA_TRY(cudaSetDevice(c->device));
+    std::string err;
+    const long long off = slab_off(c);
+    double* buf[2] = {c->scratch - off, c->out - off};
+    if (int st = lsr_reinit_slab_sweep(grid_params(c->grid), buf[k & 1], buf[(k + 1) & 1], c->rb, c->reinit_nn,
+                                       rc->dtau, residual, c->stream, &err))
+        return set_err(st, err);
+    return LSR_OK;
+}
+
+// the reinitialised field is `which` (SCRATCH or OUT): clamp its owned
+// planes (reinit.cpp:143) and make it the context's OUT field
+int lsr_cuda_slab_reinit_end(lsr_cuda_ctx* c, int which, double gamma) {
+    if (int st = slab_check(c)) return st;
+    if (which != LSR_FIELD_SCRATCH && which != LSR_FIELD_OUT)
+        return set_err(LSR_ERR_CONFIG, "slab_reinit_end: the result is SCRATCH or OUT");
+    LSR_CUDA_TRY(cudaSetDevice(c->device));
+    if (which == LSR_FIELD_SCRATCH) std::swap(c->out, c->scratch);
+    const long long nxy = static_cast<long long>(c->grid.dims[0]) * c->grid.dims[1];
+    std::string err;
+    if (int st = lsr_clamp(c->out + (static_cast<long long>(c->own_lo) - c->win_lo) * nxy,
+                           static_cast<long long>(c->own_hi - c->own_lo) * nxy, gamma, c->stream, &err))
+        return set_err(st, err);
+    LSR_CUDA_TRY(cudaStreamSynchronize(c->stream));
+    c->consistent = false;
     return LSR_OK;
 }
 

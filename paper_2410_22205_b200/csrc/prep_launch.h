@@ -28,3 +28,21 @@ int lsr_prep_surface_energy(const lsr_dev::SlParams& P, const double* phi, const
 // lsr::compute_stats (cloud.cpp:480-489) with the NN sample on the device.
 int lsr_prep_compute_stats(const double* h_pts, int64_t n, int dim, double fraction, double k_s, uint64_t seed,
                            double* h_s, double* gamma_s, double* bbox6, cudaStream_t s, std::string* err);
+
+// z-slab surface energy (energy.cu): contributions of the owned cell planes
+// [k_lo, k_hi), then this rank's pieces of blocked_sum given its global offset
+struct EnergySlabWork {
+    unsigned char* flags = nullptr;
+    int* cells = nullptr;
+    double* contrib = nullptr;
+    double* partial = nullptr;
+    void* tmp = nullptr;
+    size_t tmp_bytes = 0;
+    long long cap = 0, pcap = 0, nc = 0;
+    void release();
+};
+int lsr_energy_slab_cells(const lsr_dev::SlParams& P, const double* phi_g, const double* dist_g, int p, int refine,
+                          int k_lo, int k_hi, EnergySlabWork& W, long long* n_cells, cudaStream_t s,
+                          std::string* err);
+int lsr_energy_slab_pieces(EnergySlabWork& W, long long offset, double* h_blocks, long long* n_blocks, double* h_head,
+                           long long* n_head, double* h_tail, long long* n_tail, cudaStream_t s, std::string* err);

@@ -62,6 +62,8 @@ cudaError_t launch_zt_bricks(const lsr_dev::SlParams& P, const double* dist, con
 cudaError_t launch_zt_fill(const lsr_dev::SlParams& P, const double* phi, const ZtBuffers& Z, cudaStream_t stream);
 
 cudaError_t launch_check_sorted(const int64_t* ids, long long n, unsigned long long* bad, cudaStream_t stream);
+cudaError_t launch_reach_max(const lsr_dev::SlParams& P, const double* dist, const int64_t* active, long long n,
+                             unsigned long long* max_bits, cudaStream_t stream);
 cudaError_t launch_check_ids(const int64_t* ids, long long n, long long n_nodes, unsigned long long* bad,
                              cudaStream_t stream);
 

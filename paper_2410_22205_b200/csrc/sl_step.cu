@@ -163,6 +163,35 @@ __global__ void zt_reach_kernel(SlParams P, const double* __restrict__ dist, con
     if (b >= 0 && (threadIdx.x & 31) == static_cast<unsigned>(__ffs(same) - 1)) atomicMax(reach + b, rmax);
 }
 
+// the largest foot displacement bound (cells, as zt_reach_kernel) over the
+// ids: *max_bits = max of the non-negative double bits (integer order =
+// double order). A z-slab sizes its halo planes from the max over ranks.
+__global__ void reach_max_kernel(SlParams P, const double* __restrict__ dist, const int64_t* __restrict__ active,
+                                 long long n, unsigned long long* __restrict__ max_bits) {
+    const long long a = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    unsigned long long b = 0;
+    if (a < n) {
+        const long long id = __ldg(active + a);
+        int i, j, k;
+        unflatten(P, id, i, j, k);
+        const double d_j = __ldg(dist + id);
+        const double c_j = P.p == 1 ? 1.0 : d_j / P.energy;
+        const double s = c_j * P.dt;
+        const double spread = sqrt(fmax(0.0, c_j * P.delta * d_j * P.dt / P.pd));
+        double m = fabs(s * grad_axis(P, dist, id, i, P.nx, 1));
+        m = fmax(m, fabs(s * grad_axis(P, dist, id, j, P.ny, P.nx)));
+        if (P.dim == 3) m = fmax(m, fabs(s * grad_axis(P, dist, id, k, P.nz, P.nxy)));
+        double cells = (m + 1.4143 * spread) / P.dx;
+        if (!(cells >= 0.0)) cells = 1e300;  // NaN / inf d: no finite halo covers it
+        b = static_cast<unsigned long long>(__double_as_longlong(cells));
+    }
+    for (int off = 16; off > 0; off >>= 1) {
+        const unsigned long long o = __shfl_xor_sync(0xffffffffu, b, off);
+        b = o > b ? o : b;
+    }
+    if ((threadIdx.x & 31) == 0 && b) atomicMax(max_bits, b);
+}
+
 __device__ __forceinline__ int floor_div(int a, int b) { return a >= 0 ? a / b : -((-a + b - 1) / b); }
 
 // a brick b0 whose feet reach [i - rn, i + rp] reads table nodes x, y in
@@ -513,6 +542,14 @@ cudaError_t launch_zt_fill(const SlParams& P, const double* phi, const ZtBuffers
 cudaError_t launch_check_sorted(const int64_t* ids, long long n, unsigned long long* bad, cudaStream_t stream) {
     if (n <= 1) return cudaSuccess;
     check_sorted_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, stream>>>(ids, n, bad);
+    lsr_note_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_reach_max(const SlParams& P, const double* dist, const int64_t* active, long long n,
+                             unsigned long long* max_bits, cudaStream_t stream) {
+    if (n <= 0) return cudaSuccess;
+    reach_max_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, stream>>>(P, dist, active, n, max_bits);
     lsr_note_launch();
     return cudaGetLastError();
 }

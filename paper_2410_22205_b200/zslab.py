@@ -163,3 +163,287 @@ class SlabStepper:
             exchange_halo(self.dist, self.out, self.s, self.halo)
         self.phi, self.out = self.out, self.phi
         return 0
+
+
+# ---------------------------------------------------------------------------
+# The whole loop over z-slabs (driver.cpp:185-203 on each rank's owned
+# planes). One iteration is written once, as a generator over one rank's
+# SlabContext that yields its collective requests:
+#   ("allgather", obj) -> list of every rank's obj
+#   ("allreduce_max", x) -> max over ranks
+#   ("exchange", field, h) -> h halo planes of `field` swapped with both neighbours
+# A runner serves the requests: DistRunner over torch.distributed (one rank
+# per process, NCCL between GPUs or gloo), or InProcessRunner, which steps
+# several ranks' generators in lockstep in one process (one GPU, ranks run
+# one after another, the exchanges are device copies) — the same per-rank
+# code either way. Every phase gives the owned nodes the bits the
+# whole-grid loop gives them (band, E_2 via the ranks' blocked_sum pieces,
+# SL, one-step, the Jacobi sweeps with a global stop rule, clamp).
+
+FIELD_PHI, FIELD_DIST, FIELD_OUT, FIELD_SCRATCH = 0, 1, 2, 3
+BLOCK = 4096  # blocked_sum's block (parallel.hpp:28)
+
+
+class HaloTooSmall(Exception):
+    """The feet of some rank reach beyond the resident planes: widen and redo."""
+
+    def __init__(self, need: int):
+        super().__init__(f"halo too small: need {need} planes")
+        self.need = need
+
+
+def blocked_sum_pieces(pieces) -> float:
+    """blocked_sum (parallel.hpp:26-42) of the concatenation of the ranks'
+    contribution lists, from each rank's (full-block sums, head, tail): raw
+    contributions are added serially inside their block, block partials in
+    block order — the reference's exact operation sequence."""
+    total, acc, pos = 0.0, 0.0, 0
+
+    def raw(vals):
+        nonlocal total, acc, pos
+        for v in vals:
+            acc += float(v)
+            pos += 1
+            if pos % BLOCK == 0:
+                total += acc
+                acc = 0.0
+
+    for blocks, head, tail in pieces:
+        raw(head)
+        for b in blocks:
+            assert pos % BLOCK == 0
+            total += float(b)
+            pos += BLOCK
+        raw(tail)
+    if pos % BLOCK:
+        total += acc
+    return total
+
+
+def loop_iteration(ctx, rank: int, cfg, rcfg, gamma: float, refine: int, halo: int, energy_override=None):
+    """One driver iteration on one rank's SlabContext (a generator yielding
+    collective requests; returns the iteration's statistics). Raises
+    HaloTooSmall (on every rank alike) before anything is committed when the
+    feet may leave the resident planes."""
+    import math
+
+    na, nt = ctx.band(gamma, FIELD_PHI)  # driver.cpp:187
+    if energy_override is None:  # driver.cpp:188, metrics.cpp:186-189
+        nc = ctx.energy_cells(FIELD_PHI, 2, refine)
+        counts = yield ("allgather", nc)
+        pieces = ctx.energy_pieces(sum(counts[:rank]))
+        e2 = math.pow(blocked_sum_pieces((yield ("allgather", pieces))), 1.0 / 2)
+    else:
+        e2 = float(energy_override)
+    skip_sl = cfg.p > 1 and e2 == 0.0  # driver.cpp:191-195
+    if not skip_sl:
+        reach = yield ("allreduce_max", ctx.max_reach(cfg, e2) if na else 0.0)
+        need = halo_planes(reach * ctx.grid.dx, ctx.grid.dx, int(cfg.interp))
+        if need > halo:
+            raise HaloTooSmall(need)
+    miss = ctx.sl_step(cfg, e2)
+    if (yield ("allreduce_max", miss)):
+        raise HaloTooSmall(halo + 2)
+    yield ("exchange", FIELD_OUT, 1)
+    # reinitialize (reinit.cpp:133-145) of phi^{n+1} on the band of phi^n
+    frozen, zero = ctx.one_step()
+    had = bool((yield ("allreduce_max", int(frozen or zero))))
+    it = 0
+    result = FIELD_OUT  # NoInterfaceError: phi^{n+1} unchanged, then clamped
+    if had:
+        yield ("exchange", FIELD_SCRATCH, 1)
+        ctx.reinit_begin(rcfg)
+        tol = rcfg.residual_tol * ctx.grid.dx
+        for k in range(rcfg.max_iters):  # reinit.cpp:110-130
+            r = yield ("allreduce_max", ctx.reinit_sweep(rcfg, k))
+            it = k + 1
+            if r < tol:
+                break
+            yield ("exchange", FIELD_SCRATCH if it % 2 == 0 else FIELD_OUT, 1)
+        result = FIELD_SCRATCH if it % 2 == 0 else FIELD_OUT
+    ctx.reinit_end(result, gamma)
+    yield ("exchange", FIELD_OUT, halo)
+    ctx.swap()  # driver.cpp:203
+    return dict(energy=e2, n_active=na, n_tube=nt, reinit_iterations=it, had_interface=had)
+
+
+def _exchange_pairs(ranks, h):
+    """(src rank, dst rank, first plane, planes) of a halo exchange of h planes."""
+    for r in range(len(ranks) - 1):
+        lo, hi = ranks[r], ranks[r + 1]
+        yield r + 1, r, hi.own_lo, min(h, hi.own_hi - hi.own_lo)      # upper's bottom planes -> lower's top halo
+        yield r, r + 1, lo.own_hi - min(h, lo.own_hi - lo.own_lo), min(h, lo.own_hi - lo.own_lo)
+
+
+class InProcessRunner:
+    """Runs the ranks of one job in this process (one GPU): every rank's
+    generator is advanced to its next collective request, the request is
+    served for all ranks together, and the results are sent back."""
+
+    def __init__(self, ctxs):
+        self.ctxs = ctxs
+
+    def exchange(self, field, h):
+        for src, dst, p0, n in _exchange_pairs(self.ctxs, h):
+            if n > 0:
+                s, d = self.ctxs[src], self.ctxs[dst]
+                d.copy_planes(field, p0, n, s.plane_ptr(field, p0), to_field=True)
+
+    def run(self, gens):
+        vals = [None] * len(gens)
+        done = [None] * len(gens)
+        while True:
+            reqs = []
+            for r, g in enumerate(gens):
+                try:
+                    reqs.append(g.send(vals[r]))
+                except StopIteration as e:
+                    done[r] = e.value
+                    reqs.append(None)
+            if all(q is None for q in reqs):
+                return done
+            if any(q is None for q in reqs) or len({q[0] for q in reqs}) != 1:
+                raise RuntimeError(f"ranks out of step: {[q and q[0] for q in reqs]}")
+            kind = reqs[0][0]
+            if kind == "allgather":
+                allv = [q[1] for q in reqs]
+                vals = [allv] * len(gens)
+            elif kind == "allreduce_max":
+                m = max(q[1] for q in reqs)
+                vals = [m] * len(gens)
+            elif kind == "exchange":
+                self.exchange(reqs[0][1], reqs[0][2])
+                vals = [None] * len(gens)
+            else:
+                raise RuntimeError(kind)
+
+
+class DistRunner:
+    """Serves one rank's requests over torch.distributed (NCCL between GPUs,
+    or gloo): plane exchanges through device staging buffers and
+    send/recv, reductions and gathers as collectives."""
+
+    def __init__(self, dist, ctx, cuts):
+        import torch
+
+        self.dist, self.ctx, self.torch = dist, ctx, torch
+        self.rank, self.world = dist.get_rank(), dist.get_world_size()
+        self.cuts = cuts
+        self.dev = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend() == "nccl" else None
+
+    def exchange(self, field, h):
+        torch, dist, c = self.torch, self.dist, self.ctx
+        nxy = c.nxy
+        ops, recvs = [], []
+        for nb, mine0, theirs0, n in self._neighbours(h):
+            send = torch.empty(n * nxy, dtype=torch.float64, device="cuda")
+            c.copy_planes(field, mine0, n, send.data_ptr(), to_field=False)
+            recv = torch.empty(n * nxy, dtype=torch.float64, device="cuda")
+            ops += [dist.P2POp(dist.isend, send, nb), dist.P2POp(dist.irecv, recv, nb)]
+            recvs.append((theirs0, n, recv))
+        if ops:
+            torch.cuda.synchronize()
+            for q in dist.batch_isend_irecv(ops):
+                q.wait()
+            torch.cuda.synchronize()
+        for p0, n, buf in recvs:
+            c.copy_planes(field, p0, n, buf.data_ptr(), to_field=True)
+
+    def _neighbours(self, h):
+        """(neighbour rank, my first plane to send, first halo plane to receive, planes)"""
+        r, cuts = self.rank, self.cuts
+        out = []
+        if r > 0:
+            n = min(h, cuts[r + 1] - cuts[r], cuts[r] - cuts[r - 1])
+            out.append((r - 1, cuts[r], cuts[r] - n, n))
+        if r < self.world - 1:
+            n = min(h, cuts[r + 1] - cuts[r], cuts[r + 2] - cuts[r + 1])
+            out.append((r + 1, cuts[r + 1] - n, cuts[r + 1], n))
+        return out
+
+    def run(self, gen):
+        torch, dist = self.torch, self.dist
+        val = None
+        while True:
+            try:
+                q = gen.send(val)
+            except StopIteration as e:
+                return e.value
+            if q[0] == "allgather":
+                out = [None] * self.world
+                dist.all_gather_object(out, q[1])
+                val = out
+            elif q[0] == "allreduce_max":
+                t = torch.tensor([float(q[1])], dtype=torch.float64, device=self.dev or "cpu")
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                val = float(t.item())
+            elif q[0] == "exchange":
+                self.exchange(q[1], q[2])
+                val = None
+            else:
+                raise RuntimeError(q[0])
+
+
+class SlabLoop:
+    """The loop over all ranks of one process (InProcessRunner) or this
+    process's rank (DistRunner). make_ctx(win_lo, win_hi, own_lo, own_hi)
+    creates a SlabContext; fill(ctx) uploads phi^0 and d for its window. On
+    HaloTooSmall every rank widens its window (phi carried over, d
+    refilled) and redoes the iteration."""
+
+    def __init__(self, grid, cuts, ranks, halo, make_ctx, fill_dist, runner_factory):
+        self.grid, self.cuts, self.ranks, self.halo = grid, list(int(c) for c in cuts), list(ranks), int(halo)
+        self.make_ctx, self.fill_dist, self.runner_factory = make_ctx, fill_dist, runner_factory
+        self._check_halo()
+        self.ctxs = [self._new_ctx(r) for r in self.ranks]
+        self.runner = runner_factory(self.ctxs)
+        self.regrows = 0
+
+    def _check_halo(self):
+        thin = min(b - a for a, b in zip(self.cuts[:-1], self.cuts[1:]))
+        if len(self.cuts) > 2 and thin < self.halo:
+            raise ValueError(f"slabs of {thin} planes cannot feed halos of {self.halo} planes (one hop only)")
+
+    def window(self, r):
+        nz = self.grid.dims[2]
+        return max(0, self.cuts[r] - self.halo), min(nz, self.cuts[r + 1] + self.halo), self.cuts[r], self.cuts[r + 1]
+
+    def _new_ctx(self, r):
+        c = self.make_ctx(*self.window(r))
+        self.fill_dist(c)
+        return c
+
+    def upload_phi(self, phi_window_of):
+        for r, c in zip(self.ranks, self.ctxs):
+            c.upload(FIELD_PHI, phi_window_of(c))
+
+    def widen(self, need):
+        old = self.ctxs
+        self.halo = max(need, self.halo + 1)
+        self._check_halo()
+        self.ctxs = [self._new_ctx(r) for r in self.ranks]
+        for o, c in zip(old, self.ctxs):  # the owned planes of phi^n carry over, the halo comes by exchange
+            c.copy_planes(FIELD_PHI, o.own_lo, o.own_hi - o.own_lo, o.plane_ptr(FIELD_PHI, o.own_lo), to_field=True)
+            o.close()
+        self.runner = self.runner_factory(self.ctxs)
+        self._exchange_phi()
+        self.regrows += 1
+
+    def _exchange_phi(self):
+        def g(c):
+            yield ("exchange", FIELD_PHI, self.halo)
+        self._run([g(c) for c in self.ctxs])
+
+    def _run(self, gens):
+        if isinstance(self.runner, InProcessRunner):
+            return self.runner.run(gens)
+        return [self.runner.run(gens[0])]
+
+    def step(self, cfg, rcfg, gamma, refine=5, energy_override=None):
+        while True:
+            gens = [loop_iteration(c, r, cfg, rcfg, gamma, refine, self.halo, energy_override)
+                    for r, c in zip(self.ranks, self.ctxs)]
+            try:
+                return self._run(gens)
+            except HaloTooSmall as e:
+                self.widen(e.need)

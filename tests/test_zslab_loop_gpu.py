@@ -1,0 +1,91 @@
+"""The whole loop over z-slabs (driver.cpp:185-203 split over
+ranks, paper_2410_22205_b200.zslab.SlabLoop): 2 and 3 slabs run in one
+process on one GPU (InProcessRunner: the ranks advance in lockstep, the halo
+exchanges are device copies, no kernel waits on another rank) must give the
+bits of the single-GPU loop (Context.loop_step) after every iteration —
+phi on every owned plane, E_2, |active|, |tube| and the reinit sweep count —
+including a run that starts with too small a halo and widens it."""
+import numpy as np
+import pytest
+
+from conftest import bits
+
+pytestmark = pytest.mark.gpu
+
+
+def _case(lsr, dims, seed=7):
+    g = lsr.Grid(3, (-1.0, -1.0, -1.0), 2.0 / (max(dims) - 1), tuple(dims))
+    x, y, z = g.mesh()
+    r = np.sqrt(x * x + y * y + z * z)
+    rng = np.random.default_rng(seed)
+    bump = 0.04 * np.sin(5 * x + rng.uniform()) * np.cos(3 * y)
+    phi0 = (r - 0.9 + bump).ravel()
+    dist = (np.abs(np.sqrt((x - 0.03) ** 2 + y * y + (z + 0.02) ** 2) - 0.5) + 1e-3 * np.cos(17 * r)).ravel()
+    return g, phi0, dist
+
+
+def _single(lsr, g, phi0, dist, cfg, rcfg, iters):
+    ctx = lsr.Context(g)
+    ctx.upload(0, phi0)
+    ctx.upload(1, dist)
+    stats, fields = [], []
+    for _ in range(iters):
+        stats.append(ctx.loop_step(cfg, rcfg, 5))
+        fields.append(ctx.download(0).copy())
+    ctx.close()
+    return stats, fields
+
+
+def _sharded(lsr, g, phi0, dist, cfg, rcfg, iters, world, halo):
+    from paper_2410_22205_b200 import zslab
+
+    nz, nxy = g.dims[2], g.dims[0] * g.dims[1]
+    band = np.flatnonzero(np.abs(phi0) < cfg.band.gamma)
+    cuts = zslab.plan_cuts(band, nxy, nz, world, min_planes=max(halo, 8))
+
+    def make_ctx(wl, wh, ol, oh):
+        return lsr.SlabContext(g, wl, wh, ol, oh)
+
+    def fill(c):
+        c.upload(1, dist[c.win_lo * nxy:c.win_hi * nxy])
+
+    loop = zslab.SlabLoop(g, cuts, range(world), halo, make_ctx, fill, zslab.InProcessRunner)
+    loop.upload_phi(lambda c: phi0[c.win_lo * nxy:c.win_hi * nxy])
+    stats, fields = [], []
+    for _ in range(iters):
+        st = loop.step(cfg, rcfg, cfg.band.gamma)
+        assert len({(s["energy"], s["reinit_iterations"], s["had_interface"]) for s in st}) == 1
+        stats.append(dict(energy=st[0]["energy"], n_active=sum(s["n_active"] for s in st),
+                          n_tube=sum(s["n_tube"] for s in st), reinit_iterations=st[0]["reinit_iterations"]))
+        full = np.empty(g.num_nodes())
+        for c in loop.ctxs:
+            w = c.download(0)
+            full[c.own_lo * nxy:c.own_hi * nxy] = w[(c.own_lo - c.win_lo) * nxy:(c.own_hi - c.win_lo) * nxy]
+        fields.append(full)
+    return stats, fields, loop
+
+
+@pytest.mark.parametrize("dims,interp,world,halo", [
+    ((64, 64, 64), 1, 2, 6),
+    ((64, 64, 64), 1, 3, 6),
+    ((40, 48, 56), 0, 2, 5),    # nx % 16 != 0: the scalar band passes
+    ((64, 64, 64), 1, 2, 3),    # too small a halo: widened and redone
+])
+def test_slab_loop_matches_single_gpu_loop(gpu, dims, interp, world, halo):
+    lsr = gpu
+    g, phi0, dist = _case(lsr, dims)
+    bp = lsr.default_band_params(3, g.dx)
+    cfg = lsr.StepConfig(p=2, delta=1.0, dt=0.25 * g.dx, band=bp, interp=lsr.InterpolatorKind(interp))
+    rcfg = lsr.ReinitConfig.defaults(g.dx, bp.gamma)
+    iters = 4
+    ref_stats, ref_fields = _single(lsr, g, phi0, dist, cfg, rcfg, iters)
+    stats, fields, loop = _sharded(lsr, g, phi0, dist, cfg, rcfg, iters, world, halo)
+    for n in range(iters):
+        for key in ("energy", "n_active", "n_tube", "reinit_iterations"):
+            assert stats[n][key] == ref_stats[n][key], (n, key, stats[n][key], ref_stats[n][key])
+        diff = np.count_nonzero(bits(fields[n]) != bits(ref_fields[n]))
+        assert diff == 0, f"iteration {n + 1}: {diff} nodes differ"
+    if halo == 3:
+        assert loop.regrows >= 1
+    for c in loop.ctxs:
+        c.close()
