@@ -329,23 +329,29 @@ class DistRunner:
         self.dist, self.ctx, self.torch = dist, ctx, torch
         self.rank, self.world = dist.get_rank(), dist.get_world_size()
         self.cuts = cuts
-        self.dev = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend() == "nccl" else None
+        nccl = dist.get_backend() == "nccl"
+        self.dev = torch.device("cuda", torch.cuda.current_device()) if nccl else None
+        # staging buffers of the plane exchange: device memory under NCCL
+        # (the context copies planes device to device); host memory under gloo
+        self.staging = "cuda" if nccl else "cpu"
 
     def exchange(self, field, h):
         torch, dist, c = self.torch, self.dist, self.ctx
         nxy = c.nxy
         ops, recvs = [], []
         for nb, mine0, theirs0, n in self._neighbours(h):
-            send = torch.empty(n * nxy, dtype=torch.float64, device="cuda")
+            send = torch.empty(n * nxy, dtype=torch.float64, device=self.staging)
             c.copy_planes(field, mine0, n, send.data_ptr(), to_field=False)
-            recv = torch.empty(n * nxy, dtype=torch.float64, device="cuda")
+            recv = torch.empty(n * nxy, dtype=torch.float64, device=self.staging)
             ops += [dist.P2POp(dist.isend, send, nb), dist.P2POp(dist.irecv, recv, nb)]
             recvs.append((theirs0, n, recv))
         if ops:
-            torch.cuda.synchronize()
+            if self.staging == "cuda":
+                torch.cuda.synchronize()
             for q in dist.batch_isend_irecv(ops):
                 q.wait()
-            torch.cuda.synchronize()
+            if self.staging == "cuda":
+                torch.cuda.synchronize()
         for p0, n, buf in recvs:
             c.copy_planes(field, p0, n, buf.data_ptr(), to_field=True)
 

@@ -270,3 +270,204 @@ def test_slab_kernel_matches_whole_grid_and_counts_misses(gpu):
         else:
             assert misses == 0
             assert np.array_equal(bits(got), bits(whole.values))
+
+
+# ---------------------------------------------------------------------------
+# The whole-loop driver (zslab.SlabLoop): blocked_sum from the ranks' pieces,
+# and the rank protocol over gloo with a numpy stand-in for the slab context
+# (the bit-exactness of the real phases against the single-GPU loop is
+# test_zslab_loop_gpu.py).
+
+def _pieces(vals, offset):
+    """This rank's blocked_sum pieces as lsr_cuda_slab_energy_pieces forms them."""
+    s0 = (4096 - offset % 4096) % 4096
+    head = vals[:min(s0, vals.size)]
+    full = (vals.size - s0) // 4096 if vals.size > s0 else 0
+    blocks = [0.0] * full
+    for b in range(full):
+        acc = 0.0
+        for v in vals[s0 + 4096 * b:s0 + 4096 * (b + 1)]:
+            acc += float(v)
+        blocks[b] = acc
+    return np.array(blocks), head, vals[s0 + 4096 * full:] if vals.size > s0 else vals[:0]
+
+
+def _blocked_sum(vals):  # parallel.hpp:26-42
+    total = 0.0
+    for b in range(0, vals.size, 4096):
+        acc = 0.0
+        for v in vals[b:b + 4096]:
+            acc += float(v)
+        total += acc
+    return total
+
+
+@pytest.mark.parametrize("sizes", [[0], [5], [4096], [9000, 0, 3, 12000], [100, 100, 100], [4095, 1, 8193, 4096]])
+def test_blocked_sum_from_rank_pieces(sizes):
+    from paper_2410_22205_b200 import zslab
+
+    rng = np.random.default_rng(len(sizes) + sum(sizes))
+    allv = rng.standard_normal(sum(sizes)) * np.exp(rng.uniform(-20, 20, sum(sizes)))
+    pieces, off = [], 0
+    for n in sizes:
+        pieces.append(_pieces(allv[off:off + n], off))
+        off += n
+    assert zslab.blocked_sum_pieces(pieces) == _blocked_sum(allv)
+
+
+class _MockSlab:
+    """numpy stand-in for SlabContext with z-coupled toy phases: every phase
+    reads the planes next to the owned ones, so a wrong or missing halo
+    exchange changes the result."""
+
+    def __init__(self, nxy, nz, wl, wh, ol, oh):
+        import types
+
+        self.grid = types.SimpleNamespace(dims=(nxy, 1, nz), dx=0.1)
+        self.nxy, self.win_lo, self.win_hi, self.own_lo, self.own_hi = nxy, wl, wh, ol, oh
+        self.f = {k: np.zeros((wh - wl) * nxy) for k in (0, 1, 2, 3)}
+
+    def _pl(self, f, k):
+        k = min(max(k, 0), self.grid.dims[2] - 1)
+        return self.f[f][(k - self.win_lo) * self.nxy:(k - self.win_lo + 1) * self.nxy]
+
+    def upload(self, which, v):
+        self.f[which][:] = v
+
+    def close(self):
+        pass
+
+    def plane_ptr(self, which, plane):
+        return self.f[which].ctypes.data + 8 * (plane - self.win_lo) * self.nxy
+
+    def copy_planes(self, which, p0, n, ptr, to_field):
+        import ctypes
+
+        a = self.plane_ptr(which, p0)
+        if to_field:
+            ctypes.memmove(a, ptr, 8 * n * self.nxy)
+        else:
+            ctypes.memmove(ptr, a, 8 * n * self.nxy)
+
+    def _owned(self, f):
+        return self.f[f][(self.own_lo - self.win_lo) * self.nxy:(self.own_hi - self.win_lo) * self.nxy]
+
+    def _stencil(self, src, dst, a, b):
+        for k in range(self.own_lo, self.own_hi):
+            self._pl(dst, k)[:] = a * self._pl(src, k) + b * (self._pl(src, k - 1) + self._pl(src, k + 1))
+
+    def band(self, gamma, which=0):
+        na = int(np.count_nonzero(np.abs(self._owned(which)) < gamma))
+        return na, na + 1
+
+    def energy_cells(self, which=0, p=2, refine=5):
+        self._contrib = np.abs(self._owned(which))
+        self.n_cells = self._contrib.size
+        return self.n_cells
+
+    def energy_pieces(self, offset):
+        return _pieces(self._contrib, offset)
+
+    def max_reach(self, cfg, e2):
+        return 0.5
+
+    def sl_step(self, cfg, e2):
+        self.f[2][:] = self.f[0]
+        self._stencil(0, 2, 0.5 + 0.01 * e2, 0.25)
+        return 0
+
+    def one_step(self):
+        self._stencil(2, 3, 0.9, 0.05)
+        return True, False
+
+    def reinit_begin(self, rcfg):
+        self.f[2][:] = self.f[3]
+        return 1
+
+    def reinit_sweep(self, rcfg, k):
+        cur, nxt = (3, 2) if k % 2 == 0 else (2, 3)
+        self._stencil(cur, nxt, 0.5, 0.25)
+        return float(np.max(np.abs(self._owned(nxt) - self._owned(cur))))
+
+    def reinit_end(self, which, gamma):
+        if which == 3:
+            self.f[2], self.f[3] = self.f[3], self.f[2]
+        o = self._owned(2)
+        o[:] = np.minimum(np.maximum(o, -gamma), gamma)
+
+    def swap(self):
+        self.f[0], self.f[2] = self.f[2], self.f[0]
+
+
+_LOOP_NZ, _LOOP_NXY, _LOOP_ITERS = 24, 6, 3
+
+
+def _loop_cfg():
+    import types
+
+    cfg = types.SimpleNamespace(p=2, interp=1)
+    rcfg = types.SimpleNamespace(max_iters=9, residual_tol=1e-3)
+    phi = np.sin(np.arange(_LOOP_NZ * _LOOP_NXY) * 0.37) * 0.8
+    return cfg, rcfg, phi
+
+
+def _run_mock_loop(runner_factory, ranks, cuts, halo):
+    from paper_2410_22205_b200 import zslab
+
+    cfg, rcfg, phi = _loop_cfg()
+    nxy = _LOOP_NXY
+
+    def make(wl, wh, ol, oh):
+        return _MockSlab(nxy, _LOOP_NZ, wl, wh, ol, oh)
+
+    loop = zslab.SlabLoop(types_grid(), cuts, ranks, halo, make, lambda c: None, runner_factory)
+    loop.upload_phi(lambda c: phi[c.win_lo * nxy:c.win_hi * nxy])
+    stats = [loop.step(cfg, rcfg, 0.7) for _ in range(_LOOP_ITERS)]
+    owned = [c._owned(0).copy() for c in loop.ctxs]
+    return stats, owned
+
+
+def types_grid():
+    import types
+
+    return types.SimpleNamespace(dims=(_LOOP_NXY, 1, _LOOP_NZ), dx=0.1)
+
+
+def _loop_worker(rank, world, port, outdir):
+    import sys
+
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import torch.distributed as dist
+
+    from paper_2410_22205_b200 import zslab
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    cuts = [0, 10, _LOOP_NZ] if world == 2 else [0, 8, 16, _LOOP_NZ]
+    stats, owned = _run_mock_loop(lambda ctxs: zslab.DistRunner(dist, ctxs[0], cuts), [rank], cuts, 3)
+    np.save(os.path.join(outdir, f"loop{rank}.npy"), owned[0])
+    np.save(os.path.join(outdir, f"stats{rank}.npy"), np.array([[s[0]["energy"], s[0]["reinit_iterations"],
+                                                                 s[0]["n_active"]] for s in stats]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_slab_loop_protocol_gloo_matches_one_rank(tmp_path, world):
+    """SlabLoop over torch.distributed (gloo, world 2 and 3, DistRunner) gives
+    the one-rank loop's fields and statistics; so does the in-process runner."""
+    import torch.multiprocessing as mp
+
+    from paper_2410_22205_b200 import zslab
+
+    ref_stats, ref_owned = _run_mock_loop(zslab.InProcessRunner, [0], [0, _LOOP_NZ], 3)
+    mp.spawn(_loop_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    got = np.concatenate([np.load(tmp_path / f"loop{r}.npy") for r in range(world)])
+    assert np.array_equal(bits(got), bits(ref_owned[0]))
+    for r in range(world):
+        st = np.load(tmp_path / f"stats{r}.npy")
+        assert np.array_equal(st[:, :2], np.array([[s[0]["energy"], s[0]["reinit_iterations"]] for s in ref_stats]))
+    cuts = [0, 10, _LOOP_NZ] if world == 2 else [0, 8, 16, _LOOP_NZ]
+    in_stats, in_owned = _run_mock_loop(zslab.InProcessRunner, list(range(world)), cuts, 3)
+    assert np.array_equal(bits(np.concatenate(in_owned)), bits(ref_owned[0]))
