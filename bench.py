@@ -228,12 +228,19 @@ def run_ours(args):
     import paper_2410_22205_b200 as lsr
 
     world, rank, local = dist_env()
+    if args.debug_same_device:  # N ranks on cuda:0 over gloo: a 1-GPU smoke of the N > 1 code path
+        local = 0
+        args.exchange = "nccl"
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.debug_same_device:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    red_dev = "cpu" if args.debug_same_device else "cuda"  # where reductions' tensors live
     cfg = CONFIGS[args.config]
     g, w, step = make_inputs(lsr, cfg)
     pts, phi, active = w["pts"], w["phi"], w["active"]
@@ -287,8 +294,7 @@ def run_ours(args):
         out_t.copy_(phi_t)
         d_t = torch.from_numpy(h_d[sl].copy()).cuda()
         ids_t = torch.from_numpy(mine).cuda()
-        del h_d
-        ctx.close()  # the whole-grid context was only needed for d and E_2
+        # (the whole-grid context stays: d for the slab loop, the e2e slabs and the CPU baseline)
         bad_t = torch.full((1,), np.iinfo(np.int64).max, dtype=torch.int64, device="cuda")
         miss_t = torch.zeros(1, dtype=torch.int64, device="cuda")
         L = lsr.lib()
@@ -371,7 +377,7 @@ def run_ours(args):
         dist.barrier()
     tot = np.array([sum(step_ms), sum(kernel_ms), float(mine.size)], dtype=np.float64)
     if world > 1:
-        t = torch.tensor(tot[:2], device="cuda")
+        t = torch.tensor(tot[:2], device=red_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         tot[:2] = t.cpu().numpy()
     ms_total = float(tot[0])
@@ -399,6 +405,23 @@ def run_ours(args):
     loop = None
     if rank == 0 and world == 1 and not args.no_loop:
         loop = measure_loop(lsr, g, phi, ctx, step, cpu_too=not args.no_cpu_baseline)
+    if world > 1:
+        # the same metric end to end and the whole loop, both over z-slabs
+        # (zslab.SlabLoop / SlabContext); guarded: a failure is reported in
+        # the line, the SL measurement above stands
+        def guarded(fn):
+            try:
+                return fn()
+            except Exception as ex:  # noqa: BLE001
+                return {"error": f"{type(ex).__name__}: {ex}"}
+
+        if not args.no_e2e:
+            e2e = guarded(lambda: measure_e2e_slabs(lsr, g, phi, ctx, active, step, e2, args, dist, world, rank,
+                                                    red_dev))
+        if not args.no_loop:
+            loop = guarded(lambda: measure_loop_slabs(lsr, g, phi, ctx, step, dist, world, rank, red_dev))
+        if rank == 0 and not args.no_cpu_baseline:
+            cpu = guarded(lambda: cpu_baseline(g, phi, ctx, active, step, e2, lsr))
 
     if rank == 0:
         line = {
@@ -450,6 +473,8 @@ def run_ours(args):
                         "also holds the z-line table fill (table_fill_ms_avg) and the sparse resync",
             },
             "gpu_launches": int(launches),
+            **({"debug_same_device": "N ranks on one GPU over gloo: a code-path smoke, not a multi-GPU number"}
+               if args.debug_same_device else {}),
             "clocks": clk.summary(),
             "setup_s": {"build_distance": t_dist, "surface_energy": t_energy},
         }
@@ -587,6 +612,107 @@ def measure_e2e(lsr, g, phi, ctx, active, step, e2, args):
                       "out back): the GPU pulls the phi/d values the step reads (zero-copy) plus 1/8 of the planes "
                       "whole (DMA), returns the updated values, host threads copy phi to out and scatter them",
             "steps": args.e2e_steps}
+
+
+def _max_over_ranks(dist, x, dev):
+    import torch
+
+    t = torch.tensor([float(x)], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def _sum_over_ranks(dist, x, dev):
+    import torch
+
+    t = torch.tensor([float(x)], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+def _slab_ctx(lsr, g, whole, wl, wh, ol, oh):
+    """A SlabContext for resident planes [wl, wh), owned [ol, oh), with d
+    copied from the whole-grid context."""
+    nxy = g.dims[0] * g.dims[1]
+    c = lsr.SlabContext(g, wl, wh, ol, oh)
+    c.copy_planes(lsr._api.FIELD_DIST, wl, wh - wl, whole.field_ptr(lsr._api.FIELD_DIST) + 8 * wl * nxy, True)
+    return c
+
+
+def measure_e2e_slabs(lsr, g, phi, whole, active, step, e2, args, dist, world, rank, dev):
+    """N > 1 end to end through the slab API: every step each rank uploads its
+    resident planes of phi from pinned host memory, runs the SL step on its
+    owned active nodes, and reads its window of out back; the time is the max
+    over ranks (host clock, barrier before each step)."""
+    import torch
+
+    from paper_2410_22205_b200 import zslab
+
+    nxy = g.dims[0] * g.dims[1]
+    halo = zslab.halo_planes(max_displacement(g, whole.download(lsr._api.FIELD_DIST), active, step, e2), g.dx,
+                             int(step.interp))
+    cuts = zslab.plan_cuts(active, nxy, g.dims[2], world, min_planes=halo)
+    nz = g.dims[2]
+    c = _slab_ctx(lsr, g, whole, max(0, int(cuts[rank]) - halo), min(nz, int(cuts[rank + 1]) + halo),
+                  int(cuts[rank]), int(cuts[rank + 1]))
+    h_phi = torch.empty(c.n_resident, dtype=torch.float64, pin_memory=True).numpy()
+    h_out = torch.empty(c.n_resident, dtype=torch.float64, pin_memory=True).numpy()
+    h_phi[:] = phi[c.win_lo * nxy:c.win_hi * nxy]
+    c.upload(lsr._api.FIELD_PHI, h_phi)
+    c.band(step.band.gamma)
+    ts = []
+    for i in range(2 + args.e2e_steps):
+        dist.barrier()
+        t0 = time.perf_counter()
+        c.upload(lsr._api.FIELD_PHI, h_phi)
+        if c.sl_step(step, e2):
+            raise RuntimeError("halo too small")
+        lsr.lib().lsr_cuda_download_field(c.h, lsr._api.FIELD_OUT, h_out.ctypes.data)
+        if i >= 2:
+            ts.append(time.perf_counter() - t0)
+    t = _max_over_ranks(dist, float(np.mean(ts)), dev)
+    h2d = _sum_over_ranks(dist, 8 * c.n_resident, dev)
+    c.close()
+    return {"value": active.size / t, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(h2d),
+            "ms_per_step": 1e3 * t, "steps": args.e2e_steps, "halo_planes": halo,
+            "timing": "max over ranks of the host clock around: upload of the rank's resident planes of phi "
+                      "(pinned), lsr_cuda_slab_sl_step, download of its window of out (pinned)"}
+
+
+def measure_loop_slabs(lsr, g, phi, whole, step, dist, world, rank, dev, steps=5):
+    """N > 1: the whole driver iteration over z-slabs (zslab.SlabLoop with the
+    torch.distributed runner): band, E_2 (blocked_sum from the ranks'
+    pieces), SL, the one-step and Jacobi sweeps with plane exchanges and a
+    global stop rule, clamp. Wall time per iteration, max over ranks."""
+    import torch
+
+    from paper_2410_22205_b200 import zslab
+
+    nxy = g.dims[0] * g.dims[1]
+    band = np.flatnonzero(np.abs(phi) < step.band.gamma)
+    halo = 6
+    cuts = zslab.plan_cuts(band, nxy, g.dims[2], world, min_planes=3 * halo)
+    rc = lsr.ReinitConfig.defaults(g.dx, step.band.gamma)
+    loop = zslab.SlabLoop(g, cuts, [rank], halo, lambda wl, wh, ol, oh: _slab_ctx(lsr, g, whole, wl, wh, ol, oh),
+                          lambda c: None, lambda ctxs: zslab.DistRunner(dist, ctxs[0], cuts))
+    loop.upload_phi(lambda c: phi[c.win_lo * nxy:c.win_hi * nxy])
+    ts, its = [], []
+    for i in range(steps):
+        dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        st = loop.step(step, rc, step.band.gamma)
+        torch.cuda.synchronize()
+        if i >= 1:
+            ts.append(time.perf_counter() - t0)
+        its.append(st[0]["reinit_iterations"])
+    t = _max_over_ranks(dist, float(np.mean(ts)), dev)
+    for c in loop.ctxs:
+        c.close()
+    return {"gpu_total_ms_per_step": 1e3 * t, "steps": steps, "timed": steps - 1, "halo_planes": loop.halo,
+            "regrows": loop.regrows, "reinit_iterations": its,
+            "what": "driver.cpp:187-203 over z-slabs (zslab.SlabLoop, NCCL): wall time per iteration incl. the "
+                    "per-sweep residual allreduce and plane exchanges, max over ranks, iterations 2..N from phi^0"}
 
 
 def measure_loop(lsr, g, phi, ctx, step, steps=6, cpu_too=True):
@@ -757,6 +883,8 @@ def main():
     ap.add_argument("--no-loop", action="store_true")
     ap.add_argument("--exchange", choices=["fused", "nccl"], default="fused",
                     help="N > 1: fused SL + peer halo push (default) or NCCL plane exchange")
+    ap.add_argument("--debug-same-device", action="store_true",
+                    help="N > 1 on one GPU over gloo (host-staged exchanges): a smoke of the N > 1 code path")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

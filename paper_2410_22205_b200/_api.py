@@ -629,6 +629,8 @@ class SlabContext:
     the owned planes [own_lo, own_hi). Node ids are global. See
     paper_2410_22205_b200.zslab.SlabLoop for the driver."""
 
+    device_memory = True  # fields live on the device (zslab.DistRunner stages planes there)
+
     def __init__(self, grid: Grid, win_lo: int, win_hi: int, own_lo: int, own_hi: int, device: int = 0):
         self.grid = grid
         self.win_lo, self.win_hi, self.own_lo, self.own_hi = int(win_lo), int(win_hi), int(own_lo), int(own_hi)

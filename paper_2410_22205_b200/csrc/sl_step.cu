@@ -92,7 +92,8 @@ __global__ void __launch_bounds__(kSlThreadsW3, kSlMinBlocksW3) sl_step_zt_kerne
         return;
     }
     const bool use_zt = __ldg(P.ztab_bad) == 0u;
-    store_update(P, id, k, sl_node<3, 1>(P, phi, dist, id, i, j, k, use_zt), out, bad);
+    const double next = sl_node<3, 1>(P, phi, dist, id, i, j, k, use_zt);
+    store_update(P, id, k, next, out, bad);
 }
 
 // The z-line table of the 3d WENO fast path. For node n = (i, j, k),

@@ -98,6 +98,15 @@ def exchange_halo(dist, out, s: Slab, halo: int) -> None:
         e = min(s.z_base + s.z_planes, s.hi + halo)
         ops.append(dist.P2POp(dist.irecv, out[s.local(s.hi):s.local(e)], s.rank + 1))
     del P
+    if ops and out.is_cuda and dist.get_backend() == "gloo":  # gloo moves host tensors: stage through host memory
+        staged = [(op, op.tensor, op.tensor.cpu()) for op in ops]
+        ops = [dist.P2POp(op.op, h, op.peer) for op, _, h in staged]
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+        for op, dev_t, h in staged:
+            if op.op == dist.irecv:
+                dev_t.copy_(h)
+        return
     if ops:
         for req in dist.batch_isend_irecv(ops):
             req.wait()
@@ -331,9 +340,11 @@ class DistRunner:
         self.cuts = cuts
         nccl = dist.get_backend() == "nccl"
         self.dev = torch.device("cuda", torch.cuda.current_device()) if nccl else None
-        # staging buffers of the plane exchange: device memory under NCCL
-        # (the context copies planes device to device); host memory under gloo
-        self.staging = "cuda" if nccl else "cpu"
+        # staging buffers of the plane exchange: device memory for a device
+        # context (it copies planes device to device); gloo moves host
+        # tensors, so under gloo they are copied through host memory
+        self.staging = "cuda" if getattr(ctx, "device_memory", False) else "cpu"
+        self.wire_host = not nccl
 
     def exchange(self, field, h):
         torch, dist, c = self.torch, self.dist, self.ctx
@@ -343,16 +354,23 @@ class DistRunner:
             send = torch.empty(n * nxy, dtype=torch.float64, device=self.staging)
             c.copy_planes(field, mine0, n, send.data_ptr(), to_field=False)
             recv = torch.empty(n * nxy, dtype=torch.float64, device=self.staging)
-            ops += [dist.P2POp(dist.isend, send, nb), dist.P2POp(dist.irecv, recv, nb)]
-            recvs.append((theirs0, n, recv))
+            if self.wire_host and send.is_cuda:
+                ops += [dist.P2POp(dist.isend, send.cpu(), nb)]
+                host_recv = torch.empty(n * nxy, dtype=torch.float64)
+                ops += [dist.P2POp(dist.irecv, host_recv, nb)]
+                recvs.append((theirs0, n, recv, host_recv))
+            else:
+                ops += [dist.P2POp(dist.isend, send, nb), dist.P2POp(dist.irecv, recv, nb)]
+                recvs.append((theirs0, n, recv, None))
         if ops:
             if self.staging == "cuda":
                 torch.cuda.synchronize()
             for q in dist.batch_isend_irecv(ops):
                 q.wait()
-            if self.staging == "cuda":
+        for p0, n, buf, host in recvs:
+            if host is not None:
+                buf.copy_(host)
                 torch.cuda.synchronize()
-        for p0, n, buf in recvs:
             c.copy_planes(field, p0, n, buf.data_ptr(), to_field=True)
 
     def _neighbours(self, h):

@@ -89,3 +89,31 @@ def test_slab_loop_matches_single_gpu_loop(gpu, dims, interp, world, halo):
         assert loop.regrows >= 1
     for c in loop.ctxs:
         c.close()
+
+
+@pytest.mark.parametrize("config,world,iters", [(3, 4, 4), (4, 2, 3)])
+def test_slab_loop_full_size_configs(gpu, config, world, iters):
+    """BASELINE configs 3 (256^3 noisy torus, 100 k points, WENO) and 4
+    (512^3 bumpy sphere, 1 M points, WENO) at full size: the slab loop's
+    phi after every iteration is bit-identical to the single-GPU loop's."""
+    lsr = gpu
+    n, npts, sig = {3: (256, 100_000, 0.5), 4: (512, 1_000_000, 0.0)}[config]
+    g = lsr.cube_grid(n, 3)
+    pts = lsr.cloud_generate(config, npts, seed=2410, sigma=sig * g.dx)
+    ax = g.axes()
+    phi0 = (np.sqrt(ax[0][None, None, :] ** 2 + ax[1][None, :, None] ** 2 + ax[2][:, None, None] ** 2) - 0.9).ravel()
+    ctx = lsr.Context(g)
+    ctx.build_distance(pts)
+    dist = ctx.download(1)
+    ctx.close()
+    bp = lsr.default_band_params(3, g.dx)
+    cfg = lsr.StepConfig(p=2, delta=1.0, dt=0.25 * g.dx, band=bp, interp=lsr.InterpolatorKind(1))
+    rcfg = lsr.ReinitConfig.defaults(g.dx, bp.gamma)
+    ref_stats, ref_fields = _single(lsr, g, phi0, dist, cfg, rcfg, iters)
+    stats, fields, loop = _sharded(lsr, g, phi0, dist, cfg, rcfg, iters, world, 8)
+    for it in range(iters):
+        for key in ("energy", "n_active", "n_tube", "reinit_iterations"):
+            assert stats[it][key] == ref_stats[it][key], (it, key)
+        assert np.count_nonzero(bits(fields[it]) != bits(ref_fields[it])) == 0, f"iteration {it + 1}"
+    for c in loop.ctxs:
+        c.close()
