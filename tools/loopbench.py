@@ -11,7 +11,8 @@ ap.add_argument("--config", type=int, default=4)
 ap.add_argument("--steps", type=int, default=5)
 a = ap.parse_args()
 cfg = bench.CONFIGS[a.config]
-g, pts, phi, active, step = bench.make_inputs(lsr, cfg)
+g, w, step = bench.make_inputs(lsr, cfg)
+pts, phi = w["pts"], w["phi"]
 ctx = lsr.Context(g)
 t0 = time.perf_counter(); ctx.build_distance(pts); tdist = time.perf_counter() - t0
 ctx.upload(0, phi)
