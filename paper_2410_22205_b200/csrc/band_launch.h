@@ -61,7 +61,7 @@ int lsr_reinit_iterate(const lsr_dev::SlParams& P, double** phi, double** scratc
                        int* iterations, cudaStream_t s, std::string* err);
 int lsr_reinitialize(const lsr_dev::SlParams& P, double** phi, double** scratch, const BandBuffers& B, double gamma,
                      const ReinitParams& R, ReinitBuffers& W, int* iterations, int* had_interface, cudaStream_t s,
-                     std::string* err);
+                     std::string* err, bool clamp_sparse = false);
 
 // z-slab forms (band_reinit.cu): owned planes [own_lo, own_hi) of buffers
 // resident on [win_lo, win_hi), passed shifted to global node ids

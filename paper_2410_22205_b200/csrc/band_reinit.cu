@@ -563,6 +563,16 @@ __global__ void iter_check(IterState* st, double tol) {
     if (residual < tol) st->done = 1;
 }
 
+// clamp_field on a node list (the sparse form of the loop's clamp, see
+// lsr_reinitialize): same per-node expression as clamp_kernel
+__global__ void clamp_ids(double* __restrict__ f, const long long* __restrict__ ids, long long n, double gamma) {
+    const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    const long long id = ids[t];
+    const double v = f[id], c = smin(smax(v, -gamma), gamma);
+    if (__double_as_longlong(c) != __double_as_longlong(v)) f[id] = c;
+}
+
 __global__ void copy_ids(const double* __restrict__ src, double* __restrict__ dst, const long long* __restrict__ ids,
                          long long n) {
     const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -866,9 +876,15 @@ int lsr_reinit_iterate(const SlParams& P, double** phi, double** scratch, const 
     return LSR_OK;
 }
 
+// clamp_sparse: the field equalled a fully clamped field except on the tube
+// of B and the nodes the one-step / sweeps may change (the one-step's frozen
+// nodes, the tube's nodes) — e.g. phi^{n+1} of the driver loop, built from a
+// clamped phi^n by an SL step on the ACTIVE nodes (a subset of the tube).
+// Clamping is elementwise and idempotent, so clamping just those nodes gives
+// the bits of the full clamp_field (grid.cpp:126-134).
 int lsr_reinitialize(const SlParams& P, double** phi, double** scratch, const BandBuffers& B, double gamma,
                      const ReinitParams& R, ReinitBuffers& W, int* iterations, int* had_interface, cudaStream_t s,
-                     std::string* err) {
+                     std::string* err, bool clamp_sparse) {
     if (!(R.dtau > 0.0)) {
         *err = "reinit: dtau must be positive";  // reinit.hpp:14-17
         return LSR_ERR_CONFIG;
@@ -886,7 +902,22 @@ int lsr_reinitialize(const SlParams& P, double** phi, double** scratch, const Ba
     // left as it was, then clamped
     if (*had_interface)
         if (int st = lsr_reinit_iterate(P, phi, scratch, B.tube, B.n_tube, R, W, true, iterations, s, err)) return st;
-    return lsr_clamp(*phi, n, gamma, s, err, B.state, W.clamp_outside);
+    if (!clamp_sparse) return lsr_clamp(*phi, n, gamma, s, err, B.state, W.clamp_outside);
+    if (!(gamma > 0.0)) {
+        *err = "clamp_field: gamma must be positive";  // grid.cpp:127
+        return LSR_ERR_CONFIG;
+    }
+    const long long nf = *had_interface ? W.n_frozen : 0;
+    if (B.n_tube > 0) {
+        clamp_ids<<<static_cast<unsigned>((B.n_tube + 255) / 256), 256, 0, s>>>(*phi, B.tube, B.n_tube, gamma);
+        lsr_note_launch();
+    }
+    if (nf > 0) {
+        clamp_ids<<<static_cast<unsigned>((nf + 255) / 256), 256, 0, s>>>(*phi, W.frozen_ids, nf, gamma);
+        lsr_note_launch();
+    }
+    BR_TRY(cudaGetLastError());
+    return LSR_OK;
 }
 
 // ---------------------------------------------------------------------------

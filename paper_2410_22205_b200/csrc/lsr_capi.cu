@@ -175,6 +175,12 @@ struct lsr_cuda_ctx {
     // z-slab context (lsr_cuda_slab_create): fields hold the resident planes
     // [win_lo, win_hi) of the global grid `grid`; work is done on the owned
     // planes [own_lo, own_hi); n = resident nodes
+    // the loop's clamp bookkeeping: `phi` was fully clamped to clamped_gamma
+    // by the loop step that set clamped_seq, and no entry point that may
+    // write phi or out (each bumps seq) ran since
+    uint64_t seq = 1, clamped_seq = 0;
+    const double* clamped_phi = nullptr;
+    double clamped_gamma = 0.0;
     bool slab = false;
     int win_lo = 0, win_hi = 0, own_lo = 0, own_hi = 0;
     EnergySlabWork ew;
@@ -367,6 +373,7 @@ int lsr_cuda_upload_field(lsr_cuda_ctx* c, int which, const double* host) {
     if (!c || !host) return set_err(LSR_ERR_CONFIG, "upload: null argument");
     double** slot = field_slot(c, which);
     if (!slot) return set_err(LSR_ERR_CONFIG, "upload: unknown field");
+    c->seq++;  // may write phi or out
     LSR_CUDA_TRY(cudaSetDevice(c->device));
     LSR_CUDA_TRY(cudaMemcpyAsync(*slot, host, sizeof(double) * c->n, cudaMemcpyHostToDevice, c->stream));
     LSR_CUDA_TRY(cudaStreamSynchronize(c->stream));
@@ -389,12 +396,14 @@ int lsr_cuda_field_ptr(lsr_cuda_ctx* c, int which, double** dptr) {
     if (!c || !dptr) return set_err(LSR_ERR_CONFIG, "field_ptr: null argument");
     double** slot = field_slot(c, which);
     if (!slot) return set_err(LSR_ERR_CONFIG, "field_ptr: unknown field");
+    c->seq++;  // may write phi or out
     *dptr = *slot;
     return LSR_OK;
 }
 
 int lsr_cuda_mark_dirty(lsr_cuda_ctx* c, int which) {
     if (!c) return set_err(LSR_ERR_CONFIG, "null context");
+    c->seq++;  // may write phi or out
     if (which != LSR_FIELD_DIST) c->consistent = false;
     else c->zt_bricks = false;
     return LSR_OK;
@@ -519,6 +528,7 @@ int enqueue_step(lsr_cuda_ctx* c, const lsr_step_cfg* cfg, double energy_p, bool
 int lsr_cuda_sl_step(lsr_cuda_ctx* c, const lsr_step_cfg* cfg, double energy_p, int64_t* bad_node) {
     if (bad_node) *bad_node = -1;
     if (!c) return set_err(LSR_ERR_CONFIG, "null context");
+    c->seq++;  // may write phi or out
     if (int st = check_cfg(cfg, energy_p)) return st;
     if (c->async_n > 0) return set_err(LSR_ERR_CONFIG, "sl_step: asynchronous steps pending (call lsr_cuda_sync)");
     LSR_CUDA_TRY(cudaSetDevice(c->device));
@@ -537,6 +547,7 @@ int lsr_cuda_sl_step(lsr_cuda_ctx* c, const lsr_step_cfg* cfg, double energy_p, 
 
 int lsr_cuda_sl_step_async(lsr_cuda_ctx* c, const lsr_step_cfg* cfg, double energy_p) {
     if (!c) return set_err(LSR_ERR_CONFIG, "null context");
+    c->seq++;  // may write phi or out
     if (int st = check_cfg(cfg, energy_p)) return st;
     LSR_CUDA_TRY(cudaSetDevice(c->device));
     if (c->async_n >= kMaxAsyncSteps) return set_err(LSR_ERR_CONFIG, "sl_step_async: too many pending steps");
@@ -588,6 +599,7 @@ int lsr_cuda_async_times(lsr_cuda_ctx* c, float* kernel_ms, float* step_ms, floa
 
 int lsr_cuda_swap(lsr_cuda_ctx* c) {
     if (!c) return set_err(LSR_ERR_CONFIG, "null context");
+    c->seq++;  // may write phi or out
     std::swap(c->phi, c->out);  // out and phi still differ only at `dirty`
     return LSR_OK;
 }
@@ -1342,6 +1354,7 @@ int lsr_cuda_clamp_field(lsr_cuda_ctx* c, int which, double gamma) {
     if (!c) return set_err(LSR_ERR_CONFIG, "null context");
     double** slot = field_slot(c, which);
     if (!slot) return set_err(LSR_ERR_CONFIG, "clamp_field: unknown field");
+    c->seq++;  // may write phi or out
     LSR_CUDA_TRY(cudaSetDevice(c->device));
     std::string err;
     if (int st = lsr_clamp(*slot, c->n, gamma, c->stream, &err)) return set_err(st, err);
@@ -1351,11 +1364,12 @@ int lsr_cuda_clamp_field(lsr_cuda_ctx* c, int which, double gamma) {
     return LSR_OK;
 }
 
-int lsr_cuda_reinitialize(lsr_cuda_ctx* c, int which, double gamma, const lsr_reinit_cfg* rc, int* iterations,
-                          int* had_interface) {
+static int reinitialize_impl(lsr_cuda_ctx* c, int which, double gamma, const lsr_reinit_cfg* rc, int* iterations,
+                             int* had_interface, bool clamp_sparse) {
     if (!c || !rc) return set_err(LSR_ERR_CONFIG, "reinitialize: null argument");
     double** slot = field_slot(c, which);
     if (!slot || which == LSR_FIELD_DIST) return set_err(LSR_ERR_CONFIG, "reinitialize: phi must be PHI or OUT");
+    c->seq++;  // may write phi or out
     if (!c->band.state) return set_err(LSR_ERR_CONFIG, "reinitialize: build the band first (lsr_cuda_narrow_band)");
     LSR_CUDA_TRY(cudaSetDevice(c->device));
     if (!c->scratch) LSR_CUDA_TRY(cudaMalloc(&c->scratch, sizeof(double) * c->n));
@@ -1363,13 +1377,18 @@ int lsr_cuda_reinitialize(lsr_cuda_ctx* c, int which, double gamma, const lsr_re
     std::string err;
     int it = 0, had = 0;
     const int st = lsr_reinitialize(grid_params(c->grid), slot, &c->scratch, c->band, gamma, R, c->rb, &it, &had,
-                                    c->stream, &err);
+                                    c->stream, &err, clamp_sparse);
     if (st) return set_err(st, err);
     LSR_CUDA_TRY(cudaStreamSynchronize(c->stream));
     c->consistent = false;  // the clamp may touch any node
     if (iterations) *iterations = it;
     if (had_interface) *had_interface = had;
     return LSR_OK;
+}
+
+int lsr_cuda_reinitialize(lsr_cuda_ctx* c, int which, double gamma, const lsr_reinit_cfg* rc, int* iterations,
+                          int* had_interface) {
+    return reinitialize_impl(c, which, gamma, rc, iterations, had_interface, false);
 }
 
 int lsr_cuda_set_band(lsr_cuda_ctx* c, const uint8_t* state, const int64_t* active, int64_t n_active,
@@ -1402,6 +1421,7 @@ int lsr_cuda_set_band(lsr_cuda_ctx* c, const uint8_t* state, const int64_t* acti
 
 int lsr_cuda_interface_one_step(lsr_cuda_ctx* c, int which, uint8_t* frozen, int* had_interface) {
     if (!c) return set_err(LSR_ERR_CONFIG, "null context");
+    c->seq++;  // may write phi or out
     double** slot = field_slot(c, which);
     if (!slot || which == LSR_FIELD_DIST) return set_err(LSR_ERR_CONFIG, "interface_one_step: phi must be PHI or OUT");
     LSR_CUDA_TRY(cudaSetDevice(c->device));
@@ -1425,6 +1445,7 @@ int lsr_cuda_reinit_iterate(lsr_cuda_ctx* c, int which, const uint8_t* frozen, c
     if (!c || !rc) return set_err(LSR_ERR_CONFIG, "reinit_iterate: null argument");
     double** slot = field_slot(c, which);
     if (!slot || which == LSR_FIELD_DIST) return set_err(LSR_ERR_CONFIG, "reinit_iterate: phi must be PHI or OUT");
+    c->seq++;  // may write phi or out
     if (!c->band.state) return set_err(LSR_ERR_CONFIG, "reinit_iterate: no band (lsr_cuda_narrow_band / set_band)");
     LSR_CUDA_TRY(cudaSetDevice(c->device));
     if (!c->scratch) LSR_CUDA_TRY(cudaMalloc(&c->scratch, sizeof(double) * c->n));
@@ -1492,6 +1513,10 @@ int lsr_cuda_loop_step(lsr_cuda_ctx* c, const lsr_step_cfg* cfg, const lsr_reini
         }
     } evg{ev};
     lsr_loop_stats S{};
+    // phi^n fully clamped by the previous loop step and untouched since: phi^{n+1}
+    // can then differ from a clamped field only on the band's tube and the
+    // one-step's frozen nodes, and the final clamp visits just those
+    const bool clamp_sparse = c->clamped_seq == c->seq && c->clamped_phi == c->phi && c->clamped_gamma == cfg->gamma;
     cudaEventRecord(ev[0], c->stream);
     int64_t na = 0, nt = 0;
     // 1. band of phi^n (driver.cpp:187)
@@ -1514,7 +1539,7 @@ int lsr_cuda_loop_step(lsr_cuda_ctx* c, const lsr_step_cfg* cfg, const lsr_reini
     cudaEventRecord(ev[3], c->stream);
     // 4. reinitialise phi^{n+1} on the band of phi^n (driver.cpp:196)
     int it = 0, had = 0;
-    if (int st = lsr_cuda_reinitialize(c, LSR_FIELD_OUT, cfg->gamma, rc, &it, &had)) return st;
+    if (int st = reinitialize_impl(c, LSR_FIELD_OUT, cfg->gamma, rc, &it, &had, clamp_sparse)) return st;
     cudaEventRecord(ev[4], c->stream);
     // 5. swap (driver.cpp:203). phi^{n+1} differs from phi^n (the buffer that
     // becomes `out`) only where the SL step, the one-step, the sweeps or the
@@ -1541,6 +1566,9 @@ int lsr_cuda_loop_step(lsr_cuda_ctx* c, const lsr_step_cfg* cfg, const lsr_reini
         c->consistent = false;
     }
     std::swap(c->phi, c->out);
+    c->clamped_seq = ++c->seq;
+    c->clamped_phi = c->phi;
+    c->clamped_gamma = cfg->gamma;
     LSR_CUDA_TRY(cudaStreamSynchronize(c->stream));
     S.energy = e2;
     S.n_active = na;
