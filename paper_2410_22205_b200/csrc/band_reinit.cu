@@ -312,7 +312,10 @@ __device__ __forceinline__ void load4(const double* src, double* dst) {
 // kMarch consecutive planes and keeps the planes k-1, k, k+1 of its row in
 // registers, so each plane costs three row loads (z+1, y-1, y+1) instead of
 // five; same per-node arithmetic as one_step
-constexpr int kMarch = 16;
+#ifndef LSR_MARCH_PLANES
+#define LSR_MARCH_PLANES 16
+#endif
+constexpr int kMarch = LSR_MARCH_PLANES;
 
 #ifndef LSR_MARCH_MINB
 #define LSR_MARCH_MINB 4  // 64 registers: occupancy beats the few spills (reinit 4.82 -> 4.71 ms at 512^3)
