@@ -133,6 +133,8 @@ void zt_attach(SlParams& P, const ZtBuffers& Z) {
 }
 
 int numerical_error(const lsr_grid& g, unsigned long long bad, int64_t* bad_node) {
+    if (bad >= static_cast<unsigned long long>(num_nodes(g)))  // the kernels' mark of an id outside the grid
+        return set_err(LSR_ERR_CONFIG, "sl_step: ids must be node ids of the grid");
     if (bad_node) *bad_node = static_cast<int64_t>(bad);
     const int64_t id = static_cast<int64_t>(bad);
     const int i = static_cast<int>(id % g.dims[0]);
@@ -476,7 +478,7 @@ int enqueue_step(lsr_cuda_ctx* c, const lsr_step_cfg* cfg, double energy_p, bool
     if (!c->consistent) {
         LSR_CUDA_TRY(cudaMemcpyAsync(c->out, c->phi, sizeof(double) * c->n, cudaMemcpyDeviceToDevice, sr));
     } else {
-        LSR_CUDA_TRY(launch_resync(c->phi, c->out, c->dirty, c->n_dirty, sr));
+        LSR_CUDA_TRY(launch_resync(c->phi, c->out, c->dirty, c->n_dirty, c->n, sr));
     }
     if (reset_bad) LSR_CUDA_TRY(cudaMemsetAsync(c->d_bad, 0xff, sizeof(unsigned long long), sr));
     // 3d WENO: the z-line table of phi on the bricks around the active set
@@ -979,7 +981,9 @@ static int sl_step_host_pipelined(lsr_cuda_ctx* c, const double* phi, const doub
             if (trace && ch == nch - 1 && part == 0) t_last_res = ms_since();
             const int64_t len = first[ch + 1] - first[ch];
             const int64_t t0 = first[ch] + len * part / kParts, t1 = first[ch] + len * (part + 1) / kParts;
-            for (int64_t t = t0; t < t1; ++t) out[active[t]] = h_res[t];
+            const uint64_t nn = static_cast<uint64_t>(c->n);
+            for (int64_t t = t0; t < t1; ++t)
+                if (static_cast<uint64_t>(active[t]) < nn) out[active[t]] = h_res[t];  // else reported by the step
         });
     }
     // on every exit the host jobs (which reference this frame) are joined;
@@ -1051,7 +1055,7 @@ static int sl_step_host_pipelined(lsr_cuda_ctx* c, const double* phi, const doub
         const long long n = first[ch + 1] - first[ch];
         LSR_CUDA_TRY(launch_sl_step(P, cfg->interp, c->phi, c->dist, c->active + first[ch], n, c->out, c->d_bad, cmp));
         const bool whole = ch < nfull;
-        if (!whole) LSR_CUDA_TRY(launch_gather_ids(c->out, c->active + first[ch], n, c->d_res + first[ch], cmp));
+        if (!whole) LSR_CUDA_TRY(launch_gather_ids(c->out, c->active + first[ch], n, c->d_res + first[ch], c->n, cmp));
         LSR_CUDA_TRY(cudaEventRecord(c->ev_cmp[ch], cmp));
         LSR_CUDA_TRY(cudaStreamWaitEvent(down, c->ev_cmp[ch], 0));
         if (!whole) {
@@ -1195,10 +1199,8 @@ int lsr_cuda_sl_step_host(const lsr_grid* grid, const double* phi, const double*
     if (int st = check_cfg(cfg, energy_p)) return st;
     if (!phi || !dist || !out || (n_active > 0 && !active)) return set_err(LSR_ERR_CONFIG, "sl_step: null argument");
     if (out == phi) return set_err(LSR_ERR_CONFIG, "sl_step: out must not alias phi");
-    {
-        const int64_t nodes = static_cast<int64_t>(grid->dims[0]) * grid->dims[1] * grid->dims[2];
-        if (!ids_in_grid(active, n_active, nodes)) return set_err(LSR_ERR_CONFIG, "sl_step: ids must be node ids of the grid");
-    }
+    // ids outside the grid are never dereferenced on the device or in the
+    // host scatter; the step reports them as a ConfigError (numerical_error)
     struct Cache {
         lsr_cuda_ctx* ctx = nullptr;
         ~Cache() { lsr_cuda_destroy(ctx); }

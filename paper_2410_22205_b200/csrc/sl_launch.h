@@ -67,7 +67,8 @@ cudaError_t launch_reach_max(const lsr_dev::SlParams& P, const double* dist, con
 cudaError_t launch_check_ids(const int64_t* ids, long long n, long long n_nodes, unsigned long long* bad,
                              cudaStream_t stream);
 
-cudaError_t launch_resync(const double* phi, double* out, const int64_t* ids, long long n, cudaStream_t stream);
+cudaError_t launch_resync(const double* phi, double* out, const int64_t* ids, long long n, long long n_nodes,
+                          cudaStream_t stream);
 
 cudaError_t launch_weno_selftest(const lsr_dev::SlParams& P, unsigned long long seed, long long n,
                                  unsigned long long* counts);
@@ -81,5 +82,5 @@ cudaError_t launch_scatter_runs(const double* packed, const long long* desc, lon
                                 long long vend, double* field, cudaStream_t stream);
 
 // res[t] = field[ids[t]] for t < n
-cudaError_t launch_gather_ids(const double* field, const int64_t* ids, long long n, double* res,
+cudaError_t launch_gather_ids(const double* field, const int64_t* ids, long long n, double* res, long long n_nodes,
                               cudaStream_t stream);

@@ -34,6 +34,16 @@ __device__ __forceinline__ void node_ijk(const SlParams& P, long long id, int& i
     }
 }
 
+// an id outside the grid is never dereferenced: it is recorded as the
+// node count N in *bad (atomicMin with the non-finite ids, which are < N),
+// which the host reports as a ConfigError
+__device__ __forceinline__ bool id_outside(const SlParams& P, long long id, unsigned long long* bad) {
+    const unsigned long long n = static_cast<unsigned long long>(P.nxy * P.nz);
+    if (static_cast<unsigned long long>(id) < n) return false;
+    atomicMin(bad, n);
+    return true;
+}
+
 // the write of one update (evolve.cpp:107-117): out, the smallest
 // non-finite id, and the fused halo exchange — the neighbours read these
 // planes next step, so the update goes straight into their resident buffers
@@ -65,6 +75,7 @@ __global__ void __launch_bounds__(kSlThreads, kSlMinBlocks) sl_step_kernel(SlPar
     const long long a = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (a >= n_active) return;
     const long long id = __ldg(active + a);
+    if (id_outside(P, id, bad)) return;
     int i, j, k;
     node_ijk(P, id, i, j, k);
     if (slab_node_miss(P, k)) {  // nothing of a non-resident node is read or written
@@ -85,6 +96,7 @@ __global__ void __launch_bounds__(kSlThreadsW3, kSlMinBlocksW3) sl_step_zt_kerne
     const long long a = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (a >= n_active) return;
     const long long id = __ldg(active + a);
+    if (id_outside(P, id, bad)) return;
     int i, j, k;
     node_ijk(P, id, i, j, k);
     if (slab_node_miss(P, k)) {
@@ -134,11 +146,10 @@ __global__ void zt_reach_kernel(SlParams P, const double* __restrict__ dist, con
     unsigned r = 0;
     long long id = 0;
     int i = 0, j = 0, k = 0;
-    if (a < n) {
-        id = __ldg(active + a);
-        unflatten(P, id, i, j, k);
-    }
-    if (a < n && !slab_node_miss(P, k)) {  // (a non-resident node is counted by the SL kernel)
+    const bool inside = a < n && static_cast<unsigned long long>(id = __ldg(active + a)) <
+                                     static_cast<unsigned long long>(P.nxy * P.nz);
+    if (inside) unflatten(P, id, i, j, k);
+    if (inside && !slab_node_miss(P, k)) {  // (a non-resident node is counted by the SL kernel)
         b = brick_of(i, j, k, nbx, nby);
         const double d_j = __ldg(dist + id);
         const double c_j = P.p == 1 ? 1.0 : d_j / P.energy;  // scale_factor (evolve.cpp:32-38)
@@ -285,10 +296,11 @@ __global__ void __launch_bounds__(256) zt_fill_kernel(SlParams P, const double* 
 // out[ids] = phi[ids]: re-establishes "out equals phi off the active set"
 // after the previous step wrote out (or after a swap) without the O(N) copy.
 __global__ void resync_kernel(const double* __restrict__ phi, double* __restrict__ out,
-                              const int64_t* __restrict__ ids, long long n) {
+                              const int64_t* __restrict__ ids, long long n, long long n_nodes) {
     const long long a = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (a >= n) return;
     const long long id = __ldg(ids + a);
+    if (static_cast<unsigned long long>(id) >= static_cast<unsigned long long>(n_nodes)) return;  // (reported by the step)
     out[id] = __ldg(phi + id);
 }
 
@@ -453,19 +465,21 @@ __global__ void scatter_runs_kernel(const double* __restrict__ packed, const lon
 
 // res[t] = field[ids[t]]: the updated values of one chunk, packed for the D2H
 __global__ void gather_ids_kernel(const double* __restrict__ field, const int64_t* __restrict__ ids, long long n,
-                                  double* __restrict__ res) {
+                                  double* __restrict__ res, long long n_nodes) {
     const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (t < n) res[t] = field[ids[t]];
+    if (t >= n) return;
+    const long long id = ids[t];
+    res[t] = static_cast<unsigned long long>(id) < static_cast<unsigned long long>(n_nodes) ? field[id] : 0.0;
 }
 
 }  // namespace lsr_dev
 
 using namespace lsr_dev;
 
-cudaError_t launch_gather_ids(const double* field, const int64_t* ids, long long n, double* res,
+cudaError_t launch_gather_ids(const double* field, const int64_t* ids, long long n, double* res, long long n_nodes,
                               cudaStream_t stream) {
     if (n <= 0) return cudaSuccess;
-    gather_ids_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, stream>>>(field, ids, n, res);
+    gather_ids_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, stream>>>(field, ids, n, res, n_nodes);
     lsr_note_launch();
     return cudaGetLastError();
 }
@@ -563,10 +577,11 @@ cudaError_t launch_check_ids(const int64_t* ids, long long n, long long n_nodes,
     return cudaGetLastError();
 }
 
-cudaError_t launch_resync(const double* phi, double* out, const int64_t* ids, long long n, cudaStream_t stream) {
+cudaError_t launch_resync(const double* phi, double* out, const int64_t* ids, long long n, long long n_nodes,
+                          cudaStream_t stream) {
     if (n <= 0) return cudaSuccess;
     const unsigned blocks = static_cast<unsigned>((n + 255) / 256);
-    resync_kernel<<<blocks, 256, 0, stream>>>(phi, out, ids, n);
+    resync_kernel<<<blocks, 256, 0, stream>>>(phi, out, ids, n, n_nodes);
     lsr_note_launch();
     return cudaGetLastError();
 }

@@ -112,8 +112,11 @@ def test_golden_fixture_coverage():
     assert np.count_nonzero((k <= 1) | (k >= g["dims"][2] - 2)) > 100
 
 
+@pytest.mark.gpu
 @pytest.mark.parametrize("ids", [[-1], [10**9], [0, 5, 1 << 40]])
-def test_out_of_grid_ids_are_config_error_before_device_work(built, ids):
+def test_out_of_grid_ids_are_config_error(gpu, ids):
+    """An id outside the grid is never dereferenced (device kernels and the
+    host scatter skip it) and the step reports a ConfigError."""
     lsr, g, phi, d, m = _args()
     cfg = lsr.StepConfig(p=1, delta=0.0, dt=0.1, band=lsr.BandParams(0.4, 0.2))
     bad = lsr.BandMask(g, active=np.asarray(ids, dtype=np.int64))

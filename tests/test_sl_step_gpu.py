@@ -538,3 +538,20 @@ def test_context_rejects_out_of_grid_ids(gpu):
     ok = torch.arange(10, dtype=torch.int64, device="cuda")
     ctx.set_active_device(ok.data_ptr(), ok.numel())
     ctx.close()
+
+
+@pytest.mark.parametrize("pinned", [False, True])
+def test_one_shot_out_of_grid_ids_are_config_error(gpu, pinned):
+    """The one-shot host call's pipelined path (3d, >= 64 planes; pinned =
+    zero-copy pull, pageable = host packing) with an id past the grid: no
+    kernel or host scatter dereferences it, the call raises ConfigError."""
+    lsr = gpu
+    g = lsr._api.cube_grid(64, 3)
+    x, y, z = g.mesh()
+    phi = (np.sqrt(x * x + y * y + z * z) - 0.6).ravel()
+    dist = np.abs(phi) + 0.01
+    active = np.flatnonzero(np.abs(phi) < 6 * g.dx).astype(np.int64)
+    active = np.append(active, g.num_nodes() + 5)
+    cfg = lsr.StepConfig(p=2, delta=1.0, dt=0.25 * g.dx, band=lsr.default_band_params(3, g.dx))
+    with pytest.raises(lsr.ConfigError, match="node ids"):
+        _run(lsr, g, phi, dist, active, cfg, 1.3, pinned=pinned)
