@@ -65,17 +65,19 @@ def _sharded(lsr, g, phi0, dist, cfg, rcfg, iters, world, halo):
     return stats, fields, loop
 
 
-@pytest.mark.parametrize("dims,interp,world,halo", [
-    ((64, 64, 64), 1, 2, 6),
-    ((64, 64, 64), 1, 3, 6),
-    ((40, 48, 56), 0, 2, 5),    # nx % 16 != 0: the scalar band passes
-    ((64, 64, 64), 1, 2, 3),    # too small a halo: widened and redone
+@pytest.mark.parametrize("dims,interp,world,halo,p,delta", [
+    ((64, 64, 64), 1, 2, 6, 2, 1.0),
+    ((64, 64, 64), 1, 3, 6, 2, 1.0),
+    ((40, 48, 56), 0, 2, 5, 2, 1.0),    # nx % 16 != 0: the scalar band passes
+    ((64, 64, 64), 1, 2, 3, 2, 1.0),    # too small a halo: widened and redone
+    ((64, 64, 64), 1, 4, 6, 1, 0.0),    # p = 1, delta = 0: no z-line table, coinciding feet
+    ((48, 32, 96), 1, 3, 6, 2, 0.5),    # elongated grid, delta = 1/2
 ])
-def test_slab_loop_matches_single_gpu_loop(gpu, dims, interp, world, halo):
+def test_slab_loop_matches_single_gpu_loop(gpu, dims, interp, world, halo, p, delta):
     lsr = gpu
     g, phi0, dist = _case(lsr, dims)
     bp = lsr.default_band_params(3, g.dx)
-    cfg = lsr.StepConfig(p=2, delta=1.0, dt=0.25 * g.dx, band=bp, interp=lsr.InterpolatorKind(interp))
+    cfg = lsr.StepConfig(p=p, delta=delta, dt=0.25 * g.dx, band=bp, interp=lsr.InterpolatorKind(interp))
     rcfg = lsr.ReinitConfig.defaults(g.dx, bp.gamma)
     iters = 4
     ref_stats, ref_fields = _single(lsr, g, phi0, dist, cfg, rcfg, iters)
