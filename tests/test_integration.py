@@ -8,6 +8,9 @@ liblsr_b200.so in place of the units it replaces (oracle/Makefile target
   Option A: minus evolve.cpp                          (sl_step on the GPU)
   Option B: minus evolve.cpp, grid.cpp, distance.cpp, reinit.cpp
             (band, clamp, distance field, reinitialisation on the GPU too)
+  Option C: all reference units and headers + include/lsr_cuda.h, the
+            snippet's lsr_cuda_sl_step_host call beside lsr::sl_step
+            (tests/cpp/capi_snippet_main.cpp)
 
 CPU tests: all three programs build and link, and liblsr_b200.so defines
 every external lsr:: symbol the replaced reference units define. GPU test:
@@ -78,3 +81,18 @@ def test_run_schedule_bit_identical_in_all_builds(gpu, tmp_path):
     assert len(out["ref"]) > 1_000_000
     assert out["optA"] == out["ref"]
     assert out["optB"] == out["ref"]
+
+
+@pytest.mark.gpu
+def test_option_c_snippet_matches_reference_sl_step(gpu):
+    """INTEGRATION.md Option C (the C-ABI call in place of lsr::sl_step,
+    compiled against the reference's own headers) writes the same bytes into
+    `next` as the reference's lsr::sl_step: 2d and 3d, Q1 and WENO, (p, delta)
+    in {(1, 0), (2, 1), (2, 1/2)}, including a 72^3 grid that takes the
+    pipelined one-shot path."""
+    exe = os.path.join(REF_DIR, "capi_snippet")
+    if not os.path.exists(exe):
+        pytest.skip("integration programs not built (no reference tree on this machine)")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), (r.stdout, r.stderr)
+    assert r.stdout.count(" 0 differ") == 5, r.stdout
