@@ -557,6 +557,133 @@ __global__ void __launch_bounds__(kJacThreads, LSR_JAC_MINB)
     }
 }
 
+// The same sweep as a persistent, software-pipelined kernel: each thread
+// walks the node list in rounds of kPipeNPT nodes (stride = the grid's
+// thread count, so consecutive threads keep consecutive list entries) and
+// issues the next round's id / sign / neighbour-mask loads before it waits
+// on the current round's seven gathers, so a thread always has two rounds of
+// loads in flight instead of one batch per CTA lifetime (the per-node
+// arithmetic is jacobi's: same bits).
+#ifndef LSR_JAC_PIPE
+#define LSR_JAC_PIPE 1
+#endif
+#ifndef LSR_JAC_PIPE_NPT
+#define LSR_JAC_PIPE_NPT 2
+#endif
+#ifndef LSR_JAC_PIPE_THREADS
+#define LSR_JAC_PIPE_THREADS 256
+#endif
+#ifndef LSR_JAC_PIPE_MINB
+#define LSR_JAC_PIPE_MINB 3
+#endif
+constexpr int kPipeNPT = LSR_JAC_PIPE_NPT;
+constexpr int kPipeThreads = LSR_JAC_PIPE_THREADS;
+
+template <class IdT>
+__global__ void __launch_bounds__(kPipeThreads, LSR_JAC_PIPE_MINB)
+    jacobi_pipe(SlParams P, const double* __restrict__ cur, double* __restrict__ nxt, const IdT* __restrict__ nodes,
+                const double* __restrict__ sgn, const unsigned char* __restrict__ nbr, long long nn, double dtau,
+                IterState* __restrict__ st) {
+    const long long T = static_cast<long long>(gridDim.x) * blockDim.x;
+    const long long g = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const long long stv[3] = {1, P.nx, P.nxy};
+    long long id[kPipeNPT];
+    double sg[kPipeNPT];
+    unsigned mk[kPipeNPT];
+    long long t0 = g;  // this thread's first node of the round: t0 + r * T, r < kPipeNPT
+#pragma unroll
+    for (int r = 0; r < kPipeNPT; ++r) {
+        const long long t = t0 + r * T;
+        id[r] = t < nn ? static_cast<long long>(nodes[t]) : -1;
+        sg[r] = t < nn ? sgn[t] : 0.0;
+        mk[r] = t < nn ? nbr[t] : 0u;
+    }
+    if (*reinterpret_cast<volatile int*>(&st->done)) return;
+    unsigned long long bitsmax = 0;
+    while (__syncthreads_or(id[0] >= 0)) {
+        // this round's gathers
+        double pc[kPipeNPT], vm[kPipeNPT][3], vp[kPipeNPT][3];
+        bool hm[kPipeNPT][3], hp[kPipeNPT][3];
+#pragma unroll
+        for (int r = 0; r < kPipeNPT; ++r) {
+            pc[r] = id[r] >= 0 ? __ldg(cur + id[r]) : 0.0;
+#pragma unroll
+            for (int ax = 0; ax < 3; ++ax) {
+                hm[r][ax] = (mk[r] >> (2 * ax)) & 1u;
+                hp[r][ax] = (mk[r] >> (2 * ax + 1)) & 1u;
+                vm[r][ax] = hm[r][ax] ? __ldg(cur + id[r] - stv[ax]) : 0.0;
+                vp[r][ax] = hp[r][ax] ? __ldg(cur + id[r] + stv[ax]) : 0.0;
+            }
+        }
+        // the next round's list entries, in flight while this round computes
+        const long long tn = t0 + kPipeNPT * T;
+        long long idn[kPipeNPT];
+        double sgn_n[kPipeNPT];
+        unsigned mkn[kPipeNPT];
+#pragma unroll
+        for (int r = 0; r < kPipeNPT; ++r) {
+            const long long t = tn + r * T;
+            idn[r] = t < nn ? static_cast<long long>(nodes[t]) : -1;
+            sgn_n[r] = t < nn ? sgn[t] : 0.0;
+            mkn[r] = t < nn ? nbr[t] : 0u;
+        }
+#pragma unroll
+        for (int r = 0; r < kPipeNPT; ++r) {
+            if (id[r] < 0) continue;
+            const double s = sg[r];
+            double gn;
+            if (!(LSR_JAC_INTERIOR && P.dim == 3 && mk[r] == 63u && godunov_interior(P, pc[r], vm[r], vp[r], s, gn)))
+                gn = godunov_vals(P, pc[r], vm[r], vp[r], hm[r], hp[r], s);
+            const double upd = -dtau * s * (gn - 1.0);
+            nxt[id[r]] = pc[r] + upd;
+            const double a = fabs(upd);
+            if (a > 0.0) {
+                const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(a));
+                bitsmax = b > bitsmax ? b : bitsmax;
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < kPipeNPT; ++r) {
+            id[r] = idn[r];
+            sg[r] = sgn_n[r];
+            mk[r] = mkn[r];
+        }
+        t0 = tn;
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        const unsigned long long o = __shfl_xor_sync(0xffffffffu, bitsmax, off);
+        bitsmax = o > bitsmax ? o : bitsmax;
+    }
+    __shared__ unsigned long long wmax[kPipeThreads / 32];
+    if ((threadIdx.x & 31) == 0) wmax[threadIdx.x >> 5] = bitsmax;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long m = 0;
+#pragma unroll
+        for (int w = 0; w < kPipeThreads / 32; ++w) m = wmax[w] > m ? wmax[w] : m;
+        if (m) atomicMax(&st->residual_bits, m);
+    }
+}
+
+// one sweep cur -> nxt over the node list (W.nodes32 when the ids fit 4 bytes)
+template <class IdT>
+static void launch_jacobi(const SlParams& P, const double* cur, double* nxt, const IdT* ids, const ReinitBuffers& W,
+                          long long nn, double dtau, IterState* st, cudaStream_t s) {
+    if (nn <= 0) return;
+    if (LSR_JAC_PIPE) {
+        // persistent: the resident CTAs (148 SMs x LSR_JAC_PIPE_MINB), or fewer for short lists
+        const long long want = (nn + kPipeThreads * kPipeNPT - 1) / (kPipeThreads * kPipeNPT);
+        const long long cap = 148LL * LSR_JAC_PIPE_MINB;
+        jacobi_pipe<<<static_cast<unsigned>(want < cap ? want : cap), kPipeThreads, 0, s>>>(P, cur, nxt, ids, W.sgn,
+                                                                                            W.nbr, nn, dtau, st);
+    } else {
+        const unsigned g = static_cast<unsigned>((nn + kJacThreads * kJacNPT - 1) / (kJacThreads * kJacNPT));
+        jacobi<<<g, kJacThreads, 0, s>>>(P, cur, nxt, ids, W.sgn, W.nbr, nn, dtau, st);
+    }
+    lsr_note_launch();
+}
+
 // the stop rule after a sweep (reinit.cpp:275-278)
 __global__ void iter_check(IterState* st, double tol) {
     if (st->done) return;
@@ -850,16 +977,8 @@ int lsr_reinit_iterate(const SlParams& P, double** phi, double** scratch, const 
     BR_TRY(cudaMemsetAsync(st, 0, sizeof(IterState), s));
     double* buf[2] = {*phi, *scratch};
     for (int k = 0; k < R.max_iters; ++k) {
-        if (nn > 0) {
-            const unsigned g = static_cast<unsigned>((nn + kJacThreads * kJacNPT - 1) / (kJacThreads * kJacNPT));
-            if (n <= 0xffffffffLL)
-                jacobi<<<g, kJacThreads, 0, s>>>(P, buf[k & 1], buf[(k + 1) & 1], W.nodes32, W.sgn, W.nbr, nn, R.dtau,
-                                                 st);
-            else
-                jacobi<<<g, kJacThreads, 0, s>>>(P, buf[k & 1], buf[(k + 1) & 1], W.nodes, W.sgn, W.nbr, nn, R.dtau,
-                                                 st);
-            lsr_note_launch();
-        }
+        if (n <= 0xffffffffLL) launch_jacobi(P, buf[k & 1], buf[(k + 1) & 1], W.nodes32, W, nn, R.dtau, st, s);
+        else launch_jacobi(P, buf[k & 1], buf[(k + 1) & 1], W.nodes, W, nn, R.dtau, st, s);
         iter_check<<<1, 1, 0, s>>>(st, tol);
         lsr_note_launch();
     }
@@ -1042,14 +1161,10 @@ int lsr_reinit_slab_sweep(const SlParams& P, const double* cur_g, double* nxt_g,
                           double dtau, double* residual, cudaStream_t s, std::string* err) {
     IterState* st = reinterpret_cast<IterState*>(W.scal);
     BR_TRY(cudaMemsetAsync(st, 0, sizeof(IterState), s));
-    if (nn > 0) {
-        const unsigned g = static_cast<unsigned>((nn + kJacThreads * kJacNPT - 1) / (kJacThreads * kJacNPT));
-        if (static_cast<long long>(P.nxy) * P.nz <= 0xffffffffLL)
-            jacobi<<<g, kJacThreads, 0, s>>>(P, cur_g, nxt_g, W.nodes32, W.sgn, W.nbr, nn, dtau, st);
-        else
-            jacobi<<<g, kJacThreads, 0, s>>>(P, cur_g, nxt_g, W.nodes, W.sgn, W.nbr, nn, dtau, st);
-        lsr_note_launch();
-    }
+    if (static_cast<long long>(P.nxy) * P.nz <= 0xffffffffLL)
+        launch_jacobi(P, cur_g, nxt_g, W.nodes32, W, nn, dtau, st, s);
+    else
+        launch_jacobi(P, cur_g, nxt_g, W.nodes, W, nn, dtau, st, s);
     unsigned long long bits = 0;
     BR_TRY(cudaMemcpyAsync(&bits, &st->residual_bits, sizeof bits, cudaMemcpyDeviceToHost, s));
     BR_TRY(cudaStreamSynchronize(s));
