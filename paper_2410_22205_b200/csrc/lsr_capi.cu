@@ -412,6 +412,7 @@ int lsr_cuda_mark_dirty(lsr_cuda_ctx* c, int which) {
 }
 
 int lsr_cuda_set_active(lsr_cuda_ctx* c, const int64_t* ids, int64_t n) {
+    if (c && c->slab) return set_err(LSR_ERR_CONFIG, "set_active: a z-slab context (use lsr_cuda_slab_*)");
     if (!c || (n > 0 && !ids) || n < 0) return set_err(LSR_ERR_CONFIG, "set_active: bad argument");
     if (!ids_in_grid(ids, n, c->n)) return set_err(LSR_ERR_CONFIG, "set_active: ids must be node ids of the grid");
     LSR_CUDA_TRY(cudaSetDevice(c->device));
@@ -426,6 +427,7 @@ int lsr_cuda_set_active(lsr_cuda_ctx* c, const int64_t* ids, int64_t n) {
 }
 
 int lsr_cuda_set_active_device(lsr_cuda_ctx* c, const int64_t* d_ids, int64_t n) {
+    if (c && c->slab) return set_err(LSR_ERR_CONFIG, "set_active_device: a z-slab context (use lsr_cuda_slab_*)");
     if (!c || (n > 0 && !d_ids) || n < 0) return set_err(LSR_ERR_CONFIG, "set_active_device: bad argument");
     LSR_CUDA_TRY(cudaSetDevice(c->device));
     if (int st = ensure_ids(&c->active, &c->cap_active, n)) return st;
@@ -528,6 +530,7 @@ int enqueue_step(lsr_cuda_ctx* c, const lsr_step_cfg* cfg, double energy_p, bool
 }  // namespace
 
 int lsr_cuda_sl_step(lsr_cuda_ctx* c, const lsr_step_cfg* cfg, double energy_p, int64_t* bad_node) {
+    if (c && c->slab) return set_err(LSR_ERR_CONFIG, "sl_step: a z-slab context (use lsr_cuda_slab_*)");
     if (bad_node) *bad_node = -1;
     if (!c) return set_err(LSR_ERR_CONFIG, "null context");
     c->seq++;  // may write phi or out
@@ -548,6 +551,7 @@ int lsr_cuda_sl_step(lsr_cuda_ctx* c, const lsr_step_cfg* cfg, double energy_p, 
 }
 
 int lsr_cuda_sl_step_async(lsr_cuda_ctx* c, const lsr_step_cfg* cfg, double energy_p) {
+    if (c && c->slab) return set_err(LSR_ERR_CONFIG, "sl_step_async: a z-slab context (use lsr_cuda_slab_*)");
     if (!c) return set_err(LSR_ERR_CONFIG, "null context");
     c->seq++;  // may write phi or out
     if (int st = check_cfg(cfg, energy_p)) return st;
@@ -1246,6 +1250,7 @@ int lsr_cuda_sl_step_host(const lsr_grid* grid, const double* phi, const double*
 
 int lsr_cuda_ctx_build_distance(lsr_cuda_ctx* c, const double* pts, int64_t n, int dim, int seed_only,
                                 double* sentinel, int* rounds) {
+    if (c && c->slab) return set_err(LSR_ERR_CONFIG, "ctx_build_distance: a z-slab context (use lsr_cuda_slab_*)");
     if (!c || (n > 0 && !pts)) return set_err(LSR_ERR_CONFIG, "build_distance: null argument");
     LSR_CUDA_TRY(cudaSetDevice(c->device));
     if (!c->exact) LSR_CUDA_TRY(cudaMalloc(&c->exact, static_cast<size_t>(c->n)));
@@ -1263,6 +1268,7 @@ int lsr_cuda_ctx_build_distance(lsr_cuda_ctx* c, const double* pts, int64_t n, i
 }
 
 int lsr_cuda_surface_energy(lsr_cuda_ctx* c, int which, int p, int refine, double* energy) {
+    if (c && c->slab) return set_err(LSR_ERR_CONFIG, "surface_energy: a z-slab context (use lsr_cuda_slab_*)");
     if (!c || !energy) return set_err(LSR_ERR_CONFIG, "surface_energy: null argument");
     double** slot = field_slot(c, which);
     if (!slot || which == LSR_FIELD_DIST) return set_err(LSR_ERR_CONFIG, "surface_energy: phi must be PHI or OUT");
@@ -1317,6 +1323,7 @@ static SlParams grid_params(const lsr_grid& g) {
 }
 
 int lsr_cuda_narrow_band(lsr_cuda_ctx* c, int which, double gamma, int64_t* n_active, int64_t* n_tube) {
+    if (c && c->slab) return set_err(LSR_ERR_CONFIG, "narrow_band: a z-slab context (use lsr_cuda_slab_*)");
     if (!c) return set_err(LSR_ERR_CONFIG, "null context");
     double** slot = field_slot(c, which);
     if (!slot || which == LSR_FIELD_DIST) return set_err(LSR_ERR_CONFIG, "narrow_band: phi must be PHI or OUT");
@@ -1353,6 +1360,7 @@ int lsr_cuda_band_download(lsr_cuda_ctx* c, uint8_t* state, int64_t* active, int
 }
 
 int lsr_cuda_clamp_field(lsr_cuda_ctx* c, int which, double gamma) {
+    if (c && c->slab) return set_err(LSR_ERR_CONFIG, "clamp_field: a z-slab context (use lsr_cuda_slab_*)");
     if (!c) return set_err(LSR_ERR_CONFIG, "null context");
     double** slot = field_slot(c, which);
     if (!slot) return set_err(LSR_ERR_CONFIG, "clamp_field: unknown field");
@@ -1390,11 +1398,13 @@ static int reinitialize_impl(lsr_cuda_ctx* c, int which, double gamma, const lsr
 
 int lsr_cuda_reinitialize(lsr_cuda_ctx* c, int which, double gamma, const lsr_reinit_cfg* rc, int* iterations,
                           int* had_interface) {
+    if (c && c->slab) return set_err(LSR_ERR_CONFIG, "reinitialize: a z-slab context (use lsr_cuda_slab_*)");
     return reinitialize_impl(c, which, gamma, rc, iterations, had_interface, false);
 }
 
 int lsr_cuda_set_band(lsr_cuda_ctx* c, const uint8_t* state, const int64_t* active, int64_t n_active,
                       const int64_t* tube, int64_t n_tube) {
+    if (c && c->slab) return set_err(LSR_ERR_CONFIG, "set_band: a z-slab context (use lsr_cuda_slab_*)");
     if (!c || !state || (n_active > 0 && !active) || (n_tube > 0 && !tube))
         return set_err(LSR_ERR_CONFIG, "set_band: null argument");
     if (n_active < 0 || n_tube < 0 || n_active > c->n || n_tube > c->n)
@@ -1422,6 +1432,7 @@ int lsr_cuda_set_band(lsr_cuda_ctx* c, const uint8_t* state, const int64_t* acti
 }
 
 int lsr_cuda_interface_one_step(lsr_cuda_ctx* c, int which, uint8_t* frozen, int* had_interface) {
+    if (c && c->slab) return set_err(LSR_ERR_CONFIG, "interface_one_step: a z-slab context (use lsr_cuda_slab_*)");
     if (!c) return set_err(LSR_ERR_CONFIG, "null context");
     c->seq++;  // may write phi or out
     double** slot = field_slot(c, which);
@@ -1444,6 +1455,7 @@ int lsr_cuda_interface_one_step(lsr_cuda_ctx* c, int which, uint8_t* frozen, int
 
 int lsr_cuda_reinit_iterate(lsr_cuda_ctx* c, int which, const uint8_t* frozen, const lsr_reinit_cfg* rc,
                             int* iterations) {
+    if (c && c->slab) return set_err(LSR_ERR_CONFIG, "reinit_iterate: a z-slab context (use lsr_cuda_slab_*)");
     if (!c || !rc) return set_err(LSR_ERR_CONFIG, "reinit_iterate: null argument");
     double** slot = field_slot(c, which);
     if (!slot || which == LSR_FIELD_DIST) return set_err(LSR_ERR_CONFIG, "reinit_iterate: phi must be PHI or OUT");
@@ -1467,6 +1479,7 @@ int lsr_cuda_reinit_iterate(lsr_cuda_ctx* c, int which, const uint8_t* frozen, c
 }
 
 int lsr_cuda_fast_sweep(lsr_cuda_ctx* c, const uint8_t* exact, double sentinel, int* rounds) {
+    if (c && c->slab) return set_err(LSR_ERR_CONFIG, "fast_sweep: a z-slab context (use lsr_cuda_slab_*)");
     if (!c) return set_err(LSR_ERR_CONFIG, "null context");
     LSR_CUDA_TRY(cudaSetDevice(c->device));
     if (!c->exact) {
@@ -1503,6 +1516,7 @@ void lsr_cuda_reinit_defaults(double dx, double gamma, lsr_reinit_cfg* rc) {  //
 
 int lsr_cuda_loop_step(lsr_cuda_ctx* c, const lsr_step_cfg* cfg, const lsr_reinit_cfg* rc, int energy_refine,
                        double energy_override, lsr_loop_stats* stats) {
+    if (c && c->slab) return set_err(LSR_ERR_CONFIG, "loop_step: a z-slab context (use lsr_cuda_slab_*)");
     if (!c || !cfg || !rc) return set_err(LSR_ERR_CONFIG, "loop_step: null argument");
     if (int st = check_cfg(cfg, 1.0)) return st;
     LSR_CUDA_TRY(cudaSetDevice(c->device));
