@@ -802,13 +802,12 @@ int lsr_band_build(const SlParams& P, const double* phi, double gamma, BandBuffe
     unsigned char* t = reinterpret_cast<unsigned char*>(B.active);
     unsigned char* u = reinterpret_cast<unsigned char*>(B.tube);
     band_passes(P, phi, gamma, 0, n, 0, n, t, u, B.state, s);
-    const size_t tb = lsr_compact::scratch_bytes(n);
+    // ACTIVE and tube lists from one count pass and one write pass over the state bytes
+    const size_t tb = lsr_compact::scratch_bytes2(n);
     if (int st = ensure_tmp(B, tb, err)) return st;
-    BR_TRY(lsr_compact::compact(lsr_compact::BytePred<StateIs1>{B.state, {}}, lsr_compact::Identity{}, n, B.active,
-                                B.counts, B.tmp, tb, s));
-    BR_TRY(lsr_compact::compact(lsr_compact::BytePred<NonZero>{B.state, {}}, lsr_compact::Identity{}, n, B.tube,
-                                B.counts + 1, B.tmp, tb, s));
-    for (int q = 0; q < 4; ++q) lsr_note_launch();
+    BR_TRY(lsr_compact::compact2(lsr_compact::BytePred<StateIs1>{B.state, {}}, NonZero{}, lsr_compact::Identity{}, n,
+                                 B.active, B.tube, B.counts, B.tmp, tb, s));
+    for (int q = 0; q < 2; ++q) lsr_note_launch();
     long long h[2];
     BR_TRY(cudaMemcpyAsync(h, B.counts, sizeof h, cudaMemcpyDeviceToHost, s));
     BR_TRY(cudaStreamSynchronize(s));
@@ -1073,13 +1072,11 @@ int lsr_band_build_slab(const SlParams& P, const double* phi_g, double gamma, Ba
     const long long a1 = static_cast<long long>(min(own_hi + 1, win_hi)) * P.nxy;
     const long long b0 = static_cast<long long>(own_lo) * P.nxy, b1 = static_cast<long long>(own_hi) * P.nxy;
     band_passes(P, phi_g, gamma, a0, a1, b0, b1, t, u, state, s);
-    const size_t tb = lsr_compact::scratch_bytes(b1 - b0);
+    const size_t tb = lsr_compact::scratch_bytes2(b1 - b0);
     if (int st = ensure_tmp(B, tb, err)) return st;
-    BR_TRY(lsr_compact::compact(lsr_compact::BytePred<StateIs1>{state + b0, {}}, OffsetId{b0}, b1 - b0, B.active,
-                                B.counts, B.tmp, tb, s));
-    BR_TRY(lsr_compact::compact(lsr_compact::BytePred<NonZero>{state + b0, {}}, OffsetId{b0}, b1 - b0, B.tube,
-                                B.counts + 1, B.tmp, tb, s));
-    for (int q = 0; q < 4; ++q) lsr_note_launch();
+    BR_TRY(lsr_compact::compact2(lsr_compact::BytePred<StateIs1>{state + b0, {}}, NonZero{}, OffsetId{b0}, b1 - b0,
+                                 B.active, B.tube, B.counts, B.tmp, tb, s));
+    for (int q = 0; q < 2; ++q) lsr_note_launch();
     long long h[2];
     BR_TRY(cudaMemcpyAsync(h, B.counts, sizeof h, cudaMemcpyDeviceToHost, s));
     BR_TRY(cudaStreamSynchronize(s));
