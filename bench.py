@@ -773,6 +773,7 @@ def cpu_baseline(g, phi, ctx, active, step, e2, lsr, reps=3):
     cc = dict(p=step.p, interp=int(step.interp), delta=step.delta, dt=step.dt, fallback_c=step.fallback_c,
               fallback_alpha=step.fallback_alpha, gamma=step.band.gamma, beta=step.band.beta)
     threads = os.cpu_count() or 1
+    serial = None
     if bindings.reference_available():
         R = bindings.Reference()
         R.set_threads(threads)
@@ -780,6 +781,16 @@ def cpu_baseline(g, phi, ctx, active, step, e2, lsr, reps=3):
         secs = [R.ctx_sl_step(h, cc, e2, serial=False) for _ in range(reps)]
         R.ctx_free(h)
         kind = "reference"
+        # lsr::ref::sl_step on 1 thread too, on a bounded
+        # sample of the band (every k-th active node; its O(N) copy included)
+        k = max(1, active.size // 400_000)
+        sample = np.ascontiguousarray(active[::k])
+        h = R.ctx(gd, phi, d, sample)
+        ssec = min(R.ctx_sl_step(h, cc, e2, serial=True) for _ in range(2))
+        R.ctx_free(h)
+        serial = {"value": sample.size / ssec, "unit": UNIT, "cores": 1,
+                  "sample": f"every {k}th active node ({sample.size} nodes), lsr::ref::sl_step incl. its O(N) copy, "
+                            f"best of 2", "seconds": ssec}
     else:
         O = bindings.Restatement()
         secs = []
@@ -789,9 +800,12 @@ def cpu_baseline(g, phi, ctx, active, step, e2, lsr, reps=3):
             secs.append(time.perf_counter() - t0)
         kind = "port"
     best = min(secs)
-    return {"value": active.size / best, "unit": UNIT, "cores": threads, "cpu_model": cpu_model(), "kind": kind,
-            "sample": f"full band ({active.size} active nodes) of the same workload, best of {reps} calls of "
-                      f"lsr::sl_step incl. its internal O(N) copy", "seconds": secs}
+    out = {"value": active.size / best, "unit": UNIT, "cores": threads, "cpu_model": cpu_model(), "kind": kind,
+           "sample": f"full band ({active.size} active nodes) of the same workload, best of {reps} calls of "
+                     f"lsr::sl_step incl. its internal O(N) copy", "seconds": secs}
+    if serial:
+        out["serial_reference"] = serial
+    return out
 
 
 # ---------------------------------------------------------------------------
