@@ -133,6 +133,10 @@ int lsr_cuda_async_times(lsr_cuda_ctx* ctx, float* kernel_ms, float* step_ms, fl
                          int* n);
 /* std::swap(phi.values, next.values) (driver.cpp:203): O(1) */
 int lsr_cuda_swap(lsr_cuda_ctx* ctx);
+/* 3d WENO step form: 0 = the z-line table kernel (default), 1 = each 8^3
+ * brick's phi (+ halo) staged in shared memory by one TMA tensor copy
+ * (the measured alternative); same bits either way */
+int lsr_cuda_set_sl_mode(lsr_cuda_ctx* ctx, int mode);
 /* device time (ms, CUDA events on the context stream) of the last SL kernel
  * and of the last whole sl_step (sync of out + kernel) */
 int lsr_cuda_last_times(lsr_cuda_ctx* ctx, float* kernel_ms, float* step_ms);

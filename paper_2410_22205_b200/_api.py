@@ -112,6 +112,7 @@ def lib() -> C.CDLL:
     L.lsr_cuda_set_active_device.argtypes = [C.c_void_p, C.c_void_p, C.c_int64]
     L.lsr_cuda_sl_step.argtypes = [C.c_void_p, P(CStepCfg), C.c_double, P(C.c_int64)]
     L.lsr_cuda_swap.argtypes = [C.c_void_p]
+    L.lsr_cuda_set_sl_mode.argtypes = [C.c_void_p, C.c_int]
     L.lsr_cuda_sl_step_async.argtypes = [C.c_void_p, P(CStepCfg), C.c_double]
     L.lsr_cuda_sync.argtypes = [C.c_void_p, P(C.c_int64)]
     L.lsr_cuda_async_times.argtypes = [C.c_void_p, P(C.c_float), P(C.c_float), P(C.c_float), C.c_int, P(C.c_int)]
@@ -558,6 +559,10 @@ class Context:
 
     def swap(self):
         _check(lib().lsr_cuda_swap(self.h))
+
+    def set_sl_mode(self, mode: int):
+        """3d WENO step form: 0 = z-line table (default), 1 = TMA-staged bricks."""
+        _check(lib().lsr_cuda_set_sl_mode(self.h, int(mode)))
 
     def build_distance(self, points: np.ndarray, dim: int | None = None, seed_only: bool = False):
         """Device-resident lsr::build_distance_field into the DIST field."""

@@ -183,6 +183,12 @@ struct lsr_cuda_ctx {
     uint64_t seq = 1, clamped_seq = 0;
     const double* clamped_phi = nullptr;
     double clamped_gamma = 0.0;
+    // SL step form for 3d WENO: 0 = z-line table (default), 1 = TMA bricks
+    // (sl_step_box_kernel); the brick grouping is kept per active set
+    int sl_mode = 0;
+    BoxBuffers box{};
+    long long box_nb = 0, box_cap_ids = 0, box_listed = 0;
+    bool box_valid = false;
     bool slab = false;
     int win_lo = 0, win_hi = 0, own_lo = 0, own_hi = 0;
     EnergySlabWork ew;
@@ -341,6 +347,13 @@ int lsr_cuda_destroy(lsr_cuda_ctx* c) {
     cudaFree(c->zt.reach);
     cudaFree(c->zt.list);
     cudaFree(c->zt.count);
+    cudaFree(c->box.count);
+    cudaFree(c->box.off);
+    cudaFree(c->box.cursor);
+    cudaFree(c->box.list);
+    cudaFree(c->box.d_listed);
+    cudaFree(c->box.ids);
+    cudaFree(c->box.tmp);
     for (auto& e : c->ev_down)
         if (e) cudaEventDestroy(e);
     for (auto& e : c->ev_up)
@@ -380,7 +393,8 @@ int lsr_cuda_upload_field(lsr_cuda_ctx* c, int which, const double* host) {
     LSR_CUDA_TRY(cudaMemcpyAsync(*slot, host, sizeof(double) * c->n, cudaMemcpyHostToDevice, c->stream));
     LSR_CUDA_TRY(cudaStreamSynchronize(c->stream));
     if (which != LSR_FIELD_DIST) c->consistent = false;
-    else c->zt_bricks = false;  // the covered bricks depend on d
+    else c->zt_bricks = false;
+    c->box_valid = false;  // the covered bricks depend on d
     return LSR_OK;
 }
 
@@ -408,6 +422,7 @@ int lsr_cuda_mark_dirty(lsr_cuda_ctx* c, int which) {
     c->seq++;  // may write phi or out
     if (which != LSR_FIELD_DIST) c->consistent = false;
     else c->zt_bricks = false;
+    c->box_valid = false;
     return LSR_OK;
 }
 
@@ -422,6 +437,7 @@ int lsr_cuda_set_active(lsr_cuda_ctx* c, const int64_t* ids, int64_t n) {
     LSR_CUDA_TRY(cudaStreamSynchronize(c->stream));
     c->n_active = n;
     c->zt_bricks = false;
+    c->box_valid = false;
     c->dirty_is_active = false;
     return LSR_OK;
 }
@@ -446,6 +462,7 @@ int lsr_cuda_set_active_device(lsr_cuda_ctx* c, const int64_t* d_ids, int64_t n)
     }
     c->n_active = n;
     c->zt_bricks = false;
+    c->box_valid = false;
     c->dirty_is_active = false;
     return LSR_OK;
 }
@@ -461,8 +478,33 @@ int enqueue_step(lsr_cuda_ctx* c, const lsr_step_cfg* cfg, double energy_p, bool
     cudaStream_t s = c->stream;
     // delta = 0: the four feet coincide and one interpolation per node does
     // not amortise the fill (1.31 vs 1.27 ms at 512^3), so no table
-    const bool use_table = LSR_ZTAB && c->grid.dim == 3 && cfg->interp == 1 && P.fast_weno && c->grid.dims[2] >= 4 &&
-                           cfg->delta > 0.0;
+    const bool use_box = c->sl_mode == 1 && c->grid.dim == 3 && cfg->interp == 1 && P.fast_weno;
+    const bool use_table = !use_box && LSR_ZTAB && c->grid.dim == 3 && cfg->interp == 1 && P.fast_weno &&
+                           c->grid.dims[2] >= 4 && cfg->delta > 0.0;
+    if (use_box && !c->box_valid) {
+        const long long nb = static_cast<long long>((c->grid.dims[0] + 7) / 8) * ((c->grid.dims[1] + 7) / 8) *
+                             ((c->grid.dims[2] + 7) / 8);
+        if (nb > c->box_nb) {
+            for (void* q : {static_cast<void*>(c->box.count), static_cast<void*>(c->box.off),
+                            static_cast<void*>(c->box.cursor), static_cast<void*>(c->box.list), c->box.tmp})
+                cudaFree(q);
+            c->box.tmp_bytes = box_tmp_bytes(nb);
+            LSR_CUDA_TRY(cudaMalloc(&c->box.count, sizeof(unsigned) * (nb + 1)));
+            LSR_CUDA_TRY(cudaMalloc(&c->box.off, sizeof(unsigned) * (nb + 1)));
+            LSR_CUDA_TRY(cudaMalloc(&c->box.cursor, sizeof(unsigned) * nb));
+            LSR_CUDA_TRY(cudaMalloc(&c->box.list, sizeof(unsigned) * nb));
+            LSR_CUDA_TRY(cudaMalloc(&c->box.tmp, c->box.tmp_bytes));
+            if (!c->box.d_listed) LSR_CUDA_TRY(cudaMalloc(&c->box.d_listed, sizeof(long long)));
+            c->box_nb = nb;
+        }
+        if (c->n_active > c->box_cap_ids) {
+            cudaFree(c->box.ids);
+            LSR_CUDA_TRY(cudaMalloc(&c->box.ids, sizeof(int64_t) * static_cast<size_t>(c->n_active)));
+            c->box_cap_ids = c->n_active;
+        }
+        LSR_CUDA_TRY(launch_box_bricks(P, c->active, c->n_active, c->box, &c->box_listed, s));
+        c->box_valid = true;
+    }
     if (use_table && !c->s_aux) {
         LSR_CUDA_TRY(cudaStreamCreateWithFlags(&c->s_aux, cudaStreamNonBlocking));
         LSR_CUDA_TRY(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
@@ -511,7 +553,9 @@ int enqueue_step(lsr_cuda_ctx* c, const lsr_step_cfg* cfg, double energy_p, bool
         LSR_CUDA_TRY(cudaStreamWaitEvent(s, c->ev_join, 0));
     }
     LSR_CUDA_TRY(cudaEventRecord(ev[2], s));
-    LSR_CUDA_TRY(launch_sl_step(P, cfg->interp, c->phi, c->dist, c->active, c->n_active, c->out, c->d_bad, s));
+    if (!(use_box && launch_sl_step_box(P, c->phi, c->dist, c->box, c->box_listed, c->n_active, c->out, c->d_bad, s)))
+        LSR_CUDA_TRY(launch_sl_step(P, cfg->interp, c->phi, c->dist, c->active, c->n_active, c->out, c->d_bad, s));
+    LSR_CUDA_TRY(cudaGetLastError());
     LSR_CUDA_TRY(cudaEventRecord(ev[3], s));
     // the ids written now are where out may differ from phi after the swap
     if (!c->dirty_is_active) {
@@ -600,6 +644,13 @@ int lsr_cuda_async_times(lsr_cuda_ctx* c, float* kernel_ms, float* step_ms, floa
         if (table_ms) table_ms[i] = c->async_table_ms[i];
     }
     *n = m;
+    return LSR_OK;
+}
+
+int lsr_cuda_set_sl_mode(lsr_cuda_ctx* c, int mode) {
+    if (!c) return set_err(LSR_ERR_CONFIG, "null context");
+    if (mode != 0 && mode != 1) return set_err(LSR_ERR_CONFIG, "set_sl_mode: 0 (z-line table) or 1 (TMA bricks)");
+    c->sl_mode = mode;
     return LSR_OK;
 }
 
@@ -936,6 +987,7 @@ static int sl_step_host_pipelined(lsr_cuda_ctx* c, const double* phi, const doub
         LSR_CUDA_TRY(cudaMemcpyAsync(c->phi, phi, sizeof(double) * chunk_off(prefetch), cudaMemcpyHostToDevice, up));
     c->n_active = n_active;
     c->zt_bricks = false;
+    c->box_valid = false;
     c->dirty_is_active = false;
     c->consistent = false;
     // per-chunk ranges of the (ascending) ids
@@ -1232,6 +1284,7 @@ int lsr_cuda_sl_step_host(const lsr_grid* grid, const double* phi, const double*
         LSR_CUDA_TRY(cudaMemcpyAsync(c->active, active, sizeof(int64_t) * n_active, cudaMemcpyHostToDevice, s));
     c->n_active = n_active;
     c->zt_bricks = false;
+    c->box_valid = false;
     c->dirty_is_active = false;
     c->consistent = false;
     int64_t bad = -1;
@@ -1254,7 +1307,8 @@ int lsr_cuda_ctx_build_distance(lsr_cuda_ctx* c, const double* pts, int64_t n, i
     if (!c || (n > 0 && !pts)) return set_err(LSR_ERR_CONFIG, "build_distance: null argument");
     LSR_CUDA_TRY(cudaSetDevice(c->device));
     if (!c->exact) LSR_CUDA_TRY(cudaMalloc(&c->exact, static_cast<size_t>(c->n)));
-    c->zt_bricks = false;  // the covered bricks depend on d
+    c->zt_bricks = false;
+    c->box_valid = false;  // the covered bricks depend on d
     std::string err;
     double sent = 0.0;
     int r = 0;
@@ -1339,6 +1393,7 @@ int lsr_cuda_narrow_band(lsr_cuda_ctx* c, int which, double gamma, int64_t* n_ac
                                      c->stream));
     c->n_active = na;
     c->zt_bricks = false;
+    c->box_valid = false;
     c->dirty_is_active = false;
     if (n_active) *n_active = na;
     if (n_tube) *n_tube = nt;
@@ -1370,7 +1425,8 @@ int lsr_cuda_clamp_field(lsr_cuda_ctx* c, int which, double gamma) {
     if (int st = lsr_clamp(*slot, c->n, gamma, c->stream, &err)) return set_err(st, err);
     LSR_CUDA_TRY(cudaStreamSynchronize(c->stream));
     if (which != LSR_FIELD_DIST) c->consistent = false;
-    else c->zt_bricks = false;  // the covered bricks depend on d
+    else c->zt_bricks = false;
+    c->box_valid = false;  // the covered bricks depend on d
     return LSR_OK;
 }
 
@@ -1426,6 +1482,7 @@ int lsr_cuda_set_band(lsr_cuda_ctx* c, const uint8_t* state, const int64_t* acti
         LSR_CUDA_TRY(cudaMemcpyAsync(c->active, active, sizeof(int64_t) * n_active, cudaMemcpyHostToDevice, s));
     c->n_active = n_active;
     c->zt_bricks = false;
+    c->box_valid = false;
     c->dirty_is_active = false;
     LSR_CUDA_TRY(cudaStreamSynchronize(s));
     return LSR_OK;
@@ -1493,7 +1550,8 @@ int lsr_cuda_fast_sweep(lsr_cuda_ctx* c, const uint8_t* exact, double sentinel, 
     if (int st = lsr_prep_fast_sweep(&c->grid, c->dist, c->exact, sentinel, &r, c->stream, &err))
         return set_err(st, err);
     LSR_CUDA_TRY(cudaStreamSynchronize(c->stream));
-    c->zt_bricks = false;  // the covered bricks depend on d
+    c->zt_bricks = false;
+    c->box_valid = false;  // the covered bricks depend on d
     if (rounds) *rounds = r;
     return LSR_OK;
 }

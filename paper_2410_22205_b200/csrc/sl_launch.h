@@ -84,3 +84,22 @@ cudaError_t launch_scatter_runs(const double* packed, const long long* desc, lon
 // res[t] = field[ids[t]] for t < n
 cudaError_t launch_gather_ids(const double* field, const int64_t* ids, long long n, double* res, long long n_nodes,
                               cudaStream_t stream);
+
+// the TMA brick form of the 3d WENO step (sl_step.cu, sl_node_box): active
+// ids grouped by 8^3 brick; one CTA per non-empty brick stages the brick's
+// phi (+ halo) with one TMA tensor copy
+struct BoxBuffers {
+    unsigned* count = nullptr;   // nbricks + 1
+    unsigned* off = nullptr;     // nbricks + 1 (exclusive scan of count)
+    unsigned* cursor = nullptr;  // nbricks
+    unsigned* list = nullptr;    // non-empty bricks, ascending
+    long long* d_listed = nullptr;
+    int64_t* ids = nullptr;      // active ids grouped by brick
+    void* tmp = nullptr;
+    size_t tmp_bytes = 0;
+};
+size_t box_tmp_bytes(long long nbricks);
+cudaError_t launch_box_bricks(const lsr_dev::SlParams& P, const int64_t* active, long long n, const BoxBuffers& X,
+                              long long* n_listed, cudaStream_t stream);
+bool launch_sl_step_box(const lsr_dev::SlParams& P, const double* phi, const double* dist, const BoxBuffers& X,
+                        long long n_listed, long long n_ids, double* out, unsigned long long* bad, cudaStream_t stream);

@@ -8,11 +8,16 @@
 // node: consecutive lanes take consecutive ids, i.e. neighbouring nodes of
 // the same x-row, so their WENO stencils overlap and the 4x4x4 gathers hit
 // L1 and coalesce into few sectors per warp load.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
+
+#include <cub/cub.cuh>
 
 #include <algorithm>
 #include <cstdint>
 
+#include "compact.cuh"
 #include "sl_device.cuh"
 #include "sl_launch.h"
 
@@ -106,6 +111,100 @@ __global__ void __launch_bounds__(kSlThreadsW3, kSlMinBlocksW3) sl_step_zt_kerne
     const bool use_zt = __ldg(P.ztab_bad) == 0u;
     const double next = sl_node<3, 1>(P, phi, dist, id, i, j, k, use_zt);
     store_update(P, id, k, next, out, bad);
+}
+
+// ---- the TMA brick form of the 3d WENO step (sl_node_box) ----------------
+
+#ifndef LSR_BOX_MINB
+#define LSR_BOX_MINB 4
+#endif
+constexpr int kBoxThreads = 256;
+constexpr int kBoxMinBlocks = LSR_BOX_MINB;  // 4 x 52 KB of staged phi per SM
+constexpr int kBoxBytes = kBoxEX * kBoxEY * kBoxEZ * 8;
+
+__device__ __forceinline__ long long brick8_of(const SlParams& P, long long id, int nbx, int nby) {
+    int i, j, k;
+    unflatten(P, id, i, j, k);
+    return (static_cast<long long>(k / kSlBrick) * nby + j / kSlBrick) * nbx + i / kSlBrick;
+}
+
+// count[b] = active nodes in brick b (one atomic per (warp, brick))
+__global__ void box_count_kernel(SlParams P, const int64_t* __restrict__ active, long long n, int nbx, int nby,
+                                 unsigned* __restrict__ count) {
+    const long long a = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const long long b = a < n ? brick8_of(P, __ldg(active + a), nbx, nby) : -1;
+    const unsigned same = __match_any_sync(0xffffffffu, b);
+    if (b >= 0 && (threadIdx.x & 31) == static_cast<unsigned>(__ffs(same) - 1))
+        atomicAdd(count + b, static_cast<unsigned>(__popc(same)));
+}
+
+// ids grouped by brick: ids[off[b] + r] for the r-th of brick b's nodes (any order inside a brick)
+__global__ void box_scatter_kernel(SlParams P, const int64_t* __restrict__ active, long long n, int nbx, int nby,
+                                   const unsigned* __restrict__ off, unsigned* __restrict__ cursor,
+                                   int64_t* __restrict__ ids) {
+    const long long a = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t id = a < n ? __ldg(active + a) : 0;
+    const long long b = a < n ? brick8_of(P, id, nbx, nby) : -1;
+    const unsigned same = __match_any_sync(0xffffffffu, b);
+    const int lane = threadIdx.x & 31, lead = __ffs(same) - 1;
+    unsigned base = 0;
+    if (b >= 0 && lane == lead) base = atomicAdd(cursor + b, static_cast<unsigned>(__popc(same)));
+    base = __shfl_sync(same, base, lead);
+    if (b >= 0) ids[off[b] + base + __popc(same & ((1u << lane) - 1u))] = id;
+}
+
+struct NonEmpty {
+    const unsigned* count;
+    __device__ bool operator()(long long b) const { return count[b] != 0u; }
+};
+
+__device__ __forceinline__ unsigned box_smem_u32(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+
+__global__ void __launch_bounds__(kBoxThreads, kBoxMinBlocks) sl_step_box_kernel(const __grid_constant__ CUtensorMap tmap, SlParams P,
+                                                                  const double* __restrict__ phi,
+                                                                  const double* __restrict__ dist,
+                                                                  const unsigned* __restrict__ list,
+                                                                  const unsigned* __restrict__ off, long long n_listed,
+                                                                  const int64_t* __restrict__ ids, long long n_ids,
+                                                                  int nbx, int nby, double* __restrict__ out,
+                                                                  unsigned long long* __restrict__ bad) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    unsigned long long* bar = reinterpret_cast<unsigned long long*>(smem);
+    double* box = reinterpret_cast<double*>(smem + 128);
+    const long long q = blockIdx.x;
+    const unsigned b = list[q];
+    const long long lo = off[b], hi = q + 1 < n_listed ? off[list[q + 1]] : n_ids;
+    const int bi = static_cast<int>(b % nbx), bj = static_cast<int>((b / nbx) % nby),
+              bk = static_cast<int>(b / (static_cast<unsigned>(nbx) * nby));
+    const int x0 = max(bi * kSlBrick - kBoxLoX, 0), y0 = max(bj * kSlBrick - kBoxLo, 0),
+              z0 = max(bk * kSlBrick - kBoxLo, 0);
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(box_smem_u32(bar)));
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(box_smem_u32(bar)),
+                     "r"(kBoxBytes)
+                     : "memory");
+        asm volatile(
+            "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+            "[%5];\n" ::"r"(box_smem_u32(box)),
+            "l"(reinterpret_cast<unsigned long long>(&tmap)), "r"(x0), "r"(y0), "r"(z0), "r"(box_smem_u32(bar))
+            : "memory");
+    }
+    __syncthreads();  // the barrier is initialised before anyone waits on it
+    asm volatile(
+        "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n @!p bra WAIT_%=;\n}\n" ::"r"(
+            box_smem_u32(bar))
+        : "memory");
+    const PhiBox B{box, x0, y0, z0};
+    for (long long t = lo + threadIdx.x; t < hi; t += blockDim.x) {
+        const long long id = __ldg(ids + t);
+        if (id_outside(P, id, bad)) continue;
+        int i, j, k;
+        node_ijk(P, id, i, j, k);
+        store_update(P, id, k, sl_node_box(P, phi, dist, id, i, j, k, B), out, bad);
+    }
 }
 
 // The z-line table of the 3d WENO fast path. For node n = (i, j, k),
@@ -567,6 +666,85 @@ cudaError_t launch_reach_max(const SlParams& P, const double* dist, const int64_
     reach_max_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, stream>>>(P, dist, active, n, max_bits);
     lsr_note_launch();
     return cudaGetLastError();
+}
+
+// the brick grouping of an active set for the TMA brick step
+cudaError_t launch_box_bricks(const SlParams& P, const int64_t* active, long long n, const BoxBuffers& X,
+                              long long* n_listed, cudaStream_t stream) {
+    const int nbx = (P.nx + kSlBrick - 1) / kSlBrick, nby = (P.ny + kSlBrick - 1) / kSlBrick,
+              nbz = (P.nz + kSlBrick - 1) / kSlBrick;
+    const long long nb = static_cast<long long>(nbx) * nby * nbz;
+    cudaError_t e = cudaMemsetAsync(X.count, 0, sizeof(unsigned) * (nb + 1), stream);
+    if (e == cudaSuccess) e = cudaMemsetAsync(X.cursor, 0, sizeof(unsigned) * nb, stream);
+    if (e != cudaSuccess) return e;
+    *n_listed = 0;
+    if (n <= 0) return cudaSuccess;
+    const unsigned g = static_cast<unsigned>((n + 255) / 256);
+    box_count_kernel<<<g, 256, 0, stream>>>(P, active, n, nbx, nby, X.count);
+    size_t tb = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tb, X.count, X.off, static_cast<int>(nb + 1));
+    if (tb > X.tmp_bytes) return cudaErrorMemoryAllocation;
+    e = cub::DeviceScan::ExclusiveSum(X.tmp, tb, X.count, X.off, static_cast<int>(nb + 1), stream);
+    if (e != cudaSuccess) return e;
+    box_scatter_kernel<<<g, 256, 0, stream>>>(P, active, n, nbx, nby, X.off, X.cursor, X.ids);
+    e = lsr_compact::compact(NonEmpty{X.count}, lsr_compact::Identity{}, nb, X.list, X.d_listed,
+                             static_cast<char*>(X.tmp) + X.tmp_bytes / 2, X.tmp_bytes / 2, stream);
+    if (e != cudaSuccess) return e;
+    for (int r = 0; r < 4; ++r) lsr_note_launch();
+    long long h = 0;
+    e = cudaMemcpyAsync(&h, X.d_listed, sizeof h, cudaMemcpyDeviceToHost, stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+    *n_listed = h;
+    return e;
+}
+
+size_t box_tmp_bytes(long long nbricks) {
+    size_t tb = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tb, static_cast<unsigned*>(nullptr), static_cast<unsigned*>(nullptr),
+                                  static_cast<int>(nbricks + 1));
+    const size_t c = lsr_compact::scratch_bytes(nbricks);
+    return 2 * ((std::max(tb + 256, c) + 255) / 256 * 256);  // two 256-byte-aligned halves
+}
+
+static bool box_tensor_map(const SlParams& P, const double* phi, CUtensorMap* map) {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &fn, 12000, cudaEnableDefault, &q) !=
+                cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            return static_cast<PFN_cuTensorMapEncodeTiled_v12000>(nullptr);
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }();
+    if (!encode || (P.nx * 8) % 16 != 0) return false;
+    const cuuint64_t dims[3] = {static_cast<cuuint64_t>(P.nx), static_cast<cuuint64_t>(P.ny),
+                                static_cast<cuuint64_t>(P.nz)};
+    const cuuint64_t str[2] = {static_cast<cuuint64_t>(P.nx) * 8, static_cast<cuuint64_t>(P.nxy) * 8};
+    const cuuint32_t box[3] = {kBoxEX, kBoxEY, kBoxEZ};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    return encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(phi), dims, str, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// false (nothing launched) when the tensor map cannot be made
+bool launch_sl_step_box(const SlParams& P, const double* phi, const double* dist, const BoxBuffers& X,
+                        long long n_listed, long long n_ids, double* out, unsigned long long* bad, cudaStream_t stream) {
+    CUtensorMap map;
+    if (!box_tensor_map(P, phi, &map)) return false;
+    static int attr_dev = -1;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (attr_dev != dev) {
+        cudaFuncSetAttribute(sl_step_box_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kBoxBytes + 128);
+        attr_dev = dev;
+    }
+    if (n_listed <= 0) return true;
+    const int nbx = (P.nx + kSlBrick - 1) / kSlBrick, nby = (P.ny + kSlBrick - 1) / kSlBrick;
+    sl_step_box_kernel<<<static_cast<unsigned>(n_listed), kBoxThreads, kBoxBytes + 128, stream>>>(
+        map, P, phi, dist, X.list, X.off, n_listed, X.ids, n_ids, nbx, nby, out, bad);
+    lsr_note_launch();
+    return true;
 }
 
 cudaError_t launch_check_ids(const int64_t* ids, long long n, long long n_nodes, unsigned long long* bad,

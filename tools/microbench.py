@@ -22,6 +22,7 @@ def main():
     ap.add_argument("--delta", type=float, default=1.0)
     ap.add_argument("--zslab", type=int, nargs=2, default=None, help="only band nodes with k in [lo, hi)")
     ap.add_argument("--order", default="id", help="thread order of the active ids: id or bXYZ (brick extents)")
+    ap.add_argument("--mode", type=int, default=0, help="3d WENO step form: 0 z-line table, 1 TMA bricks")
     a = ap.parse_args()
     g = lsr._api.cube_grid(a.n, 3)
     ax = g.axes()
@@ -40,6 +41,7 @@ def main():
         band = band[np.lexsort((band, key))]
     cfg = lsr.StepConfig(p=2, delta=a.delta, dt=0.25 * g.dx, band=bp, interp=lsr.InterpolatorKind(a.interp))
     ctx = lsr.Context(g)
+    ctx.set_sl_mode(a.mode)
     ctx.upload(0, phi)
     ctx.upload(1, dist)
     ctx.set_active(band)
@@ -51,7 +53,7 @@ def main():
             ks.append(k)
             ss.append(st)
     kmed = float(np.median(ks))
-    print(json.dumps(dict(n=a.n, interp=a.interp, active=int(band.size), kernel_ms=kmed, step_ms=float(np.median(ss)),
+    print(json.dumps(dict(n=a.n, interp=a.interp, mode=a.mode, active=int(band.size), kernel_ms=kmed, step_ms=float(np.median(ss)),
                           node_updates_per_s=band.size / (kmed * 1e-3),
                           kernel_ms_all=[round(x, 4) for x in ks])))
 
