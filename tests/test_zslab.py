@@ -471,3 +471,43 @@ def test_slab_loop_protocol_gloo_matches_one_rank(tmp_path, world):
     cuts = [0, 10, _LOOP_NZ] if world == 2 else [0, 8, 16, _LOOP_NZ]
     in_stats, in_owned = _run_mock_loop(zslab.InProcessRunner, list(range(world)), cuts, 3)
     assert np.array_equal(bits(np.concatenate(in_owned)), bits(ref_owned[0]))
+
+
+@pytest.mark.parametrize("win,own", [((0, 20), (10, 30)),   # owned beyond the window
+                                     ((5, 40), (5, 20)),    # window must start at own_lo - 1
+                                     ((0, 20), (0, 20)),    # window must end at own_hi + 1
+                                     ((0, 40), (20, 20)),   # empty ownership
+                                     ((-1, 40), (0, 10))])
+def test_slab_create_rejects_bad_windows_before_device_work(built, win, own):
+    import paper_2410_22205_b200 as lsr
+
+    g = lsr._api.cube_grid(N, 3)
+    with pytest.raises(lsr.ConfigError):
+        lsr.SlabContext(g, win[0], win[1], own[0], own[1])
+
+
+def test_slab_create_needs_3d_and_aligned_planes(built):
+    import paper_2410_22205_b200 as lsr
+
+    with pytest.raises(lsr.ConfigError):
+        lsr.SlabContext(lsr._api.cube_grid(16, 2), 0, 1, 0, 1)
+    g = lsr.Grid(3, (-1.0, -1.0, -1.0), 0.1, (9, 7, 20))  # 63 nodes per plane
+    with pytest.raises(lsr.ConfigError, match="multiple of 16"):
+        lsr.SlabContext(g, 0, 11, 0, 10)
+
+
+@pytest.mark.gpu
+def test_whole_grid_entry_points_reject_slab_contexts(gpu):
+    import ctypes as C
+
+    lsr = gpu
+    g = lsr._api.cube_grid(32, 3)
+    c = lsr.SlabContext(g, 0, 17, 0, 16)
+    L = lsr.lib()
+    cfg = lsr.StepConfig(p=1, delta=0.0, dt=0.1 * g.dx, band=lsr.default_band_params(3, g.dx))
+    bad = C.c_int64(-1)
+    assert L.lsr_cuda_sl_step(c.h, C.byref(cfg.c()), 1.0, C.byref(bad)) == 1  # LSR_ERR_CONFIG
+    assert b"slab" in L.lsr_cuda_last_error_string()
+    na, nt = C.c_int64(), C.c_int64()
+    assert L.lsr_cuda_narrow_band(c.h, 0, 0.1, C.byref(na), C.byref(nt)) == 1
+    c.close()
