@@ -93,17 +93,19 @@ def test_slab_loop_matches_single_gpu_loop(gpu, dims, interp, world, halo, p, de
         c.close()
 
 
-@pytest.mark.parametrize("config,world,iters", [(3, 4, 4), (4, 2, 3)])
+@pytest.mark.parametrize("config,world,iters", [(3, 4, 4), (4, 2, 3), (5, 4, 1)])
 def test_slab_loop_full_size_configs(gpu, config, world, iters):
-    """BASELINE configs 3 (256^3 noisy torus, 100 k points, WENO) and 4
-    (512^3 bumpy sphere, 1 M points, WENO) at full size: the slab loop's
-    phi after every iteration is bit-identical to the single-GPU loop's."""
+    """BASELINE configs 3 (256^3 noisy torus, 100 k points, WENO), 4 (512^3
+    bumpy sphere, 1 M points, WENO) and 5 (1024^3 three tori, 4 M points,
+    WENO; 4 slabs) at full size: the slab loop's phi after every iteration
+    is bit-identical to the single-GPU loop's."""
     lsr = gpu
-    n, npts, sig = {3: (256, 100_000, 0.5), 4: (512, 1_000_000, 0.0)}[config]
+    n, npts, sig = {3: (256, 100_000, 0.5), 4: (512, 1_000_000, 0.0), 5: (1024, 4_000_000, 0.25)}[config]
+    r0 = 0.95 if config == 5 else 0.9  # config 5's tori reach |x| = 0.9
     g = lsr.cube_grid(n, 3)
     pts = lsr.cloud_generate(config, npts, seed=2410, sigma=sig * g.dx)
     ax = g.axes()
-    phi0 = (np.sqrt(ax[0][None, None, :] ** 2 + ax[1][None, :, None] ** 2 + ax[2][:, None, None] ** 2) - 0.9).ravel()
+    phi0 = (np.sqrt(ax[0][None, None, :] ** 2 + ax[1][None, :, None] ** 2 + ax[2][:, None, None] ** 2) - r0).ravel()
     ctx = lsr.Context(g)
     ctx.build_distance(pts)
     dist = ctx.download(1)
