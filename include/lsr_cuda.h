@@ -278,6 +278,21 @@ typedef struct lsr_loop_stats {
 } lsr_loop_stats;
 int lsr_cuda_loop_step(lsr_cuda_ctx* ctx, const lsr_step_cfg* cfg, const lsr_reinit_cfg* rcfg, int energy_refine,
                        double energy_override, lsr_loop_stats* stats);
+/* K iterations of the same loop body, device-controlled: the band counts,
+ * the interface-cell count, E_2 (blocked_sum and pow on the device), the
+ * p > 1 && E_2 == 0 skip, the NoInterface case and the Jacobi stop rule are
+ * all decided on the device, so the K iterations are enqueued without a host
+ * round trip and the host synchronises once, at the end, to read the K
+ * records (stats[0..K), NULL = none; ms = device time per phase). use_graph:
+ * iterations after the first are replays of a captured CUDA graph of one
+ * iteration. *done = iterations completed (K, or the index of the first one
+ * that failed: non-finite update, E_2 NaN, a 2d front outside the hull — the
+ * reference throws there; the fields are then unspecified). E_2 differs from
+ * lsr_cuda_loop_step's (host glibc pow) only where glibc's pow(x, 0.5) is
+ * not the correctly rounded sqrt. The box SL form (lsr_cuda_set_sl_mode 1) is
+ * not used here. */
+int lsr_cuda_loop_run(lsr_cuda_ctx* ctx, const lsr_step_cfg* cfg, const lsr_reinit_cfg* rcfg, int energy_refine,
+                      int iterations, int use_graph, lsr_loop_stats* stats, int* done);
 
 /* ---- z-slab loop (driver.cpp:185-203 split over ranks) ----
  * A slab context holds the resident planes [win_lo, win_hi) of the global

@@ -137,6 +137,8 @@ def lib() -> C.CDLL:
     L.lsr_cuda_reinit_defaults.argtypes = [C.c_double, C.c_double, P(CReinitCfg)]
     L.lsr_cuda_reinit_defaults.restype = None
     L.lsr_cuda_loop_step.argtypes = [C.c_void_p, P(CStepCfg), P(CReinitCfg), C.c_int, C.c_double, P(CLoopStats)]
+    L.lsr_cuda_loop_run.argtypes = [C.c_void_p, P(CStepCfg), P(CReinitCfg), C.c_int, C.c_int, C.c_int,
+                                    P(CLoopStats), P(C.c_int)]
     L.lsr_cuda_sl_step_device_fused.argtypes = [P(CGrid), C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_void_p,
                                                 C.c_void_p, C.c_void_p, C.c_int64, P(CStepCfg), C.c_double,
                                                 C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_int32,
@@ -614,6 +616,21 @@ class Context:
                                         -1.0 if energy_override is None else float(energy_override), C.byref(s)))
         return dict(energy=s.energy, n_active=s.n_active, n_tube=s.n_tube, reinit_iterations=s.reinit_iterations,
                     had_interface=bool(s.had_interface), ms=list(s.ms))
+
+    def loop_run(self, cfg: StepConfig, rcfg: "ReinitConfig", iterations: int, energy_refine: int = 5,
+                 use_graph: bool = True) -> list[dict]:
+        """`iterations` driver iterations (driver.cpp:187-203) controlled on the
+        device: one host synchronisation for all of them (lsr_cuda_loop_run);
+        the GPU's own E_2 every iteration. Returns one record per iteration."""
+        n = int(iterations)
+        if n < 1:
+            raise ConfigError("loop_run: iterations must be >= 1")
+        recs = (CLoopStats * n)()
+        done = C.c_int(0)
+        _check(lib().lsr_cuda_loop_run(self.h, C.byref(cfg.c()), C.byref(rcfg.c()), int(energy_refine), n,
+                                       1 if use_graph else 0, recs, C.byref(done)))
+        return [dict(energy=r.energy, n_active=r.n_active, n_tube=r.n_tube, reinit_iterations=r.reinit_iterations,
+                     had_interface=bool(r.had_interface), ms=list(r.ms)) for r in recs]
 
     def last_times(self):
         k, s = C.c_float(), C.c_float()

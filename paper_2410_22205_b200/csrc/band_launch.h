@@ -63,6 +63,26 @@ int lsr_reinitialize(const lsr_dev::SlParams& P, double** phi, double** scratch,
                      const ReinitParams& R, ReinitBuffers& W, int* iterations, int* had_interface, cudaStream_t s,
                      std::string* err, bool clamp_sparse = false);
 
+// device-controlled loop (band_reinit.cu, lsr_cuda_loop_run): the words one
+// iteration's reinit keeps in device memory instead of reading them back
+struct ReinitLoopDev {
+    int flags[2];            // the one-step's any_frozen, any_zero
+    int clamp_outside;       // the dense clamp changed a node outside the tube
+    int pad;
+    long long counts[2];     // frozen ids, sweep nodes
+    unsigned long long residual_bits;  // the sweeps' control (band_reinit.cu IterState)
+    int done;
+    int iterations;
+};
+int lsr_band_enqueue(const lsr_dev::SlParams& P, const double* phi, double gamma, BandBuffers& B, cudaStream_t s,
+                     std::string* err);
+int lsr_reinit_loop_reserve(long long n, ReinitBuffers& W, std::string* err);
+int lsr_reinit_enqueue(const lsr_dev::SlParams& P, double* b, double* c, const BandBuffers& B, double gamma,
+                       const ReinitParams& R, ReinitBuffers& W, ReinitLoopDev* L, bool clamp_sparse, cudaStream_t s,
+                       std::string* err);
+int lsr_loop_sync_fields(const lsr_dev::SlParams& P, const double* b, double* a, const BandBuffers& B,
+                         const ReinitBuffers& W, const ReinitLoopDev* L, cudaStream_t s, std::string* err);
+
 // z-slab forms (band_reinit.cu): owned planes [own_lo, own_hi) of buffers
 // resident on [win_lo, win_hi), passed shifted to global node ids
 int lsr_band_build_slab(const lsr_dev::SlParams& P, const double* phi_g, double gamma, BandBuffers& B, int win_lo,

@@ -388,11 +388,13 @@ struct TubeId {
 // smoothed sign at entry (reinit.cpp:250-257); also each node's neighbour
 // mask for the sweeps (bit 2*ax: the -1 neighbour along ax exists, bit
 // 2*ax+1: the +1 one), so the sweeps need no index arithmetic
+// (nn_dev: the count in device memory (the device loop), grid-strided)
 __global__ void sign_kernel(SlParams P, const double* __restrict__ phi, const long long* __restrict__ nodes,
                             long long nn, double eps2, double* __restrict__ sgn, unsigned char* __restrict__ nbr,
-                            unsigned* __restrict__ nodes32) {
-    const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (t >= nn) return;
+                            unsigned* __restrict__ nodes32, const long long* __restrict__ nn_dev = nullptr) {
+    const long long n_ = nn_dev != nullptr ? __ldg(nn_dev) : nn;
+    const long long step_ = nn_dev != nullptr ? static_cast<long long>(gridDim.x) * blockDim.x : n_;
+    for (long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; t < n_; t += step_) {
     const long long id = nodes[t];
     if (nodes32) nodes32[t] = static_cast<unsigned>(id);  // 4-byte ids for the sweeps when the grid allows
     const double v = __ldg(phi + id);
@@ -402,6 +404,7 @@ __global__ void sign_kernel(SlParams P, const double* __restrict__ phi, const lo
     unsigned m = (i > 0 ? 1u : 0u) | (i < P.nx - 1 ? 2u : 0u) | (j > 0 ? 4u : 0u) | (j < P.ny - 1 ? 8u : 0u);
     if (P.dim == 3) m |= (k > 0 ? 16u : 0u) | (k < P.nz - 1 ? 32u : 0u);
     nbr[t] = static_cast<unsigned char>(m);
+    }
 }
 
 // godunov_norm (reinit.cpp:63-84) on values already loaded: pc = phi at the
@@ -583,7 +586,8 @@ template <class IdT>
 __global__ void __launch_bounds__(kPipeThreads, LSR_JAC_PIPE_MINB)
     jacobi_pipe(SlParams P, const double* __restrict__ cur, double* __restrict__ nxt, const IdT* __restrict__ nodes,
                 const double* __restrict__ sgn, const unsigned char* __restrict__ nbr, long long nn, double dtau,
-                IterState* __restrict__ st) {
+                IterState* __restrict__ st, const long long* __restrict__ nn_dev) {
+    if (nn_dev != nullptr) nn = __ldg(nn_dev);  // the device loop's node count
     const long long T = static_cast<long long>(gridDim.x) * blockDim.x;
     const long long g = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
     const long long stv[3] = {1, P.nx, P.nxy};
@@ -669,14 +673,22 @@ __global__ void __launch_bounds__(kPipeThreads, LSR_JAC_PIPE_MINB)
 // one sweep cur -> nxt over the node list (W.nodes32 when the ids fit 4 bytes)
 template <class IdT>
 static void launch_jacobi(const SlParams& P, const double* cur, double* nxt, const IdT* ids, const ReinitBuffers& W,
-                          long long nn, double dtau, IterState* st, cudaStream_t s) {
+                          long long nn, double dtau, IterState* st, cudaStream_t s,
+                          const long long* nn_dev = nullptr) {
+    if (nn_dev != nullptr) {  // device count: the persistent sweep on every resident CTA
+        jacobi_pipe<<<148u * LSR_JAC_PIPE_MINB, kPipeThreads, 0, s>>>(P, cur, nxt, ids, W.sgn, W.nbr, 0, dtau, st,
+                                                                      nn_dev);
+        lsr_note_launch();
+        return;
+    }
     if (nn <= 0) return;
     if (LSR_JAC_PIPE) {
         // persistent: the resident CTAs (148 SMs x LSR_JAC_PIPE_MINB), or fewer for short lists
         const long long want = (nn + kPipeThreads * kPipeNPT - 1) / (kPipeThreads * kPipeNPT);
         const long long cap = 148LL * LSR_JAC_PIPE_MINB;
         jacobi_pipe<<<static_cast<unsigned>(want < cap ? want : cap), kPipeThreads, 0, s>>>(P, cur, nxt, ids, W.sgn,
-                                                                                            W.nbr, nn, dtau, st);
+                                                                                            W.nbr, nn, dtau, st,
+                                                                                            nullptr);
     } else {
         const unsigned g = static_cast<unsigned>((nn + kJacThreads * kJacNPT - 1) / (kJacThreads * kJacNPT));
         jacobi<<<g, kJacThreads, 0, s>>>(P, cur, nxt, ids, W.sgn, W.nbr, nn, dtau, st);
@@ -709,6 +721,64 @@ __global__ void copy_ids(const double* __restrict__ src, double* __restrict__ ds
     if (t >= n) return;
     const long long id = ids[t];
     dst[id] = src[id];
+}
+
+// ---- device-loop forms (lsr_cuda_loop_run): list lengths in device memory,
+// a fixed grid striding over them (no host round trip for the count)
+constexpr unsigned kDevGrid = 148 * 8;
+
+__global__ void copy_ids_dev(const double* __restrict__ src, double* __restrict__ dst,
+                             const long long* __restrict__ ids, const long long* __restrict__ n_dev) {
+    const long long n = __ldg(n_dev);
+    for (long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; t < n;
+         t += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const long long id = ids[t];
+        dst[id] = src[id];
+    }
+}
+
+__global__ void clamp_ids_dev(double* __restrict__ f, const long long* __restrict__ ids,
+                              const long long* __restrict__ n_dev, double gamma) {
+    const long long n = __ldg(n_dev);
+    for (long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; t < n;
+         t += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const long long id = ids[t];
+        const double v = f[id], c = smin(smax(v, -gamma), gamma);
+        if (__double_as_longlong(c) != __double_as_longlong(v)) f[id] = c;
+    }
+}
+
+// the sweeps start (or, without an interface, are skipped: reinit.cpp:140-142)
+__global__ void reinit_begin(IterState* st, const int* __restrict__ flags) {
+    st->residual_bits = 0;
+    st->iterations = 0;
+    st->done = (flags[0] || flags[1]) ? 0 : 1;
+}
+
+// after the sweeps the result is in b (an even sweep count) or c (odd): copy
+// it over the node list into the other buffer, so that b holds the result
+// and the two agree on the list
+__global__ void sweep_parity(double* __restrict__ b, double* __restrict__ c, const long long* __restrict__ ids,
+                             const long long* __restrict__ n_dev, const IterState* __restrict__ st) {
+    const long long n = __ldg(n_dev);
+    const bool odd = (st->iterations & 1) != 0;
+    const double* src = odd ? c : b;
+    double* dst = odd ? b : c;
+    for (long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; t < n;
+         t += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const long long id = ids[t];
+        dst[id] = src[id];
+    }
+}
+
+// dst = src on every node when *flag is set (the dense clamp changed a node
+// outside the tube), else nothing
+__global__ void copy_all_if(const double* __restrict__ src, double* __restrict__ dst, long long n,
+                            const int* __restrict__ flag) {
+    if (!*flag) return;
+    for (long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; t < n;
+         t += static_cast<long long>(gridDim.x) * blockDim.x)
+        dst[t] = src[t];
 }
 
 }  // namespace
@@ -1166,5 +1236,129 @@ int lsr_reinit_slab_sweep(const SlParams& P, const double* cur_g, double* nxt_g,
     BR_TRY(cudaMemcpyAsync(&bits, &st->residual_bits, sizeof bits, cudaMemcpyDeviceToHost, s));
     BR_TRY(cudaStreamSynchronize(s));
     std::memcpy(residual, &bits, sizeof bits);
+    return LSR_OK;
+}
+
+// ---------------------------------------------------------------------------
+// The device-controlled loop (lsr_cuda_loop_run, lsr_capi.cu): the band and
+// reinitialisation phases with every count kept in device memory, so that a
+// loop iteration is enqueued (and captured into a CUDA graph) without a host
+// round trip.
+
+// narrow_band (grid.cpp:76-123): the dilation passes and the fused two-list
+// compaction; the counts stay in B.counts ([0] ACTIVE, [1] tube)
+int lsr_band_enqueue(const SlParams& P, const double* phi, double gamma, BandBuffers& B, cudaStream_t s,
+                     std::string* err) {
+    const long long n = P.nxy * P.nz;
+    if (int st = B.reserve(n, err)) return st;
+    const size_t tb = lsr_compact::scratch_bytes2(n);
+    if (int st = ensure_tmp(B, tb, err)) return st;
+    unsigned char* t = reinterpret_cast<unsigned char*>(B.active);
+    unsigned char* u = reinterpret_cast<unsigned char*>(B.tube);
+    band_passes(P, phi, gamma, 0, n, 0, n, t, u, B.state, s);
+    BR_TRY(lsr_compact::compact2(lsr_compact::BytePred<StateIs1>{B.state, {}}, NonZero{}, lsr_compact::Identity{}, n,
+                                 B.active, B.tube, B.counts, B.tmp, tb, s));
+    for (int q = 0; q < 2; ++q) lsr_note_launch();
+    return LSR_OK;
+}
+
+// buffers the loop's reinit needs, allocated before any capture
+int lsr_reinit_loop_reserve(long long n, ReinitBuffers& W, std::string* err) {
+    if (int st = W.reserve(n, err)) return st;
+    const size_t tb = lsr_compact::scratch_bytes2(n);
+    if (tb > W.tmp_bytes) {
+        cudaFree(W.tmp);
+        W.tmp = nullptr;
+        BR_TRY(cudaMalloc(&W.tmp, tb));
+        W.tmp_bytes = tb;
+    }
+    return LSR_OK;
+}
+
+// reinitialize (reinit.cpp:133-145) of b (phi^{n+1}) on the band B of phi^n,
+// c = the scratch field; the result is left in b, and c agrees with b on the
+// frozen and swept nodes. Same kernels and bits as lsr_reinitialize, but
+// nothing is read back: the one-step's flags decide on the device whether
+// the sweeps run (reinit_begin), the frozen ids and the sweep list come from
+// one compaction over the frozen flags and the band state, the sweep count
+// decides which buffer is copied where (sweep_parity). clamp_sparse: b
+// equalled a clamped field except on the tube and the frozen nodes (see
+// lsr_reinitialize); otherwise the dense clamp flags changes outside the
+// tube in L->clamp_outside.
+int lsr_reinit_enqueue(const SlParams& P, double* b, double* c, const BandBuffers& B, double gamma,
+                       const ReinitParams& R, ReinitBuffers& W, ReinitLoopDev* L, bool clamp_sparse, cudaStream_t s,
+                       std::string* err) {
+    if (!(R.dtau > 0.0)) {
+        *err = "reinit: dtau must be positive";  // reinit.hpp:14-17
+        return LSR_ERR_CONFIG;
+    }
+    if (R.max_iters < 1) {
+        *err = "reinit: max_iters must be >= 1";
+        return LSR_ERR_CONFIG;
+    }
+    if (!(gamma > 0.0)) {
+        *err = "clamp_field: gamma must be positive";  // grid.cpp:127
+        return LSR_ERR_CONFIG;
+    }
+    const long long n = P.nxy * P.nz;
+    if (int st = lsr_reinit_loop_reserve(n, W, err)) return st;
+    BR_TRY(cudaMemsetAsync(L, 0, sizeof(ReinitLoopDev), s));
+    int* flags = L->flags;
+    // interface_one_step (reinit.cpp:18-59): b -> c on every node
+    if (P.dim == 3 && P.nx % 4 == 0) {
+        const long long threads = static_cast<long long>(P.nx / 4) * P.ny * ((P.nz + kMarch - 1) / kMarch);
+        one_step_march<<<static_cast<unsigned>((threads + 255) / 256), 256, 0, s>>>(
+            P, b, c, reinterpret_cast<unsigned*>(W.frozen), flags, flags + 1, 0, P.nz);
+    } else {
+        one_step<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(P, b, c, W.frozen, n, flags, flags + 1, 0);
+    }
+    lsr_note_launch();
+    // frozen ids and the sweep list (tube minus frozen, reinit.cpp:94-98), ascending
+    BR_TRY(lsr_compact::compact2m(lsr_compact::BytePred<NonZero>{W.frozen, {}},
+                                  lsr_compact::ByteAndNot{B.state, W.frozen}, lsr_compact::Identity{}, n,
+                                  W.frozen_ids, W.nodes, L->counts, W.tmp, W.tmp_bytes, s));
+    for (int q = 0; q < 2; ++q) lsr_note_launch();
+    // b takes the one-step's values (`ScalarField next = phi` after it, reinit.cpp:109)
+    copy_ids_dev<<<kDevGrid, 256, 0, s>>>(c, b, W.frozen_ids, L->counts);
+    const bool small = n <= 0xffffffffLL;
+    sign_kernel<<<kDevGrid, 256, 0, s>>>(P, b, W.nodes, 0, R.sign_eps * R.sign_eps, W.sgn, W.nbr,
+                                         small ? W.nodes32 : nullptr, L->counts + 1);
+    IterState* st = reinterpret_cast<IterState*>(&L->residual_bits);
+    reinit_begin<<<1, 1, 0, s>>>(st, flags);
+    for (int q = 0; q < 3; ++q) lsr_note_launch();
+    const double tol = R.residual_tol * P.dx;
+    double* buf[2] = {b, c};
+    for (int k = 0; k < R.max_iters; ++k) {
+        if (small) launch_jacobi(P, buf[k & 1], buf[(k + 1) & 1], W.nodes32, W, 0, R.dtau, st, s, L->counts + 1);
+        else launch_jacobi(P, buf[k & 1], buf[(k + 1) & 1], W.nodes, W, 0, R.dtau, st, s, L->counts + 1);
+        iter_check<<<1, 1, 0, s>>>(st, tol);
+        lsr_note_launch();
+    }
+    sweep_parity<<<kDevGrid, 256, 0, s>>>(b, c, W.nodes, L->counts + 1, st);
+    lsr_note_launch();
+    // clamp_field (reinit.cpp:144)
+    if (clamp_sparse) {
+        clamp_ids_dev<<<kDevGrid, 256, 0, s>>>(b, B.tube, B.counts + 1, gamma);
+        clamp_ids_dev<<<kDevGrid, 256, 0, s>>>(b, W.frozen_ids, L->counts, gamma);
+        for (int q = 0; q < 2; ++q) lsr_note_launch();
+    } else if (int e = lsr_clamp(b, n, gamma, s, err, B.state, &L->clamp_outside)) {
+        return e;
+    }
+    BR_TRY(cudaGetLastError());
+    return LSR_OK;
+}
+
+// after an iteration: a (phi^n, the next iteration's out) takes b's values
+// (phi^{n+1}) where they may differ — the tube of phi^n, the frozen nodes,
+// and (if the dense clamp reported it) anywhere — so that the two fields are
+// equal when the next iteration's SL step writes its updates into a
+int lsr_loop_sync_fields(const SlParams& P, const double* b, double* a, const BandBuffers& B, const ReinitBuffers& W,
+                         const ReinitLoopDev* L, cudaStream_t s, std::string* err) {
+    const long long n = P.nxy * P.nz;
+    copy_ids_dev<<<kDevGrid, 256, 0, s>>>(b, a, B.tube, B.counts + 1);
+    copy_ids_dev<<<kDevGrid, 256, 0, s>>>(b, a, W.frozen_ids, L->counts);
+    copy_all_if<<<kDevGrid, 256, 0, s>>>(b, a, n, &L->clamp_outside);
+    for (int q = 0; q < 3; ++q) lsr_note_launch();
+    BR_TRY(cudaGetLastError());
     return LSR_OK;
 }

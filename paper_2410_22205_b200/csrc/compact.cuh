@@ -240,4 +240,98 @@ cudaError_t compact2(BytePred<T1> p1, T2 test2, Item item, long long n, Out* out
     return cudaGetLastError();
 }
 
+// a[i] != 0 && b[i] == 0 over two byte arrays (16 of each per thread)
+struct ByteAndNot {
+    const unsigned char* a;
+    const unsigned char* b;
+    __device__ __forceinline__ unsigned mask16(long long base, long long n) const {
+        unsigned m = 0;
+        if (base + kItems <= n) {
+            const uint4 va = *reinterpret_cast<const uint4*>(a + base);
+            const uint4 vb = *reinterpret_cast<const uint4*>(b + base);
+            const unsigned wa[4] = {va.x, va.y, va.z, va.w}, wb[4] = {vb.x, vb.y, vb.z, vb.w};
+#pragma unroll
+            for (int q = 0; q < kItems; ++q) {
+                const unsigned x = (wa[q >> 2] >> (8 * (q & 3))) & 0xffu, y = (wb[q >> 2] >> (8 * (q & 3))) & 0xffu;
+                m |= (x != 0 && y == 0 ? 1u : 0u) << q;
+            }
+        } else {
+            for (int q = 0; q < kItems && base + q < n; ++q) m |= (a[base + q] != 0 && b[base + q] == 0 ? 1u : 0u) << q;
+        }
+        return m;
+    }
+};
+
+// compact2 over two mask providers (anything with mask16(base, n), e.g. a
+// BytePred and a ByteAndNot over different arrays): both lists in one count
+// and one write pass
+template <class M1, class M2>
+__global__ void __launch_bounds__(kThreads) count_tiles_m2(M1 p1, M2 p2, long long n, long long* __restrict__ c1,
+                                                           long long* __restrict__ c2) {
+    const long long base = static_cast<long long>(blockIdx.x) * kTile + static_cast<long long>(threadIdx.x) * kItems;
+    const int a = base < n ? __popc(p1.mask16(base, n)) : 0;
+    const int b = base < n ? __popc(p2.mask16(base, n)) : 0;
+    using Reduce = cub::BlockReduce<int, kThreads>;
+    __shared__ typename Reduce::TempStorage tmp;
+    const int ta = Reduce(tmp).Sum(a);
+    __syncthreads();
+    const int tb = Reduce(tmp).Sum(b);
+    if (threadIdx.x == 0) {
+        c1[blockIdx.x] = ta;
+        c2[blockIdx.x] = tb;
+    }
+}
+
+template <class M1, class M2, class Item, class Out>
+__global__ void __launch_bounds__(kThreads) write_tiles_m2(M1 p1, M2 p2, Item item, long long n,
+                                                           const long long* __restrict__ o1,
+                                                           const long long* __restrict__ o2, Out* __restrict__ out1,
+                                                           Out* __restrict__ out2) {
+    const long long base = static_cast<long long>(blockIdx.x) * kTile + static_cast<long long>(threadIdx.x) * kItems;
+    unsigned m1 = base < n ? p1.mask16(base, n) : 0u, m2 = base < n ? p2.mask16(base, n) : 0u;
+    using Scan = cub::BlockScan<int, kThreads>;
+    __shared__ typename Scan::TempStorage tmp;
+    int r1, r2;
+    Scan(tmp).ExclusiveSum(__popc(m1), r1);
+    __syncthreads();
+    Scan(tmp).ExclusiveSum(__popc(m2), r2);
+    Out* a = out1 + o1[blockIdx.x] + r1;
+    while (m1) {
+        const int q = __ffs(m1) - 1;
+        m1 &= m1 - 1;
+        *a++ = item(base + q);
+    }
+    Out* b = out2 + o2[blockIdx.x] + r2;
+    while (m2) {
+        const int q = __ffs(m2) - 1;
+        m2 &= m2 - 1;
+        *b++ = item(base + q);
+    }
+}
+
+template <class M1, class M2, class Item, class Out>
+cudaError_t compact2m(M1 p1, M2 p2, Item item, long long n, Out* out1, Out* out2, long long* d_count2, void* scratch,
+                      size_t scratch_size, cudaStream_t s) {
+    if (n <= 0) return cudaMemsetAsync(d_count2, 0, 2 * sizeof(long long), s);
+    const long long tiles = (n + kTile - 1) / kTile;
+    long long* c1 = static_cast<long long*>(scratch);
+    long long* off1 = c1 + (tiles + 1);
+    long long* c2 = off1 + (tiles + 1);
+    long long* off2 = c2 + (tiles + 1);
+    void* scan_tmp = off2 + (tiles + 1);
+    size_t scan_bytes = scratch_size - 4 * (tiles + 1) * sizeof(long long);
+    cudaError_t e = cudaMemsetAsync(c1 + tiles, 0, sizeof(long long), s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(c2 + tiles, 0, sizeof(long long), s);
+    if (e != cudaSuccess) return e;
+    count_tiles_m2<<<static_cast<unsigned>(tiles), kThreads, 0, s>>>(p1, p2, n, c1, c2);
+    e = cub::DeviceScan::ExclusiveSum(scan_tmp, scan_bytes, c1, off1, static_cast<int>(tiles + 1), s);
+    if (e == cudaSuccess) e = cub::DeviceScan::ExclusiveSum(scan_tmp, scan_bytes, c2, off2, static_cast<int>(tiles + 1), s);
+    if (e != cudaSuccess) return e;
+    write_tiles_m2<<<static_cast<unsigned>(tiles), kThreads, 0, s>>>(p1, p2, item, n, off1, off2, out1, out2);
+    e = cudaMemcpyAsync(d_count2, off1 + tiles, sizeof(long long), cudaMemcpyDeviceToDevice, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(d_count2 + 1, off2 + tiles, sizeof(long long), cudaMemcpyDeviceToDevice, s);
+    if (e != cudaSuccess) return e;
+    return cudaGetLastError();
+}
+
 }  // namespace lsr_compact

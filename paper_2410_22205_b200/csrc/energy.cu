@@ -221,11 +221,14 @@ __device__ __forceinline__ void load_corners(const SlParams& P, const double* __
 #ifndef LSR_EN_MINB
 #define LSR_EN_MINB 8  // 64 registers, 8 CTAs of 128 per SM (E_2 at 512^3: 1.06 -> 0.97 ms)
 #endif
+template <bool kDev>
 __global__ void __launch_bounds__(LSR_EN_THREADS, LSR_EN_MINB) contrib_3d_hoisted(SlParams P, const double* __restrict__ phi, const double* __restrict__ dist,
                                    const int* __restrict__ cells, long long nc, int r, double dxp, double select,
-                                   int p, double* __restrict__ contrib) {
-    const long long c = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (c >= nc) return;
+                                   int p, double* __restrict__ contrib, const long long* __restrict__ nc_dev) {
+    // kDev (the device loop): the cell count in device memory, grid-strided
+    const long long n_ = kDev ? __ldg(nc_dev) : nc;
+    for (long long c = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; c < n_;
+         c += static_cast<long long>(gridDim.x) * blockDim.x) {
     const long long cid = cells[c];
     const unsigned cx = P.nx - 1, cy = P.ny - 1;
     const unsigned row = static_cast<unsigned>(cid) / cx;
@@ -265,6 +268,8 @@ __global__ void __launch_bounds__(LSR_EN_THREADS, LSR_EN_MINB) contrib_3d_hoiste
                 acc += powp(fabs(vd), p) * dxp * dxp;
             }
     contrib[c] = acc;
+    if (!kDev) break;
+    }
 }
 
 struct Pt {
@@ -289,11 +294,13 @@ __device__ __forceinline__ bool inside_hull(const SlParams& P, Pt a) {  // Grid:
 }
 
 // energy_2d per-cell contribution (metrics.cpp:124-137, front_segments_2d :79-109)
+template <bool kDev>
 __global__ void contrib_2d(SlParams P, const double* __restrict__ phi, const double* __restrict__ dist,
                            const int* __restrict__ cells, long long nc, int p, double* __restrict__ contrib,
-                           int* __restrict__ out_of_domain) {
-    const long long c = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (c >= nc) return;
+                           int* __restrict__ out_of_domain, const long long* __restrict__ nc_dev) {
+    const long long n_ = kDev ? __ldg(nc_dev) : nc;
+    for (long long c = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; c < n_;
+         c += static_cast<long long>(gridDim.x) * blockDim.x) {
     // segment table of the 16 corner cases (metrics.cpp:80-84)
     const signed char table[16][2] = {{-1, -1}, {3, 0}, {0, 1}, {3, 1}, {1, 2}, {-2, 0}, {0, 2}, {3, 2},
                                       {2, 3},   {0, 2}, {-2, 0}, {1, 2}, {1, 3}, {0, 1}, {3, 0}, {-1, -1}};
@@ -338,6 +345,8 @@ __global__ void contrib_2d(SlParams P, const double* __restrict__ phi, const dou
         acc += len * 0.5 * (powp(fabs(da), p) + powp(fabs(db), p));
     }
     contrib[c] = acc;
+    if (!kDev) break;
+    }
 }
 
 // blocked_sum's in-block serial sums (parallel.hpp:31-37)
@@ -355,17 +364,39 @@ struct CellIdFrom {  // a z-slab's cells: index i of its range is global cell ba
     __device__ int operator()(long long c) const { return static_cast<int>(base + c); }
 };
 
-__global__ void block_partials(const double* __restrict__ contrib, long long n, double* __restrict__ partial) {
+__global__ void block_partials(const double* __restrict__ contrib, long long n, double* __restrict__ partial,
+                               const long long* __restrict__ n_dev = nullptr) {
     __shared__ double buf[4096];
-    const long long lo = static_cast<long long>(blockIdx.x) * 4096;
-    const int len = static_cast<int>(min(n - lo, 4096LL));
-    for (int t = threadIdx.x; t < len; t += blockDim.x) buf[t] = contrib[lo + t];
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double s = 0.0;
-        for (int t = 0; t < len; ++t) s += buf[t];
-        partial[blockIdx.x] = s;
+    // n_dev (the device loop): the count in device memory, CTAs stride over blocks
+    const long long n_ = n_dev != nullptr ? __ldg(n_dev) : n;
+    const long long nblk = (n_ + 4095) / 4096;
+    for (long long blk = blockIdx.x; blk < nblk; blk += (n_dev != nullptr ? gridDim.x : nblk)) {
+        const long long lo = blk * 4096;
+        const int len = static_cast<int>(min(n_ - lo, 4096LL));
+        for (int t = threadIdx.x; t < len; t += blockDim.x) buf[t] = contrib[lo + t];
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double s = 0.0;
+            for (int t = 0; t < len; ++t) s += buf[t];
+            partial[blk] = s;
+        }
+        __syncthreads();
     }
+}
+
+// blocked_sum's final serial pass over the block partials in block order
+// (parallel.hpp:39-40) and pow(total, 1/p) (metrics.cpp:142,183), on the
+// device for the device-controlled loop: sqrt for p = 2 (the correctly
+// rounded value, which glibc's pow returns except in rare hard cases), CUDA's
+// pow otherwise. *e2 = the energy; flags bit 0 = out of domain (2d)
+__global__ void energy_finish(const double* __restrict__ partial, const long long* __restrict__ n_dev, int p,
+                              const int* __restrict__ ood, double* __restrict__ e2, int* __restrict__ flags) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    const long long nblk = (*n_dev + 4095) / 4096;
+    double total = 0.0;
+    for (long long b = 0; b < nblk; ++b) total += partial[b];
+    *e2 = p == 2 ? sqrt(total) : (p == 1 ? total : pow(total, 1.0 / p));
+    if (*ood) *flags |= 1;
 }
 
 }  // namespace
@@ -479,13 +510,13 @@ int lsr_prep_surface_energy(const SlParams& P, const double* phi, const double* 
             const double select = std::sqrt(3.0) / 2.0 * dxp;  // metrics.cpp:157
             const unsigned g = static_cast<unsigned>((nc + 127) / 128);
             if (r <= kMaxRefine)
-                contrib_3d_hoisted<<<static_cast<unsigned>((nc + LSR_EN_THREADS - 1) / LSR_EN_THREADS), LSR_EN_THREADS,
-                                     0, s>>>(P, phi, dist, W.cells, nc, r, dxp, select, p, W.contrib);
+                contrib_3d_hoisted<false><<<static_cast<unsigned>((nc + LSR_EN_THREADS - 1) / LSR_EN_THREADS), LSR_EN_THREADS,
+                                     0, s>>>(P, phi, dist, W.cells, nc, r, dxp, select, p, W.contrib, nullptr);
             else
                 contrib_3d<<<g, 128, 0, s>>>(P, phi, dist, W.cells, nc, r, dxp, select, p, W.contrib);
         } else {
-            contrib_2d<<<static_cast<unsigned>((nc + 127) / 128), 128, 0, s>>>(P, phi, dist, W.cells, nc, p,
-                                                                                W.contrib, W.scal + 1);
+            contrib_2d<false><<<static_cast<unsigned>((nc + 127) / 128), 128, 0, s>>>(P, phi, dist, W.cells, nc, p,
+                                                                                W.contrib, W.scal + 1, nullptr);
         }
         lsr_note_launch();
         block_partials<<<static_cast<unsigned>(nblk), 256, 0, s>>>(W.contrib, nc, W.partial);
@@ -583,8 +614,8 @@ int lsr_energy_slab_cells(const SlParams& P, const double* phi_g, const double* 
         const double dxp = P.dx / refine;
         const double select = std::sqrt(3.0) / 2.0 * dxp;  // metrics.cpp:157
         if (refine <= kMaxRefine)
-            contrib_3d_hoisted<<<static_cast<unsigned>((nc + LSR_EN_THREADS - 1) / LSR_EN_THREADS), LSR_EN_THREADS, 0,
-                                 s>>>(P, phi_g, dist_g, W.cells, nc, refine, dxp, select, p, W.contrib);
+            contrib_3d_hoisted<false><<<static_cast<unsigned>((nc + LSR_EN_THREADS - 1) / LSR_EN_THREADS), LSR_EN_THREADS, 0,
+                                 s>>>(P, phi_g, dist_g, W.cells, nc, refine, dxp, select, p, W.contrib, nullptr);
         else
             contrib_3d<<<static_cast<unsigned>((nc + 127) / 128), 128, 0, s>>>(P, phi_g, dist_g, W.cells, nc, refine,
                                                                                dxp, select, p, W.contrib);
@@ -632,4 +663,93 @@ void EnergySlabWork::release() {
     cudaFree(partial);
     cudaFree(tmp);
     *this = EnergySlabWork{};
+}
+
+// ---------------------------------------------------------------------------
+// E_p inside the device-controlled loop (lsr_cuda_loop_run): the interface
+// cells, their contributions and blocked_sum with the cell count in device
+// memory; nothing is read back.
+
+void EnergyLoopWork::release() {
+    cudaFree(flags);
+    cudaFree(cells);
+    cudaFree(contrib);
+    cudaFree(partial);
+    cudaFree(nc);
+    cudaFree(ood);
+    cudaFree(tmp);
+    *this = EnergyLoopWork{};
+}
+
+int lsr_energy_loop_reserve(const SlParams& P, EnergyLoopWork& W, std::string* err) {
+#define EL_TRY(x)                                                       \
+    do {                                                                \
+        cudaError_t e_ = (x);                                           \
+        if (e_ != cudaSuccess) {                                        \
+            *err = std::string(#x) + ": " + cudaGetErrorString(e_);     \
+            return LSR_ERR_CUDA;                                        \
+        }                                                               \
+    } while (0)
+    const long long ncells = static_cast<long long>(P.nx - 1) * (P.ny - 1) * (P.dim == 3 ? (P.nz - 1) : 1);
+    if (ncells > 0x7fffffffLL) {
+        *err = "surface_energy: grids of 2^31 cells or more are not supported";
+        return LSR_ERR_CONFIG;
+    }
+    if (ncells <= W.cap) return LSR_OK;
+    W.release();
+    EL_TRY(cudaMalloc(&W.flags, ncells));
+    EL_TRY(cudaMalloc(&W.cells, sizeof(int) * ncells));
+    EL_TRY(cudaMalloc(&W.contrib, sizeof(double) * ncells));
+    EL_TRY(cudaMalloc(&W.partial, sizeof(double) * ((ncells + 4095) / 4096 + 1)));
+    EL_TRY(cudaMalloc(&W.nc, sizeof(long long)));
+    EL_TRY(cudaMalloc(&W.ood, sizeof(int)));
+    W.tmp_bytes = lsr_compact::scratch_bytes(ncells);
+    EL_TRY(cudaMalloc(&W.tmp, W.tmp_bytes));
+    W.cap = ncells;
+    return LSR_OK;
+}
+
+int lsr_energy_enqueue(const SlParams& P, const double* phi, const double* dist, int p, int refine,
+                       EnergyLoopWork& W, long long est_cells, double* d_e2, int* d_flags, cudaStream_t s,
+                       std::string* err) {
+    if (p < 1 || (P.dim == 3 && refine < 1)) {
+        *err = "surface_energy: invalid p or refinement";  // metrics.cpp:115,147
+        return LSR_ERR_CONFIG;
+    }
+    if (P.dim == 3 && refine > kMaxRefine) {
+        *err = "surface_energy: the device loop supports subcell_refine <= 8";
+        return LSR_ERR_CONFIG;
+    }
+    if (int st = lsr_energy_loop_reserve(P, W, err)) return st;
+    const long long ncells = W.cap;
+    EL_TRY(cudaMemsetAsync(W.ood, 0, sizeof(int), s));
+    const int T = 256;
+    if (P.dim == 3 && P.nx % 4 == 0) {
+        const unsigned tpr = static_cast<unsigned>((P.nx - 1 + 3) / 4);
+        const long long nt = static_cast<long long>(P.ny - 1) * tpr * ((P.nz - 1 + kMarchCells - 1) / kMarchCells);
+        flag_cells_march<<<static_cast<unsigned>((nt + T - 1) / T), T, 0, s>>>(P, phi, tpr, W.flags, 0, P.nz - 1);
+    } else {
+        flag_cells<<<static_cast<unsigned>((ncells + T - 1) / T), T, 0, s>>>(P, phi, 0, ncells, W.flags);
+    }
+    lsr_note_launch();
+    EL_TRY(lsr_compact::compact(lsr_compact::BytePred<FlagSet>{W.flags, {}}, CellId{}, ncells, W.cells, W.nc, W.tmp,
+                                W.tmp_bytes, s));
+    for (int q = 0; q < 2; ++q) lsr_note_launch();
+    // the contributions: an estimate of the count sizes the grid, which strides past it
+    const long long est = est_cells > 0 ? est_cells : 1;
+    if (P.dim == 3) {
+        const double dxp = P.dx / refine;
+        const double select = std::sqrt(3.0) / 2.0 * dxp;  // metrics.cpp:157
+        contrib_3d_hoisted<true><<<static_cast<unsigned>((est + LSR_EN_THREADS - 1) / LSR_EN_THREADS), LSR_EN_THREADS, 0,
+                             s>>>(P, phi, dist, W.cells, 0, refine, dxp, select, p, W.contrib, W.nc);
+    } else {
+        contrib_2d<true><<<static_cast<unsigned>((est + 127) / 128), 128, 0, s>>>(P, phi, dist, W.cells, 0, p, W.contrib,
+                                                                           W.ood, W.nc);
+    }
+    block_partials<<<148 * 4, 256, 0, s>>>(W.contrib, 0, W.partial, W.nc);
+    energy_finish<<<1, 32, 0, s>>>(W.partial, W.nc, p, W.ood, d_e2, d_flags);
+    for (int q = 0; q < 3; ++q) lsr_note_launch();
+    EL_TRY(cudaGetLastError());
+    return LSR_OK;
+#undef EL_TRY
 }

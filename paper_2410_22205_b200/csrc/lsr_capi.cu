@@ -192,6 +192,21 @@ struct lsr_cuda_ctx {
     bool slab = false;
     int win_lo = 0, win_hi = 0, own_lo = 0, own_hi = 0;
     EnergySlabWork ew;
+    // the device-controlled loop (lsr_cuda_loop_run): its device words,
+    // per-iteration records, count estimates and captured iteration graphs
+    struct LoopRun {
+        EnergyLoopWork ew;
+        ReinitLoopDev* rl = nullptr;
+        double* e2 = nullptr;
+        int* flags = nullptr;
+        int* k = nullptr;
+        void* stats = nullptr;  // LoopDevStat[cap]
+        int cap = 0;
+        long long est_active = 0, est_cells = 0;
+        cudaGraphExec_t exec[2] = {nullptr, nullptr};
+        std::string key[2];
+        int64_t launches[2] = {0, 0};  // kernels per replay (for lsr_cuda_kernel_launches)
+    } lr;
     long long reinit_nn = 0;
     unsigned long long* d_aux = nullptr;  // [0] halo misses, [1] reach bits
     // pipelined host entry: compute / D2H streams, per-chunk events, miss counter
@@ -327,6 +342,14 @@ int lsr_cuda_destroy(lsr_cuda_ctx* c) {
     cudaFree(c->exact);
     cudaFree(c->scratch);
     c->ew.release();
+    c->lr.ew.release();
+    cudaFree(c->lr.rl);
+    cudaFree(c->lr.e2);
+    cudaFree(c->lr.flags);
+    cudaFree(c->lr.k);
+    cudaFree(c->lr.stats);
+    for (auto& g : c->lr.exec)
+        if (g) cudaGraphExecDestroy(g);
     cudaFree(c->d_aux);
     c->band.release();
     c->rb.release();
@@ -1654,6 +1677,286 @@ int lsr_cuda_loop_step(lsr_cuda_ctx* c, const lsr_step_cfg* cfg, const lsr_reini
     cudaEventElapsedTime(&S.ms[2], ev[2], ev[3]);
     cudaEventElapsedTime(&S.ms[3], ev[3], ev[4]);
     if (stats) *stats = S;
+    return LSR_OK;
+}
+
+// ---- the device-controlled loop ------------------------------------------
+
+extern "C++" {
+namespace {
+
+// one iteration's record, written by the device (globaltimer marks at the
+// phase boundaries: start, band, E_2, SL, reinit)
+struct LoopDevStat {
+    double energy;
+    long long n_active, n_tube, n_cells, n_frozen;
+    int iterations, had_interface;
+    unsigned long long bad;
+    int flags, pad;
+    unsigned long long t[5];
+};
+
+__device__ __forceinline__ unsigned long long global_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+__global__ void loop_mark(LoopDevStat* st, const int* k, int phase) { st[*k].t[phase] = global_ns(); }
+
+// the iteration's record; clears the SL bad-node word and the flags for the
+// next iteration and advances the index
+__global__ void loop_record(LoopDevStat* st, int* k, const double* e2, const long long* band_counts,
+                            const long long* n_cells, const ReinitLoopDev* rl, unsigned long long* bad, int* flags,
+                            int p) {
+    LoopDevStat& r = st[*k];
+    r.t[4] = global_ns();
+    r.energy = *e2;
+    r.n_active = band_counts[0];
+    r.n_tube = band_counts[1];
+    r.n_cells = *n_cells;
+    r.n_frozen = rl->counts[0];
+    r.had_interface = (rl->flags[0] || rl->flags[1]) ? 1 : 0;
+    r.iterations = r.had_interface ? rl->iterations : 0;
+    r.bad = *bad;
+    // bit 0: a 2d front left the hull (E_2); bit 1: E_2 is NaN with p > 1
+    // (sl_step's "energy must be positive", evolve.cpp:45-46)
+    r.flags = *flags | ((p > 1 && isnan(*e2)) ? 2 : 0);
+    *bad = ~0ULL;
+    *flags = 0;
+    *k += 1;
+}
+
+int loop_reserve(lsr_cuda_ctx* c, int iterations) {
+    auto& L = c->lr;
+    if (!L.rl) LSR_CUDA_TRY(cudaMalloc(&L.rl, sizeof(ReinitLoopDev)));
+    if (!L.e2) LSR_CUDA_TRY(cudaMalloc(&L.e2, sizeof(double)));
+    if (!L.flags) LSR_CUDA_TRY(cudaMalloc(&L.flags, sizeof(int)));
+    if (!L.k) LSR_CUDA_TRY(cudaMalloc(&L.k, sizeof(int)));
+    if (iterations > L.cap) {
+        cudaFree(L.stats);
+        L.stats = nullptr;
+        L.cap = 0;
+        LSR_CUDA_TRY(cudaMalloc(&L.stats, sizeof(LoopDevStat) * static_cast<size_t>(iterations)));
+        L.cap = iterations;
+    }
+    if (!c->scratch) LSR_CUDA_TRY(cudaMalloc(&c->scratch, sizeof(double) * c->n));
+    std::string err;
+    if (int st = c->band.reserve(c->n, &err)) return set_err(st, err);
+    if (int st = lsr_reinit_loop_reserve(c->n, c->rb, &err)) return set_err(st, err);
+    if (int st = lsr_energy_loop_reserve(grid_params(c->grid), L.ew, &err)) return set_err(st, err);
+    if (!c->zt.zt && c->grid.dim == 3) {
+        const long long nb = zt_num_bricks(c->grid.dims);
+        LSR_CUDA_TRY(cudaMalloc(&c->zt.zt, sizeof(double) * 4 * static_cast<size_t>(c->n)));
+        LSR_CUDA_TRY(cudaMalloc(&c->zt.zc, sizeof(double) * 2 * static_cast<size_t>(c->n)));
+        LSR_CUDA_TRY(cudaMalloc(&c->zt.mark, static_cast<size_t>(nb)));
+        LSR_CUDA_TRY(cudaMalloc(&c->zt.reach, sizeof(unsigned) * static_cast<size_t>(nb)));
+        LSR_CUDA_TRY(cudaMalloc(&c->zt.list, sizeof(unsigned) * static_cast<size_t>(nb)));
+        LSR_CUDA_TRY(cudaMalloc(&c->zt.count, 2 * sizeof(unsigned)));
+    }
+    return LSR_OK;
+}
+
+// enqueues one loop iteration (driver.cpp:187-203) on the context stream: phi^n
+// in a, out (equal to a on entry) in b; afterwards both hold phi^{n+1}. No
+// host round trip and no allocation: capturable into a CUDA graph.
+int enqueue_loop_iteration(lsr_cuda_ctx* c, double* a, double* b, const lsr_step_cfg* cfg, const lsr_reinit_cfg* rc,
+                           int refine, bool clamp_sparse) {
+    auto& L = c->lr;
+    cudaStream_t s = c->stream;
+    const SlParams G = grid_params(c->grid);
+    LoopDevStat* st = static_cast<LoopDevStat*>(L.stats);
+    std::string err;
+    loop_mark<<<1, 1, 0, s>>>(st, L.k, 0);
+    // 1. band of phi^n (driver.cpp:187)
+    if (int e = lsr_band_enqueue(G, a, cfg->gamma, c->band, s, &err)) return set_err(e, err);
+    loop_mark<<<1, 1, 0, s>>>(st, L.k, 1);
+    // 2. E_2 of phi^n (driver.cpp:188)
+    if (int e = lsr_energy_enqueue(G, a, c->dist, 2, refine, L.ew, L.est_cells, L.e2, L.flags, s, &err))
+        return set_err(e, err);
+    loop_mark<<<1, 1, 0, s>>>(st, L.k, 2);
+    // 3. sl_step a -> b on the band's ACTIVE ids, E_2 read on the device; the
+    // kernels skip when p > 1 and E_2 == 0 (driver.cpp:191-195; b already
+    // equals a)
+    SlParams P = make_params(c->grid, *cfg, 1.0);
+    P.energy_dev = L.e2;
+    P.n_dev = c->band.counts;
+    const int64_t* ids = reinterpret_cast<const int64_t*>(c->band.active);
+    const bool use_table = LSR_ZTAB && c->grid.dim == 3 && cfg->interp == 1 && P.fast_weno &&
+                           c->grid.dims[2] >= 4 && cfg->delta > 0.0;
+    if (use_table) {
+        LSR_CUDA_TRY(launch_zt_bricks(P, c->dist, ids, L.est_active, c->zt, s));
+        LSR_CUDA_TRY(launch_zt_fill(P, a, c->zt, s));
+        zt_attach(P, c->zt);
+    }
+    LSR_CUDA_TRY(launch_sl_step(P, cfg->interp, a, c->dist, ids, L.est_active, b, c->d_bad, s));
+    loop_mark<<<1, 1, 0, s>>>(st, L.k, 3);
+    // 4. reinitialise phi^{n+1} on the band of phi^n (driver.cpp:196), then a
+    // takes phi^{n+1} where it may differ (the swap, driver.cpp:203, is the
+    // caller's exchange of a and b)
+    const ReinitParams R{rc->dtau, rc->max_iters, rc->residual_tol, rc->sign_eps};
+    if (int e = lsr_reinit_enqueue(G, b, c->scratch, c->band, cfg->gamma, R, c->rb, L.rl, clamp_sparse, s, &err))
+        return set_err(e, err);
+    if (int e = lsr_loop_sync_fields(G, b, a, c->band, c->rb, L.rl, s, &err)) return set_err(e, err);
+    loop_record<<<1, 1, 0, s>>>(st, L.k, L.e2, c->band.counts, L.ew.nc, L.rl, c->d_bad, L.flags, cfg->p);
+    for (int q = 0; q < 5; ++q) lsr_note_launch();
+    LSR_CUDA_TRY(cudaGetLastError());
+    return LSR_OK;
+}
+
+std::string loop_key(const lsr_cuda_ctx* c, const double* a, const double* b, const lsr_step_cfg* cfg,
+                     const lsr_reinit_cfg* rc, int refine) {
+    std::string k;
+    const auto put = [&k](const void* p, size_t n) { k.append(static_cast<const char*>(p), n); };
+    put(&a, sizeof a);
+    put(&b, sizeof b);
+    put(&c->scratch, sizeof c->scratch);
+    put(&c->dist, sizeof c->dist);
+    put(cfg, sizeof *cfg);
+    put(rc, sizeof *rc);
+    put(&refine, sizeof refine);
+    put(&c->lr.est_active, sizeof c->lr.est_active);
+    put(&c->lr.est_cells, sizeof c->lr.est_cells);
+    return k;
+}
+
+// the graph of one iteration with (a, b) in slot q, captured on first use and
+// whenever its key changes
+int loop_graph(lsr_cuda_ctx* c, int q, double* a, double* b, const lsr_step_cfg* cfg, const lsr_reinit_cfg* rc,
+               int refine, cudaGraphExec_t* out) {
+    auto& L = c->lr;
+    const std::string key = loop_key(c, a, b, cfg, rc, refine);
+    if (L.exec[q] && L.key[q] == key) {
+        *out = L.exec[q];
+        return LSR_OK;
+    }
+    if (L.exec[q]) cudaGraphExecDestroy(L.exec[q]);
+    L.exec[q] = nullptr;
+    const int64_t n0 = lsr_cuda_kernel_launches();
+    LSR_CUDA_TRY(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+    const int st = enqueue_loop_iteration(c, a, b, cfg, rc, refine, true);
+    cudaGraph_t g = nullptr;
+    const cudaError_t ce = cudaStreamEndCapture(c->stream, &g);
+    if (st) {
+        if (g) cudaGraphDestroy(g);
+        return st;
+    }
+    LSR_CUDA_TRY(ce);
+    const cudaError_t ie = cudaGraphInstantiate(&L.exec[q], g, 0);
+    cudaGraphDestroy(g);
+    LSR_CUDA_TRY(ie);
+    L.key[q] = key;
+    L.launches[q] = lsr_cuda_kernel_launches() - n0;
+    g_launches.fetch_sub(L.launches[q], std::memory_order_relaxed);  // counted when replayed
+    *out = L.exec[q];
+    return LSR_OK;
+}
+
+}  // namespace
+}  // extern "C++"
+
+int lsr_cuda_loop_run(lsr_cuda_ctx* c, const lsr_step_cfg* cfg, const lsr_reinit_cfg* rc, int energy_refine,
+                      int iterations, int use_graph, lsr_loop_stats* stats, int* done) {
+    if (done) *done = 0;
+    if (c && c->slab) return set_err(LSR_ERR_CONFIG, "loop_run: a z-slab context (use lsr_cuda_slab_*)");
+    if (!c || !cfg || !rc) return set_err(LSR_ERR_CONFIG, "loop_run: null argument");
+    if (iterations < 1) return set_err(LSR_ERR_CONFIG, "loop_run: iterations must be >= 1");
+    if (int st = check_cfg(cfg, 1.0)) return st;
+    if (!(rc->dtau > 0.0) || rc->max_iters < 1) return set_err(LSR_ERR_CONFIG, "reinit: invalid configuration");
+    if (!(cfg->gamma > 0.0)) return set_err(LSR_ERR_CONFIG, "narrow_band: gamma must be positive");
+    if (c->grid.dim == 3 && (energy_refine < 1 || energy_refine > 8))
+        return set_err(LSR_ERR_CONFIG, "loop_run: energy_refine must be in [1, 8]");
+    LSR_CUDA_TRY(cudaSetDevice(c->device));
+    auto& L = c->lr;
+    if (int st = loop_reserve(c, iterations)) return st;
+    cudaStream_t s = c->stream;
+    // count estimates size the grids of the count-driven launches (the
+    // kernels stride past them, so they decide speed only): the last run's
+    // counts, or the band of phi now
+    if (L.est_active <= 0) {
+        long long na = 0, nt = 0;
+        std::string err;
+        if (int st = lsr_band_build(grid_params(c->grid), c->phi, cfg->gamma, c->band, &na, &nt, s, &err))
+            return set_err(st, err);
+        L.est_active = na > 0 ? na : 1;
+        L.est_cells = na / 4 + 1;
+    }
+    const bool first_sparse =
+        c->clamped_seq == c->seq && c->clamped_phi == c->phi && c->clamped_gamma == cfg->gamma;
+    c->seq++;
+    LSR_CUDA_TRY(cudaMemsetAsync(L.k, 0, sizeof(int), s));
+    LSR_CUDA_TRY(cudaMemsetAsync(L.flags, 0, sizeof(int), s));
+    LSR_CUDA_TRY(cudaMemsetAsync(c->d_bad, 0xff, sizeof(unsigned long long), s));
+    // out = phi on entry (afterwards every iteration leaves the two equal)
+    LSR_CUDA_TRY(cudaMemcpyAsync(c->out, c->phi, sizeof(double) * c->n, cudaMemcpyDeviceToDevice, s));
+    double* a = c->phi;
+    double* b = c->out;
+    for (int it = 0; it < iterations; ++it) {
+        if (it == 0 || !use_graph) {
+            if (int st = enqueue_loop_iteration(c, a, b, cfg, rc, energy_refine, it > 0 || first_sparse)) return st;
+        } else {
+            cudaGraphExec_t g = nullptr;
+            const int q = (a == c->phi) ? 0 : 1;
+            if (int st = loop_graph(c, q, a, b, cfg, rc, energy_refine, &g)) return st;
+            LSR_CUDA_TRY(cudaGraphLaunch(g, s));
+            g_launches.fetch_add(L.launches[q], std::memory_order_relaxed);
+        }
+        std::swap(a, b);
+    }
+    // the one host synchronisation of the run: the per-iteration records
+    std::vector<LoopDevStat> h(static_cast<size_t>(iterations));
+    LSR_CUDA_TRY(cudaMemcpyAsync(h.data(), L.stats, sizeof(LoopDevStat) * h.size(), cudaMemcpyDeviceToHost, s));
+    LSR_CUDA_TRY(cudaStreamSynchronize(s));
+    // the context after the run: phi = phi^{n+K} (fully clamped), out equal
+    // to it, the active set = the band of the last iteration's phi^n
+    c->phi = a;
+    c->out = b;
+    c->consistent = true;
+    c->n_dirty = 0;
+    c->dirty_is_active = false;
+    c->zt_bricks = false;
+    c->box_valid = false;
+    c->clamped_seq = ++c->seq;
+    c->clamped_phi = c->phi;
+    c->clamped_gamma = cfg->gamma;
+    const LoopDevStat& last = h.back();
+    c->band.n_active = last.n_active;
+    c->band.n_tube = last.n_tube;
+    c->rb.n_frozen = last.n_frozen;
+    if (int st = ensure_ids(&c->active, &c->cap_active, last.n_active)) return st;
+    if (last.n_active > 0)
+        LSR_CUDA_TRY(cudaMemcpyAsync(c->active, c->band.active, sizeof(int64_t) * last.n_active,
+                                     cudaMemcpyDeviceToDevice, s));
+    c->n_active = last.n_active;
+    L.est_active = last.n_active + last.n_active / 16 + 256;
+    L.est_cells = last.n_cells + last.n_cells / 16 + 256;
+    for (int it = 0; it < iterations; ++it) {
+        const LoopDevStat& r = h[static_cast<size_t>(it)];
+        if (stats) {
+            lsr_loop_stats& o = stats[it];
+            o.energy = r.energy;
+            o.n_active = r.n_active;
+            o.n_tube = r.n_tube;
+            o.reinit_iterations = r.iterations;
+            o.had_interface = r.had_interface;
+            for (int q = 0; q < 4; ++q) o.ms[q] = static_cast<float>(1e-6 * static_cast<double>(r.t[q + 1] - r.t[q]));
+        }
+        // the first failing iteration ends the run (the reference throws
+        // there; later iterations' results are unspecified)
+        if (r.flags & 1) {
+            if (done) *done = it;
+            return set_err(LSR_ERR_OUT_OF_DOMAIN, "locate_cell: point outside grid hull");
+        }
+        if (r.flags & 2) {
+            if (done) *done = it;
+            return set_err(LSR_ERR, "sl_step: energy must be positive for p > 1");
+        }
+        if (r.bad != ~0ULL) {
+            if (done) *done = it;
+            return numerical_error(c->grid, r.bad, nullptr);
+        }
+    }
+    if (done) *done = iterations;
     return LSR_OK;
 }
 

@@ -25,6 +25,28 @@ int lsr_prep_fast_sweep(const lsr_grid* g, double* d_field, const unsigned char*
 int lsr_prep_surface_energy(const lsr_dev::SlParams& P, const double* phi, const double* dist, int p, int refine,
                             double* energy, int64_t* n_cells, cudaStream_t s, std::string* err);
 
+// E_p for the device-controlled loop (energy.cu): the same kernels with the
+// cell count kept in device memory and blocked_sum's final pass plus pow on
+// the device; *d_e2 = E_p, *d_flags |= 1 when a 2d front leaves the hull
+// (interp_q1 -> locate_cell throws, grid.cpp:40). Buffers sized for every
+// cell of the grid are reserved first (no allocation while enqueueing).
+struct EnergyLoopWork {
+    unsigned char* flags = nullptr;
+    int* cells = nullptr;
+    double* contrib = nullptr;
+    double* partial = nullptr;
+    long long* nc = nullptr;  // [0] interface cells
+    int* ood = nullptr;
+    void* tmp = nullptr;
+    size_t tmp_bytes = 0;
+    long long cap = 0;
+    void release();
+};
+int lsr_energy_loop_reserve(const lsr_dev::SlParams& P, EnergyLoopWork& W, std::string* err);
+int lsr_energy_enqueue(const lsr_dev::SlParams& P, const double* phi, const double* dist, int p, int refine,
+                       EnergyLoopWork& W, long long est_cells, double* d_e2, int* d_flags, cudaStream_t s,
+                       std::string* err);
+
 // lsr::compute_stats (cloud.cpp:480-489) with the NN sample on the device.
 int lsr_prep_compute_stats(const double* h_pts, int64_t n, int dim, double fraction, double k_s, uint64_t seed,
                            double* h_s, double* gamma_s, double* bbox6, cudaStream_t s, std::string* err);

@@ -70,24 +70,42 @@ __device__ __forceinline__ void store_update(const SlParams& P, long long id, in
     if (pushed) __threadfence_system();
 }
 
+// The device-controlled loop (loop_device.cu) launches the SL kernels on an
+// active count that lives in device memory (P.n_dev) and an E_2 the same
+// iteration computed on the device (P.energy_dev): the launch covers an
+// estimate of the count with one thread per node, and a TAIL launch of the
+// same kernel (a grid-stride loop from `base`) takes whatever lies beyond the
+// estimate. p > 1 with E_2 == 0 skips the step (driver.cpp:191-195: out keeps
+// phi, which the loop already holds in out); a non-finite E_2 is reported by
+// the loop. Host-driven launches: n_dev = energy_dev = null, base = 0.
+__device__ __forceinline__ long long sl_count(const SlParams& P, long long n_active) {
+    if (P.n_dev == nullptr) return n_active;
+    if (P.energy_dev != nullptr && P.p > 1 && !(__ldg(P.energy_dev) > 0.0)) return 0;
+    return __ldg(P.n_dev);
+}
+
 // one thread per active node (Q1, 2d)
-template <int DIM, int KIND>
+template <int DIM, int KIND, bool TAIL>
 __global__ void __launch_bounds__(kSlThreads, kSlMinBlocks) sl_step_kernel(SlParams P, const double* __restrict__ phi,
                                                                            const double* __restrict__ dist,
                                                                            const int64_t* __restrict__ active,
                                                                            long long n_active, double* __restrict__ out,
-                                                                           unsigned long long* __restrict__ bad) {
-    const long long a = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (a >= n_active) return;
-    const long long id = __ldg(active + a);
-    if (id_outside(P, id, bad)) return;
-    int i, j, k;
-    node_ijk(P, id, i, j, k);
-    if (slab_node_miss(P, k)) {  // nothing of a non-resident node is read or written
-        atomicAdd(P.halo_miss, 1ULL);
-        return;
+                                                                           unsigned long long* __restrict__ bad,
+                                                                           long long base) {
+    const long long n = sl_count(P, n_active);
+    for (long long a = base + static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; a < n;
+         a += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const long long id = __ldg(active + a);
+        if (!id_outside(P, id, bad)) {
+            int i, j, k;
+            node_ijk(P, id, i, j, k);
+            if (slab_node_miss(P, k))  // nothing of a non-resident node is read or written
+                atomicAdd(P.halo_miss, 1ULL);
+            else
+                store_update(P, id, k, sl_node<DIM, KIND>(P, phi, dist, id, i, j, k), out, bad);
+        }
+        if (!TAIL) break;
     }
-    store_update(P, id, k, sl_node<DIM, KIND>(P, phi, dist, id, i, j, k), out, bad);
 }
 
 // 3d WENO with the z-line table, one thread per active node (its own launch
@@ -95,22 +113,27 @@ __global__ void __launch_bounds__(kSlThreads, kSlMinBlocks) sl_step_kernel(SlPar
 // recomputing the node's gradients and basis, measured slower: 3.77 / 4.22
 // ms against 2.93 ms at 512^3 — the feet of a warp's nodes then touch 2-4x
 // as many L1 lines per table load, and L1 wavefronts are the busiest unit.)
+template <bool TAIL>
 __global__ void __launch_bounds__(kSlThreadsW3, kSlMinBlocksW3) sl_step_zt_kernel(
     SlParams P, const double* __restrict__ phi, const double* __restrict__ dist, const int64_t* __restrict__ active,
-    long long n_active, double* __restrict__ out, unsigned long long* __restrict__ bad) {
-    const long long a = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (a >= n_active) return;
-    const long long id = __ldg(active + a);
-    if (id_outside(P, id, bad)) return;
-    int i, j, k;
-    node_ijk(P, id, i, j, k);
-    if (slab_node_miss(P, k)) {
-        atomicAdd(P.halo_miss, 1ULL);
-        return;
+    long long n_active, double* __restrict__ out, unsigned long long* __restrict__ bad, long long base) {
+    const long long n = sl_count(P, n_active);
+    for (long long a = base + static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; a < n;
+         a += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const long long id = __ldg(active + a);
+        if (!id_outside(P, id, bad)) {
+            int i, j, k;
+            node_ijk(P, id, i, j, k);
+            if (slab_node_miss(P, k)) {
+                atomicAdd(P.halo_miss, 1ULL);
+            } else {
+                const bool use_zt = __ldg(P.ztab_bad) == 0u;
+                const double next = sl_node<3, 1>(P, phi, dist, id, i, j, k, use_zt);
+                store_update(P, id, k, next, out, bad);
+            }
+        }
+        if (!TAIL) break;
     }
-    const bool use_zt = __ldg(P.ztab_bad) == 0u;
-    const double next = sl_node<3, 1>(P, phi, dist, id, i, j, k, use_zt);
-    store_update(P, id, k, next, out, bad);
 }
 
 // ---- the TMA brick form of the 3d WENO step (sl_node_box) ----------------
@@ -238,9 +261,9 @@ __device__ __forceinline__ long long brick_of(int i, int j, int k, int nbx, int 
 // bound on a foot's displacement in cells along any axis, a foot cell lies in
 // [i - ceil(D), i + floor(D)]; packed as ceil(D) << 8 | floor(D) (monotone in
 // D, so atomicMax keeps the largest), D capped at kZtMaxReach
-__global__ void zt_reach_kernel(SlParams P, const double* __restrict__ dist, const int64_t* __restrict__ active,
-                                long long n, int nbx, int nby, unsigned* __restrict__ reach) {
-    const long long a = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+__device__ __forceinline__ void zt_reach_one(const SlParams& P, const double* __restrict__ dist,
+                                             const int64_t* __restrict__ active, long long a, long long n, int nbx,
+                                             int nby, unsigned* __restrict__ reach) {
     long long b = -1;
     unsigned r = 0;
     long long id = 0;
@@ -251,7 +274,7 @@ __global__ void zt_reach_kernel(SlParams P, const double* __restrict__ dist, con
     if (inside && !slab_node_miss(P, k)) {  // (a non-resident node is counted by the SL kernel)
         b = brick_of(i, j, k, nbx, nby);
         const double d_j = __ldg(dist + id);
-        const double c_j = P.p == 1 ? 1.0 : d_j / P.energy;  // scale_factor (evolve.cpp:32-38)
+        const double c_j = P.p == 1 ? 1.0 : d_j / energy_of(P);  // scale_factor (evolve.cpp:32-38)
         const double s = c_j * P.dt;
         const double spread = sqrt(fmax(0.0, c_j * P.delta * d_j * P.dt / P.pd));
         double m = fabs(s * grad_axis(P, dist, id, i, P.nx, 1));
@@ -274,6 +297,22 @@ __global__ void zt_reach_kernel(SlParams P, const double* __restrict__ dist, con
     if (b >= 0 && (threadIdx.x & 31) == static_cast<unsigned>(__ffs(same) - 1)) atomicMax(reach + b, rmax);
 }
 
+// one thread per active id; with P.n_dev (the device loop) the count is read
+// from device memory and the grid strides over it (whole warps per round,
+// as the warp-level reduction needs)
+__global__ void zt_reach_kernel(SlParams P, const double* __restrict__ dist, const int64_t* __restrict__ active,
+                                long long n, int nbx, int nby, unsigned* __restrict__ reach) {
+    const long long first = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (P.n_dev == nullptr) {
+        zt_reach_one(P, dist, active, first, n, nbx, nby, reach);
+        return;
+    }
+    const long long nd = __ldg(P.n_dev);
+    const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+    for (long long a = first; a - static_cast<long long>(threadIdx.x & 31) < nd; a += stride)
+        zt_reach_one(P, dist, active, a, nd, nbx, nby, reach);
+}
+
 // the largest foot displacement bound (cells, as zt_reach_kernel) over the
 // ids: *max_bits = max of the non-negative double bits (integer order =
 // double order). A z-slab sizes its halo planes from the max over ranks.
@@ -286,7 +325,7 @@ __global__ void reach_max_kernel(SlParams P, const double* __restrict__ dist, co
         int i, j, k;
         unflatten(P, id, i, j, k);
         const double d_j = __ldg(dist + id);
-        const double c_j = P.p == 1 ? 1.0 : d_j / P.energy;
+        const double c_j = P.p == 1 ? 1.0 : d_j / energy_of(P);
         const double s = c_j * P.dt;
         const double spread = sqrt(fmax(0.0, c_j * P.delta * d_j * P.dt / P.pd));
         double m = fabs(s * grad_axis(P, dist, id, i, P.nx, 1));
@@ -606,23 +645,44 @@ cudaError_t launch_weno_selftest(const SlParams& P, unsigned long long seed, lon
     return cudaGetLastError();
 }
 
+template <bool TAIL>
+static void sl_launch_form(const SlParams& P, int kind, const double* phi, const double* dist, const int64_t* active,
+                           long long n_active, double* out, unsigned long long* bad, long long base,
+                           unsigned blocks, unsigned blocks_w3, cudaStream_t stream) {
+    if (P.dim == 2) {
+        if (kind == 0)
+            sl_step_kernel<2, 0, TAIL><<<blocks, kSlThreads, 0, stream>>>(P, phi, dist, active, n_active, out, bad, base);
+        else
+            sl_step_kernel<2, 1, TAIL><<<blocks, kSlThreads, 0, stream>>>(P, phi, dist, active, n_active, out, bad, base);
+    } else if (kind == 0) {
+        sl_step_kernel<3, 0, TAIL><<<blocks, kSlThreads, 0, stream>>>(P, phi, dist, active, n_active, out, bad, base);
+    } else if (LSR_ZTAB && P.ztab != nullptr) {
+        sl_step_zt_kernel<TAIL><<<blocks_w3, kSlThreadsW3, 0, stream>>>(P, phi, dist, active, n_active, out, bad, base);
+    } else {
+        sl_step_kernel<3, 1, TAIL><<<blocks, kSlThreads, 0, stream>>>(P, phi, dist, active, n_active, out, bad, base);
+    }
+    lsr_note_launch();
+}
+
 cudaError_t launch_sl_step(const SlParams& P, int kind, const double* phi, const double* dist,
                            const int64_t* active, long long n_active, double* out, unsigned long long* bad,
                            cudaStream_t stream) {
+    if (P.n_dev != nullptr) {
+        // device count (the loop): n_active is the estimate the launch covers;
+        // the tail launch takes any ids beyond it
+        const long long est = n_active > 0 ? n_active : 1;
+        const bool w3 = P.dim == 3 && kind != 0 && LSR_ZTAB && P.ztab != nullptr;
+        const int T = w3 ? kSlThreadsW3 : kSlThreads;
+        const long long blk = (est + T - 1) / T;
+        sl_launch_form<false>(P, kind, phi, dist, active, est, out, bad, 0, static_cast<unsigned>(blk),
+                              static_cast<unsigned>(blk), stream);
+        sl_launch_form<true>(P, kind, phi, dist, active, est, out, bad, blk * T, 148u * 2u, 148u * 2u, stream);
+        return cudaGetLastError();
+    }
     if (n_active <= 0) return cudaSuccess;
     const unsigned blocks = static_cast<unsigned>((n_active + kSlThreads - 1) / kSlThreads);
     const unsigned blocks_w3 = static_cast<unsigned>((n_active + kSlThreadsW3 - 1) / kSlThreadsW3);
-    if (P.dim == 2) {
-        if (kind == 0) sl_step_kernel<2, 0><<<blocks, kSlThreads, 0, stream>>>(P, phi, dist, active, n_active, out, bad);
-        else sl_step_kernel<2, 1><<<blocks, kSlThreads, 0, stream>>>(P, phi, dist, active, n_active, out, bad);
-    } else if (kind == 0) {
-        sl_step_kernel<3, 0><<<blocks, kSlThreads, 0, stream>>>(P, phi, dist, active, n_active, out, bad);
-    } else if (LSR_ZTAB && P.ztab != nullptr) {
-        sl_step_zt_kernel<<<blocks_w3, kSlThreadsW3, 0, stream>>>(P, phi, dist, active, n_active, out, bad);
-    } else {
-        sl_step_kernel<3, 1><<<blocks, kSlThreads, 0, stream>>>(P, phi, dist, active, n_active, out, bad);
-    }
-    lsr_note_launch();
+    sl_launch_form<false>(P, kind, phi, dist, active, n_active, out, bad, 0, blocks, blocks_w3, stream);
     return cudaGetLastError();
 }
 
@@ -634,10 +694,12 @@ cudaError_t launch_zt_bricks(const SlParams& P, const double* dist, const int64_
     cudaError_t e = cudaMemsetAsync(Z.mark, 0, static_cast<size_t>(nbricks), stream);
     if (e == cudaSuccess) e = cudaMemsetAsync(Z.reach, 0, sizeof(unsigned) * static_cast<size_t>(nbricks), stream);
     if (e == cudaSuccess) e = cudaMemsetAsync(Z.count, 0, sizeof(unsigned), stream);
-    if (e != cudaSuccess || n_active <= 0) return e;
+    if (e != cudaSuccess || (n_active <= 0 && P.n_dev == nullptr)) return e;
     const unsigned gb = static_cast<unsigned>((nbricks + 255) / 256);
-    zt_reach_kernel<<<static_cast<unsigned>((n_active + 255) / 256), 256, 0, stream>>>(P, dist, active, n_active, nbx,
-                                                                                      nby, Z.reach);
+    // device count (P.n_dev): n_active is an estimate, the grid strides past it
+    const long long est = n_active > 0 ? n_active : 1;
+    zt_reach_kernel<<<static_cast<unsigned>((est + 255) / 256), 256, 0, stream>>>(P, dist, active, n_active, nbx, nby,
+                                                                                 Z.reach);
     zt_cover_kernel<<<gb, 256, 0, stream>>>(Z.reach, nbx, nby, nbz, Z.mark);
     zt_list_kernel<<<gb, 256, 0, stream>>>(Z.mark, nbricks, Z.list, Z.count);
     for (int r = 0; r < 3; ++r) lsr_note_launch();
