@@ -275,6 +275,8 @@ typedef struct lsr_loop_stats {
     int32_t reinit_iterations;
     int32_t had_interface;
     float ms[4];
+    int32_t dense_one_step; /* the one-step visited every node (else the tube only: lsr_cuda_loop_run) */
+    int32_t reserved;
 } lsr_loop_stats;
 int lsr_cuda_loop_step(lsr_cuda_ctx* ctx, const lsr_step_cfg* cfg, const lsr_reinit_cfg* rcfg, int energy_refine,
                        double energy_override, lsr_loop_stats* stats);

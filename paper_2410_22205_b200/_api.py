@@ -178,7 +178,8 @@ class CReinitCfg(C.Structure):  # ReinitConfig (reinit.hpp:7-18)
 
 class CLoopStats(C.Structure):
     _fields_ = [("energy", C.c_double), ("n_active", C.c_int64), ("n_tube", C.c_int64),
-                ("reinit_iterations", C.c_int32), ("had_interface", C.c_int32), ("ms", C.c_float * 4)]
+                ("reinit_iterations", C.c_int32), ("had_interface", C.c_int32), ("ms", C.c_float * 4),
+                ("dense_one_step", C.c_int32), ("reserved", C.c_int32)]
 
 
 @dataclass
@@ -630,7 +631,8 @@ class Context:
         _check(lib().lsr_cuda_loop_run(self.h, C.byref(cfg.c()), C.byref(rcfg.c()), int(energy_refine), n,
                                        1 if use_graph else 0, recs, C.byref(done)))
         return [dict(energy=r.energy, n_active=r.n_active, n_tube=r.n_tube, reinit_iterations=r.reinit_iterations,
-                     had_interface=bool(r.had_interface), ms=list(r.ms)) for r in recs]
+                     had_interface=bool(r.had_interface), ms=list(r.ms), dense_one_step=bool(r.dense_one_step))
+                for r in recs]
 
     def last_times(self):
         k, s = C.c_float(), C.c_float()

@@ -215,15 +215,34 @@ __global__ void clamp_kernel(double* __restrict__ f, long long n, double gamma, 
     if (state && __double_as_longlong(c) != __double_as_longlong(v) && !state[id]) *outside = 1;
 }
 
+// The device loop's one-step gate (lsr_reinit_enqueue): the dense one-step
+// runs only when *only_if is set (the field may have a "hard jump", below),
+// and it reports hard jumps of its input in *hard. A hard jump is an axis
+// pair of opposite signs with neither node ACTIVE (|phi| < gamma fails for
+// both). Without one, every sign-change pair of the SL output has a node in
+// the band's ACTIVE set, so every frozen node lies in the tube and the
+// one-step can visit the tube only (one_step_tube).
+struct OneStepGate {
+    const int* only_if;
+    int* hard;
+    double gamma;
+};
+
+__device__ __forceinline__ bool hard_pair(double pj, double pk, double gamma) {
+    return pj * pk < 0.0 && !(fabs(pj) < gamma) && !(fabs(pk) < gamma);
+}
+
 // interface_one_step (reinit.cpp:24-46); `prev` is read-only, `out` gets every
 // node. The two "any" flags are raised once per warp (a single-address store
 // from every frozen node serialises in L2).
 // (prev, out, frozen point at node `base`, items [0, n): a z-slab's owned ids)
+template <bool kGate = false>
 __global__ void one_step(SlParams P, const double* __restrict__ prev, double* __restrict__ out,
                          unsigned char* __restrict__ frozen, long long n, int* __restrict__ any_frozen,
-                         int* __restrict__ any_zero, long long base) {
+                         int* __restrict__ any_zero, long long base, OneStepGate gate = {}) {
+    if (kGate && !*gate.only_if) return;
     const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-    bool is_zero = false, is_frozen = false;
+    bool is_zero = false, is_frozen = false, is_hard = false;
     if (t < n) {
         const long long id = base + t;
         prev -= base;
@@ -250,6 +269,7 @@ __global__ void one_step(SlParams P, const double* __restrict__ prev, double* __
                 if (!has[q]) continue;
                 const double pk = v[q];
                 if (pj * pk >= 0.0) continue;
+                if (kGate && hard_pair(pj, pk, gate.gamma)) is_hard = true;
                 const double crossing = P.dx * fabs(pj) / (fabs(pj) + fabs(pk));
                 best = best < 0.0 ? crossing : smin(best, crossing);
             }
@@ -266,13 +286,16 @@ __global__ void one_step(SlParams P, const double* __restrict__ prev, double* __
         if (zb) *any_zero = 1;
         if (fb) *any_frozen = 1;
     }
+    if (kGate && __any_sync(0xffffffffu, is_hard) && (threadIdx.x & 31) == 0) *gate.hard = 1;
 }
 
 // one_step for 3d grids with nx % 4 == 0: four consecutive nodes of a row
 // per thread, the node values and their y/z neighbours as 16-byte loads;
 // per node the same arithmetic in the same neighbour order as one_step
+template <bool kGate = false>
 __device__ __forceinline__ void one_node(const SlParams& P, double pj, const double* v, const bool* has,
-                                         double& val, bool& is_zero, bool& is_frozen) {
+                                         double& val, bool& is_zero, bool& is_frozen, bool* is_hard = nullptr,
+                                         double gamma = 0.0) {
     val = pj;
     if (pj == 0.0) {
         is_zero = true;
@@ -290,6 +313,7 @@ __device__ __forceinline__ void one_node(const SlParams& P, double pj, const dou
         if (!has[q]) continue;
         const double pk = v[q];
         if (pj * pk >= 0.0) continue;
+        if (kGate && hard_pair(pj, pk, gamma)) *is_hard = true;
         const double crossing = P.dx * fabs(pj) / (fabs(pj) + fabs(pk));
         best = best < 0.0 ? crossing : smin(best, crossing);
     }
@@ -321,9 +345,12 @@ constexpr int kMarch = LSR_MARCH_PLANES;
 #define LSR_MARCH_MINB 4  // 64 registers: occupancy beats the few spills (reinit 4.82 -> 4.71 ms at 512^3)
 #endif
 // planes [k_lo, k_hi) (the whole grid: 0, nz; a z-slab: its owned planes)
+template <bool kGate = false>
 __global__ void __launch_bounds__(256, LSR_MARCH_MINB) one_step_march(SlParams P, const double* __restrict__ prev, double* __restrict__ out,
                                unsigned* __restrict__ frozen4, int* __restrict__ any_frozen,
-                               int* __restrict__ any_zero, int k_lo, int k_hi) {
+                               int* __restrict__ any_zero, int k_lo, int k_hi, OneStepGate gate = {}) {
+    if (kGate && !*gate.only_if) return;
+    bool hard = false;
     const int qx = P.nx / 4;
     const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
     const long long rows = static_cast<long long>(qx) * P.ny;  // (x-quad, j) pairs
@@ -353,7 +380,7 @@ __global__ void __launch_bounds__(256, LSR_MARCH_MINB) one_step_march(SlParams P
                 const double v[6] = {q > 0 ? c[q - 1] : xl, q < 3 ? c[q + 1] : xr, ym[q], yp[q], zm[q], zp[q]};
                 const bool has[6] = {x0 + q > 0, x0 + q + 1 < P.nx, hy[0], hy[1], hz[0], hz[1]};
                 bool z = false, f = false;
-                one_node(P, c[q], v, has, res[q], z, f);
+                one_node<kGate>(P, c[q], v, has, res[q], z, f, &hard, gate.gamma);
                 zero |= z;
                 froz |= f;
                 fb |= (f ? 1u : 0u) << (8 * q);
@@ -372,6 +399,47 @@ __global__ void __launch_bounds__(256, LSR_MARCH_MINB) one_step_march(SlParams P
     if ((threadIdx.x & 31) == 0) {
         if (zb) *any_zero = 1;
         if (fbal) *any_frozen = 1;
+    }
+    if (kGate && __any_sync(0xffffffffu, hard) && (threadIdx.x & 31) == 0) *gate.hard = 1;
+}
+
+// interface_one_step on the band's tube only (the device loop, when the field
+// has no hard jump — see OneStepGate): the tube nodes' values and frozen
+// flags, same per-node arithmetic and neighbour order as one_step. Nodes off
+// the tube are neither frozen nor changed, and the loop keeps `out` equal to
+// `prev` there. Runs only when *gate.only_if is clear.
+__global__ void one_step_tube(SlParams P, const double* __restrict__ prev, double* __restrict__ out,
+                              unsigned char* __restrict__ frozen, const long long* __restrict__ tube,
+                              const long long* __restrict__ n_dev, int* __restrict__ any_frozen,
+                              int* __restrict__ any_zero, const int* __restrict__ dense) {
+    if (*dense) return;
+    const long long n = __ldg(n_dev);
+    bool zero = false, froz = false;
+    const long long T = static_cast<long long>(gridDim.x) * blockDim.x;
+    for (long long t0 = static_cast<long long>(blockIdx.x) * blockDim.x; t0 < n; t0 += T) {
+        const long long t = t0 + threadIdx.x;
+        if (t >= n) break;
+        const long long id = __ldg(tube + t);
+        int i, j, k;
+        lsr_dev::unflatten(P, id, i, j, k);
+        const bool has[6] = {i > 0, i + 1 < P.nx, j > 0, j + 1 < P.ny, P.dim == 3 && k > 0, P.dim == 3 && k + 1 < P.nz};
+        const long long st[3] = {1, P.nx, P.nxy};
+        double v[6];
+#pragma unroll
+        for (int q = 0; q < 6; ++q) v[q] = __ldg(prev + (has[q] ? id + ((q & 1) ? st[q >> 1] : -st[q >> 1]) : id));
+        const double pj = __ldg(prev + id);
+        double val;
+        bool z = false, f = false;
+        one_node(P, pj, v, has, val, z, f);
+        out[id] = val;
+        if (f) frozen[id] = 1;  // the flags are all clear on entry (lsr_loop_sync_fields clears them)
+        zero |= z;
+        froz |= f;
+    }
+    const unsigned zb = __ballot_sync(0xffffffffu, zero), fb = __ballot_sync(0xffffffffu, froz);
+    if ((threadIdx.x & 31) == 0) {
+        if (zb) *any_zero = 1;
+        if (fb) *any_frozen = 1;
     }
 }
 
@@ -769,6 +837,38 @@ __global__ void sweep_parity(double* __restrict__ b, double* __restrict__ c, con
         const long long id = ids[t];
         dst[id] = src[id];
     }
+}
+
+// the end of a device-loop iteration over an id list (tube or frozen ids):
+// a and c take b's values, the frozen flags (when given) are cleared, and a
+// node of b that is not ACTIVE and has an axis neighbour of the opposite sign
+// that is not ACTIVE either (a hard jump, see OneStepGate) raises *hard
+__global__ void loop_finish(SlParams P, const double* __restrict__ b, double* __restrict__ a, double* __restrict__ c,
+                            const long long* __restrict__ ids, const long long* __restrict__ n_dev,
+                            unsigned char* __restrict__ frozen, double gamma, int* __restrict__ hard) {
+    const long long n = __ldg(n_dev);
+    bool h = false;
+    const long long T = static_cast<long long>(gridDim.x) * blockDim.x;
+    for (long long t0 = static_cast<long long>(blockIdx.x) * blockDim.x; t0 < n; t0 += T) {
+        const long long t = t0 + threadIdx.x;
+        if (t >= n) break;
+        const long long id = ids[t];
+        const double v = b[id];
+        a[id] = v;
+        c[id] = v;
+        if (frozen) frozen[id] = 0;
+        if (!(fabs(v) < gamma)) {
+            int i, j, k;
+            lsr_dev::unflatten(P, id, i, j, k);
+            const bool has[6] = {i > 0, i + 1 < P.nx, j > 0, j + 1 < P.ny, P.dim == 3 && k > 0,
+                                 P.dim == 3 && k + 1 < P.nz};
+            const long long st[3] = {1, P.nx, P.nxy};
+#pragma unroll
+            for (int q = 0; q < 6; ++q)
+                if (has[q] && hard_pair(v, b[id + ((q & 1) ? st[q >> 1] : -st[q >> 1])], gamma)) h = true;
+        }
+    }
+    if (__any_sync(0xffffffffu, h) && (threadIdx.x & 31) == 0) *hard = 1;
 }
 
 // dst = src on every node when *flag is set (the dense clamp changed a node
@@ -1286,8 +1386,8 @@ int lsr_reinit_loop_reserve(long long n, ReinitBuffers& W, std::string* err) {
 // lsr_reinitialize); otherwise the dense clamp flags changes outside the
 // tube in L->clamp_outside.
 int lsr_reinit_enqueue(const SlParams& P, double* b, double* c, const BandBuffers& B, double gamma,
-                       const ReinitParams& R, ReinitBuffers& W, ReinitLoopDev* L, bool clamp_sparse, cudaStream_t s,
-                       std::string* err) {
+                       const ReinitParams& R, ReinitBuffers& W, ReinitLoopDev* L, bool clamp_sparse, int* hard,
+                       cudaStream_t s, std::string* err) {
     if (!(R.dtau > 0.0)) {
         *err = "reinit: dtau must be positive";  // reinit.hpp:14-17
         return LSR_ERR_CONFIG;
@@ -1304,15 +1404,21 @@ int lsr_reinit_enqueue(const SlParams& P, double* b, double* c, const BandBuffer
     if (int st = lsr_reinit_loop_reserve(n, W, err)) return st;
     BR_TRY(cudaMemsetAsync(L, 0, sizeof(ReinitLoopDev), s));
     int* flags = L->flags;
-    // interface_one_step (reinit.cpp:18-59): b -> c on every node
+    // interface_one_step (reinit.cpp:18-59), b -> c: on every node when hard[0]
+    // is set (the field may hold a hard jump: the run's first iteration, or
+    // one found by the last check), which also reports hard jumps of b in
+    // hard[1]; otherwise on the tube only (one_step_tube; c equals b off it)
+    const OneStepGate gate{hard, hard + 1, gamma};
     if (P.dim == 3 && P.nx % 4 == 0) {
         const long long threads = static_cast<long long>(P.nx / 4) * P.ny * ((P.nz + kMarch - 1) / kMarch);
-        one_step_march<<<static_cast<unsigned>((threads + 255) / 256), 256, 0, s>>>(
-            P, b, c, reinterpret_cast<unsigned*>(W.frozen), flags, flags + 1, 0, P.nz);
+        one_step_march<true><<<static_cast<unsigned>((threads + 255) / 256), 256, 0, s>>>(
+            P, b, c, reinterpret_cast<unsigned*>(W.frozen), flags, flags + 1, 0, P.nz, gate);
     } else {
-        one_step<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(P, b, c, W.frozen, n, flags, flags + 1, 0);
+        one_step<true><<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(P, b, c, W.frozen, n, flags, flags + 1,
+                                                                              0, gate);
     }
-    lsr_note_launch();
+    one_step_tube<<<kDevGrid, 256, 0, s>>>(P, b, c, W.frozen, B.tube, B.counts + 1, flags, flags + 1, hard);
+    for (int q = 0; q < 2; ++q) lsr_note_launch();
     // frozen ids and the sweep list (tube minus frozen, reinit.cpp:94-98), ascending
     BR_TRY(lsr_compact::compact2m(lsr_compact::BytePred<NonZero>{W.frozen, {}},
                                   lsr_compact::ByteAndNot{B.state, W.frozen}, lsr_compact::Identity{}, n,
@@ -1352,13 +1458,20 @@ int lsr_reinit_enqueue(const SlParams& P, double* b, double* c, const BandBuffer
 // (phi^{n+1}) where they may differ — the tube of phi^n, the frozen nodes,
 // and (if the dense clamp reported it) anywhere — so that the two fields are
 // equal when the next iteration's SL step writes its updates into a
-int lsr_loop_sync_fields(const SlParams& P, const double* b, double* a, const BandBuffers& B, const ReinitBuffers& W,
-                         const ReinitLoopDev* L, cudaStream_t s, std::string* err) {
+// ... and c (the scratch field) too, the frozen flags are cleared, and the
+// tube and frozen nodes of phi^{n+1} are checked for hard jumps (hard[1]):
+// pairs with both nodes off them kept the values (and signs, and
+// non-ACTIVE-ness: the clamp preserves both) they had in phi^n, which the
+// previous check (or the dense one-step) cleared
+int lsr_loop_sync_fields(const SlParams& P, const double* b, double* a, double* c, const BandBuffers& B,
+                         ReinitBuffers& W, const ReinitLoopDev* L, double gamma, int* hard, cudaStream_t s,
+                         std::string* err) {
     const long long n = P.nxy * P.nz;
-    copy_ids_dev<<<kDevGrid, 256, 0, s>>>(b, a, B.tube, B.counts + 1);
-    copy_ids_dev<<<kDevGrid, 256, 0, s>>>(b, a, W.frozen_ids, L->counts);
+    loop_finish<<<kDevGrid, 256, 0, s>>>(P, b, a, c, B.tube, B.counts + 1, nullptr, gamma, hard + 1);
+    loop_finish<<<kDevGrid, 256, 0, s>>>(P, b, a, c, W.frozen_ids, L->counts, W.frozen, gamma, hard + 1);
     copy_all_if<<<kDevGrid, 256, 0, s>>>(b, a, n, &L->clamp_outside);
-    for (int q = 0; q < 3; ++q) lsr_note_launch();
+    copy_all_if<<<kDevGrid, 256, 0, s>>>(b, c, n, &L->clamp_outside);
+    for (int q = 0; q < 4; ++q) lsr_note_launch();
     BR_TRY(cudaGetLastError());
     return LSR_OK;
 }

@@ -200,6 +200,7 @@ struct lsr_cuda_ctx {
         double* e2 = nullptr;
         int* flags = nullptr;
         int* k = nullptr;
+        int* hard = nullptr;    // [0] dense one-step this iteration, [1] a hard jump found for the next
         void* stats = nullptr;  // LoopDevStat[cap]
         int cap = 0;
         long long est_active = 0, est_cells = 0;
@@ -347,6 +348,7 @@ int lsr_cuda_destroy(lsr_cuda_ctx* c) {
     cudaFree(c->lr.e2);
     cudaFree(c->lr.flags);
     cudaFree(c->lr.k);
+    cudaFree(c->lr.hard);
     cudaFree(c->lr.stats);
     for (auto& g : c->lr.exec)
         if (g) cudaGraphExecDestroy(g);
@@ -1672,6 +1674,7 @@ int lsr_cuda_loop_step(lsr_cuda_ctx* c, const lsr_step_cfg* cfg, const lsr_reini
     S.n_tube = nt;
     S.reinit_iterations = it;
     S.had_interface = had;
+    S.dense_one_step = 1;
     cudaEventElapsedTime(&S.ms[0], ev[0], ev[1]);
     cudaEventElapsedTime(&S.ms[1], ev[1], ev[2]);
     cudaEventElapsedTime(&S.ms[2], ev[2], ev[3]);
@@ -1708,7 +1711,7 @@ __global__ void loop_mark(LoopDevStat* st, const int* k, int phase) { st[*k].t[p
 // next iteration and advances the index
 __global__ void loop_record(LoopDevStat* st, int* k, const double* e2, const long long* band_counts,
                             const long long* n_cells, const ReinitLoopDev* rl, unsigned long long* bad, int* flags,
-                            int p) {
+                            int p, int* hard) {
     LoopDevStat& r = st[*k];
     r.t[4] = global_ns();
     r.energy = *e2;
@@ -1722,8 +1725,11 @@ __global__ void loop_record(LoopDevStat* st, int* k, const double* e2, const lon
     // bit 0: a 2d front left the hull (E_2); bit 1: E_2 is NaN with p > 1
     // (sl_step's "energy must be positive", evolve.cpp:45-46)
     r.flags = *flags | ((p > 1 && isnan(*e2)) ? 2 : 0);
+    r.pad = hard[0];  // this iteration ran the dense one-step
     *bad = ~0ULL;
     *flags = 0;
+    hard[0] = hard[1];
+    hard[1] = 0;
     *k += 1;
 }
 
@@ -1733,6 +1739,7 @@ int loop_reserve(lsr_cuda_ctx* c, int iterations) {
     if (!L.e2) LSR_CUDA_TRY(cudaMalloc(&L.e2, sizeof(double)));
     if (!L.flags) LSR_CUDA_TRY(cudaMalloc(&L.flags, sizeof(int)));
     if (!L.k) LSR_CUDA_TRY(cudaMalloc(&L.k, sizeof(int)));
+    if (!L.hard) LSR_CUDA_TRY(cudaMalloc(&L.hard, 2 * sizeof(int)));
     if (iterations > L.cap) {
         cudaFree(L.stats);
         L.stats = nullptr;
@@ -1795,10 +1802,12 @@ int enqueue_loop_iteration(lsr_cuda_ctx* c, double* a, double* b, const lsr_step
     // takes phi^{n+1} where it may differ (the swap, driver.cpp:203, is the
     // caller's exchange of a and b)
     const ReinitParams R{rc->dtau, rc->max_iters, rc->residual_tol, rc->sign_eps};
-    if (int e = lsr_reinit_enqueue(G, b, c->scratch, c->band, cfg->gamma, R, c->rb, L.rl, clamp_sparse, s, &err))
+    if (int e = lsr_reinit_enqueue(G, b, c->scratch, c->band, cfg->gamma, R, c->rb, L.rl, clamp_sparse, L.hard, s,
+                                   &err))
         return set_err(e, err);
-    if (int e = lsr_loop_sync_fields(G, b, a, c->band, c->rb, L.rl, s, &err)) return set_err(e, err);
-    loop_record<<<1, 1, 0, s>>>(st, L.k, L.e2, c->band.counts, L.ew.nc, L.rl, c->d_bad, L.flags, cfg->p);
+    if (int e = lsr_loop_sync_fields(G, b, a, c->scratch, c->band, c->rb, L.rl, cfg->gamma, L.hard, s, &err))
+        return set_err(e, err);
+    loop_record<<<1, 1, 0, s>>>(st, L.k, L.e2, c->band.counts, L.ew.nc, L.rl, c->d_bad, L.flags, cfg->p, L.hard);
     for (int q = 0; q < 5; ++q) lsr_note_launch();
     LSR_CUDA_TRY(cudaGetLastError());
     return LSR_OK;
@@ -1887,6 +1896,10 @@ int lsr_cuda_loop_run(lsr_cuda_ctx* c, const lsr_step_cfg* cfg, const lsr_reinit
     LSR_CUDA_TRY(cudaMemsetAsync(L.k, 0, sizeof(int), s));
     LSR_CUDA_TRY(cudaMemsetAsync(L.flags, 0, sizeof(int), s));
     LSR_CUDA_TRY(cudaMemsetAsync(c->d_bad, 0xff, sizeof(unsigned long long), s));
+    // the first iteration runs the dense one-step (nothing is known of phi's
+    // hard jumps yet; its one-step and checks tell the next iteration)
+    const int hard0[2] = {1, 0};
+    LSR_CUDA_TRY(cudaMemcpyAsync(L.hard, hard0, sizeof hard0, cudaMemcpyHostToDevice, s));
     // out = phi on entry (afterwards every iteration leaves the two equal)
     LSR_CUDA_TRY(cudaMemcpyAsync(c->out, c->phi, sizeof(double) * c->n, cudaMemcpyDeviceToDevice, s));
     double* a = c->phi;
@@ -1940,6 +1953,8 @@ int lsr_cuda_loop_run(lsr_cuda_ctx* c, const lsr_step_cfg* cfg, const lsr_reinit
             o.reinit_iterations = r.iterations;
             o.had_interface = r.had_interface;
             for (int q = 0; q < 4; ++q) o.ms[q] = static_cast<float>(1e-6 * static_cast<double>(r.t[q + 1] - r.t[q]));
+            o.dense_one_step = r.pad;
+            o.reserved = 0;
         }
         // the first failing iteration ends the run (the reference throws
         // there; later iterations' results are unspecified)

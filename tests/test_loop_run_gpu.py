@@ -76,6 +76,9 @@ def test_loop_run_matches_host_loop(gpu, config, iters):
     recs = _compare(lsr, g, pts, phi, cfg, rc, iters)
     assert all(r["reinit_iterations"] > 0 for r in recs)
     assert all(sum(r["ms"]) > 0 for r in recs)
+    # the run's first one-step visits every node; the smooth fields after it
+    # have no hard jump, so the rest visit the tube only
+    assert recs[0]["dense_one_step"] and not any(r["dense_one_step"] for r in recs[1:])
 
 
 def test_loop_run_2d_config1(gpu):
@@ -112,3 +115,19 @@ def test_loop_run_config_errors(gpu):
         assert len(ctx.loop_run(cfg, rc, 2)) == 2
     finally:
         ctx.close()
+
+
+def test_loop_run_hard_jump_keeps_dense_one_step(gpu):
+    """A field with opposite-sign neighbours that are both outside the band
+    (a "hard jump", here a slab of the far corner flipped to -1): the one-step
+    freezes nodes away from the tube, so the device loop must keep visiting
+    every node while such pairs exist — and stay bit-identical to the host loop."""
+    lsr = gpu
+    g, pts, phi, cfg, rc = _setup(lsr, 2, n=64)
+    ax = g.axes()
+    x = np.broadcast_to(ax[0][None, None, :], (64, 64, 64)).ravel()
+    y = np.broadcast_to(ax[1][None, :, None], (64, 64, 64)).ravel()
+    phi = phi.copy()
+    phi[(x > 0.9) & (y > 0.9)] = -1.0
+    recs = _compare(lsr, g, pts, phi, cfg, rc, 6)
+    assert recs[0]["dense_one_step"] and recs[1]["dense_one_step"]
