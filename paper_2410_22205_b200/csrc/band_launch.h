@@ -73,9 +73,11 @@ struct ReinitLoopDev {
     unsigned long long residual_bits;  // the sweeps' control (band_reinit.cu IterState)
     int done;
     int iterations;
+    unsigned arrived;
+    unsigned pad2;
 };
 int lsr_band_enqueue(const lsr_dev::SlParams& P, const double* phi, double gamma, BandBuffers& B, cudaStream_t s,
-                     std::string* err);
+                     std::string* err, const int* hard = nullptr);
 int lsr_reinit_loop_reserve(long long n, ReinitBuffers& W, std::string* err);
 // hard[0]: run the dense one-step (the field may hold a hard jump); hard[1]:
 // set when this iteration finds one in phi^{n+1} (see band_reinit.cu
@@ -83,9 +85,9 @@ int lsr_reinit_loop_reserve(long long n, ReinitBuffers& W, std::string* err);
 int lsr_reinit_enqueue(const lsr_dev::SlParams& P, double* b, double* c, const BandBuffers& B, double gamma,
                        const ReinitParams& R, ReinitBuffers& W, ReinitLoopDev* L, bool clamp_sparse, int* hard,
                        cudaStream_t s, std::string* err);
-int lsr_loop_sync_fields(const lsr_dev::SlParams& P, const double* b, double* a, double* c, const BandBuffers& B,
-                         ReinitBuffers& W, const ReinitLoopDev* L, double gamma, int* hard, cudaStream_t s,
-                         std::string* err);
+int lsr_loop_sync_fields(const lsr_dev::SlParams& P, double* b, double* a, double* c, const BandBuffers& B,
+                         ReinitBuffers& W, const ReinitLoopDev* L, double gamma, int* hard, bool clamp_sparse,
+                         cudaStream_t s, std::string* err);
 
 // z-slab forms (band_reinit.cu): owned planes [own_lo, own_hi) of buffers
 // resident on [win_lo, win_hi), passed shifted to global node ids

@@ -50,11 +50,21 @@ __device__ __forceinline__ double markstein(double a, double c, double rc) {
     return __fma_rn(__fma_rn(-q, c, a), rc, q);
 }
 
+constexpr int kTubeBatch = 4;  // list entries per thread and round in the device loop's list passes
+
 struct IterState {  // device-side control of the Jacobi sweeps
     unsigned long long residual_bits;
     int done;
     int iterations;
+    unsigned arrived;  // CTAs of the running sweep that have reduced their residual (jacobi_pipe's fused stop rule)
+    unsigned pad;
 };
+
+// the stop rule after a sweep (reinit.cpp:125-128) on the sweep's residual
+__device__ __forceinline__ void stop_rule(IterState* st, unsigned long long residual_bits, double tol) {
+    st->iterations += 1;
+    if (__longlong_as_double(static_cast<long long>(residual_bits)) < tol) st->done = 1;
+}
 
 // narrow_band state (grid.cpp:85-116): 1 ACTIVE, 2 REINIT_HALO, 0 INACTIVE.
 // The halo test "some node of the 3^dim box is ACTIVE" is a separable
@@ -125,6 +135,51 @@ __global__ void band_pass_x4(SlParams P, const double* __restrict__ phi, double 
     t[q] = o0 | (o1 << 8) | (o2 << 16) | (o3 << 24);
 }
 
+// band_pass_x4's quad: the 4 output bytes of nodes id .. id + 3
+__device__ __forceinline__ unsigned band_quad(const SlParams& P, const double* __restrict__ phi, double gamma,
+                                              long long id, int x0) {
+    const double2 a = __ldg(reinterpret_cast<const double2*>(phi + id));
+    const double2 b = __ldg(reinterpret_cast<const double2*>(phi + id) + 1);
+    const bool c0 = fabs(a.x) < gamma, c1 = fabs(a.y) < gamma, c2 = fabs(b.x) < gamma, c3 = fabs(b.y) < gamma;
+    const bool l = x0 > 0 && fabs(__ldg(phi + id - 1)) < gamma;
+    const bool r = x0 + 4 < P.nx && fabs(__ldg(phi + id + 4)) < gamma;
+    const unsigned o0 = (c0 ? 2u : 0u) | ((c0 || l || c1) ? 1u : 0u);
+    const unsigned o1 = (c1 ? 2u : 0u) | ((c1 || c0 || c2) ? 1u : 0u);
+    const unsigned o2 = (c2 ? 2u : 0u) | ((c2 || c1 || c3) ? 1u : 0u);
+    const unsigned o3 = (c3 ? 2u : 0u) | ((c3 || c2 || r) ? 1u : 0u);
+    return o0 | (o1 << 8) | (o2 << 16) | (o3 << 24);
+}
+
+// The device loop's x pass (rows of whole 16-node groups): 16 nodes per
+// thread. old_state = the band's state bytes of the previous iteration; when
+// *skip_if_clear == 0 the field differs from that iteration's only on its
+// tube — SL on the ACTIVE nodes, one-step and sweeps on the tube, a clamp
+// that only produces +-gamma — so a node off the old tube is not ACTIVE now
+// either, and a quad whose nodes and x-neighbours were all off the tube
+// gives 0 without phi being read (most of the grid).
+__global__ void band_pass_x16(SlParams P, const double* __restrict__ phi, double gamma, long long n16,
+                              uint4* __restrict__ t, const unsigned char* __restrict__ old_state,
+                              const int* __restrict__ skip_if_clear) {
+    const long long q = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (q >= n16) return;
+    const long long id = 16 * q;
+    const int x0 = static_cast<int>(id % P.nx);
+    unsigned w[4] = {1u, 1u, 1u, 1u}, l = 1u, r = 1u;  // nonzero: the quad is evaluated
+    if (*skip_if_clear == 0) {
+        const uint4 o = __ldg(reinterpret_cast<const uint4*>(old_state + id));
+        w[0] = o.x, w[1] = o.y, w[2] = o.z, w[3] = o.w;
+        l = x0 > 0 ? __ldg(old_state + id - 1) : 0u;
+        r = x0 + 16 < P.nx ? __ldg(old_state + id + 16) : 0u;
+    }
+    unsigned out[4];
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {
+        const unsigned left = g == 0 ? l : (w[g - 1] >> 24), right = g == 3 ? r : (w[g + 1] & 0xffu);
+        out[g] = (w[g] | left | right) ? band_quad(P, phi, gamma, id + 4 * g, x0 + 4 * g) : 0u;
+    }
+    t[q] = make_uint4(out[0], out[1], out[2], out[3]);
+}
+
 __device__ __forceinline__ uint4 or4(uint4 a, uint4 b) { return make_uint4(a.x | b.x, a.y | b.y, a.z | b.z, a.w | b.w); }
 
 // per byte: core (bit 1) -> 1, else dilated (bit 0) -> 2, else 0
@@ -133,25 +188,52 @@ __device__ __forceinline__ unsigned state_bytes(unsigned core_bits, unsigned dil
     return b1 | ((b0 & ~b1) << 1);
 }
 
+// (c1, c2, the device loop's final pass over the whole grid: the CTA's 4096
+// nodes are one compaction tile (compact.cuh), whose ACTIVE and tube counts
+// it leaves in c1[blockIdx.x], c2[blockIdx.x] — compact2's count pass)
 __global__ void band_pass_yz16(SlParams P, int axis, const uint4* __restrict__ in, long long base16, long long end16,
-                               uint4* __restrict__ out, uint4* __restrict__ state) {
+                               uint4* __restrict__ out, uint4* __restrict__ state, long long* __restrict__ c1 = nullptr,
+                               long long* __restrict__ c2 = nullptr) {
     const long long q = base16 + static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (q >= end16) return;
-    const long long row = (16 * q) / P.nx;
-    const int j = static_cast<int>(row % P.ny), k = static_cast<int>(row / P.ny);
-    const long long st = (axis == 1 ? P.nx : P.nxy) / 16;
-    const bool has_m = axis == 1 ? j > 0 : k > 0, has_p = axis == 1 ? j < P.ny - 1 : k < P.nz - 1;
-    const uint4 c = in[q];
-    uint4 d = c;
-    if (has_m) d = or4(d, in[q - st]);
-    if (has_p) d = or4(d, in[q + st]);
-    const unsigned m = 0x01010101u;
-    if (axis == 1 && P.dim == 3) {  // keep core (bit 1) and the y-dilated bit 0 for the z pass
-        out[q] = make_uint4((c.x & (m << 1)) | (d.x & m), (c.y & (m << 1)) | (d.y & m), (c.z & (m << 1)) | (d.z & m),
-                            (c.w & (m << 1)) | (d.w & m));
-    } else {
-        state[q] = make_uint4(state_bytes(c.x >> 1, d.x), state_bytes(c.y >> 1, d.y), state_bytes(c.z >> 1, d.z),
-                              state_bytes(c.w >> 1, d.w));
+    int na = 0, nt = 0;
+    if (q < end16) {
+        const long long row = (16 * q) / P.nx;
+        const int j = static_cast<int>(row % P.ny), k = static_cast<int>(row / P.ny);
+        const long long st = (axis == 1 ? P.nx : P.nxy) / 16;
+        const bool has_m = axis == 1 ? j > 0 : k > 0, has_p = axis == 1 ? j < P.ny - 1 : k < P.nz - 1;
+        const uint4 c = in[q];
+        uint4 d = c;
+        if (has_m) d = or4(d, in[q - st]);
+        if (has_p) d = or4(d, in[q + st]);
+        const unsigned m = 0x01010101u;
+        if (axis == 1 && P.dim == 3) {  // keep core (bit 1) and the y-dilated bit 0 for the z pass
+            out[q] = make_uint4((c.x & (m << 1)) | (d.x & m), (c.y & (m << 1)) | (d.y & m),
+                                (c.z & (m << 1)) | (d.z & m), (c.w & (m << 1)) | (d.w & m));
+        } else {
+            const uint4 sb = make_uint4(state_bytes(c.x >> 1, d.x), state_bytes(c.y >> 1, d.y),
+                                        state_bytes(c.z >> 1, d.z), state_bytes(c.w >> 1, d.w));
+            state[q] = sb;
+            if (c1 != nullptr) {  // state bytes: 1 ACTIVE, 2 halo
+                na = __popc(sb.x & m) + __popc(sb.y & m) + __popc(sb.z & m) + __popc(sb.w & m);
+                nt = __popc((sb.x | (sb.x >> 1)) & m) + __popc((sb.y | (sb.y >> 1)) & m) +
+                     __popc((sb.z | (sb.z >> 1)) & m) + __popc((sb.w | (sb.w >> 1)) & m);
+            }
+        }
+    }
+    if (c1 != nullptr) {  // uniform per launch
+        const int v = __reduce_add_sync(0xffffffffu, (na << 16) | nt);  // both counts <= 4096 per CTA, 512 per warp
+        __shared__ int wsum[8];
+        if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = v;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int a = 0, b = 0;
+            for (int w = 0; w < 8; ++w) {
+                a += wsum[w] >> 16;
+                b += wsum[w] & 0xffff;
+            }
+            c1[blockIdx.x] = a;
+            c2[blockIdx.x] = b;
+        }
     }
 }
 
@@ -228,8 +310,11 @@ struct OneStepGate {
     double gamma;
 };
 
+// (a NaN product counts as one: a NaN node is in no band, and the sparse
+// forms of the loop — this one-step, the E_2 cell flags — must not miss it)
 __device__ __forceinline__ bool hard_pair(double pj, double pk, double gamma) {
-    return pj * pk < 0.0 && !(fabs(pj) < gamma) && !(fabs(pk) < gamma);
+    const double pr = pj * pk;
+    return pr != pr || (pr < 0.0 && !(fabs(pj) < gamma) && !(fabs(pk) < gamma));
 }
 
 // interface_one_step (reinit.cpp:24-46); `prev` is read-only, `out` gets every
@@ -415,26 +500,41 @@ __global__ void one_step_tube(SlParams P, const double* __restrict__ prev, doubl
     if (*dense) return;
     const long long n = __ldg(n_dev);
     bool zero = false, froz = false;
-    const long long T = static_cast<long long>(gridDim.x) * blockDim.x;
-    for (long long t0 = static_cast<long long>(blockIdx.x) * blockDim.x; t0 < n; t0 += T) {
-        const long long t = t0 + threadIdx.x;
-        if (t >= n) break;
-        const long long id = __ldg(tube + t);
-        int i, j, k;
-        lsr_dev::unflatten(P, id, i, j, k);
-        const bool has[6] = {i > 0, i + 1 < P.nx, j > 0, j + 1 < P.ny, P.dim == 3 && k > 0, P.dim == 3 && k + 1 < P.nz};
-        const long long st[3] = {1, P.nx, P.nxy};
-        double v[6];
+    constexpr int kB = 2;  // entries per thread and round, their 7 loads each in flight together
+    const long long T = static_cast<long long>(gridDim.x) * blockDim.x * kB;
+    const long long st[3] = {1, P.nx, P.nxy};
+    for (long long t0 = static_cast<long long>(blockIdx.x) * blockDim.x * kB; t0 < n; t0 += T) {
+        long long id[kB];
 #pragma unroll
-        for (int q = 0; q < 6; ++q) v[q] = __ldg(prev + (has[q] ? id + ((q & 1) ? st[q >> 1] : -st[q >> 1]) : id));
-        const double pj = __ldg(prev + id);
-        double val;
-        bool z = false, f = false;
-        one_node(P, pj, v, has, val, z, f);
-        out[id] = val;
-        if (f) frozen[id] = 1;  // the flags are all clear on entry (lsr_loop_sync_fields clears them)
-        zero |= z;
-        froz |= f;
+        for (int u = 0; u < kB; ++u) {
+            const long long t = t0 + u * blockDim.x + threadIdx.x;
+            id[u] = t < n ? __ldg(tube + t) : -1;
+        }
+        bool has[kB][6];
+        double v[kB][6], pj[kB];
+#pragma unroll
+        for (int u = 0; u < kB; ++u) {
+            if (id[u] < 0) continue;
+            int i, j, k;
+            lsr_dev::unflatten(P, id[u], i, j, k);
+            has[u][0] = i > 0, has[u][1] = i + 1 < P.nx, has[u][2] = j > 0, has[u][3] = j + 1 < P.ny;
+            has[u][4] = P.dim == 3 && k > 0, has[u][5] = P.dim == 3 && k + 1 < P.nz;
+#pragma unroll
+            for (int q = 0; q < 6; ++q)
+                v[u][q] = __ldg(prev + (has[u][q] ? id[u] + ((q & 1) ? st[q >> 1] : -st[q >> 1]) : id[u]));
+            pj[u] = __ldg(prev + id[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < kB; ++u) {
+            if (id[u] < 0) continue;
+            double val;
+            bool z = false, f = false;
+            one_node(P, pj[u], v[u], has[u], val, z, f);
+            out[id[u]] = val;
+            if (f) frozen[id[u]] = 1;  // the flags are all clear on entry (lsr_loop_sync_fields clears them)
+            zero |= z;
+            froz |= f;
+        }
     }
     const unsigned zb = __ballot_sync(0xffffffffu, zero), fb = __ballot_sync(0xffffffffu, froz);
     if ((threadIdx.x & 31) == 0) {
@@ -461,17 +561,33 @@ __global__ void sign_kernel(SlParams P, const double* __restrict__ phi, const lo
                             long long nn, double eps2, double* __restrict__ sgn, unsigned char* __restrict__ nbr,
                             unsigned* __restrict__ nodes32, const long long* __restrict__ nn_dev = nullptr) {
     const long long n_ = nn_dev != nullptr ? __ldg(nn_dev) : nn;
-    const long long step_ = nn_dev != nullptr ? static_cast<long long>(gridDim.x) * blockDim.x : n_;
-    for (long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; t < n_; t += step_) {
-    const long long id = nodes[t];
-    if (nodes32) nodes32[t] = static_cast<unsigned>(id);  // 4-byte ids for the sweeps when the grid allows
-    const double v = __ldg(phi + id);
-    sgn[t] = v / sqrt(v * v + eps2);
-    int i, j, k;
-    lsr_dev::unflatten(P, id, i, j, k);
-    unsigned m = (i > 0 ? 1u : 0u) | (i < P.nx - 1 ? 2u : 0u) | (j > 0 ? 4u : 0u) | (j < P.ny - 1 ? 8u : 0u);
-    if (P.dim == 3) m |= (k > 0 ? 16u : 0u) | (k < P.nz - 1 ? 32u : 0u);
-    nbr[t] = static_cast<unsigned char>(m);
+    // host count: one entry per thread; device count: the grid strides, a
+    // thread taking kTubeBatch entries per round with their loads in flight together
+    const int nb = nn_dev != nullptr ? kTubeBatch : 1;
+    const long long step_ = nn_dev != nullptr ? static_cast<long long>(gridDim.x) * blockDim.x * nb : n_;
+    for (long long t0 = static_cast<long long>(blockIdx.x) * blockDim.x * nb; t0 < n_; t0 += step_) {
+        long long id[kTubeBatch];
+        double v[kTubeBatch];
+#pragma unroll
+        for (int u = 0; u < kTubeBatch; ++u) {
+            const long long t = t0 + u * blockDim.x + threadIdx.x;
+            id[u] = (u < nb && t < n_) ? nodes[t] : -1;
+        }
+#pragma unroll
+        for (int u = 0; u < kTubeBatch; ++u) v[u] = id[u] >= 0 ? __ldg(phi + id[u]) : 0.0;
+#pragma unroll
+        for (int u = 0; u < kTubeBatch; ++u) {
+            if (id[u] < 0) continue;
+            const long long t = t0 + u * blockDim.x + threadIdx.x;
+            if (nodes32) nodes32[t] = static_cast<unsigned>(id[u]);  // 4-byte ids for the sweeps when the grid allows
+            sgn[t] = v[u] / sqrt(v[u] * v[u] + eps2);
+            int i, j, k;
+            lsr_dev::unflatten(P, id[u], i, j, k);
+            unsigned m = (i > 0 ? 1u : 0u) | (i < P.nx - 1 ? 2u : 0u) | (j > 0 ? 4u : 0u) | (j < P.ny - 1 ? 8u : 0u);
+            if (P.dim == 3) m |= (k > 0 ? 16u : 0u) | (k < P.nz - 1 ? 32u : 0u);
+            nbr[t] = static_cast<unsigned char>(m);
+        }
+        if (nn_dev == nullptr) break;
     }
 }
 
@@ -654,7 +770,7 @@ template <class IdT>
 __global__ void __launch_bounds__(kPipeThreads, LSR_JAC_PIPE_MINB)
     jacobi_pipe(SlParams P, const double* __restrict__ cur, double* __restrict__ nxt, const IdT* __restrict__ nodes,
                 const double* __restrict__ sgn, const unsigned char* __restrict__ nbr, long long nn, double dtau,
-                IterState* __restrict__ st, const long long* __restrict__ nn_dev) {
+                IterState* __restrict__ st, const long long* __restrict__ nn_dev, double tol, int rule) {
     if (nn_dev != nullptr) nn = __ldg(nn_dev);  // the device loop's node count
     const long long T = static_cast<long long>(gridDim.x) * blockDim.x;
     const long long g = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -735,43 +851,66 @@ __global__ void __launch_bounds__(kPipeThreads, LSR_JAC_PIPE_MINB)
 #pragma unroll
         for (int w = 0; w < kPipeThreads / 32; ++w) m = wmax[w] > m ? wmax[w] : m;
         if (m) atomicMax(&st->residual_bits, m);
+        if (rule) {
+            // the stop rule, applied by the last CTA to arrive (rule == 0: the
+            // caller reads the residual itself, e.g. a z-slab's rank)
+            __threadfence();
+            if (atomicAdd(&st->arrived, 1u) == gridDim.x - 1) {
+                __threadfence();
+                const unsigned long long rb = atomicExch(&st->residual_bits, 0ULL);
+                st->arrived = 0;
+                stop_rule(st, rb, tol);
+            }
+        }
     }
 }
 
+// the stop rule after a sweep as its own launch (sweeps without the fused rule)
+__global__ void iter_check(IterState* st, double tol) {
+    if (st->done) return;
+    const unsigned long long rb = st->residual_bits;
+    st->residual_bits = 0;
+    stop_rule(st, rb, tol);
+}
+
 // one sweep cur -> nxt over the node list (W.nodes32 when the ids fit 4 bytes)
+// (tol != nullptr: the sweep also applies the stop rule with *tol — one
+// launch per sweep; nullptr: the residual is left in st for the caller)
 template <class IdT>
 static void launch_jacobi(const SlParams& P, const double* cur, double* nxt, const IdT* ids, const ReinitBuffers& W,
                           long long nn, double dtau, IterState* st, cudaStream_t s,
-                          const long long* nn_dev = nullptr) {
+                          const long long* nn_dev = nullptr, const double* tol = nullptr) {
+    const double tolv = tol ? *tol : 0.0;
+    const int rule = tol ? 1 : 0;
     if (nn_dev != nullptr) {  // device count: the persistent sweep on every resident CTA
         jacobi_pipe<<<148u * LSR_JAC_PIPE_MINB, kPipeThreads, 0, s>>>(P, cur, nxt, ids, W.sgn, W.nbr, 0, dtau, st,
-                                                                      nn_dev);
+                                                                      nn_dev, tolv, rule);
         lsr_note_launch();
         return;
     }
-    if (nn <= 0) return;
+    if (nn <= 0 || !LSR_JAC_PIPE) {  // no sweep kernel, or the one without the fused rule
+        if (nn > 0) {
+            const unsigned g = static_cast<unsigned>((nn + kJacThreads * kJacNPT - 1) / (kJacThreads * kJacNPT));
+            jacobi<<<g, kJacThreads, 0, s>>>(P, cur, nxt, ids, W.sgn, W.nbr, nn, dtau, st);
+            lsr_note_launch();
+        }
+        if (rule) {
+            iter_check<<<1, 1, 0, s>>>(st, tolv);
+            lsr_note_launch();
+        }
+        return;
+    }
     if (LSR_JAC_PIPE) {
         // persistent: the resident CTAs (148 SMs x LSR_JAC_PIPE_MINB), or fewer for short lists
         const long long want = (nn + kPipeThreads * kPipeNPT - 1) / (kPipeThreads * kPipeNPT);
         const long long cap = 148LL * LSR_JAC_PIPE_MINB;
         jacobi_pipe<<<static_cast<unsigned>(want < cap ? want : cap), kPipeThreads, 0, s>>>(P, cur, nxt, ids, W.sgn,
                                                                                             W.nbr, nn, dtau, st,
-                                                                                            nullptr);
-    } else {
-        const unsigned g = static_cast<unsigned>((nn + kJacThreads * kJacNPT - 1) / (kJacThreads * kJacNPT));
-        jacobi<<<g, kJacThreads, 0, s>>>(P, cur, nxt, ids, W.sgn, W.nbr, nn, dtau, st);
+                                                                                            nullptr, tolv, rule);
     }
     lsr_note_launch();
 }
 
-// the stop rule after a sweep (reinit.cpp:275-278)
-__global__ void iter_check(IterState* st, double tol) {
-    if (st->done) return;
-    st->iterations += 1;
-    const double residual = __longlong_as_double(static_cast<long long>(st->residual_bits));
-    st->residual_bits = 0;
-    if (residual < tol) st->done = 1;
-}
 
 // clamp_field on a node list (the sparse form of the loop's clamp, see
 // lsr_reinitialize): same per-node expression as clamp_kernel
@@ -805,8 +944,11 @@ __global__ void copy_ids_dev(const double* __restrict__ src, double* __restrict_
     }
 }
 
+// (only_if: nothing is done when *only_if == 0 — the loop's fused tail runs instead)
 __global__ void clamp_ids_dev(double* __restrict__ f, const long long* __restrict__ ids,
-                              const long long* __restrict__ n_dev, double gamma) {
+                              const long long* __restrict__ n_dev, double gamma,
+                              const int* __restrict__ only_if = nullptr) {
+    if (only_if != nullptr && *only_if == 0) return;
     const long long n = __ldg(n_dev);
     for (long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; t < n;
          t += static_cast<long long>(gridDim.x) * blockDim.x) {
@@ -827,7 +969,9 @@ __global__ void reinit_begin(IterState* st, const int* __restrict__ flags) {
 // it over the node list into the other buffer, so that b holds the result
 // and the two agree on the list
 __global__ void sweep_parity(double* __restrict__ b, double* __restrict__ c, const long long* __restrict__ ids,
-                             const long long* __restrict__ n_dev, const IterState* __restrict__ st) {
+                             const long long* __restrict__ n_dev, const IterState* __restrict__ st,
+                             const int* __restrict__ only_if = nullptr) {
+    if (only_if != nullptr && *only_if == 0) return;
     const long long n = __ldg(n_dev);
     const bool odd = (st->iterations & 1) != 0;
     const double* src = odd ? c : b;
@@ -845,7 +989,9 @@ __global__ void sweep_parity(double* __restrict__ b, double* __restrict__ c, con
 // that is not ACTIVE either (a hard jump, see OneStepGate) raises *hard
 __global__ void loop_finish(SlParams P, const double* __restrict__ b, double* __restrict__ a, double* __restrict__ c,
                             const long long* __restrict__ ids, const long long* __restrict__ n_dev,
-                            unsigned char* __restrict__ frozen, double gamma, int* __restrict__ hard) {
+                            unsigned char* __restrict__ frozen, double gamma, int* __restrict__ hard,
+                            const int* __restrict__ only_if = nullptr) {
+    if (only_if != nullptr && *only_if == 0) return;
     const long long n = __ldg(n_dev);
     bool h = false;
     const long long T = static_cast<long long>(gridDim.x) * blockDim.x;
@@ -866,6 +1012,63 @@ __global__ void loop_finish(SlParams P, const double* __restrict__ b, double* __
 #pragma unroll
             for (int q = 0; q < 6; ++q)
                 if (has[q] && hard_pair(v, b[id + ((q & 1) ? st[q >> 1] : -st[q >> 1])], gamma)) h = true;
+        }
+    }
+    if (__any_sync(0xffffffffu, h) && (threadIdx.x & 31) == 0) *hard = 1;
+}
+
+// The tail of a device-loop iteration in one pass over the tube, for
+// iterations that ran the tube one-step (*dense == 0: the frozen nodes lie in
+// the tube) and the sparse clamp: sweep_parity, clamp_ids_dev on the tube and
+// the frozen ids, and both loop_finish launches. The sweeps' result R is b
+// (even count) or c (odd); off the sweep list b and c agree (frozen nodes:
+// copy_ids_dev; off the tube: the loop's invariant a = b = c). Per tube node:
+// v = clamp(R) goes to b, a and c, the frozen flag is cleared, and a node
+// that is not ACTIVE is checked for hard jumps against its neighbours' final
+// values clamp(R[nbr]) — the clamp is idempotent, so it does not matter
+// whether a neighbour's entry of R has been rewritten by its own thread yet.
+__global__ void loop_tail(SlParams P, double* __restrict__ b, double* __restrict__ a, double* __restrict__ c,
+                          const long long* __restrict__ tube, const long long* __restrict__ n_dev,
+                          unsigned char* __restrict__ frozen, const IterState* __restrict__ st, double gamma,
+                          int* __restrict__ hard, const int* __restrict__ dense) {
+    if (*dense != 0) return;
+    const long long n = __ldg(n_dev);
+    const double* R = (st->iterations & 1) ? c : b;
+    bool h = false;
+    // kTubeBatch entries per thread and round, their loads issued together
+    // (one entry per round left the pass waiting on two dependent loads)
+    const long long T = static_cast<long long>(gridDim.x) * blockDim.x * kTubeBatch;
+    for (long long t0 = static_cast<long long>(blockIdx.x) * blockDim.x * kTubeBatch; t0 < n; t0 += T) {
+        long long id[kTubeBatch];
+        double r[kTubeBatch];
+#pragma unroll
+        for (int u = 0; u < kTubeBatch; ++u) {
+            const long long t = t0 + u * blockDim.x + threadIdx.x;
+            id[u] = t < n ? tube[t] : -1;
+        }
+#pragma unroll
+        for (int u = 0; u < kTubeBatch; ++u) r[u] = id[u] >= 0 ? R[id[u]] : 0.0;
+#pragma unroll
+        for (int u = 0; u < kTubeBatch; ++u) {
+            if (id[u] < 0) continue;
+            const double v = smin(smax(r[u], -gamma), gamma);  // clamp_field (grid.cpp:126-134)
+            b[id[u]] = v;
+            a[id[u]] = v;
+            c[id[u]] = v;
+            frozen[id[u]] = 0;
+            if (!(fabs(v) < gamma)) {
+                int i, j, k;
+                lsr_dev::unflatten(P, id[u], i, j, k);
+                const bool has[6] = {i > 0, i + 1 < P.nx, j > 0, j + 1 < P.ny, P.dim == 3 && k > 0,
+                                     P.dim == 3 && k + 1 < P.nz};
+                const long long sd[3] = {1, P.nx, P.nxy};
+                double w[6];
+#pragma unroll
+                for (int q = 0; q < 6; ++q) w[q] = has[q] ? R[id[u] + ((q & 1) ? sd[q >> 1] : -sd[q >> 1])] : v;
+#pragma unroll
+                for (int q = 0; q < 6; ++q)
+                    if (has[q] && hard_pair(v, smin(smax(w[q], -gamma), gamma), gamma)) h = true;
+            }
         }
     }
     if (__any_sync(0xffffffffu, h) && (threadIdx.x & 31) == 0) *hard = 1;
@@ -931,19 +1134,25 @@ static int ensure_tmp(BandBuffers& B, size_t bytes, std::string* err) {
 // z-slab passes its owned ids as [b0, b1) and one plane more on each side as
 // [a0, a1) (the z pass reads the y-dilated planes next to its own).
 static void band_passes(const SlParams& P, const double* phi, double gamma, long long a0, long long a1, long long b0,
-                        long long b1, unsigned char* t, unsigned char* u, unsigned char* state, cudaStream_t s) {
+                        long long b1, unsigned char* t, unsigned char* u, unsigned char* state, cudaStream_t s,
+                        const int* skip_if_clear = nullptr, long long* c1 = nullptr, long long* c2 = nullptr) {
     const auto grid = [](long long items) { return static_cast<unsigned>((items + 255) / 256); };
     if (P.nx % 16 == 0) {  // rows of whole 16-byte vectors
-        band_pass_x4<<<grid((a1 - a0) / 4), 256, 0, s>>>(P, phi, gamma, a0 / 4, a1 / 4, reinterpret_cast<unsigned*>(t));
+        if (skip_if_clear != nullptr && a0 == 0)
+            band_pass_x16<<<grid(a1 / 16), 256, 0, s>>>(P, phi, gamma, a1 / 16, reinterpret_cast<uint4*>(t), state,
+                                                       skip_if_clear);
+        else
+            band_pass_x4<<<grid((a1 - a0) / 4), 256, 0, s>>>(P, phi, gamma, a0 / 4, a1 / 4,
+                                                             reinterpret_cast<unsigned*>(t));
         const uint4* t16 = reinterpret_cast<const uint4*>(t);
         const uint4* u16c = reinterpret_cast<const uint4*>(u);
         uint4* u16 = reinterpret_cast<uint4*>(u);
         uint4* st16 = reinterpret_cast<uint4*>(state);
         if (P.dim == 3) {
             band_pass_yz16<<<grid((a1 - a0) / 16), 256, 0, s>>>(P, 1, t16, a0 / 16, a1 / 16, u16, st16);
-            band_pass_yz16<<<grid((b1 - b0) / 16), 256, 0, s>>>(P, 2, u16c, b0 / 16, b1 / 16, nullptr, st16);
+            band_pass_yz16<<<grid((b1 - b0) / 16), 256, 0, s>>>(P, 2, u16c, b0 / 16, b1 / 16, nullptr, st16, c1, c2);
         } else {
-            band_pass_yz16<<<grid((b1 - b0) / 16), 256, 0, s>>>(P, 1, t16, b0 / 16, b1 / 16, u16, st16);
+            band_pass_yz16<<<grid((b1 - b0) / 16), 256, 0, s>>>(P, 1, t16, b0 / 16, b1 / 16, u16, st16, c1, c2);
         }
     } else {
         band_pass_x<<<grid(a1 - a0), 256, 0, s>>>(P, phi, gamma, a0, a1, t);
@@ -1146,10 +1355,8 @@ int lsr_reinit_iterate(const SlParams& P, double** phi, double** scratch, const 
     BR_TRY(cudaMemsetAsync(st, 0, sizeof(IterState), s));
     double* buf[2] = {*phi, *scratch};
     for (int k = 0; k < R.max_iters; ++k) {
-        if (n <= 0xffffffffLL) launch_jacobi(P, buf[k & 1], buf[(k + 1) & 1], W.nodes32, W, nn, R.dtau, st, s);
-        else launch_jacobi(P, buf[k & 1], buf[(k + 1) & 1], W.nodes, W, nn, R.dtau, st, s);
-        iter_check<<<1, 1, 0, s>>>(st, tol);
-        lsr_note_launch();
+        if (n <= 0xffffffffLL) launch_jacobi(P, buf[k & 1], buf[(k + 1) & 1], W.nodes32, W, nn, R.dtau, st, s, nullptr, &tol);
+        else launch_jacobi(P, buf[k & 1], buf[(k + 1) & 1], W.nodes, W, nn, R.dtau, st, s, nullptr, &tol);
     }
     BR_TRY(cudaGetLastError());
     IterState h{};
@@ -1348,17 +1555,24 @@ int lsr_reinit_slab_sweep(const SlParams& P, const double* cur_g, double* nxt_g,
 // narrow_band (grid.cpp:76-123): the dilation passes and the fused two-list
 // compaction; the counts stay in B.counts ([0] ACTIVE, [1] tube)
 int lsr_band_enqueue(const SlParams& P, const double* phi, double gamma, BandBuffers& B, cudaStream_t s,
-                     std::string* err) {
+                     std::string* err, const int* hard) {
     const long long n = P.nxy * P.nz;
     if (int st = B.reserve(n, err)) return st;
     const size_t tb = lsr_compact::scratch_bytes2(n);
     if (int st = ensure_tmp(B, tb, err)) return st;
     unsigned char* t = reinterpret_cast<unsigned char*>(B.active);
     unsigned char* u = reinterpret_cast<unsigned char*>(B.tube);
-    band_passes(P, phi, gamma, 0, n, 0, n, t, u, B.state, s);
+    // hard (the loop's hard[0], see OneStepGate): clear when phi differs from the
+    // previous iteration's phi only on that iteration's tube, whose state
+    // bytes B.state still holds — the x pass then skips quads off that tube
+    // rows of whole 16-node groups: the final pass also counts per compaction tile
+    const bool counted = P.nx % 16 == 0;
+    long long *c1 = nullptr, *c2 = nullptr;
+    if (counted) lsr_compact::compact2_counts(B.tmp, n, &c1, &c2);
+    band_passes(P, phi, gamma, 0, n, 0, n, t, u, B.state, s, hard, c1, c2);
     BR_TRY(lsr_compact::compact2(lsr_compact::BytePred<StateIs1>{B.state, {}}, NonZero{}, lsr_compact::Identity{}, n,
-                                 B.active, B.tube, B.counts, B.tmp, tb, s));
-    for (int q = 0; q < 2; ++q) lsr_note_launch();
+                                 B.active, B.tube, B.counts, B.tmp, tb, s, counted));
+    for (int q = 0; q < (counted ? 1 : 2); ++q) lsr_note_launch();
     return LSR_OK;
 }
 
@@ -1435,17 +1649,18 @@ int lsr_reinit_enqueue(const SlParams& P, double* b, double* c, const BandBuffer
     const double tol = R.residual_tol * P.dx;
     double* buf[2] = {b, c};
     for (int k = 0; k < R.max_iters; ++k) {
-        if (small) launch_jacobi(P, buf[k & 1], buf[(k + 1) & 1], W.nodes32, W, 0, R.dtau, st, s, L->counts + 1);
-        else launch_jacobi(P, buf[k & 1], buf[(k + 1) & 1], W.nodes, W, 0, R.dtau, st, s, L->counts + 1);
-        iter_check<<<1, 1, 0, s>>>(st, tol);
-        lsr_note_launch();
+        if (small) launch_jacobi(P, buf[k & 1], buf[(k + 1) & 1], W.nodes32, W, 0, R.dtau, st, s, L->counts + 1, &tol);
+        else launch_jacobi(P, buf[k & 1], buf[(k + 1) & 1], W.nodes, W, 0, R.dtau, st, s, L->counts + 1, &tol);
     }
-    sweep_parity<<<kDevGrid, 256, 0, s>>>(b, c, W.nodes, L->counts + 1, st);
+    // the sweeps' result into b, then clamp_field (reinit.cpp:144). With the
+    // sparse clamp and the tube one-step (hard[0] clear) both are left to
+    // loop_tail (lsr_loop_sync_fields), which does them in its one pass
+    const int* tail_off = clamp_sparse ? hard : nullptr;
+    sweep_parity<<<kDevGrid, 256, 0, s>>>(b, c, W.nodes, L->counts + 1, st, tail_off);
     lsr_note_launch();
-    // clamp_field (reinit.cpp:144)
     if (clamp_sparse) {
-        clamp_ids_dev<<<kDevGrid, 256, 0, s>>>(b, B.tube, B.counts + 1, gamma);
-        clamp_ids_dev<<<kDevGrid, 256, 0, s>>>(b, W.frozen_ids, L->counts, gamma);
+        clamp_ids_dev<<<kDevGrid, 256, 0, s>>>(b, B.tube, B.counts + 1, gamma, tail_off);
+        clamp_ids_dev<<<kDevGrid, 256, 0, s>>>(b, W.frozen_ids, L->counts, gamma, tail_off);
         for (int q = 0; q < 2; ++q) lsr_note_launch();
     } else if (int e = lsr_clamp(b, n, gamma, s, err, B.state, &L->clamp_outside)) {
         return e;
@@ -1463,12 +1678,18 @@ int lsr_reinit_enqueue(const SlParams& P, double* b, double* c, const BandBuffer
 // pairs with both nodes off them kept the values (and signs, and
 // non-ACTIVE-ness: the clamp preserves both) they had in phi^n, which the
 // previous check (or the dense one-step) cleared
-int lsr_loop_sync_fields(const SlParams& P, const double* b, double* a, double* c, const BandBuffers& B,
-                         ReinitBuffers& W, const ReinitLoopDev* L, double gamma, int* hard, cudaStream_t s,
-                         std::string* err) {
+int lsr_loop_sync_fields(const SlParams& P, double* b, double* a, double* c, const BandBuffers& B,
+                         ReinitBuffers& W, const ReinitLoopDev* L, double gamma, int* hard, bool clamp_sparse,
+                         cudaStream_t s, std::string* err) {
     const long long n = P.nxy * P.nz;
-    loop_finish<<<kDevGrid, 256, 0, s>>>(P, b, a, c, B.tube, B.counts + 1, nullptr, gamma, hard + 1);
-    loop_finish<<<kDevGrid, 256, 0, s>>>(P, b, a, c, W.frozen_ids, L->counts, W.frozen, gamma, hard + 1);
+    const int* tail_off = clamp_sparse ? hard : nullptr;  // as in lsr_reinit_enqueue
+    if (clamp_sparse) {
+        const IterState* st = reinterpret_cast<const IterState*>(&L->residual_bits);
+        loop_tail<<<kDevGrid, 256, 0, s>>>(P, b, a, c, B.tube, B.counts + 1, W.frozen, st, gamma, hard + 1, hard);
+        lsr_note_launch();
+    }
+    loop_finish<<<kDevGrid, 256, 0, s>>>(P, b, a, c, B.tube, B.counts + 1, nullptr, gamma, hard + 1, tail_off);
+    loop_finish<<<kDevGrid, 256, 0, s>>>(P, b, a, c, W.frozen_ids, L->counts, W.frozen, gamma, hard + 1, tail_off);
     copy_all_if<<<kDevGrid, 256, 0, s>>>(b, a, n, &L->clamp_outside);
     copy_all_if<<<kDevGrid, 256, 0, s>>>(b, c, n, &L->clamp_outside);
     for (int q = 0; q < 4; ++q) lsr_note_launch();

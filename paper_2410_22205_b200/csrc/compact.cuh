@@ -110,6 +110,23 @@ struct Identity {
     __device__ long long operator()(long long i) const { return i; }
 };
 
+// A tile's selected items, ranked, go to shared memory and from there to
+// out[0 .. total) with consecutive threads storing consecutive entries (the
+// per-thread runs written straight to global memory made 8-byte stores at 16
+// scattered addresses per warp instruction). All threads of the CTA call it.
+template <class Item, class Out>
+__device__ __forceinline__ void staged_write(Out* __restrict__ stage, Out* __restrict__ out, int total, int rank,
+                                             unsigned mask, long long base, Item item) {
+    while (mask) {
+        const int q = __ffs(mask) - 1;
+        mask &= mask - 1;
+        stage[rank++] = item(base + q);
+    }
+    __syncthreads();
+    for (int x = threadIdx.x; x < total; x += kThreads) out[x] = stage[x];
+    __syncthreads();
+}
+
 // scratch bytes compact() needs for n items
 inline size_t scratch_bytes(long long n) {
     const long long tiles = (n + kTile - 1) / kTile;
@@ -190,6 +207,7 @@ __global__ void __launch_bounds__(kThreads) write_tiles_bytes2(BytePred<T1> p1, 
                                                                const long long* __restrict__ o1,
                                                                const long long* __restrict__ o2, Out* __restrict__ out1,
                                                                Out* __restrict__ out2) {
+    if (o1[blockIdx.x + 1] == o1[blockIdx.x] && o2[blockIdx.x + 1] == o2[blockIdx.x]) return;  // nothing selected
     const long long base = static_cast<long long>(blockIdx.x) * kTile + static_cast<long long>(threadIdx.x) * kItems;
     BytePred<T2> p2{p1.a, test2};
     unsigned m1 = base < n ? p1.mask16(base, n) : 0u, m2 = base < n ? p2.mask16(base, n) : 0u;
@@ -199,25 +217,24 @@ __global__ void __launch_bounds__(kThreads) write_tiles_bytes2(BytePred<T1> p1, 
     Scan(tmp).ExclusiveSum(__popc(m1), r1);
     __syncthreads();
     Scan(tmp).ExclusiveSum(__popc(m2), r2);
-    Out* a = out1 + o1[blockIdx.x] + r1;
-    while (m1) {
-        const int q = __ffs(m1) - 1;
-        m1 &= m1 - 1;
-        *a++ = item(base + q);
-    }
-    Out* b = out2 + o2[blockIdx.x] + r2;
-    while (m2) {
-        const int q = __ffs(m2) - 1;
-        m2 &= m2 - 1;
-        *b++ = item(base + q);
-    }
+    __shared__ Out stage[kTile];
+    staged_write(stage, out1 + o1[blockIdx.x], static_cast<int>(o1[blockIdx.x + 1] - o1[blockIdx.x]), r1, m1, base, item);
+    staged_write(stage, out2 + o2[blockIdx.x], static_cast<int>(o2[blockIdx.x + 1] - o2[blockIdx.x]), r2, m2, base, item);
 }
 
 inline size_t scratch_bytes2(long long n) { return 2 * scratch_bytes(n); }
 
+// where compact2 keeps its per-tile counts (a producer of the bytes may fill
+// them itself and pass counted = true)
+inline void compact2_counts(void* scratch, long long n, long long** c1, long long** c2) {
+    const long long tiles = (n + kTile - 1) / kTile;
+    *c1 = static_cast<long long*>(scratch);
+    *c2 = *c1 + 2 * (tiles + 1);
+}
+
 template <class T1, class T2, class Item, class Out>
 cudaError_t compact2(BytePred<T1> p1, T2 test2, Item item, long long n, Out* out1, Out* out2, long long* d_count2,
-                     void* scratch, size_t scratch_size, cudaStream_t s) {
+                     void* scratch, size_t scratch_size, cudaStream_t s, bool counted = false) {
     if (n <= 0) return cudaMemsetAsync(d_count2, 0, 2 * sizeof(long long), s);
     const long long tiles = (n + kTile - 1) / kTile;
     long long* c1 = static_cast<long long*>(scratch);
@@ -229,7 +246,7 @@ cudaError_t compact2(BytePred<T1> p1, T2 test2, Item item, long long n, Out* out
     cudaError_t e = cudaMemsetAsync(c1 + tiles, 0, sizeof(long long), s);
     if (e == cudaSuccess) e = cudaMemsetAsync(c2 + tiles, 0, sizeof(long long), s);
     if (e != cudaSuccess) return e;
-    count_tiles_bytes2<<<static_cast<unsigned>(tiles), kThreads, 0, s>>>(p1, test2, n, c1, c2);
+    if (!counted) count_tiles_bytes2<<<static_cast<unsigned>(tiles), kThreads, 0, s>>>(p1, test2, n, c1, c2);
     e = cub::DeviceScan::ExclusiveSum(scan_tmp, scan_bytes, c1, off1, static_cast<int>(tiles + 1), s);
     if (e == cudaSuccess) e = cub::DeviceScan::ExclusiveSum(scan_tmp, scan_bytes, c2, off2, static_cast<int>(tiles + 1), s);
     if (e != cudaSuccess) return e;
@@ -287,6 +304,7 @@ __global__ void __launch_bounds__(kThreads) write_tiles_m2(M1 p1, M2 p2, Item it
                                                            const long long* __restrict__ o1,
                                                            const long long* __restrict__ o2, Out* __restrict__ out1,
                                                            Out* __restrict__ out2) {
+    if (o1[blockIdx.x + 1] == o1[blockIdx.x] && o2[blockIdx.x + 1] == o2[blockIdx.x]) return;  // nothing selected
     const long long base = static_cast<long long>(blockIdx.x) * kTile + static_cast<long long>(threadIdx.x) * kItems;
     unsigned m1 = base < n ? p1.mask16(base, n) : 0u, m2 = base < n ? p2.mask16(base, n) : 0u;
     using Scan = cub::BlockScan<int, kThreads>;
@@ -295,18 +313,9 @@ __global__ void __launch_bounds__(kThreads) write_tiles_m2(M1 p1, M2 p2, Item it
     Scan(tmp).ExclusiveSum(__popc(m1), r1);
     __syncthreads();
     Scan(tmp).ExclusiveSum(__popc(m2), r2);
-    Out* a = out1 + o1[blockIdx.x] + r1;
-    while (m1) {
-        const int q = __ffs(m1) - 1;
-        m1 &= m1 - 1;
-        *a++ = item(base + q);
-    }
-    Out* b = out2 + o2[blockIdx.x] + r2;
-    while (m2) {
-        const int q = __ffs(m2) - 1;
-        m2 &= m2 - 1;
-        *b++ = item(base + q);
-    }
+    __shared__ Out stage[kTile];
+    staged_write(stage, out1 + o1[blockIdx.x], static_cast<int>(o1[blockIdx.x + 1] - o1[blockIdx.x]), r1, m1, base, item);
+    staged_write(stage, out2 + o2[blockIdx.x], static_cast<int>(o2[blockIdx.x + 1] - o2[blockIdx.x]), r2, m2, base, item);
 }
 
 template <class M1, class M2, class Item, class Out>
@@ -330,6 +339,83 @@ cudaError_t compact2m(M1 p1, M2 p2, Item item, long long n, Out* out1, Out* out2
     write_tiles_m2<<<static_cast<unsigned>(tiles), kThreads, 0, s>>>(p1, p2, item, n, off1, off2, out1, out2);
     e = cudaMemcpyAsync(d_count2, off1 + tiles, sizeof(long long), cudaMemcpyDeviceToDevice, s);
     if (e == cudaSuccess) e = cudaMemcpyAsync(d_count2 + 1, off2 + tiles, sizeof(long long), cudaMemcpyDeviceToDevice, s);
+    if (e != cudaSuccess) return e;
+    return cudaGetLastError();
+}
+
+// compact() over one mask provider (anything with mask16(base, n), e.g. a
+// GatedBytes): the same three passes; tiles the provider reports empty cost
+// one predicate evaluation
+template <class M>
+__global__ void __launch_bounds__(kThreads) count_tiles_m(M p, long long n, long long* __restrict__ counts) {
+    const long long base = static_cast<long long>(blockIdx.x) * kTile + static_cast<long long>(threadIdx.x) * kItems;
+    const int c = base < n ? __popc(p.mask16(base, n)) : 0;
+    using Reduce = cub::BlockReduce<int, kThreads>;
+    __shared__ typename Reduce::TempStorage tmp;
+    const int total = Reduce(tmp).Sum(c);
+    if (threadIdx.x == 0) counts[blockIdx.x] = total;
+}
+
+template <class M, class Item, class Out>
+__global__ void __launch_bounds__(kThreads) write_tiles_m(M p, Item item, long long n,
+                                                          const long long* __restrict__ offsets,
+                                                          Out* __restrict__ out) {
+    if (offsets[blockIdx.x + 1] == offsets[blockIdx.x]) return;  // nothing selected in this tile
+    const long long base = static_cast<long long>(blockIdx.x) * kTile + static_cast<long long>(threadIdx.x) * kItems;
+    unsigned mask = base < n ? p.mask16(base, n) : 0u;
+    using Scan = cub::BlockScan<int, kThreads>;
+    __shared__ typename Scan::TempStorage tmp;
+    int rank;
+    Scan(tmp).ExclusiveSum(__popc(mask), rank);
+    __shared__ Out stage[kTile];
+    staged_write(stage, out + offsets[blockIdx.x], static_cast<int>(offsets[blockIdx.x + 1] - offsets[blockIdx.x]), rank,
+                 mask, base, item);
+}
+
+// flag bytes a[0 .. min(n, *n_dev)) (n_dev null: a[0 .. n)), selected where
+// nonzero — but nothing at all unless (*gate != 0) == open (gate null: always
+// open). Lets two alternative selections be enqueued back to back into one
+// output, the device deciding which of them runs.
+struct GatedBytes {
+    const unsigned char* a;
+    const long long* n_dev;
+    const int* gate;
+    int open;
+    __device__ __forceinline__ unsigned mask16(long long base, long long n) const {
+        if (gate != nullptr && (*gate != 0) != (open != 0)) return 0u;
+        if (n_dev != nullptr) {
+            const long long nd = *n_dev;
+            n = nd < n ? nd : n;
+        }
+        unsigned m = 0;
+        if (base + kItems <= n) {
+            const uint4 v = *reinterpret_cast<const uint4*>(a + base);
+            const unsigned w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int q = 0; q < kItems; ++q) m |= (((w[q >> 2] >> (8 * (q & 3))) & 0xffu) != 0 ? 1u : 0u) << q;
+        } else {
+            for (int q = 0; q < kItems && base + q < n; ++q) m |= (a[base + q] != 0 ? 1u : 0u) << q;
+        }
+        return m;
+    }
+};
+
+template <class M, class Item, class Out>
+cudaError_t compact_m(M p, Item item, long long n, Out* out, long long* d_count, void* scratch, size_t scratch_size,
+                      cudaStream_t s) {
+    if (n <= 0) return cudaMemsetAsync(d_count, 0, sizeof(long long), s);
+    const long long tiles = (n + kTile - 1) / kTile;
+    long long* counts = static_cast<long long*>(scratch);
+    long long* offsets = counts + (tiles + 1);
+    void* scan_tmp = offsets + (tiles + 1);
+    size_t scan_bytes = scratch_size - 2 * (tiles + 1) * sizeof(long long);
+    cudaError_t e = cudaMemsetAsync(counts + tiles, 0, sizeof(long long), s);
+    if (e != cudaSuccess) return e;
+    count_tiles_m<<<static_cast<unsigned>(tiles), kThreads, 0, s>>>(p, n, counts);
+    e = cub::DeviceScan::ExclusiveSum(scan_tmp, scan_bytes, counts, offsets, static_cast<int>(tiles + 1), s);
+    if (e != cudaSuccess) return e;
+    write_tiles_m<<<static_cast<unsigned>(tiles), kThreads, 0, s>>>(p, item, n, offsets, out);
+    e = cudaMemcpyAsync(d_count, offsets + tiles, sizeof(long long), cudaMemcpyDeviceToDevice, s);
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }

@@ -46,8 +46,10 @@ __device__ __forceinline__ double powp(double a, int p) {
 
 // interface_cells' corner test (metrics.cpp:23-31, 40-52)
 // cells [base, end); flags indexed by global cell id
+// (only_if, the device loop: nothing is done when *only_if == 0)
 __global__ void flag_cells(SlParams P, const double* __restrict__ phi, long long base, long long end,
-                           unsigned char* __restrict__ flags) {
+                           unsigned char* __restrict__ flags, const int* __restrict__ only_if = nullptr) {
+    if (only_if != nullptr && *only_if == 0) return;
     const long long c = base + static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (c >= end) return;
     const unsigned cx = P.nx - 1, cy = P.ny - 1;  // cells < 2^31 (cub's int item count)
@@ -124,7 +126,9 @@ __device__ __forceinline__ void row_classes(const SlParams& P, const double* __r
 
 // cell planes [k_lo, k_hi) (whole grid: 0, nz - 1); flags indexed by global cell id
 __global__ void flag_cells_march(SlParams P, const double* __restrict__ phi, unsigned tpr,
-                                 unsigned char* __restrict__ flags, int k_lo, int k_hi) {
+                                 unsigned char* __restrict__ flags, int k_lo, int k_hi,
+                                 const int* __restrict__ only_if = nullptr) {
+    if (only_if != nullptr && *only_if == 0) return;
     const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
     const int cx = P.nx - 1, cy = P.ny - 1;
     const long long rows = static_cast<long long>(tpr) * cy;  // (x-quad, j) pairs
@@ -155,6 +159,76 @@ __global__ void flag_cells_march(SlParams P, const double* __restrict__ phi, uns
         }
     }
 }
+
+// The interface cells from the band's tube (the device loop, when phi has no
+// hard jump: every axis pair of opposite signs then has an ACTIVE node, see
+// band_reinit.cu OneStepGate). A cell with a zero corner, or with corners of
+// both signs — hence an edge path between them, hence an opposite-sign edge
+// or a zero corner on it — has an ACTIVE corner (|0| < gamma), and its base
+// corner, at most one node below that corner on every axis, is in the tube
+// (the ACTIVE set dilated by one, grid.cpp:98-116). So the tube entries whose
+// node is a cell's base corner cover every interface cell, in ascending cell
+// order (cell ids are monotone in base-node ids). tflags[t] = the corner test
+// (metrics.cpp:23-31, 40-52) of the cell based at tube[t]; runs only when
+// *hard == 0 (else the dense kernels above run).
+__global__ void flag_cells_tube(SlParams P, const double* __restrict__ phi, const long long* __restrict__ tube,
+                                const long long* __restrict__ n_dev, unsigned char* __restrict__ tflags,
+                                const int* __restrict__ hard) {
+    if (*hard != 0) return;
+    const long long n = __ldg(n_dev);
+    constexpr int kB = 2;  // entries per thread and round, their corner loads in flight together
+    const long long T = static_cast<long long>(gridDim.x) * blockDim.x * kB;
+    const int kz = P.dim == 3 ? 1 : 0;
+    for (long long t0 = static_cast<long long>(blockIdx.x) * blockDim.x * kB; t0 < n; t0 += T) {
+        long long id[kB];
+#pragma unroll
+        for (int u = 0; u < kB; ++u) {
+            const long long t = t0 + u * blockDim.x + threadIdx.x;
+            id[u] = t < n ? __ldg(tube + t) : -1;
+        }
+        double v[kB][8];
+        bool cell[kB];
+#pragma unroll
+        for (int u = 0; u < kB; ++u) {
+            cell[u] = false;
+            if (id[u] < 0) continue;
+            int i, j, k;
+            lsr_dev::unflatten(P, id[u], i, j, k);
+            cell[u] = i < P.nx - 1 && j < P.ny - 1 && (P.dim != 3 || k < P.nz - 1);
+            if (!cell[u]) continue;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const int dk = (q >> 2) & kz;  // 2d: the four corners twice
+                v[u][q] = __ldg(phi + id[u] + dk * P.nxy + ((q >> 1) & 1) * P.nx + (q & 1));
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < kB; ++u) {
+            if (id[u] < 0) continue;
+            unsigned m = 0;
+            if (cell[u]) {
+#pragma unroll
+                for (int q = 0; q < 8; ++q) m |= sign_class(v[u][q]);
+            }
+            tflags[t0 + u * blockDim.x + threadIdx.x] = ((m & 4u) || (m & 3u) == 3u) ? 1 : 0;  // zero corner, or both signs
+        }
+    }
+}
+
+struct TubeCellId {  // the cell whose base corner is the node tube[t]
+    const long long* tube;
+    int nx, ny, dim;
+    __device__ int operator()(long long t) const {
+        const long long id = tube[t];
+        const long long row = id / nx;
+        const int i = static_cast<int>(id - row * nx);
+        const long long k = dim == 3 ? row / ny : 0;
+        const int j = static_cast<int>(row - k * ny);
+        return static_cast<int>((k * (ny - 1) + j) * (nx - 1) + i);
+    }
+};
+
+__global__ void add_counts(long long* __restrict__ nc) { nc[0] = nc[1] + nc[2]; }
 
 // energy_3d per-cell contribution (metrics.cpp:161-178)
 __global__ void contrib_3d(SlParams P, const double* __restrict__ phi, const double* __restrict__ dist,
@@ -697,13 +771,14 @@ int lsr_energy_loop_reserve(const SlParams& P, EnergyLoopWork& W, std::string* e
     }
     if (ncells <= W.cap) return LSR_OK;
     W.release();
-    EL_TRY(cudaMalloc(&W.flags, ncells));
+    const long long nodes = P.nxy * P.nz;  // the tube's flags are per tube entry (<= nodes)
+    EL_TRY(cudaMalloc(&W.flags, nodes));
     EL_TRY(cudaMalloc(&W.cells, sizeof(int) * ncells));
     EL_TRY(cudaMalloc(&W.contrib, sizeof(double) * ncells));
     EL_TRY(cudaMalloc(&W.partial, sizeof(double) * ((ncells + 4095) / 4096 + 1)));
-    EL_TRY(cudaMalloc(&W.nc, sizeof(long long)));
+    EL_TRY(cudaMalloc(&W.nc, 3 * sizeof(long long)));  // [0] interface cells = [1] dense + [2] tube selection
     EL_TRY(cudaMalloc(&W.ood, sizeof(int)));
-    W.tmp_bytes = lsr_compact::scratch_bytes(ncells);
+    W.tmp_bytes = lsr_compact::scratch_bytes(nodes);
     EL_TRY(cudaMalloc(&W.tmp, W.tmp_bytes));
     W.cap = ncells;
     return LSR_OK;
@@ -711,7 +786,8 @@ int lsr_energy_loop_reserve(const SlParams& P, EnergyLoopWork& W, std::string* e
 
 int lsr_energy_enqueue(const SlParams& P, const double* phi, const double* dist, int p, int refine,
                        EnergyLoopWork& W, long long est_cells, double* d_e2, int* d_flags, cudaStream_t s,
-                       std::string* err) {
+                       std::string* err, const long long* tube, const long long* n_tube_dev, long long est_tube,
+                       const int* hard) {
     if (p < 1 || (P.dim == 3 && refine < 1)) {
         *err = "surface_energy: invalid p or refinement";  // metrics.cpp:115,147
         return LSR_ERR_CONFIG;
@@ -724,17 +800,34 @@ int lsr_energy_enqueue(const SlParams& P, const double* phi, const double* dist,
     const long long ncells = W.cap;
     EL_TRY(cudaMemsetAsync(W.ood, 0, sizeof(int), s));
     const int T = 256;
+    // the interface cells, ascending (metrics.cpp:150-156): every cell tested
+    // (when *hard != 0, or always without a tube), or the cells based at the
+    // tube's nodes (flag_cells_tube); the device decides, both selections go
+    // to W.cells and the one that did not run selects nothing
+    const bool sparse = tube != nullptr && n_tube_dev != nullptr && hard != nullptr;
+    const int* dense_if = sparse ? hard : nullptr;
     if (P.dim == 3 && P.nx % 4 == 0) {
         const unsigned tpr = static_cast<unsigned>((P.nx - 1 + 3) / 4);
         const long long nt = static_cast<long long>(P.ny - 1) * tpr * ((P.nz - 1 + kMarchCells - 1) / kMarchCells);
-        flag_cells_march<<<static_cast<unsigned>((nt + T - 1) / T), T, 0, s>>>(P, phi, tpr, W.flags, 0, P.nz - 1);
+        flag_cells_march<<<static_cast<unsigned>((nt + T - 1) / T), T, 0, s>>>(P, phi, tpr, W.flags, 0, P.nz - 1,
+                                                                                dense_if);
     } else {
-        flag_cells<<<static_cast<unsigned>((ncells + T - 1) / T), T, 0, s>>>(P, phi, 0, ncells, W.flags);
+        flag_cells<<<static_cast<unsigned>((ncells + T - 1) / T), T, 0, s>>>(P, phi, 0, ncells, W.flags, dense_if);
     }
     lsr_note_launch();
-    EL_TRY(lsr_compact::compact(lsr_compact::BytePred<FlagSet>{W.flags, {}}, CellId{}, ncells, W.cells, W.nc, W.tmp,
-                                W.tmp_bytes, s));
+    EL_TRY(lsr_compact::compact_m(lsr_compact::GatedBytes{W.flags, nullptr, dense_if, 1}, CellId{}, ncells, W.cells,
+                                  sparse ? W.nc + 1 : W.nc, W.tmp, W.tmp_bytes, s));
     for (int q = 0; q < 2; ++q) lsr_note_launch();
+    if (sparse) {
+        const long long nodes = P.nxy * P.nz;
+        const long long est = est_tube > 0 ? est_tube : 1;
+        flag_cells_tube<<<static_cast<unsigned>((est + T - 1) / T), T, 0, s>>>(P, phi, tube, n_tube_dev, W.flags, hard);
+        EL_TRY(lsr_compact::compact_m(lsr_compact::GatedBytes{W.flags, n_tube_dev, hard, 0},
+                                      TubeCellId{tube, P.nx, P.ny, P.dim}, nodes, W.cells, W.nc + 2, W.tmp,
+                                      W.tmp_bytes, s));
+        add_counts<<<1, 1, 0, s>>>(W.nc);
+        for (int q = 0; q < 4; ++q) lsr_note_launch();
+    }
     // the contributions: an estimate of the count sizes the grid, which strides past it
     const long long est = est_cells > 0 ? est_cells : 1;
     if (P.dim == 3) {

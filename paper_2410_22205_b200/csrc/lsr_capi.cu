@@ -234,6 +234,8 @@ struct lsr_cuda_ctx {
     unsigned long long* bm = nullptr;  // node bitmaps of the zero-copy pull (transfer.cu)
     int64_t cap_bm = 0;
     ZtBuffers zt{};  // z-line table of the 3d WENO path (sl_launch.h)
+    double* bd = nullptr;    // per-brick max d and max |grad d| (launch_brick_d); valid for the current d:
+    bool bd_valid = false;
     bool zt_bricks = false;  // zt.list holds the covered bricks of the current active set ...
     double zt_key[4] = {0, 0, 0, 0};  // ... for this (E, dt, delta, p) (and the current d)
     cudaStream_t s_aux = nullptr;  // resync beside the table fill
@@ -372,6 +374,7 @@ int lsr_cuda_destroy(lsr_cuda_ctx* c) {
     cudaFree(c->zt.reach);
     cudaFree(c->zt.list);
     cudaFree(c->zt.count);
+    cudaFree(c->bd);
     cudaFree(c->box.count);
     cudaFree(c->box.off);
     cudaFree(c->box.cursor);
@@ -419,6 +422,7 @@ int lsr_cuda_upload_field(lsr_cuda_ctx* c, int which, const double* host) {
     LSR_CUDA_TRY(cudaStreamSynchronize(c->stream));
     if (which != LSR_FIELD_DIST) c->consistent = false;
     else c->zt_bricks = false;
+    c->bd_valid = false;
     c->box_valid = false;  // the covered bricks depend on d
     return LSR_OK;
 }
@@ -447,6 +451,7 @@ int lsr_cuda_mark_dirty(lsr_cuda_ctx* c, int which) {
     c->seq++;  // may write phi or out
     if (which != LSR_FIELD_DIST) c->consistent = false;
     else c->zt_bricks = false;
+    c->bd_valid = false;
     c->box_valid = false;
     return LSR_OK;
 }
@@ -462,6 +467,7 @@ int lsr_cuda_set_active(lsr_cuda_ctx* c, const int64_t* ids, int64_t n) {
     LSR_CUDA_TRY(cudaStreamSynchronize(c->stream));
     c->n_active = n;
     c->zt_bricks = false;
+    c->bd_valid = false;
     c->box_valid = false;
     c->dirty_is_active = false;
     return LSR_OK;
@@ -487,6 +493,7 @@ int lsr_cuda_set_active_device(lsr_cuda_ctx* c, const int64_t* d_ids, int64_t n)
     }
     c->n_active = n;
     c->zt_bricks = false;
+    c->bd_valid = false;
     c->box_valid = false;
     c->dirty_is_active = false;
     return LSR_OK;
@@ -1012,6 +1019,7 @@ static int sl_step_host_pipelined(lsr_cuda_ctx* c, const double* phi, const doub
         LSR_CUDA_TRY(cudaMemcpyAsync(c->phi, phi, sizeof(double) * chunk_off(prefetch), cudaMemcpyHostToDevice, up));
     c->n_active = n_active;
     c->zt_bricks = false;
+    c->bd_valid = false;
     c->box_valid = false;
     c->dirty_is_active = false;
     c->consistent = false;
@@ -1309,6 +1317,7 @@ int lsr_cuda_sl_step_host(const lsr_grid* grid, const double* phi, const double*
         LSR_CUDA_TRY(cudaMemcpyAsync(c->active, active, sizeof(int64_t) * n_active, cudaMemcpyHostToDevice, s));
     c->n_active = n_active;
     c->zt_bricks = false;
+    c->bd_valid = false;
     c->box_valid = false;
     c->dirty_is_active = false;
     c->consistent = false;
@@ -1333,6 +1342,7 @@ int lsr_cuda_ctx_build_distance(lsr_cuda_ctx* c, const double* pts, int64_t n, i
     LSR_CUDA_TRY(cudaSetDevice(c->device));
     if (!c->exact) LSR_CUDA_TRY(cudaMalloc(&c->exact, static_cast<size_t>(c->n)));
     c->zt_bricks = false;
+    c->bd_valid = false;
     c->box_valid = false;  // the covered bricks depend on d
     std::string err;
     double sent = 0.0;
@@ -1418,6 +1428,7 @@ int lsr_cuda_narrow_band(lsr_cuda_ctx* c, int which, double gamma, int64_t* n_ac
                                      c->stream));
     c->n_active = na;
     c->zt_bricks = false;
+    c->bd_valid = false;
     c->box_valid = false;
     c->dirty_is_active = false;
     if (n_active) *n_active = na;
@@ -1451,6 +1462,7 @@ int lsr_cuda_clamp_field(lsr_cuda_ctx* c, int which, double gamma) {
     LSR_CUDA_TRY(cudaStreamSynchronize(c->stream));
     if (which != LSR_FIELD_DIST) c->consistent = false;
     else c->zt_bricks = false;
+    c->bd_valid = false;
     c->box_valid = false;  // the covered bricks depend on d
     return LSR_OK;
 }
@@ -1507,6 +1519,7 @@ int lsr_cuda_set_band(lsr_cuda_ctx* c, const uint8_t* state, const int64_t* acti
         LSR_CUDA_TRY(cudaMemcpyAsync(c->active, active, sizeof(int64_t) * n_active, cudaMemcpyHostToDevice, s));
     c->n_active = n_active;
     c->zt_bricks = false;
+    c->bd_valid = false;
     c->box_valid = false;
     c->dirty_is_active = false;
     LSR_CUDA_TRY(cudaStreamSynchronize(s));
@@ -1576,6 +1589,7 @@ int lsr_cuda_fast_sweep(lsr_cuda_ctx* c, const uint8_t* exact, double sentinel, 
         return set_err(st, err);
     LSR_CUDA_TRY(cudaStreamSynchronize(c->stream));
     c->zt_bricks = false;
+    c->bd_valid = false;
     c->box_valid = false;  // the covered bricks depend on d
     if (rounds) *rounds = r;
     return LSR_OK;
@@ -1761,6 +1775,10 @@ int loop_reserve(lsr_cuda_ctx* c, int iterations) {
         LSR_CUDA_TRY(cudaMalloc(&c->zt.list, sizeof(unsigned) * static_cast<size_t>(nb)));
         LSR_CUDA_TRY(cudaMalloc(&c->zt.count, 2 * sizeof(unsigned)));
     }
+    if (!c->bd && c->grid.dim == 3) {
+        LSR_CUDA_TRY(cudaMalloc(&c->bd, sizeof(double) * 2 * static_cast<size_t>(zt_num_bricks(c->grid.dims))));
+        c->bd_valid = false;
+    }
     return LSR_OK;
 }
 
@@ -1776,10 +1794,12 @@ int enqueue_loop_iteration(lsr_cuda_ctx* c, double* a, double* b, const lsr_step
     std::string err;
     loop_mark<<<1, 1, 0, s>>>(st, L.k, 0);
     // 1. band of phi^n (driver.cpp:187)
-    if (int e = lsr_band_enqueue(G, a, cfg->gamma, c->band, s, &err)) return set_err(e, err);
+    if (int e = lsr_band_enqueue(G, a, cfg->gamma, c->band, s, &err, L.hard)) return set_err(e, err);
     loop_mark<<<1, 1, 0, s>>>(st, L.k, 1);
     // 2. E_2 of phi^n (driver.cpp:188)
-    if (int e = lsr_energy_enqueue(G, a, c->dist, 2, refine, L.ew, L.est_cells, L.e2, L.flags, s, &err))
+    // (interface cells from the band's tube unless phi^n may hold a hard jump, L.hard[0])
+    if (int e = lsr_energy_enqueue(G, a, c->dist, 2, refine, L.ew, L.est_cells, L.e2, L.flags, s, &err, c->band.tube,
+                                   c->band.counts + 1, L.est_active + L.est_active / 4, L.hard))
         return set_err(e, err);
     loop_mark<<<1, 1, 0, s>>>(st, L.k, 2);
     // 3. sl_step a -> b on the band's ACTIVE ids, E_2 read on the device; the
@@ -1792,7 +1812,12 @@ int enqueue_loop_iteration(lsr_cuda_ctx* c, double* a, double* b, const lsr_step
     const bool use_table = LSR_ZTAB && c->grid.dim == 3 && cfg->interp == 1 && P.fast_weno &&
                            c->grid.dims[2] >= 4 && cfg->delta > 0.0;
     if (use_table) {
-        LSR_CUDA_TRY(launch_zt_bricks(P, c->dist, ids, L.est_active, c->zt, s));
+        // covered bricks: from the band's state bytes and the per-brick maxima
+        // of d (rows of whole 4-node brick words), else from the active ids
+        if (c->grid.dims[0] % 4 == 0 && c->bd_valid)
+            LSR_CUDA_TRY(launch_zt_bricks_state(P, c->band.state, c->bd, c->zt, s));
+        else
+            LSR_CUDA_TRY(launch_zt_bricks(P, c->dist, ids, L.est_active, c->zt, s));
         LSR_CUDA_TRY(launch_zt_fill(P, a, c->zt, s));
         zt_attach(P, c->zt);
     }
@@ -1805,7 +1830,8 @@ int enqueue_loop_iteration(lsr_cuda_ctx* c, double* a, double* b, const lsr_step
     if (int e = lsr_reinit_enqueue(G, b, c->scratch, c->band, cfg->gamma, R, c->rb, L.rl, clamp_sparse, L.hard, s,
                                    &err))
         return set_err(e, err);
-    if (int e = lsr_loop_sync_fields(G, b, a, c->scratch, c->band, c->rb, L.rl, cfg->gamma, L.hard, s, &err))
+    if (int e = lsr_loop_sync_fields(G, b, a, c->scratch, c->band, c->rb, L.rl, cfg->gamma, L.hard, clamp_sparse, s,
+                                      &err))
         return set_err(e, err);
     loop_record<<<1, 1, 0, s>>>(st, L.k, L.e2, c->band.counts, L.ew.nc, L.rl, c->d_bad, L.flags, cfg->p, L.hard);
     for (int q = 0; q < 5; ++q) lsr_note_launch();
@@ -1826,6 +1852,7 @@ std::string loop_key(const lsr_cuda_ctx* c, const double* a, const double* b, co
     put(&refine, sizeof refine);
     put(&c->lr.est_active, sizeof c->lr.est_active);
     put(&c->lr.est_cells, sizeof c->lr.est_cells);
+    put(&c->bd_valid, sizeof c->bd_valid);
     return k;
 }
 
@@ -1889,6 +1916,10 @@ int lsr_cuda_loop_run(lsr_cuda_ctx* c, const lsr_step_cfg* cfg, const lsr_reinit
             return set_err(st, err);
         L.est_active = na > 0 ? na : 1;
         L.est_cells = na / 4 + 1;
+    }
+    if (c->grid.dim == 3 && c->grid.dims[0] % 4 == 0 && !c->bd_valid) {
+        LSR_CUDA_TRY(launch_brick_d(grid_params(c->grid), c->dist, c->bd, s));
+        c->bd_valid = true;
     }
     const bool first_sparse =
         c->clamped_seq == c->seq && c->clamped_phi == c->phi && c->clamped_gamma == cfg->gamma;

@@ -35,7 +35,7 @@ struct EnergyLoopWork {
     int* cells = nullptr;
     double* contrib = nullptr;
     double* partial = nullptr;
-    long long* nc = nullptr;  // [0] interface cells
+    long long* nc = nullptr;  // [0] interface cells ([1], [2]: the dense and the tube selection's counts)
     int* ood = nullptr;
     void* tmp = nullptr;
     size_t tmp_bytes = 0;
@@ -45,7 +45,8 @@ struct EnergyLoopWork {
 int lsr_energy_loop_reserve(const lsr_dev::SlParams& P, EnergyLoopWork& W, std::string* err);
 int lsr_energy_enqueue(const lsr_dev::SlParams& P, const double* phi, const double* dist, int p, int refine,
                        EnergyLoopWork& W, long long est_cells, double* d_e2, int* d_flags, cudaStream_t s,
-                       std::string* err);
+                       std::string* err, const long long* tube = nullptr, const long long* n_tube_dev = nullptr,
+                       long long est_tube = 0, const int* hard = nullptr);
 
 // lsr::compute_stats (cloud.cpp:480-489) with the NN sample on the device.
 int lsr_prep_compute_stats(const double* h_pts, int64_t n, int dim, double fraction, double k_s, uint64_t seed,

@@ -60,6 +60,11 @@ cudaError_t launch_zt_bricks(const lsr_dev::SlParams& P, const double* dist, con
                              const ZtBuffers& Z, cudaStream_t stream);
 // table entries of the listed bricks from phi (every step)
 cudaError_t launch_zt_fill(const lsr_dev::SlParams& P, const double* phi, const ZtBuffers& Z, cudaStream_t stream);
+// the device loop's form: per-brick maxima of d and |grad d| (once per d),
+// then the covered bricks from the band's state bytes and E (sl_step.cu)
+cudaError_t launch_brick_d(const lsr_dev::SlParams& P, const double* dist, double* bd, cudaStream_t stream);
+cudaError_t launch_zt_bricks_state(const lsr_dev::SlParams& P, const unsigned char* state, const double* bd,
+                                   const ZtBuffers& Z, cudaStream_t stream);
 
 cudaError_t launch_check_sorted(const int64_t* ids, long long n, unsigned long long* bad, cudaStream_t stream);
 cudaError_t launch_reach_max(const lsr_dev::SlParams& P, const double* dist, const int64_t* active, long long n,

@@ -374,6 +374,102 @@ __global__ void zt_cover_kernel(const unsigned* __restrict__ reach, int nbx, int
     }
 }
 
+// ---- the covered bricks from the band's state bytes (the device loop) ----
+// The per-node reach above needs a pass over the active ids and their d
+// stencils every iteration. Its bound is monotone in d_j and in |grad d|, and
+// both are fields of the run, not of the iteration: brick_d_kernel keeps, per
+// brick, bd[2b] = max d and bd[2b + 1] = max |centered_gradient(d)| component
+// over the brick's nodes (once per d), and zt_cover_state_kernel bounds the
+// reach of every brick holding an ACTIVE node (state byte 1) from them and
+// this iteration's E. The bound is looser than the per-node one by the
+// variation of d over a brick; like it, it only decides which bricks the table
+// covers (speed), never a result.
+
+// one thread per (brick, row of the brick): its 4 nodes' d and gradient
+// components; the 16 rows of a brick sit in 16 consecutive lanes
+__global__ void brick_d_kernel(SlParams P, const double* __restrict__ dist, int nbx, int nby, int nbz,
+                               double* __restrict__ bd) {
+    const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const long long b = t >> 4;
+    const int r = static_cast<int>(t & 15);
+    double dm = 0.0, gm = 0.0;
+    const bool live = b < static_cast<long long>(nbx) * nby * nbz;
+    if (live) {
+        const int bi = static_cast<int>(b % nbx), bj = static_cast<int>((b / nbx) % nby),
+                  bk = static_cast<int>(b / (static_cast<long long>(nbx) * nby));
+        const int j = bj * kZtBrick + (r & 3), k = bk * kZtBrick + (r >> 2);
+        if (j < P.ny && k < P.nz) {
+            for (int q = 0; q < kZtBrick; ++q) {
+                const int i = bi * kZtBrick + q;
+                if (i >= P.nx) break;
+                const long long id = (static_cast<long long>(k) * P.ny + j) * P.nx + i;
+                dm = fmax(dm, __ldg(dist + id));
+                gm = fmax(gm, fabs(grad_axis(P, dist, id, i, P.nx, 1)));
+                gm = fmax(gm, fabs(grad_axis(P, dist, id, j, P.ny, P.nx)));
+                if (P.dim == 3) gm = fmax(gm, fabs(grad_axis(P, dist, id, k, P.nz, P.nxy)));
+            }
+        }
+    }
+#pragma unroll
+    for (int off = 8; off > 0; off >>= 1) {
+        dm = fmax(dm, __shfl_xor_sync(0xffffffffu, dm, off));
+        gm = fmax(gm, __shfl_xor_sync(0xffffffffu, gm, off));
+    }
+    if (live && r == 0) {
+        bd[2 * b] = dm;
+        bd[2 * b + 1] = gm;
+    }
+}
+
+// one thread per brick (nx % 4 == 0, so a brick row is one aligned 4-byte
+// word of the state): any ACTIVE node -> reach from (max d, max |grad d|, E)
+// as zt_reach_one computes it per node -> cover as zt_cover_kernel
+__global__ void zt_cover_state_kernel(SlParams P, const unsigned char* __restrict__ state,
+                                      const double* __restrict__ bd, int nbx, int nby, int nbz,
+                                      unsigned char* __restrict__ cover) {
+    const long long b = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (b >= static_cast<long long>(nbx) * nby * nbz) return;
+    const int bi = static_cast<int>(b % nbx), bj = static_cast<int>((b / nbx) % nby),
+              bk = static_cast<int>(b / (static_cast<long long>(nbx) * nby));
+    unsigned any = 0;
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+        const int j = bj * kZtBrick + (r & 3), k = bk * kZtBrick + (r >> 2);
+        if (j < P.ny && k < P.nz) {
+            const unsigned w = __ldg(reinterpret_cast<const unsigned*>(
+                state + (static_cast<long long>(k) * P.ny + j) * P.nx + bi * kZtBrick));
+            const unsigned x = w ^ 0x01010101u;  // a zero byte where the state is ACTIVE (1)
+            any |= (x - 0x01010101u) & ~x & 0x80808080u;
+        }
+    }
+    if (!any) return;
+    const double dmax = bd[2 * b], gmax = bd[2 * b + 1];
+    const double c_j = P.p == 1 ? 1.0 : dmax / energy_of(P);
+    const double sdt = c_j * P.dt;
+    const double spread = sqrt(fmax(0.0, c_j * P.delta * dmax * P.dt / P.pd));
+    const double cells = (fabs(sdt * gmax) + 1.4143 * spread) / P.dx;
+    int rn = kZtMaxReach, rp = kZtMaxReach;
+    if (cells < static_cast<double>(kZtMaxReach)) {
+        rp = static_cast<int>(floor(cells));
+        rn = static_cast<int>(ceil(cells));
+    }
+    const int lo = floor_div(-rn - 1, kZtBrick), hi = floor_div(kZtBrick + 1 + rp, kZtBrick);
+    const int loz = floor_div(-rn, kZtBrick), hiz = floor_div(kZtBrick + rp, kZtBrick);
+    for (int dk = loz; dk <= hiz; ++dk) {
+        const int z = bk + dk;
+        if (z < 0 || z >= nbz) continue;
+        for (int dj = lo; dj <= hi; ++dj) {
+            const int y = bj + dj;
+            if (y < 0 || y >= nby) continue;
+            for (int di = lo; di <= hi; ++di) {
+                const int x = bi + di;
+                if (x < 0 || x >= nbx) continue;
+                cover[(static_cast<long long>(z) * nby + y) * nbx + x] = 1;
+            }
+        }
+    }
+}
+
 // list = the covered bricks (any order)
 __global__ void zt_list_kernel(const unsigned char* __restrict__ cover, long long nbricks,
                                unsigned* __restrict__ list, unsigned* __restrict__ count) {
@@ -703,6 +799,32 @@ cudaError_t launch_zt_bricks(const SlParams& P, const double* dist, const int64_
     zt_cover_kernel<<<gb, 256, 0, stream>>>(Z.reach, nbx, nby, nbz, Z.mark);
     zt_list_kernel<<<gb, 256, 0, stream>>>(Z.mark, nbricks, Z.list, Z.count);
     for (int r = 0; r < 3; ++r) lsr_note_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_brick_d(const SlParams& P, const double* dist, double* bd, cudaStream_t stream) {
+    const int nbx = (P.nx + kZtBrick - 1) / kZtBrick, nby = (P.ny + kZtBrick - 1) / kZtBrick,
+              nbz = (P.nz + kZtBrick - 1) / kZtBrick;
+    const long long threads = 16LL * nbx * nby * nbz;
+    brick_d_kernel<<<static_cast<unsigned>((threads + 255) / 256), 256, 0, stream>>>(P, dist, nbx, nby, nbz, bd);
+    lsr_note_launch();
+    return cudaGetLastError();
+}
+
+// the covered bricks of the band whose state bytes are `state` (ACTIVE = 1);
+// needs nx % 4 == 0 and bd from launch_brick_d of the same d
+cudaError_t launch_zt_bricks_state(const SlParams& P, const unsigned char* state, const double* bd, const ZtBuffers& Z,
+                                   cudaStream_t stream) {
+    const int nbx = (P.nx + kZtBrick - 1) / kZtBrick, nby = (P.ny + kZtBrick - 1) / kZtBrick,
+              nbz = (P.nz + kZtBrick - 1) / kZtBrick;
+    const long long nbricks = static_cast<long long>(nbx) * nby * nbz;
+    cudaError_t e = cudaMemsetAsync(Z.mark, 0, static_cast<size_t>(nbricks), stream);
+    if (e == cudaSuccess) e = cudaMemsetAsync(Z.count, 0, sizeof(unsigned), stream);
+    if (e != cudaSuccess) return e;
+    const unsigned gb = static_cast<unsigned>((nbricks + 255) / 256);
+    zt_cover_state_kernel<<<gb, 256, 0, stream>>>(P, state, bd, nbx, nby, nbz, Z.mark);
+    zt_list_kernel<<<gb, 256, 0, stream>>>(Z.mark, nbricks, Z.list, Z.count);
+    for (int r = 0; r < 2; ++r) lsr_note_launch();
     return cudaGetLastError();
 }
 
