@@ -734,6 +734,28 @@ def measure_loop(lsr, g, phi, ctx, step, steps=6, cpu_too=True):
         "sl_ms_per_step": float(ms[:, 2].mean()), "active_nodes_mean": float(na.mean()), "iterations": steps - 1,
         "what": "SL phase of the device loop (band rebuilt every iteration: covered-brick list, z-line table "
                 "fill, sparse resync, SL kernel), CUDA events; loop iterations 2..N from phi^0"}
+    # the same iterations controlled on the device (lsr_cuda_loop_run: one host
+    # sync per run, iterations 2..K replayed from a CUDA graph), again from
+    # phi^0: device phase times from globaltimer marks, and the wall time of
+    # the whole call per iteration
+    run_iters = 2 * steps
+    for _ in range(2):  # the first run captures the graphs
+        ctx.upload(lsr._api.FIELD_PHI, phi)
+        t0 = time.perf_counter()
+        recs = ctx.loop_run(step, rc, run_iters, 5)
+        wall = time.perf_counter() - t0
+    rms = np.array([r["ms"] for r in recs[1:]])
+    rna = np.array([r["n_active"] for r in recs[1:]], dtype=np.float64)
+    out["device_run"] = {
+        "gpu_ms_per_step": dict(zip(("band", "energy", "sl", "reinit"), map(float, rms.mean(0)))),
+        "gpu_total_ms_per_step": float(rms.sum(1).mean()), "wall_ms_per_step": 1e3 * wall / run_iters,
+        "iterations": run_iters, "host_syncs": 1,
+        "reinit_iterations": [r["reinit_iterations"] for r in recs],
+        "same_bands_as_host_loop": [r["n_active"] for r in recs[:steps]] == [s["n_active"] for s in stats],
+        "moving_band": {"value": float(rna.sum() / (rms[:, 2].sum() * 1e-3)), "unit": UNIT,
+                        "sl_ms_per_step": float(rms[:, 2].mean())},
+        "what": "lsr_cuda_loop_run: band counts, E_2, the E_2 == 0 skip, NoInterface and the Jacobi stop rule "
+                "decided on the device; iterations 2..K (graph replays) averaged"}
     if cpu_too:
         from oracle import bindings
 
@@ -748,6 +770,8 @@ def measure_loop(lsr, g, phi, ctx, step, steps=6, cpu_too=True):
             out["cpu_reference_total_ms_per_step"] = float(1e3 * sum(sec))
             out["cpu_cores"] = os.cpu_count()
             out["loop_speedup_vs_cpu_reference"] = out["cpu_reference_total_ms_per_step"] / out["gpu_total_ms_per_step"]
+            out["device_run"]["speedup_vs_cpu_reference"] = (out["cpu_reference_total_ms_per_step"] /
+                                                             out["device_run"]["gpu_total_ms_per_step"])
     return out
 
 

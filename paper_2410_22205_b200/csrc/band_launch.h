@@ -75,6 +75,7 @@ struct ReinitLoopDev {
     int iterations;
     unsigned arrived;
     unsigned pad2;
+    long long parts[4];      // list lengths of the dense ([0], [1]) and the tube ([2], [3]) selection
 };
 int lsr_band_enqueue(const lsr_dev::SlParams& P, const double* phi, double gamma, BandBuffers& B, cudaStream_t s,
                      std::string* err, const int* hard = nullptr);

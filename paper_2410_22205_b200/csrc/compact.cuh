@@ -110,20 +110,23 @@ struct Identity {
     __device__ long long operator()(long long i) const { return i; }
 };
 
-// A tile's selected items, ranked, go to shared memory and from there to
-// out[0 .. total) with consecutive threads storing consecutive entries (the
-// per-thread runs written straight to global memory made 8-byte stores at 16
-// scattered addresses per warp instruction). All threads of the CTA call it.
+// A tile's selected items, ranked: their offsets within the tile go to shared
+// memory, and consecutive threads then store consecutive entries
+// out[x] = item(tile + offset[x]) (the per-thread runs written straight to
+// global memory made 8-byte stores at 16 scattered addresses per warp
+// instruction, and an item that is itself a load — a list entry — was
+// fetched by 16 dependent iterations per thread). All threads of the CTA call it.
 template <class Item, class Out>
-__device__ __forceinline__ void staged_write(Out* __restrict__ stage, Out* __restrict__ out, int total, int rank,
-                                             unsigned mask, long long base, Item item) {
+__device__ __forceinline__ void staged_write(unsigned short* __restrict__ stage, Out* __restrict__ out, int total,
+                                             int rank, unsigned mask, long long tile, Item item) {
+    const unsigned local = threadIdx.x * kItems;
     while (mask) {
         const int q = __ffs(mask) - 1;
         mask &= mask - 1;
-        stage[rank++] = item(base + q);
+        stage[rank++] = static_cast<unsigned short>(local + q);
     }
     __syncthreads();
-    for (int x = threadIdx.x; x < total; x += kThreads) out[x] = stage[x];
+    for (int x = threadIdx.x; x < total; x += kThreads) out[x] = item(tile + stage[x]);
     __syncthreads();
 }
 
@@ -217,9 +220,10 @@ __global__ void __launch_bounds__(kThreads) write_tiles_bytes2(BytePred<T1> p1, 
     Scan(tmp).ExclusiveSum(__popc(m1), r1);
     __syncthreads();
     Scan(tmp).ExclusiveSum(__popc(m2), r2);
-    __shared__ Out stage[kTile];
-    staged_write(stage, out1 + o1[blockIdx.x], static_cast<int>(o1[blockIdx.x + 1] - o1[blockIdx.x]), r1, m1, base, item);
-    staged_write(stage, out2 + o2[blockIdx.x], static_cast<int>(o2[blockIdx.x + 1] - o2[blockIdx.x]), r2, m2, base, item);
+    __shared__ unsigned short stage[kTile];
+    const long long tile = static_cast<long long>(blockIdx.x) * kTile;
+    staged_write(stage, out1 + o1[blockIdx.x], static_cast<int>(o1[blockIdx.x + 1] - o1[blockIdx.x]), r1, m1, tile, item);
+    staged_write(stage, out2 + o2[blockIdx.x], static_cast<int>(o2[blockIdx.x + 1] - o2[blockIdx.x]), r2, m2, tile, item);
 }
 
 inline size_t scratch_bytes2(long long n) { return 2 * scratch_bytes(n); }
@@ -313,9 +317,10 @@ __global__ void __launch_bounds__(kThreads) write_tiles_m2(M1 p1, M2 p2, Item it
     Scan(tmp).ExclusiveSum(__popc(m1), r1);
     __syncthreads();
     Scan(tmp).ExclusiveSum(__popc(m2), r2);
-    __shared__ Out stage[kTile];
-    staged_write(stage, out1 + o1[blockIdx.x], static_cast<int>(o1[blockIdx.x + 1] - o1[blockIdx.x]), r1, m1, base, item);
-    staged_write(stage, out2 + o2[blockIdx.x], static_cast<int>(o2[blockIdx.x + 1] - o2[blockIdx.x]), r2, m2, base, item);
+    __shared__ unsigned short stage[kTile];
+    const long long tile = static_cast<long long>(blockIdx.x) * kTile;
+    staged_write(stage, out1 + o1[blockIdx.x], static_cast<int>(o1[blockIdx.x + 1] - o1[blockIdx.x]), r1, m1, tile, item);
+    staged_write(stage, out2 + o2[blockIdx.x], static_cast<int>(o2[blockIdx.x + 1] - o2[blockIdx.x]), r2, m2, tile, item);
 }
 
 template <class M1, class M2, class Item, class Out>
@@ -367,9 +372,9 @@ __global__ void __launch_bounds__(kThreads) write_tiles_m(M p, Item item, long l
     __shared__ typename Scan::TempStorage tmp;
     int rank;
     Scan(tmp).ExclusiveSum(__popc(mask), rank);
-    __shared__ Out stage[kTile];
+    __shared__ unsigned short stage[kTile];
     staged_write(stage, out + offsets[blockIdx.x], static_cast<int>(offsets[blockIdx.x + 1] - offsets[blockIdx.x]), rank,
-                 mask, base, item);
+                 mask, static_cast<long long>(blockIdx.x) * kTile, item);
 }
 
 // flag bytes a[0 .. min(n, *n_dev)) (n_dev null: a[0 .. n)), selected where
@@ -396,6 +401,40 @@ struct GatedBytes {
         } else {
             for (int q = 0; q < kItems && base + q < n; ++q) m |= (a[base + q] != 0 ? 1u : 0u) << q;
         }
+        return m;
+    }
+};
+
+// any mask provider behind a device-side gate: selects nothing unless
+// (*gate != 0) == open
+template <class M>
+struct Gated {
+    M m;
+    const int* gate;
+    int open;
+    __device__ __forceinline__ unsigned mask16(long long base, long long n) const {
+        if ((*gate != 0) != (open != 0)) return 0u;
+        return m.mask16(base, n);
+    }
+};
+
+// entries t < *n_dev of a list whose flag byte a[t] is nonzero (want = 1) or zero (want = 0)
+struct ListFlag {
+    const unsigned char* a;
+    const long long* n_dev;
+    int want;
+    __device__ __forceinline__ unsigned mask16(long long base, long long n) const {
+        const long long nd = *n_dev;
+        n = nd < n ? nd : n;
+        unsigned m = 0;
+        if (base + kItems <= n) {
+            const uint4 v = *reinterpret_cast<const uint4*>(a + base);
+            const unsigned w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int q = 0; q < kItems; ++q) m |= (((w[q >> 2] >> (8 * (q & 3))) & 0xffu) != 0 ? 1u : 0u) << q;
+            return want ? m : (~m & 0xffffu);
+        }
+        for (int q = 0; q < kItems && base + q < n; ++q) m |= ((a[base + q] != 0) == (want != 0) ? 1u : 0u) << q;
         return m;
     }
 };

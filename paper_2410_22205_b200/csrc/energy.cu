@@ -176,7 +176,7 @@ __global__ void flag_cells_tube(SlParams P, const double* __restrict__ phi, cons
                                 const int* __restrict__ hard) {
     if (*hard != 0) return;
     const long long n = __ldg(n_dev);
-    constexpr int kB = 2;  // entries per thread and round, their corner loads in flight together
+    constexpr int kB = 1;  // entries per thread and round (2 measured slower)
     const long long T = static_cast<long long>(gridDim.x) * blockDim.x * kB;
     const int kz = P.dim == 3 ? 1 : 0;
     for (long long t0 = static_cast<long long>(blockIdx.x) * blockDim.x * kB; t0 < n; t0 += T) {
