@@ -131,3 +131,15 @@ def test_loop_run_hard_jump_keeps_dense_one_step(gpu):
     phi[(x > 0.9) & (y > 0.9)] = -1.0
     recs = _compare(lsr, g, pts, phi, cfg, rc, 6)
     assert recs[0]["dense_one_step"] and recs[1]["dense_one_step"]
+
+
+@pytest.mark.parametrize("n", [36, 34, 48])
+def test_loop_run_grid_shapes(gpu, n):
+    """Row lengths that take the other forms of the band and table passes:
+    36 (whole 4-node brick words but no 16-node groups: scalar band passes,
+    covered bricks from the state bytes), 34 (neither: covered bricks from the
+    active ids), 48 (both, the forms the configs run)."""
+    lsr = gpu
+    g, pts, phi, cfg, rc = _setup(lsr, 3, n=n)
+    recs = _compare(lsr, g, pts, phi, cfg, rc, 7)
+    assert not any(r["dense_one_step"] for r in recs[1:])

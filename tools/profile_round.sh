@@ -23,5 +23,11 @@ $LOOP > gpurun_out/loop_plain_$R.log 2>&1 || exit 1
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
     -k regex:"count_tiles|write_tiles|Scan|band_|flag_|contrib|block_partials|one_step|sign_|jacobi|iter_check|clamp_|sl_step|resync|copy_ids|zt_" \
     --csv --log-file gpurun_out/loop_launches_$R.csv $LOOP > gpurun_out/ncu_loop_$R.log 2>&1
+# 5b. the device-controlled loop (lsr_cuda_loop_run, graph replays): per-kernel
+# durations and DRAM bytes of one iteration (tools/loop_run_roofline.py)
+python tools/loopbench.py --steps 1 --run 12 > gpurun_out/loop_run_plain_$R.log 2>&1 || exit 1
+ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
+    --csv --log-file gpurun_out/loop_run_launches_$R.csv python tools/loopbench.py --steps 1 --run 3 \
+    > gpurun_out/ncu_loop_run_$R.log 2>&1
 # 6. the reference arm (the driver runs it too)
 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_ref_$R.json 2> gpurun_out/bench_ref_$R.err
