@@ -641,17 +641,31 @@ __device__ __forceinline__ double godunov_vals(const SlParams& P, double pc, con
 // the square, and a NaN u (v) is selected exactly when the reference's max
 // returns its NaN (finite) term. Returns false (the caller takes
 // godunov_vals) when a selected c is outside div_const's Markstein range.
+__device__ __forceinline__ double flip_sign(double x, unsigned m) {  // x, or -x when m = 0x80000000 (exact)
+    return __hiloint2double(__double2hiint(x) ^ static_cast<int>(m), __double2loint(x));
+}
+// markstein_ok also for -0 (the quotient is squared: the sign of a zero vanishes)
+__device__ __forceinline__ bool markstein_ok_z(double a) {
+    const long long bits = __double_as_longlong(a);
+    const unsigned e = static_cast<unsigned>(bits >> 32) & 0x7ff00000u;
+    return ((e - 0x07b00000u) <= (0x78300000u - 0x07b00000u)) | ((bits << 1) == 0);
+}
+// The sgn <= 0 pair min(dm, 0), max(dp, 0) is the negative of
+// max(-dm, 0), min(-dp, 0): negating both differences (a sign-bit flip)
+// reduces it to the sgn > 0 form with every magnitude unchanged (zeros may
+// change sign, NaNs stay NaN), and only magnitudes reach the result.
 __device__ __forceinline__ bool godunov_interior(const SlParams& P, double pc, const double* vm, const double* vp,
                                                  double sgn, double& gn) {
     double acc = 0.0;
     bool ok = P.fast_div != 0;
+    const unsigned m = sgn > 0.0 ? 0u : 0x80000000u;
 #pragma unroll
     for (int ax = 0; ax < 3; ++ax) {
         const double dm = pc - vm[ax], dp = vp[ax] - pc;
-        const double u = sgn > 0.0 ? smax(dm, 0.0) : smin(dm, 0.0);
-        const double v = sgn > 0.0 ? smin(dp, 0.0) : smax(dp, 0.0);
+        const double u = smax(flip_sign(dm, m), 0.0);
+        const double v = smin(flip_sign(dp, m), 0.0);
         const double c = fabs(u) < fabs(v) ? v : u;
-        ok = ok & markstein_ok(c);
+        ok = ok & markstein_ok_z(c);
         const double q = markstein(c, P.dx, P.rdx);
         acc += q * q;
     }
@@ -791,7 +805,7 @@ __global__ void __launch_bounds__(kPipeThreads, LSR_JAC_PIPE_MINB)
     }
     if (*reinterpret_cast<volatile int*>(&st->done)) return;
     unsigned long long bitsmax = 0;
-    while (__syncthreads_or(id[0] >= 0)) {
+    while (__any_sync(0xffffffffu, id[0] >= 0)) {  // per warp: no CTA barrier inside the sweep
         // this round's gathers
         double pc[kPipeNPT], vm[kPipeNPT][3], vp[kPipeNPT][3];
         bool hm[kPipeNPT][3], hp[kPipeNPT][3];

@@ -33,6 +33,17 @@ def selected_term(dm, dp, dx, sgn):
     return q * q
 
 
+def flipped_term(dm, dp, dx, sgn):
+    """godunov_interior as shipped: for sgn <= 0 both differences are negated
+    (a sign-bit flip) and the sgn > 0 pair max(., 0), min(., 0) is used."""
+    if not sgn > 0:
+        dm, dp = -dm, -dp
+    u, v = smax(dm, 0.0), smin(dp, 0.0)
+    c = np.where(np.abs(u) < np.abs(v), v, u)
+    q = c / dx
+    return q * q
+
+
 def test_one_division_per_axis_is_bit_exact():
     rng = np.random.default_rng(7)
     n = 2_000_000
@@ -47,6 +58,8 @@ def test_one_division_per_axis_is_bit_exact():
             r = reference_term(dm, dp, dx, sgn)
             s = selected_term(dm, dp, dx, sgn)
             assert np.array_equal(r.view(np.int64), s.view(np.int64)), sgn
+            f = flipped_term(dm, dp, dx, sgn)
+            assert np.array_equal(r.view(np.int64), f.view(np.int64)), sgn
 
 
 def test_nan_operands_pick_the_same_term():
@@ -60,3 +73,6 @@ def test_nan_operands_pick_the_same_term():
             assert np.array_equal(np.isnan(r), np.isnan(s))
             ok = ~np.isnan(r)
             assert np.array_equal(r[ok].view(np.int64), s[ok].view(np.int64))
+            f = flipped_term(dm.ravel(), dp.ravel(), dx, sgn)
+            assert np.array_equal(np.isnan(r), np.isnan(f))
+            assert np.array_equal(r[ok].view(np.int64), f[ok].view(np.int64))
