@@ -143,3 +143,18 @@ def test_loop_run_grid_shapes(gpu, n):
     g, pts, phi, cfg, rc = _setup(lsr, 3, n=n)
     recs = _compare(lsr, g, pts, phi, cfg, rc, 7)
     assert not any(r["dense_one_step"] for r in recs[1:])
+
+
+def test_loop_run_without_interface(gpu):
+    """A field that never changes sign: no interface cell, so E_2 == 0 and the
+    SL step is skipped (driver.cpp:191-195), and the one-step finds no
+    interface, so only the clamp acts (reinit.cpp:140-144) — decided on the
+    device, in the dense first iteration and in the sparse ones after it."""
+    lsr = gpu
+    g, pts, phi, cfg, rc = _setup(lsr, 2, n=32)
+    ax = g.axes()
+    r = np.sqrt(ax[0][None, None, :] ** 2 + ax[1][None, :, None] ** 2 + ax[2][:, None, None] ** 2).ravel()
+    phi = r + 0.05  # positive everywhere, inside the band near the centre
+    recs = _compare(lsr, g, pts, phi, cfg, rc, 4)
+    assert all(r["energy"] == 0.0 and not r["had_interface"] and r["reinit_iterations"] == 0 for r in recs)
+    assert all(r["n_active"] > 0 for r in recs)
