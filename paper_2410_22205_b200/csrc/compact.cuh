@@ -110,6 +110,14 @@ struct Identity {
     __device__ long long operator()(long long i) const { return i; }
 };
 
+// The loop's compactions run as persistent launches: a CTA per resident slot
+// walks the tiles (most of them empty — a band's tiles, a gated-off twin, a
+// list far shorter than its capacity), instead of one CTA launch per tile.
+inline unsigned persistent_grid(long long tiles) {
+    const long long cap = 148LL * 8;
+    return static_cast<unsigned>(tiles < cap ? tiles : cap);
+}
+
 // A tile's selected items, ranked: their offsets within the tile go to shared
 // memory, and consecutive threads then store consecutive entries
 // out[x] = item(tile + offset[x]) (the per-thread runs written straight to
@@ -207,23 +215,25 @@ __global__ void __launch_bounds__(kThreads) count_tiles_bytes2(BytePred<T1> p1, 
 
 template <class T1, class T2, class Item, class Out>
 __global__ void __launch_bounds__(kThreads) write_tiles_bytes2(BytePred<T1> p1, T2 test2, Item item, long long n,
-                                                               const long long* __restrict__ o1,
+                                                               long long tiles, const long long* __restrict__ o1,
                                                                const long long* __restrict__ o2, Out* __restrict__ out1,
                                                                Out* __restrict__ out2) {
-    if (o1[blockIdx.x + 1] == o1[blockIdx.x] && o2[blockIdx.x + 1] == o2[blockIdx.x]) return;  // nothing selected
-    const long long base = static_cast<long long>(blockIdx.x) * kTile + static_cast<long long>(threadIdx.x) * kItems;
-    BytePred<T2> p2{p1.a, test2};
-    unsigned m1 = base < n ? p1.mask16(base, n) : 0u, m2 = base < n ? p2.mask16(base, n) : 0u;
     using Scan = cub::BlockScan<int, kThreads>;
     __shared__ typename Scan::TempStorage tmp;
-    int r1, r2;
-    Scan(tmp).ExclusiveSum(__popc(m1), r1);
-    __syncthreads();
-    Scan(tmp).ExclusiveSum(__popc(m2), r2);
     __shared__ unsigned short stage[kTile];
-    const long long tile = static_cast<long long>(blockIdx.x) * kTile;
-    staged_write(stage, out1 + o1[blockIdx.x], static_cast<int>(o1[blockIdx.x + 1] - o1[blockIdx.x]), r1, m1, tile, item);
-    staged_write(stage, out2 + o2[blockIdx.x], static_cast<int>(o2[blockIdx.x + 1] - o2[blockIdx.x]), r2, m2, tile, item);
+    BytePred<T2> p2{p1.a, test2};
+    for (long long t = blockIdx.x; t < tiles; t += gridDim.x) {
+        const long long a0 = o1[t], a1 = o1[t + 1], b0 = o2[t], b1 = o2[t + 1];
+        if (a1 == a0 && b1 == b0) continue;  // nothing selected in this tile
+        const long long tile = t * kTile, base = tile + static_cast<long long>(threadIdx.x) * kItems;
+        const unsigned m1 = base < n ? p1.mask16(base, n) : 0u, m2 = base < n ? p2.mask16(base, n) : 0u;
+        int r1, r2;
+        Scan(tmp).ExclusiveSum(__popc(m1), r1);
+        __syncthreads();
+        Scan(tmp).ExclusiveSum(__popc(m2), r2);
+        staged_write(stage, out1 + a0, static_cast<int>(a1 - a0), r1, m1, tile, item);
+        staged_write(stage, out2 + b0, static_cast<int>(b1 - b0), r2, m2, tile, item);
+    }
 }
 
 inline size_t scratch_bytes2(long long n) { return 2 * scratch_bytes(n); }
@@ -254,7 +264,8 @@ cudaError_t compact2(BytePred<T1> p1, T2 test2, Item item, long long n, Out* out
     e = cub::DeviceScan::ExclusiveSum(scan_tmp, scan_bytes, c1, off1, static_cast<int>(tiles + 1), s);
     if (e == cudaSuccess) e = cub::DeviceScan::ExclusiveSum(scan_tmp, scan_bytes, c2, off2, static_cast<int>(tiles + 1), s);
     if (e != cudaSuccess) return e;
-    write_tiles_bytes2<<<static_cast<unsigned>(tiles), kThreads, 0, s>>>(p1, test2, item, n, off1, off2, out1, out2);
+    // (a CTA per tile: the band's live tiles gain more from independent CTAs than from fewer launches)
+    write_tiles_bytes2<<<static_cast<unsigned>(tiles), kThreads, 0, s>>>(p1, test2, item, n, tiles, off1, off2, out1, out2);
     e = cudaMemcpyAsync(d_count2, off1 + tiles, sizeof(long long), cudaMemcpyDeviceToDevice, s);
     if (e == cudaSuccess) e = cudaMemcpyAsync(d_count2 + 1, off2 + tiles, sizeof(long long), cudaMemcpyDeviceToDevice, s);
     if (e != cudaSuccess) return e;
@@ -287,40 +298,45 @@ struct ByteAndNot {
 // BytePred and a ByteAndNot over different arrays): both lists in one count
 // and one write pass
 template <class M1, class M2>
-__global__ void __launch_bounds__(kThreads) count_tiles_m2(M1 p1, M2 p2, long long n, long long* __restrict__ c1,
-                                                           long long* __restrict__ c2) {
-    const long long base = static_cast<long long>(blockIdx.x) * kTile + static_cast<long long>(threadIdx.x) * kItems;
-    const int a = base < n ? __popc(p1.mask16(base, n)) : 0;
-    const int b = base < n ? __popc(p2.mask16(base, n)) : 0;
+__global__ void __launch_bounds__(kThreads) count_tiles_m2(M1 p1, M2 p2, long long n, long long tiles,
+                                                           long long* __restrict__ c1, long long* __restrict__ c2) {
     using Reduce = cub::BlockReduce<int, kThreads>;
     __shared__ typename Reduce::TempStorage tmp;
-    const int ta = Reduce(tmp).Sum(a);
-    __syncthreads();
-    const int tb = Reduce(tmp).Sum(b);
-    if (threadIdx.x == 0) {
-        c1[blockIdx.x] = ta;
-        c2[blockIdx.x] = tb;
+    for (long long t = blockIdx.x; t < tiles; t += gridDim.x) {
+        const long long base = t * kTile + static_cast<long long>(threadIdx.x) * kItems;
+        const int a = base < n ? __popc(p1.mask16(base, n)) : 0;
+        const int b = base < n ? __popc(p2.mask16(base, n)) : 0;
+        const int ta = Reduce(tmp).Sum(a);
+        __syncthreads();
+        const int tb = Reduce(tmp).Sum(b);
+        if (threadIdx.x == 0) {
+            c1[t] = ta;
+            c2[t] = tb;
+        }
+        __syncthreads();
     }
 }
 
 template <class M1, class M2, class Item, class Out>
-__global__ void __launch_bounds__(kThreads) write_tiles_m2(M1 p1, M2 p2, Item item, long long n,
+__global__ void __launch_bounds__(kThreads) write_tiles_m2(M1 p1, M2 p2, Item item, long long n, long long tiles,
                                                            const long long* __restrict__ o1,
                                                            const long long* __restrict__ o2, Out* __restrict__ out1,
                                                            Out* __restrict__ out2) {
-    if (o1[blockIdx.x + 1] == o1[blockIdx.x] && o2[blockIdx.x + 1] == o2[blockIdx.x]) return;  // nothing selected
-    const long long base = static_cast<long long>(blockIdx.x) * kTile + static_cast<long long>(threadIdx.x) * kItems;
-    unsigned m1 = base < n ? p1.mask16(base, n) : 0u, m2 = base < n ? p2.mask16(base, n) : 0u;
     using Scan = cub::BlockScan<int, kThreads>;
     __shared__ typename Scan::TempStorage tmp;
-    int r1, r2;
-    Scan(tmp).ExclusiveSum(__popc(m1), r1);
-    __syncthreads();
-    Scan(tmp).ExclusiveSum(__popc(m2), r2);
     __shared__ unsigned short stage[kTile];
-    const long long tile = static_cast<long long>(blockIdx.x) * kTile;
-    staged_write(stage, out1 + o1[blockIdx.x], static_cast<int>(o1[blockIdx.x + 1] - o1[blockIdx.x]), r1, m1, tile, item);
-    staged_write(stage, out2 + o2[blockIdx.x], static_cast<int>(o2[blockIdx.x + 1] - o2[blockIdx.x]), r2, m2, tile, item);
+    for (long long t = blockIdx.x; t < tiles; t += gridDim.x) {
+        const long long a0 = o1[t], a1 = o1[t + 1], b0 = o2[t], b1 = o2[t + 1];
+        if (a1 == a0 && b1 == b0) continue;  // nothing selected in this tile
+        const long long tile = t * kTile, base = tile + static_cast<long long>(threadIdx.x) * kItems;
+        const unsigned m1 = base < n ? p1.mask16(base, n) : 0u, m2 = base < n ? p2.mask16(base, n) : 0u;
+        int r1, r2;
+        Scan(tmp).ExclusiveSum(__popc(m1), r1);
+        __syncthreads();
+        Scan(tmp).ExclusiveSum(__popc(m2), r2);
+        staged_write(stage, out1 + a0, static_cast<int>(a1 - a0), r1, m1, tile, item);
+        staged_write(stage, out2 + b0, static_cast<int>(b1 - b0), r2, m2, tile, item);
+    }
 }
 
 template <class M1, class M2, class Item, class Out>
@@ -337,11 +353,11 @@ cudaError_t compact2m(M1 p1, M2 p2, Item item, long long n, Out* out1, Out* out2
     cudaError_t e = cudaMemsetAsync(c1 + tiles, 0, sizeof(long long), s);
     if (e == cudaSuccess) e = cudaMemsetAsync(c2 + tiles, 0, sizeof(long long), s);
     if (e != cudaSuccess) return e;
-    count_tiles_m2<<<static_cast<unsigned>(tiles), kThreads, 0, s>>>(p1, p2, n, c1, c2);
+    count_tiles_m2<<<persistent_grid(tiles), kThreads, 0, s>>>(p1, p2, n, tiles, c1, c2);
     e = cub::DeviceScan::ExclusiveSum(scan_tmp, scan_bytes, c1, off1, static_cast<int>(tiles + 1), s);
     if (e == cudaSuccess) e = cub::DeviceScan::ExclusiveSum(scan_tmp, scan_bytes, c2, off2, static_cast<int>(tiles + 1), s);
     if (e != cudaSuccess) return e;
-    write_tiles_m2<<<static_cast<unsigned>(tiles), kThreads, 0, s>>>(p1, p2, item, n, off1, off2, out1, out2);
+    write_tiles_m2<<<persistent_grid(tiles), kThreads, 0, s>>>(p1, p2, item, n, tiles, off1, off2, out1, out2);
     e = cudaMemcpyAsync(d_count2, off1 + tiles, sizeof(long long), cudaMemcpyDeviceToDevice, s);
     if (e == cudaSuccess) e = cudaMemcpyAsync(d_count2 + 1, off2 + tiles, sizeof(long long), cudaMemcpyDeviceToDevice, s);
     if (e != cudaSuccess) return e;
@@ -352,29 +368,35 @@ cudaError_t compact2m(M1 p1, M2 p2, Item item, long long n, Out* out1, Out* out2
 // GatedBytes): the same three passes; tiles the provider reports empty cost
 // one predicate evaluation
 template <class M>
-__global__ void __launch_bounds__(kThreads) count_tiles_m(M p, long long n, long long* __restrict__ counts) {
-    const long long base = static_cast<long long>(blockIdx.x) * kTile + static_cast<long long>(threadIdx.x) * kItems;
-    const int c = base < n ? __popc(p.mask16(base, n)) : 0;
+__global__ void __launch_bounds__(kThreads) count_tiles_m(M p, long long n, long long tiles,
+                                                          long long* __restrict__ counts) {
     using Reduce = cub::BlockReduce<int, kThreads>;
     __shared__ typename Reduce::TempStorage tmp;
-    const int total = Reduce(tmp).Sum(c);
-    if (threadIdx.x == 0) counts[blockIdx.x] = total;
+    for (long long t = blockIdx.x; t < tiles; t += gridDim.x) {
+        const long long base = t * kTile + static_cast<long long>(threadIdx.x) * kItems;
+        const int c = base < n ? __popc(p.mask16(base, n)) : 0;
+        const int total = Reduce(tmp).Sum(c);
+        if (threadIdx.x == 0) counts[t] = total;
+        __syncthreads();
+    }
 }
 
 template <class M, class Item, class Out>
-__global__ void __launch_bounds__(kThreads) write_tiles_m(M p, Item item, long long n,
+__global__ void __launch_bounds__(kThreads) write_tiles_m(M p, Item item, long long n, long long tiles,
                                                           const long long* __restrict__ offsets,
                                                           Out* __restrict__ out) {
-    if (offsets[blockIdx.x + 1] == offsets[blockIdx.x]) return;  // nothing selected in this tile
-    const long long base = static_cast<long long>(blockIdx.x) * kTile + static_cast<long long>(threadIdx.x) * kItems;
-    unsigned mask = base < n ? p.mask16(base, n) : 0u;
     using Scan = cub::BlockScan<int, kThreads>;
     __shared__ typename Scan::TempStorage tmp;
-    int rank;
-    Scan(tmp).ExclusiveSum(__popc(mask), rank);
     __shared__ unsigned short stage[kTile];
-    staged_write(stage, out + offsets[blockIdx.x], static_cast<int>(offsets[blockIdx.x + 1] - offsets[blockIdx.x]), rank,
-                 mask, static_cast<long long>(blockIdx.x) * kTile, item);
+    for (long long t = blockIdx.x; t < tiles; t += gridDim.x) {
+        const long long a0 = offsets[t], a1 = offsets[t + 1];
+        if (a1 == a0) continue;  // nothing selected in this tile
+        const long long tile = t * kTile, base = tile + static_cast<long long>(threadIdx.x) * kItems;
+        const unsigned mask = base < n ? p.mask16(base, n) : 0u;
+        int rank;
+        Scan(tmp).ExclusiveSum(__popc(mask), rank);
+        staged_write(stage, out + a0, static_cast<int>(a1 - a0), rank, mask, tile, item);
+    }
 }
 
 // flag bytes a[0 .. min(n, *n_dev)) (n_dev null: a[0 .. n)), selected where
@@ -450,10 +472,10 @@ cudaError_t compact_m(M p, Item item, long long n, Out* out, long long* d_count,
     size_t scan_bytes = scratch_size - 2 * (tiles + 1) * sizeof(long long);
     cudaError_t e = cudaMemsetAsync(counts + tiles, 0, sizeof(long long), s);
     if (e != cudaSuccess) return e;
-    count_tiles_m<<<static_cast<unsigned>(tiles), kThreads, 0, s>>>(p, n, counts);
+    count_tiles_m<<<persistent_grid(tiles), kThreads, 0, s>>>(p, n, tiles, counts);
     e = cub::DeviceScan::ExclusiveSum(scan_tmp, scan_bytes, counts, offsets, static_cast<int>(tiles + 1), s);
     if (e != cudaSuccess) return e;
-    write_tiles_m<<<static_cast<unsigned>(tiles), kThreads, 0, s>>>(p, item, n, offsets, out);
+    write_tiles_m<<<persistent_grid(tiles), kThreads, 0, s>>>(p, item, n, tiles, offsets, out);
     e = cudaMemcpyAsync(d_count, offsets + tiles, sizeof(long long), cudaMemcpyDeviceToDevice, s);
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
