@@ -502,42 +502,39 @@ __global__ void one_step_tube(SlParams P, const double* __restrict__ prev, doubl
     if (*dense) return;
     const long long n = __ldg(n_dev);
     bool zero = false, froz = false;
-    constexpr int kB = 1;  // entries per thread and round (2 measured slower: registers)
-    const long long T = static_cast<long long>(gridDim.x) * blockDim.x * kB;
+    // one entry per thread and round; the next round's id is loaded while this
+    // round's seven values are in flight (as the sweeps do, jacobi_pipe)
+    const long long T = static_cast<long long>(gridDim.x) * blockDim.x;
     const long long st[3] = {1, P.nx, P.nxy};
-    for (long long t0 = static_cast<long long>(blockIdx.x) * blockDim.x * kB; t0 < n; t0 += T) {
-        long long id[kB];
-#pragma unroll
-        for (int u = 0; u < kB; ++u) {
-            const long long t = t0 + u * blockDim.x + threadIdx.x;
-            id[u] = t < n ? __ldg(tube + t) : -1;
-        }
-        bool has[kB][6];
-        double v[kB][6], pj[kB];
-#pragma unroll
-        for (int u = 0; u < kB; ++u) {
-            if (id[u] < 0) continue;
+    long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    long long id = t < n ? __ldg(tube + t) : -1;
+    while (__any_sync(0xffffffffu, id >= 0)) {
+        bool has[6] = {false, false, false, false, false, false};
+        double v[6], pj = 0.0;
+        if (id >= 0) {
             int i, j, k;
-            lsr_dev::unflatten(P, id[u], i, j, k);
-            has[u][0] = i > 0, has[u][1] = i + 1 < P.nx, has[u][2] = j > 0, has[u][3] = j + 1 < P.ny;
-            has[u][4] = P.dim == 3 && k > 0, has[u][5] = P.dim == 3 && k + 1 < P.nz;
+            lsr_dev::unflatten(P, id, i, j, k);
+            has[0] = i > 0, has[1] = i + 1 < P.nx, has[2] = j > 0, has[3] = j + 1 < P.ny;
+            has[4] = P.dim == 3 && k > 0, has[5] = P.dim == 3 && k + 1 < P.nz;
 #pragma unroll
             for (int q = 0; q < 6; ++q)
-                v[u][q] = __ldg(prev + (has[u][q] ? id[u] + ((q & 1) ? st[q >> 1] : -st[q >> 1]) : id[u]));
-            pj[u] = __ldg(prev + id[u]);
+                v[q] = __ldg(prev + (has[q] ? id + ((q & 1) ? st[q >> 1] : -st[q >> 1]) : id));
+            pj = __ldg(prev + id);
         }
-#pragma unroll
-        for (int u = 0; u < kB; ++u) {
-            if (id[u] < 0) continue;
+        const long long tn = t + T;
+        const long long idn = tn < n ? __ldg(tube + tn) : -1;
+        if (id >= 0) {
             double val;
             bool z = false, f = false;
-            one_node(P, pj[u], v[u], has[u], val, z, f);
-            out[id[u]] = val;
-            if (f) frozen[id[u]] = 1;  // the flags are all clear on entry (lsr_loop_sync_fields clears them)
-            ftube[t0 + u * blockDim.x + threadIdx.x] = f ? 1 : 0;
+            one_node(P, pj, v, has, val, z, f);
+            out[id] = val;
+            if (f) frozen[id] = 1;  // the flags are all clear on entry (lsr_loop_sync_fields clears them)
+            ftube[t] = f ? 1 : 0;
             zero |= z;
             froz |= f;
         }
+        id = idn;
+        t = tn;
     }
     const unsigned zb = __ballot_sync(0xffffffffu, zero), fb = __ballot_sync(0xffffffffu, froz);
     if ((threadIdx.x & 31) == 0) {
