@@ -479,7 +479,16 @@ def run_ours(args):
             "setup_s": {"build_distance": t_dist, "surface_energy": t_energy},
         }
         if loop and loop.get("moving_band"):
-            line["moving_band"] = loop["moving_band"]
+            # the band-changing rate of the faster loop form (device-controlled), the host-driven one beside it
+            mb = dict(loop["moving_band"])
+            dr = (loop.get("device_run") or {}).get("moving_band")
+            if dr:
+                mb = {**mb, "value": dr["value"], "sl_ms_per_step": dr["sl_ms_per_step"],
+                      "host_driven_value": loop["moving_band"]["value"],
+                      "what": "SL phase of the device-controlled loop (lsr_cuda_loop_run: band rebuilt every "
+                              "iteration, covered bricks from the band's state bytes, z-line table fill, SL kernel), "
+                              "globaltimer marks; host_driven_value: the same phase of lsr_cuda_loop_step"}
+            line["moving_band"] = mb
         if e2e:
             line["e2e"] = e2e
         if cpu:
