@@ -451,6 +451,7 @@ __global__ void block_partials(const double* __restrict__ contrib, long long n, 
         __syncthreads();
         if (threadIdx.x == 0) {
             double s = 0.0;
+#pragma unroll 16  // the loads of 16 terms ahead of the serial add chain (same order, same bits)
             for (int t = 0; t < len; ++t) s += buf[t];
             partial[blk] = s;
         }

@@ -39,8 +39,13 @@ CASES = {
 }
 
 
-@pytest.mark.parametrize("config", sorted(CASES))
-def test_final_phi_with_own_energy(gpu, reference, config):
+_REF = {}  # config -> the reference run (configs up to 512^3: shared by the two forms of the GPU loop)
+
+
+@pytest.mark.parametrize("config,device_loop", [(c, False) for c in sorted(CASES)] + [(2, True), (3, True), (4, True)])
+def test_final_phi_with_own_energy(gpu, reference, config, device_loop):
+    """device_loop: all the iterations in one lsr_cuda_loop_run call (one host
+    synchronisation, graph replays) instead of one lsr_cuda_loop_step each."""
     lsr = gpu
     n, npts, sig, interp, r0, iters = CASES[config]
     g = lsr.cube_grid(n, 3)
@@ -63,11 +68,19 @@ def test_final_phi_with_own_energy(gpu, reference, config):
             del dref
         ctx.upload(0, phi)
         rc = lsr.ReinitConfig.defaults(g.dx, bp.gamma)
-        stats = [ctx.loop_step(cfg, rc, 5) for _ in range(iters)]  # the GPU's own E_2 every iteration
+        if device_loop:
+            stats = ctx.loop_run(cfg, rc, iters, 5)
+        else:
+            stats = [ctx.loop_step(cfg, rc, 5) for _ in range(iters)]  # the GPU's own E_2 every iteration
         got = ctx.download(0)
     finally:
         ctx.close()
-    ref_phi, e2, na, its = reference.loop_run(gd, phi, d, ccfg, iters, inplace=True)  # phi becomes ref_phi
+    if config in _REF:
+        ref_phi, e2, na, its = _REF.pop(config)
+    else:
+        ref_phi, e2, na, its = reference.loop_run(gd, phi, d, ccfg, iters, inplace=True)  # phi becomes ref_phi
+        if n <= 512:
+            _REF[config] = (ref_phi, e2, na, its)
     del d
     assert [s["n_active"] for s in stats] == na.tolist()
     assert [s["reinit_iterations"] for s in stats] == its.tolist()
