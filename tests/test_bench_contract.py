@@ -101,6 +101,10 @@ def test_our_arm_json_line(gpu):
     assert 0 < rf["compulsory_frac"] < 1 and rf["compulsory_bytes_per_update"] == 32
     mb = d["moving_band"]
     assert mb["value"] > 0 and mb["unit"] == d["unit"] and mb["sl_ms_per_step"] > 0
+    # the whole loop: host-driven and device-controlled (one host sync per run), same bands
+    dr = d["loop"]["device_run"]
+    assert dr["host_syncs"] == 1 and dr["same_bands_as_host_loop"] and dr["gpu_total_ms_per_step"] > 0
+    assert set(dr["gpu_ms_per_step"]) == {"band", "energy", "sl", "reinit"}
     # the reference arm prints the very same config block
     from oracle import bindings
 
