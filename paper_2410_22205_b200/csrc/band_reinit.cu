@@ -117,25 +117,8 @@ __global__ void band_pass_z(SlParams P, const unsigned char* __restrict__ u, lon
 // pass makes 4 nodes per thread (two 16-byte loads of phi, one 4-byte store),
 // the y/z passes 16 per thread (16-byte loads and stores, bytewise logic on
 // 32-bit lanes). Same results as the scalar passes above.
-__global__ void band_pass_x4(SlParams P, const double* __restrict__ phi, double gamma, long long base4, long long end4,
-                             unsigned* __restrict__ t) {
-    const long long q = base4 + static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (q >= end4) return;
-    const long long id = 4 * q;
-    const int x0 = static_cast<int>(id % P.nx);
-    const double2 a = __ldg(reinterpret_cast<const double2*>(phi + id));
-    const double2 b = __ldg(reinterpret_cast<const double2*>(phi + id) + 1);
-    const bool c0 = fabs(a.x) < gamma, c1 = fabs(a.y) < gamma, c2 = fabs(b.x) < gamma, c3 = fabs(b.y) < gamma;
-    const bool l = x0 > 0 && fabs(__ldg(phi + id - 1)) < gamma;
-    const bool r = x0 + 4 < P.nx && fabs(__ldg(phi + id + 4)) < gamma;
-    const unsigned o0 = (c0 ? 2u : 0u) | ((c0 || l || c1) ? 1u : 0u);
-    const unsigned o1 = (c1 ? 2u : 0u) | ((c1 || c0 || c2) ? 1u : 0u);
-    const unsigned o2 = (c2 ? 2u : 0u) | ((c2 || c1 || c3) ? 1u : 0u);
-    const unsigned o3 = (c3 ? 2u : 0u) | ((c3 || c2 || r) ? 1u : 0u);
-    t[q] = o0 | (o1 << 8) | (o2 << 16) | (o3 << 24);
-}
 
-// band_pass_x4's quad: the 4 output bytes of nodes id .. id + 3
+// the x pass of a quad: the 4 output bytes of nodes id .. id + 3 (x0 = the first node's i)
 __device__ __forceinline__ unsigned band_quad(const SlParams& P, const double* __restrict__ phi, double gamma,
                                               long long id, int x0) {
     const double2 a = __ldg(reinterpret_cast<const double2*>(phi + id));
@@ -148,6 +131,14 @@ __device__ __forceinline__ unsigned band_quad(const SlParams& P, const double* _
     const unsigned o2 = (c2 ? 2u : 0u) | ((c2 || c1 || c3) ? 1u : 0u);
     const unsigned o3 = (c3 ? 2u : 0u) | ((c3 || c2 || r) ? 1u : 0u);
     return o0 | (o1 << 8) | (o2 << 16) | (o3 << 24);
+}
+
+__global__ void band_pass_x4(SlParams P, const double* __restrict__ phi, double gamma, long long base4, long long end4,
+                             unsigned* __restrict__ t) {
+    const long long q = base4 + static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (q >= end4) return;
+    const long long id = 4 * q;
+    t[q] = band_quad(P, phi, gamma, id, static_cast<int>(id % P.nx));
 }
 
 // The device loop's x pass (rows of whole 16-node groups): 16 nodes per

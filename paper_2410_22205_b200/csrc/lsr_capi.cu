@@ -421,8 +421,7 @@ int lsr_cuda_upload_field(lsr_cuda_ctx* c, int which, const double* host) {
     LSR_CUDA_TRY(cudaMemcpyAsync(*slot, host, sizeof(double) * c->n, cudaMemcpyHostToDevice, c->stream));
     LSR_CUDA_TRY(cudaStreamSynchronize(c->stream));
     if (which != LSR_FIELD_DIST) c->consistent = false;
-    else c->zt_bricks = false;
-    c->bd_valid = false;
+    else c->zt_bricks = c->bd_valid = false;  // d changed: its covered bricks and per-brick maxima
     c->box_valid = false;  // the covered bricks depend on d
     return LSR_OK;
 }
@@ -450,8 +449,7 @@ int lsr_cuda_mark_dirty(lsr_cuda_ctx* c, int which) {
     if (!c) return set_err(LSR_ERR_CONFIG, "null context");
     c->seq++;  // may write phi or out
     if (which != LSR_FIELD_DIST) c->consistent = false;
-    else c->zt_bricks = false;
-    c->bd_valid = false;
+    else c->zt_bricks = c->bd_valid = false;  // d changed: its covered bricks and per-brick maxima
     c->box_valid = false;
     return LSR_OK;
 }
@@ -467,7 +465,6 @@ int lsr_cuda_set_active(lsr_cuda_ctx* c, const int64_t* ids, int64_t n) {
     LSR_CUDA_TRY(cudaStreamSynchronize(c->stream));
     c->n_active = n;
     c->zt_bricks = false;
-    c->bd_valid = false;
     c->box_valid = false;
     c->dirty_is_active = false;
     return LSR_OK;
@@ -493,7 +490,6 @@ int lsr_cuda_set_active_device(lsr_cuda_ctx* c, const int64_t* d_ids, int64_t n)
     }
     c->n_active = n;
     c->zt_bricks = false;
-    c->bd_valid = false;
     c->box_valid = false;
     c->dirty_is_active = false;
     return LSR_OK;
@@ -1428,7 +1424,6 @@ int lsr_cuda_narrow_band(lsr_cuda_ctx* c, int which, double gamma, int64_t* n_ac
                                      c->stream));
     c->n_active = na;
     c->zt_bricks = false;
-    c->bd_valid = false;
     c->box_valid = false;
     c->dirty_is_active = false;
     if (n_active) *n_active = na;
@@ -1461,8 +1456,7 @@ int lsr_cuda_clamp_field(lsr_cuda_ctx* c, int which, double gamma) {
     if (int st = lsr_clamp(*slot, c->n, gamma, c->stream, &err)) return set_err(st, err);
     LSR_CUDA_TRY(cudaStreamSynchronize(c->stream));
     if (which != LSR_FIELD_DIST) c->consistent = false;
-    else c->zt_bricks = false;
-    c->bd_valid = false;
+    else c->zt_bricks = c->bd_valid = false;  // d changed: its covered bricks and per-brick maxima
     c->box_valid = false;  // the covered bricks depend on d
     return LSR_OK;
 }
@@ -1519,7 +1513,6 @@ int lsr_cuda_set_band(lsr_cuda_ctx* c, const uint8_t* state, const int64_t* acti
         LSR_CUDA_TRY(cudaMemcpyAsync(c->active, active, sizeof(int64_t) * n_active, cudaMemcpyHostToDevice, s));
     c->n_active = n_active;
     c->zt_bricks = false;
-    c->bd_valid = false;
     c->box_valid = false;
     c->dirty_is_active = false;
     LSR_CUDA_TRY(cudaStreamSynchronize(s));

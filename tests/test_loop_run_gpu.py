@@ -158,3 +158,31 @@ def test_loop_run_without_interface(gpu):
     recs = _compare(lsr, g, pts, phi, cfg, rc, 4)
     assert all(r["energy"] == 0.0 and not r["had_interface"] and r["reinit_iterations"] == 0 for r in recs)
     assert all(r["n_active"] > 0 for r in recs)
+
+
+def test_loop_run_after_distance_change(gpu):
+    """The per-brick maxima of d behind the table's coverage are rebuilt when d
+    changes: a run, a new cloud on the same context, another run — equal to a
+    host-driven loop on a fresh context with the second cloud."""
+    lsr = gpu
+    g, pts, phi, cfg, rc = _setup(lsr, 3, n=64)
+    pts2 = 0.8 * pts
+    dev, host = lsr.Context(g), lsr.Context(g)
+    try:
+        dev.build_distance(pts)
+        dev.upload(0, phi)
+        dev.loop_run(cfg, rc, 3, 5)
+        dev.build_distance(pts2)
+        dev.upload(0, phi)
+        recs = dev.loop_run(cfg, rc, 4, 5)
+        host.build_distance(pts2)
+        host.upload(0, phi)
+        ref = [host.loop_step(cfg, rc, 5) for _ in range(4)]
+        assert [r["n_active"] for r in recs] == [r["n_active"] for r in ref]
+        if all(a["energy"] == b["energy"] for a, b in zip(ref, recs)):
+            assert np.array_equal(bits(host.download(0)), bits(dev.download(0)))
+        else:
+            assert np.max(np.abs(host.download(0) - dev.download(0))) <= 1e-12 * cfg.band.gamma
+    finally:
+        dev.close()
+        host.close()
