@@ -16,14 +16,16 @@
 #ifndef LSR_SL_MIN_BLOCKS
 #define LSR_SL_MIN_BLOCKS 4
 #endif
-// 3d WENO (sl_step_w3_kernel, z-line table or per-line): 6 CTAs of 192
-// threads at 56 registers (36 warps/SM; 7 x 192, 10 x 128, 5 x 256, 8 x 128,
-// 12 x 96 measured 3-33 % slower at 512^3)
+// 3d WENO with the z-line table (sl_step_zt_kernel): 4 CTAs of 256 threads at
+// 64 registers (32 warps/SM). With one x-column per loop iteration
+// (weno3_interior_zt) at 512^3: 4 x 256 2.74 ms, 8 x 128 2.75, 9 x 128 2.76,
+// 6 x 192 (56 registers, the previous loop form's best) 2.77, 5 x 192 2.88,
+// 10 x 128 2.96.
 #ifndef LSR_SL_THREADS_W3
-#define LSR_SL_THREADS_W3 192
+#define LSR_SL_THREADS_W3 256
 #endif
 #ifndef LSR_SL_MIN_BLOCKS_W3
-#define LSR_SL_MIN_BLOCKS_W3 6
+#define LSR_SL_MIN_BLOCKS_W3 4
 #endif
 constexpr int kSlThreads = LSR_SL_THREADS;
 constexpr int kSlThreadsW3 = LSR_SL_THREADS_W3;
